@@ -1,0 +1,175 @@
+/*
+ * saix_b200.h -- C ABI of libsaix_b200.so, the sm_100a implementation of the
+ * reference `saix` longest-overlap hot path (DC3 suffix array -> LCP ->
+ * sparse-table RMQ -> cross-sequence overlap scan).
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers unless the name ends in `_host`.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream) and performs no hidden device
+ *     allocation: scratch comes from the caller's `ws` of at least the size
+ *     the matching *_workspace_bytes() returns.
+ *   - Return 0 on success or a negative SAIX_E* code; saix_last_error()
+ *     returns a thread-local message for the last failure on this thread.
+ *   - Positions, ranks and LCP values are uint32 on the device (n < 2^32-4);
+ *     the Python layer widens them to the reference's int64 arrays.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to the reference checkout, pkg/src/saix/...).
+ */
+#ifndef SAIX_B200_H
+#define SAIX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SAIX_API __attribute__((visibility("default")))
+#else
+#define SAIX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAIX_OK 0
+#define SAIX_EINVAL (-22)   /* bad argument: reference ValueError            */
+#define SAIX_ERANGE (-34)   /* index out of range: reference IndexError      */
+#define SAIX_ENOSPC (-28)   /* workspace smaller than *_workspace_bytes()     */
+#define SAIX_ECUDA (-100)   /* CUDA runtime error (message has the details)   */
+#define SAIX_ESEQ (-101)    /* illegal residue: reference SequenceError       */
+
+SAIX_API const char *saix_last_error(void);
+SAIX_API int saix_abi_version(void);
+
+/* ---------------------------------------------------------------- encode */
+
+/* encode (sequence.py:144-157) fused with GeneralizedText.build
+ * (overlap.py:83-95): ASCII A and B -> u8 GSA ranks encode(A)+1 ++ [1] ++
+ * encode(B)+1, n = na+nb+1.  keep_n selects NPolicy.KEEP (N -> rank 5).
+ * *bad_pos (device int64, caller sets INT64_MAX) receives the smallest GSA
+ * offset of an illegal residue (offset na+1+i for B[i]). */
+SAIX_API int saix_encode_gsa(const uint8_t *a_ascii, int64_t na, const uint8_t *b_ascii,
+                    int64_t nb, int keep_n, uint8_t *gsa, int64_t *bad_pos,
+                    void *stream);
+
+/* encode (sequence.py:144-157) alone: ASCII -> u8 ranks (A1 C2 G3 T4 [N5]). */
+SAIX_API int saix_encode(const uint8_t *ascii, int64_t n, int keep_n, uint8_t *ranks,
+                int64_t *bad_pos, void *stream);
+
+/* ------------------------------------------------------------------- DC3 */
+
+/* Level-0 introspection (Dc3Workspace, suffix_index.py:119-140,414-449).
+ * Device arrays may be NULL individually; sizes: triple_text m,
+ * sample_rank n+3 (1-based ranks by position), sorted_samples m,
+ * sorted_nonsamples ceil(n/3).  The scalar outputs are written by the call. */
+typedef struct saix_dc3_probe {
+    uint32_t *triple_text;
+    uint32_t *sample_rank;
+    uint32_t *sorted_samples;
+    uint32_t *sorted_nonsamples;
+    int64_t n_samples;            /* m (incl. the padding sample)           */
+    int64_t n_sorted_samples;     /* real samples (< n)                      */
+    int64_t n_sorted_nonsamples;  /* k = ceil(n/3)                           */
+    int32_t depth;                /* recursion levels below the top          */
+    int32_t reserved;
+} saix_dc3_probe;
+
+SAIX_API size_t saix_dc3_workspace_bytes(int64_t n, int text_bytes);
+
+/* build_sa_dc3 (suffix_index.py:395-399) + SuffixArray.from_order (96-101).
+ * text: n ranks in 1..sigma (0 never appears), text_bytes = 1 (u8) or 4 (u32).
+ * sa, isa: n entries each (isa = the reference's 0-based `rank`; may be NULL
+ * only if not needed).  probe may be NULL. */
+SAIX_API int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sigma,
+             uint32_t *sa, uint32_t *isa, void *ws, size_t ws_bytes,
+             saix_dc3_probe *probe, void *stream);
+
+/* merge_sample_nonsample (suffix_index.py:452-457, _merge 362-378): step 3
+ * alone.  sample_rank: n+3 by position; sorted_samples (ms entries) and
+ * sorted_nonsamples (k entries) as in the probe. */
+SAIX_API int saix_dc3_merge(const void *text, int text_bytes, int64_t n,
+                   const uint32_t *sample_rank, const uint32_t *sorted_samples,
+                   int64_t ms, const uint32_t *sorted_nonsamples, int64_t k,
+                   uint32_t *sa, void *stream);
+
+/* ------------------------------------------------------------------- LCP */
+
+SAIX_API size_t saix_lcp_workspace_bytes(int64_t n);
+
+/* build_lcp (suffix_index.py:479-506): lcp[r] = |lcp(suffix sa[r-1],
+ * suffix sa[r])|, lcp[0] = 0. */
+SAIX_API int saix_lcp(const void *text, int text_bytes, int64_t n, const uint32_t *sa,
+             const uint32_t *isa, uint32_t *lcp, void *ws, size_t ws_bytes,
+             void *stream);
+
+/* ------------------------------------------------------------------- RMQ */
+
+#define SAIX_SPARSE_PACK32 0  /* entry = (value-bias) << ibits | index, u32 */
+#define SAIX_SPARSE_PACK64 1  /* same packing in u64                        */
+#define SAIX_SPARSE_INDEX 2   /* entry = u32 index; values gathered (int64) */
+
+typedef struct saix_sparse_plan {
+    int64_t n;
+    int64_t value_bias;    /* subtracted before packing (min value)        */
+    int64_t table_bytes;   /* bytes the table needs                        */
+    int32_t levels;        /* SparseTable levels (rmq.py:38-47)            */
+    int32_t mode;          /* SAIX_SPARSE_*                                */
+    int32_t index_bits;
+    int32_t value_bits;
+} saix_sparse_plan;
+
+/* Choose the table layout for n values in [vmin, vmax]. */
+SAIX_API int saix_sparse_plan_make(int64_t n, int64_t vmin, int64_t vmax,
+                          saix_sparse_plan *plan);
+
+/* SparseTable.__init__ (rmq.py:33-50).  values: n entries of
+ * value_bytes = 4 (u32, e.g. a device LCP array) or 8 (int64). */
+SAIX_API int saix_sparse_build(const saix_sparse_plan *plan, const void *values,
+                      int value_bytes, void *table, void *stream);
+
+/* SparseTable.query / query_sparse (rmq.py:52-58, 254-259), batched:
+ * out_index[t] = leftmost argmin of values[min(i,j)..max(i,j)].
+ * out_value (nullable) receives values[out_index].  Out-of-range pairs set
+ * *err (device int32, caller zeroes) to 1 (reference: IndexError). */
+SAIX_API int saix_sparse_query(const saix_sparse_plan *plan, const void *table,
+                      const void *values, int value_bytes, const int64_t *qi,
+                      const int64_t *qj, int64_t q, int64_t *out_index,
+                      int64_t *out_value, int32_t *err, void *stream);
+
+/* lcp_query (overlap.py:58-69), batched over an engine whose sparse table
+ * was built over its LCP array: i == j -> n - i, otherwise
+ * lcp[argmin(lcp[lo+1..hi])] with lo/hi the sorted ranks isa[i], isa[j]. */
+SAIX_API int saix_lcp_query(const saix_sparse_plan *plan, const void *table,
+                   const void *lcp, int lcp_bytes, const uint32_t *isa,
+                   const int64_t *qi, const int64_t *qj, int64_t q,
+                   int64_t *out, int32_t *err, void *stream);
+
+/* --------------------------------------------------------------- overlap */
+
+SAIX_API size_t saix_overlap_workspace_bytes(int64_t n);
+
+/* The scan half of longest_overlap (overlap.py:128-152) over a generalized
+ * suffix array of n = |A|+|B|+1 with the separator at `boundary` = |A|:
+ * out3 (device int64[3]) = {length, pos_a, pos_b}, (0,0,0) when no
+ * cross-sequence pair shares a prefix. */
+SAIX_API int saix_overlap_scan(const uint32_t *sa, const uint32_t *lcp, int64_t n,
+                      int64_t boundary, int64_t *out3, void *ws, size_t ws_bytes,
+                      void *stream);
+
+SAIX_API size_t saix_longest_overlap_workspace_bytes(int64_t na, int64_t nb);
+
+/* longest_overlap (overlap.py:110-152) end to end on the device: encode +
+ * GSA + DC3 + LCP + scan.  a_ascii/b_ascii are device buffers; out3 and
+ * bad_pos are device int64 (bad_pos set to INT64_MAX by the callee). */
+SAIX_API int saix_longest_overlap(const uint8_t *a_ascii, int64_t na,
+                         const uint8_t *b_ascii, int64_t nb, int keep_n,
+                         int64_t *out3, int64_t *bad_pos, void *ws,
+                         size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SAIX_B200_H */

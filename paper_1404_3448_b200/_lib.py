@@ -1,0 +1,184 @@
+"""ctypes binding of libsaix_b200.so (include/saix_b200.h) + device plumbing.
+
+PyTorch is used only for device memory, streams and host<->device copies.
+There is no CPU fallback: every compute call needs the CUDA library and a
+visible GPU and raises RuntimeError otherwise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+_c = ctypes
+_vp = _c.c_void_p
+_i64 = _c.c_int64
+_int = _c.c_int
+
+SAIX_OK = 0
+SAIX_EINVAL = -22
+SAIX_ERANGE = -34
+SAIX_ENOSPC = -28
+SAIX_ECUDA = -100
+SAIX_ESEQ = -101
+
+SPARSE_PACK32, SPARSE_PACK64, SPARSE_INDEX = 0, 1, 2
+
+
+class Dc3Probe(_c.Structure):
+    _fields_ = [
+        ("triple_text", _vp),
+        ("sample_rank", _vp),
+        ("sorted_samples", _vp),
+        ("sorted_nonsamples", _vp),
+        ("n_samples", _i64),
+        ("n_sorted_samples", _i64),
+        ("n_sorted_nonsamples", _i64),
+        ("depth", _c.c_int32),
+        ("reserved", _c.c_int32),
+    ]
+
+
+class SparsePlan(_c.Structure):
+    _fields_ = [
+        ("n", _i64),
+        ("value_bias", _i64),
+        ("table_bytes", _i64),
+        ("levels", _c.c_int32),
+        ("mode", _c.c_int32),
+        ("index_bits", _c.c_int32),
+        ("value_bits", _c.c_int32),
+    ]
+
+
+# name -> (restype, argtypes); mirrors include/saix_b200.h exactly
+SIGNATURES = {
+    "saix_last_error": (_c.c_char_p, []),
+    "saix_abi_version": (_int, []),
+    "saix_encode_gsa": (_int, [_vp, _i64, _vp, _i64, _int, _vp, _vp, _vp]),
+    "saix_encode": (_int, [_vp, _i64, _int, _vp, _vp, _vp]),
+    "saix_dc3_workspace_bytes": (_c.c_size_t, [_i64, _int]),
+    "saix_dc3": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _c.c_size_t,
+                        _c.POINTER(Dc3Probe), _vp]),
+    "saix_dc3_merge": (_int, [_vp, _int, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "saix_lcp_workspace_bytes": (_c.c_size_t, [_i64]),
+    "saix_lcp": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_sparse_plan_make": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),
+    "saix_sparse_build": (_int, [_c.POINTER(SparsePlan), _vp, _int, _vp, _vp]),
+    "saix_sparse_query": (_int, [_c.POINTER(SparsePlan), _vp, _vp, _int, _vp, _vp, _i64,
+                                 _vp, _vp, _vp, _vp]),
+    "saix_lcp_query": (_int, [_c.POINTER(SparsePlan), _vp, _vp, _int, _vp, _vp, _vp, _i64,
+                              _vp, _vp, _vp]),
+    "saix_overlap_workspace_bytes": (_c.c_size_t, [_i64]),
+    "saix_overlap_scan": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_longest_overlap_workspace_bytes": (_c.c_size_t, [_i64, _i64]),
+    "saix_longest_overlap": (_int, [_vp, _i64, _vp, _i64, _int, _vp, _vp, _vp, _c.c_size_t, _vp]),
+}
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libsaix_b200.so (building it in-tree when nvcc is available)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if not os.path.exists(path) and build_if_missing and os.path.exists(_build.NVCC):
+        _build.build()
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"libsaix_b200.so not found at {path}; build it with "
+            "`python -c 'import __graft_entry__; __graft_entry__.build()'` "
+            "(there is no CPU fallback)")
+    L = _c.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == SAIX_OK:
+        return
+    msg = load().saix_last_error().decode(errors="replace")
+    if rc == SAIX_ERANGE:
+        raise IndexError(msg or what)
+    if rc == SAIX_EINVAL:
+        raise ValueError(msg or what)
+    raise RuntimeError(f"{what}: saix error {rc}: {msg}")
+
+
+# ------------------------------------------------------------------ torch
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def device():
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("paper_1404_3448_b200 needs a CUDA device (B200); "
+                           "there is no CPU fallback")
+    load()
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch().cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def empty(n: int, dtype, dev=None):
+    t = torch()
+    return t.empty(max(int(n), 1), dtype=dtype, device=dev or device())
+
+
+def workspace(nbytes: int):
+    return empty(nbytes, torch().uint8)
+
+
+def to_device(arr: np.ndarray, dev=None):
+    """Host numpy -> device tensor (pinned staging for large arrays)."""
+    t = torch()
+    h = t.from_numpy(np.ascontiguousarray(arr))
+    if h.numel() == 0:
+        return t.empty(1, dtype=h.dtype, device=dev or device())
+    return h.to(dev or device(), non_blocking=False)
+
+
+def to_host(t_dev, n: int | None = None, dtype=np.int64) -> np.ndarray:
+    """Device tensor -> host numpy (widened to `dtype`)."""
+    if n is not None:
+        t_dev = t_dev[:n]
+    a = t_dev.cpu().numpy()
+    if n == 0:
+        a = a[:0]
+    return a.astype(dtype, copy=False) if a.dtype != dtype else a
+
+
+def u32_to_i64_host(t_dev, n: int) -> np.ndarray:
+    """u32 device array (stored in an int32 tensor) -> host int64."""
+    if n == 0:
+        return np.zeros(0, np.int64)
+    return t_dev[:n].cpu().numpy().view(np.uint32).astype(np.int64)

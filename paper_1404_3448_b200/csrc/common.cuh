@@ -1,0 +1,138 @@
+// common.cuh -- error plumbing, workspace carving and small device helpers
+// shared by every kernel file of libsaix_b200.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/saix_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libsaix_b200 targets sm_100a (B200) only"
+#endif
+
+namespace saix {
+
+using u8 = uint8_t;
+using u32 = uint32_t;
+using u64 = uint64_t;
+using i64 = int64_t;
+
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
+// ---------------------------------------------------------------- errors
+
+void set_error(const char *fmt, ...);
+
+#define SAIX_CUDA(call)                                                        \
+    do {                                                                       \
+        cudaError_t e_ = (call);                                               \
+        if (e_ != cudaSuccess) {                                               \
+            ::saix::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,       \
+                              cudaGetErrorString(e_));                         \
+            return SAIX_ECUDA;                                                 \
+        }                                                                      \
+    } while (0)
+
+#define SAIX_LAUNCHED()                                                        \
+    do {                                                                       \
+        cudaError_t e_ = cudaGetLastError();                                   \
+        if (e_ != cudaSuccess) {                                               \
+            ::saix::set_error("%s:%d kernel launch: %s", __FILE__, __LINE__,   \
+                              cudaGetErrorString(e_));                         \
+            return SAIX_ECUDA;                                                 \
+        }                                                                      \
+    } while (0)
+
+#define SAIX_TRY(expr)                                                         \
+    do {                                                                       \
+        int rc_ = (expr);                                                      \
+        if (rc_ != SAIX_OK) return rc_;                                        \
+    } while (0)
+
+// ------------------------------------------------------------- workspace
+
+// Bump allocator over the caller's workspace.  With base == nullptr it only
+// measures (used by the *_workspace_bytes planners).
+struct Arena {
+    char *base = nullptr;
+    size_t cap = 0;
+    size_t off = 0;
+    size_t peak = 0;
+    bool overflow = false;
+
+    static constexpr size_t kAlign = 256;
+
+    template <typename T>
+    T *alloc(i64 count) {
+        size_t bytes = (size_t)(count > 0 ? count : 1) * sizeof(T);
+        off = (off + kAlign - 1) & ~(kAlign - 1);
+        size_t at = off;
+        off += bytes;
+        if (off > peak) peak = off;
+        if (base == nullptr) return nullptr;
+        if (off > cap) {
+            overflow = true;
+            return nullptr;
+        }
+        return reinterpret_cast<T *>(base + at);
+    }
+    size_t mark() const { return off; }
+    void reset(size_t m) { off = m; }
+};
+
+#define SAIX_ARENA_OK(arena)                                                   \
+    do {                                                                       \
+        if ((arena).overflow) {                                                \
+            ::saix::set_error("workspace too small (%zu bytes needed)",        \
+                              (arena).peak);                                   \
+            return SAIX_ENOSPC;                                                \
+        }                                                                      \
+    } while (0)
+
+// --------------------------------------------------------------- helpers
+
+__host__ __device__ inline i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
+
+inline int grid_for(i64 n, int threads, int max_blocks = kNumSMs * 32) {
+    i64 b = ceil_div(n > 0 ? n : 1, threads);
+    return (int)(b < max_blocks ? b : max_blocks);
+}
+
+__device__ __forceinline__ u32 lanemask_lt() {
+    u32 m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+inline int bits_for(u64 v) {  // bit width of v (>= 1), like int.bit_length()
+    int b = 1;
+    while (b < 64 && (v >> b)) b++;
+    return b;
+}
+
+// DC3 sample layout (suffix_index.py:149-153): mod-1 positions 1,4,... and
+// mod-2 positions 2,5,... below limit = n+1 if n%3==1 else n.
+struct SampleLayout {
+    i64 n, m1, m2, m, k;  // k = number of mod-0 positions = ceil(n/3)
+    bool pad;             // padding sample n present (n % 3 == 1)
+    __host__ __device__ static SampleLayout of(i64 n) {
+        SampleLayout s;
+        s.n = n;
+        i64 limit = (n % 3 == 1) ? n + 1 : n;
+        s.m1 = limit > 1 ? (limit + 1) / 3 : 0;
+        s.m2 = limit > 2 ? limit / 3 : 0;
+        s.m = s.m1 + s.m2;
+        s.k = (n + 2) / 3;
+        s.pad = (n % 3 == 1);
+        return s;
+    }
+    __host__ __device__ i64 pos(i64 s) const { return s < m1 ? 3 * s + 1 : 3 * (s - m1) + 2; }
+};
+
+}  // namespace saix

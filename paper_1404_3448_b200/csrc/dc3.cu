@@ -1,0 +1,553 @@
+// dc3.cu -- DC3 / skew suffix array construction on sm_100a.
+//
+// Restates the reference recursion (suffix_index.py:381-392 `_dc3`) level by
+// level as HBM-streaming kernels; the recursion driver stays on the host and
+// reads back one u32 (`distinct`) per level.
+//
+// Level layout (text T of length N, ranks 0..sigma, virtual zero padding):
+//   sample index s in [0, m): s < m1 -> position 3s+1 (mod-1 block),
+//                             else  -> position 3(s-m1)+2 (mod-2 block)
+//   tt[s]    triple name of sample s  (the recursion string, `triple_text`)
+//   SAc, ISAc  suffix array / inverse of tt (sample indices, 0-based ranks);
+//            the reference's 1-based `rank_of[pos(s)]` is ISAc[s] + 1.
+// Steps per level (reference lines):
+//   1 naming  (_name_triples 221-253): dense names of sample triples, either
+//             by a presence bitmap over the (sigma+1)^3 code space when that
+//             is small (levels 0-1 on DNA: no sort at all) or by an LSD radix
+//             sort of packed triple keys + adjacent-difference scan.
+//   2 recurse (_sort_samples 256-271) iff distinct < m.
+//   3 mod-0   (_sort_nonsamples 274-290): mod-1 samples in rank order, one
+//             position left, stably split by first character.
+//   4 merge   (_merge_walk 173-218): merge-path partition with the DC3
+//             comparator, ISA scattered in the same kernel.
+#include "radix.cuh"
+
+namespace saix {
+
+template <typename TT>
+struct Text {
+    const TT *t;
+    i64 n;
+    __device__ __forceinline__ u32 operator()(i64 p) const { return p < n ? (u32)t[p] : 0u; }
+};
+
+// ------------------------------------------------------------ naming
+
+template <typename TT>
+__global__ void k_bitmap_set(Text<TT> T, SampleLayout L, u64 s1, u32 *__restrict__ bm,
+                             u32 nwords, int use_smem) {
+    extern __shared__ u32 shb[];
+    if (use_smem) {
+        for (u32 w = threadIdx.x; w < nwords; w += blockDim.x) shb[w] = 0;
+        __syncthreads();
+    }
+    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < L.m; s += (i64)gridDim.x * blockDim.x) {
+        i64 p = L.pos(s);
+        u64 code = ((u64)T(p) * s1 + T(p + 1)) * s1 + T(p + 2);
+        u32 w = (u32)(code >> 5), bit = 1u << (code & 31);
+        u32 *dst = use_smem ? shb : bm;
+        if (!(dst[w] & bit)) atomicOr(&dst[w], bit);
+    }
+    if (use_smem) {
+        __syncthreads();
+        for (u32 w = threadIdx.x; w < nwords; w += blockDim.x)
+            if (shb[w]) atomicOr(&bm[w], shb[w]);
+    }
+}
+
+struct PopcIn {
+    const u32 *bm;
+    __device__ u32 operator()(i64 i) const { return __popc(bm[i]); }
+};
+struct StoreExcl {
+    u32 *out;
+    __device__ void operator()(i64 i, u32 excl, u32) const { out[i] = excl; }
+};
+
+template <typename TT>
+__global__ void k_bitmap_name(Text<TT> T, SampleLayout L, u64 s1, const u32 *__restrict__ bm,
+                              const u32 *__restrict__ wp, u32 *__restrict__ tt) {
+    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < L.m; s += (i64)gridDim.x * blockDim.x) {
+        i64 p = L.pos(s);
+        u64 code = ((u64)T(p) * s1 + T(p + 1)) * s1 + T(p + 2);
+        u32 w = (u32)(code >> 5);
+        u32 below = bm[w] & ((1u << (code & 31)) - 1u);
+        tt[s] = wp[w] + __popc(below) + 1u;
+    }
+}
+
+template <typename TT>
+__global__ void k_triple_keys(Text<TT> T, SampleLayout L, int b, u64 *__restrict__ keys,
+                              u32 *__restrict__ vals) {
+    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < L.m; s += (i64)gridDim.x * blockDim.x) {
+        i64 p = L.pos(s);
+        keys[s] = ((u64)T(p) << (2 * b)) | ((u64)T(p + 1) << b) | (u64)T(p + 2);
+        vals[s] = (u32)s;
+    }
+}
+
+// wide alphabets (3 * bits(sigma) > 64): sort by the third char first ...
+template <typename TT>
+__global__ void k_third_char_keys(Text<TT> T, SampleLayout L, u64 *__restrict__ keys,
+                                  u32 *__restrict__ vals) {
+    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < L.m; s += (i64)gridDim.x * blockDim.x) {
+        keys[s] = T(L.pos(s) + 2);
+        vals[s] = (u32)s;
+    }
+}
+// ... then stably by the first two chars, gathered through the permutation.
+template <typename TT>
+__global__ void k_first_two_keys(Text<TT> T, SampleLayout L, int b, const u32 *__restrict__ vals,
+                                 u64 *__restrict__ keys) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < L.m; i += (i64)gridDim.x * blockDim.x) {
+        i64 p = L.pos(vals[i]);
+        keys[i] = ((u64)T(p) << b) | (u64)T(p + 1);
+    }
+}
+
+struct FlagPacked {
+    const u64 *keys;
+    __device__ u32 operator()(i64 i) const { return (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u; }
+};
+template <typename TT>
+struct FlagGather {
+    Text<TT> T;
+    SampleLayout L;
+    const u32 *vals;
+    __device__ u32 operator()(i64 i) const {
+        if (i == 0) return 1u;
+        i64 p = L.pos(vals[i]), q = L.pos(vals[i - 1]);
+        return (T(p) != T(q) || T(p + 1) != T(q + 1) || T(p + 2) != T(q + 2)) ? 1u : 0u;
+    }
+};
+struct ScatterName {
+    const u32 *vals;
+    u32 *tt;
+    __device__ void operator()(i64 i, u32 excl, u32 v) const { tt[vals[i]] = excl + v; }
+};
+
+// all names distinct: the names are the 1-based sample ranks
+__global__ void k_unique_from_names(const u32 *__restrict__ tt, i64 m, u32 *__restrict__ sac,
+                                    u32 *__restrict__ isac) {
+    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < m; s += (i64)gridDim.x * blockDim.x) {
+        u32 r = tt[s] - 1u;
+        isac[s] = r;
+        sac[r] = (u32)s;
+    }
+}
+__global__ void k_unique_from_sorted(const u32 *__restrict__ vals, i64 m, u32 *__restrict__ sac,
+                                     u32 *__restrict__ isac) {
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (i64)gridDim.x * blockDim.x) {
+        u32 s = vals[r];
+        sac[r] = s;
+        isac[s] = (u32)r;
+    }
+}
+
+// ------------------------------------------------------------ mod-0 order
+
+template <typename TT>
+struct Mod1Flag {
+    const u32 *sac;
+    i64 m1;
+    __device__ u32 operator()(i64 i) const { return sac[i] < (u32)m1 ? 1u : 0u; }
+};
+template <typename TT>
+struct Mod0Emit {
+    Text<TT> T;
+    const u32 *sac;
+    u32 *keys;
+    u32 *vals;
+    __device__ void operator()(i64 i, u32 excl, u32 v) const {
+        if (v) {
+            u32 s = sac[i];
+            keys[excl] = T(3 * (i64)s);
+            vals[excl] = s;
+        }
+    }
+};
+
+// ------------------------------------------------------------ merge
+
+// Comparator of the merge step (suffix_index.py:192-202, `_merge_walk`):
+// suffix(a) < suffix(b) for sample position a and non-sample position b.
+template <typename TT, class Rank>
+__device__ __forceinline__ bool dc3_a_first(const Text<TT> &T, const Rank &R, i64 a, i64 b) {
+    u32 ca = T(a), cb = T(b);
+    if (ca != cb) return ca < cb;
+    if (a % 3 == 1) return R(a + 1) < R(b + 1);
+    u32 ca2 = T(a + 1), cb2 = T(b + 1);
+    if (ca2 != cb2) return ca2 < cb2;
+    return R(a + 2) < R(b + 2);
+}
+
+// 1-based sample rank by position from the child's 0-based ISA over sample
+// indices (the reference's `rank_of`, 0 at non-sample / beyond-limit spots).
+struct RankFromIsa {
+    SampleLayout L;
+    const u32 *isac;
+    __device__ __forceinline__ u32 operator()(i64 p) const {
+        i64 j = p / 3;
+        i64 r = p - 3 * j;
+        if (r == 1) return j < L.m1 ? isac[j] + 1u : 0u;
+        if (r == 2) return j < L.m2 ? isac[L.m1 + j] + 1u : 0u;
+        return 0u;
+    }
+};
+struct RankByPos {
+    const u32 *rank;
+    __device__ __forceinline__ u32 operator()(i64 p) const { return rank[p]; }
+};
+
+// Merge inputs: sorted samples as sample indices / sorted mod-0 as indices.
+template <typename TT>
+struct MergeIdx {
+    Text<TT> T;
+    RankFromIsa R;
+    const u32 *A, *B;
+    __device__ __forceinline__ i64 apos(i64 i) const { return R.L.pos(A[i]); }
+    __device__ __forceinline__ i64 bpos(i64 j) const { return 3 * (i64)B[j]; }
+    __device__ __forceinline__ bool a_first(i64 a, i64 b) const { return dc3_a_first(T, R, a, b); }
+};
+// Merge inputs given as positions with a by-position rank array
+// (merge_sample_nonsample, suffix_index.py:452-457).
+template <typename TT>
+struct MergePos {
+    Text<TT> T;
+    RankByPos R;
+    const u32 *A, *B;
+    __device__ __forceinline__ i64 apos(i64 i) const { return A[i]; }
+    __device__ __forceinline__ i64 bpos(i64 j) const { return B[j]; }
+    __device__ __forceinline__ bool a_first(i64 a, i64 b) const { return dc3_a_first(T, R, a, b); }
+};
+
+constexpr int MERGE_ITEMS = 8;
+
+// Merge path: each thread finds its diagonal split by binary search with
+// the DC3 comparator, then merges MERGE_ITEMS outputs; ISA scattered inline.
+template <class V>
+__global__ void k_merge(V v, i64 na, i64 nb, u32 *__restrict__ sa, u32 *__restrict__ isa) {
+    i64 total = na + nb;
+    i64 d0 = ((i64)blockIdx.x * blockDim.x + threadIdx.x) * MERGE_ITEMS;
+    if (d0 >= total) return;
+    i64 lo = d0 > nb ? d0 - nb : 0, hi = d0 < na ? d0 : na;
+    while (lo < hi) {
+        i64 mid = (lo + hi) >> 1;
+        if (v.a_first(v.apos(mid), v.bpos(d0 - 1 - mid))) lo = mid + 1;
+        else hi = mid;
+    }
+    i64 i = lo, j = d0 - lo;
+    for (int r = 0; r < MERGE_ITEMS && d0 + r < total; r++) {
+        i64 p;
+        if (j >= nb) p = v.apos(i++);
+        else if (i >= na) p = v.bpos(j++);
+        else {
+            i64 a = v.apos(i), b = v.bpos(j);
+            if (v.a_first(a, b)) { p = a; i++; }
+            else { p = b; j++; }
+        }
+        sa[d0 + r] = (u32)p;
+        if (isa) isa[p] = (u32)(d0 + r);
+    }
+}
+
+// ------------------------------------------------------------ probes
+
+__global__ void k_probe_rank(RankFromIsa R, i64 n3, u32 *__restrict__ out) {
+    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < n3; p += (i64)gridDim.x * blockDim.x)
+        out[p] = R(p);
+}
+__global__ void k_probe_samples(SampleLayout L, const u32 *__restrict__ sac, i64 from,
+                                u32 *__restrict__ out) {
+    for (i64 r = from + (i64)blockIdx.x * blockDim.x + threadIdx.x; r < L.m; r += (i64)gridDim.x * blockDim.x)
+        out[r - from] = (u32)L.pos(sac[r]);
+}
+__global__ void k_times3(const u32 *__restrict__ in, i64 k, u32 *__restrict__ out) {
+    for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (i64)gridDim.x * blockDim.x)
+        out[j] = 3u * in[j];
+}
+__global__ void k_iota_pair(u32 *sa, u32 *isa, i64 n) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        sa[i] = (u32)i;
+        if (isa) isa[i] = (u32)i;
+    }
+}
+
+// ------------------------------------------------------------ driver
+
+constexpr int K_THREADS = 256;
+constexpr u64 kBitmapMaxCodes = (u64)1 << 31;
+
+struct Dc3Ctx {
+    Arena *ar;
+    cudaStream_t st;
+    int max_depth;
+};
+
+static bool use_bitmap(u64 sigma, i64 m) {
+    u64 s1 = sigma + 1;
+    if (s1 >= ((u64)1 << 21)) return false;
+    u64 codes = s1 * s1 * s1;
+    if (codes > kBitmapMaxCodes) return false;
+    u64 words = codes / 32 + 1;
+    u64 lim = (u64)(2 * m) > ((u64)1 << 16) ? (u64)(2 * m) : ((u64)1 << 16);
+    return words <= lim;
+}
+
+static int read_u32(const u32 *d, u32 *h, cudaStream_t st) {
+    SAIX_CUDA(cudaMemcpyAsync(h, d, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    SAIX_CUDA(cudaStreamSynchronize(st));
+    return SAIX_OK;
+}
+
+template <typename TT>
+static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *ISA,
+                     saix_dc3_probe *probe, int depth);
+
+// Steps 1-2: names of the sample triples, then SAc/ISAc (recursing if needed).
+template <typename TT>
+static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma, u32 *tt,
+                        u32 *SAc, u32 *ISAc, u32 *d_scal, int depth) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    size_t mark = ar.mark();
+    i64 m = L.m;
+    int g = grid_for(m, K_THREADS);
+    u32 D = 0;
+    u32 *sorted_vals = nullptr;
+    if (use_bitmap(sigma, m)) {
+        u64 s1 = sigma + 1;
+        u64 codes = s1 * s1 * s1;
+        u32 nwords = (u32)(codes / 32 + 1);
+        u32 *bm = ar.alloc<u32>(nwords);
+        u32 *wp = ar.alloc<u32>(nwords);
+        u32 *tmp = ar.alloc<u32>(scan_tmp_words(nwords));
+        SAIX_ARENA_OK(ar);
+        SAIX_CUDA(cudaMemsetAsync(bm, 0, (size_t)nwords * 4, st));
+        int use_smem = nwords * 4 <= 48 * 1024;
+        int gs = use_smem ? (g < 2 * kNumSMs ? g : 2 * kNumSMs) : g;
+        k_bitmap_set<TT><<<gs, K_THREADS, use_smem ? nwords * 4 : 0, st>>>(T, L, s1, bm, nwords, use_smem);
+        SAIX_LAUNCHED();
+        SAIX_TRY(scan_transform(PopcIn{bm}, StoreExcl{wp}, nwords, tmp, d_scal, st));
+        k_bitmap_name<TT><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, tt);
+        SAIX_LAUNCHED();
+        SAIX_TRY(read_u32(d_scal, &D, st));
+    } else {
+        int b = bits_for(sigma);
+        u64 *k0 = ar.alloc<u64>(m), *k1 = ar.alloc<u64>(m);
+        u32 *v0 = ar.alloc<u32>(m), *v1 = ar.alloc<u32>(m);
+        u32 *scratch = ar.alloc<u32>(radix_scratch_words(m));
+        u32 *tmp = ar.alloc<u32>(scan_tmp_words(m));
+        SAIX_ARENA_OK(ar);
+        u64 *keys = k0;
+        u32 *vals = v0;
+        if (3 * b <= 64) {
+            k_triple_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, b, k0, v0);
+            SAIX_LAUNCHED();
+            SAIX_TRY(radix_sort_pairs<u64>(keys, vals, keys == k0 ? k1 : k0, vals == v0 ? v1 : v0, m, 0,
+                                           3 * b, scratch, st));
+            SAIX_TRY(scan_transform(FlagPacked{keys}, ScatterName{vals, tt}, m, tmp, d_scal, st));
+        } else {
+            k_third_char_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, k0, v0);
+            SAIX_LAUNCHED();
+            SAIX_TRY(radix_sort_pairs<u64>(keys, vals, k1, v1, m, 0, b, scratch, st));
+            u64 *ka = keys == k0 ? k1 : k0;
+            k_first_two_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, b, vals, ka);
+            SAIX_LAUNCHED();
+            keys = ka;
+            SAIX_TRY(radix_sort_pairs<u64>(keys, vals, keys == k0 ? k1 : k0, vals == v0 ? v1 : v0, m, 0,
+                                           2 * b, scratch, st));
+            SAIX_TRY(scan_transform(FlagGather<TT>{T, L, vals}, ScatterName{vals, tt}, m, tmp, d_scal, st));
+        }
+        sorted_vals = vals;
+        SAIX_TRY(read_u32(d_scal, &D, st));
+    }
+    if ((i64)D == m) {
+        if (sorted_vals) k_unique_from_sorted<<<g, K_THREADS, 0, st>>>(sorted_vals, m, SAc, ISAc);
+        else k_unique_from_names<<<g, K_THREADS, 0, st>>>(tt, m, SAc, ISAc);
+        SAIX_LAUNCHED();
+        ar.reset(mark);
+    } else {
+        ar.reset(mark);
+        SAIX_TRY(dc3_level<u32>(c, tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
+    }
+    return SAIX_OK;
+}
+
+template <typename TT>
+static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *ISA,
+                     saix_dc3_probe *probe, int depth) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    if (depth > c.max_depth) c.max_depth = depth;
+    if (N <= 1) {
+        if (N == 1) {
+            k_iota_pair<<<1, 32, 0, st>>>(SA, ISA, 1);
+            SAIX_LAUNCHED();
+        }
+        return SAIX_OK;
+    }
+    SampleLayout L = SampleLayout::of(N);
+    size_t mark0 = ar.mark();
+    u32 *tt = ar.alloc<u32>(L.m);
+    u32 *SAc = ar.alloc<u32>(L.m);
+    u32 *ISAc = ar.alloc<u32>(L.m);
+    u32 *d_scal = ar.alloc<u32>(8);
+    SAIX_ARENA_OK(ar);
+    Text<TT> T{text, N};
+
+    SAIX_TRY(sort_samples<TT>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth));
+
+    // step 3: mod-0 suffixes = mod-1 samples in rank order, minus one,
+    // stably split by their first character
+    size_t mark1 = ar.mark();
+    i64 k = L.k;
+    u32 *k0 = ar.alloc<u32>(k), *k1 = ar.alloc<u32>(k);
+    u32 *v0 = ar.alloc<u32>(k), *v1 = ar.alloc<u32>(k);
+    u32 *scratch = ar.alloc<u32>(radix_scratch_words(k));
+    u32 *tmp = ar.alloc<u32>(scan_tmp_words(L.m));
+    SAIX_ARENA_OK(ar);
+    SAIX_TRY(scan_transform(Mod1Flag<TT>{SAc, L.m1}, Mod0Emit<TT>{T, SAc, k0, v0}, L.m, tmp, nullptr, st));
+    u32 *keys = k0, *vals = v0;
+    SAIX_TRY(radix_sort_pairs<u32>(keys, vals, k1, v1, k, 0, bits_for(sigma), scratch, st));
+
+    // step 4: merge real samples (skip the padding sample at rank 1) with mod-0
+    RankFromIsa R{L, ISAc};
+    i64 pad = L.pad ? 1 : 0;
+    i64 na = L.m - pad;
+    i64 nthreads = ceil_div(N, MERGE_ITEMS);
+    MergeIdx<TT> V{T, R, SAc + pad, vals};
+    k_merge<MergeIdx<TT>><<<(unsigned)ceil_div(nthreads, K_THREADS), K_THREADS, 0, st>>>(V, na, k, SA, ISA);
+    SAIX_LAUNCHED();
+
+    if (probe) {
+        int g = grid_for(N + 3, K_THREADS);
+        if (probe->triple_text)
+            SAIX_CUDA(cudaMemcpyAsync(probe->triple_text, tt, (size_t)L.m * 4, cudaMemcpyDeviceToDevice, st));
+        if (probe->sample_rank) {
+            k_probe_rank<<<g, K_THREADS, 0, st>>>(R, N + 3, probe->sample_rank);
+            SAIX_LAUNCHED();
+        }
+        if (probe->sorted_samples) {
+            k_probe_samples<<<g, K_THREADS, 0, st>>>(L, SAc, pad, probe->sorted_samples);
+            SAIX_LAUNCHED();
+        }
+        if (probe->sorted_nonsamples) {
+            k_times3<<<g, K_THREADS, 0, st>>>(vals, k, probe->sorted_nonsamples);
+            SAIX_LAUNCHED();
+        }
+        probe->n_samples = L.m;
+        probe->n_sorted_samples = na;
+        probe->n_sorted_nonsamples = k;
+    }
+    (void)mark1;
+    ar.reset(mark0);
+    return SAIX_OK;
+}
+
+// Upper bound of the workspace the driver carves (persistent arrays of every
+// level + the largest level's temporaries), see DESIGN.md "DC3 workspace".
+static size_t dc3_plan(i64 n) {
+    size_t persistent = 0, temps = 0;
+    i64 N = n;
+    while (N > 1) {
+        SampleLayout L = SampleLayout::of(N);
+        i64 m = L.m, k = L.k;
+        persistent += (size_t)(3 * m + 8) * 4 + 4 * Arena::kAlign;
+        size_t sort_t = (size_t)m * 24 + (size_t)(radix_scratch_words(m) + scan_tmp_words(m)) * 4;
+        i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
+        size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
+        size_t post_t = (size_t)k * 16 + (size_t)(radix_scratch_words(k) + scan_tmp_words(m)) * 4;
+        size_t t = sort_t > bm_t ? sort_t : bm_t;
+        t = t > post_t ? t : post_t;
+        t += 8 * Arena::kAlign;
+        if (t > temps) temps = t;
+        N = m;
+    }
+    return persistent + temps + (1 << 16);
+}
+
+}  // namespace saix
+
+using namespace saix;
+
+extern "C" size_t saix_dc3_workspace_bytes(int64_t n, int text_bytes) {
+    (void)text_bytes;
+    return dc3_plan(n);
+}
+
+extern "C" int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sigma, uint32_t *sa,
+                        uint32_t *isa, void *ws, size_t ws_bytes, saix_dc3_probe *probe, void *stream) {
+    if (n < 0 || n > (int64_t)0xFFFFFFF0LL || (text_bytes != 1 && text_bytes != 4) || sigma < 1 ||
+        (n > 0 && (!text || !sa))) {
+        set_error("saix_dc3: invalid arguments (n=%lld, text_bytes=%d, sigma=%lld)", (long long)n,
+                  text_bytes, (long long)sigma);
+        return SAIX_EINVAL;
+    }
+    if (text_bytes == 1 && sigma > 255) {
+        set_error("saix_dc3: sigma %lld does not fit u8 text", (long long)sigma);
+        return SAIX_EINVAL;
+    }
+    if (ws_bytes < dc3_plan(n)) {
+        set_error("saix_dc3: workspace %zu < %zu bytes", ws_bytes, dc3_plan(n));
+        return SAIX_ENOSPC;
+    }
+    Arena ar;
+    ar.base = (char *)ws;
+    ar.cap = ws_bytes;
+    Dc3Ctx c{&ar, (cudaStream_t)stream, 0};
+    if (probe) {
+        probe->depth = 0;
+        probe->n_samples = probe->n_sorted_samples = 0;
+        probe->n_sorted_nonsamples = 0;
+    }
+    if (n == 0) return SAIX_OK;
+    if (n == 1) {
+        // Dc3Workspace of a single character: pad sample 1 names (0,0,0)
+        k_iota_pair<<<1, 32, 0, (cudaStream_t)stream>>>(sa, isa, 1);
+        SAIX_LAUNCHED();
+        if (probe) {
+            u32 h[4] = {1u, 0u, 0u, 0u};
+            if (probe->triple_text)
+                SAIX_CUDA(cudaMemcpyAsync(probe->triple_text, h, 4, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+            if (probe->sample_rank) {
+                u32 r[4] = {0u, 1u, 0u, 0u};
+                SAIX_CUDA(cudaMemcpyAsync(probe->sample_rank, r, 16, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+            }
+            if (probe->sorted_nonsamples)
+                SAIX_CUDA(cudaMemsetAsync(probe->sorted_nonsamples, 0, 4, (cudaStream_t)stream));
+            probe->n_samples = 1;
+            probe->n_sorted_nonsamples = 1;
+            SAIX_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+        }
+        return SAIX_OK;
+    }
+    int rc = text_bytes == 1
+                 ? dc3_level<u8>(c, (const u8 *)text, n, (u64)sigma, sa, isa, probe, 0)
+                 : dc3_level<u32>(c, (const u32 *)text, n, (u64)sigma, sa, isa, probe, 0);
+    if (rc) return rc;
+    if (probe) probe->depth = c.max_depth;
+    return SAIX_OK;
+}
+
+extern "C" int saix_dc3_merge(const void *text, int text_bytes, int64_t n, const uint32_t *sample_rank,
+                              const uint32_t *sorted_samples, int64_t ms, const uint32_t *sorted_nonsamples,
+                              int64_t k, uint32_t *sa, void *stream) {
+    if (n < 0 || ms < 0 || k < 0 || (text_bytes != 1 && text_bytes != 4) || ms + k > n + 1) {
+        set_error("saix_dc3_merge: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    i64 total = ms + k;
+    if (total == 0) return SAIX_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned grid = (unsigned)ceil_div(ceil_div(total, MERGE_ITEMS), K_THREADS);
+    if (text_bytes == 1) {
+        MergePos<u8> V{Text<u8>{(const u8 *)text, n}, RankByPos{sample_rank}, sorted_samples, sorted_nonsamples};
+        k_merge<MergePos<u8>><<<grid, K_THREADS, 0, st>>>(V, ms, k, sa, nullptr);
+    } else {
+        MergePos<u32> V{Text<u32>{(const u32 *)text, n}, RankByPos{sample_rank}, sorted_samples, sorted_nonsamples};
+        k_merge<MergePos<u32>><<<grid, K_THREADS, 0, st>>>(V, ms, k, sa, nullptr);
+    }
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}

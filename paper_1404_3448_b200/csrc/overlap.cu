@@ -1,0 +1,361 @@
+// overlap.cu -- encode / generalized text and the longest-overlap scan
+// (overlap.py:72-152) on sm_100a, plus the end-to-end pair pipeline.
+//
+// Scan, two streaming passes over the GSA's (sa, lcp):
+//   pass 1  best = max lcp[i] over adjacent pairs whose suffixes start on
+//           opposite sides of the separator (overlap.py:129-136); block max +
+//           one atomicMax per CTA.
+//   pass 2  runs = maximal SA intervals with lcp >= best; per run min A-pos /
+//           min B-pos (overlap.py:138-152) as a segmented min-scan
+//           (reduce -> scan tile carries -> apply).  Every A position lies in
+//           exactly one run, so the reference's lexicographic (minA, minB)
+//           choice is a u64 atomicMin of (minA << 32 | minB) at run ends.
+#include "scan.cuh"
+
+namespace saix {
+
+// ------------------------------------------------------------ encode
+
+__device__ __forceinline__ u32 rank_of_ascii(u32 c, int keep_n) {
+    // encode LUT (sequence.py:144-150): A1 C2 G3 T4, N5 under NPolicy.KEEP
+    switch (c) {
+        case 'A': return 1;
+        case 'C': return 2;
+        case 'G': return 3;
+        case 'T': return 4;
+        case 'N': return keep_n ? 5u : 0u;
+        default: return 0;
+    }
+}
+
+__global__ void k_encode_gsa(const u8 *__restrict__ a, i64 na, const u8 *__restrict__ b, i64 nb, int keep_n,
+                             int shift, u8 *__restrict__ out, i64 *__restrict__ bad) {
+    i64 n = na + nb + (b ? 1 : 0);
+    i64 local_bad = INT64_MAX;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        u32 r;
+        if (i < na) r = rank_of_ascii(a[i], keep_n);
+        else if (i == na) r = 0xFFu;  // separator
+        else r = rank_of_ascii(b[i - na - 1], keep_n);
+        if (r == 0) {
+            if (i < local_bad) local_bad = i;
+            r = 1;
+        }
+        out[i] = r == 0xFFu ? 1u : (u8)(r + shift);
+    }
+    if (local_bad != INT64_MAX) atomicMin((unsigned long long *)bad, (unsigned long long)local_bad);
+}
+
+// ------------------------------------------------------------ pass 1
+
+constexpr int OV_THREADS = 256;
+constexpr int OV_ITEMS = 16;
+constexpr int OV_TILE = OV_THREADS * OV_ITEMS;
+
+__device__ __forceinline__ int side_of(u32 p, u32 boundary) { return p < boundary ? 0 : (p > boundary ? 1 : -1); }
+
+__global__ void __launch_bounds__(OV_THREADS)
+k_cross_max(const u32 *__restrict__ sa, const u32 *__restrict__ lcp, i64 n, u32 boundary, u32 *best) {
+    u32 mx = 0;
+    for (i64 i = 1 + (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        int a = side_of(sa[i - 1], boundary), b = side_of(sa[i], boundary);
+        if (a >= 0 && b >= 0 && a != b) mx = max(mx, lcp[i]);
+    }
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ u32 sh[OV_THREADS / 32];
+    if (lane_id() == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        mx = threadIdx.x < OV_THREADS / 32 ? sh[threadIdx.x] : 0;
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (threadIdx.x == 0 && mx) atomicMax(best, mx);
+    }
+}
+
+// ------------------------------------------------------------ pass 2
+
+struct Seg {  // segmented-min state: head flag + min A / min B position
+    u32 f, a, b;
+};
+__device__ __forceinline__ Seg seg_combine(Seg l, Seg r) {
+    if (r.f) return r;
+    return Seg{l.f, min(l.a, r.a), min(l.b, r.b)};
+}
+__device__ __forceinline__ Seg seg_shfl_up(Seg s, int o) {
+    return Seg{__shfl_up_sync(0xffffffffu, s.f, o), __shfl_up_sync(0xffffffffu, s.a, o),
+               __shfl_up_sync(0xffffffffu, s.b, o)};
+}
+constexpr u32 kInf = 0xFFFFFFFFu;
+
+__device__ __forceinline__ Seg seg_elem(u32 p, u32 l, i64 i, u32 best, u32 boundary) {
+    Seg s;
+    s.f = (i == 0 || l < best) ? 1u : 0u;
+    s.a = p < boundary ? p : kInf;
+    s.b = p > boundary ? p : kInf;
+    return s;
+}
+
+// Block-wide exclusive segmented scan of per-thread aggregates; returns the
+// carry-in for this thread and the block aggregate.
+__device__ Seg block_seg_exclusive(Seg v, Seg &block_total) {
+    __shared__ Seg sh[OV_THREADS / 32 + 1];
+    int w = threadIdx.x >> 5, lane = lane_id();
+    Seg inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        Seg y = seg_shfl_up(inc, o);
+        if (lane >= o) inc = seg_combine(y, inc);
+    }
+    if (lane == 31) sh[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        Seg x = lane < OV_THREADS / 32 ? sh[lane] : Seg{0u, kInf, kInf};
+        Seg xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            Seg y = seg_shfl_up(xi, o);
+            if (lane >= o) xi = seg_combine(y, xi);
+        }
+        Seg ex = seg_shfl_up(xi, 1);
+        if (lane == 0) ex = Seg{0u, kInf, kInf};
+        if (lane < OV_THREADS / 32) sh[lane] = ex;
+        if (lane == OV_THREADS / 32 - 1) sh[OV_THREADS / 32] = xi;
+    }
+    __syncthreads();
+    Seg prev = seg_shfl_up(inc, 1);
+    Seg carry = sh[w];
+    if (lane > 0) carry = seg_combine(carry, prev);
+    block_total = sh[OV_THREADS / 32];
+    __syncthreads();
+    return carry;
+}
+
+__device__ __forceinline__ void load_tile(const u32 *__restrict__ sa, const u32 *__restrict__ lcp, i64 n, i64 base,
+                                          u32 *sh_sa, u32 *sh_l) {
+    for (int x = threadIdx.x; x < OV_TILE; x += OV_THREADS) {
+        i64 i = base + x;
+        sh_sa[x + (x >> 5)] = i < n ? sa[i] : 0u;  // never read past n
+        sh_l[x + (x >> 5)] = i < n ? lcp[i] : 0u;
+    }
+}
+
+__global__ void __launch_bounds__(OV_THREADS)
+k_runs_reduce(const u32 *__restrict__ sa, const u32 *__restrict__ lcp, i64 n, const u32 *__restrict__ best_p,
+              u32 boundary, Seg *__restrict__ tile_agg) {
+    __shared__ u32 sh_sa[OV_TILE + OV_TILE / 32], sh_l[OV_TILE + OV_TILE / 32];
+    u32 best = *best_p;
+    i64 base = (i64)blockIdx.x * OV_TILE;
+    if (best == 0) {
+        if (threadIdx.x == 0) tile_agg[blockIdx.x] = Seg{0u, kInf, kInf};
+        return;
+    }
+    load_tile(sa, lcp, n, base, sh_sa, sh_l);
+    __syncthreads();
+    Seg acc{0u, kInf, kInf};
+    for (int r = 0; r < OV_ITEMS; r++) {
+        int x = threadIdx.x * OV_ITEMS + r;
+        i64 i = base + x;
+        if (i >= n) break;
+        acc = seg_combine(acc, seg_elem(sh_sa[x + (x >> 5)], sh_l[x + (x >> 5)], i, best, boundary));
+    }
+    Seg tot;
+    block_seg_exclusive(acc, tot);
+    if (threadIdx.x == 0) tile_agg[blockIdx.x] = tot;
+}
+
+// Single CTA: exclusive segmented scan of tile aggregates (tile carries).
+__global__ void __launch_bounds__(OV_THREADS) k_runs_carry(Seg *__restrict__ agg, i64 ntiles) {
+    Seg carry{0u, kInf, kInf};
+    for (i64 c = 0; c < ntiles; c += OV_THREADS) {
+        i64 t = c + threadIdx.x;
+        Seg v = t < ntiles ? agg[t] : Seg{0u, kInf, kInf};
+        Seg tot;
+        Seg ex = block_seg_exclusive(v, tot);
+        if (t < ntiles) agg[t] = seg_combine(carry, ex);
+        carry = seg_combine(carry, tot);
+    }
+}
+
+__global__ void __launch_bounds__(OV_THREADS)
+k_runs_apply(const u32 *__restrict__ sa, const u32 *__restrict__ lcp, i64 n, const u32 *__restrict__ best_p,
+             u32 boundary, const Seg *__restrict__ tile_carry, unsigned long long *__restrict__ winner) {
+    __shared__ u32 sh_sa[OV_TILE + OV_TILE / 32], sh_l[OV_TILE + OV_TILE / 32];
+    u32 best = *best_p;
+    if (best == 0) return;
+    i64 base = (i64)blockIdx.x * OV_TILE;
+    load_tile(sa, lcp, n, base, sh_sa, sh_l);
+    __syncthreads();
+    Seg acc{0u, kInf, kInf};
+    for (int r = 0; r < OV_ITEMS; r++) {
+        int x = threadIdx.x * OV_ITEMS + r;
+        i64 i = base + x;
+        if (i >= n) break;
+        acc = seg_combine(acc, seg_elem(sh_sa[x + (x >> 5)], sh_l[x + (x >> 5)], i, best, boundary));
+    }
+    Seg tot;
+    Seg carry = seg_combine(tile_carry[blockIdx.x], block_seg_exclusive(acc, tot));
+    Seg run = carry;
+    for (int r = 0; r < OV_ITEMS; r++) {
+        int x = threadIdx.x * OV_ITEMS + r;
+        i64 i = base + x;
+        if (i >= n) break;
+        run = seg_combine(run, seg_elem(sh_sa[x + (x >> 5)], sh_l[x + (x >> 5)], i, best, boundary));
+        bool end;
+        if (i + 1 >= n) end = true;
+        else if (x + 1 < OV_TILE) end = sh_l[(x + 1) + ((x + 1) >> 5)] < best;
+        else end = lcp[i + 1] < best;
+        if (end && run.a != kInf && run.b != kInf)
+            atomicMin(winner, ((unsigned long long)run.a << 32) | run.b);
+    }
+}
+
+__global__ void k_overlap_finish(const u32 *__restrict__ best_p, const unsigned long long *__restrict__ winner,
+                                 u32 boundary, i64 *__restrict__ out3) {
+    u32 best = *best_p;
+    unsigned long long w = *winner;
+    if (best == 0 || w == ~0ull) {
+        out3[0] = out3[1] = out3[2] = 0;
+    } else {
+        out3[0] = best;
+        out3[1] = (i64)(w >> 32);
+        out3[2] = (i64)(w & 0xFFFFFFFFull) - (i64)boundary - 1;
+    }
+}
+
+struct OverlapWs {
+    u32 *best;
+    unsigned long long *winner;
+    Seg *agg;
+};
+
+static OverlapWs carve_overlap(Arena &ar, i64 n) {
+    OverlapWs w;
+    w.best = ar.alloc<u32>(2);
+    w.winner = ar.alloc<unsigned long long>(1);
+    w.agg = ar.alloc<Seg>(ceil_div(n > 0 ? n : 1, OV_TILE) + 1);
+    return w;
+}
+
+static int overlap_scan(const u32 *sa, const u32 *lcp, i64 n, i64 boundary, i64 *out3, OverlapWs w,
+                        cudaStream_t st) {
+    SAIX_CUDA(cudaMemsetAsync(w.best, 0, sizeof(u32), st));
+    SAIX_CUDA(cudaMemsetAsync(w.winner, 0xFF, sizeof(unsigned long long), st));
+    i64 ntiles = ceil_div(n, OV_TILE);
+    int g = grid_for(n, OV_THREADS, kNumSMs * 8);
+    k_cross_max<<<g, OV_THREADS, 0, st>>>(sa, lcp, n, (u32)boundary, w.best);
+    SAIX_LAUNCHED();
+    k_runs_reduce<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg);
+    SAIX_LAUNCHED();
+    k_runs_carry<<<1, OV_THREADS, 0, st>>>(w.agg, ntiles);
+    SAIX_LAUNCHED();
+    k_runs_apply<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg, w.winner);
+    SAIX_LAUNCHED();
+    k_overlap_finish<<<1, 1, 0, st>>>(w.best, w.winner, (u32)boundary, out3);
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}
+
+}  // namespace saix
+
+using namespace saix;
+
+extern "C" int saix_encode_gsa(const uint8_t *a_ascii, int64_t na, const uint8_t *b_ascii, int64_t nb, int keep_n,
+                               uint8_t *gsa, int64_t *bad_pos, void *stream) {
+    if (na < 0 || nb < 0 || !gsa || !bad_pos || (na && !a_ascii) || (nb && !b_ascii)) {
+        set_error("saix_encode_gsa: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    i64 n = na + nb + 1;
+    k_encode_gsa<<<grid_for(n, 256), 256, 0, st>>>(a_ascii, na, b_ascii ? b_ascii : a_ascii, nb, keep_n, 1, gsa,
+                                                     bad_pos);
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}
+
+extern "C" int saix_encode(const uint8_t *ascii, int64_t n, int keep_n, uint8_t *ranks, int64_t *bad_pos,
+                           void *stream) {
+    if (n < 0 || (n && (!ascii || !ranks)) || !bad_pos) {
+        set_error("saix_encode: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    if (n == 0) return SAIX_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_encode_gsa<<<grid_for(n, 256), 256, 0, st>>>(ascii, n, nullptr, 0, keep_n, 0, ranks, bad_pos);
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}
+
+extern "C" size_t saix_overlap_workspace_bytes(int64_t n) {
+    Arena ar;
+    carve_overlap(ar, n);
+    return ar.peak + Arena::kAlign;
+}
+
+extern "C" int saix_overlap_scan(const uint32_t *sa, const uint32_t *lcp, int64_t n, int64_t boundary, int64_t *out3,
+                                 void *ws, size_t ws_bytes, void *stream) {
+    if (n < 0 || !out3 || (n > 0 && (!sa || !lcp)) || boundary < 0 || boundary >= (n > 0 ? n : 1)) {
+        set_error("saix_overlap_scan: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    Arena ar{(char *)ws, ws_bytes};
+    OverlapWs w = carve_overlap(ar, n);
+    SAIX_ARENA_OK(ar);
+    return overlap_scan(sa, lcp, n, boundary, out3, w, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------ pipeline
+
+namespace saix {
+struct PairWs {
+    u8 *gsa;
+    u32 *sa, *isa, *lcp;
+    OverlapWs ov;
+    void *rest;
+    size_t rest_bytes;
+};
+static size_t pair_ws(Arena &ar, i64 n, PairWs *w) {
+    PairWs t;
+    t.gsa = ar.alloc<u8>(n + 8);
+    t.sa = ar.alloc<u32>(n);
+    t.isa = ar.alloc<u32>(n);
+    t.lcp = ar.alloc<u32>(n);
+    t.ov = carve_overlap(ar, n);
+    size_t need = saix_dc3_workspace_bytes(n, 1);
+    size_t l = saix_lcp_workspace_bytes(n);
+    if (l > need) need = l;
+    t.rest = ar.alloc<char>((i64)need);
+    t.rest_bytes = need;
+    if (w) *w = t;
+    return ar.peak;
+}
+}  // namespace saix
+
+extern "C" size_t saix_longest_overlap_workspace_bytes(int64_t na, int64_t nb) {
+    Arena ar;
+    return pair_ws(ar, na + nb + 1, nullptr) + Arena::kAlign;
+}
+
+extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const uint8_t *b_ascii, int64_t nb,
+                                    int keep_n, int64_t *out3, int64_t *bad_pos, void *ws, size_t ws_bytes,
+                                    void *stream) {
+    if (na < 0 || nb < 0 || !out3 || !bad_pos) {
+        set_error("saix_longest_overlap: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    SAIX_CUDA(cudaMemsetAsync(bad_pos, 0x7F, sizeof(int64_t), st));
+    if (na == 0 || nb == 0) {  // overlap.py:120-121
+        // the reference returns before encoding, so nothing is validated
+        SAIX_CUDA(cudaMemsetAsync(out3, 0, 3 * sizeof(int64_t), st));
+        return SAIX_OK;
+    }
+    i64 n = na + nb + 1;
+    Arena ar{(char *)ws, ws_bytes};
+    PairWs w;
+    pair_ws(ar, n, &w);
+    SAIX_ARENA_OK(ar);
+    SAIX_TRY(saix_encode_gsa(a_ascii, na, b_ascii, nb, keep_n, w.gsa, bad_pos, stream));
+    int sigma = (keep_n ? 5 : 4) + 1;  // max(sigma_A, sigma_B) + 1 (overlap.py:88)
+    SAIX_TRY(saix_dc3(w.gsa, 1, n, sigma, w.sa, w.isa, w.rest, w.rest_bytes, nullptr, stream));
+    SAIX_TRY(saix_lcp(w.gsa, 1, n, w.sa, w.isa, w.lcp, w.rest, w.rest_bytes, stream));
+    return overlap_scan(w.sa, w.lcp, n, na, out3, w.ov, st);
+}

@@ -1,0 +1,207 @@
+"""LCP queries and longest-overlap search on the B200 -- drop-in for
+``saix.overlap`` (overlap.py:28-180).
+
+``longest_overlap`` runs end to end on the device: ASCII A and B are copied
+once, encoded into the generalized text on the GPU, and DC3, Kasai LCP and
+the two-pass overlap scan run back to back on one stream; only the three
+result integers (plus the residue-check word) come back.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+from dataclasses import dataclass, field
+from typing import Any, Literal
+
+import numpy as np
+
+from . import _lib
+from .rmq import SparseTable
+from .sequence import (DnaSequence, NPolicy, RankedText, SequenceError, alphabet, encode,
+                       residue_error)
+from .suffix_index import (LcpArray, SuffixArray, _device_index_of, build_lcp, build_sa_dc3)
+
+RmqKind = Literal["sparse", "cartesian"]
+
+SEPARATOR_RANK = 1  # between the padding sentinel 0 and every residue rank
+INT64_MAX = np.iinfo(np.int64).max
+
+
+@dataclass(frozen=True, eq=False)
+class LcpQueryEngine:
+    """Text + suffix array + LCP array + RMQ over the LCP (overlap.py:28-55)."""
+
+    text: RankedText
+    sa: SuffixArray
+    lcp: LcpArray
+    rmq: SparseTable | None
+    _isa_dev: Any = field(default=None, repr=False, compare=False)
+
+    @classmethod
+    def build(cls, text: RankedText, rmq_kind: RmqKind = "sparse",
+              sa: SuffixArray | None = None) -> "LcpQueryEngine":
+        sa = sa or build_sa_dc3(text)
+        lcp = build_lcp(text, sa)
+        return cls.from_parts(text, sa, lcp, rmq_kind)
+
+    @classmethod
+    def from_parts(cls, text: RankedText, sa: SuffixArray, lcp: LcpArray,
+                   rmq_kind: RmqKind = "sparse") -> "LcpQueryEngine":
+        if rmq_kind not in ("sparse", "cartesian"):
+            raise ValueError(f"unknown rmq kind {rmq_kind!r}")
+        if text.n == 0:
+            return cls(text=text, sa=sa, lcp=lcp, rmq=None)
+        # both engines answer leftmost-argmin identically (rmq.py:1-15); the
+        # device sparse table serves either kind
+        dev_vals = (lcp._dev[1], 4) if lcp._dev is not None else None
+        rmq = SparseTable(lcp.lcp, _device_values=dev_vals)
+        isa = _device_index_of(text, sa).isa
+        return cls(text=text, sa=sa, lcp=lcp, rmq=rmq, _isa_dev=isa)
+
+
+def lcp_query_batch(engine: LcpQueryEngine, i, j) -> np.ndarray:
+    """Vectorised ``lcp_query`` (overlap.py:58-69): one device kernel."""
+    n = engine.text.n
+    qi = np.ascontiguousarray(i, dtype=np.int64)
+    qj = np.ascontiguousarray(j, dtype=np.int64)
+    if qi.shape != qj.shape:
+        raise ValueError("i and j must have the same shape")
+    if qi.size == 0:
+        return np.zeros(qi.shape, np.int64)
+    if n == 0:
+        raise IndexError(f"positions ({int(qi.ravel()[0])}, {int(qj.ravel()[0])}) "
+                         f"out of bounds for length 0")
+    st = engine.rmq
+    t = _lib.torch()
+    L = _lib.load()
+    di, dj = _lib.to_device(qi.ravel()), _lib.to_device(qj.ravel())
+    out = t.empty(qi.size, dtype=t.int64, device=di.device)
+    st._err.zero_()
+    rc = L.saix_lcp_query(ctypes.byref(st.plan), _lib.ptr(st._table), _lib.ptr(st._vals), st._vbytes,
+                          _lib.ptr(engine._isa_dev), _lib.ptr(di), _lib.ptr(dj), qi.size, _lib.ptr(out),
+                          _lib.ptr(st._err), _lib.stream_ptr())
+    _lib.check(rc, "saix_lcp_query")
+    res = out.cpu().numpy()
+    if int(st._err.item()):
+        f = qi.ravel(), qj.ravel()
+        bad = np.flatnonzero((f[0] < 0) | (f[0] >= n) | (f[1] < 0) | (f[1] >= n))[0]
+        raise IndexError(f"positions ({int(f[0][bad])}, {int(f[1][bad])}) out of bounds for length {n}")
+    return res.reshape(qi.shape)
+
+
+def lcp_query(engine: LcpQueryEngine, i: int, j: int) -> int:
+    """Longest common prefix of suffix(i) and suffix(j) (overlap.py:58-69)."""
+    n = engine.text.n
+    if not (0 <= i < n) or not (0 <= j < n):
+        raise IndexError(f"positions ({i}, {j}) out of bounds for length {n}")
+    return int(lcp_query_batch(engine, np.array([i]), np.array([j]))[0])
+
+
+@dataclass(frozen=True, eq=False)
+class GeneralizedText:
+    """encode(A)+1 ++ [separator 1] ++ encode(B)+1 (overlap.py:72-98)."""
+
+    ranks: np.ndarray
+    boundary: int
+    len_a: int
+    len_b: int
+    sigma: int
+
+    @classmethod
+    def build(cls, a: DnaSequence, b: DnaSequence,
+              policy: NPolicy = NPolicy.REJECT) -> "GeneralizedText":
+        ra, rb = encode(a, policy), encode(b, policy)
+        ranks = np.concatenate([ra.ranks + 1, np.array([SEPARATOR_RANK], np.int64), rb.ranks + 1])
+        return cls(ranks=ranks, boundary=ra.n, len_a=ra.n, len_b=rb.n,
+                   sigma=max(ra.sigma, rb.sigma) + 1)
+
+    def to_ranked_text(self) -> RankedText:
+        return RankedText(ranks=self.ranks, sigma=self.sigma)
+
+
+@dataclass(frozen=True)
+class OverlapResult:
+    """Longest common substring of A and B; zero length pins positions to 0."""
+
+    length: int
+    pos_a: int
+    pos_b: int
+
+
+def _ascii(seq: DnaSequence) -> np.ndarray:
+    return np.frombuffer(seq.residues.encode("ascii"), dtype=np.uint8)
+
+
+class OverlapPipeline:
+    """Reusable device buffers for the end-to-end pair pipeline
+    (saix_longest_overlap): ASCII in, (length, pos_a, pos_b) out."""
+
+    def __init__(self, na: int, nb: int):
+        t = _lib.torch()
+        L = _lib.load()
+        dev = _lib.device()
+        self.na, self.nb = na, nb
+        self.a = t.empty(max(na, 1), dtype=t.uint8, device=dev)
+        self.b = t.empty(max(nb, 1), dtype=t.uint8, device=dev)
+        self.res = t.zeros(4, dtype=t.int64, device=dev)  # out3 + bad_pos
+        self.ws = _lib.workspace(L.saix_longest_overlap_workspace_bytes(na, nb))
+
+    def run_device(self, policy: NPolicy = NPolicy.REJECT) -> None:
+        """Run on the already-resident self.a / self.b (no host traffic)."""
+        L = _lib.load()
+        rc = L.saix_longest_overlap(_lib.ptr(self.a), self.na, _lib.ptr(self.b), self.nb,
+                                    int(policy is NPolicy.KEEP), _lib.ptr(self.res),
+                                    _lib.ptr(self.res) + 24, _lib.ptr(self.ws), self.ws.numel(),
+                                    _lib.stream_ptr())
+        _lib.check(rc, "saix_longest_overlap")
+
+    def run(self, a_host, b_host, policy: NPolicy = NPolicy.REJECT) -> np.ndarray:
+        """Host ASCII in, host int64[4] (length, pos_a, pos_b, bad_pos) out."""
+        t = _lib.torch()
+        self.a[: self.na].copy_(t.from_numpy(a_host), non_blocking=True)
+        self.b[: self.nb].copy_(t.from_numpy(b_host), non_blocking=True)
+        self.run_device(policy)
+        return self.res.cpu().numpy()
+
+
+def longest_overlap(a: DnaSequence, b: DnaSequence,
+                    policy: NPolicy = NPolicy.REJECT) -> OverlapResult:
+    """Longest common substring of A and B via the generalized suffix array
+    (overlap.py:110-152), ties to the smallest A position then B position."""
+    if len(a) == 0 or len(b) == 0:
+        return OverlapResult(0, 0, 0)
+    ha, hb = _ascii(a), _ascii(b)
+    res = OverlapPipeline(len(ha), len(hb)).run(ha, hb, policy)
+    bad = int(res[3])
+    if bad != INT64_MAX:
+        if bad < len(ha):
+            raise residue_error(a, bad, policy)
+        raise residue_error(b, bad - len(ha) - 1, policy)
+    return OverlapResult(int(res[0]), int(res[1]), int(res[2]))
+
+
+def overlap_report(result: OverlapResult, a: DnaSequence, b: DnaSequence) -> tuple[str, str]:
+    """Human summary + one-object JSON record (overlap.py:155-173)."""
+    sub = a.residues[result.pos_a:result.pos_a + result.length]
+    if sub != b.residues[result.pos_b:result.pos_b + result.length]:
+        raise ValueError("overlap result does not match the given sequences")
+    record = {"length": result.length, "posA": result.pos_a, "posB": result.pos_b,
+              "substring": sub}
+    if result.length:
+        human = (f"overlap of {result.length} residues: {a.id}[{result.pos_a}] "
+                 f"= {b.id}[{result.pos_b}] = {sub!r}")
+    else:
+        human = f"no overlap between {a.id} and {b.id}"
+    return human, json.dumps(record)
+
+
+def parse_overlap_record(payload: str) -> OverlapResult:
+    """Inverse of the JSON half of overlap_report (overlap.py:176-180)."""
+    rec = json.loads(payload)
+    return OverlapResult(length=rec["length"], pos_a=rec["posA"], pos_b=rec["posB"])
+
+
+__all__ = ["GeneralizedText", "LcpQueryEngine", "OverlapPipeline", "OverlapResult",
+           "SequenceError", "alphabet", "lcp_query", "lcp_query_batch", "longest_overlap",
+           "overlap_report", "parse_overlap_record"]
