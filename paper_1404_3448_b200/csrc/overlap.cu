@@ -207,6 +207,11 @@ k_runs_apply(const u32 *__restrict__ sa, const u32 *__restrict__ lcp, i64 n, con
     }
 }
 
+__global__ void k_pipeline_init(i64 *__restrict__ out3, i64 *__restrict__ bad) {
+    out3[0] = out3[1] = out3[2] = 0;
+    *bad = INT64_MAX;
+}
+
 __global__ void k_overlap_finish(const u32 *__restrict__ best_p, const unsigned long long *__restrict__ winner,
                                  u32 boundary, i64 *__restrict__ out3) {
     u32 best = *best_p;
@@ -342,12 +347,10 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
         return SAIX_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    SAIX_CUDA(cudaMemsetAsync(bad_pos, 0x7F, sizeof(int64_t), st));
-    if (na == 0 || nb == 0) {  // overlap.py:120-121
-        // the reference returns before encoding, so nothing is validated
-        SAIX_CUDA(cudaMemsetAsync(out3, 0, 3 * sizeof(int64_t), st));
-        return SAIX_OK;
-    }
+    k_pipeline_init<<<1, 1, 0, st>>>(out3, bad_pos);
+    SAIX_LAUNCHED();
+    // overlap.py:120-121: empty input returns before encoding (no validation)
+    if (na == 0 || nb == 0) return SAIX_OK;
     i64 n = na + nb + 1;
     Arena ar{(char *)ws, ws_bytes};
     PairWs w;

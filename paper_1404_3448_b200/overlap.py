@@ -146,6 +146,10 @@ class OverlapPipeline:
         self.b = t.empty(max(nb, 1), dtype=t.uint8, device=dev)
         self.res = t.zeros(4, dtype=t.int64, device=dev)  # out3 + bad_pos
         self.ws = _lib.workspace(L.saix_longest_overlap_workspace_bytes(na, nb))
+        # pinned host staging: the e2e path copies host ASCII in and 32 B out
+        self.ha = t.empty(max(na, 1), dtype=t.uint8, pin_memory=True)
+        self.hb = t.empty(max(nb, 1), dtype=t.uint8, pin_memory=True)
+        self.hres = t.empty(4, dtype=t.int64, pin_memory=True)
 
     def run_device(self, policy: NPolicy = NPolicy.REJECT) -> None:
         """Run on the already-resident self.a / self.b (no host traffic)."""
@@ -156,13 +160,24 @@ class OverlapPipeline:
                                     _lib.stream_ptr())
         _lib.check(rc, "saix_longest_overlap")
 
+    def stage(self, a_host: np.ndarray, b_host: np.ndarray) -> None:
+        """Copy host ASCII into the pinned staging buffers (outside timing)."""
+        self.ha.numpy()[: self.na] = a_host
+        self.hb.numpy()[: self.nb] = b_host
+
+    def run_staged(self, policy: NPolicy = NPolicy.REJECT) -> np.ndarray:
+        """Pinned host -> device, pipeline, result -> pinned host (e2e step)."""
+        self.a[: self.na].copy_(self.ha[: self.na], non_blocking=True)
+        self.b[: self.nb].copy_(self.hb[: self.nb], non_blocking=True)
+        self.run_device(policy)
+        self.hres.copy_(self.res, non_blocking=True)
+        _lib.torch().cuda.current_stream().synchronize()
+        return self.hres.numpy().copy()
+
     def run(self, a_host, b_host, policy: NPolicy = NPolicy.REJECT) -> np.ndarray:
         """Host ASCII in, host int64[4] (length, pos_a, pos_b, bad_pos) out."""
-        t = _lib.torch()
-        self.a[: self.na].copy_(t.from_numpy(a_host), non_blocking=True)
-        self.b[: self.nb].copy_(t.from_numpy(b_host), non_blocking=True)
-        self.run_device(policy)
-        return self.res.cpu().numpy()
+        self.stage(a_host, b_host)
+        return self.run_staged(policy)
 
 
 def longest_overlap(a: DnaSequence, b: DnaSequence,
