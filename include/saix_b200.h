@@ -86,13 +86,15 @@ SAIX_API int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sigma
              uint32_t *sa, uint32_t *isa, void *ws, size_t ws_bytes,
              saix_dc3_probe *probe, void *stream);
 
+SAIX_API size_t saix_dc3_merge_workspace_bytes(int64_t total);
+
 /* merge_sample_nonsample (suffix_index.py:452-457, _merge 362-378): step 3
  * alone.  sample_rank: n+3 by position; sorted_samples (ms entries) and
- * sorted_nonsamples (k entries) as in the probe. */
+ * sorted_nonsamples (k entries) as in the probe; sa gets ms+k entries. */
 SAIX_API int saix_dc3_merge(const void *text, int text_bytes, int64_t n,
                    const uint32_t *sample_rank, const uint32_t *sorted_samples,
                    int64_t ms, const uint32_t *sorted_nonsamples, int64_t k,
-                   uint32_t *sa, void *stream);
+                   uint32_t *sa, void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------- LCP */
 

@@ -64,7 +64,8 @@ SIGNATURES = {
     "saix_dc3_workspace_bytes": (_c.c_size_t, [_i64, _int]),
     "saix_dc3": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _c.c_size_t,
                         _c.POINTER(Dc3Probe), _vp]),
-    "saix_dc3_merge": (_int, [_vp, _int, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "saix_dc3_merge_workspace_bytes": (_c.c_size_t, [_i64]),
+    "saix_dc3_merge": (_int, [_vp, _int, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
     "saix_lcp_workspace_bytes": (_c.c_size_t, [_i64]),
     "saix_lcp": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_sparse_plan_make": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),

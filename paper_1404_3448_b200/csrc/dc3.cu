@@ -199,6 +199,32 @@ struct RankByPos {
     __device__ __forceinline__ u32 operator()(i64 p) const { return rank[p]; }
 };
 
+// Comparison record of one suffix p: the two leading characters and the
+// 1-based sample ranks one and two positions on.  Everything the DC3
+// comparator can ask about p, fetched once.
+struct MRec {
+    u32 pos, c0, c1, r1, r2;
+};
+
+template <typename TT, class Rank>
+__device__ __forceinline__ MRec make_rec(const Text<TT> &T, const Rank &R, i64 p) {
+    MRec m;
+    m.pos = (u32)p;
+    m.c0 = T(p);
+    m.c1 = T(p + 1);
+    m.r1 = (p % 3 == 2) ? 0u : R(p + 1);  // mod-2 samples never use r1
+    m.r2 = (p % 3 == 1) ? 0u : R(p + 2);  // mod-1 samples never use r2
+    return m;
+}
+
+// suffix(a) < suffix(b), a a sample, b a non-sample (suffix_index.py:192-202)
+__device__ __forceinline__ bool rec_a_first(const MRec &a, const MRec &b) {
+    if (a.c0 != b.c0) return a.c0 < b.c0;
+    if (a.pos % 3 == 1) return a.r1 < b.r1;
+    if (a.c1 != b.c1) return a.c1 < b.c1;
+    return a.r2 < b.r2;
+}
+
 // Merge inputs: sorted samples as sample indices / sorted mod-0 as indices.
 template <typename TT>
 struct MergeIdx {
@@ -207,7 +233,7 @@ struct MergeIdx {
     const u32 *A, *B;
     __device__ __forceinline__ i64 apos(i64 i) const { return R.L.pos(A[i]); }
     __device__ __forceinline__ i64 bpos(i64 j) const { return 3 * (i64)B[j]; }
-    __device__ __forceinline__ bool a_first(i64 a, i64 b) const { return dc3_a_first(T, R, a, b); }
+    __device__ __forceinline__ MRec rec(i64 p) const { return make_rec(T, R, p); }
 };
 // Merge inputs given as positions with a by-position rank array
 // (merge_sample_nonsample, suffix_index.py:452-457).
@@ -218,38 +244,85 @@ struct MergePos {
     const u32 *A, *B;
     __device__ __forceinline__ i64 apos(i64 i) const { return A[i]; }
     __device__ __forceinline__ i64 bpos(i64 j) const { return B[j]; }
-    __device__ __forceinline__ bool a_first(i64 a, i64 b) const { return dc3_a_first(T, R, a, b); }
+    __device__ __forceinline__ MRec rec(i64 p) const { return make_rec(T, R, p); }
 };
 
-constexpr int MERGE_ITEMS = 8;
+// Merge path in two kernels.  k_merge_partition splits the output into
+// MT_TILE-sized diagonals with one global binary search per tile;
+// k_merge_tile stages the tile's samples and non-samples as comparison
+// records in shared memory, merges them with per-thread merge paths in
+// shared memory, writes SA coalesced and scatters ISA.
+constexpr int MT_THREADS = 256;
+constexpr int MT_ITEMS = 8;
+constexpr int MT_TILE = MT_THREADS * MT_ITEMS;  // 2048 outputs per CTA
 
-// Merge path: each thread finds its diagonal split by binary search with
-// the DC3 comparator, then merges MERGE_ITEMS outputs; ISA scattered inline.
 template <class V>
-__global__ void k_merge(V v, i64 na, i64 nb, u32 *__restrict__ sa, u32 *__restrict__ isa) {
+__global__ void k_merge_partition(V v, i64 na, i64 nb, i64 ntiles, u32 *__restrict__ split) {
     i64 total = na + nb;
-    i64 d0 = ((i64)blockIdx.x * blockDim.x + threadIdx.x) * MERGE_ITEMS;
-    if (d0 >= total) return;
-    i64 lo = d0 > nb ? d0 - nb : 0, hi = d0 < na ? d0 : na;
-    while (lo < hi) {
-        i64 mid = (lo + hi) >> 1;
-        if (v.a_first(v.apos(mid), v.bpos(d0 - 1 - mid))) lo = mid + 1;
-        else hi = mid;
-    }
-    i64 i = lo, j = d0 - lo;
-    for (int r = 0; r < MERGE_ITEMS && d0 + r < total; r++) {
-        i64 p;
-        if (j >= nb) p = v.apos(i++);
-        else if (i >= na) p = v.bpos(j++);
-        else {
-            i64 a = v.apos(i), b = v.bpos(j);
-            if (v.a_first(a, b)) { p = a; i++; }
-            else { p = b; j++; }
+    for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t <= ntiles; t += (i64)gridDim.x * blockDim.x) {
+        i64 d = t * MT_TILE < total ? t * MT_TILE : total;
+        i64 lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+        while (lo < hi) {
+            i64 mid = (lo + hi) >> 1;
+            if (rec_a_first(v.rec(v.apos(mid)), v.rec(v.bpos(d - 1 - mid)))) lo = mid + 1;
+            else hi = mid;
         }
-        sa[d0 + r] = (u32)p;
-        if (isa) isa[p] = (u32)(d0 + r);
+        split[t] = (u32)lo;
     }
 }
+
+template <class V>
+__global__ void __launch_bounds__(MT_THREADS)
+k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, u32 *__restrict__ isa) {
+    __shared__ MRec sh[MT_TILE];
+    __shared__ u32 out[MT_TILE];
+    i64 total = na + nb;
+    i64 d0 = (i64)blockIdx.x * MT_TILE;
+    i64 d1 = d0 + MT_TILE < total ? d0 + MT_TILE : total;
+    i64 i0 = split[blockIdx.x], i1 = split[blockIdx.x + 1];
+    i64 j0 = d0 - i0;
+    int nat = (int)(i1 - i0), cnt = (int)(d1 - d0), nbt = cnt - nat;
+    for (int x = threadIdx.x; x < cnt; x += MT_THREADS)
+        sh[x] = v.rec(x < nat ? v.apos(i0 + x) : v.bpos(j0 + (x - nat)));
+    __syncthreads();
+    const MRec *A = sh, *B = sh + nat;
+    int dt = threadIdx.x * MT_ITEMS;
+    if (dt < cnt) {
+        int lo = dt > nbt ? dt - nbt : 0, hi = dt < nat ? dt : nat;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (rec_a_first(A[mid], B[dt - 1 - mid])) lo = mid + 1;
+            else hi = mid;
+        }
+        int i = lo, j = dt - lo;
+#pragma unroll
+        for (int r = 0; r < MT_ITEMS; r++) {
+            if (dt + r >= cnt) break;
+            bool takeA = j >= nbt || (i < nat && rec_a_first(A[i], B[j]));
+            out[dt + r] = takeA ? A[i++].pos : B[j++].pos;
+        }
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < cnt; x += MT_THREADS) {
+        u32 p = out[x];
+        sa[d0 + x] = p;
+        if (isa) isa[p] = (u32)(d0 + x);
+    }
+}
+
+template <class V>
+static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStream_t st) {
+    i64 total = na + nb;
+    if (total == 0) return SAIX_OK;
+    i64 ntiles = ceil_div(total, MT_TILE);
+    k_merge_partition<V><<<grid_for(ntiles + 1, 128), 128, 0, st>>>(v, na, nb, ntiles, split);
+    SAIX_LAUNCHED();
+    k_merge_tile<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa);
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}
+
+inline i64 merge_split_words(i64 total) { return ceil_div(total > 0 ? total : 1, MT_TILE) + 2; }
 
 // ------------------------------------------------------------ probes
 
@@ -406,6 +479,7 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     u32 *v0 = ar.alloc<u32>(k), *v1 = ar.alloc<u32>(k);
     u32 *scratch = ar.alloc<u32>(radix_scratch_words(k));
     u32 *tmp = ar.alloc<u32>(scan_tmp_words(L.m));
+    u32 *split = ar.alloc<u32>(merge_split_words(N));
     SAIX_ARENA_OK(ar);
     SAIX_TRY(scan_transform(Mod1Flag<TT>{SAc, L.m1}, Mod0Emit<TT>{T, SAc, k0, v0}, L.m, tmp, nullptr, st));
     u32 *keys = k0, *vals = v0;
@@ -415,10 +489,8 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     RankFromIsa R{L, ISAc};
     i64 pad = L.pad ? 1 : 0;
     i64 na = L.m - pad;
-    i64 nthreads = ceil_div(N, MERGE_ITEMS);
     MergeIdx<TT> V{T, R, SAc + pad, vals};
-    k_merge<MergeIdx<TT>><<<(unsigned)ceil_div(nthreads, K_THREADS), K_THREADS, 0, st>>>(V, na, k, SA, ISA);
-    SAIX_LAUNCHED();
+    SAIX_TRY(merge_run(V, na, k, split, SA, ISA, st));
 
     if (probe) {
         int g = grid_for(N + 3, K_THREADS);
@@ -457,7 +529,8 @@ static size_t dc3_plan(i64 n) {
         size_t sort_t = (size_t)m * 24 + (size_t)(radix_scratch_words(m) + scan_tmp_words(m)) * 4;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
-        size_t post_t = (size_t)k * 16 + (size_t)(radix_scratch_words(k) + scan_tmp_words(m)) * 4;
+        size_t post_t = (size_t)k * 16 + (size_t)(radix_scratch_words(k) + scan_tmp_words(m) +
+                                                  merge_split_words(N)) * 4;
         size_t t = sort_t > bm_t ? sort_t : bm_t;
         t = t > post_t ? t : post_t;
         t += 8 * Arena::kAlign;
@@ -530,9 +603,13 @@ extern "C" int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sig
     return SAIX_OK;
 }
 
+extern "C" size_t saix_dc3_merge_workspace_bytes(int64_t total) {
+    return (size_t)merge_split_words(total) * 4 + Arena::kAlign;
+}
+
 extern "C" int saix_dc3_merge(const void *text, int text_bytes, int64_t n, const uint32_t *sample_rank,
                               const uint32_t *sorted_samples, int64_t ms, const uint32_t *sorted_nonsamples,
-                              int64_t k, uint32_t *sa, void *stream) {
+                              int64_t k, uint32_t *sa, void *ws, size_t ws_bytes, void *stream) {
     if (n < 0 || ms < 0 || k < 0 || (text_bytes != 1 && text_bytes != 4) || ms + k > n + 1) {
         set_error("saix_dc3_merge: invalid arguments");
         return SAIX_EINVAL;
@@ -540,14 +617,18 @@ extern "C" int saix_dc3_merge(const void *text, int text_bytes, int64_t n, const
     i64 total = ms + k;
     if (total == 0) return SAIX_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    unsigned grid = (unsigned)ceil_div(ceil_div(total, MERGE_ITEMS), K_THREADS);
+    if (!ws || ws_bytes < saix_dc3_merge_workspace_bytes(total)) {
+        set_error("saix_dc3_merge: workspace too small");
+        return SAIX_ENOSPC;
+    }
+    u32 *split = (u32 *)ws;
+    int rc;
     if (text_bytes == 1) {
         MergePos<u8> V{Text<u8>{(const u8 *)text, n}, RankByPos{sample_rank}, sorted_samples, sorted_nonsamples};
-        k_merge<MergePos<u8>><<<grid, K_THREADS, 0, st>>>(V, ms, k, sa, nullptr);
+        rc = merge_run(V, ms, k, split, sa, nullptr, st);
     } else {
         MergePos<u32> V{Text<u32>{(const u32 *)text, n}, RankByPos{sample_rank}, sorted_samples, sorted_nonsamples};
-        k_merge<MergePos<u32>><<<grid, K_THREADS, 0, st>>>(V, ms, k, sa, nullptr);
+        rc = merge_run(V, ms, k, split, sa, nullptr, st);
     }
-    SAIX_LAUNCHED();
-    return SAIX_OK;
+    return rc;
 }

@@ -1,13 +1,17 @@
-// lcp.cu -- Kasai LCP (suffix_index.py:460-506 `_kasai_scan`) on sm_100a.
+// lcp.cu -- LCP array (suffix_index.py:460-506 `_kasai_scan`) on sm_100a.
 //
 // The reference walks text positions in order so the matched length h drops
-// by at most one per step.  Here every thread owns a contiguous chunk of
-// LCP_CHUNK text positions and runs the same h-decrement walk inside it,
-// starting from a seed; chunk seeds come from a sparse pass that computes
-// the exact PLCP value at every chunk start (word-parallel compares), so the
-// in-chunk walk never restarts from zero.  ISA is staged through shared
-// memory in coalesced tiles; SA[r-1] and the partner text are gathers and
-// lcp[r] is a scatter (one random access each).
+// by at most one per step (Kasai).  The same walk is done here in the
+// permuted-LCP (PLCP / Phi) formulation so every phase has exactly one
+// random-access target:
+//   k_phi         Phi[sa[r]] = sa[r-1]                   (scatter)
+//   k_lcp_seeds   exact PLCP at every chunk start        (word compares)
+//   k_plcp        per-thread h-decrement walk over a chunk of LCP_CHUNK text
+//                 positions, Phi staged/overwritten in shared memory
+//                 (partner text is the only gather)
+//   k_lcp_permute lcp[r] = PLCP[sa[r]]                   (gather)
+// At C2 size each random target (Phi/PLCP 80 MB, u8 text 20 MB) fits the
+// 126 MB L2, so the scatter/gathers stay on chip.
 #include "common.cuh"
 
 namespace saix {
@@ -47,61 +51,86 @@ __device__ __forceinline__ u32 extend_match<u8>(const u8 *__restrict__ T, i64 n,
     }
 }
 
+constexpr u32 kNone = 0xFFFFFFFFu;
+
+// Phi[sa[r]] = sa[r-1]: the text-order predecessor map (one scatter).
+__global__ void k_phi(const u32 *__restrict__ sa, i64 n, u32 *__restrict__ phi) {
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x)
+        phi[sa[r]] = r ? sa[r - 1] : kNone;
+}
+
 // Exact PLCP at every chunk start (seed of the in-chunk walk).
 template <typename TT>
-__global__ void k_lcp_seeds(const TT *__restrict__ T, i64 n, const u32 *__restrict__ sa,
-                            const u32 *__restrict__ isa, u32 *__restrict__ seeds, i64 nchunks) {
+__global__ void k_lcp_seeds(const TT *__restrict__ T, i64 n, const u32 *__restrict__ phi,
+                            u32 *__restrict__ seeds, i64 nchunks) {
     for (i64 c = (i64)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += (i64)gridDim.x * blockDim.x) {
         i64 i = c * LCP_CHUNK;
-        u32 r = isa[i];
-        seeds[c] = r == 0 ? 0u : extend_match<TT>(T, n, i, sa[r - 1], 0u);
+        u32 j = phi[i];
+        seeds[c] = j == kNone ? 0u : extend_match<TT>(T, n, i, j, 0u);
     }
 }
 
+// PLCP in text order, Kasai's h-decrement walk per chunk (in place: the
+// phi tile is staged in shared memory and overwritten with PLCP values).
 template <typename TT>
 __global__ void __launch_bounds__(LCP_THREADS)
-k_lcp_kasai(const TT *__restrict__ T, i64 n, const u32 *__restrict__ sa, const u32 *__restrict__ isa,
-            const u32 *__restrict__ seeds, u32 *__restrict__ lcp) {
+k_plcp(const TT *__restrict__ T, i64 n, u32 *__restrict__ phi_plcp, const u32 *__restrict__ seeds) {
     __shared__ u32 sh[LCP_TILE + LCP_TILE / 32];
     i64 base = (i64)blockIdx.x * LCP_TILE;
     for (int x = threadIdx.x; x < LCP_TILE; x += LCP_THREADS) {
         i64 i = base + x;
-        sh[x + (x >> 5)] = i < n ? isa[i] : 0u;
+        sh[x + (x >> 5)] = i < n ? phi_plcp[i] : kNone;
     }
     __syncthreads();
     i64 start = base + (i64)threadIdx.x * LCP_CHUNK;
-    if (start >= n) return;
-    u32 h = seeds[start / LCP_CHUNK];
-    for (int c = 0; c < LCP_CHUNK; c++) {
-        i64 i = start + c;
-        if (i >= n) break;
-        int x = threadIdx.x * LCP_CHUNK + c;
-        u32 r = sh[x + (x >> 5)];
-        if (r == 0) {
-            lcp[0] = 0;
-            h = 0;
-            continue;
+    if (start < n) {
+        u32 h = seeds[start / LCP_CHUNK];
+        for (int c = 0; c < LCP_CHUNK; c++) {
+            i64 i = start + c;
+            if (i >= n) break;
+            int x = threadIdx.x * LCP_CHUNK + c;
+            u32 j = sh[x + (x >> 5)];
+            if (j == kNone) {
+                h = 0;
+            } else if (c > 0) {
+                h = extend_match<TT>(T, n, i, j, h);
+            }
+            sh[x + (x >> 5)] = h;
+            if (h) h--;
         }
-        if (c > 0) h = extend_match<TT>(T, n, i, sa[r - 1], h);
-        lcp[r] = h;
-        if (h) h--;
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < LCP_TILE; x += LCP_THREADS) {
+        i64 i = base + x;
+        if (i < n) phi_plcp[i] = sh[x + (x >> 5)];
     }
 }
 
-static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, const u32 *isa, u32 *lcp, u32 *seeds,
+// lcp[r] = PLCP[sa[r]] (one gather; lcp[0] = PLCP[sa[0]] = 0).
+__global__ void k_lcp_permute(const u32 *__restrict__ sa, i64 n, const u32 *__restrict__ plcp,
+                              u32 *__restrict__ lcp) {
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x)
+        lcp[r] = plcp[sa[r]];
+}
+
+static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32 *phi, u32 *seeds,
                    cudaStream_t st) {
     i64 nchunks = ceil_div(n, LCP_CHUNK);
-    int g = grid_for(nchunks, 256);
+    int g = grid_for(n, 256);
     unsigned tiles = (unsigned)ceil_div(n, LCP_TILE);
+    k_phi<<<g, 256, 0, st>>>(sa, n, phi);
+    SAIX_LAUNCHED();
     if (tb == 1) {
-        k_lcp_seeds<u8><<<g, 256, 0, st>>>((const u8 *)text, n, sa, isa, seeds, nchunks);
+        k_lcp_seeds<u8><<<grid_for(nchunks, 256), 256, 0, st>>>((const u8 *)text, n, phi, seeds, nchunks);
         SAIX_LAUNCHED();
-        k_lcp_kasai<u8><<<tiles, LCP_THREADS, 0, st>>>((const u8 *)text, n, sa, isa, seeds, lcp);
+        k_plcp<u8><<<tiles, LCP_THREADS, 0, st>>>((const u8 *)text, n, phi, seeds);
     } else {
-        k_lcp_seeds<u32><<<g, 256, 0, st>>>((const u32 *)text, n, sa, isa, seeds, nchunks);
+        k_lcp_seeds<u32><<<grid_for(nchunks, 256), 256, 0, st>>>((const u32 *)text, n, phi, seeds, nchunks);
         SAIX_LAUNCHED();
-        k_lcp_kasai<u32><<<tiles, LCP_THREADS, 0, st>>>((const u32 *)text, n, sa, isa, seeds, lcp);
+        k_plcp<u32><<<tiles, LCP_THREADS, 0, st>>>((const u32 *)text, n, phi, seeds);
     }
+    SAIX_LAUNCHED();
+    k_lcp_permute<<<g, 256, 0, st>>>(sa, n, phi, lcp);
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
@@ -111,12 +140,15 @@ static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, const u32 *is
 using namespace saix;
 
 extern "C" size_t saix_lcp_workspace_bytes(int64_t n) {
-    return (size_t)(ceil_div(n > 0 ? n : 1, LCP_CHUNK) + 64) * 4 + Arena::kAlign;
+    Arena ar;
+    ar.alloc<u32>(n);
+    ar.alloc<u32>(ceil_div(n > 0 ? n : 1, LCP_CHUNK) + 1);
+    return ar.peak + Arena::kAlign;
 }
 
 extern "C" int saix_lcp(const void *text, int text_bytes, int64_t n, const uint32_t *sa, const uint32_t *isa,
                         uint32_t *lcp, void *ws, size_t ws_bytes, void *stream) {
-    if (n < 0 || (text_bytes != 1 && text_bytes != 4) || (n > 0 && (!text || !sa || !isa || !lcp))) {
+    if (n < 0 || (text_bytes != 1 && text_bytes != 4) || (n > 0 && (!text || !sa || !lcp))) {
         set_error("saix_lcp: invalid arguments");
         return SAIX_EINVAL;
     }
@@ -130,5 +162,10 @@ extern "C" int saix_lcp(const void *text, int text_bytes, int64_t n, const uint3
         set_error("saix_lcp: u8 text must be 4-byte aligned");
         return SAIX_EINVAL;
     }
-    return lcp_run(text, text_bytes, n, sa, isa, lcp, (u32 *)ws, (cudaStream_t)stream);
+    (void)isa;  // the Phi formulation needs only SA
+    Arena ar{(char *)ws, ws_bytes};
+    u32 *phi = ar.alloc<u32>(n);
+    u32 *seeds = ar.alloc<u32>(ceil_div(n, LCP_CHUNK) + 1);
+    SAIX_ARENA_OK(ar);
+    return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, (cudaStream_t)stream);
 }

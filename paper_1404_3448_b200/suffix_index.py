@@ -283,7 +283,9 @@ def merge_sample_nonsample(workspace: Dc3Workspace, text: RankedText) -> SuffixA
     a = _lib.to_device(ss.astype(np.uint32).view(np.int32))
     b = _lib.to_device(sn.astype(np.uint32).view(np.int32))
     out = _lib.empty(total, t.int32)
+    ws = _lib.workspace(L.saix_dc3_merge_workspace_bytes(total))
     rc = L.saix_dc3_merge(_lib.ptr(dt.t), dt.bytes, n, _lib.ptr(rank), _lib.ptr(a), ss.shape[0],
-                          _lib.ptr(b), sn.shape[0], _lib.ptr(out), _lib.stream_ptr())
+                          _lib.ptr(b), sn.shape[0], _lib.ptr(out), _lib.ptr(ws), ws.numel(),
+                          _lib.stream_ptr())
     _lib.check(rc, "saix_dc3_merge")
     return SuffixArray.from_order(_lib.u32_to_i64_host(out, total))
