@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 longest-overlap hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c3|c5]
+
+Default workload (BASELINE.json configs[1], "C2"): a single synthetic pair of
+2 x 10 Mbp random ACGT sequences (gen_random seeds 11/12 on rank 0; rank r
+uses 11+2r/12+2r), full pipeline on one B200 per rank: encode -> generalized
+text -> DC3 suffix array -> LCP -> overlap scan.  A "step" is one pass of that
+pipeline over one pair.  Metric: Mbases/s of generalized-text bases through
+the whole pipeline (20,000,001 per pair); value is the whole-job aggregate
+over ranks; N > 1 runs independent replicas (weak scaling, no data-path
+collective: a single long pair does not shard).
+
+--impl reference times the reference algorithm on the host (the C oracle
+port in oracle/, kind "port": the reference is pure Python, nothing to
+compile) on the same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DC3 suffix-array Mbases/s; longest-overlap pairs/s at 1/2/4/8 B200 vs host CPU"
+L2_FLUSH_BYTES = 512 << 20
+
+
+# ------------------------------------------------------------------ helpers
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peak_gbs():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def count_our_launches(fn) -> int:
+    """Kernels from libsaix_b200 (all named k_*) launched by one call of fn."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    n = 0
+    for e in prof.events():
+        name = e.name or ""
+        if e.device_type.name == "CUDA" and ("k_" in name.split("(")[0].split("<")[0]):
+            n += 1
+    return n
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch of `kernel` from a committed
+    `ncu --set full` capture summary (profiles/ncu_traffic.json), if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ workloads
+
+def c2_inputs(rank: int):
+    from paper_1404_3448_b200.sequence import gen_random
+    a = gen_random(10_000_000, 11 + 2 * rank)
+    b = gen_random(10_000_000, 12 + 2 * rank)
+    return (np.frombuffer(a.residues.encode(), np.uint8), np.frombuffer(b.residues.encode(), np.uint8))
+
+
+def run_reference(args, rank):
+    """Reference algorithm (C oracle port) on the host, same metric/config."""
+    import oracle
+    if args.workload != "c2":
+        print(json.dumps({"impl": "reference", "unavailable": f"workload {args.workload} not wired for the CPU arm"}))
+        return
+    ha, hb = c2_inputs(0)
+    a, b = ha.tobytes(), hb.tobytes()
+    n = len(a) + len(b) + 1
+    for _ in range(args.warmup):
+        oracle.longest_overlap(a, b)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        res = oracle.longest_overlap(a, b)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n * args.steps / tot / 1e6
+    cb = {"value": value, "unit": "Mbases/s", "cores": 1, "kind": "port",
+          "sample": "full C2 pair (2 x 10 Mbp, GSA n=20,000,001) per step, oracle/saix_oracle.c single thread"}
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mbases/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": {"workload": "C2", "gsa_bases": n, "result": list(res)},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "Mbases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def bench_c2(args, rank, world, dist):
+    import torch
+
+    import paper_1404_3448_b200 as sx
+    from paper_1404_3448_b200 import _lib
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ha, hb = c2_inputs(rank)
+    n_gsa = len(ha) + len(hb) + 1
+    pipe = sx.OverlapPipeline(len(ha), len(hb))
+    pipe.stage(ha, hb)
+    res0 = pipe.run_staged()                       # correctness pre-check (bench.py:112-117)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def timed(step_fn, k):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        barrier()
+        torch.cuda.synchronize()
+        for e0, e1 in evs:
+            flush.zero_()                          # L2 flushed between timed steps (outside events)
+            e0.record(st)
+            step_fn()
+            e1.record(st)
+        torch.cuda.synchronize()
+        barrier()
+        ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+        if dist is not None:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        pipe.run_device()
+        pipe.run_staged()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    _lib.prof_enable(not args.no_prof)
+    ms_dev = timed(pipe.run_device, args.steps)    # value: inputs resident in HBM
+    prof = _lib.prof_collect()
+    _lib.prof_enable(False)
+    ms_e2e = timed(pipe.run_staged, args.steps)    # e2e: pinned host in, 32 B out
+    clk = clocks.stop()
+
+    launches_per_step = count_our_launches(pipe.run_device)
+    peak, peak_kind = measured_peak_gbs()
+    dom = max(prof, key=lambda e: e["ms"]) if prof else None
+    roof = None
+    if dom:
+        per_launch_ms = dom["ms"] / dom["launches"]
+        per_launch_bytes = dom["bytes"] / dom["launches"]
+        ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom["name"], "achieved": round(ach, 1), "peak": peak,
+                "peak_source": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
+                "traffic": ncu_traffic(dom["name"]),
+                "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
+                "share_of_step": round(dom["ms"] / ms_dev, 4) if ms_dev else None}
+    stage = {e["name"]: round(e["ms"] / args.steps, 4) for e in sorted(prof, key=lambda e: -e["ms"])}
+
+    pairs = world * args.steps
+    value = n_gsa * pairs / (ms_dev * 1e-3) / 1e6
+    e2e_value = n_gsa * pairs / (ms_e2e * 1e-3) / 1e6
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        t0 = time.perf_counter()
+        ref = oracle.longest_overlap(ha.tobytes(), hb.tobytes())
+        dt = time.perf_counter() - t0
+        assert tuple(int(x) for x in res0[:3]) == ref, (res0, ref)
+        cpu = {"value": n_gsa / dt / 1e6, "unit": "Mbases/s", "cores": 1, "kind": "port",
+               "sample": "one full C2 pair (2 x 10 Mbp), oracle/saix_oracle.c single thread "
+                         f"({dt:.1f} s); result matched the GPU's {tuple(ref)}"}
+
+    results = [int(x) for x in res0[:3]]
+    if dist is not None:
+        t = torch.tensor(results, device=dev, dtype=torch.int64)
+        allr = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(allr, t)
+        results = [[int(x) for x in r.tolist()] for r in allr]
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "Mbases/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_dev / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
+            "config": {"workload": "C2: 2 x 10 Mbp random ACGT pair (gen_random seeds 11/12 + 2*rank), "
+                                   "encode+DC3+LCP+overlap scan per step",
+                       "gsa_bases_per_pair": n_gsa, "l2": "flushed between timed steps (512 MiB write)",
+                       "parallelism": f"replicas x{world}"},
+            "pairs_per_s": round(pairs / (ms_dev * 1e-3), 3),
+            "e2e": {"value": round(e2e_value, 2), "unit": "Mbases/s", "h2d_bytes_per_step": len(ha) + len(hb),
+                    "d2h_bytes_per_step": 32, "ms_per_step": round(ms_e2e / args.steps, 4)},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+            "stage_ms_per_step": stage, "result": results,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["c2"], default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prof", action="store_true", help="time without per-kernel events")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_env()
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, rank)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        bench_c2(args, rank, world, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -43,6 +43,21 @@ extern "C" {
 SAIX_API const char *saix_last_error(void);
 SAIX_API int saix_abi_version(void);
 
+/* Per-kernel CUDA-event timing for measurement tools (bench.py): when
+ * enabled every instrumented launch is bracketed by events on its stream and
+ * tagged with its algorithmic bytes (DESIGN.md roofline model).
+ * saix_prof_enable(on) clears the log; saix_prof_collect() synchronizes the
+ * events, aggregates by kernel name into `out` and returns the entry count. */
+typedef struct saix_prof_entry {
+    char name[64];
+    int64_t launches;
+    double total_ms;
+    double bytes;
+} saix_prof_entry;
+
+SAIX_API void saix_prof_enable(int on);
+SAIX_API int saix_prof_collect(saix_prof_entry *out, int max_entries);
+
 /* ---------------------------------------------------------------- encode */
 
 /* encode (sequence.py:144-157) fused with GeneralizedText.build

@@ -43,6 +43,11 @@ class Dc3Probe(_c.Structure):
     ]
 
 
+class ProfEntry(_c.Structure):
+    _fields_ = [("name", _c.c_char * 64), ("launches", _i64), ("total_ms", _c.c_double),
+                ("bytes", _c.c_double)]
+
+
 class SparsePlan(_c.Structure):
     _fields_ = [
         ("n", _i64),
@@ -59,6 +64,8 @@ class SparsePlan(_c.Structure):
 SIGNATURES = {
     "saix_last_error": (_c.c_char_p, []),
     "saix_abi_version": (_int, []),
+    "saix_prof_enable": (None, [_int]),
+    "saix_prof_collect": (_int, [_c.POINTER(ProfEntry), _int]),
     "saix_encode_gsa": (_int, [_vp, _i64, _vp, _i64, _int, _vp, _vp, _vp]),
     "saix_encode": (_int, [_vp, _i64, _int, _vp, _vp, _vp]),
     "saix_dc3_workspace_bytes": (_c.c_size_t, [_i64, _int]),
@@ -183,3 +190,16 @@ def u32_to_i64_host(t_dev, n: int) -> np.ndarray:
     if n == 0:
         return np.zeros(0, np.int64)
     return t_dev[:n].cpu().numpy().view(np.uint32).astype(np.int64)
+
+
+def prof_enable(on: bool = True) -> None:
+    load().saix_prof_enable(int(on))
+
+
+def prof_collect() -> list[dict]:
+    """Per-kernel CUDA-event totals since prof_enable (synchronizes)."""
+    L = load()
+    buf = (ProfEntry * 256)()
+    n = L.saix_prof_collect(buf, 256)
+    return [{"name": buf[i].name.decode(), "launches": int(buf[i].launches),
+             "ms": float(buf[i].total_ms), "bytes": float(buf[i].bytes)} for i in range(min(n, 256))]

@@ -53,6 +53,27 @@ void set_error(const char *fmt, ...);
         if (rc_ != SAIX_OK) return rc_;                                        \
     } while (0)
 
+// ------------------------------------------------------------- profiling
+
+// Optional per-kernel CUDA-event timing (saix_prof_enable): each Prof scope
+// brackets one launch on its stream and carries the launch's algorithmic
+// bytes so bench.py can report achieved GB/s.
+bool prof_on();
+void prof_mark(const char *name, double bytes, cudaStream_t st, bool begin);
+
+struct Prof {
+    bool on;
+    const char *name;
+    double bytes;
+    cudaStream_t st;
+    Prof(const char *n, double b, cudaStream_t s) : on(prof_on()), name(n), bytes(b), st(s) {
+        if (on) prof_mark(name, bytes, st, true);
+    }
+    ~Prof() {
+        if (on) prof_mark(name, bytes, st, false);
+    }
+};
+
 // ------------------------------------------------------------- workspace
 
 // Bump allocator over the caller's workspace.  With base == nullptr it only

@@ -29,6 +29,7 @@ struct Text {
     const TT *t;
     i64 n;
     __device__ __forceinline__ u32 operator()(i64 p) const { return p < n ? (u32)t[p] : 0u; }
+    __host__ __device__ static constexpr int bytes() { return (int)sizeof(TT); }
 };
 
 // ------------------------------------------------------------ naming
@@ -315,9 +316,17 @@ static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStr
     i64 total = na + nb;
     if (total == 0) return SAIX_OK;
     i64 ntiles = ceil_div(total, MT_TILE);
-    k_merge_partition<V><<<grid_for(ntiles + 1, 128), 128, 0, st>>>(v, na, nb, ntiles, split);
+    {
+        Prof prof_("dc3.merge_partition", 4.0 * (ntiles + 1), st);
+        k_merge_partition<V><<<grid_for(ntiles + 1, 128), 128, 0, st>>>(v, na, nb, ntiles, split);
+    }
     SAIX_LAUNCHED();
-    k_merge_tile<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa);
+    {
+        // indices 4 + chars 2w + ranks (4 per sample, 8 per non-sample) + SA 4 + ISA 4
+        double w = (double)v.T.bytes();
+        Prof prof_("dc3.merge_tile", total * (4 + 2 * w + 8) + 4.0 * (na + 2 * nb) - (isa ? 0 : 4.0 * total), st);
+        k_merge_tile<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa);
+    }
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
@@ -399,10 +408,16 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         SAIX_CUDA(cudaMemsetAsync(bm, 0, (size_t)nwords * 4, st));
         int use_smem = nwords * 4 <= 48 * 1024;
         int gs = use_smem ? (g < 2 * kNumSMs ? g : 2 * kNumSMs) : g;
-        k_bitmap_set<TT><<<gs, K_THREADS, use_smem ? nwords * 4 : 0, st>>>(T, L, s1, bm, nwords, use_smem);
+        {
+            Prof prof_("dc3.bitmap_set", (double)sizeof(TT) * L.n, st);
+            k_bitmap_set<TT><<<gs, K_THREADS, use_smem ? nwords * 4 : 0, st>>>(T, L, s1, bm, nwords, use_smem);
+        }
         SAIX_LAUNCHED();
-        SAIX_TRY(scan_transform(PopcIn{bm}, StoreExcl{wp}, nwords, tmp, d_scal, st));
-        k_bitmap_name<TT><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, tt);
+        SAIX_TRY(scan_transform(PopcIn{bm}, StoreExcl{wp}, nwords, tmp, d_scal, st, "dc3.bitmap_scan", 8.0 * nwords));
+        {
+            Prof prof_("dc3.bitmap_name", (double)sizeof(TT) * L.n + 4.0 * m, st);
+            k_bitmap_name<TT><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, tt);
+        }
         SAIX_LAUNCHED();
         SAIX_TRY(read_u32(d_scal, &D, st));
     } else {
@@ -415,11 +430,15 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         u64 *keys = k0;
         u32 *vals = v0;
         if (3 * b <= 64) {
-            k_triple_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, b, k0, v0);
+            {
+                Prof prof_("dc3.triple_keys", (double)sizeof(TT) * L.n + 12.0 * m, st);
+                k_triple_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, b, k0, v0);
+            }
             SAIX_LAUNCHED();
             SAIX_TRY(radix_sort_pairs<u64>(keys, vals, keys == k0 ? k1 : k0, vals == v0 ? v1 : v0, m, 0,
                                            3 * b, scratch, st));
-            SAIX_TRY(scan_transform(FlagPacked{keys}, ScatterName{vals, tt}, m, tmp, d_scal, st));
+            SAIX_TRY(scan_transform(FlagPacked{keys}, ScatterName{vals, tt}, m, tmp, d_scal, st, "dc3.name_scan",
+                                    16.0 * m));
         } else {
             k_third_char_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, k0, v0);
             SAIX_LAUNCHED();
@@ -436,6 +455,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         SAIX_TRY(read_u32(d_scal, &D, st));
     }
     if ((i64)D == m) {
+        Prof prof_("dc3.unique_ranks", 12.0 * m, st);
         if (sorted_vals) k_unique_from_sorted<<<g, K_THREADS, 0, st>>>(sorted_vals, m, SAc, ISAc);
         else k_unique_from_names<<<g, K_THREADS, 0, st>>>(tt, m, SAc, ISAc);
         SAIX_LAUNCHED();
@@ -481,7 +501,8 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     u32 *tmp = ar.alloc<u32>(scan_tmp_words(L.m));
     u32 *split = ar.alloc<u32>(merge_split_words(N));
     SAIX_ARENA_OK(ar);
-    SAIX_TRY(scan_transform(Mod1Flag<TT>{SAc, L.m1}, Mod0Emit<TT>{T, SAc, k0, v0}, L.m, tmp, nullptr, st));
+    SAIX_TRY(scan_transform(Mod1Flag<TT>{SAc, L.m1}, Mod0Emit<TT>{T, SAc, k0, v0}, L.m, tmp, nullptr, st,
+                            "dc3.mod0_compact", 4.0 * L.m + (8.0 + sizeof(TT)) * k));
     u32 *keys = k0, *vals = v0;
     SAIX_TRY(radix_sort_pairs<u32>(keys, vals, k1, v1, k, 0, bits_for(sigma), scratch, st));
 

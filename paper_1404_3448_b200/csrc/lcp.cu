@@ -118,19 +118,29 @@ static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32
     i64 nchunks = ceil_div(n, LCP_CHUNK);
     int g = grid_for(n, 256);
     unsigned tiles = (unsigned)ceil_div(n, LCP_TILE);
-    k_phi<<<g, 256, 0, st>>>(sa, n, phi);
-    SAIX_LAUNCHED();
-    if (tb == 1) {
-        k_lcp_seeds<u8><<<grid_for(nchunks, 256), 256, 0, st>>>((const u8 *)text, n, phi, seeds, nchunks);
-        SAIX_LAUNCHED();
-        k_plcp<u8><<<tiles, LCP_THREADS, 0, st>>>((const u8 *)text, n, phi, seeds);
-    } else {
-        k_lcp_seeds<u32><<<grid_for(nchunks, 256), 256, 0, st>>>((const u32 *)text, n, phi, seeds, nchunks);
-        SAIX_LAUNCHED();
-        k_plcp<u32><<<tiles, LCP_THREADS, 0, st>>>((const u32 *)text, n, phi, seeds);
+    {
+        Prof prof_("lcp.phi", 8.0 * n, st);
+        k_phi<<<g, 256, 0, st>>>(sa, n, phi);
     }
     SAIX_LAUNCHED();
-    k_lcp_permute<<<g, 256, 0, st>>>(sa, n, phi, lcp);
+    {
+        Prof prof_("lcp.seeds", 8.0 * nchunks, st);
+        if (tb == 1)
+            k_lcp_seeds<u8><<<grid_for(nchunks, 256), 256, 0, st>>>((const u8 *)text, n, phi, seeds, nchunks);
+        else
+            k_lcp_seeds<u32><<<grid_for(nchunks, 256), 256, 0, st>>>((const u32 *)text, n, phi, seeds, nchunks);
+    }
+    SAIX_LAUNCHED();
+    {
+        Prof prof_("lcp.plcp", (8.0 + tb) * n, st);
+        if (tb == 1) k_plcp<u8><<<tiles, LCP_THREADS, 0, st>>>((const u8 *)text, n, phi, seeds);
+        else k_plcp<u32><<<tiles, LCP_THREADS, 0, st>>>((const u32 *)text, n, phi, seeds);
+    }
+    SAIX_LAUNCHED();
+    {
+        Prof prof_("lcp.permute", 12.0 * n, st);
+        k_lcp_permute<<<g, 256, 0, st>>>(sa, n, phi, lcp);
+    }
     SAIX_LAUNCHED();
     return SAIX_OK;
 }

@@ -245,13 +245,17 @@ static int overlap_scan(const u32 *sa, const u32 *lcp, i64 n, i64 boundary, i64 
     SAIX_CUDA(cudaMemsetAsync(w.winner, 0xFF, sizeof(unsigned long long), st));
     i64 ntiles = ceil_div(n, OV_TILE);
     int g = grid_for(n, OV_THREADS, kNumSMs * 8);
-    k_cross_max<<<g, OV_THREADS, 0, st>>>(sa, lcp, n, (u32)boundary, w.best);
+    {
+        Prof prof_("overlap.cross_max", 8.0 * n, st);
+        k_cross_max<<<g, OV_THREADS, 0, st>>>(sa, lcp, n, (u32)boundary, w.best);
+    }
     SAIX_LAUNCHED();
-    k_runs_reduce<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg);
-    SAIX_LAUNCHED();
-    k_runs_carry<<<1, OV_THREADS, 0, st>>>(w.agg, ntiles);
-    SAIX_LAUNCHED();
-    k_runs_apply<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg, w.winner);
+    {
+        Prof prof_("overlap.runs", 16.0 * n, st);
+        k_runs_reduce<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg);
+        k_runs_carry<<<1, OV_THREADS, 0, st>>>(w.agg, ntiles);
+        k_runs_apply<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg, w.winner);
+    }
     SAIX_LAUNCHED();
     k_overlap_finish<<<1, 1, 0, st>>>(w.best, w.winner, (u32)boundary, out3);
     SAIX_LAUNCHED();
@@ -270,6 +274,7 @@ extern "C" int saix_encode_gsa(const uint8_t *a_ascii, int64_t na, const uint8_t
     }
     cudaStream_t st = (cudaStream_t)stream;
     i64 n = na + nb + 1;
+    Prof prof_("encode.gsa", 2.0 * n, st);
     k_encode_gsa<<<grid_for(n, 256), 256, 0, st>>>(a_ascii, na, b_ascii ? b_ascii : a_ascii, nb, keep_n, 1, gsa,
                                                      bad_pos);
     SAIX_LAUNCHED();

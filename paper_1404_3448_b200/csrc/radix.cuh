@@ -129,9 +129,12 @@ int radix_sort_pairs(K *&keys, u32 *&vals, K *keys_alt, u32 *vals_alt, i64 n, in
     u32 *hist = scratch;
     u32 *stmp = scratch + hw;
     for (int shift = begin_bit; shift < end_bit; shift += RS_BITS) {
+        Prof prof_(sizeof(K) == 8 ? "radix.pass64" : "radix.pass32",
+                   (double)n * (3 * sizeof(K) + 2 * 4), st);
         k_radix_upsweep<K><<<(unsigned)ntiles, RS_THREADS, 0, st>>>(keys, n, shift, hist, ntiles);
         SAIX_LAUNCHED();
-        SAIX_TRY(scan_transform(HistLoad{hist}, HistStore{hist}, hw, stmp, nullptr, st));
+        SAIX_TRY(scan_transform(HistLoad{hist}, HistStore{hist}, hw, stmp, nullptr, st, "radix.histscan",
+                                8.0 * hw));
         k_radix_downsweep<K><<<(unsigned)ntiles, RS_THREADS, 0, st>>>(keys, vals, n, shift, hist,
                                                                       ntiles, keys_alt, vals_alt);
         SAIX_LAUNCHED();

@@ -168,6 +168,8 @@ extern "C" int saix_sparse_build(const saix_sparse_plan *plan, const void *value
         i64 len = n - ((i64)1 << k) + 1;
         i64 half = k ? ((i64)1 << (k - 1)) : 0;
         int g = grid_for(len, 256);
+        int esz = plan->mode == SAIX_SPARSE_PACK64 ? 8 : 4;
+        Prof prof_(k == 0 ? "rmq.level0" : "rmq.level", k == 0 ? (double)(value_bytes + esz) * n : 3.0 * esz * len, st);
         if (plan->mode == SAIX_SPARSE_PACK32 || plan->mode == SAIX_SPARSE_PACK64) {
             bool p32 = plan->mode == SAIX_SPARSE_PACK32;
             if (k == 0) {
@@ -211,6 +213,8 @@ extern "C" int saix_sparse_query(const saix_sparse_plan *plan, const void *table
     cudaStream_t st = (cudaStream_t)stream;
     int g = grid_for(q, 256);
     PlanDev P = dev_plan(plan);
+    // 2 x int64 in, int64 out, two random table probes at one 32 B sector each
+    Prof prof_("rmq.query", 88.0 * q, st);
     if (value_bytes == 4)
         k_sparse_query<u32><<<g, 256, 0, st>>>(P, table, Vals<u32>{(const u32 *)values}, qi, qj, q, out_index, out_value, err);
     else
@@ -231,6 +235,7 @@ extern "C" int saix_lcp_query(const saix_sparse_plan *plan, const void *table, c
     cudaStream_t st = (cudaStream_t)stream;
     int g = grid_for(q, 256);
     PlanDev P = dev_plan(plan);
+    Prof prof_("rmq.lcp_query", 152.0 * q, st);
     if (lcp_bytes == 8)
         k_lcp_query<i64><<<g, 256, 0, st>>>(P, table, Vals<i64>{(const i64 *)lcp}, isa, qi, qj, q, out, err);
     else

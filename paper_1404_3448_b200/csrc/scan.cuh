@@ -124,7 +124,9 @@ inline i64 scan_tmp_words(i64 n) { return ceil_div(n > 0 ? n : 1, SCAN_TILE) + 1
 // Exclusive scan of in(0..n) fed to out(); *d_total (device, nullable) gets
 // the sum.  tmp must hold scan_tmp_words(n) u32.
 template <class In, class Out>
-int scan_transform(In in, Out out, i64 n, u32 *tmp, u32 *d_total, cudaStream_t st) {
+int scan_transform(In in, Out out, i64 n, u32 *tmp, u32 *d_total, cudaStream_t st,
+                   const char *prof_name = "scan", double prof_bytes = 0) {
+    Prof prof_(prof_name, prof_bytes, st);
     if (n <= 0) {
         if (d_total) SAIX_CUDA(cudaMemsetAsync(d_total, 0, sizeof(u32), st));
         return SAIX_OK;
