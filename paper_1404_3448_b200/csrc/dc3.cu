@@ -234,6 +234,8 @@ struct MergeIdx {
     const u32 *A, *B;
     __device__ __forceinline__ i64 apos(i64 i) const { return R.L.pos(A[i]); }
     __device__ __forceinline__ i64 bpos(i64 j) const { return 3 * (i64)B[j]; }
+    __device__ __forceinline__ i64 apos_cs(i64 i) const { return R.L.pos(__ldcs(A + i)); }
+    __device__ __forceinline__ i64 bpos_cs(i64 j) const { return 3 * (i64)__ldcs(B + j); }
     __device__ __forceinline__ MRec rec(i64 p) const { return make_rec(T, R, p); }
 };
 // Merge inputs given as positions with a by-position rank array
@@ -245,6 +247,8 @@ struct MergePos {
     const u32 *A, *B;
     __device__ __forceinline__ i64 apos(i64 i) const { return A[i]; }
     __device__ __forceinline__ i64 bpos(i64 j) const { return B[j]; }
+    __device__ __forceinline__ i64 apos_cs(i64 i) const { return A[i]; }
+    __device__ __forceinline__ i64 bpos_cs(i64 j) const { return B[j]; }
     __device__ __forceinline__ MRec rec(i64 p) const { return make_rec(T, R, p); }
 };
 
@@ -257,18 +261,39 @@ constexpr int MT_THREADS = 256;
 constexpr int MT_ITEMS = 8;
 constexpr int MT_TILE = MT_THREADS * MT_ITEMS;  // 2048 outputs per CTA
 
+// One warp per tile boundary: a 33-ary search (each lane probes one split
+// candidate per round) so a split costs ~log_32(n) dependent gather rounds.
 template <class V>
 __global__ void k_merge_partition(V v, i64 na, i64 nb, i64 ntiles, u32 *__restrict__ split) {
     i64 total = na + nb;
-    for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t <= ntiles; t += (i64)gridDim.x * blockDim.x) {
+    int lane = lane_id();
+    i64 warps = ((i64)gridDim.x * blockDim.x) >> 5;
+    for (i64 t = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t <= ntiles; t += warps) {
         i64 d = t * MT_TILE < total ? t * MT_TILE : total;
+        // invariant: answer in [lo, hi]; P(x) = a_first(A[x], B[d-1-x]) is
+        // true for x < answer and false from answer on
         i64 lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
         while (lo < hi) {
-            i64 mid = (lo + hi) >> 1;
-            if (rec_a_first(v.rec(v.apos(mid)), v.rec(v.bpos(d - 1 - mid)))) lo = mid + 1;
-            else hi = mid;
+            i64 span = hi - lo;
+            i64 x = lo + (span * (lane + 1)) / 33;  // candidates in [lo, hi)
+            bool p = x < hi && rec_a_first(v.rec(v.apos(x)), v.rec(v.bpos(d - 1 - x)));
+            u32 tr = __ballot_sync(0xffffffffu, p);
+            u32 fl = __ballot_sync(0xffffffffu, x < hi && !p);
+            // last true candidate -> lo = x+1; first false candidate -> hi = x
+            if (tr) {
+                int lt = 31 - __clz(tr);
+                lo = __shfl_sync(0xffffffffu, x, lt) + 1;
+            }
+            if (fl) {
+                int lf = __ffs(fl) - 1;
+                hi = __shfl_sync(0xffffffffu, x, lf);
+            }
+            if (span <= 32) {
+                // every candidate in [lo, hi) was probed this round
+                break;
+            }
         }
-        split[t] = (u32)lo;
+        if (lane == 0) split[t] = (u32)lo;
     }
 }
 
@@ -283,8 +308,16 @@ k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict
     i64 i0 = split[blockIdx.x], i1 = split[blockIdx.x + 1];
     i64 j0 = d0 - i0;
     int nat = (int)(i1 - i0), cnt = (int)(d1 - d0), nbt = cnt - nat;
-    for (int x = threadIdx.x; x < cnt; x += MT_THREADS)
-        sh[x] = v.rec(x < nat ? v.apos(i0 + x) : v.bpos(j0 + (x - nat)));
+#pragma unroll
+    for (int q = 0; q < MT_ITEMS; q++) {
+        int x = threadIdx.x + q * MT_THREADS;
+        if (x < cnt) sh[x].pos = (u32)(x < nat ? v.apos_cs(i0 + x) : v.bpos_cs(j0 + (x - nat)));
+    }
+#pragma unroll
+    for (int q = 0; q < MT_ITEMS; q++) {
+        int x = threadIdx.x + q * MT_THREADS;
+        if (x < cnt) sh[x] = v.rec(sh[x].pos);
+    }
     __syncthreads();
     const MRec *A = sh, *B = sh + nat;
     int dt = threadIdx.x * MT_ITEMS;
@@ -306,7 +339,7 @@ k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict
     __syncthreads();
     for (int x = threadIdx.x; x < cnt; x += MT_THREADS) {
         u32 p = out[x];
-        sa[d0 + x] = p;
+        __stcs(sa + d0 + x, p);
         if (isa) isa[p] = (u32)(d0 + x);
     }
 }
@@ -318,7 +351,7 @@ static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStr
     i64 ntiles = ceil_div(total, MT_TILE);
     {
         Prof prof_("dc3.merge_partition", 4.0 * (ntiles + 1), st);
-        k_merge_partition<V><<<grid_for(ntiles + 1, 128), 128, 0, st>>>(v, na, nb, ntiles, split);
+        k_merge_partition<V><<<grid_for((ntiles + 1) * 32, 128), 128, 0, st>>>(v, na, nb, ntiles, split);
     }
     SAIX_LAUNCHED();
     {

@@ -363,7 +363,9 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
     SAIX_ARENA_OK(ar);
     SAIX_TRY(saix_encode_gsa(a_ascii, na, b_ascii, nb, keep_n, w.gsa, bad_pos, stream));
     int sigma = (keep_n ? 5 : 4) + 1;  // max(sigma_A, sigma_B) + 1 (overlap.py:88)
-    SAIX_TRY(saix_dc3(w.gsa, 1, n, sigma, w.sa, w.isa, w.rest, w.rest_bytes, nullptr, stream));
+    // the pipeline never needs the top-level ISA (LCP runs on Phi/SA), so
+    // the merge skips that scatter
+    SAIX_TRY(saix_dc3(w.gsa, 1, n, sigma, w.sa, nullptr, w.rest, w.rest_bytes, nullptr, stream));
     SAIX_TRY(saix_lcp(w.gsa, 1, n, w.sa, w.isa, w.lcp, w.rest, w.rest_bytes, stream));
     return overlap_scan(w.sa, w.lcp, n, na, out3, w.ov, st);
 }
