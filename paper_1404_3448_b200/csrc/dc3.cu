@@ -20,6 +20,7 @@
 //             position left, stably split by first character.
 //   4 merge   (_merge_walk 173-218): merge-path partition with the DC3
 //             comparator, ISA scattered in the same kernel.
+#include "onesweep.cuh"
 #include "radix.cuh"
 
 namespace saix {
@@ -65,15 +66,16 @@ struct StoreExcl {
     __device__ void operator()(i64 i, u32 excl, u32) const { out[i] = excl; }
 };
 
-template <typename TT>
+// OT = u8 when the names fit a byte: the recursion string is then a u8 text
+template <typename TT, typename OT>
 __global__ void k_bitmap_name(Text<TT> T, SampleLayout L, u64 s1, const u32 *__restrict__ bm,
-                              const u32 *__restrict__ wp, u32 *__restrict__ tt) {
+                              const u32 *__restrict__ wp, OT *__restrict__ tt) {
     for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < L.m; s += (i64)gridDim.x * blockDim.x) {
         i64 p = L.pos(s);
         u64 code = ((u64)T(p) * s1 + T(p + 1)) * s1 + T(p + 2);
         u32 w = (u32)(code >> 5);
         u32 below = bm[w] & ((1u << (code & 31)) - 1u);
-        tt[s] = wp[w] + __popc(below) + 1u;
+        tt[s] = (OT)(wp[w] + __popc(below) + 1u);
     }
 }
 
@@ -105,6 +107,35 @@ __global__ void k_first_two_keys(Text<TT> T, SampleLayout L, int b, const u32 *_
         keys[i] = ((u64)T(p) << b) | (u64)T(p + 1);
     }
 }
+
+// onesweep sources: packed triple keys of the samples, read from the text
+template <typename TT>
+struct TripleSrc {
+    Text<TT> T;
+    SampleLayout L;
+    int b;
+    __device__ __forceinline__ bool get(i64 s, u64 &k, u32 &v) const {
+        i64 p = L.pos(s);
+        k = ((u64)T(p) << (2 * b)) | ((u64)T(p + 1) << b) | (u64)T(p + 2);
+        v = (u32)s;
+        return true;
+    }
+};
+// mod-0 split source: mod-1 samples in rank order (s < m1), keyed by the
+// first character of the mod-0 suffix 3s (suffix_index.py:274-290)
+template <typename TT>
+struct Mod0Src {
+    Text<TT> T;
+    const u32 *sac;
+    u32 m1;
+    __device__ __forceinline__ bool get(i64 i, u32 &k, u32 &v) const {
+        u32 s = __ldcs(sac + i);
+        if (s >= m1) return false;
+        k = T(3 * (i64)s);
+        v = s;
+        return true;
+    }
+};
 
 struct FlagPacked {
     const u64 *keys;
@@ -422,13 +453,14 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
 // Steps 1-2: names of the sample triples, then SAc/ISAc (recursing if needed).
 template <typename TT>
 static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma, u32 *tt,
-                        u32 *SAc, u32 *ISAc, u32 *d_scal, int depth) {
+                        u32 *SAc, u32 *ISAc, u32 *d_scal, int depth, bool keep_u32) {
     Arena &ar = *c.ar;
     cudaStream_t st = c.st;
     size_t mark = ar.mark();
     i64 m = L.m;
     int g = grid_for(m, K_THREADS);
     u32 D = 0;
+    bool narrow = false;  // recursion string stored as u8
     u32 *sorted_vals = nullptr;
     if (use_bitmap(sigma, m)) {
         u64 s1 = sigma + 1;
@@ -447,29 +479,28 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         }
         SAIX_LAUNCHED();
         SAIX_TRY(scan_transform(PopcIn{bm}, StoreExcl{wp}, nwords, tmp, d_scal, st, "dc3.bitmap_scan", 8.0 * nwords));
+        SAIX_TRY(read_u32(d_scal, &D, st));
+        narrow = !keep_u32 && D <= 255 && (i64)D < m;
         {
-            Prof prof_("dc3.bitmap_name", (double)sizeof(TT) * L.n + 4.0 * m, st);
-            k_bitmap_name<TT><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, tt);
+            Prof prof_("dc3.bitmap_name", (double)sizeof(TT) * L.n + (narrow ? 1.0 : 4.0) * m, st);
+            if (narrow) k_bitmap_name<TT, u8><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, (u8 *)tt);
+            else k_bitmap_name<TT, u32><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, tt);
         }
         SAIX_LAUNCHED();
-        SAIX_TRY(read_u32(d_scal, &D, st));
     } else {
         int b = bits_for(sigma);
         u64 *k0 = ar.alloc<u64>(m), *k1 = ar.alloc<u64>(m);
         u32 *v0 = ar.alloc<u32>(m), *v1 = ar.alloc<u32>(m);
-        u32 *scratch = ar.alloc<u32>(radix_scratch_words(m));
+        u32 *scratch = ar.alloc<u32>(radix_scratch_words(m) > os_scratch_words(m) ? radix_scratch_words(m)
+                                                                                  : os_scratch_words(m));
         u32 *tmp = ar.alloc<u32>(scan_tmp_words(m));
         SAIX_ARENA_OK(ar);
         u64 *keys = k0;
         u32 *vals = v0;
         if (3 * b <= 64) {
-            {
-                Prof prof_("dc3.triple_keys", (double)sizeof(TT) * L.n + 12.0 * m, st);
-                k_triple_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, b, k0, v0);
-            }
-            SAIX_LAUNCHED();
-            SAIX_TRY(radix_sort_pairs<u64>(keys, vals, keys == k0 ? k1 : k0, vals == v0 ? v1 : v0, m, 0,
-                                           3 * b, scratch, st));
+            int passes = (3 * b + OS_BITS - 1) / OS_BITS;
+            SAIX_TRY(onesweep_sort<u64>(TripleSrc<TT>{T, L, b}, m, m, 0, passes, k0, v0, k1, v1, scratch, keys, vals,
+                                        nullptr, st, "dc3.triple_sort"));
             SAIX_TRY(scan_transform(FlagPacked{keys}, ScatterName{vals, tt}, m, tmp, d_scal, st, "dc3.name_scan",
                                     16.0 * m));
         } else {
@@ -495,7 +526,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         ar.reset(mark);
     } else {
         ar.reset(mark);
-        SAIX_TRY(dc3_level<u32>(c, tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
+        if (narrow) SAIX_TRY(dc3_level<u8>(c, (const u8 *)tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
+        else SAIX_TRY(dc3_level<u32>(c, tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
     }
     return SAIX_OK;
 }
@@ -522,7 +554,7 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     SAIX_ARENA_OK(ar);
     Text<TT> T{text, N};
 
-    SAIX_TRY(sort_samples<TT>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth));
+    SAIX_TRY(sort_samples<TT>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth, probe != nullptr));
 
     // step 3: mod-0 suffixes = mod-1 samples in rank order, minus one,
     // stably split by their first character
@@ -530,14 +562,15 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     i64 k = L.k;
     u32 *k0 = ar.alloc<u32>(k), *k1 = ar.alloc<u32>(k);
     u32 *v0 = ar.alloc<u32>(k), *v1 = ar.alloc<u32>(k);
-    u32 *scratch = ar.alloc<u32>(radix_scratch_words(k));
-    u32 *tmp = ar.alloc<u32>(scan_tmp_words(L.m));
+    u32 *scratch = ar.alloc<u32>(os_scratch_words(L.m));
     u32 *split = ar.alloc<u32>(merge_split_words(N));
     SAIX_ARENA_OK(ar);
-    SAIX_TRY(scan_transform(Mod1Flag<TT>{SAc, L.m1}, Mod0Emit<TT>{T, SAc, k0, v0}, L.m, tmp, nullptr, st,
-                            "dc3.mod0_compact", 4.0 * L.m + (8.0 + sizeof(TT)) * k));
     u32 *keys = k0, *vals = v0;
-    SAIX_TRY(radix_sort_pairs<u32>(keys, vals, k1, v1, k, 0, bits_for(sigma), scratch, st));
+    {
+        int passes = (bits_for(sigma) + OS_BITS - 1) / OS_BITS;
+        SAIX_TRY(onesweep_sort<u32>(Mod0Src<TT>{T, SAc, (u32)L.m1}, L.m, k, 0, passes, k0, v0, k1, v1, scratch,
+                                    keys, vals, nullptr, st, "dc3.mod0_split"));
+    }
 
     // step 4: merge real samples (skip the padding sample at rank 1) with mod-0
     RankFromIsa R{L, ISAc};
@@ -580,11 +613,11 @@ static size_t dc3_plan(i64 n) {
         SampleLayout L = SampleLayout::of(N);
         i64 m = L.m, k = L.k;
         persistent += (size_t)(3 * m + 8) * 4 + 4 * Arena::kAlign;
-        size_t sort_t = (size_t)m * 24 + (size_t)(radix_scratch_words(m) + scan_tmp_words(m)) * 4;
+        i64 sw = radix_scratch_words(m) > os_scratch_words(m) ? radix_scratch_words(m) : os_scratch_words(m);
+        size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
-        size_t post_t = (size_t)k * 16 + (size_t)(radix_scratch_words(k) + scan_tmp_words(m) +
-                                                  merge_split_words(N)) * 4;
+        size_t post_t = (size_t)k * 16 + (size_t)(os_scratch_words(m) + merge_split_words(N)) * 4;
         size_t t = sort_t > bm_t ? sort_t : bm_t;
         t = t > post_t ? t : post_t;
         t += 8 * Arena::kAlign;

@@ -1,0 +1,255 @@
+// onesweep.cuh -- stable LSD radix sort, one kernel per 8-bit digit pass with
+// decoupled look-back (the B200 realisation of the reference's per-digit
+// split passes, parallel_sort.py:150-203).
+//
+//   k_os_hist   one read of the source: privatised histograms of every digit
+//               pass at once (all passes' counts are permutation-invariant)
+//   k_os_scan   per-pass exclusive digit offsets (one CTA)
+//   k_os_pass   per tile (in atomic-ticket order): load, warp-stable ranking
+//               with __match_any_sync, publish the tile's per-digit counts,
+//               look back over earlier tiles' status words for the digit's
+//               global prefix, stage the tile digit-sorted in shared memory,
+//               write runs out coalesced.
+//
+// Sources are functors so the first pass can build keys on the fly (DC3
+// triple keys straight from the text; the mod-0 split straight from the
+// sample order with an in-line filter) without materialising a key array:
+//   struct Src { __device__ bool get(i64 i, K &key, u32 &val) const; };
+// Items for which get() returns false are dropped (filter); the output holds
+// the valid items only, in stable order.
+#pragma once
+
+#include "common.cuh"
+
+namespace saix {
+
+constexpr int OS_BITS = 8;
+constexpr int OS_RADIX = 1 << OS_BITS;
+constexpr int OS_THREADS = 256;
+constexpr int OS_WARPS = OS_THREADS / 32;
+constexpr int OS_ITEMS = 16;
+constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096
+constexpr int OS_MAX_PASSES = 8;
+constexpr u32 OS_FLAG_AGG = 1u << 30, OS_FLAG_PRE = 2u << 30, OS_MASK = (1u << 30) - 1;
+static_assert(OS_THREADS == OS_RADIX, "one thread per digit in the look-back phase");
+
+template <typename K>
+struct ArraySrc {
+    const K *keys;
+    const u32 *vals;
+    __device__ __forceinline__ bool get(i64 i, K &k, u32 &v) const {
+        k = keys[i];
+        v = vals[i];
+        return true;
+    }
+};
+
+inline i64 os_tiles(i64 n) { return ceil_div(n > 0 ? n : 1, OS_TILE); }
+
+// Scratch: hist [passes][256] + offsets + status [tiles][256] + ticket.
+inline i64 os_scratch_words(i64 n) { return 2 * OS_MAX_PASSES * OS_RADIX + 64 + os_tiles(n) * OS_RADIX + 64; }
+
+template <typename K, class Src>
+__global__ void __launch_bounds__(OS_THREADS)
+k_os_hist(Src src, i64 n, int shift0, int passes, u32 *__restrict__ hist) {
+    __shared__ u32 sh[OS_MAX_PASSES][OS_RADIX];
+    for (int x = threadIdx.x; x < OS_MAX_PASSES * OS_RADIX; x += OS_THREADS) (&sh[0][0])[x] = 0;
+    __syncthreads();
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        K k;
+        u32 v;
+        if (!src.get(i, k, v)) continue;
+        for (int p = 0; p < passes; p++) atomicAdd(&sh[p][(u32)(k >> (shift0 + OS_BITS * p)) & (OS_RADIX - 1)], 1u);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < passes * OS_RADIX; x += OS_THREADS)
+        if ((&sh[0][0])[x]) atomicAdd(&hist[x], (&sh[0][0])[x]);
+}
+
+// One CTA of 256 threads: exclusive scan over digits of every pass.
+__global__ void __launch_bounds__(OS_RADIX) k_os_scan(const u32 *__restrict__ hist, int passes, u32 *__restrict__ offs,
+                                                       u32 *__restrict__ total) {
+    __shared__ u32 sh[OS_RADIX];
+    for (int p = 0; p < passes; p++) {
+        u32 v = hist[p * OS_RADIX + threadIdx.x];
+        sh[threadIdx.x] = v;
+        __syncthreads();
+        // Hillis-Steele inclusive scan over 256 digits
+        for (int o = 1; o < OS_RADIX; o <<= 1) {
+            u32 y = threadIdx.x >= o ? sh[threadIdx.x - o] : 0u;
+            __syncthreads();
+            sh[threadIdx.x] += y;
+            __syncthreads();
+        }
+        offs[p * OS_RADIX + threadIdx.x] = sh[threadIdx.x] - v;
+        if (p == 0 && threadIdx.x == OS_RADIX - 1 && total) *total = sh[threadIdx.x];
+        __syncthreads();
+    }
+}
+
+template <typename K, class Src>
+__global__ void __launch_bounds__(OS_THREADS)
+k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restrict__ status, u32 *__restrict__ ticket,
+          K *__restrict__ keys_out, u32 *__restrict__ vals_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    K *sk = reinterpret_cast<K *>(smem);
+    u32 *sv = reinterpret_cast<u32 *>(sk + OS_TILE);
+    u32(*cnt)[OS_RADIX] = reinterpret_cast<u32(*)[OS_RADIX]>(sv + OS_TILE);
+    u32 *tile_excl = &cnt[OS_WARPS][0];
+    u32 *gbase = tile_excl + OS_RADIX;
+    __shared__ u32 sh_tile, sh_warp[OS_WARPS + 1];
+
+    if (threadIdx.x == 0) sh_tile = atomicAdd(ticket, 1u);
+    int w = threadIdx.x >> 5, lane = lane_id();
+    for (int d = lane; d < OS_RADIX; d += 32) cnt[w][d] = 0;
+    __syncthreads();
+    const u32 tile = sh_tile;
+    i64 seg = (i64)tile * OS_TILE + (i64)w * (32 * OS_ITEMS);
+    K k[OS_ITEMS];
+    u32 v[OS_ITEMS], rank[OS_ITEMS], dig[OS_ITEMS];
+    u32 lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < OS_ITEMS; r++) {
+        i64 i = seg + r * 32 + lane;
+        bool ok = i < n && src.get(i, k[r], v[r]);
+        u32 d = ok ? ((u32)(k[r] >> shift) & (OS_RADIX - 1)) : (u32)OS_RADIX;
+        dig[r] = d;
+        u32 peers = __match_any_sync(0xffffffffu, d);
+        u32 before = __popc(peers & lt);
+        u32 cur = ok ? cnt[w][d] : 0u;
+        __syncwarp();
+        if (ok && before == 0) cnt[w][d] = cur + __popc(peers);
+        __syncwarp();
+        rank[r] = cur + before;
+    }
+    __syncthreads();
+    // thread d owns digit d: warp-exclusive prefixes, tile count, look-back
+    {
+        const int d = threadIdx.x;
+        u32 run = 0;
+#pragma unroll
+        for (int q = 0; q < OS_WARPS; q++) {
+            u32 c = cnt[q][d];
+            cnt[q][d] = run;
+            run += c;
+        }
+        u32 *my = status + (i64)tile * OS_RADIX + d;
+        u32 excl = 0;
+        if (tile == 0) {
+            *(volatile u32 *)my = OS_FLAG_PRE | run;
+        } else {
+            *(volatile u32 *)my = OS_FLAG_AGG | run;
+            i64 t = (i64)tile - 1;
+            while (true) {
+                u32 s = *(volatile const u32 *)(status + t * OS_RADIX + d);
+                if ((s & ~OS_MASK) == 0) continue;  // predecessor not published yet
+                excl += s & OS_MASK;
+                if (s & OS_FLAG_PRE) break;
+                t--;
+            }
+            *(volatile u32 *)my = OS_FLAG_PRE | (excl + run);
+        }
+        gbase[d] = offs[d] + excl;
+        // exclusive scan of tile counts over digits (tile-local staging offsets)
+        u32 inc = run;
+        for (int o = 1; o < 32; o <<= 1) {
+            u32 y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) sh_warp[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            u32 x = lane < OS_WARPS ? sh_warp[lane] : 0u;
+            u32 xi = x;
+            for (int o = 1; o < 32; o <<= 1) {
+                u32 y = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += y;
+            }
+            if (lane < OS_WARPS) sh_warp[lane] = xi - x;
+            if (lane == OS_WARPS - 1) sh_warp[OS_WARPS] = xi;
+        }
+        __syncthreads();
+        tile_excl[d] = sh_warp[w] + inc - run;
+    }
+    __syncthreads();
+    const u32 valid = sh_warp[OS_WARPS];
+#pragma unroll
+    for (int r = 0; r < OS_ITEMS; r++) {
+        u32 d = dig[r];
+        if (d < OS_RADIX) {
+            u32 lp = tile_excl[d] + cnt[w][d] + rank[r];
+            sk[lp] = k[r];
+            sv[lp] = v[r];
+        }
+    }
+    __syncthreads();
+    for (u32 x = threadIdx.x; x < valid; x += OS_THREADS) {
+        K kk = sk[x];
+        u32 d = (u32)(kk >> shift) & (OS_RADIX - 1);
+        u32 dst = gbase[d] + (x - tile_excl[d]);
+        keys_out[dst] = kk;
+        vals_out[dst] = sv[x];
+    }
+}
+
+template <typename K>
+constexpr size_t os_pass_smem() {
+    return (size_t)OS_TILE * (sizeof(K) + 4) + (size_t)(OS_WARPS + 2) * OS_RADIX * 4;
+}
+
+// Sort `n` source items on bits [shift0, shift0 + 8*passes).  Pass 0 reads
+// `src` (which may filter); n_out is the number of valid items, which the
+// caller must know on the host when passes > 1.  Later passes ping-pong
+// between (k0,v0) and (k1,v1); out_k/out_v receive the result buffers.
+template <typename K, class Src>
+int onesweep_sort(Src src, i64 n, i64 n_out, int shift0, int passes, K *k0, u32 *v0, K *k1, u32 *v1, u32 *scratch,
+                  K *&out_k, u32 *&out_v, u32 *d_count, cudaStream_t st, const char *prof = "onesweep") {
+    if (passes < 1 || passes > OS_MAX_PASSES || n >= ((i64)1 << 30)) {
+        set_error("onesweep_sort: unsupported passes=%d n=%lld", passes, (long long)n);
+        return SAIX_EINVAL;
+    }
+    static bool attr_set = false;
+    if (!attr_set) {
+        SAIX_CUDA(cudaFuncSetAttribute(k_os_pass<K, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)os_pass_smem<K>()));
+        SAIX_CUDA(cudaFuncSetAttribute(k_os_pass<K, ArraySrc<K>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)os_pass_smem<K>()));
+        attr_set = true;
+    }
+    u32 *hist = scratch;
+    u32 *offs = hist + OS_MAX_PASSES * OS_RADIX;
+    u32 *ticket = offs + OS_MAX_PASSES * OS_RADIX;  // 32 words, one per pass
+    u32 *status = ticket + 64;
+    Prof prof_(prof, ((double)n + (double)n_out * (2 * passes - 1)) * (sizeof(K) + 4), st);
+    SAIX_CUDA(cudaMemsetAsync(hist, 0, (size_t)(OS_MAX_PASSES * OS_RADIX) * 4, st));
+    SAIX_CUDA(cudaMemsetAsync(ticket, 0, 64 * 4, st));
+    k_os_hist<K, Src><<<grid_for(n, OS_THREADS, kNumSMs * 4), OS_THREADS, 0, st>>>(src, n, shift0, passes, hist);
+    SAIX_LAUNCHED();
+    k_os_scan<<<1, OS_RADIX, 0, st>>>(hist, passes, offs, d_count);
+    SAIX_LAUNCHED();
+    K *ok = k0;
+    u32 *ov = v0;
+    for (int p = 0; p < passes; p++) {
+        i64 np = p == 0 ? n : n_out;
+        i64 ntiles = os_tiles(np);
+        SAIX_CUDA(cudaMemsetAsync(status, 0, (size_t)ntiles * OS_RADIX * 4, st));
+        K *dk = (p % 2 == 0) ? k0 : k1;
+        u32 *dv = (p % 2 == 0) ? v0 : v1;
+        if (p == 0) {
+            k_os_pass<K, Src><<<(unsigned)ntiles, OS_THREADS, os_pass_smem<K>(), st>>>(
+                src, n, shift0, offs, status, ticket, dk, dv);
+        } else {
+            ArraySrc<K> as{ok, ov};
+            k_os_pass<K, ArraySrc<K>><<<(unsigned)ntiles, OS_THREADS, os_pass_smem<K>(), st>>>(
+                as, np, shift0 + OS_BITS * p, offs + OS_RADIX * p, status, ticket + p, dk, dv);
+        }
+        SAIX_LAUNCHED();
+        ok = dk;
+        ov = dv;
+    }
+    out_k = ok;
+    out_v = ov;
+    return SAIX_OK;
+}
+
+}  // namespace saix
