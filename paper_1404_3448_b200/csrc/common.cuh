@@ -137,6 +137,12 @@ inline int bits_for(u64 v) {  // bit width of v (>= 1), like int.bit_length()
     return b;
 }
 
+// LCP (lcp.cu) with the pipeline option of folding longest_overlap's pass 1
+// (max LCP over cross-sequence adjacent pairs, separator at `boundary`) into
+// the final permute kernel; boundary < 0 disables it.
+int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
+                cudaStream_t st, i64 boundary, u32 *best);
+
 // DC3 sample layout (suffix_index.py:149-153): mod-1 positions 1,4,... and
 // mod-2 positions 2,5,... below limit = n+1 if n%3==1 else n.
 struct SampleLayout {

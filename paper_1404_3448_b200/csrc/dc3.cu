@@ -109,14 +109,16 @@ __global__ void k_first_two_keys(Text<TT> T, SampleLayout L, int b, const u32 *_
 }
 
 // onesweep sources: packed triple keys of the samples, read from the text
+// Mixed-radix triple key ((c0 s1 + c1) s1 + c2), s1 = sigma + 1: order-
+// preserving and 3 log2(s1) bits instead of 3 ceil(log2(s1)).
 template <typename TT>
 struct TripleSrc {
     Text<TT> T;
     SampleLayout L;
-    int b;
+    u64 s1;
     __device__ __forceinline__ bool get(i64 s, u64 &k, u32 &v) const {
         i64 p = L.pos(s);
-        k = ((u64)T(p) << (2 * b)) | ((u64)T(p + 1) << b) | (u64)T(p + 2);
+        k = ((u64)T(p) * s1 + T(p + 1)) * s1 + T(p + 2);
         v = (u32)s;
         return true;
     }
@@ -133,6 +135,16 @@ struct Mod0Src {
         if (s >= m1) return false;
         k = T(3 * (i64)s);
         v = s;
+        return true;
+    }
+};
+// the same multiset of mod-0 first characters, streamed in text order
+template <typename TT>
+struct Mod0HistSrc {
+    Text<TT> T;
+    __device__ __forceinline__ bool get(i64 j, u32 &k, u32 &v) const {
+        k = T(3 * j);
+        v = 0;
         return true;
     }
 };
@@ -472,7 +484,9 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         SAIX_ARENA_OK(ar);
         SAIX_CUDA(cudaMemsetAsync(bm, 0, (size_t)nwords * 4, st));
         int use_smem = nwords * 4 <= 48 * 1024;
-        int gs = use_smem ? (g < 2 * kNumSMs ? g : 2 * kNumSMs) : g;
+        // tiny bitmaps (level 0: <= 216 codes) merge cheaply from every CTA;
+        // larger ones are privatised in fewer, longer-lived CTAs
+        int gs = (use_smem && nwords > 1024) ? (g < 2 * kNumSMs ? g : 2 * kNumSMs) : g;
         {
             Prof prof_("dc3.bitmap_set", (double)sizeof(TT) * L.n, st);
             k_bitmap_set<TT><<<gs, K_THREADS, use_smem ? nwords * 4 : 0, st>>>(T, L, s1, bm, nwords, use_smem);
@@ -498,9 +512,12 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         u64 *keys = k0;
         u32 *vals = v0;
         if (3 * b <= 64) {
-            int passes = (3 * b + OS_BITS - 1) / OS_BITS;
-            SAIX_TRY(onesweep_sort<u64>(TripleSrc<TT>{T, L, b}, m, m, 0, passes, k0, v0, k1, v1, scratch, keys, vals,
-                                        nullptr, st, "dc3.triple_sort"));
+            u64 s1 = sigma + 1;
+            int kb = bits_for(s1 * s1 * s1 - 1);
+            int passes = (kb + OS_BITS - 1) / OS_BITS;
+            TripleSrc<TT> src{T, L, s1};
+            SAIX_TRY(onesweep_sort<u64>(src, m, src, m, m, 0, passes, k0, v0, k1, v1, scratch, keys, vals, nullptr,
+                                        st, "dc3.triple_sort"));
             SAIX_TRY(scan_transform(FlagPacked{keys}, ScatterName{vals, tt}, m, tmp, d_scal, st, "dc3.name_scan",
                                     16.0 * m));
         } else {
@@ -568,8 +585,8 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     u32 *keys = k0, *vals = v0;
     {
         int passes = (bits_for(sigma) + OS_BITS - 1) / OS_BITS;
-        SAIX_TRY(onesweep_sort<u32>(Mod0Src<TT>{T, SAc, (u32)L.m1}, L.m, k, 0, passes, k0, v0, k1, v1, scratch,
-                                    keys, vals, nullptr, st, "dc3.mod0_split"));
+        SAIX_TRY(onesweep_sort<u32>(Mod0Src<TT>{T, SAc, (u32)L.m1}, L.m, Mod0HistSrc<TT>{T}, k, k, 0, passes, k0,
+                                    v0, k1, v1, scratch, keys, vals, nullptr, st, "dc3.mod0_split"));
     }
 
     // step 4: merge real samples (skip the padding sample at rank 1) with mod-0

@@ -106,15 +106,31 @@ k_plcp(const TT *__restrict__ T, i64 n, u32 *__restrict__ phi_plcp, const u32 *_
     }
 }
 
-// lcp[r] = PLCP[sa[r]] (one gather; lcp[0] = PLCP[sa[0]] = 0).
+// lcp[r] = PLCP[sa[r]] (one gather; lcp[0] = PLCP[sa[0]] = 0).  With
+// best != nullptr it also folds in longest_overlap's first pass
+// (overlap.py:129-136): max lcp over adjacent pairs on opposite sides of the
+// separator at `boundary`.
 __global__ void k_lcp_permute(const u32 *__restrict__ sa, i64 n, const u32 *__restrict__ plcp,
-                              u32 *__restrict__ lcp) {
-    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x)
-        lcp[r] = plcp[sa[r]];
+                              u32 *__restrict__ lcp, u32 boundary, u32 *best) {
+    u32 mx = 0;
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x) {
+        u32 p = sa[r];
+        u32 l = plcp[p];
+        __stcs(lcp + r, l);
+        if (best && r > 0) {
+            u32 q = sa[r - 1];
+            bool cross = p != boundary && q != boundary && ((p < boundary) != (q < boundary));
+            if (cross && l > mx) mx = l;
+        }
+    }
+    if (best) {
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane_id() == 0 && mx) atomicMax(best, mx);
+    }
 }
 
 static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32 *phi, u32 *seeds,
-                   cudaStream_t st) {
+                   cudaStream_t st, i64 boundary, u32 *best) {
     i64 nchunks = ceil_div(n, LCP_CHUNK);
     int g = grid_for(n, 256);
     unsigned tiles = (unsigned)ceil_div(n, LCP_TILE);
@@ -139,10 +155,20 @@ static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32
     SAIX_LAUNCHED();
     {
         Prof prof_("lcp.permute", 12.0 * n, st);
-        k_lcp_permute<<<g, 256, 0, st>>>(sa, n, phi, lcp);
+        k_lcp_permute<<<g, 256, 0, st>>>(sa, n, phi, lcp, boundary >= 0 ? (u32)boundary : 0u,
+                                         boundary >= 0 ? best : nullptr);
     }
     SAIX_LAUNCHED();
     return SAIX_OK;
+}
+
+int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
+                cudaStream_t st, i64 boundary, u32 *best) {
+    Arena ar{(char *)ws, ws_bytes};
+    u32 *phi = ar.alloc<u32>(n);
+    u32 *seeds = ar.alloc<u32>(ceil_div(n, LCP_CHUNK) + 1);
+    SAIX_ARENA_OK(ar);
+    return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, st, boundary, best);
 }
 
 }  // namespace saix
@@ -173,9 +199,5 @@ extern "C" int saix_lcp(const void *text, int text_bytes, int64_t n, const uint3
         return SAIX_EINVAL;
     }
     (void)isa;  // the Phi formulation needs only SA
-    Arena ar{(char *)ws, ws_bytes};
-    u32 *phi = ar.alloc<u32>(n);
-    u32 *seeds = ar.alloc<u32>(ceil_div(n, LCP_CHUNK) + 1);
-    SAIX_ARENA_OK(ar);
-    return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, (cudaStream_t)stream);
+    return lcp_compute(text, text_bytes, n, sa, lcp, ws, ws_bytes, (cudaStream_t)stream, -1, nullptr);
 }

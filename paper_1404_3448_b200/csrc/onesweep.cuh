@@ -49,17 +49,27 @@ inline i64 os_tiles(i64 n) { return ceil_div(n > 0 ? n : 1, OS_TILE); }
 // Scratch: hist [passes][256] + offsets + status [tiles][256] + ticket.
 inline i64 os_scratch_words(i64 n) { return 2 * OS_MAX_PASSES * OS_RADIX + 64 + os_tiles(n) * OS_RADIX + 64; }
 
+// Digit histograms of every pass in one read.  Few distinct digits per warp
+// are the common case (small alphabets, high key bits), so counts are
+// warp-aggregated with __match_any_sync before the shared-memory atomic.
 template <typename K, class Src>
 __global__ void __launch_bounds__(OS_THREADS)
 k_os_hist(Src src, i64 n, int shift0, int passes, u32 *__restrict__ hist) {
     __shared__ u32 sh[OS_MAX_PASSES][OS_RADIX];
     for (int x = threadIdx.x; x < OS_MAX_PASSES * OS_RADIX; x += OS_THREADS) (&sh[0][0])[x] = 0;
     __syncthreads();
-    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-        K k;
+    const u32 lt = lanemask_lt();
+    const i64 stride = (i64)gridDim.x * blockDim.x;
+    for (i64 base = (i64)blockIdx.x * blockDim.x; base < n; base += stride) {  // warp-uniform trip count
+        i64 i = base + threadIdx.x;
+        K k = 0;
         u32 v;
-        if (!src.get(i, k, v)) continue;
-        for (int p = 0; p < passes; p++) atomicAdd(&sh[p][(u32)(k >> (shift0 + OS_BITS * p)) & (OS_RADIX - 1)], 1u);
+        bool ok = i < n && src.get(i, k, v);
+        for (int p = 0; p < passes; p++) {
+            u32 d = ok ? ((u32)(k >> (shift0 + OS_BITS * p)) & (OS_RADIX - 1)) : (u32)OS_RADIX;
+            u32 peers = __match_any_sync(0xffffffffu, d);
+            if (ok && (peers & lt) == 0) atomicAdd(&sh[p][d], (u32)__popc(peers));
+        }
     }
     __syncthreads();
     for (int x = threadIdx.x; x < passes * OS_RADIX; x += OS_THREADS)
@@ -201,9 +211,14 @@ constexpr size_t os_pass_smem() {
 // `src` (which may filter); n_out is the number of valid items, which the
 // caller must know on the host when passes > 1.  Later passes ping-pong
 // between (k0,v0) and (k1,v1); out_k/out_v receive the result buffers.
-template <typename K, class Src>
-int onesweep_sort(Src src, i64 n, i64 n_out, int shift0, int passes, K *k0, u32 *v0, K *k1, u32 *v1, u32 *scratch,
-                  K *&out_k, u32 *&out_v, u32 *d_count, cudaStream_t st, const char *prof = "onesweep") {
+//
+// `hsrc` (n_h items) must enumerate the same multiset of valid keys as `src`
+// in any order (digit counts are permutation-invariant); it lets the
+// histogram stream over a cheaper source than pass 0's gather.
+template <typename K, class Src, class HSrc>
+int onesweep_sort(Src src, i64 n, HSrc hsrc, i64 n_h, i64 n_out, int shift0, int passes, K *k0, u32 *v0, K *k1,
+                  u32 *v1, u32 *scratch, K *&out_k, u32 *&out_v, u32 *d_count, cudaStream_t st,
+                  const char *prof = "onesweep") {
     if (passes < 1 || passes > OS_MAX_PASSES || n >= ((i64)1 << 30)) {
         set_error("onesweep_sort: unsupported passes=%d n=%lld", passes, (long long)n);
         return SAIX_EINVAL;
@@ -221,9 +236,10 @@ int onesweep_sort(Src src, i64 n, i64 n_out, int shift0, int passes, K *k0, u32 
     u32 *ticket = offs + OS_MAX_PASSES * OS_RADIX;  // 32 words, one per pass
     u32 *status = ticket + 64;
     Prof prof_(prof, ((double)n + (double)n_out * (2 * passes - 1)) * (sizeof(K) + 4), st);
+    if (n <= 0) return SAIX_OK;
     SAIX_CUDA(cudaMemsetAsync(hist, 0, (size_t)(OS_MAX_PASSES * OS_RADIX) * 4, st));
     SAIX_CUDA(cudaMemsetAsync(ticket, 0, 64 * 4, st));
-    k_os_hist<K, Src><<<grid_for(n, OS_THREADS, kNumSMs * 4), OS_THREADS, 0, st>>>(src, n, shift0, passes, hist);
+    k_os_hist<K, HSrc><<<grid_for(n_h, OS_THREADS, kNumSMs * 8), OS_THREADS, 0, st>>>(hsrc, n_h, shift0, passes, hist);
     SAIX_LAUNCHED();
     k_os_scan<<<1, OS_RADIX, 0, st>>>(hist, passes, offs, d_count);
     SAIX_LAUNCHED();

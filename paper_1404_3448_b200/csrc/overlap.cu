@@ -28,20 +28,40 @@ __device__ __forceinline__ u32 rank_of_ascii(u32 c, int keep_n) {
     }
 }
 
+__device__ __forceinline__ u32 encode_at(const u8 *__restrict__ a, i64 na, const u8 *__restrict__ b, i64 i,
+                                          int keep_n, int shift, i64 &local_bad) {
+    u32 r;
+    if (i < na) r = rank_of_ascii(a[i], keep_n);
+    else if (i == na) return 1u;  // separator rank (overlap.py:25)
+    else r = rank_of_ascii(b[i - na - 1], keep_n);
+    if (r == 0) {
+        if (i < local_bad) local_bad = i;
+        r = 1;
+    }
+    return r + shift;
+}
+
+// Four output ranks per thread, stored as one u32 word (out must be 4-byte
+// aligned; the ABI entry points check and fall back to bytes otherwise).
 __global__ void k_encode_gsa(const u8 *__restrict__ a, i64 na, const u8 *__restrict__ b, i64 nb, int keep_n,
-                             int shift, u8 *__restrict__ out, i64 *__restrict__ bad) {
+                             int shift, u8 *__restrict__ out, i64 *__restrict__ bad, int words) {
     i64 n = na + nb + (b ? 1 : 0);
     i64 local_bad = INT64_MAX;
-    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-        u32 r;
-        if (i < na) r = rank_of_ascii(a[i], keep_n);
-        else if (i == na) r = 0xFFu;  // separator
-        else r = rank_of_ascii(b[i - na - 1], keep_n);
-        if (r == 0) {
-            if (i < local_bad) local_bad = i;
-            r = 1;
+    i64 stride = (i64)gridDim.x * blockDim.x;
+    if (words) {
+        u32 *out32 = reinterpret_cast<u32 *>(out);
+        i64 nw = n / 4;
+        for (i64 w = (i64)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride) {
+            u32 word = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) word |= encode_at(a, na, b, 4 * w + j, keep_n, shift, local_bad) << (8 * j);
+            out32[w] = word;
         }
-        out[i] = r == 0xFFu ? 1u : (u8)(r + shift);
+        for (i64 i = 4 * nw + (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+            out[i] = (u8)encode_at(a, na, b, i, keep_n, shift, local_bad);
+    } else {
+        for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+            out[i] = (u8)encode_at(a, na, b, i, keep_n, shift, local_bad);
     }
     if (local_bad != INT64_MAX) atomicMin((unsigned long long *)bad, (unsigned long long)local_bad);
 }
@@ -139,7 +159,7 @@ __device__ __forceinline__ void load_tile(const u32 *__restrict__ sa, const u32 
 
 __global__ void __launch_bounds__(OV_THREADS)
 k_runs_reduce(const u32 *__restrict__ sa, const u32 *__restrict__ lcp, i64 n, const u32 *__restrict__ best_p,
-              u32 boundary, Seg *__restrict__ tile_agg) {
+              u32 boundary, Seg *__restrict__ tile_agg, u32 *__restrict__ tile_join) {
     __shared__ u32 sh_sa[OV_TILE + OV_TILE / 32], sh_l[OV_TILE + OV_TILE / 32];
     u32 best = *best_p;
     i64 base = (i64)blockIdx.x * OV_TILE;
@@ -147,7 +167,32 @@ k_runs_reduce(const u32 *__restrict__ sa, const u32 *__restrict__ lcp, i64 n, co
         if (threadIdx.x == 0) tile_agg[blockIdx.x] = Seg{0u, kInf, kInf};
         return;
     }
-    load_tile(sa, lcp, n, base, sh_sa, sh_l);
+    // Most tiles hold no adjacent pair with lcp >= best: every element is
+    // then a singleton run (one side only, never a candidate) and only the
+    // last element can open a run into the next tile.  Such tiles read the
+    // LCP tile and one SA entry.
+    int join = 0;
+    for (int x = threadIdx.x; x < OV_TILE; x += OV_THREADS) {
+        i64 i = base + x;
+        u32 l = i < n ? __ldcs(lcp + i) : 0u;
+        sh_l[x + (x >> 5)] = l;
+        join |= (i > 0 && i < n && l >= best);
+    }
+    join = __syncthreads_or(join);
+    if (!join) {
+        if (threadIdx.x == 0) {
+            i64 last = (base + OV_TILE < n ? base + OV_TILE : n) - 1;
+            u32 p = sa[last];
+            tile_agg[blockIdx.x] = Seg{1u, p < boundary ? p : kInf, p > boundary ? p : kInf};
+            tile_join[blockIdx.x] = 0;
+        }
+        return;
+    }
+    if (threadIdx.x == 0) tile_join[blockIdx.x] = 1;
+    for (int x = threadIdx.x; x < OV_TILE; x += OV_THREADS) {
+        i64 i = base + x;
+        sh_sa[x + (x >> 5)] = i < n ? sa[i] : 0u;
+    }
     __syncthreads();
     Seg acc{0u, kInf, kInf};
     for (int r = 0; r < OV_ITEMS; r++) {
@@ -176,10 +221,11 @@ __global__ void __launch_bounds__(OV_THREADS) k_runs_carry(Seg *__restrict__ agg
 
 __global__ void __launch_bounds__(OV_THREADS)
 k_runs_apply(const u32 *__restrict__ sa, const u32 *__restrict__ lcp, i64 n, const u32 *__restrict__ best_p,
-             u32 boundary, const Seg *__restrict__ tile_carry, unsigned long long *__restrict__ winner) {
+             u32 boundary, const Seg *__restrict__ tile_carry, const u32 *__restrict__ tile_join,
+             unsigned long long *__restrict__ winner) {
     __shared__ u32 sh_sa[OV_TILE + OV_TILE / 32], sh_l[OV_TILE + OV_TILE / 32];
     u32 best = *best_p;
-    if (best == 0) return;
+    if (best == 0 || !tile_join[blockIdx.x]) return;  // no join: no candidate run ends here
     i64 base = (i64)blockIdx.x * OV_TILE;
     load_tile(sa, lcp, n, base, sh_sa, sh_l);
     __syncthreads();
@@ -229,6 +275,7 @@ struct OverlapWs {
     u32 *best;
     unsigned long long *winner;
     Seg *agg;
+    u32 *join;
 };
 
 static OverlapWs carve_overlap(Arena &ar, i64 n) {
@@ -236,25 +283,30 @@ static OverlapWs carve_overlap(Arena &ar, i64 n) {
     w.best = ar.alloc<u32>(2);
     w.winner = ar.alloc<unsigned long long>(1);
     w.agg = ar.alloc<Seg>(ceil_div(n > 0 ? n : 1, OV_TILE) + 1);
+    w.join = ar.alloc<u32>(ceil_div(n > 0 ? n : 1, OV_TILE) + 1);
     return w;
 }
 
+// best_ready: *w.best already holds the cross-adjacent maximum (the pipeline
+// computes it inside the LCP permute kernel).
 static int overlap_scan(const u32 *sa, const u32 *lcp, i64 n, i64 boundary, i64 *out3, OverlapWs w,
-                        cudaStream_t st) {
-    SAIX_CUDA(cudaMemsetAsync(w.best, 0, sizeof(u32), st));
+                        cudaStream_t st, bool best_ready = false) {
     SAIX_CUDA(cudaMemsetAsync(w.winner, 0xFF, sizeof(unsigned long long), st));
     i64 ntiles = ceil_div(n, OV_TILE);
     int g = grid_for(n, OV_THREADS, kNumSMs * 8);
-    {
+    if (!best_ready) {
+        SAIX_CUDA(cudaMemsetAsync(w.best, 0, sizeof(u32), st));
         Prof prof_("overlap.cross_max", 8.0 * n, st);
         k_cross_max<<<g, OV_THREADS, 0, st>>>(sa, lcp, n, (u32)boundary, w.best);
     }
     SAIX_LAUNCHED();
     {
-        Prof prof_("overlap.runs", 16.0 * n, st);
-        k_runs_reduce<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg);
+        // the run scan must read every LCP entry; SA only where runs join
+        Prof prof_("overlap.runs", 4.0 * n, st);
+        k_runs_reduce<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg, w.join);
         k_runs_carry<<<1, OV_THREADS, 0, st>>>(w.agg, ntiles);
-        k_runs_apply<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg, w.winner);
+        k_runs_apply<<<(unsigned)ntiles, OV_THREADS, 0, st>>>(sa, lcp, n, w.best, (u32)boundary, w.agg, w.join,
+                                                              w.winner);
     }
     SAIX_LAUNCHED();
     k_overlap_finish<<<1, 1, 0, st>>>(w.best, w.winner, (u32)boundary, out3);
@@ -275,8 +327,9 @@ extern "C" int saix_encode_gsa(const uint8_t *a_ascii, int64_t na, const uint8_t
     cudaStream_t st = (cudaStream_t)stream;
     i64 n = na + nb + 1;
     Prof prof_("encode.gsa", 2.0 * n, st);
-    k_encode_gsa<<<grid_for(n, 256), 256, 0, st>>>(a_ascii, na, b_ascii ? b_ascii : a_ascii, nb, keep_n, 1, gsa,
-                                                     bad_pos);
+    int words = ((uintptr_t)gsa & 3) == 0;
+    k_encode_gsa<<<grid_for(words ? n / 4 + 1 : n, 256), 256, 0, st>>>(a_ascii, na, b_ascii ? b_ascii : a_ascii, nb,
+                                                                      keep_n, 1, gsa, bad_pos, words);
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
@@ -289,7 +342,9 @@ extern "C" int saix_encode(const uint8_t *ascii, int64_t n, int keep_n, uint8_t 
     }
     if (n == 0) return SAIX_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    k_encode_gsa<<<grid_for(n, 256), 256, 0, st>>>(ascii, n, nullptr, 0, keep_n, 0, ranks, bad_pos);
+    int words = ((uintptr_t)ranks & 3) == 0;
+    k_encode_gsa<<<grid_for(words ? n / 4 + 1 : n, 256), 256, 0, st>>>(ascii, n, nullptr, 0, keep_n, 0, ranks,
+                                                                      bad_pos, words);
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
@@ -366,6 +421,7 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
     // the pipeline never needs the top-level ISA (LCP runs on Phi/SA), so
     // the merge skips that scatter
     SAIX_TRY(saix_dc3(w.gsa, 1, n, sigma, w.sa, nullptr, w.rest, w.rest_bytes, nullptr, stream));
-    SAIX_TRY(saix_lcp(w.gsa, 1, n, w.sa, w.isa, w.lcp, w.rest, w.rest_bytes, stream));
-    return overlap_scan(w.sa, w.lcp, n, na, out3, w.ov, st);
+    SAIX_CUDA(cudaMemsetAsync(w.ov.best, 0, sizeof(u32), st));
+    SAIX_TRY(lcp_compute(w.gsa, 1, n, w.sa, w.lcp, w.rest, w.rest_bytes, st, na, w.ov.best));
+    return overlap_scan(w.sa, w.lcp, n, na, out3, w.ov, st, true);
 }
