@@ -6,7 +6,7 @@
 //               pass at once (all passes' counts are permutation-invariant)
 //   k_os_scan   per-pass exclusive digit offsets (one CTA)
 //   k_os_pass   per tile (in atomic-ticket order): load, warp-stable ranking
-//               with __match_any_sync, publish the tile's per-digit counts,
+//               (8-ballot peer masks), publish the tile's per-digit counts,
 //               look back over earlier tiles' status words for the digit's
 //               global prefix, stage the tile digit-sorted in shared memory,
 //               write runs out coalesced.
@@ -33,6 +33,20 @@ constexpr int OS_MAX_PASSES = 8;
 constexpr u32 OS_FLAG_AGG = 1u << 30, OS_FLAG_PRE = 2u << 30, OS_MASK = (1u << 30) - 1;
 static_assert(OS_THREADS == OS_RADIX, "one thread per digit in the look-back phase");
 
+// Peer mask of lanes holding the same 8-bit digit: eight ballots + ANDs
+// (cheaper than __match_any_sync on sm_100).  Lanes with d == OS_RADIX (no
+// item) differ from every valid digit in bit 8 via the `valid` ballot.
+__device__ __forceinline__ u32 digit_peers(u32 d) {
+    u32 peers = __ballot_sync(0xffffffffu, d < OS_RADIX);
+    if (d >= OS_RADIX) peers = ~peers;
+#pragma unroll
+    for (int b = 0; b < OS_BITS; b++) {
+        u32 m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? m : ~m;
+    }
+    return peers;
+}
+
 template <typename K>
 struct ArraySrc {
     const K *keys;
@@ -51,7 +65,7 @@ inline i64 os_scratch_words(i64 n) { return 2 * OS_MAX_PASSES * OS_RADIX + 64 + 
 
 // Digit histograms of every pass in one read.  Few distinct digits per warp
 // are the common case (small alphabets, high key bits), so counts are
-// warp-aggregated with __match_any_sync before the shared-memory atomic.
+// warp-aggregated when the digit is uniform across the warp (vote only).
 template <typename K, class Src>
 __global__ void __launch_bounds__(OS_THREADS)
 k_os_hist(Src src, i64 n, int shift0, int passes, u32 *__restrict__ hist) {
@@ -65,10 +79,18 @@ k_os_hist(Src src, i64 n, int shift0, int passes, u32 *__restrict__ hist) {
         K k = 0;
         u32 v;
         bool ok = i < n && src.get(i, k, v);
+        u32 okm = __ballot_sync(0xffffffffu, ok);
         for (int p = 0; p < passes; p++) {
             u32 d = ok ? ((u32)(k >> (shift0 + OS_BITS * p)) & (OS_RADIX - 1)) : (u32)OS_RADIX;
-            u32 peers = __match_any_sync(0xffffffffu, d);
-            if (ok && (peers & lt) == 0) atomicAdd(&sh[p][d], (u32)__popc(peers));
+            // uniform digit across the valid lanes (high key bits, small
+            // alphabets): one atomic for the warp; else one per lane
+            u32 d0 = __shfl_sync(0xffffffffu, d, __ffs(okm ? okm : 1u) - 1);
+            bool uni = __all_sync(0xffffffffu, !ok || d == d0);
+            if (uni) {
+                if (okm && (okm & lt) == 0 && ok) atomicAdd(&sh[p][d], (u32)__popc(okm));
+            } else if (ok) {
+                atomicAdd(&sh[p][d], 1u);
+            }
         }
     }
     __syncthreads();
@@ -124,7 +146,7 @@ k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restri
         bool ok = i < n && src.get(i, k[r], v[r]);
         u32 d = ok ? ((u32)(k[r] >> shift) & (OS_RADIX - 1)) : (u32)OS_RADIX;
         dig[r] = d;
-        u32 peers = __match_any_sync(0xffffffffu, d);
+        u32 peers = digit_peers(d);
         u32 before = __popc(peers & lt);
         u32 cur = ok ? cnt[w][d] : 0u;
         __syncwarp();
