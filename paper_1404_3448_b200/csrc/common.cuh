@@ -140,8 +140,14 @@ inline int bits_for(u64 v) {  // bit width of v (>= 1), like int.bit_length()
 // LCP (lcp.cu) with the pipeline option of folding longest_overlap's pass 1
 // (max LCP over cross-sequence adjacent pairs, separator at `boundary`) into
 // the final permute kernel; boundary < 0 disables it.
+// phi_in (nullable): a precomputed Phi array (Phi[sa[r]] = sa[r-1]) that the
+// call may overwrite (it becomes PLCP); the DC3 merge can emit it.
 int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
-                cudaStream_t st, i64 boundary, u32 *best);
+                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in = nullptr);
+
+// DC3 (dc3.cu); phi (nullable) receives Phi of the top-level suffix array.
+int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, u32 *phi, void *ws,
+                size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream);
 
 // DC3 sample layout (suffix_index.py:149-153): mod-1 positions 1,4,... and
 // mod-2 positions 2,5,... below limit = n+1 if n%3==1 else n.

@@ -342,9 +342,11 @@ __global__ void k_merge_partition(V v, i64 na, i64 nb, i64 ntiles, u32 *__restri
 
 template <class V>
 __global__ void __launch_bounds__(MT_THREADS)
-k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, u32 *__restrict__ isa) {
+k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, u32 *__restrict__ isa,
+             u32 *__restrict__ phi) {
     __shared__ MRec sh[MT_TILE];
-    __shared__ u32 out[MT_TILE];
+    __shared__ u32 prev_tile_last;
+    u32 *out = reinterpret_cast<u32 *>(sh);  // reused for the output tile after the merge
     i64 total = na + nb;
     i64 d0 = (i64)blockIdx.x * MT_TILE;
     i64 d1 = d0 + MT_TILE < total ? d0 + MT_TILE : total;
@@ -361,9 +363,23 @@ k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict
         int x = threadIdx.x + q * MT_THREADS;
         if (x < cnt) sh[x] = v.rec(sh[x].pos);
     }
+    if (phi && threadIdx.x == 0) {
+        // SA[d0-1] is the later of the previous tile's last sample / non-sample
+        u32 last = 0xFFFFFFFFu;
+        if (i0 > 0 && j0 > 0) {
+            MRec a = v.rec(v.apos(i0 - 1)), b = v.rec(v.bpos(j0 - 1));
+            last = rec_a_first(a, b) ? b.pos : a.pos;
+        } else if (i0 > 0) {
+            last = (u32)v.apos(i0 - 1);
+        } else if (j0 > 0) {
+            last = (u32)v.bpos(j0 - 1);
+        }
+        prev_tile_last = last;
+    }
     __syncthreads();
     const MRec *A = sh, *B = sh + nat;
     int dt = threadIdx.x * MT_ITEMS;
+    u32 res[MT_ITEMS];
     if (dt < cnt) {
         int lo = dt > nbt ? dt - nbt : 0, hi = dt < nat ? dt : nat;
         while (lo < hi) {
@@ -376,19 +392,25 @@ k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict
         for (int r = 0; r < MT_ITEMS; r++) {
             if (dt + r >= cnt) break;
             bool takeA = j >= nbt || (i < nat && rec_a_first(A[i], B[j]));
-            out[dt + r] = takeA ? A[i++].pos : B[j++].pos;
+            res[r] = takeA ? A[i++].pos : B[j++].pos;
         }
     }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < MT_ITEMS; r++)
+        if (dt + r < cnt) out[dt + r] = res[r];
     __syncthreads();
     for (int x = threadIdx.x; x < cnt; x += MT_THREADS) {
         u32 p = out[x];
         __stcs(sa + d0 + x, p);
         if (isa) isa[p] = (u32)(d0 + x);
+        // Phi[sa[d]] = sa[d-1] for the LCP stage (lcp.cu), fused here
+        if (phi) phi[p] = x ? out[x - 1] : prev_tile_last;
     }
 }
 
 template <class V>
-static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStream_t st) {
+static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStream_t st, u32 *phi = nullptr) {
     i64 total = na + nb;
     if (total == 0) return SAIX_OK;
     i64 ntiles = ceil_div(total, MT_TILE);
@@ -400,8 +422,10 @@ static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStr
     {
         // indices 4 + chars 2w + ranks (4 per sample, 8 per non-sample) + SA 4 + ISA 4
         double w = (double)v.T.bytes();
-        Prof prof_("dc3.merge_tile", total * (4 + 2 * w + 8) + 4.0 * (na + 2 * nb) - (isa ? 0 : 4.0 * total), st);
-        k_merge_tile<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa);
+        Prof prof_("dc3.merge_tile",
+                   total * (4 + 2 * w + 4) + 4.0 * (na + 2 * nb) + (isa ? 4.0 * total : 0) + (phi ? 4.0 * total : 0),
+                   st);
+        k_merge_tile<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa, phi);
     }
     SAIX_LAUNCHED();
     return SAIX_OK;
@@ -460,7 +484,7 @@ static int read_u32(const u32 *d, u32 *h, cudaStream_t st) {
 
 template <typename TT>
 static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *ISA,
-                     saix_dc3_probe *probe, int depth);
+                     saix_dc3_probe *probe, int depth, u32 *PHI = nullptr);
 
 // Steps 1-2: names of the sample triples, then SAc/ISAc (recursing if needed).
 template <typename TT>
@@ -551,7 +575,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
 
 template <typename TT>
 static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *ISA,
-                     saix_dc3_probe *probe, int depth) {
+                     saix_dc3_probe *probe, int depth, u32 *PHI) {
     Arena &ar = *c.ar;
     cudaStream_t st = c.st;
     if (depth > c.max_depth) c.max_depth = depth;
@@ -594,7 +618,7 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     i64 pad = L.pad ? 1 : 0;
     i64 na = L.m - pad;
     MergeIdx<TT> V{T, R, SAc + pad, vals};
-    SAIX_TRY(merge_run(V, na, k, split, SA, ISA, st));
+    SAIX_TRY(merge_run(V, na, k, split, SA, ISA, st, PHI));
 
     if (probe) {
         int g = grid_for(N + 3, K_THREADS);
@@ -655,6 +679,12 @@ extern "C" size_t saix_dc3_workspace_bytes(int64_t n, int text_bytes) {
 
 extern "C" int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sigma, uint32_t *sa,
                         uint32_t *isa, void *ws, size_t ws_bytes, saix_dc3_probe *probe, void *stream) {
+    return dc3_compute(text, text_bytes, n, sigma, sa, isa, nullptr, ws, ws_bytes, probe, (cudaStream_t)stream);
+}
+
+namespace saix {
+int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, u32 *phi, void *ws,
+                size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream) {
     if (n < 0 || n > (int64_t)0xFFFFFFF0LL || (text_bytes != 1 && text_bytes != 4) || sigma < 1 ||
         (n > 0 && (!text || !sa))) {
         set_error("saix_dc3: invalid arguments (n=%lld, text_bytes=%d, sigma=%lld)", (long long)n,
@@ -683,6 +713,7 @@ extern "C" int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sig
         // Dc3Workspace of a single character: pad sample 1 names (0,0,0)
         k_iota_pair<<<1, 32, 0, (cudaStream_t)stream>>>(sa, isa, 1);
         SAIX_LAUNCHED();
+        if (phi) SAIX_CUDA(cudaMemsetAsync(phi, 0xFF, 4, (cudaStream_t)stream));
         if (probe) {
             u32 h[4] = {1u, 0u, 0u, 0u};
             if (probe->triple_text)
@@ -700,12 +731,13 @@ extern "C" int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sig
         return SAIX_OK;
     }
     int rc = text_bytes == 1
-                 ? dc3_level<u8>(c, (const u8 *)text, n, (u64)sigma, sa, isa, probe, 0)
-                 : dc3_level<u32>(c, (const u32 *)text, n, (u64)sigma, sa, isa, probe, 0);
+                 ? dc3_level<u8>(c, (const u8 *)text, n, (u64)sigma, sa, isa, probe, 0, phi)
+                 : dc3_level<u32>(c, (const u32 *)text, n, (u64)sigma, sa, isa, probe, 0, phi);
     if (rc) return rc;
     if (probe) probe->depth = c.max_depth;
     return SAIX_OK;
 }
+}  // namespace saix
 
 extern "C" size_t saix_dc3_merge_workspace_bytes(int64_t total) {
     return (size_t)merge_split_words(total) * 4 + Arena::kAlign;

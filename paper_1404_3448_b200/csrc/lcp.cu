@@ -130,11 +130,11 @@ __global__ void k_lcp_permute(const u32 *__restrict__ sa, i64 n, const u32 *__re
 }
 
 static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32 *phi, u32 *seeds,
-                   cudaStream_t st, i64 boundary, u32 *best) {
+                   cudaStream_t st, i64 boundary, u32 *best, bool phi_ready) {
     i64 nchunks = ceil_div(n, LCP_CHUNK);
     int g = grid_for(n, 256);
     unsigned tiles = (unsigned)ceil_div(n, LCP_TILE);
-    {
+    if (!phi_ready) {
         Prof prof_("lcp.phi", 8.0 * n, st);
         k_phi<<<g, 256, 0, st>>>(sa, n, phi);
     }
@@ -163,12 +163,12 @@ static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32
 }
 
 int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
-                cudaStream_t st, i64 boundary, u32 *best) {
+                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in) {
     Arena ar{(char *)ws, ws_bytes};
-    u32 *phi = ar.alloc<u32>(n);
+    u32 *phi = phi_in ? phi_in : ar.alloc<u32>(n);
     u32 *seeds = ar.alloc<u32>(ceil_div(n, LCP_CHUNK) + 1);
     SAIX_ARENA_OK(ar);
-    return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, st, boundary, best);
+    return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, st, boundary, best, phi_in != nullptr);
 }
 
 }  // namespace saix

@@ -171,13 +171,28 @@ k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restri
             *(volatile u32 *)my = OS_FLAG_PRE | run;
         } else {
             *(volatile u32 *)my = OS_FLAG_AGG | run;
+            // windowed look-back: 8 predecessors per round trip, so a chain
+            // of aggregate-only tiles costs 1/8 of the serial L2 latency
+            constexpr int WIN = 8;
             i64 t = (i64)tile - 1;
             while (true) {
-                u32 s = *(volatile const u32 *)(status + t * OS_RADIX + d);
-                if ((s & ~OS_MASK) == 0) continue;  // predecessor not published yet
-                excl += s & OS_MASK;
-                if (s & OS_FLAG_PRE) break;
-                t--;
+                u32 s[WIN];
+#pragma unroll
+                for (int q = 0; q < WIN; q++)
+                    s[q] = (t - q >= 0) ? *(volatile const u32 *)(status + (t - q) * OS_RADIX + d) : OS_FLAG_PRE;
+                int q = 0;
+                bool done = false;
+#pragma unroll
+                for (; q < WIN; q++) {
+                    if ((s[q] & ~OS_MASK) == 0) break;  // not published yet: resume here
+                    excl += s[q] & OS_MASK;
+                    if (s[q] & OS_FLAG_PRE) {
+                        done = true;
+                        break;
+                    }
+                }
+                if (done) break;
+                t -= q;
             }
             *(volatile u32 *)my = OS_FLAG_PRE | (excl + run);
         }

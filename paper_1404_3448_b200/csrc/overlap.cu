@@ -372,7 +372,7 @@ extern "C" int saix_overlap_scan(const uint32_t *sa, const uint32_t *lcp, int64_
 namespace saix {
 struct PairWs {
     u8 *gsa;
-    u32 *sa, *isa, *lcp;
+    u32 *sa, *isa, *lcp, *phi;
     OverlapWs ov;
     void *rest;
     size_t rest_bytes;
@@ -383,6 +383,7 @@ static size_t pair_ws(Arena &ar, i64 n, PairWs *w) {
     t.sa = ar.alloc<u32>(n);
     t.isa = ar.alloc<u32>(n);
     t.lcp = ar.alloc<u32>(n);
+    t.phi = ar.alloc<u32>(n);
     t.ov = carve_overlap(ar, n);
     size_t need = saix_dc3_workspace_bytes(n, 1);
     size_t l = saix_lcp_workspace_bytes(n);
@@ -420,8 +421,8 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
     int sigma = (keep_n ? 5 : 4) + 1;  // max(sigma_A, sigma_B) + 1 (overlap.py:88)
     // the pipeline never needs the top-level ISA (LCP runs on Phi/SA), so
     // the merge skips that scatter
-    SAIX_TRY(saix_dc3(w.gsa, 1, n, sigma, w.sa, nullptr, w.rest, w.rest_bytes, nullptr, stream));
+    SAIX_TRY(dc3_compute(w.gsa, 1, n, sigma, w.sa, nullptr, w.phi, w.rest, w.rest_bytes, nullptr, st));
     SAIX_CUDA(cudaMemsetAsync(w.ov.best, 0, sizeof(u32), st));
-    SAIX_TRY(lcp_compute(w.gsa, 1, n, w.sa, w.lcp, w.rest, w.rest_bytes, st, na, w.ov.best));
+    SAIX_TRY(lcp_compute(w.gsa, 1, n, w.sa, w.lcp, w.rest, w.rest_bytes, st, na, w.ov.best, w.phi));
     return overlap_scan(w.sa, w.lcp, n, na, out3, w.ov, st, true);
 }
