@@ -140,10 +140,10 @@ inline int bits_for(u64 v) {  // bit width of v (>= 1), like int.bit_length()
 // LCP (lcp.cu) with the pipeline option of folding longest_overlap's pass 1
 // (max LCP over cross-sequence adjacent pairs, separator at `boundary`) into
 // the final permute kernel; boundary < 0 disables it.
-// phi_in (nullable): a precomputed Phi array (Phi[sa[r]] = sa[r-1]) that the
-// call may overwrite (it becomes PLCP); the DC3 merge can emit it.
+// phi_in (nullable): caller storage for Phi/PLCP; phi_ready says it already
+// holds Phi (Phi[sa[r]] = sa[r-1], e.g. emitted by the DC3 merge).
 int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
-                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in = nullptr);
+                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in = nullptr, bool phi_ready = false);
 
 // DC3 (dc3.cu); phi (nullable) receives Phi of the top-level suffix array.
 int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, u32 *phi, void *ws,

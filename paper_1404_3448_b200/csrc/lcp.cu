@@ -163,12 +163,12 @@ static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32
 }
 
 int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
-                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in) {
+                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in, bool phi_ready) {
     Arena ar{(char *)ws, ws_bytes};
     u32 *phi = phi_in ? phi_in : ar.alloc<u32>(n);
     u32 *seeds = ar.alloc<u32>(ceil_div(n, LCP_CHUNK) + 1);
     SAIX_ARENA_OK(ar);
-    return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, st, boundary, best, phi_in != nullptr);
+    return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, st, boundary, best, phi_ready);
 }
 
 }  // namespace saix
