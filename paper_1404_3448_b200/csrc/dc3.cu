@@ -390,9 +390,14 @@ k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict
         int i = lo, j = dt - lo;
 #pragma unroll
         for (int r = 0; r < MT_ITEMS; r++) {
-            if (dt + r >= cnt) break;
+            bool live = dt + r < cnt;
             bool takeA = j >= nbt || (i < nat && rec_a_first(A[i], B[j]));
-            res[r] = takeA ? A[i++].pos : B[j++].pos;
+            u32 pa = i < nat ? A[i].pos : 0u, pb = j < nbt ? B[j].pos : 0u;
+            res[r] = takeA ? pa : pb;
+            if (live) {
+                if (takeA) i++;
+                else j++;
+            }
         }
     }
     __syncthreads();

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(OS_RADIX) k_os_scan(const u32 *__restrict__ hi
 }
 
 template <typename K, class Src>
-__global__ void __launch_bounds__(OS_THREADS)
+__global__ void __launch_bounds__(OS_THREADS, 2)
 k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restrict__ status, u32 *__restrict__ ticket,
           K *__restrict__ keys_out, u32 *__restrict__ vals_out) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -140,12 +140,17 @@ k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restri
     K k[OS_ITEMS];
     u32 v[OS_ITEMS], rank[OS_ITEMS], dig[OS_ITEMS];
     u32 lt = lanemask_lt();
+    // all loads first (16 in flight per thread), then the ranking rounds
 #pragma unroll
     for (int r = 0; r < OS_ITEMS; r++) {
         i64 i = seg + r * 32 + lane;
         bool ok = i < n && src.get(i, k[r], v[r]);
-        u32 d = ok ? ((u32)(k[r] >> shift) & (OS_RADIX - 1)) : (u32)OS_RADIX;
-        dig[r] = d;
+        dig[r] = ok ? ((u32)(k[r] >> shift) & (OS_RADIX - 1)) : (u32)OS_RADIX;
+    }
+#pragma unroll
+    for (int r = 0; r < OS_ITEMS; r++) {
+        u32 d = dig[r];
+        bool ok = d < OS_RADIX;
         u32 peers = digit_peers(d);
         u32 before = __popc(peers & lt);
         u32 cur = ok ? cnt[w][d] : 0u;
@@ -171,9 +176,9 @@ k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restri
             *(volatile u32 *)my = OS_FLAG_PRE | run;
         } else {
             *(volatile u32 *)my = OS_FLAG_AGG | run;
-            // windowed look-back: 8 predecessors per round trip, so a chain
-            // of aggregate-only tiles costs 1/8 of the serial L2 latency
-            constexpr int WIN = 8;
+            // windowed look-back: 32 predecessors per round trip, so a chain
+            // of aggregate-only tiles costs 1/32 of the serial L2 latency
+            constexpr int WIN = 32;
             i64 t = (i64)tile - 1;
             while (true) {
                 u32 s[WIN];
