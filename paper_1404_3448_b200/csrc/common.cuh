@@ -141,12 +141,12 @@ inline int bits_for(u64 v) {  // bit width of v (>= 1), like int.bit_length()
 // (max LCP over cross-sequence adjacent pairs, separator at `boundary`) into
 // the final permute kernel; boundary < 0 disables it.
 // phi_in (nullable): caller storage for Phi/PLCP; phi_ready says it already
-// holds Phi (Phi[sa[r]] = sa[r-1], e.g. emitted by the DC3 merge).
+// holds Phi (Phi[sa[r]] = sa[r-1]).
 int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
                 cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in = nullptr, bool phi_ready = false);
 
-// DC3 (dc3.cu); phi (nullable) receives Phi of the top-level suffix array.
-int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, u32 *phi, void *ws,
+// DC3 (dc3.cu); isa may be null when the caller does not need the ranks.
+int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, void *ws,
                 size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream);
 
 // DC3 sample layout (suffix_index.py:149-153): mod-1 positions 1,4,... and

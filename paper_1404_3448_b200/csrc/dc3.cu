@@ -269,17 +269,101 @@ __device__ __forceinline__ bool rec_a_first(const MRec &a, const MRec &b) {
     return a.r2 < b.r2;
 }
 
+// Per-triplet comparison block E[j] (j in [0, k)) built by one streaming
+// pass over the text and the child's ISA: the four characters T(3j..3j+3)
+// and the sample ranks R(3j+1), R(3j+2), R(3j+4).  Every suffix p the merge
+// compares (non-sample 3j, mod-1 3j+1, mod-2 3j+2) finds its whole DC3
+// comparison record in E[p / 3], so the merge does one 16 B (u8 text) or
+// 32 B (wider text) gather per element instead of 2-3 dependent ones.
+struct EBlock8 {  // u8 text
+    u32 chars, r1, r2, r4;
+};
+struct EBlock32 {  // u32 text
+    u32 c0, c1, c2, c3, r1, r2, r4, pad;
+};
+template <typename TT>
+struct EBlockOf {
+    using type = EBlock32;
+};
+template <>
+struct EBlockOf<u8> {
+    using type = EBlock8;
+};
+
+template <typename TT>
+__global__ void k_build_eblocks(Text<TT> T, RankFromIsa R, i64 k, typename EBlockOf<TT>::type *__restrict__ E) {
+    for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (i64)gridDim.x * blockDim.x) {
+        i64 p = 3 * j;
+        u32 r1 = R(p + 1), r2 = R(p + 2), r4 = R(p + 4);
+        if constexpr (sizeof(TT) == 1) {
+            u32 ch = T(p) | (T(p + 1) << 8) | (T(p + 2) << 16) | (T(p + 3) << 24);
+            __stcs(reinterpret_cast<uint4 *>(E + j), make_uint4(ch, r1, r2, r4));
+        } else {
+            uint4 *dst = reinterpret_cast<uint4 *>(E + j);
+            __stcs(dst, make_uint4(T(p), T(p + 1), T(p + 2), T(p + 3)));
+            __stcs(dst + 1, make_uint4(r1, r2, r4, 0u));
+        }
+    }
+}
+
+template <typename TT>
+__device__ __forceinline__ MRec rec_from_eblock(const typename EBlockOf<TT>::type *__restrict__ E, i64 p) {
+    i64 j = p / 3;
+    int r = (int)(p - 3 * j);
+    u32 c[4], r1, r2, r4;
+    if constexpr (sizeof(TT) == 1) {
+        uint4 e = __ldg(reinterpret_cast<const uint4 *>(E + j));
+        c[0] = e.x & 0xFF;
+        c[1] = (e.x >> 8) & 0xFF;
+        c[2] = (e.x >> 16) & 0xFF;
+        c[3] = e.x >> 24;
+        r1 = e.y;
+        r2 = e.z;
+        r4 = e.w;
+    } else {
+        uint4 a = __ldg(reinterpret_cast<const uint4 *>(E + j));
+        uint4 b = __ldg(reinterpret_cast<const uint4 *>(E + j) + 1);
+        c[0] = a.x;
+        c[1] = a.y;
+        c[2] = a.z;
+        c[3] = a.w;
+        r1 = b.x;
+        r2 = b.y;
+        r4 = b.z;
+    }
+    MRec m;
+    m.pos = (u32)p;
+    if (r == 0) {  // non-sample 3j: (c0, c1, R(3j+1), R(3j+2))
+        m.c0 = c[0];
+        m.c1 = c[1];
+        m.r1 = r1;
+        m.r2 = r2;
+    } else if (r == 1) {  // mod-1 sample: (c0, R(p+1))
+        m.c0 = c[1];
+        m.c1 = 0;
+        m.r1 = r2;
+        m.r2 = 0;
+    } else {  // mod-2 sample: (c0, c1, R(p+2))
+        m.c0 = c[2];
+        m.c1 = c[3];
+        m.r1 = 0;
+        m.r2 = r4;
+    }
+    return m;
+}
+
 // Merge inputs: sorted samples as sample indices / sorted mod-0 as indices.
 template <typename TT>
 struct MergeIdx {
     Text<TT> T;
     RankFromIsa R;
     const u32 *A, *B;
+    const typename EBlockOf<TT>::type *E;
     __device__ __forceinline__ i64 apos(i64 i) const { return R.L.pos(A[i]); }
     __device__ __forceinline__ i64 bpos(i64 j) const { return 3 * (i64)B[j]; }
     __device__ __forceinline__ i64 apos_cs(i64 i) const { return R.L.pos(__ldcs(A + i)); }
     __device__ __forceinline__ i64 bpos_cs(i64 j) const { return 3 * (i64)__ldcs(B + j); }
-    __device__ __forceinline__ MRec rec(i64 p) const { return make_rec(T, R, p); }
+    __device__ __forceinline__ MRec rec(i64 p) const { return rec_from_eblock<TT>(E, p); }
 };
 // Merge inputs given as positions with a by-position rank array
 // (merge_sample_nonsample, suffix_index.py:452-457).
@@ -342,11 +426,9 @@ __global__ void k_merge_partition(V v, i64 na, i64 nb, i64 ntiles, u32 *__restri
 
 template <class V>
 __global__ void __launch_bounds__(MT_THREADS)
-k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, u32 *__restrict__ isa,
-             u32 *__restrict__ phi) {
+k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, u32 *__restrict__ isa) {
     __shared__ MRec sh[MT_TILE];
-    __shared__ u32 prev_tile_last;
-    u32 *out = reinterpret_cast<u32 *>(sh);  // reused for the output tile after the merge
+    __shared__ u32 out[MT_TILE];
     i64 total = na + nb;
     i64 d0 = (i64)blockIdx.x * MT_TILE;
     i64 d1 = d0 + MT_TILE < total ? d0 + MT_TILE : total;
@@ -363,23 +445,9 @@ k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict
         int x = threadIdx.x + q * MT_THREADS;
         if (x < cnt) sh[x] = v.rec(sh[x].pos);
     }
-    if (phi && threadIdx.x == 0) {
-        // SA[d0-1] is the later of the previous tile's last sample / non-sample
-        u32 last = 0xFFFFFFFFu;
-        if (i0 > 0 && j0 > 0) {
-            MRec a = v.rec(v.apos(i0 - 1)), b = v.rec(v.bpos(j0 - 1));
-            last = rec_a_first(a, b) ? b.pos : a.pos;
-        } else if (i0 > 0) {
-            last = (u32)v.apos(i0 - 1);
-        } else if (j0 > 0) {
-            last = (u32)v.bpos(j0 - 1);
-        }
-        prev_tile_last = last;
-    }
     __syncthreads();
     const MRec *A = sh, *B = sh + nat;
     int dt = threadIdx.x * MT_ITEMS;
-    u32 res[MT_ITEMS];
     if (dt < cnt) {
         int lo = dt > nbt ? dt - nbt : 0, hi = dt < nat ? dt : nat;
         while (lo < hi) {
@@ -390,32 +458,21 @@ k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict
         int i = lo, j = dt - lo;
 #pragma unroll
         for (int r = 0; r < MT_ITEMS; r++) {
-            bool live = dt + r < cnt;
+            if (dt + r >= cnt) break;
             bool takeA = j >= nbt || (i < nat && rec_a_first(A[i], B[j]));
-            u32 pa = i < nat ? A[i].pos : 0u, pb = j < nbt ? B[j].pos : 0u;
-            res[r] = takeA ? pa : pb;
-            if (live) {
-                if (takeA) i++;
-                else j++;
-            }
+            out[dt + r] = takeA ? A[i++].pos : B[j++].pos;
         }
     }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < MT_ITEMS; r++)
-        if (dt + r < cnt) out[dt + r] = res[r];
     __syncthreads();
     for (int x = threadIdx.x; x < cnt; x += MT_THREADS) {
         u32 p = out[x];
         __stcs(sa + d0 + x, p);
         if (isa) isa[p] = (u32)(d0 + x);
-        // Phi[sa[d]] = sa[d-1] for the LCP stage (lcp.cu), fused here
-        if (phi) phi[p] = x ? out[x - 1] : prev_tile_last;
     }
 }
 
 template <class V>
-static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStream_t st, u32 *phi = nullptr) {
+static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStream_t st) {
     i64 total = na + nb;
     if (total == 0) return SAIX_OK;
     i64 ntiles = ceil_div(total, MT_TILE);
@@ -427,10 +484,8 @@ static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStr
     {
         // indices 4 + chars 2w + ranks (4 per sample, 8 per non-sample) + SA 4 + ISA 4
         double w = (double)v.T.bytes();
-        Prof prof_("dc3.merge_tile",
-                   total * (4 + 2 * w + 4) + 4.0 * (na + 2 * nb) + (isa ? 4.0 * total : 0) + (phi ? 4.0 * total : 0),
-                   st);
-        k_merge_tile<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa, phi);
+        Prof prof_("dc3.merge_tile", total * (4 + 2 * w + 4) + 4.0 * (na + 2 * nb) + (isa ? 4.0 * total : 0), st);
+        k_merge_tile<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa);
     }
     SAIX_LAUNCHED();
     return SAIX_OK;
@@ -489,7 +544,7 @@ static int read_u32(const u32 *d, u32 *h, cudaStream_t st) {
 
 template <typename TT>
 static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *ISA,
-                     saix_dc3_probe *probe, int depth, u32 *PHI = nullptr);
+                     saix_dc3_probe *probe, int depth);
 
 // Steps 1-2: names of the sample triples, then SAc/ISAc (recursing if needed).
 template <typename TT>
@@ -580,7 +635,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
 
 template <typename TT>
 static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *ISA,
-                     saix_dc3_probe *probe, int depth, u32 *PHI) {
+                     saix_dc3_probe *probe, int depth) {
     Arena &ar = *c.ar;
     cudaStream_t st = c.st;
     if (depth > c.max_depth) c.max_depth = depth;
@@ -622,8 +677,16 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     RankFromIsa R{L, ISAc};
     i64 pad = L.pad ? 1 : 0;
     i64 na = L.m - pad;
-    MergeIdx<TT> V{T, R, SAc + pad, vals};
-    SAIX_TRY(merge_run(V, na, k, split, SA, ISA, st, PHI));
+    using EB = typename EBlockOf<TT>::type;
+    EB *E = ar.alloc<EB>(k);
+    SAIX_ARENA_OK(ar);
+    {
+        Prof prof_("dc3.eblocks", (double)sizeof(TT) * N + 8.0 * L.m + (double)sizeof(EB) * k, st);
+        k_build_eblocks<TT><<<grid_for(k, K_THREADS), K_THREADS, 0, st>>>(T, R, k, E);
+    }
+    SAIX_LAUNCHED();
+    MergeIdx<TT> V{T, R, SAc + pad, vals, E};
+    SAIX_TRY(merge_run(V, na, k, split, SA, ISA, st));
 
     if (probe) {
         int g = grid_for(N + 3, K_THREADS);
@@ -663,7 +726,7 @@ static size_t dc3_plan(i64 n) {
         size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
-        size_t post_t = (size_t)k * 16 + (size_t)(os_scratch_words(m) + merge_split_words(N)) * 4;
+        size_t post_t = (size_t)k * 16 + (size_t)k * 32 + (size_t)(os_scratch_words(m) + merge_split_words(N)) * 4;
         size_t t = sort_t > bm_t ? sort_t : bm_t;
         t = t > post_t ? t : post_t;
         t += 8 * Arena::kAlign;
@@ -684,11 +747,11 @@ extern "C" size_t saix_dc3_workspace_bytes(int64_t n, int text_bytes) {
 
 extern "C" int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sigma, uint32_t *sa,
                         uint32_t *isa, void *ws, size_t ws_bytes, saix_dc3_probe *probe, void *stream) {
-    return dc3_compute(text, text_bytes, n, sigma, sa, isa, nullptr, ws, ws_bytes, probe, (cudaStream_t)stream);
+    return dc3_compute(text, text_bytes, n, sigma, sa, isa, ws, ws_bytes, probe, (cudaStream_t)stream);
 }
 
 namespace saix {
-int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, u32 *phi, void *ws,
+int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, void *ws,
                 size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream) {
     if (n < 0 || n > (int64_t)0xFFFFFFF0LL || (text_bytes != 1 && text_bytes != 4) || sigma < 1 ||
         (n > 0 && (!text || !sa))) {
@@ -718,7 +781,6 @@ int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32
         // Dc3Workspace of a single character: pad sample 1 names (0,0,0)
         k_iota_pair<<<1, 32, 0, (cudaStream_t)stream>>>(sa, isa, 1);
         SAIX_LAUNCHED();
-        if (phi) SAIX_CUDA(cudaMemsetAsync(phi, 0xFF, 4, (cudaStream_t)stream));
         if (probe) {
             u32 h[4] = {1u, 0u, 0u, 0u};
             if (probe->triple_text)
@@ -736,8 +798,8 @@ int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32
         return SAIX_OK;
     }
     int rc = text_bytes == 1
-                 ? dc3_level<u8>(c, (const u8 *)text, n, (u64)sigma, sa, isa, probe, 0, phi)
-                 : dc3_level<u32>(c, (const u32 *)text, n, (u64)sigma, sa, isa, probe, 0, phi);
+                 ? dc3_level<u8>(c, (const u8 *)text, n, (u64)sigma, sa, isa, probe, 0)
+                 : dc3_level<u32>(c, (const u32 *)text, n, (u64)sigma, sa, isa, probe, 0);
     if (rc) return rc;
     if (probe) probe->depth = c.max_depth;
     return SAIX_OK;

@@ -422,9 +422,9 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
     // the pipeline never needs the top-level ISA (LCP runs on Phi/SA), so
     // the merge skips that scatter
     // Phi is built by its own scatter kernel (lcp.cu): emitting it from the
-    // level-0 merge (dc3_compute's phi argument) measured slower on B200 --
-    // the 4 B scatter evicts the merge's L2-resident text/rank gathers.
-    SAIX_TRY(dc3_compute(w.gsa, 1, n, sigma, w.sa, nullptr, nullptr, w.rest, w.rest_bytes, nullptr, st));
+    // level-0 merge measured slower on B200 -- the 4 B scatter evicts the
+    // merge's L2-resident text/rank gathers.
+    SAIX_TRY(dc3_compute(w.gsa, 1, n, sigma, w.sa, nullptr, w.rest, w.rest_bytes, nullptr, st));
     SAIX_CUDA(cudaMemsetAsync(w.ov.best, 0, sizeof(u32), st));
     SAIX_TRY(lcp_compute(w.gsa, 1, n, w.sa, w.lcp, w.rest, w.rest_bytes, st, na, w.ov.best, w.phi));
     return overlap_scan(w.sa, w.lcp, n, na, out3, w.ov, st, true);
