@@ -164,6 +164,15 @@ struct FlagGather {
         return (T(p) != T(q) || T(p + 1) != T(q + 1) || T(p + 2) != T(q + 2)) ? 1u : 0u;
     }
 };
+// number of distinct keys in a sorted array (heads of equal-key runs)
+__global__ void k_count_distinct(const u64 *__restrict__ keys, i64 m, u32 *__restrict__ count) {
+    u32 c = 0;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (i64)gridDim.x * blockDim.x)
+        c += (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane_id() == 0 && c) atomicAdd(count, c);
+}
+
 struct ScatterName {
     const u32 *vals;
     u32 *tt;
@@ -602,8 +611,19 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             TripleSrc<TT> src{T, L, s1};
             SAIX_TRY(onesweep_sort<u64>(src, m, src, m, m, 0, passes, k0, v0, k1, v1, scratch, keys, vals, nullptr,
                                         st, "dc3.triple_sort"));
-            SAIX_TRY(scan_transform(FlagPacked{keys}, ScatterName{vals, tt}, m, tmp, d_scal, st, "dc3.name_scan",
-                                    16.0 * m));
+            // count distinct triples first: when all are distinct (the last
+            // recursion level) the sorted order already is the rank order and
+            // the recursion string is never needed
+            SAIX_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(u32), st));
+            {
+                Prof prof_("dc3.count_names", 8.0 * m, st);
+                k_count_distinct<<<grid_for(m, K_THREADS, kNumSMs * 8), K_THREADS, 0, st>>>(keys, m, d_scal);
+            }
+            SAIX_LAUNCHED();
+            SAIX_TRY(read_u32(d_scal, &D, st));
+            if ((i64)D < m || keep_u32)
+                SAIX_TRY(scan_transform(FlagPacked{keys}, ScatterName{vals, tt}, m, tmp, nullptr, st,
+                                        "dc3.name_scan", 16.0 * m));
         } else {
             k_third_char_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, k0, v0);
             SAIX_LAUNCHED();
@@ -615,9 +635,9 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             SAIX_TRY(radix_sort_pairs<u64>(keys, vals, keys == k0 ? k1 : k0, vals == v0 ? v1 : v0, m, 0,
                                            2 * b, scratch, st));
             SAIX_TRY(scan_transform(FlagGather<TT>{T, L, vals}, ScatterName{vals, tt}, m, tmp, d_scal, st));
+            SAIX_TRY(read_u32(d_scal, &D, st));
         }
         sorted_vals = vals;
-        SAIX_TRY(read_u32(d_scal, &D, st));
     }
     if ((i64)D == m) {
         Prof prof_("dc3.unique_ranks", 12.0 * m, st);

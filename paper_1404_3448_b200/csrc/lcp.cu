@@ -56,7 +56,7 @@ constexpr u32 kNone = 0xFFFFFFFFu;
 // Phi[sa[r]] = sa[r-1]: the text-order predecessor map (one scatter).
 __global__ void k_phi(const u32 *__restrict__ sa, i64 n, u32 *__restrict__ phi) {
     for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x)
-        phi[sa[r]] = r ? sa[r - 1] : kNone;
+        phi[__ldcs(sa + r)] = r ? sa[r - 1] : kNone;
 }
 
 // Exact PLCP at every chunk start (seed of the in-chunk walk).
@@ -114,7 +114,7 @@ __global__ void k_lcp_permute(const u32 *__restrict__ sa, i64 n, const u32 *__re
                               u32 *__restrict__ lcp, u32 boundary, u32 *best) {
     u32 mx = 0;
     for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x) {
-        u32 p = sa[r];
+        u32 p = __ldcs(sa + r);
         u32 l = plcp[p];
         __stcs(lcp + r, l);
         if (best && r > 0) {

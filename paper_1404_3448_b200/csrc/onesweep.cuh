@@ -19,6 +19,8 @@
 // the valid items only, in stable order.
 #pragma once
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace saix {
@@ -27,7 +29,8 @@ constexpr int OS_BITS = 8;
 constexpr int OS_RADIX = 1 << OS_BITS;
 constexpr int OS_THREADS = 256;
 constexpr int OS_WARPS = OS_THREADS / 32;
-constexpr int OS_ITEMS = 16;
+constexpr int OS_ITEMS = 16;                    // default items per thread
+constexpr int OS_MIN_ITEMS = 8;                 // smallest variant (scratch sizing)
 constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096
 constexpr int OS_MAX_PASSES = 8;
 constexpr u32 OS_FLAG_AGG = 1u << 30, OS_FLAG_PRE = 2u << 30, OS_MASK = (1u << 30) - 1;
@@ -58,7 +61,7 @@ struct ArraySrc {
     }
 };
 
-inline i64 os_tiles(i64 n) { return ceil_div(n > 0 ? n : 1, OS_TILE); }
+inline i64 os_tiles(i64 n, int items = OS_MIN_ITEMS) { return ceil_div(n > 0 ? n : 1, (i64)OS_THREADS * items); }
 
 // Scratch: hist [passes][256] + offsets + status [tiles][256] + ticket.
 inline i64 os_scratch_words(i64 n) { return 2 * OS_MAX_PASSES * OS_RADIX + 64 + os_tiles(n) * OS_RADIX + 64; }
@@ -119,14 +122,15 @@ __global__ void __launch_bounds__(OS_RADIX) k_os_scan(const u32 *__restrict__ hi
     }
 }
 
-template <typename K, class Src>
+template <typename K, class Src, int ITEMS>
 __global__ void __launch_bounds__(OS_THREADS, 2)
 k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restrict__ status, u32 *__restrict__ ticket,
           K *__restrict__ keys_out, u32 *__restrict__ vals_out) {
+    constexpr int TILE = OS_THREADS * ITEMS;
     extern __shared__ __align__(16) unsigned char smem[];
     K *sk = reinterpret_cast<K *>(smem);
-    u32 *sv = reinterpret_cast<u32 *>(sk + OS_TILE);
-    u32(*cnt)[OS_RADIX] = reinterpret_cast<u32(*)[OS_RADIX]>(sv + OS_TILE);
+    u32 *sv = reinterpret_cast<u32 *>(sk + TILE);
+    u32(*cnt)[OS_RADIX] = reinterpret_cast<u32(*)[OS_RADIX]>(sv + TILE);
     u32 *tile_excl = &cnt[OS_WARPS][0];
     u32 *gbase = tile_excl + OS_RADIX;
     __shared__ u32 sh_tile, sh_warp[OS_WARPS + 1];
@@ -136,19 +140,19 @@ k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restri
     for (int d = lane; d < OS_RADIX; d += 32) cnt[w][d] = 0;
     __syncthreads();
     const u32 tile = sh_tile;
-    i64 seg = (i64)tile * OS_TILE + (i64)w * (32 * OS_ITEMS);
-    K k[OS_ITEMS];
-    u32 v[OS_ITEMS], rank[OS_ITEMS], dig[OS_ITEMS];
+    i64 seg = (i64)tile * TILE + (i64)w * (32 * ITEMS);
+    K k[ITEMS];
+    u32 v[ITEMS], rank[ITEMS], dig[ITEMS];
     u32 lt = lanemask_lt();
     // all loads first (16 in flight per thread), then the ranking rounds
 #pragma unroll
-    for (int r = 0; r < OS_ITEMS; r++) {
+    for (int r = 0; r < ITEMS; r++) {
         i64 i = seg + r * 32 + lane;
         bool ok = i < n && src.get(i, k[r], v[r]);
         dig[r] = ok ? ((u32)(k[r] >> shift) & (OS_RADIX - 1)) : (u32)OS_RADIX;
     }
 #pragma unroll
-    for (int r = 0; r < OS_ITEMS; r++) {
+    for (int r = 0; r < ITEMS; r++) {
         u32 d = dig[r];
         bool ok = d < OS_RADIX;
         u32 peers = digit_peers(d);
@@ -226,7 +230,7 @@ k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restri
     __syncthreads();
     const u32 valid = sh_warp[OS_WARPS];
 #pragma unroll
-    for (int r = 0; r < OS_ITEMS; r++) {
+    for (int r = 0; r < ITEMS; r++) {
         u32 d = dig[r];
         if (d < OS_RADIX) {
             u32 lp = tile_excl[d] + cnt[w][d] + rank[r];
@@ -244,9 +248,45 @@ k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restri
     }
 }
 
-template <typename K>
+template <typename K, int ITEMS>
 constexpr size_t os_pass_smem() {
-    return (size_t)OS_TILE * (sizeof(K) + 4) + (size_t)(OS_WARPS + 2) * OS_RADIX * 4;
+    return (size_t)OS_THREADS * ITEMS * (sizeof(K) + 4) + (size_t)(OS_WARPS + 2) * OS_RADIX * 4;
+}
+
+inline int os_items_choice() {
+    static int v = [] {
+        const char *e = getenv("SAIX_OS_ITEMS");
+        int x = e ? atoi(e) : OS_ITEMS;
+        return (x == 8 || x == 12 || x == 16) ? x : OS_ITEMS;
+    }();
+    return v;
+}
+
+template <typename K, class Src, int ITEMS>
+static int os_launch_pass(Src src, i64 np, int shift, const u32 *offs, u32 *status, u32 *ticket, K *dk, u32 *dv,
+                          cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        SAIX_CUDA(cudaFuncSetAttribute(k_os_pass<K, Src, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)os_pass_smem<K, ITEMS>()));
+        attr = true;
+    }
+    i64 ntiles = os_tiles(np, ITEMS);
+    SAIX_CUDA(cudaMemsetAsync(status, 0, (size_t)ntiles * OS_RADIX * 4, st));
+    k_os_pass<K, Src, ITEMS><<<(unsigned)ntiles, OS_THREADS, os_pass_smem<K, ITEMS>(), st>>>(src, np, shift, offs,
+                                                                                             status, ticket, dk, dv);
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}
+
+template <typename K, class Src>
+static int os_pass_any(Src src, i64 np, int shift, const u32 *offs, u32 *status, u32 *ticket, K *dk, u32 *dv,
+                       cudaStream_t st) {
+    switch (os_items_choice()) {
+        case 8: return os_launch_pass<K, Src, 8>(src, np, shift, offs, status, ticket, dk, dv, st);
+        case 12: return os_launch_pass<K, Src, 12>(src, np, shift, offs, status, ticket, dk, dv, st);
+        default: return os_launch_pass<K, Src, 16>(src, np, shift, offs, status, ticket, dk, dv, st);
+    }
 }
 
 // Sort `n` source items on bits [shift0, shift0 + 8*passes).  Pass 0 reads
@@ -265,14 +305,6 @@ int onesweep_sort(Src src, i64 n, HSrc hsrc, i64 n_h, i64 n_out, int shift0, int
         set_error("onesweep_sort: unsupported passes=%d n=%lld", passes, (long long)n);
         return SAIX_EINVAL;
     }
-    static bool attr_set = false;
-    if (!attr_set) {
-        SAIX_CUDA(cudaFuncSetAttribute(k_os_pass<K, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)os_pass_smem<K>()));
-        SAIX_CUDA(cudaFuncSetAttribute(k_os_pass<K, ArraySrc<K>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)os_pass_smem<K>()));
-        attr_set = true;
-    }
     u32 *hist = scratch;
     u32 *offs = hist + OS_MAX_PASSES * OS_RADIX;
     u32 *ticket = offs + OS_MAX_PASSES * OS_RADIX;  // 32 words, one per pass
@@ -289,19 +321,14 @@ int onesweep_sort(Src src, i64 n, HSrc hsrc, i64 n_h, i64 n_out, int shift0, int
     u32 *ov = v0;
     for (int p = 0; p < passes; p++) {
         i64 np = p == 0 ? n : n_out;
-        i64 ntiles = os_tiles(np);
-        SAIX_CUDA(cudaMemsetAsync(status, 0, (size_t)ntiles * OS_RADIX * 4, st));
         K *dk = (p % 2 == 0) ? k0 : k1;
         u32 *dv = (p % 2 == 0) ? v0 : v1;
         if (p == 0) {
-            k_os_pass<K, Src><<<(unsigned)ntiles, OS_THREADS, os_pass_smem<K>(), st>>>(
-                src, n, shift0, offs, status, ticket, dk, dv);
+            SAIX_TRY((os_pass_any<K, Src>(src, n, shift0, offs, status, ticket, dk, dv, st)));
         } else {
-            ArraySrc<K> as{ok, ov};
-            k_os_pass<K, ArraySrc<K>><<<(unsigned)ntiles, OS_THREADS, os_pass_smem<K>(), st>>>(
-                as, np, shift0 + OS_BITS * p, offs + OS_RADIX * p, status, ticket + p, dk, dv);
+            SAIX_TRY((os_pass_any<K, ArraySrc<K>>(ArraySrc<K>{ok, ov}, np, shift0 + OS_BITS * p, offs + OS_RADIX * p,
+                                                  status, ticket + p, dk, dv, st)));
         }
-        SAIX_LAUNCHED();
         ok = dk;
         ov = dv;
     }
