@@ -138,6 +138,33 @@ struct Mod0Src {
         return true;
     }
 };
+// Small-alphabet mod-0 split without a sort.  Mod-0 suffix 3j sorts by
+// (T(3j), R(3j+1)); bit isac[j] of the per-character bitmap B[T(3j)] marks
+// it in sample-rank order.  One flattened popcount scan over the bitmaps
+// (character-major) gives every suffix its output slot:
+//   slot(j) = prefix[c][r >> 5] + popc(B[c][r >> 5] & below(r)),  r = isac[j].
+template <typename TT>
+__global__ void k_mod0_bits(Text<TT> T, const u32 *__restrict__ isac, i64 k, i64 words_per_char,
+                            u32 *__restrict__ bits) {
+    for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (i64)gridDim.x * blockDim.x) {
+        u32 r = __ldcs(isac + j);
+        u32 c = T(3 * j);
+        atomicOr(&bits[(i64)c * words_per_char + (r >> 5)], 1u << (r & 31));
+    }
+}
+template <typename TT>
+__global__ void k_mod0_place(Text<TT> T, const u32 *__restrict__ isac, i64 k, i64 words_per_char,
+                             const u32 *__restrict__ bits, const u32 *__restrict__ prefix, u32 *__restrict__ out) {
+    for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (i64)gridDim.x * blockDim.x) {
+        u32 r = __ldcs(isac + j);
+        u32 c = T(3 * j);
+        i64 w = (i64)c * words_per_char + (r >> 5);
+        out[prefix[w] + __popc(bits[w] & ((1u << (r & 31)) - 1u))] = (u32)j;
+    }
+}
+static bool mod0_use_bitmaps(u64 sigma) { return sigma + 1 <= 128; }
+inline i64 mod0_bitmap_words(u64 sigma, i64 m) { return (i64)(sigma + 1) * (ceil_div(m, 32) + 1); }
+
 // the same multiset of mod-0 first characters, streamed in text order
 template <typename TT>
 struct Mod0HistSrc {
@@ -687,7 +714,22 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     u32 *split = ar.alloc<u32>(merge_split_words(N));
     SAIX_ARENA_OK(ar);
     u32 *keys = k0, *vals = v0;
-    {
+    if (mod0_use_bitmaps(sigma)) {
+        i64 wpc = ceil_div(L.m, 32) + 1;
+        i64 nw = mod0_bitmap_words(sigma, L.m);
+        u32 *bits = ar.alloc<u32>(nw);
+        u32 *prefix = ar.alloc<u32>(nw);
+        u32 *tmp = ar.alloc<u32>(scan_tmp_words(nw));
+        SAIX_ARENA_OK(ar);
+        Prof prof_("dc3.mod0_split", (8.0 + 2 * sizeof(TT)) * k + 4.0 * k + 8.0 * nw, st);
+        SAIX_CUDA(cudaMemsetAsync(bits, 0, (size_t)nw * 4, st));
+        int g = grid_for(k, K_THREADS);
+        k_mod0_bits<TT><<<g, K_THREADS, 0, st>>>(T, ISAc, k, wpc, bits);
+        SAIX_LAUNCHED();
+        SAIX_TRY(scan_transform(PopcIn{bits}, StoreExcl{prefix}, nw, tmp, nullptr, st, "dc3.mod0_scan", 8.0 * nw));
+        k_mod0_place<TT><<<g, K_THREADS, 0, st>>>(T, ISAc, k, wpc, bits, prefix, v0);
+        SAIX_LAUNCHED();
+    } else {
         int passes = (bits_for(sigma) + OS_BITS - 1) / OS_BITS;
         SAIX_TRY(onesweep_sort<u32>(Mod0Src<TT>{T, SAc, (u32)L.m1}, L.m, Mod0HistSrc<TT>{T}, k, k, 0, passes, k0,
                                     v0, k1, v1, scratch, keys, vals, nullptr, st, "dc3.mod0_split"));
@@ -746,7 +788,9 @@ static size_t dc3_plan(i64 n) {
         size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
-        size_t post_t = (size_t)k * 16 + (size_t)k * 32 + (size_t)(os_scratch_words(m) + merge_split_words(N)) * 4;
+        i64 bw = mod0_bitmap_words(127, m);
+        size_t post_t = (size_t)k * 16 + (size_t)k * 32 +
+                        (size_t)(os_scratch_words(m) + merge_split_words(N) + 2 * bw + scan_tmp_words(bw)) * 4;
         size_t t = sort_t > bm_t ? sort_t : bm_t;
         t = t > post_t ? t : post_t;
         t += 8 * Arena::kAlign;
