@@ -149,6 +149,35 @@ int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp
 int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, void *ws,
                 size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream);
 
+// L2 eviction-priority hints (sm_80+ createpolicy / L2::cache_hint): random
+// gather targets that should stay on chip are loaded / stored evict_last,
+// while streaming arrays use the .cs (evict-first) variants.
+__device__ __forceinline__ u64 l2_evict_last() {
+    u64 p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 ldg_last(const uint4 *a, u64 pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ u32 ldg_last(const u32 *a, u64 pol) {
+    u32 r;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ u32 ld_last(const u32 *a, u64 pol) {  // coherent (buffer written earlier)
+    u32 r;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void st_last(u32 *a, u32 v, u64 pol) {
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+}
+
 // DC3 sample layout (suffix_index.py:149-153): mod-1 positions 1,4,... and
 // mod-2 positions 2,5,... below limit = n+1 if n%3==1 else n.
 struct SampleLayout {

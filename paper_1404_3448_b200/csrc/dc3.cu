@@ -143,25 +143,35 @@ struct Mod0Src {
 // it in sample-rank order.  One flattened popcount scan over the bitmaps
 // (character-major) gives every suffix its output slot:
 //   slot(j) = prefix[c][r >> 5] + popc(B[c][r >> 5] & below(r)),  r = isac[j].
+// bitmap word and its exclusive popcount prefix interleaved: one 8 B gather
+// per mod-0 suffix in the placement pass
 template <typename TT>
 __global__ void k_mod0_bits(Text<TT> T, const u32 *__restrict__ isac, i64 k, i64 words_per_char,
-                            u32 *__restrict__ bits) {
+                            uint2 *__restrict__ pb) {
     for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (i64)gridDim.x * blockDim.x) {
         u32 r = __ldcs(isac + j);
         u32 c = T(3 * j);
-        atomicOr(&bits[(i64)c * words_per_char + (r >> 5)], 1u << (r & 31));
+        atomicOr(&pb[(i64)c * words_per_char + (r >> 5)].x, 1u << (r & 31));
     }
 }
 template <typename TT>
 __global__ void k_mod0_place(Text<TT> T, const u32 *__restrict__ isac, i64 k, i64 words_per_char,
-                             const u32 *__restrict__ bits, const u32 *__restrict__ prefix, u32 *__restrict__ out) {
+                             const uint2 *__restrict__ pb, u32 *__restrict__ out) {
     for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (i64)gridDim.x * blockDim.x) {
         u32 r = __ldcs(isac + j);
         u32 c = T(3 * j);
-        i64 w = (i64)c * words_per_char + (r >> 5);
-        out[prefix[w] + __popc(bits[w] & ((1u << (r & 31)) - 1u))] = (u32)j;
+        uint2 e = pb[(i64)c * words_per_char + (r >> 5)];
+        out[e.y + __popc(e.x & ((1u << (r & 31)) - 1u))] = (u32)j;
     }
 }
+struct PbPopc {
+    const uint2 *pb;
+    __device__ u32 operator()(i64 i) const { return __popc(pb[i].x); }
+};
+struct PbStore {
+    uint2 *pb;
+    __device__ void operator()(i64 i, u32 excl, u32) const { pb[i].y = excl; }
+};
 static bool mod0_use_bitmaps(u64 sigma) { return sigma + 1 <= 128; }
 inline i64 mod0_bitmap_words(u64 sigma, i64 m) { return (i64)(sigma + 1) * (ceil_div(m, 32) + 1); }
 
@@ -343,12 +353,12 @@ __global__ void k_build_eblocks(Text<TT> T, RankFromIsa R, i64 k, typename EBloc
 }
 
 template <typename TT>
-__device__ __forceinline__ MRec rec_from_eblock(const typename EBlockOf<TT>::type *__restrict__ E, i64 p) {
+__device__ __forceinline__ MRec rec_from_eblock(const typename EBlockOf<TT>::type *__restrict__ E, i64 p, u64 pol) {
     i64 j = p / 3;
     int r = (int)(p - 3 * j);
     u32 c[4], r1, r2, r4;
     if constexpr (sizeof(TT) == 1) {
-        uint4 e = __ldg(reinterpret_cast<const uint4 *>(E + j));
+        uint4 e = ldg_last(reinterpret_cast<const uint4 *>(E + j), pol);
         c[0] = e.x & 0xFF;
         c[1] = (e.x >> 8) & 0xFF;
         c[2] = (e.x >> 16) & 0xFF;
@@ -357,8 +367,8 @@ __device__ __forceinline__ MRec rec_from_eblock(const typename EBlockOf<TT>::typ
         r2 = e.z;
         r4 = e.w;
     } else {
-        uint4 a = __ldg(reinterpret_cast<const uint4 *>(E + j));
-        uint4 b = __ldg(reinterpret_cast<const uint4 *>(E + j) + 1);
+        uint4 a = ldg_last(reinterpret_cast<const uint4 *>(E + j), pol);
+        uint4 b = ldg_last(reinterpret_cast<const uint4 *>(E + j) + 1, pol);
         c[0] = a.x;
         c[1] = a.y;
         c[2] = a.z;
@@ -399,7 +409,7 @@ struct MergeIdx {
     __device__ __forceinline__ i64 bpos(i64 j) const { return 3 * (i64)B[j]; }
     __device__ __forceinline__ i64 apos_cs(i64 i) const { return R.L.pos(__ldcs(A + i)); }
     __device__ __forceinline__ i64 bpos_cs(i64 j) const { return 3 * (i64)__ldcs(B + j); }
-    __device__ __forceinline__ MRec rec(i64 p) const { return rec_from_eblock<TT>(E, p); }
+    __device__ __forceinline__ MRec rec(i64 p) const { return rec_from_eblock<TT>(E, p, l2_evict_last()); }
 };
 // Merge inputs given as positions with a by-position rank array
 // (merge_sample_nonsample, suffix_index.py:452-457).
@@ -717,17 +727,16 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     if (mod0_use_bitmaps(sigma)) {
         i64 wpc = ceil_div(L.m, 32) + 1;
         i64 nw = mod0_bitmap_words(sigma, L.m);
-        u32 *bits = ar.alloc<u32>(nw);
-        u32 *prefix = ar.alloc<u32>(nw);
+        uint2 *pb = ar.alloc<uint2>(nw);
         u32 *tmp = ar.alloc<u32>(scan_tmp_words(nw));
         SAIX_ARENA_OK(ar);
         Prof prof_("dc3.mod0_split", (8.0 + 2 * sizeof(TT)) * k + 4.0 * k + 8.0 * nw, st);
-        SAIX_CUDA(cudaMemsetAsync(bits, 0, (size_t)nw * 4, st));
+        SAIX_CUDA(cudaMemsetAsync(pb, 0, (size_t)nw * 8, st));
         int g = grid_for(k, K_THREADS);
-        k_mod0_bits<TT><<<g, K_THREADS, 0, st>>>(T, ISAc, k, wpc, bits);
+        k_mod0_bits<TT><<<g, K_THREADS, 0, st>>>(T, ISAc, k, wpc, pb);
         SAIX_LAUNCHED();
-        SAIX_TRY(scan_transform(PopcIn{bits}, StoreExcl{prefix}, nw, tmp, nullptr, st, "dc3.mod0_scan", 8.0 * nw));
-        k_mod0_place<TT><<<g, K_THREADS, 0, st>>>(T, ISAc, k, wpc, bits, prefix, v0);
+        SAIX_TRY(scan_transform(PbPopc{pb}, PbStore{pb}, nw, tmp, nullptr, st, "dc3.mod0_scan", 12.0 * nw));
+        k_mod0_place<TT><<<g, K_THREADS, 0, st>>>(T, ISAc, k, wpc, pb, v0);
         SAIX_LAUNCHED();
     } else {
         int passes = (bits_for(sigma) + OS_BITS - 1) / OS_BITS;

@@ -55,8 +55,9 @@ constexpr u32 kNone = 0xFFFFFFFFu;
 
 // Phi[sa[r]] = sa[r-1]: the text-order predecessor map (one scatter).
 __global__ void k_phi(const u32 *__restrict__ sa, i64 n, u32 *__restrict__ phi) {
+    u64 pol = l2_evict_last();  // the scatter target stays on chip, SA streams through
     for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x)
-        phi[__ldcs(sa + r)] = r ? sa[r - 1] : kNone;
+        st_last(phi + __ldcs(sa + r), r ? sa[r - 1] : kNone, pol);
 }
 
 // Exact PLCP at every chunk start (seed of the in-chunk walk).
@@ -113,9 +114,10 @@ k_plcp(const TT *__restrict__ T, i64 n, u32 *__restrict__ phi_plcp, const u32 *_
 __global__ void k_lcp_permute(const u32 *__restrict__ sa, i64 n, const u32 *__restrict__ plcp,
                               u32 *__restrict__ lcp, u32 boundary, u32 *best) {
     u32 mx = 0;
+    u64 pol = l2_evict_last();
     for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x) {
         u32 p = __ldcs(sa + r);
-        u32 l = plcp[p];
+        u32 l = ld_last(plcp + p, pol);
         __stcs(lcp + r, l);
         if (best && r > 0) {
             u32 q = sa[r - 1];
