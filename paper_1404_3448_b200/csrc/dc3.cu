@@ -398,6 +398,55 @@ __device__ __forceinline__ MRec rec_from_eblock(const typename EBlockOf<TT>::typ
     return m;
 }
 
+// Compact 8-byte block when 2 bits(m) + 3 bits(sigma) <= 64:
+//   r1 | r2 << rb | c0 << 2rb | c1 << 2rb+cb | c2 << 2rb+2cb
+// (R(3j+4) and T(3j+3) are the next block's r1 and c0, so they are not
+// stored).  Random gathers on B200 only stay in L2 while the target is
+// below ~64 MB (profiles/r1_l2_random_gather_probe.txt); at C2 level 0 the
+// compact blocks are 53 MB instead of 107 MB.  E[k] is a zero sentinel.
+__global__ void k_build_ecompact_u8(Text<u8> T, RankFromIsa R, i64 k, int rb, int cb, u64 *__restrict__ E) {
+    for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j <= k; j += (i64)gridDim.x * blockDim.x) {
+        u64 x = 0;
+        if (j < k) {
+            i64 p = 3 * j;
+            x = (u64)R(p + 1) | ((u64)R(p + 2) << rb) | ((u64)T(p) << (2 * rb)) | ((u64)T(p + 1) << (2 * rb + cb)) |
+                ((u64)T(p + 2) << (2 * rb + 2 * cb));
+        }
+        __stcs(E + j, x);
+    }
+}
+
+struct ECompact {
+    const u64 *E;
+    int rb, cb;
+    __device__ __forceinline__ MRec rec(i64 p) const {
+        i64 j = p / 3;
+        int r = (int)(p - 3 * j);
+        u64 rm = ((u64)1 << rb) - 1, cm = ((u64)1 << cb) - 1;
+        u64 x = __ldg(E + j);
+        MRec m;
+        m.pos = (u32)p;
+        if (r == 0) {
+            m.c0 = (u32)((x >> (2 * rb)) & cm);
+            m.c1 = (u32)((x >> (2 * rb + cb)) & cm);
+            m.r1 = (u32)(x & rm);
+            m.r2 = (u32)((x >> rb) & rm);
+        } else if (r == 1) {
+            m.c0 = (u32)((x >> (2 * rb + cb)) & cm);
+            m.c1 = 0;
+            m.r1 = (u32)((x >> rb) & rm);
+            m.r2 = 0;
+        } else {
+            u64 y = __ldg(E + j + 1);
+            m.c0 = (u32)((x >> (2 * rb + 2 * cb)) & cm);
+            m.c1 = (u32)((y >> (2 * rb)) & cm);
+            m.r1 = 0;
+            m.r2 = (u32)(y & rm);
+        }
+        return m;
+    }
+};
+
 // Merge inputs: sorted samples as sample indices / sorted mod-0 as indices.
 template <typename TT>
 struct MergeIdx {
@@ -405,11 +454,14 @@ struct MergeIdx {
     RankFromIsa R;
     const u32 *A, *B;
     const typename EBlockOf<TT>::type *E;
+    ECompact EC;  // used when EC.E != nullptr
     __device__ __forceinline__ i64 apos(i64 i) const { return R.L.pos(A[i]); }
     __device__ __forceinline__ i64 bpos(i64 j) const { return 3 * (i64)B[j]; }
     __device__ __forceinline__ i64 apos_cs(i64 i) const { return R.L.pos(__ldcs(A + i)); }
     __device__ __forceinline__ i64 bpos_cs(i64 j) const { return 3 * (i64)__ldcs(B + j); }
-    __device__ __forceinline__ MRec rec(i64 p) const { return rec_from_eblock<TT>(E, p, l2_evict_last()); }
+    __device__ __forceinline__ MRec rec(i64 p) const {
+        return EC.E ? EC.rec(p) : rec_from_eblock<TT>(E, p, l2_evict_last());
+    }
 };
 // Merge inputs given as positions with a by-position rank array
 // (merge_sample_nonsample, suffix_index.py:452-457).
@@ -749,14 +801,25 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     i64 pad = L.pad ? 1 : 0;
     i64 na = L.m - pad;
     using EB = typename EBlockOf<TT>::type;
-    EB *E = ar.alloc<EB>(k);
-    SAIX_ARENA_OK(ar);
-    {
+    int rb = bits_for((u64)L.m), cb = bits_for(sigma);
+    bool compact = sizeof(TT) == 1 && 2 * rb + 3 * cb <= 64;
+    EB *E = nullptr;
+    ECompact EC{nullptr, rb, cb};
+    if (compact) {
+        u64 *E64 = ar.alloc<u64>(k + 1);
+        SAIX_ARENA_OK(ar);
+        Prof prof_("dc3.eblocks", (double)sizeof(TT) * N + 8.0 * L.m + 8.0 * k, st);
+        k_build_ecompact_u8<<<grid_for(k + 1, K_THREADS), K_THREADS, 0, st>>>(
+            Text<u8>{(const u8 *)text, N}, R, k, rb, cb, E64);
+        EC.E = E64;
+    } else {
+        E = ar.alloc<EB>(k);
+        SAIX_ARENA_OK(ar);
         Prof prof_("dc3.eblocks", (double)sizeof(TT) * N + 8.0 * L.m + (double)sizeof(EB) * k, st);
         k_build_eblocks<TT><<<grid_for(k, K_THREADS), K_THREADS, 0, st>>>(T, R, k, E);
     }
     SAIX_LAUNCHED();
-    MergeIdx<TT> V{T, R, SAc + pad, vals, E};
+    MergeIdx<TT> V{T, R, SAc + pad, vals, E, EC};
     SAIX_TRY(merge_run(V, na, k, split, SA, ISA, st));
 
     if (probe) {

@@ -75,7 +75,8 @@ __global__ void k_lcp_seeds(const TT *__restrict__ T, i64 n, const u32 *__restri
 // phi tile is staged in shared memory and overwritten with PLCP values).
 template <typename TT>
 __global__ void __launch_bounds__(LCP_THREADS)
-k_plcp(const TT *__restrict__ T, i64 n, u32 *__restrict__ phi_plcp, const u32 *__restrict__ seeds) {
+k_plcp(const TT *__restrict__ T, i64 n, u32 *__restrict__ phi_plcp, const u32 *__restrict__ seeds,
+       u8 *__restrict__ plcp8) {
     __shared__ u32 sh[LCP_TILE + LCP_TILE / 32];
     i64 base = (i64)blockIdx.x * LCP_TILE;
     for (int x = threadIdx.x; x < LCP_TILE; x += LCP_THREADS) {
@@ -103,7 +104,11 @@ k_plcp(const TT *__restrict__ T, i64 n, u32 *__restrict__ phi_plcp, const u32 *_
     __syncthreads();
     for (int x = threadIdx.x; x < LCP_TILE; x += LCP_THREADS) {
         i64 i = base + x;
-        if (i < n) phi_plcp[i] = sh[x + (x >> 5)];
+        if (i < n) {
+            u32 h = sh[x + (x >> 5)];
+            phi_plcp[i] = h;
+            plcp8[i] = (u8)(h < 255 ? h : 255);
+        }
     }
 }
 
@@ -111,13 +116,15 @@ k_plcp(const TT *__restrict__ T, i64 n, u32 *__restrict__ phi_plcp, const u32 *_
 // best != nullptr it also folds in longest_overlap's first pass
 // (overlap.py:129-136): max lcp over adjacent pairs on opposite sides of the
 // separator at `boundary`.
+// The gather reads a byte copy of PLCP (values >= 255 escape to the u32
+// array): n bytes stay L2-resident where the 4n-byte array would not.
 __global__ void k_lcp_permute(const u32 *__restrict__ sa, i64 n, const u32 *__restrict__ plcp,
-                              u32 *__restrict__ lcp, u32 boundary, u32 *best) {
+                              const u8 *__restrict__ plcp8, u32 *__restrict__ lcp, u32 boundary, u32 *best) {
     u32 mx = 0;
-    u64 pol = l2_evict_last();
     for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x) {
         u32 p = __ldcs(sa + r);
-        u32 l = ld_last(plcp + p, pol);
+        u32 l = plcp8[p];
+        if (l == 255) l = plcp[p];
         __stcs(lcp + r, l);
         if (best && r > 0) {
             u32 q = sa[r - 1];
@@ -131,7 +138,7 @@ __global__ void k_lcp_permute(const u32 *__restrict__ sa, i64 n, const u32 *__re
     }
 }
 
-static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32 *phi, u32 *seeds,
+static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32 *phi, u32 *seeds, u8 *plcp8,
                    cudaStream_t st, i64 boundary, u32 *best, bool phi_ready) {
     i64 nchunks = ceil_div(n, LCP_CHUNK);
     int g = grid_for(n, 256);
@@ -151,13 +158,13 @@ static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32
     SAIX_LAUNCHED();
     {
         Prof prof_("lcp.plcp", (8.0 + tb) * n, st);
-        if (tb == 1) k_plcp<u8><<<tiles, LCP_THREADS, 0, st>>>((const u8 *)text, n, phi, seeds);
-        else k_plcp<u32><<<tiles, LCP_THREADS, 0, st>>>((const u32 *)text, n, phi, seeds);
+        if (tb == 1) k_plcp<u8><<<tiles, LCP_THREADS, 0, st>>>((const u8 *)text, n, phi, seeds, plcp8);
+        else k_plcp<u32><<<tiles, LCP_THREADS, 0, st>>>((const u32 *)text, n, phi, seeds, plcp8);
     }
     SAIX_LAUNCHED();
     {
         Prof prof_("lcp.permute", 12.0 * n, st);
-        k_lcp_permute<<<g, 256, 0, st>>>(sa, n, phi, lcp, boundary >= 0 ? (u32)boundary : 0u,
+        k_lcp_permute<<<g, 256, 0, st>>>(sa, n, phi, plcp8, lcp, boundary >= 0 ? (u32)boundary : 0u,
                                          boundary >= 0 ? best : nullptr);
     }
     SAIX_LAUNCHED();
@@ -169,8 +176,9 @@ int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp
     Arena ar{(char *)ws, ws_bytes};
     u32 *phi = phi_in ? phi_in : ar.alloc<u32>(n);
     u32 *seeds = ar.alloc<u32>(ceil_div(n, LCP_CHUNK) + 1);
+    u8 *plcp8 = ar.alloc<u8>(n);
     SAIX_ARENA_OK(ar);
-    return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, st, boundary, best, phi_ready);
+    return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, plcp8, st, boundary, best, phi_ready);
 }
 
 }  // namespace saix
@@ -181,6 +189,7 @@ extern "C" size_t saix_lcp_workspace_bytes(int64_t n) {
     Arena ar;
     ar.alloc<u32>(n);
     ar.alloc<u32>(ceil_div(n > 0 ? n : 1, LCP_CHUNK) + 1);
+    ar.alloc<u8>(n);
     return ar.peak + Arena::kAlign;
 }
 
