@@ -569,94 +569,8 @@ k_merge_tile(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict
     }
 }
 
-// Keyed variant (when 2 bits(sigma) + bits(m) <= 63): every comparison
-// family collapses to one u64 compare -- key1 = c0 << rb | r1 (mod-1
-// samples), key2 = (c0 << cb | c1) << rb | r2 (mod-2 samples).  A sample
-// keeps only its own family's key (bit 63 = mod-2), a non-sample both, so
-// each merge step costs two 8-byte shared loads instead of two 20-byte
-// records.
-constexpr u64 KEY_FAM2 = 1ull << 63;
-
 template <class V>
-__global__ void __launch_bounds__(MT_THREADS)
-k_merge_tile_keyed(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa,
-                   u32 *__restrict__ isa, int cb, int rb) {
-    __shared__ u64 k1[MT_TILE];  // A: family key | fam bit; B: key1
-    __shared__ u64 k2[MT_TILE];  // B: key2
-    __shared__ u32 ps[MT_TILE];  // positions, then the merged output
-    i64 total = na + nb;
-    i64 d0 = (i64)blockIdx.x * MT_TILE;
-    i64 d1 = d0 + MT_TILE < total ? d0 + MT_TILE : total;
-    i64 i0 = split[blockIdx.x], i1 = split[blockIdx.x + 1];
-    i64 j0 = d0 - i0;
-    int nat = (int)(i1 - i0), cnt = (int)(d1 - d0), nbt = cnt - nat;
-    u32 pp[MT_ITEMS];
-#pragma unroll
-    for (int q = 0; q < MT_ITEMS; q++) {
-        int x = threadIdx.x + q * MT_THREADS;
-        pp[q] = x < cnt ? (u32)(x < nat ? v.apos_cs(i0 + x) : v.bpos_cs(j0 + (x - nat))) : 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < MT_ITEMS; q++) {
-        int x = threadIdx.x + q * MT_THREADS;
-        if (x < cnt) {
-            MRec m = v.rec(pp[q]);
-            u64 key1 = ((u64)m.c0 << rb) | m.r1;
-            u64 key2 = ((((u64)m.c0 << cb) | m.c1) << rb) | m.r2;
-            ps[x] = m.pos;
-            if (x < nat) {
-                k1[x] = (m.pos % 3 == 1) ? key1 : (key2 | KEY_FAM2);
-            } else {
-                k1[x] = key1;
-                k2[x] = key2;
-            }
-        }
-    }
-    __syncthreads();
-    const u64 *KA = k1, *KB1 = k1 + nat, *KB2 = k2 + nat;
-    const u32 *PA = ps, *PB = ps + nat;
-    auto a_first = [&](int a, int b) -> bool {
-        u64 ka = KA[a];
-        u64 kb = (ka & KEY_FAM2) ? KB2[b] : KB1[b];
-        return (ka & ~KEY_FAM2) < kb;
-    };
-    int dt = threadIdx.x * MT_ITEMS;
-    u32 res[MT_ITEMS];
-    if (dt < cnt) {
-        int lo = dt > nbt ? dt - nbt : 0, hi = dt < nat ? dt : nat;
-        while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if (a_first(mid, dt - 1 - mid)) lo = mid + 1;
-            else hi = mid;
-        }
-        int i = lo, j = dt - lo;
-#pragma unroll
-        for (int r = 0; r < MT_ITEMS; r++) {
-            bool live = dt + r < cnt;
-            bool takeA = j >= nbt || (i < nat && a_first(i, j));
-            u32 pa = i < nat ? PA[i] : 0u, pb = j < nbt ? PB[j] : 0u;
-            res[r] = takeA ? pa : pb;
-            if (live) {
-                if (takeA) i++;
-                else j++;
-            }
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < MT_ITEMS; r++)
-        if (dt + r < cnt) ps[dt + r] = res[r];
-    __syncthreads();
-    for (int x = threadIdx.x; x < cnt; x += MT_THREADS) {
-        u32 p = ps[x];
-        __stcs(sa + d0 + x, p);
-        if (isa) isa[p] = (u32)(d0 + x);
-    }
-}
-
-template <class V>
-static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStream_t st, int cb = 0,
-                     int rb = 0) {
+static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStream_t st) {
     i64 total = na + nb;
     if (total == 0) return SAIX_OK;
     i64 ntiles = ceil_div(total, MT_TILE);
@@ -669,10 +583,7 @@ static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStr
         // indices 4 + chars 2w + ranks (4 per sample, 8 per non-sample) + SA 4 + ISA 4
         double w = (double)v.T.bytes();
         Prof prof_("dc3.merge_tile", total * (4 + 2 * w + 4) + 4.0 * (na + 2 * nb) + (isa ? 4.0 * total : 0), st);
-        if (cb > 0 && 2 * cb + rb <= 63)
-            k_merge_tile_keyed<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa, cb, rb);
-        else
-            k_merge_tile<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa);
+        k_merge_tile<V><<<(unsigned)ntiles, MT_THREADS, 0, st>>>(v, na, nb, split, sa, isa);
     }
     SAIX_LAUNCHED();
     return SAIX_OK;
@@ -909,7 +820,7 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     }
     SAIX_LAUNCHED();
     MergeIdx<TT> V{T, R, SAc + pad, vals, E, EC};
-    SAIX_TRY(merge_run(V, na, k, split, SA, ISA, st, cb, rb));
+    SAIX_TRY(merge_run(V, na, k, split, SA, ISA, st));
 
     if (probe) {
         int g = grid_for(N + 3, K_THREADS);
