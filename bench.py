@@ -4,17 +4,22 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--workload c2|c3|c5]
 
-Default workload (BASELINE.json configs[1], "C2"): a single synthetic pair of
+Default workload (BASELINE.json configs[1], "C2"): one synthetic pair of
 2 x 10 Mbp random ACGT sequences (gen_random seeds 11/12 on rank 0; rank r
 uses 11+2r/12+2r), full pipeline on one B200 per rank: encode -> generalized
-text -> DC3 suffix array -> LCP -> overlap scan.  A "step" is one pass of that
+text -> DC3 suffix array -> LCP -> overlap scan.  A "step" is one pass of the
 pipeline over one pair.  Metric: Mbases/s of generalized-text bases through
-the whole pipeline (20,000,001 per pair); value is the whole-job aggregate
-over ranks; N > 1 runs independent replicas (weak scaling, no data-path
-collective: a single long pair does not shard).
+the whole pipeline (20,000,001 per pair); `value` is the whole-job aggregate;
+N > 1 runs independent replicas (weak scaling, no data-path collective: a
+single long pair does not shard).
 
---impl reference times the reference algorithm on the host (the C oracle
-port in oracle/, kind "port": the reference is pure Python, nothing to
+Other BASELINE configs (reported in DESIGN.md / profiles/, not the default):
+  c3  configs[2]: 256 Mbp (2^28) DC3 suffix array + LCP, Mbases/s
+  c5  configs[4]: 10^8 random sparse-table RMQ queries over the LCP array of a
+      64 Mbp (2^26) text, table build + queries per step, queries/s
+
+--impl reference times the reference algorithm on the host (the C oracle port
+in oracle/, kind "port": the reference is pure Python + numba, nothing to
 compile) on the same workload; rank 0 only.
 """
 
@@ -137,13 +142,173 @@ def ncu_traffic(kernel: str):
         return None
 
 
+def encode_ascii(residues: str, shift: int = 0) -> np.ndarray:
+    lut = np.zeros(256, np.uint8)
+    for r, ch in enumerate("ACGT", 1 + shift):
+        lut[ord(ch)] = r
+    return lut[np.frombuffer(residues.encode(), np.uint8)]
+
+
 # ------------------------------------------------------------------ workloads
 
-def c2_inputs(rank: int):
-    from paper_1404_3448_b200.sequence import gen_random
-    a = gen_random(10_000_000, 11 + 2 * rank)
-    b = gen_random(10_000_000, 12 + 2 * rank)
-    return (np.frombuffer(a.residues.encode(), np.uint8), np.frombuffer(b.residues.encode(), np.uint8))
+class C2:
+    """configs[1]: full longest-overlap pipeline on one 2 x 10 Mbp pair."""
+    name = "c2"
+    unit = "Mbases/s"
+
+    def __init__(self, rank: int):
+        from paper_1404_3448_b200.sequence import gen_random
+        import paper_1404_3448_b200 as sx
+        a = gen_random(10_000_000, 11 + 2 * rank)
+        b = gen_random(10_000_000, 12 + 2 * rank)
+        self.ha = np.frombuffer(a.residues.encode(), np.uint8)
+        self.hb = np.frombuffer(b.residues.encode(), np.uint8)
+        self.units = len(self.ha) + len(self.hb) + 1          # GSA bases per step
+        self.pipe = sx.OverlapPipeline(len(self.ha), len(self.hb))
+        self.pipe.stage(self.ha, self.hb)
+        self.result = [int(x) for x in self.pipe.run_staged()[:3]]
+        self.h2d = len(self.ha) + len(self.hb)
+        self.d2h = 32
+        self.config = {"workload": "C2: 2 x 10 Mbp random ACGT pair (gen_random seeds 11/12 + 2*rank), "
+                                   "encode+DC3+LCP+overlap scan per step",
+                       "gsa_bases_per_pair": self.units}
+
+    def step_device(self):
+        self.pipe.run_device()
+
+    def step_e2e(self):
+        self.pipe.run_staged()
+
+    def extra(self, ms_dev, steps, world):
+        return {"pairs_per_s": round(world * steps / (ms_dev * 1e-3), 3)}
+
+    def cpu_baseline(self):
+        import oracle
+        t0 = time.perf_counter()
+        ref = oracle.longest_overlap(self.ha.tobytes(), self.hb.tobytes())
+        dt = time.perf_counter() - t0
+        assert tuple(self.result) == ref, (self.result, ref)
+        return {"value": self.units / dt / 1e6, "unit": self.unit, "cores": 1, "kind": "port",
+                "sample": "one full C2 pair (2 x 10 Mbp), oracle/saix_oracle.c single thread "
+                          f"({dt:.1f} s); result matched the GPU's {tuple(ref)}"}
+
+
+class C3:
+    """configs[2]: DC3 suffix array + LCP of a 2^28 random text."""
+    name = "c3"
+    unit = "Mbases/s"
+    N = 1 << 28
+
+    def __init__(self, rank: int):
+        from paper_1404_3448_b200.sequence import gen_random
+        from paper_1404_3448_b200.suffix_index import SuffixIndexer
+        self.ranks = encode_ascii(gen_random(self.N, 1 + rank).residues)
+        self.units = self.N
+        self.ix = SuffixIndexer(self.N, 4)
+        self.ix.stage(self.ranks)
+        self.ix.run_staged()
+        self.h2d = self.N
+        self.d2h = 8 * self.N
+        self.config = {"workload": "C3: 2^28 random ACGT (gen_random seed 1 + rank), DC3 suffix array + LCP "
+                                   "per step (SA and LCP u32 resident; e2e downloads both)",
+                       "bases": self.N}
+        self.result = None
+
+    def step_device(self):
+        self.ix.run_device()
+
+    def step_e2e(self):
+        self.ix.run_staged()
+
+    def extra(self, ms_dev, steps, world):
+        return {}
+
+    def cpu_baseline(self):
+        import oracle
+        # bounded sample: DC3 + Kasai of the first 2^24 bases (~10-20 s)
+        n = 1 << 24
+        t = self.ranks[:n].astype(np.int64)
+        t0 = time.perf_counter()
+        sa, rank = oracle.dc3(t, 4)
+        oracle.lcp(t, sa, rank)
+        dt = time.perf_counter() - t0
+        return {"value": n / dt / 1e6, "unit": self.unit, "cores": 1, "kind": "port",
+                "sample": f"DC3 + LCP of the first 2^24 bases of the C3 text, single thread ({dt:.1f} s)"}
+
+
+class C5:
+    """configs[4]: 10^8 random LCP range-minimum queries over a 2^26 text."""
+    name = "c5"
+    unit = "queries/s"
+    N = 1 << 26
+    Q = 100_000_000
+
+    def __init__(self, rank: int):
+        import torch
+
+        from paper_1404_3448_b200.rmq import DeviceSparseTable
+        from paper_1404_3448_b200.sequence import gen_random
+        from paper_1404_3448_b200.suffix_index import SuffixIndexer
+        self.ranks = encode_ascii(gen_random(self.N, 1 + rank).residues)
+        self.ix = SuffixIndexer(self.N, 4)
+        self.ix.stage(self.ranks)
+        self.ix.run_staged()
+        self.st = DeviceSparseTable(self.ix.lcp, 4, self.N)
+        q = np.random.default_rng(2026 + rank).integers(0, self.N, size=(self.Q, 2))
+        self.hqi = torch.from_numpy(np.ascontiguousarray(q[:, 0])).pin_memory()
+        self.hqj = torch.from_numpy(np.ascontiguousarray(q[:, 1])).pin_memory()
+        dev = self.ix.lcp.device
+        self.qi = self.hqi.to(dev)
+        self.qj = self.hqj.to(dev)
+        self.hout = torch.empty(self.Q, dtype=torch.int64, pin_memory=True)
+        self.units = self.Q
+        self.h2d = 16 * self.Q
+        self.d2h = 8 * self.Q
+        self.config = {"workload": "C5: sparse-table build over the LCP array of a 2^26 random text + 10^8 "
+                                   "query_sparse (default_rng(2026).integers(0, n, (10^8, 2))) per step",
+                       "n": self.N, "queries": self.Q, "table_mode": int(self.st.plan.mode)}
+        self.out = None
+        self.result = None
+
+    def step_device(self):
+        self.st.rebuild()
+        self.out, _ = self.st.query_device(self.qi, self.qj)
+
+    def step_e2e(self):
+        import torch
+        self.qi.copy_(self.hqi, non_blocking=True)
+        self.qj.copy_(self.hqj, non_blocking=True)
+        self.st.rebuild()
+        out, _ = self.st.query_device(self.qi, self.qj)
+        self.hout.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    def extra(self, ms_dev, steps, world):
+        return {}
+
+    def cpu_baseline(self):
+        import oracle
+        # parity on a 10^6 prefix of the queries against the leftmost-argmin definition
+        lcp = self.ix.lcp[: self.N].cpu().numpy().view(np.uint32).astype(np.int64)
+        qi, qj = self.hqi[:1_000_000].numpy(), self.hqj[:1_000_000].numpy()
+        got = self.out[:1_000_000].cpu().numpy()
+        assert np.array_equal(got, oracle.argmin_blocked(lcp, qi, qj))
+        # timed: the reference SparseTable.query restated in C, over a bounded
+        # sample (table of the first 2^22 LCP values, 10^6 queries inside it)
+        m = 1 << 22
+        v = lcp[:m]
+        table = oracle.sparse_build(v)
+        rng = np.random.default_rng(2026)
+        si, sj = rng.integers(0, m, size=(2, 1_000_000))
+        t0 = time.perf_counter()
+        oracle.sparse_query(v, table, si, sj)
+        dt = time.perf_counter() - t0
+        return {"value": 1_000_000 / dt, "unit": self.unit, "cores": 1, "kind": "port",
+                "sample": "10^6 SparseTable.query over the first 2^22 LCP values (C port of rmq.py:52-58), "
+                          f"single thread ({dt:.2f} s); GPU answers matched the argmin oracle on 10^6 queries"}
+
+
+WORKLOADS = {"c2": C2, "c3": C3, "c5": C5}
 
 
 def run_reference(args, rank):
@@ -152,8 +317,9 @@ def run_reference(args, rank):
     if args.workload != "c2":
         print(json.dumps({"impl": "reference", "unavailable": f"workload {args.workload} not wired for the CPU arm"}))
         return
-    ha, hb = c2_inputs(0)
-    a, b = ha.tobytes(), hb.tobytes()
+    from paper_1404_3448_b200.sequence import gen_random
+    a = gen_random(10_000_000, 11).residues.encode()
+    b = gen_random(10_000_000, 12).residues.encode()
     n = len(a) + len(b) + 1
     for _ in range(args.warmup):
         oracle.longest_overlap(a, b)
@@ -176,18 +342,13 @@ def run_reference(args, rank):
     }), flush=True)
 
 
-def bench_c2(args, rank, world, dist):
+def bench(args, rank, world, dist):
     import torch
 
-    import paper_1404_3448_b200 as sx
     from paper_1404_3448_b200 import _lib
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    ha, hb = c2_inputs(rank)
-    n_gsa = len(ha) + len(hb) + 1
-    pipe = sx.OverlapPipeline(len(ha), len(hb))
-    pipe.stage(ha, hb)
-    res0 = pipe.run_staged()                       # correctness pre-check (bench.py:112-117)
+    wl = WORKLOADS[args.workload](rank)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
 
@@ -214,20 +375,20 @@ def bench_c2(args, rank, world, dist):
         return ms
 
     for _ in range(args.warmup):
-        pipe.run_device()
-        pipe.run_staged()
+        wl.step_device()
+        wl.step_e2e()
     torch.cuda.synchronize()
 
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
     _lib.prof_enable(not args.no_prof)
-    ms_dev = timed(pipe.run_device, args.steps)    # value: inputs resident in HBM
+    ms_dev = timed(wl.step_device, args.steps)    # value: inputs resident in HBM
     prof = _lib.prof_collect()
     _lib.prof_enable(False)
-    ms_e2e = timed(pipe.run_staged, args.steps)    # e2e: pinned host in, 32 B out
+    ms_e2e = timed(wl.step_e2e, args.steps)       # e2e: pinned host in, results out
     clk = clocks.stop()
 
-    launches_per_step = count_our_launches(pipe.run_device)
+    launches_per_step = count_our_launches(wl.step_device)
     peak, peak_kind = measured_peak_gbs()
     dom = max(prof, key=lambda e: e["ms"]) if prof else None
     roof = None
@@ -242,45 +403,38 @@ def bench_c2(args, rank, world, dist):
                 "share_of_step": round(dom["ms"] / ms_dev, 4) if ms_dev else None}
     stage = {e["name"]: round(e["ms"] / args.steps, 4) for e in sorted(prof, key=lambda e: -e["ms"])}
 
-    pairs = world * args.steps
-    value = n_gsa * pairs / (ms_dev * 1e-3) / 1e6
-    e2e_value = n_gsa * pairs / (ms_e2e * 1e-3) / 1e6
+    scale = 1e6 if wl.unit == "Mbases/s" else 1.0
+    value = wl.units * world * args.steps / (ms_dev * 1e-3) / scale
+    e2e_value = wl.units * world * args.steps / (ms_e2e * 1e-3) / scale
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import oracle
-        t0 = time.perf_counter()
-        ref = oracle.longest_overlap(ha.tobytes(), hb.tobytes())
-        dt = time.perf_counter() - t0
-        assert tuple(int(x) for x in res0[:3]) == ref, (res0, ref)
-        cpu = {"value": n_gsa / dt / 1e6, "unit": "Mbases/s", "cores": 1, "kind": "port",
-               "sample": "one full C2 pair (2 x 10 Mbp), oracle/saix_oracle.c single thread "
-                         f"({dt:.1f} s); result matched the GPU's {tuple(ref)}"}
+        cpu = wl.cpu_baseline()
 
-    results = [int(x) for x in res0[:3]]
-    if dist is not None:
-        t = torch.tensor(results, device=dev, dtype=torch.int64)
+    results = wl.result
+    if dist is not None and wl.result is not None:
+        t = torch.tensor(wl.result, device=dev, dtype=torch.int64)
         allr = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(allr, t)
         results = [[int(x) for x in r.tolist()] for r in allr]
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "Mbases/s", "n_gpus": world,
+            "metric": METRIC, "value": round(value, 2), "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_dev / args.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
-            "config": {"workload": "C2: 2 x 10 Mbp random ACGT pair (gen_random seeds 11/12 + 2*rank), "
-                                   "encode+DC3+LCP+overlap scan per step",
-                       "gsa_bases_per_pair": n_gsa, "l2": "flushed between timed steps (512 MiB write)",
-                       "parallelism": f"replicas x{world}"},
-            "pairs_per_s": round(pairs / (ms_dev * 1e-3), 3),
-            "e2e": {"value": round(e2e_value, 2), "unit": "Mbases/s", "h2d_bytes_per_step": len(ha) + len(hb),
-                    "d2h_bytes_per_step": 32, "ms_per_step": round(ms_e2e / args.steps, 4)},
+            "config": dict(wl.config, l2="flushed between timed steps (512 MiB write)",
+                           parallelism=f"replicas x{world}"),
+            **wl.extra(ms_dev, args.steps, world),
+            "e2e": {"value": round(e2e_value, 2), "unit": wl.unit, "h2d_bytes_per_step": wl.h2d,
+                    "d2h_bytes_per_step": wl.d2h, "ms_per_step": round(ms_e2e / args.steps, 4)},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
-            "stage_ms_per_step": stage, "result": results,
+            "stage_ms_per_step": stage,
         }
+        if results is not None:
+            line["result"] = results
         print(json.dumps(line), flush=True)
 
 
@@ -290,7 +444,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c2"], default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prof", action="store_true", help="time without per-kernel events")
     args = ap.parse_args()
@@ -309,7 +463,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
-        bench_c2(args, rank, world, dist)
+        bench(args, rank, world, dist)
     finally:
         if dist is not None:
             dist.destroy_process_group()

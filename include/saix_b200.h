@@ -137,6 +137,11 @@ typedef struct saix_sparse_plan {
     int32_t value_bits;
 } saix_sparse_plan;
 
+/* min and max of n device values (value_bytes 4 = u32, 8 = int64) into
+ * out2 (device int64[2]); lets a sparse table over a device array (e.g. an
+ * LCP array) be planned without copying it to the host. */
+SAIX_API int saix_minmax(const void *values, int value_bytes, int64_t n, int64_t *out2, void *stream);
+
 /* Choose the table layout for n values in [vmin, vmax]. */
 SAIX_API int saix_sparse_plan_make(int64_t n, int64_t vmin, int64_t vmax,
                           saix_sparse_plan *plan);

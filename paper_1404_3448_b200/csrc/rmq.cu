@@ -129,9 +129,47 @@ __global__ void k_lcp_query(PlanDev P, const void *tab, Vals<V> val, const u32 *
 
 static PlanDev dev_plan(const saix_sparse_plan *p) { return PlanDev{p->n, p->value_bias, p->mode, p->index_bits}; }
 
+__global__ void k_minmax_init(i64 *out2) {
+    out2[0] = INT64_MAX;
+    out2[1] = INT64_MIN;
+}
+
+template <typename V>
+__global__ void k_minmax(Vals<V> val, i64 n, i64 *out2) {
+    i64 lo = INT64_MAX, hi = INT64_MIN;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        i64 x = val(i);
+        lo = x < lo ? x : lo;
+        hi = x > hi ? x : hi;
+    }
+    for (int o = 16; o; o >>= 1) {
+        i64 a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if (lane_id() == 0) {
+        atomicMin((long long *)&out2[0], (long long)lo);
+        atomicMax((long long *)&out2[1], (long long)hi);
+    }
+}
+
 }  // namespace saix
 
 using namespace saix;
+
+extern "C" int saix_minmax(const void *values, int value_bytes, int64_t n, int64_t *out2, void *stream) {
+    if (!values || !out2 || n <= 0 || (value_bytes != 4 && value_bytes != 8)) {
+        set_error("saix_minmax: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    k_minmax_init<<<1, 1, 0, st>>>(out2);
+    int g = grid_for(n, 256, kNumSMs * 8);
+    if (value_bytes == 4) k_minmax<u32><<<g, 256, 0, st>>>(Vals<u32>{(const u32 *)values}, n, out2);
+    else k_minmax<i64><<<g, 256, 0, st>>>(Vals<i64>{(const i64 *)values}, n, out2);
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}
 
 extern "C" int saix_sparse_plan_make(int64_t n, int64_t vmin, int64_t vmax, saix_sparse_plan *plan) {
     if (!plan || n <= 0 || vmin > vmax || n > ((int64_t)1 << 32) - 1) {

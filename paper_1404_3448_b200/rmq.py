@@ -109,6 +109,44 @@ class SparseTable:
         return int(self.query_batch(np.array([i]), np.array([j]))[0])
 
 
+class DeviceSparseTable(SparseTable):
+    """SparseTable over a device-resident array (u32 or int64), e.g. the LCP
+    array the GPU just built: planned from a device min/max, never copied to
+    the host.  ``values`` (host) is materialised lazily for API parity."""
+
+    def __init__(self, values_dev, value_bytes: int, n: int):  # noqa: D401 - no super().__init__
+        t = _lib.torch()
+        L = _lib.load()
+        if n <= 0:
+            raise ValueError("cannot build a sparse table over an empty array")
+        mm = t.empty(2, dtype=t.int64, device=values_dev.device)
+        _lib.check(L.saix_minmax(_lib.ptr(values_dev), value_bytes, n, _lib.ptr(mm), _lib.stream_ptr()),
+                   "saix_minmax")
+        vmin, vmax = (int(x) for x in mm.tolist())
+        plan = _lib.SparsePlan()
+        _lib.check(L.saix_sparse_plan_make(n, vmin, vmax, ctypes.byref(plan)), "saix_sparse_plan_make")
+        self.plan = plan
+        self._vals, self._vbytes = values_dev, value_bytes
+        self._table = _lib.workspace(plan.table_bytes)
+        self._err = t.zeros(1, dtype=t.int32, device=values_dev.device)
+        self._table_host = None
+        self._values_host = None
+        self.rebuild()
+
+    def rebuild(self) -> None:
+        """Re-run the table build kernels (the values are unchanged)."""
+        L = _lib.load()
+        _lib.check(L.saix_sparse_build(ctypes.byref(self.plan), _lib.ptr(self._vals), self._vbytes,
+                                       _lib.ptr(self._table), _lib.stream_ptr()), "saix_sparse_build")
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._values_host is None:
+            a = self._vals[: self.n].cpu().numpy()
+            self._values_host = (a.view(np.uint32) if self._vbytes == 4 else a).astype(np.int64)
+        return self._values_host
+
+
 def build_sparse(values) -> SparseTable:
     return SparseTable(values)
 

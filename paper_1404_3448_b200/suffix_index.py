@@ -289,3 +289,47 @@ def merge_sample_nonsample(workspace: Dc3Workspace, text: RankedText) -> SuffixA
                           _lib.stream_ptr())
     _lib.check(rc, "saix_dc3_merge")
     return SuffixArray.from_order(_lib.u32_to_i64_host(out, total))
+
+
+class SuffixIndexer:
+    """Reusable device buffers for suffix array + LCP construction of texts of
+    length n (the throughput path behind ``build_sa_dc3`` + ``build_lcp``).
+
+    ``t`` (device) holds the ranks; ``run_device()`` builds SA (and ISA when
+    ``want_isa``) and LCP without host traffic; ``run_staged()`` adds the
+    pinned-host upload of the ranks and the download of SA and LCP (u32)."""
+
+    def __init__(self, n: int, sigma: int, want_isa: bool = False):
+        t = _lib.torch()
+        L = _lib.load()
+        dev = _lib.device()
+        self.n, self.sigma = int(n), int(sigma)
+        self.bytes = 1 if sigma <= 255 else 4
+        self.t = t.zeros(max(n, 1) + 8, dtype=t.uint8 if self.bytes == 1 else t.int32, device=dev)
+        self.sa = t.empty(max(n, 1), dtype=t.int32, device=dev)
+        self.isa = t.empty(max(n, 1), dtype=t.int32, device=dev) if want_isa else None
+        self.lcp = t.empty(max(n, 1), dtype=t.int32, device=dev)
+        wsz = max(L.saix_dc3_workspace_bytes(n, self.bytes), L.saix_lcp_workspace_bytes(n))
+        self.ws = _lib.workspace(wsz)
+        self.ht = t.empty(max(n, 1), dtype=self.t.dtype, pin_memory=True)
+        self.hsa = t.empty(max(n, 1), dtype=t.int32, pin_memory=True)
+        self.hlcp = t.empty(max(n, 1), dtype=t.int32, pin_memory=True)
+
+    def stage(self, ranks: np.ndarray) -> None:
+        self.ht.numpy()[: self.n] = ranks
+
+    def run_device(self) -> None:
+        L = _lib.load()
+        s = _lib.stream_ptr()
+        _lib.check(L.saix_dc3(_lib.ptr(self.t), self.bytes, self.n, self.sigma, _lib.ptr(self.sa),
+                              _lib.ptr(self.isa), _lib.ptr(self.ws), self.ws.numel(), None, s), "saix_dc3")
+        _lib.check(L.saix_lcp(_lib.ptr(self.t), self.bytes, self.n, _lib.ptr(self.sa), None,
+                              _lib.ptr(self.lcp), _lib.ptr(self.ws), self.ws.numel(), s), "saix_lcp")
+
+    def run_staged(self) -> None:
+        n = self.n
+        self.t[:n].copy_(self.ht[:n], non_blocking=True)
+        self.run_device()
+        self.hsa[:n].copy_(self.sa[:n], non_blocking=True)
+        self.hlcp[:n].copy_(self.lcp[:n], non_blocking=True)
+        _lib.torch().cuda.current_stream().synchronize()
