@@ -172,7 +172,10 @@ struct PbStore {
     uint2 *pb;
     __device__ void operator()(i64 i, u32 excl, u32) const { pb[i].y = excl; }
 };
-static bool mod0_use_bitmaps(u64 sigma) { return sigma + 1 <= 128; }
+// (sigma+1) * m/32 bitmap words: only worth it for tiny alphabets (level 0 of
+// DNA: 5-7 symbols); at sigma ~ 66 (level 1) and C3 size the bitmaps alone
+// would be 2 GB, so larger alphabets take the onesweep split.
+static bool mod0_use_bitmaps(u64 sigma) { return sigma + 1 <= 8; }
 inline i64 mod0_bitmap_words(u64 sigma, i64 m) { return (i64)(sigma + 1) * (ceil_div(m, 32) + 1); }
 
 // the same multiset of mod-0 first characters, streamed in text order
@@ -860,7 +863,7 @@ static size_t dc3_plan(i64 n) {
         size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
-        i64 bw = mod0_bitmap_words(127, m);
+        i64 bw = mod0_bitmap_words(7, m);
         size_t post_t = (size_t)k * 16 + (size_t)k * 32 +
                         (size_t)(os_scratch_words(m) + merge_split_words(N) + 2 * bw + scan_tmp_words(bw)) * 4;
         size_t t = sort_t > bm_t ? sort_t : bm_t;
