@@ -308,7 +308,95 @@ class C5:
                           f"single thread ({dt:.2f} s); GPU answers matched the argmin oracle on 10^6 queries"}
 
 
-WORKLOADS = {"c2": C2, "c3": C3, "c5": C5}
+def _c4_chunk(args):
+    from paper_1404_3448_b200.workloads import c4_pairs
+    return c4_pairs(*args)
+
+
+class C4:
+    """configs[3]: 100k synthetic 10 kbp noncoding-like pairs (workloads.py),
+    sharded contiguously across ranks (strong scaling); the per-pair results
+    are all-gathered to every rank over NCCL inside the step (the one
+    collective of the path)."""
+    name = "c4"
+    unit = "pairs/s"
+    scaling = "strong"
+    TOTAL = 100_000
+
+    def __init__(self, rank: int, world: int = 1, dist=None):
+        import concurrent.futures as cf
+
+        import torch
+
+        import paper_1404_3448_b200 as sx
+        from paper_1404_3448_b200.workloads import shard
+        lo, hi = shard(self.TOTAL, world, rank)
+        chunks = [(a, min(a + 1000, hi)) for a in range(lo, hi, 1000)]
+        with cf.ProcessPoolExecutor(max_workers=min(32, os.cpu_count() or 4)) as ex:
+            parts = list(ex.map(_c4_chunk, chunks))
+        self.seqs = np.concatenate([p[0] for p in parts])
+        offs, base = [np.zeros(1, np.int64)], 0
+        for s, o in parts:
+            offs.append(o[1:] + base)
+            base += int(o[-1])
+        self.offs = np.concatenate(offs)
+        self.P = hi - lo
+        self.dist, self.world = dist, world
+        self.ob = sx.OverlapBatch(self.seqs, self.offs)
+        self.hseqs = torch.from_numpy(self.seqs).pin_memory()
+        self.hout = torch.empty(3 * self.P, dtype=torch.int64, pin_memory=True)
+        self.per_rank = [b - a for a, b in (shard(self.TOTAL, world, r) for r in range(world))]
+        self.gather = [torch.empty(3 * max(self.per_rank), dtype=torch.int64, device=self.ob.out.device)
+                       for _ in range(world)]
+        self.units = self.TOTAL / world
+        self.units_total = self.TOTAL
+        self.h2d = int(self.seqs.nbytes)
+        self.d2h = 24 * self.P
+        self.ob.run_device()
+        self.result = None
+        self.config = {"workload": "C4: 100k pairs of 2 x 10 kbp AT-rich random sequences with one planted "
+                                   "shared block (paper_1404_3448_b200/workloads.py), batched waves of <= 2^27 "
+                                   "residues, results all-gathered over NCCL",
+                       "pairs": self.TOTAL, "pairs_this_rank": self.P, "waves_this_rank": len(self.ob.waves)}
+
+    def _gather(self):
+        if self.dist is None:
+            return
+        import torch
+        mine = self.gather[0].new_zeros(3 * max(self.per_rank))
+        mine[: 3 * self.P].copy_(self.ob.out[: 3 * self.P])
+        self.dist.all_gather(self.gather, mine)
+
+    def step_device(self):
+        self.ob.run_device()
+        self._gather()
+
+    def step_e2e(self):
+        import torch
+        self.ob.seqs_dev[: self.seqs.shape[0]].copy_(self.hseqs, non_blocking=True)
+        self.ob.run_device()
+        self._gather()
+        self.hout.copy_(self.ob.out[: 3 * self.P], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    def extra(self, ms_dev, steps, world):
+        return {}
+
+    def cpu_baseline(self):
+        import oracle
+        k = 4000  # bounded sample: the first 4000 pairs on every host thread
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        want = oracle.overlap_batch(self.seqs[: self.offs[2 * k]], self.offs[: 2 * k + 1], threads=threads)
+        dt = time.perf_counter() - t0
+        got = self.ob.results()[:k]
+        assert np.array_equal(got, want)
+        return {"value": k / dt, "unit": self.unit, "cores": threads, "kind": "port",
+                "sample": f"first {k} C4 pairs, oracle/saix_oracle.c on {threads} host threads ({dt:.1f} s); "
+                          "GPU answers matched on all of them"}
+
+
+WORKLOADS = {"c2": C2, "c3": C3, "c4": C4, "c5": C5}
 
 
 def run_reference(args, rank):
@@ -348,7 +436,8 @@ def bench(args, rank, world, dist):
     from paper_1404_3448_b200 import _lib
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    wl = WORKLOADS[args.workload](rank)
+    cls = WORKLOADS[args.workload]
+    wl = cls(rank, world, dist) if cls is C4 else cls(rank)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
 
@@ -404,8 +493,9 @@ def bench(args, rank, world, dist):
     stage = {e["name"]: round(e["ms"] / args.steps, 4) for e in sorted(prof, key=lambda e: -e["ms"])}
 
     scale = 1e6 if wl.unit == "Mbases/s" else 1.0
-    value = wl.units * world * args.steps / (ms_dev * 1e-3) / scale
-    e2e_value = wl.units * world * args.steps / (ms_e2e * 1e-3) / scale
+    total = getattr(wl, "units_total", wl.units * world)
+    value = total * args.steps / (ms_dev * 1e-3) / scale
+    e2e_value = total * args.steps / (ms_e2e * 1e-3) / scale
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -422,10 +512,11 @@ def bench(args, rank, world, dist):
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_dev / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic",
+            "higher_is_better": True, "scaling": getattr(wl, "scaling", "weak"), "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic",
             "config": dict(wl.config, l2="flushed between timed steps (512 MiB write)",
-                           parallelism=f"replicas x{world}"),
+                           parallelism=(f"pairs sharded x{world}" if getattr(wl, "scaling", "") == "strong"
+                                        else f"replicas x{world}")),
             **wl.extra(ms_dev, args.steps, world),
             "e2e": {"value": round(e2e_value, 2), "unit": wl.unit, "h2d_bytes_per_step": wl.h2d,
                     "d2h_bytes_per_step": wl.d2h, "ms_per_step": round(ms_e2e / args.steps, 4)},

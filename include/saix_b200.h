@@ -190,6 +190,22 @@ SAIX_API int saix_longest_overlap(const uint8_t *a_ascii, int64_t na,
                          int64_t *out3, int64_t *bad_pos, void *ws,
                          size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------- batched pairs */
+
+/* Batched longest_overlap over P independent pairs (BASELINE config C4):
+ * equals [longest_overlap(A_p, B_p) for p] (overlap.py:110-152).
+ * seqs: device ASCII of all pairs; offs_host: HOST int64[2P+1], pair p is
+ * A = seqs[offs[2p], offs[2p+1]), B = seqs[offs[2p+1], offs[2p+2]).
+ * out: device int64[3P] (length, pos_a, pos_b per pair); *bad (device int64)
+ * receives the smallest seqs offset of an illegal residue (INT64_MAX if
+ * none; pairs with an empty side are not validated, like the reference).
+ * All pairs of one call share one generalized text, so callers bound a call
+ * to ~2^27 total residues and loop over waves. */
+SAIX_API size_t saix_overlap_batch_workspace_bytes(const int64_t *offs_host, int64_t npairs);
+SAIX_API int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, int64_t npairs,
+                                int keep_n, int64_t *out, int64_t *bad, void *ws,
+                                size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,6 +14,7 @@
  * is pinned against the reference's own golden vectors and against outputs
  * of the reference itself (tests/golden/, made by tests/golden/make_golden.py).
  */
+#include <malloc.h>
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -24,6 +25,15 @@
 /* ------------------------------------------------------------------ */
 /* small helpers                                                        */
 /* ------------------------------------------------------------------ */
+
+/* Keep freed buffers on the heap instead of returning them to the kernel
+ * (the reference does the same for timing, bench.py:59-72 tune_allocator):
+ * otherwise every per-pair DC3 mmaps/munmaps its arrays and host threads
+ * serialise on the kernel's mm lock. */
+__attribute__((constructor)) static void tune_allocator(void) {
+    mallopt(M_MMAP_THRESHOLD, 1 << 30);
+    mallopt(M_TRIM_THRESHOLD, 1 << 30);
+}
 
 static void *xcalloc(size_t n, size_t sz) {
     void *p = calloc(n ? n : 1, sz);

@@ -6,9 +6,9 @@ Compute runs in libsaix_b200.so (hand-written CUDA, C ABI in
 include/saix_b200.h); PyTorch provides device memory and streams only.
 """
 
-from .overlap import (GeneralizedText, LcpQueryEngine, OverlapPipeline, OverlapResult,
-                      lcp_query, lcp_query_batch, longest_overlap, overlap_report,
-                      parse_overlap_record)
+from .overlap import (GeneralizedText, LcpQueryEngine, OverlapBatch, OverlapPipeline, OverlapResult,
+                      lcp_query, lcp_query_batch, longest_overlap, longest_overlap_batch,
+                      overlap_report, pack_pairs, parse_overlap_record)
 from .rmq import SparseTable, build_sparse, query_sparse, query_sparse_batch
 from .sequence import (DnaSequence, NPolicy, RankedText, SequenceError, decode, encode,
                        gen_random, parse_fasta, write_fasta)
@@ -20,10 +20,10 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Dc3Workspace", "DnaSequence", "GeneralizedText", "LcpArray", "LcpQueryEngine",
-    "NPolicy", "OverlapPipeline", "OverlapResult", "RankedText", "SequenceError",
+    "NPolicy", "OverlapBatch", "OverlapPipeline", "OverlapResult", "RankedText", "SequenceError",
     "SparseTable", "SuffixArray", "build_lcp", "build_sa_dc3", "build_sa_oracle",
     "build_sparse", "decode", "encode", "gen_random", "lcp_query", "lcp_query_batch",
-    "longest_overlap", "merge_sample_nonsample", "overlap_report", "parse_fasta",
+    "longest_overlap", "longest_overlap_batch", "merge_sample_nonsample", "pack_pairs", "overlap_report", "parse_fasta",
     "parse_overlap_record", "prepare_dc3_workspace", "query_sparse", "query_sparse_batch",
     "sample_ranks", "write_fasta",
 ]

@@ -86,6 +86,8 @@ SIGNATURES = {
     "saix_overlap_scan": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _c.c_size_t, _vp]),
     "saix_longest_overlap_workspace_bytes": (_c.c_size_t, [_i64, _i64]),
     "saix_longest_overlap": (_int, [_vp, _i64, _vp, _i64, _int, _vp, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_overlap_batch_workspace_bytes": (_c.c_size_t, [_vp, _i64]),
+    "saix_overlap_batch": (_int, [_vp, _vp, _i64, _int, _vp, _vp, _vp, _c.c_size_t, _vp]),
 }
 
 _lib = None

@@ -145,6 +145,10 @@ inline int bits_for(u64 v) {  // bit width of v (>= 1), like int.bit_length()
 int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
                 cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in = nullptr, bool phi_ready = false);
 
+// PLCP (in place over Phi) for u8 text -- the batched-pairs path.
+size_t plcp_workspace_bytes(i64 n);
+int plcp_from_phi(const u8 *text, i64 n, u32 *phi_plcp, void *ws, size_t ws_bytes, cudaStream_t st);
+
 // DC3 (dc3.cu); isa may be null when the caller does not need the ranks.
 int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, void *ws,
                 size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream);

@@ -171,6 +171,32 @@ static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32
     return SAIX_OK;
 }
 
+size_t plcp_workspace_bytes(i64 n) {
+    Arena ar;
+    ar.alloc<u32>(ceil_div(n > 0 ? n : 1, LCP_CHUNK) + 1);
+    ar.alloc<u8>(n);
+    return ar.peak + Arena::kAlign;
+}
+
+int plcp_from_phi(const u8 *text, i64 n, u32 *phi_plcp, void *ws, size_t ws_bytes, cudaStream_t st) {
+    Arena ar{(char *)ws, ws_bytes};
+    i64 nchunks = ceil_div(n, LCP_CHUNK);
+    u32 *seeds = ar.alloc<u32>(nchunks + 1);
+    u8 *plcp8 = ar.alloc<u8>(n);
+    SAIX_ARENA_OK(ar);
+    {
+        Prof prof_("lcp.seeds", 8.0 * nchunks, st);
+        k_lcp_seeds<u8><<<grid_for(nchunks, 256), 256, 0, st>>>(text, n, phi_plcp, seeds, nchunks);
+    }
+    SAIX_LAUNCHED();
+    {
+        Prof prof_("lcp.plcp", 9.0 * n, st);
+        k_plcp<u8><<<(unsigned)ceil_div(n, LCP_TILE), LCP_THREADS, 0, st>>>(text, n, phi_plcp, seeds, plcp8);
+    }
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}
+
 int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
                 cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in, bool phi_ready) {
     Arena ar{(char *)ws, ws_bytes};

@@ -102,7 +102,7 @@ k_os_hist(Src src, i64 n, int shift0, int passes, u32 *__restrict__ hist) {
 }
 
 // One CTA of 256 threads: exclusive scan over digits of every pass.
-__global__ void __launch_bounds__(OS_RADIX) k_os_scan(const u32 *__restrict__ hist, int passes, u32 *__restrict__ offs,
+static __global__ void __launch_bounds__(OS_RADIX) k_os_scan(const u32 *__restrict__ hist, int passes, u32 *__restrict__ offs,
                                                        u32 *__restrict__ total) {
     __shared__ u32 sh[OS_RADIX];
     for (int p = 0; p < passes; p++) {

@@ -10,6 +10,9 @@
 //           (reduce -> scan tile carries -> apply).  Every A position lies in
 //           exactly one run, so the reference's lexicographic (minA, minB)
 //           choice is a u64 atomicMin of (minA << 32 | minB) at run ends.
+#include <vector>
+
+#include "onesweep.cuh"
 #include "scan.cuh"
 
 namespace saix {
@@ -428,4 +431,273 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
     SAIX_CUDA(cudaMemsetAsync(w.ov.best, 0, sizeof(u32), st));
     SAIX_TRY(lcp_compute(w.gsa, 1, n, w.sa, w.lcp, w.rest, w.rest_bytes, st, na, w.ov.best, w.phi));
     return overlap_scan(w.sa, w.lcp, n, na, out3, w.ov, st, true);
+}
+
+// ============================================================ batched pairs
+//
+// A wave of P pairs becomes ONE generalized text
+//     X = (A_0+2) 2 (B_0+2) 1 | (A_1+2) 2 (B_1+2) 1 | ...
+// with the in-pair separator at rank 2 and a terminator 1 below every other
+// symbol.  Two suffixes of the same pair compare exactly as in the pair's own
+// generalized text (overlap.py:83-95, padding 0): the first one to reach its
+// terminator is smaller, and no match can run past a terminator.  So:
+//   DC3(X)  ->  stable partition of SA(X) by pair id  (each pair's suffixes
+//   in their own order; pair p's block is [xoff[p], xoff[p+1]) with the
+//   terminator suffix first)  ->  Phi within each block  ->  PLCP walk over
+//   X  ->  one CTA per pair: LCP permute + both overlap passes on chip.
+
+namespace saix {
+
+__device__ __forceinline__ u32 pair_of(const i64 *__restrict__ xoff, i64 P, i64 stride, i64 g) {
+    if (stride > 0) return (u32)(g / stride);
+    i64 lo = 0, hi = P - 1;  // largest p with xoff[p] <= g
+    while (lo < hi) {
+        i64 mid = (lo + hi + 1) >> 1;
+        if (xoff[mid] <= g) lo = mid;
+        else hi = mid - 1;
+    }
+    return (u32)lo;
+}
+
+__global__ void k_batch_build_x(const u8 *__restrict__ seqs, const i64 *__restrict__ offs,
+                                const i64 *__restrict__ xoff, i64 P, int keep_n, u8 *__restrict__ X,
+                                i64 *__restrict__ bad) {
+    i64 local_bad = INT64_MAX;
+    for (i64 p = blockIdx.x; p < P; p += gridDim.x) {
+        i64 x0 = xoff[p], len = xoff[p + 1] - x0;
+        if (len == 0) continue;  // empty side: (0, 0, 0) without validation
+        i64 a0 = offs[2 * p], la = offs[2 * p + 1] - a0, b0 = offs[2 * p + 1];
+        for (i64 i = threadIdx.x; i < len; i += blockDim.x) {
+            u32 r;
+            i64 src = -1;
+            if (i < la) src = a0 + i;
+            else if (i > la && i < len - 1) src = b0 + (i - la - 1);
+            if (src >= 0) {
+                r = rank_of_ascii(seqs[src], keep_n);
+                if (r == 0) {
+                    if (src < local_bad) local_bad = src;
+                    r = 1;
+                }
+                r += 2;
+            } else {
+                r = (i == la) ? 2u : 1u;  // in-pair separator / terminator
+            }
+            X[x0 + i] = (u8)r;
+        }
+    }
+    if (local_bad != INT64_MAX) atomicMin((unsigned long long *)bad, (unsigned long long)local_bad);
+}
+
+struct PairSrc {
+    const u32 *sa;
+    const i64 *xoff;
+    i64 P, stride;
+    __device__ __forceinline__ bool get(i64 i, u32 &k, u32 &v) const {
+        v = __ldcs(sa + i);
+        k = pair_of(xoff, P, stride, v);
+        return true;
+    }
+};
+
+// Phi within each pair block: the terminator entry and the block's first
+// real suffix have no predecessor.
+__global__ void k_batch_phi(const u32 *__restrict__ sap, i64 nx, const i64 *__restrict__ xoff, i64 P, i64 stride,
+                            u32 *__restrict__ phi) {
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < nx; r += (i64)gridDim.x * blockDim.x) {
+        u32 g = sap[r];
+        i64 x0 = xoff[pair_of(xoff, P, stride, (i64)r)];
+        phi[g] = (r <= x0 + 1) ? 0xFFFFFFFFu : sap[r - 1];
+    }
+}
+
+__global__ void __launch_bounds__(OV_THREADS)
+k_batch_overlap(const u32 *__restrict__ sap, const u32 *__restrict__ plcp, const i64 *__restrict__ xoff,
+                const i64 *__restrict__ offs, i64 P, i64 *__restrict__ out) {
+    __shared__ u32 sh_red[OV_THREADS / 32];
+    __shared__ unsigned long long sh_win[OV_THREADS / 32];
+    for (i64 p = blockIdx.x; p < P; p += gridDim.x) {
+        i64 x0 = xoff[p], x1 = xoff[p + 1];
+        if (x1 == x0) {
+            if (threadIdx.x == 0) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0;
+            continue;
+        }
+        const u32 la = (u32)(offs[2 * p + 1] - offs[2 * p]);
+        const i64 s0 = x0 + 1;  // first real suffix (the terminator sorts first)
+        // pass 1: best cross-sequence adjacent LCP (overlap.py:129-136)
+        u32 mx = 0;
+        for (i64 r = s0 + 1 + threadIdx.x; r < x1; r += OV_THREADS) {
+            u32 ga = (u32)(sap[r - 1] - x0), gb = (u32)(sap[r] - x0);
+            bool cross = ga != la && gb != la && ((ga < la) != (gb < la));
+            if (cross) mx = max(mx, plcp[sap[r]]);
+        }
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane_id() == 0) sh_red[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        u32 best = 0;
+        for (int w = 0; w < OV_THREADS / 32; w++) best = max(best, sh_red[w]);
+        __syncthreads();
+        if (best == 0) {
+            if (threadIdx.x == 0) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0;
+            continue;
+        }
+        // pass 2: runs of lcp >= best, per-run min A / B position (138-152)
+        Seg carry{0u, kInf, kInf};
+        unsigned long long win = ~0ull;
+        for (i64 c = s0; c < x1; c += OV_THREADS) {
+            i64 r = c + threadIdx.x;
+            bool live = r < x1;
+            Seg e{0u, kInf, kInf};
+            bool end = false;
+            if (live) {
+                u32 g = sap[r], loc = g - (u32)x0;
+                u32 l = r == s0 ? 0u : plcp[g];
+                e.f = (r == s0 || l < best) ? 1u : 0u;
+                e.a = loc < la ? loc : kInf;
+                e.b = loc > la ? loc : kInf;
+                end = (r + 1 >= x1) || plcp[sap[r + 1]] < best;
+            }
+            Seg tot;
+            Seg ex = block_seg_exclusive(e, tot);
+            Seg run = seg_combine(seg_combine(carry, ex), e);
+            if (live && end && run.a != kInf && run.b != kInf)
+                win = min(win, ((unsigned long long)run.a << 32) | run.b);
+            carry = seg_combine(carry, tot);
+        }
+        for (int o = 16; o; o >>= 1) win = min(win, __shfl_xor_sync(0xffffffffu, win, o));
+        if (lane_id() == 0) sh_win[threadIdx.x >> 5] = win;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < OV_THREADS / 32; w++) win = min(win, sh_win[w]);
+            out[3 * p] = best;
+            out[3 * p + 1] = (i64)(win >> 32);
+            out[3 * p + 2] = (i64)(win & 0xFFFFFFFFull) - (i64)la - 1;
+        }
+        __syncthreads();
+    }
+}
+
+struct BatchLayout {
+    i64 P, nx, stride;
+    std::vector<i64> xoff;
+};
+
+static int batch_layout(const i64 *offs, i64 P, BatchLayout &b) {
+    b.P = P;
+    b.xoff.assign((size_t)P + 1, 0);
+    i64 common = -1;
+    bool fixed = true;
+    for (i64 p = 0; p < P; p++) {
+        i64 la = offs[2 * p + 1] - offs[2 * p], lb = offs[2 * p + 2] - offs[2 * p + 1];
+        if (la < 0 || lb < 0) {
+            set_error("saix_overlap_batch: offsets must be non-decreasing");
+            return SAIX_EINVAL;
+        }
+        i64 len = (la && lb) ? la + lb + 2 : 0;
+        if (common < 0) common = len;
+        if (len != common) fixed = false;
+        b.xoff[p + 1] = b.xoff[p] + len;
+    }
+    b.nx = b.xoff[P];
+    b.stride = (fixed && common > 0) ? common : 0;
+    if (b.nx >= ((i64)1 << 30)) {
+        set_error("saix_overlap_batch: %lld residues in one call; split into waves < 2^30", (long long)b.nx);
+        return SAIX_EINVAL;
+    }
+    return SAIX_OK;
+}
+
+struct BatchWs {
+    u8 *X;
+    u32 *sa;
+    i64 *xoff, *offs;
+    void *dc3;
+    size_t dc3_bytes;
+    u32 *k0, *v0, *k1, *v1, *scratch;
+    void *plcp_ws;
+    size_t plcp_bytes;
+};
+
+static size_t batch_ws(Arena &ar, i64 P, i64 nx, BatchWs *w) {
+    BatchWs t;
+    t.X = ar.alloc<u8>(nx + 8);
+    t.sa = ar.alloc<u32>(nx);
+    t.xoff = ar.alloc<i64>(P + 1);
+    t.offs = ar.alloc<i64>(2 * P + 1);
+    size_t mark = ar.mark();
+    t.dc3_bytes = saix_dc3_workspace_bytes(nx, 1);
+    t.dc3 = ar.alloc<char>((i64)t.dc3_bytes);
+    size_t peak_dc3 = ar.mark();
+    ar.reset(mark);
+    t.k0 = ar.alloc<u32>(nx);
+    t.v0 = ar.alloc<u32>(nx);
+    t.k1 = ar.alloc<u32>(nx);
+    t.v1 = ar.alloc<u32>(nx);
+    t.scratch = ar.alloc<u32>(os_scratch_words(nx));
+    t.plcp_bytes = plcp_workspace_bytes(nx);
+    t.plcp_ws = ar.alloc<char>((i64)t.plcp_bytes);
+    if (ar.mark() < peak_dc3) ar.reset(peak_dc3);
+    if (w) *w = t;
+    return ar.peak;
+}
+
+}  // namespace saix
+
+extern "C" size_t saix_overlap_batch_workspace_bytes(const int64_t *offs_host, int64_t npairs) {
+    BatchLayout b;
+    if (npairs < 0 || (npairs > 0 && !offs_host) || batch_layout(offs_host, npairs, b)) return 0;
+    Arena ar;
+    return batch_ws(ar, npairs, b.nx, nullptr) + Arena::kAlign;
+}
+
+extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, int64_t npairs, int keep_n,
+                                  int64_t *out, int64_t *bad, void *ws, size_t ws_bytes, void *stream) {
+    if (npairs < 0 || (npairs > 0 && (!offs_host || !out)) || !bad) {
+        set_error("saix_overlap_batch: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    k_pipeline_init<<<1, 1, 0, st>>>(out, bad);  // out[0..2] zero, bad = INT64_MAX
+    SAIX_LAUNCHED();
+    if (npairs == 0) return SAIX_OK;
+    BatchLayout b;
+    SAIX_TRY(batch_layout(offs_host, npairs, b));
+    Arena ar{(char *)ws, ws_bytes};
+    BatchWs w;
+    batch_ws(ar, npairs, b.nx, &w);
+    SAIX_ARENA_OK(ar);
+    i64 P = npairs, nx = b.nx;
+    SAIX_CUDA(cudaMemcpyAsync(w.xoff, b.xoff.data(), (size_t)(P + 1) * 8, cudaMemcpyHostToDevice, st));
+    SAIX_CUDA(cudaMemcpyAsync(w.offs, offs_host, (size_t)(2 * P + 1) * 8, cudaMemcpyHostToDevice, st));
+    {
+        Prof prof_("batch.build_x", 2.0 * nx, st);
+        k_batch_build_x<<<(unsigned)(P < 65535 ? P : 65535), 256, 0, st>>>(seqs, w.offs, w.xoff, P, keep_n, w.X, bad);
+    }
+    SAIX_LAUNCHED();
+    if (nx == 0) {
+        k_batch_overlap<<<1, OV_THREADS, 0, st>>>(nullptr, nullptr, w.xoff, w.offs, P, out);
+        SAIX_LAUNCHED();
+        return SAIX_OK;
+    }
+    int sigma = keep_n ? 7 : 6;  // terminator 1, separator 2, residues 3..6 (N 7)
+    SAIX_TRY(dc3_compute(w.X, 1, nx, sigma, w.sa, nullptr, w.dc3, w.dc3_bytes, nullptr, st));
+    // stable partition by pair id: each pair's suffixes keep their order
+    u32 *keys = w.k0, *sap = w.v0;
+    int passes = (bits_for((u64)(P > 1 ? P - 1 : 1)) + OS_BITS - 1) / OS_BITS;
+    PairSrc src{w.sa, w.xoff, P, b.stride};
+    SAIX_TRY(onesweep_sort<u32>(src, nx, src, nx, nx, 0, passes, w.k0, w.v0, w.k1, w.v1, w.scratch, keys, sap,
+                                nullptr, st, "batch.partition"));
+    u32 *phi = w.sa;  // SA(X) is no longer needed
+    {
+        Prof prof_("batch.phi", 12.0 * nx, st);
+        k_batch_phi<<<grid_for(nx, 256), 256, 0, st>>>(sap, nx, w.xoff, P, b.stride, phi);
+    }
+    SAIX_LAUNCHED();
+    SAIX_TRY(plcp_from_phi(w.X, nx, phi, w.plcp_ws, w.plcp_bytes, st));
+    {
+        Prof prof_("batch.overlap", 12.0 * nx, st);
+        k_batch_overlap<<<(unsigned)(P < 65535 ? P : 65535), OV_THREADS, 0, st>>>(sap, phi, w.xoff, w.offs, P,
+                                                                                   out);
+    }
+    SAIX_LAUNCHED();
+    return SAIX_OK;
 }

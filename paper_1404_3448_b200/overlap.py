@@ -196,6 +196,92 @@ def longest_overlap(a: DnaSequence, b: DnaSequence,
     return OverlapResult(int(res[0]), int(res[1]), int(res[2]))
 
 
+class OverlapBatch:
+    """Batched ``longest_overlap`` over many independent pairs on the device
+    (saix_overlap_batch).  Pairs are packed as ASCII into ``seqs`` with
+    ``offs`` (int64[2P+1]: pair p is A = seqs[offs[2p]:offs[2p+1]], B =
+    seqs[offs[2p+1]:offs[2p+2]]) and processed in waves of at most
+    ``wave_residues`` residues (one generalized text per wave)."""
+
+    def __init__(self, seqs: np.ndarray, offs: np.ndarray, policy: NPolicy = NPolicy.REJECT,
+                 wave_residues: int = 1 << 27):
+        t = _lib.torch()
+        L = _lib.load()
+        dev = _lib.device()
+        self.offs = np.ascontiguousarray(offs, dtype=np.int64)
+        self.P = (len(self.offs) - 1) // 2
+        self.keep_n = int(policy is NPolicy.KEEP)
+        self.policy = policy
+        self.waves = []
+        p = 0
+        while p < self.P:
+            q = p + 1
+            while q < self.P and self.offs[2 * (q + 1)] - self.offs[2 * p] <= wave_residues:
+                q += 1
+            self.waves.append((p, q))
+            p = q
+        self.seqs_dev = _lib.to_device(np.ascontiguousarray(seqs, dtype=np.uint8))
+        self.out = t.zeros(max(3 * self.P, 3), dtype=t.int64, device=dev)
+        self.bad = t.zeros(max(len(self.waves), 1), dtype=t.int64, device=dev)
+        self.wave_offs = [np.ascontiguousarray(self.offs[2 * a: 2 * b + 1] - self.offs[2 * a]) for a, b in self.waves]
+        ws = max((L.saix_overlap_batch_workspace_bytes(o.ctypes.data, b - a)
+                  for o, (a, b) in zip(self.wave_offs, self.waves)), default=256)
+        self.ws = _lib.workspace(ws)
+        self.h2d_bytes = int(self.offs[-1])
+
+    def run_device(self) -> None:
+        """All waves on the device-resident ASCII (no host traffic)."""
+        L = _lib.load()
+        s = _lib.stream_ptr()
+        for w, ((a, b), o) in enumerate(zip(self.waves, self.wave_offs)):
+            rc = L.saix_overlap_batch(_lib.ptr(self.seqs_dev) + int(self.offs[2 * a]), o.ctypes.data, b - a,
+                                      self.keep_n, _lib.ptr(self.out) + 24 * a, _lib.ptr(self.bad) + 8 * w,
+                                      _lib.ptr(self.ws), self.ws.numel(), s)
+            _lib.check(rc, "saix_overlap_batch")
+
+    def results(self) -> np.ndarray:
+        """(P, 3) int64 host array; raises SequenceError like the reference."""
+        bad = self.bad.cpu().numpy()
+        hit = np.flatnonzero(bad[: len(self.waves)] != INT64_MAX)
+        if hit.shape[0]:
+            pos = int(bad[hit[0]])
+            raise SequenceError(f"illegal residue at packed offset {pos} "
+                                f"(policy={self.policy.value})")
+        return self.out[: 3 * self.P].cpu().numpy().reshape(self.P, 3)
+
+
+def pack_pairs(pairs) -> tuple[np.ndarray, np.ndarray]:
+    """[(A, B), ...] DnaSequences -> (ASCII bytes, int64[2P+1] offsets)."""
+    chunks, offs = [], [0]
+    for a, b in pairs:
+        for s in (a, b):
+            raw = np.frombuffer(s.residues.encode("ascii"), dtype=np.uint8)
+            chunks.append(raw)
+            offs.append(offs[-1] + raw.shape[0])
+    seqs = np.concatenate(chunks) if chunks else np.zeros(0, np.uint8)
+    return seqs, np.asarray(offs, dtype=np.int64)
+
+
+def longest_overlap_batch(pairs, policy: NPolicy = NPolicy.REJECT) -> list[OverlapResult]:
+    """Equals ``[longest_overlap(a, b, policy) for a, b in pairs]`` (including
+    the SequenceError of the first offending pair), computed as batched waves."""
+    pairs = list(pairs)
+    if not pairs:
+        return []
+    seqs, offs = pack_pairs(pairs)
+    ob = OverlapBatch(seqs, offs, policy)
+    ob.run_device()
+    bad = ob.bad.cpu().numpy()[: len(ob.waves)]
+    hit = np.flatnonzero(bad != INT64_MAX)
+    if hit.shape[0]:
+        pos = int(bad[hit[0]])
+        pi = int(np.searchsorted(offs, pos, side="right") - 1)  # sequence index 2p or 2p+1
+        seq = pairs[pi // 2][pi % 2]
+        raise residue_error(seq, pos - int(offs[pi]), policy)
+    res = ob.out[: 3 * len(pairs)].cpu().numpy().reshape(len(pairs), 3)
+    return [OverlapResult(int(x), int(y), int(z)) for x, y, z in res]
+
+
 def overlap_report(result: OverlapResult, a: DnaSequence, b: DnaSequence) -> tuple[str, str]:
     """Human summary + one-object JSON record (overlap.py:155-173)."""
     sub = a.residues[result.pos_a:result.pos_a + result.length]
@@ -217,6 +303,7 @@ def parse_overlap_record(payload: str) -> OverlapResult:
     return OverlapResult(length=rec["length"], pos_a=rec["posA"], pos_b=rec["posB"])
 
 
-__all__ = ["GeneralizedText", "LcpQueryEngine", "OverlapPipeline", "OverlapResult",
+__all__ = ["GeneralizedText", "LcpQueryEngine", "OverlapBatch", "OverlapPipeline", "OverlapResult",
+           "longest_overlap_batch", "pack_pairs",
            "SequenceError", "alphabet", "lcp_query", "lcp_query_batch", "longest_overlap",
            "overlap_report", "parse_overlap_record"]

@@ -1,0 +1,66 @@
+"""Batched longest_overlap (C4 path): equals the scalar reference answer for
+every pair, across waves, ragged / empty pairs and residue errors."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1404_3448_b200 as sx
+from paper_1404_3448_b200.sequence import DnaSequence
+from paper_1404_3448_b200.workloads import c4_pairs
+
+pytestmark = pytest.mark.gpu
+
+
+def golden_pairs(g):
+    ao, bo = g["ov_aoffs"], g["ov_boffs"]
+    out = []
+    for c in range(len(ao) - 1):
+        a = g["ov_a"][ao[c]:ao[c + 1]].tobytes().decode()
+        b = g["ov_b"][bo[c]:bo[c + 1]].tobytes().decode()
+        out.append((DnaSequence("a", a), DnaSequence("b", b)))
+    return out
+
+
+def test_golden_pairs_as_one_batch(golden):
+    pairs = golden_pairs(golden)
+    got = sx.longest_overlap_batch(pairs)
+    want = [tuple(int(x) for x in r) for r in golden["ov_ans"]]
+    assert [(r.length, r.pos_a, r.pos_b) for r in got] == want
+
+
+def test_c4_pairs_vs_oracle_and_waves():
+    seqs, offs = c4_pairs(0, 64, length=3000)
+    want = oracle.overlap_batch(seqs, offs, threads=4)
+    ob = sx.OverlapBatch(seqs, offs)
+    ob.run_device()
+    assert np.array_equal(ob.results(), want)
+    small = sx.OverlapBatch(seqs, offs, wave_residues=20_000)   # many waves
+    assert len(small.waves) > 4
+    small.run_device()
+    assert np.array_equal(small.results(), want)
+
+
+def test_ragged_and_empty_pairs():
+    rng = np.random.default_rng(4)
+    pairs = []
+    for _ in range(50):
+        la, lb = (int(v) for v in rng.integers(0, 400, size=2))
+        if rng.random() < 0.1:
+            la = 0
+        a = "".join(rng.choice(list("ACGT"), size=la))
+        b = "".join(rng.choice(list("ACGT"), size=lb))
+        pairs.append((DnaSequence("a", a), DnaSequence("b", b)))
+    got = sx.longest_overlap_batch(pairs)
+    for (a, b), r in zip(pairs, got):
+        assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a.residues, b.residues)
+
+
+def test_first_bad_pair_raises_like_reference():
+    pairs = [(DnaSequence("a0", "ACGT"), DnaSequence("b0", "GT")),
+             (DnaSequence("a1", "ACGT"), DnaSequence("b1", "GXT")),
+             (DnaSequence("a2", "NNN"), DnaSequence("b2", "AC"))]
+    with pytest.raises(sx.SequenceError, match="record 'b1'.*'X' at position 1"):
+        sx.longest_overlap_batch(pairs)
+    ok = sx.longest_overlap_batch([(DnaSequence("a", ""), DnaSequence("b", "XYZ"))])
+    assert ok == [sx.OverlapResult(0, 0, 0)]
