@@ -13,15 +13,15 @@
 // Steps per level (reference lines):
 //   1 naming  (_name_triples 221-253): dense names of sample triples, either
 //             by a presence bitmap over the (sigma+1)^3 code space when that
-//             is small (levels 0-1 on DNA: no sort at all) or by an LSD radix
-//             sort of packed triple keys + adjacent-difference scan.
+//             is small (levels 0-1 on DNA: no sort at all) or by an onesweep
+//             LSD radix sort of packed triple keys + adjacent-difference scan.
 //   2 recurse (_sort_samples 256-271) iff distinct < m.
 //   3 mod-0   (_sort_nonsamples 274-290): mod-1 samples in rank order, one
 //             position left, stably split by first character.
 //   4 merge   (_merge_walk 173-218): merge-path partition with the DC3
 //             comparator, ISA scattered in the same kernel.
 #include "onesweep.cuh"
-#include "radix.cuh"
+#include "scan.cuh"
 
 namespace saix {
 
@@ -76,35 +76,6 @@ __global__ void k_bitmap_name(Text<TT> T, SampleLayout L, u64 s1, const u32 *__r
         u32 w = (u32)(code >> 5);
         u32 below = bm[w] & ((1u << (code & 31)) - 1u);
         tt[s] = (OT)(wp[w] + __popc(below) + 1u);
-    }
-}
-
-template <typename TT>
-__global__ void k_triple_keys(Text<TT> T, SampleLayout L, int b, u64 *__restrict__ keys,
-                              u32 *__restrict__ vals) {
-    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < L.m; s += (i64)gridDim.x * blockDim.x) {
-        i64 p = L.pos(s);
-        keys[s] = ((u64)T(p) << (2 * b)) | ((u64)T(p + 1) << b) | (u64)T(p + 2);
-        vals[s] = (u32)s;
-    }
-}
-
-// wide alphabets (3 * bits(sigma) > 64): sort by the third char first ...
-template <typename TT>
-__global__ void k_third_char_keys(Text<TT> T, SampleLayout L, u64 *__restrict__ keys,
-                                  u32 *__restrict__ vals) {
-    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < L.m; s += (i64)gridDim.x * blockDim.x) {
-        keys[s] = T(L.pos(s) + 2);
-        vals[s] = (u32)s;
-    }
-}
-// ... then stably by the first two chars, gathered through the permutation.
-template <typename TT>
-__global__ void k_first_two_keys(Text<TT> T, SampleLayout L, int b, const u32 *__restrict__ vals,
-                                 u64 *__restrict__ keys) {
-    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < L.m; i += (i64)gridDim.x * blockDim.x) {
-        i64 p = L.pos(vals[i]);
-        keys[i] = ((u64)T(p) << b) | (u64)T(p + 1);
     }
 }
 
@@ -189,20 +160,57 @@ struct Mod0HistSrc {
     }
 };
 
+// wide-alphabet naming sources (3 bits(sigma) > 64)
+template <typename TT>
+struct ThirdSrc {
+    Text<TT> T;
+    SampleLayout L;
+    __device__ __forceinline__ bool get(i64 s, u64 &k, u32 &v) const {
+        k = T(L.pos(s) + 2);
+        v = (u32)s;
+        return true;
+    }
+};
+template <typename TT>
+struct PairGatherSrc {  // (c0, c1) of the sample at sorted slot i
+    Text<TT> T;
+    SampleLayout L;
+    const u32 *order;
+    u64 s1;
+    __device__ __forceinline__ bool get(i64 i, u64 &k, u32 &v) const {
+        v = order[i];
+        i64 p = L.pos(v);
+        k = (u64)T(p) * s1 + T(p + 1);
+        return true;
+    }
+};
+template <typename TT>
+struct PairStreamSrc {  // the same keys in sample order (histogram)
+    Text<TT> T;
+    SampleLayout L;
+    u64 s1;
+    __device__ __forceinline__ bool get(i64 s, u64 &k, u32 &v) const {
+        i64 p = L.pos(s);
+        k = (u64)T(p) * s1 + T(p + 1);
+        v = 0;
+        return true;
+    }
+};
+template <typename TT>
+struct FlagWide {  // new name iff (c0, c1) key or c2 differs from the predecessor
+    Text<TT> T;
+    SampleLayout L;
+    const u64 *keys;
+    const u32 *vals;
+    __device__ u32 operator()(i64 i) const {
+        if (i == 0 || keys[i] != keys[i - 1]) return 1u;
+        return T(L.pos(vals[i]) + 2) != T(L.pos(vals[i - 1]) + 2) ? 1u : 0u;
+    }
+};
+
 struct FlagPacked {
     const u64 *keys;
     __device__ u32 operator()(i64 i) const { return (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u; }
-};
-template <typename TT>
-struct FlagGather {
-    Text<TT> T;
-    SampleLayout L;
-    const u32 *vals;
-    __device__ u32 operator()(i64 i) const {
-        if (i == 0) return 1u;
-        i64 p = L.pos(vals[i]), q = L.pos(vals[i - 1]);
-        return (T(p) != T(q) || T(p + 1) != T(q + 1) || T(p + 2) != T(q + 2)) ? 1u : 0u;
-    }
 };
 // number of distinct keys in a sorted array (heads of equal-key runs)
 __global__ void k_count_distinct(const u64 *__restrict__ keys, i64 m, u32 *__restrict__ count) {
@@ -238,27 +246,6 @@ __global__ void k_unique_from_sorted(const u32 *__restrict__ vals, i64 m, u32 *_
 }
 
 // ------------------------------------------------------------ mod-0 order
-
-template <typename TT>
-struct Mod1Flag {
-    const u32 *sac;
-    i64 m1;
-    __device__ u32 operator()(i64 i) const { return sac[i] < (u32)m1 ? 1u : 0u; }
-};
-template <typename TT>
-struct Mod0Emit {
-    Text<TT> T;
-    const u32 *sac;
-    u32 *keys;
-    u32 *vals;
-    __device__ void operator()(i64 i, u32 excl, u32 v) const {
-        if (v) {
-            u32 s = sac[i];
-            keys[excl] = T(3 * (i64)s);
-            vals[excl] = s;
-        }
-    }
-};
 
 // ------------------------------------------------------------ merge
 
@@ -690,8 +677,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         int b = bits_for(sigma);
         u64 *k0 = ar.alloc<u64>(m), *k1 = ar.alloc<u64>(m);
         u32 *v0 = ar.alloc<u32>(m), *v1 = ar.alloc<u32>(m);
-        u32 *scratch = ar.alloc<u32>(radix_scratch_words(m) > os_scratch_words(m) ? radix_scratch_words(m)
-                                                                                  : os_scratch_words(m));
+        u32 *scratch = ar.alloc<u32>(os_scratch_words(m));
         u32 *tmp = ar.alloc<u32>(scan_tmp_words(m));
         SAIX_ARENA_OK(ar);
         u64 *keys = k0;
@@ -717,16 +703,21 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
                 SAIX_TRY(scan_transform(FlagPacked{keys}, ScatterName{vals, tt}, m, tmp, nullptr, st,
                                         "dc3.name_scan", 16.0 * m));
         } else {
-            k_third_char_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, k0, v0);
-            SAIX_LAUNCHED();
-            SAIX_TRY(radix_sort_pairs<u64>(keys, vals, k1, v1, m, 0, b, scratch, st));
-            u64 *ka = keys == k0 ? k1 : k0;
-            k_first_two_keys<TT><<<g, K_THREADS, 0, st>>>(T, L, b, vals, ka);
-            SAIX_LAUNCHED();
-            keys = ka;
-            SAIX_TRY(radix_sort_pairs<u64>(keys, vals, keys == k0 ? k1 : k0, vals == v0 ? v1 : v0, m, 0,
-                                           2 * b, scratch, st));
-            SAIX_TRY(scan_transform(FlagGather<TT>{T, L, vals}, ScatterName{vals, tt}, m, tmp, d_scal, st));
+            // wide alphabet: stable sort by the third character, then stably
+            // by the mixed-radix pair of the first two (LSD over components)
+            u64 s1 = sigma + 1;
+            ThirdSrc<TT> src1{T, L};
+            SAIX_TRY(onesweep_sort<u64>(src1, m, src1, m, m, 0, (b + OS_BITS - 1) / OS_BITS, k0, v0, k1, v1,
+                                        scratch, keys, vals, nullptr, st, "dc3.triple_sort"));
+            PairGatherSrc<TT> src2{T, L, vals, s1};
+            PairStreamSrc<TT> hsrc2{T, L, s1};
+            int kb2 = bits_for(s1 * s1 - 1);
+            u64 *ok0 = keys == k0 ? k1 : k0;   // pass 0 must not overwrite its source
+            u32 *ov0 = vals == v0 ? v1 : v0;
+            SAIX_TRY(onesweep_sort<u64>(src2, m, hsrc2, m, m, 0, (kb2 + OS_BITS - 1) / OS_BITS, ok0, ov0, keys, vals,
+                                        scratch, keys, vals, nullptr, st, "dc3.triple_sort"));
+            SAIX_TRY(scan_transform(FlagWide<TT>{T, L, keys, vals}, ScatterName{vals, tt}, m, tmp, d_scal, st,
+                                    "dc3.name_scan", 24.0 * m));
             SAIX_TRY(read_u32(d_scal, &D, st));
         }
         sorted_vals = vals;
@@ -859,7 +850,7 @@ static size_t dc3_plan(i64 n) {
         SampleLayout L = SampleLayout::of(N);
         i64 m = L.m, k = L.k;
         persistent += (size_t)(3 * m + 8) * 4 + 4 * Arena::kAlign;
-        i64 sw = radix_scratch_words(m) > os_scratch_words(m) ? radix_scratch_words(m) : os_scratch_words(m);
+        i64 sw = os_scratch_words(m);
         size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
