@@ -345,9 +345,6 @@ class C4:
         self.ob = sx.OverlapBatch(self.seqs, self.offs)
         self.hseqs = torch.from_numpy(self.seqs).pin_memory()
         self.hout = torch.empty(3 * self.P, dtype=torch.int64, pin_memory=True)
-        self.per_rank = [b - a for a, b in (shard(self.TOTAL, world, r) for r in range(world))]
-        self.gather = [torch.empty(3 * max(self.per_rank), dtype=torch.int64, device=self.ob.out.device)
-                       for _ in range(world)]
         self.units = self.TOTAL / world
         self.units_total = self.TOTAL
         self.h2d = int(self.seqs.nbytes)
@@ -362,10 +359,8 @@ class C4:
     def _gather(self):
         if self.dist is None:
             return
-        import torch
-        mine = self.gather[0].new_zeros(3 * max(self.per_rank))
-        mine[: 3 * self.P].copy_(self.ob.out[: 3 * self.P])
-        self.dist.all_gather(self.gather, mine)
+        from paper_1404_3448_b200.distributed import gather_results
+        self.full = gather_results(self.ob.out[: 3 * self.P], self.TOTAL, self.world, self.dist)
 
     def step_device(self):
         self.ob.run_device()

@@ -39,8 +39,4 @@ def c4_pairs(p0: int, p1: int, length: int = C4_LEN) -> tuple[np.ndarray, np.nda
     offs = np.arange(2 * n + 1, dtype=np.int64) * length
     return seqs, offs
 
-
-def shard(total: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous shard [lo, hi) of `total` independent pairs for `rank`
-    (GPU g gets pairs [g P/G, (g+1) P/G))."""
-    return total * rank // world, total * (rank + 1) // world
+from .distributed import shard  # noqa: E402,F401  (re-exported for bench.py)
