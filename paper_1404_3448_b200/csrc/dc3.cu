@@ -20,6 +20,7 @@
 //             position left, stably split by first character.
 //   4 merge   (_merge_walk 173-218): merge-path partition with the DC3
 //             comparator, ISA scattered in the same kernel.
+#include "bsort.cuh"
 #include "onesweep.cuh"
 #include "scan.cuh"
 
@@ -159,6 +160,35 @@ struct Mod0HistSrc {
         return true;
     }
 };
+
+// bucket-sort sources (large alphabets, bsort.cuh): bucket = leading char
+template <typename TT>
+struct TripleBucketSrc {
+    Text<TT> T;
+    SampleLayout L;
+    u64 s1;
+    __device__ __forceinline__ void get(i64 s, u32 &b, u64 &k, u32 &v) const {
+        i64 p = L.pos(s);
+        u32 c0 = T(p);
+        b = c0;
+        k = ((u64)c0 * s1 + T(p + 1)) * s1 + T(p + 2);
+        v = (u32)s;
+    }
+};
+// mod-0 suffix 3j keyed by (T(3j), R(3j+1)); streamed in text order
+template <typename TT>
+struct Mod0BucketSrc {
+    Text<TT> T;
+    const u32 *isac;
+    __device__ __forceinline__ void get(i64 j, u32 &b, u64 &k, u32 &v) const {
+        u32 c = T(3 * j);
+        b = c;
+        k = ((u64)c << 32) | (__ldcs(isac + j) + 1u);
+        v = (u32)j;
+    }
+};
+// bucket sort pays off when the leading alphabet is large and buckets small
+static bool use_bsort(u64 sigma, i64 n) { return sigma + 1 >= 4096 && n / (i64)(sigma + 1) <= 512; }
 
 // wide-alphabet naming sources (3 bits(sigma) > 64)
 template <typename TT>
@@ -677,7 +707,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         int b = bits_for(sigma);
         u64 *k0 = ar.alloc<u64>(m), *k1 = ar.alloc<u64>(m);
         u32 *v0 = ar.alloc<u32>(m), *v1 = ar.alloc<u32>(m);
-        u32 *scratch = ar.alloc<u32>(os_scratch_words(m));
+        u32 *scratch = ar.alloc<u32>(os_scratch_words(m) > bs_scratch_words(L.n + 1) ? os_scratch_words(m)
+                                                                                  : bs_scratch_words(L.n + 1));
         u32 *tmp = ar.alloc<u32>(scan_tmp_words(m));
         SAIX_ARENA_OK(ar);
         u64 *keys = k0;
@@ -687,8 +718,16 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             int kb = bits_for(s1 * s1 * s1 - 1);
             int passes = (kb + OS_BITS - 1) / OS_BITS;
             TripleSrc<TT> src{T, L, s1};
-            SAIX_TRY(onesweep_sort<u64>(src, m, src, m, m, 0, passes, k0, v0, k1, v1, scratch, keys, vals, nullptr,
-                                        st, "dc3.triple_sort"));
+            bool done = false;
+            if (use_bsort(sigma, m)) {
+                SAIX_TRY(bucket_sort(TripleBucketSrc<TT>{T, L, s1}, m, (i64)s1, k0, v0, scratch, done, st,
+                                     "dc3.triple_sort"));
+                keys = k0;
+                vals = v0;
+            }
+            if (!done)
+                SAIX_TRY(onesweep_sort<u64>(src, m, src, m, m, 0, passes, k0, v0, k1, v1, scratch, keys, vals,
+                                            nullptr, st, "dc3.triple_sort"));
             // count distinct triples first: when all are distinct (the last
             // recursion level) the sorted order already is the rank order and
             // the recursion string is never needed
@@ -766,7 +805,8 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     i64 k = L.k;
     u32 *k0 = ar.alloc<u32>(k), *k1 = ar.alloc<u32>(k);
     u32 *v0 = ar.alloc<u32>(k), *v1 = ar.alloc<u32>(k);
-    u32 *scratch = ar.alloc<u32>(os_scratch_words(L.m));
+    u32 *scratch = ar.alloc<u32>(os_scratch_words(L.m) > bs_scratch_words(N + 1) ? os_scratch_words(L.m)
+                                                                                  : bs_scratch_words(N + 1));
     u32 *split = ar.alloc<u32>(merge_split_words(N));
     SAIX_ARENA_OK(ar);
     u32 *keys = k0, *vals = v0;
@@ -785,9 +825,21 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
         k_mod0_place<TT><<<g, K_THREADS, 0, st>>>(T, ISAc, k, wpc, pb, v0);
         SAIX_LAUNCHED();
     } else {
-        int passes = (bits_for(sigma) + OS_BITS - 1) / OS_BITS;
-        SAIX_TRY(onesweep_sort<u32>(Mod0Src<TT>{T, SAc, (u32)L.m1}, L.m, Mod0HistSrc<TT>{T}, k, k, 0, passes, k0,
-                                    v0, k1, v1, scratch, keys, vals, nullptr, st, "dc3.mod0_split"));
+        bool done = false;
+        if (use_bsort(sigma, k)) {
+            // the (char, rank) keys are distinct, so an unstable bucket split
+            // followed by in-bucket sorts gives the exact order
+            u64 *k64 = ar.alloc<u64>(k);
+            SAIX_ARENA_OK(ar);
+            SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc}, k, (i64)sigma + 1, k64, v0, scratch, done, st,
+                                 "dc3.mod0_split"));
+            vals = v0;
+        }
+        if (!done) {
+            int passes = (bits_for(sigma) + OS_BITS - 1) / OS_BITS;
+            SAIX_TRY(onesweep_sort<u32>(Mod0Src<TT>{T, SAc, (u32)L.m1}, L.m, Mod0HistSrc<TT>{T}, k, k, 0, passes,
+                                        k0, v0, k1, v1, scratch, keys, vals, nullptr, st, "dc3.mod0_split"));
+        }
     }
 
     // step 4: merge real samples (skip the padding sample at rank 1) with mod-0
@@ -850,13 +902,13 @@ static size_t dc3_plan(i64 n) {
         SampleLayout L = SampleLayout::of(N);
         i64 m = L.m, k = L.k;
         persistent += (size_t)(3 * m + 8) * 4 + 4 * Arena::kAlign;
-        i64 sw = os_scratch_words(m);
+        i64 sw = os_scratch_words(m) > bs_scratch_words(N + 1) ? os_scratch_words(m) : bs_scratch_words(N + 1);
         size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
         i64 bw = mod0_bitmap_words(7, m);
-        size_t post_t = (size_t)k * 16 + (size_t)k * 32 +
-                        (size_t)(os_scratch_words(m) + merge_split_words(N) + 2 * bw + scan_tmp_words(bw)) * 4;
+        size_t post_t = (size_t)k * 16 + (size_t)k * 32 + (size_t)k * 8 +
+                        (size_t)(sw + merge_split_words(N) + 2 * bw + scan_tmp_words(bw)) * 4;
         size_t t = sort_t > bm_t ? sort_t : bm_t;
         t = t > post_t ? t : post_t;
         t += 8 * Arena::kAlign;

@@ -264,3 +264,20 @@ class TestLongestOverlap:
             b = "".join(b)
             r = sx.longest_overlap(DnaSequence("a", a), DnaSequence("b", b))
             assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a, b)
+
+
+class TestLargeAlphabets:
+    """Bucket-sort naming / mod-0 split (bsort.cuh): small buckets, medium
+    (CTA-sorted) buckets and the oversize-bucket fallback."""
+
+    @pytest.mark.parametrize("n,sigma,hot", [(60_000, 5000, 0.0), (60_000, 5000, 0.05),
+                                             (60_000, 5000, 0.5), (30_000, 70_000, 0.02)])
+    def test_skewed_wide_text_vs_oracle(self, n, sigma, hot):
+        rng = np.random.default_rng(n + sigma)
+        r = rng.integers(1, sigma + 1, size=n)
+        r[rng.random(n) < hot] = 1                      # one hot symbol -> one big bucket
+        t = RankedText(r, sigma)
+        ix = sx.build_sa_dc3(t)
+        sa, rank = oracle.dc3(r, sigma)
+        assert np.array_equal(ix.sa, sa) and np.array_equal(ix.rank, rank)
+        assert np.array_equal(sx.build_lcp(t, ix).lcp, oracle.lcp(r, sa, rank))
