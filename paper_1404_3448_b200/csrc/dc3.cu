@@ -187,8 +187,11 @@ struct Mod0BucketSrc {
         v = (u32)j;
     }
 };
-// bucket sort pays off when the leading alphabet is large and buckets small
-static bool use_bsort(u64 sigma, i64 n) { return sigma + 1 >= 4096 && n / (i64)(sigma + 1) <= 512; }
+// bucket sort pays off when the leading alphabet is large and buckets small;
+// the bucket arrays are sized by the item count (scratch: bs_scratch_words(N+1))
+static bool use_bsort(u64 sigma, i64 n) {
+    return sigma + 1 >= 4096 && (i64)(sigma + 1) <= n && n / (i64)(sigma + 1) <= 512;
+}
 
 // wide-alphabet naming sources (3 bits(sigma) > 64)
 template <typename TT>

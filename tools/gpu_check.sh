@@ -1,0 +1,18 @@
+#!/bin/bash
+# One gpurun session: GPU tests, bench lines, ncu launch list + one full capture.
+# usage: tools/gpu_check.sh TAG [tests] [bench] [ncu]
+TAG=${1:-x}; shift
+O=gpurun_out/$TAG; mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { tail -30 $O/build.log; exit 1; }
+for what in "$@"; do
+  case $what in
+    tests) timeout 1500 python -m pytest tests -m gpu -x -q > $O/tests.log 2>&1; tail -3 $O/tests.log ;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -2 $O/smoke.log ;;
+    c2|c3|c4|c5) timeout 900 python bench.py --workload $what > $O/bench_$what.json 2> $O/bench_$what.err; tail -c 600 $O/bench_$what.json; tail -3 $O/bench_$what.err ;;
+    ref) timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err; cat $O/bench_ref.json ;;
+    ncu_c2) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/c2_launches.csv python tools/profile_once.py c2 > $O/ncu_c2.log 2>&1; python tools/ncu_summary.py $O/c2_launches.csv > $O/c2_launches.txt; head -30 $O/c2_launches.txt ;;
+    ncu_c3) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/c3_launches.csv python tools/profile_once.py 268435456 > $O/ncu_c3.log 2>&1; python tools/ncu_summary.py $O/c3_launches.csv > $O/c3_launches.txt; head -30 $O/c3_launches.txt ;;
+    full_*) K=${what#full_}; timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:$K -c 1 -o $O/full_$K python tools/profile_once.py c2 > $O/ncu_full_$K.log 2>&1; tail -3 $O/ncu_full_$K.log ;;
+  esac
+done
