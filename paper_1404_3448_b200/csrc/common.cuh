@@ -150,8 +150,12 @@ size_t plcp_workspace_bytes(i64 n);
 int plcp_from_phi(const u8 *text, i64 n, u32 *phi_plcp, void *ws, size_t ws_bytes, cudaStream_t st);
 
 // DC3 (dc3.cu); isa may be null when the caller does not need the ranks.
+// phi (nullable): when the top level runs the streaming path without an ISA
+// request, Phi[sa[r]] = sa[r-1] (0xFFFFFFFF at r = 0) is produced by the
+// merge and *phi_done is set.
 int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, void *ws,
-                size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream);
+                size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream, u32 *phi = nullptr,
+                bool *phi_done = nullptr);
 
 // L2 eviction-priority hints (sm_80+ createpolicy / L2::cache_hint): random
 // gather targets that should stay on chip are loaded / stored evict_last,

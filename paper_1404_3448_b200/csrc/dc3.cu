@@ -22,6 +22,7 @@
 //             comparator, ISA scattered in the same kernel.
 #include "bsort.cuh"
 #include "onesweep.cuh"
+#include "pscatter.cuh"
 #include "scan.cuh"
 
 namespace saix {
@@ -273,7 +274,7 @@ __global__ void k_unique_from_sorted(const u32 *__restrict__ vals, i64 m, u32 *_
                                      u32 *__restrict__ isac) {
     for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (i64)gridDim.x * blockDim.x) {
         u32 s = vals[r];
-        sac[r] = s;
+        if (sac) sac[r] = s;
         isac[s] = (u32)r;
     }
 }
@@ -485,6 +486,8 @@ struct MergeIdx {
     __device__ __forceinline__ MRec rec(i64 p) const {
         return EC.E ? EC.rec(p) : rec_from_eblock<TT>(E, p, l2_evict_last());
     }
+    __device__ __forceinline__ MRec reca(i64 i) const { return rec(apos(i)); }
+    __device__ __forceinline__ MRec recb(i64 j) const { return rec(bpos(j)); }
 };
 // Merge inputs given as positions with a by-position rank array
 // (merge_sample_nonsample, suffix_index.py:452-457).
@@ -498,6 +501,8 @@ struct MergePos {
     __device__ __forceinline__ i64 apos_cs(i64 i) const { return A[i]; }
     __device__ __forceinline__ i64 bpos_cs(i64 j) const { return B[j]; }
     __device__ __forceinline__ MRec rec(i64 p) const { return make_rec(T, R, p); }
+    __device__ __forceinline__ MRec reca(i64 i) const { return rec(apos(i)); }
+    __device__ __forceinline__ MRec recb(i64 j) const { return rec(bpos(j)); }
 };
 
 // Merge path in two kernels.  k_merge_partition splits the output into
@@ -524,7 +529,7 @@ __global__ void k_merge_partition(V v, i64 na, i64 nb, i64 ntiles, u32 *__restri
         while (lo < hi) {
             i64 span = hi - lo;
             i64 x = lo + (span * (lane + 1)) / 33;  // candidates in [lo, hi)
-            bool p = x < hi && rec_a_first(v.rec(v.apos(x)), v.rec(v.bpos(d - 1 - x)));
+            bool p = x < hi && rec_a_first(v.reca(x), v.recb(d - 1 - x));
             u32 tr = __ballot_sync(0xffffffffu, p);
             u32 fl = __ballot_sync(0xffffffffu, x < hi && !p);
             // last true candidate -> lo = x+1; first false candidate -> hi = x
@@ -614,6 +619,226 @@ static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStr
 
 inline i64 merge_split_words(i64 total) { return ceil_div(total > 0 ? total : 1, MT_TILE) + 2; }
 
+// ------------------------------------------------------------ streaming level (u8 text)
+//
+// Levels with a byte text (sigma < 256: DNA levels 0-1) avoid every random
+// gather of the merge and of the mod-0 split.  Each suffix the merge needs is
+// described by one 16 B record, laid out the same for samples and non-samples:
+//   {pos, R(pos+1), R(pos+2), c0 | c1 << 8 | cprev << 16}
+// (1-based sample ranks, 0 where the reference's rank_of is 0; a mod-1 sample
+// carries only R(pos+1) and c0, a mod-2 sample only R(pos+2), c0, c1; cprev =
+// T(pos-1) rides along on mod-1 samples for the mod-0 split).
+//   1 k_srec_emit   stream the text and ISAc in triplet order; every sample's
+//                   record goes, via the bucketed scatter (pscatter.cuh), to
+//                   RS[rank] -- the samples' records in sorted order.
+//   2 mod-0 split   RS streamed in rank order; every mod-1 sample 3j+1 yields
+//                   the record of non-sample 3j, stably partitioned by
+//                   cprev = T(3j) (one onesweep pass): the non-samples sorted
+//                   by (T(3j), R(3j+1)) (suffix_index.py:274-290).
+//   3 merge         both sides are contiguous record runs per tile; output SA
+//                   (top level) and the bucketed ISA (inner levels, the
+//                   parent's ranks) or Phi pairs (top level, for the LCP).
+// Random traffic left: none outside the L2-windowed scatter passes.
+__device__ __forceinline__ bool recq_a_first(const uint4 &a, const uint4 &b) {
+    u32 ca = a.w & 0xFFu, cb = b.w & 0xFFu;
+    if (ca != cb) return ca < cb;
+    if (a.x % 3 == 1) return a.y < b.y;
+    u32 ca1 = (a.w >> 8) & 0xFFu, cb1 = (b.w >> 8) & 0xFFu;
+    if (ca1 != cb1) return ca1 < cb1;
+    return a.z < b.z;
+}
+
+constexpr int SR_THREADS = 256;
+constexpr int SR_J = 8;                      // triplets per thread
+constexpr int SR_TILE = SR_THREADS * SR_J;   // 2048 triplets -> <= 4096 records
+
+// pass A of the record scatter: item {dest = 0-based sample rank, pos, nb, chars}
+__global__ void __launch_bounds__(SR_THREADS)
+k_srec_emit(Text<u8> T, SampleLayout L, const u32 *__restrict__ isac, PsPlan plan, uint4 *__restrict__ stage) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint4 *sh_items = reinterpret_cast<uint4 *>(smem);
+    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_items + 2 * SR_TILE);
+    u32 *sh_base = sh_cnt + plan.a.buckets;
+    const i64 j0 = (i64)blockIdx.x * SR_TILE;
+    uint4 it[2 * SR_J];
+    bool ok[2 * SR_J];
+#pragma unroll
+    for (int r = 0; r < SR_J; r++) {
+        i64 j = j0 + r * SR_THREADS + threadIdx.x;
+        ok[2 * r] = j < L.m1;
+        ok[2 * r + 1] = j < L.m2;
+        if (ok[2 * r]) {
+            i64 p = 3 * j;
+            u32 cp = T(p), c0 = T(p + 1), c1 = T(p + 2), c2 = T(p + 3);
+            u32 r1 = isac[j];
+            u32 r2 = j < L.m2 ? isac[L.m1 + j] : 0xFFFFFFFFu;
+            u32 r4 = j + 1 < L.m1 ? isac[j + 1] + 1u : 0u;
+            it[2 * r] = make_uint4(r1, (u32)(p + 1), r2 + 1u, c0 | (c1 << 8) | (cp << 16));
+            if (ok[2 * r + 1]) it[2 * r + 1] = make_uint4(r2, (u32)(p + 2), r4, c1 | (c2 << 8));
+        }
+    }
+    ps_block_emit<uint4, SR_THREADS, 2 * SR_J>(it, ok, plan.a, stage, sh_items, sh_cnt, sh_base);
+}
+
+// pass B: RS[rank] = record
+struct RsApply {
+    using Out = uint4;
+    uint4 *out;
+    __device__ __forceinline__ uint4 value(const uint4 &p) const {
+        return (p.y % 3 == 1) ? make_uint4(p.y, p.z, 0u, p.w) : make_uint4(p.y, 0u, p.z, p.w);
+    }
+};
+struct U32Apply {
+    using Out = u32;
+    u32 *out;
+    __device__ __forceinline__ u32 value(const uint2 &p) const { return p.y; }
+};
+
+// mod-0 split source: RS in rank order; mod-1 sample 3j+1 at rank r gives
+// non-sample 3j = {3j, r+1, R(3j+2), T(3j) | T(3j+1) << 8} keyed by T(3j)
+struct Mod0RecSrc {
+    const uint4 *rs;
+    __device__ __forceinline__ bool get(i64 r, u32 &k, uint4 &v) const {
+        uint4 e = rs[r];
+        if (e.x % 3 != 1) return false;
+        u32 cp = (e.w >> 16) & 0xFFu;
+        k = cp;
+        v = make_uint4(e.x - 1, (u32)r + 1u, e.y, cp | ((e.w & 0xFFu) << 8));
+        return true;
+    }
+};
+
+struct RecMergeView {
+    const uint4 *A, *B;
+    __device__ __forceinline__ uint4 ra(i64 i) const { return A[i]; }
+    __device__ __forceinline__ uint4 rb(i64 j) const { return B[j]; }
+};
+
+__global__ void k_merge_partition_rec(RecMergeView v, i64 na, i64 nb, i64 ntiles, u32 *__restrict__ split) {
+    i64 total = na + nb;
+    int lane = lane_id();
+    i64 warps = ((i64)gridDim.x * blockDim.x) >> 5;
+    for (i64 t = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t <= ntiles; t += warps) {
+        i64 d = t * MT_TILE < total ? t * MT_TILE : total;
+        i64 lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+        while (lo < hi) {
+            i64 span = hi - lo;
+            i64 x = lo + (span * (lane + 1)) / 33;
+            bool p = x < hi && recq_a_first(v.ra(x), v.rb(d - 1 - x));
+            u32 tr = __ballot_sync(0xffffffffu, p);
+            u32 fl = __ballot_sync(0xffffffffu, x < hi && !p);
+            if (tr) lo = __shfl_sync(0xffffffffu, x, 31 - __clz(tr)) + 1;
+            if (fl) hi = __shfl_sync(0xffffffffu, x, __ffs(fl) - 1);
+            if (span <= 32) break;
+        }
+        if (lane == 0) split[t] = (u32)lo;
+    }
+}
+
+enum { EMIT_NONE = 0, EMIT_ISA = 1, EMIT_PHI = 2 };
+constexpr u32 kNoPred = 0xFFFFFFFFu;
+
+// Merge of record runs; MODE selects the bucketed side output:
+//   EMIT_ISA  {pos, rank}           -> ISA[pos] = rank
+//   EMIT_PHI  {pos, pos of rank-1}  -> Phi[pos]  (kNoPred at rank 0)
+template <int MODE>
+__global__ void __launch_bounds__(MT_THREADS)
+k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
+                 uint2 *__restrict__ stage) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint4 *sh = reinterpret_cast<uint4 *>(smem);
+    u32 *out = reinterpret_cast<u32 *>(sh + MT_TILE);
+    u32 *sh_cnt = out + MT_TILE;
+    u32 *sh_base = sh_cnt + plan.a.buckets;
+    __shared__ u32 sh_pred;
+    i64 total = na + nb;
+    i64 d0 = (i64)blockIdx.x * MT_TILE;
+    i64 d1 = d0 + MT_TILE < total ? d0 + MT_TILE : total;
+    i64 i0 = split[blockIdx.x], i1 = split[blockIdx.x + 1];
+    i64 j0 = d0 - i0;
+    int nat = (int)(i1 - i0), cnt = (int)(d1 - d0), nbt = cnt - nat;
+#pragma unroll
+    for (int q = 0; q < MT_ITEMS; q++) {
+        int x = threadIdx.x + q * MT_THREADS;
+        if (x < cnt) sh[x] = x < nat ? v.ra(i0 + x) : v.rb(j0 + (x - nat));
+    }
+    if (MODE == EMIT_PHI && threadIdx.x == 0) {
+        // the suffix at rank d0-1 is the larger of the two run predecessors
+        u32 pr = kNoPred;
+        if (d0 > 0) {
+            if (i0 == 0) pr = v.rb(j0 - 1).x;
+            else if (j0 == 0) pr = v.ra(i0 - 1).x;
+            else {
+                uint4 a = v.ra(i0 - 1), b = v.rb(j0 - 1);
+                pr = recq_a_first(a, b) ? b.x : a.x;
+            }
+        }
+        sh_pred = pr;
+    }
+    __syncthreads();
+    const uint4 *A = sh, *B = sh + nat;
+    int dt = threadIdx.x * MT_ITEMS;
+    if (dt < cnt) {
+        int lo = dt > nbt ? dt - nbt : 0, hi = dt < nat ? dt : nat;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (recq_a_first(A[mid], B[dt - 1 - mid])) lo = mid + 1;
+            else hi = mid;
+        }
+        int i = lo, j = dt - lo;
+#pragma unroll
+        for (int r = 0; r < MT_ITEMS; r++) {
+            if (dt + r >= cnt) break;
+            bool takeA = j >= nbt || (i < nat && recq_a_first(A[i], B[j]));
+            out[dt + r] = takeA ? A[i++].x : B[j++].x;
+        }
+    }
+    __syncthreads();
+    if (sa)
+        for (int x = threadIdx.x; x < cnt; x += MT_THREADS) __stcs(sa + d0 + x, out[x]);
+    if (MODE != EMIT_NONE) {
+        uint2 it[MT_ITEMS];
+        bool ok[MT_ITEMS];
+#pragma unroll
+        for (int q = 0; q < MT_ITEMS; q++) {
+            int x = threadIdx.x + q * MT_THREADS;
+            ok[q] = x < cnt;
+            if (ok[q]) {
+                if (MODE == EMIT_ISA) it[q] = make_uint2(out[x], (u32)(d0 + x));
+                else it[q] = make_uint2(out[x], x > 0 ? out[x - 1] : sh_pred);
+            }
+        }
+        ps_block_emit<uint2, MT_THREADS, MT_ITEMS>(it, ok, plan.a, stage, reinterpret_cast<uint2 *>(sh), sh_cnt,
+                                                   sh_base);
+    }
+}
+
+template <int MODE>
+static int merge_rec_launch(RecMergeView v, i64 na, i64 nb, const u32 *split, u32 *sa, const PsPlan &plan,
+                            uint2 *stage, cudaStream_t st) {
+    static bool attr = false;
+    size_t smem = (size_t)MT_TILE * 20 + 8 * (size_t)PS_MAX_BUCKETS;
+    if (!attr) {
+        SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_rec<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    size_t use = (size_t)MT_TILE * 20 + 8 * (size_t)(MODE == EMIT_NONE ? 1 : plan.a.buckets);
+    k_merge_tile_rec<MODE><<<(unsigned)ceil_div(na + nb, MT_TILE), MT_THREADS, use, st>>>(v, na, nb, split, sa, plan,
+                                                                                         stage);
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}
+
+// all names distinct (bitmap naming): ISAc[s] = name - 1
+__global__ void k_isa_from_names(const u32 *__restrict__ tt, i64 m, u32 *__restrict__ isac) {
+    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < m; s += (i64)gridDim.x * blockDim.x)
+        isac[s] = __ldcs(tt + s) - 1u;
+}
+
+inline bool stream_level_ok(int text_bytes, u64 sigma, i64 N, const saix_dc3_probe *probe) {
+    return text_bytes == 1 && sigma + 1 <= 256 && probe == nullptr && N < ((i64)3 << 29);
+}
+
 // ------------------------------------------------------------ probes
 
 __global__ void k_probe_rank(RankFromIsa R, i64 n3, u32 *__restrict__ out) {
@@ -665,7 +890,10 @@ static int read_u32(const u32 *d, u32 *h, cudaStream_t st) {
 
 template <typename TT>
 static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *ISA,
-                     saix_dc3_probe *probe, int depth);
+                     saix_dc3_probe *probe, int depth, u32 *Phi = nullptr, bool *phi_done = nullptr);
+
+static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA, u32 *ISA, u32 *Phi,
+                            bool *phi_done, int depth);
 
 // Steps 1-2: names of the sample triples, then SAc/ISAc (recursing if needed).
 template <typename TT>
@@ -767,7 +995,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
     if ((i64)D == m) {
         Prof prof_("dc3.unique_ranks", 12.0 * m, st);
         if (sorted_vals) k_unique_from_sorted<<<g, K_THREADS, 0, st>>>(sorted_vals, m, SAc, ISAc);
-        else k_unique_from_names<<<g, K_THREADS, 0, st>>>(tt, m, SAc, ISAc);
+        else if (SAc) k_unique_from_names<<<g, K_THREADS, 0, st>>>(tt, m, SAc, ISAc);
+        else k_isa_from_names<<<g, K_THREADS, 0, st>>>(tt, m, ISAc);
         SAIX_LAUNCHED();
         ar.reset(mark);
     } else {
@@ -780,16 +1009,20 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
 
 template <typename TT>
 static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *ISA,
-                     saix_dc3_probe *probe, int depth) {
+                     saix_dc3_probe *probe, int depth, u32 *Phi, bool *phi_done) {
     Arena &ar = *c.ar;
     cudaStream_t st = c.st;
     if (depth > c.max_depth) c.max_depth = depth;
     if (N <= 1) {
         if (N == 1) {
-            k_iota_pair<<<1, 32, 0, st>>>(SA, ISA, 1);
+            if (SA) k_iota_pair<<<1, 32, 0, st>>>(SA, ISA, 1);
+            else if (ISA) k_iota_pair<<<1, 32, 0, st>>>(ISA, nullptr, 1);
             SAIX_LAUNCHED();
         }
         return SAIX_OK;
+    }
+    if constexpr (sizeof(TT) == 1) {
+        if (stream_level_ok(1, sigma, N, probe)) return dc3_level_stream(c, text, N, sigma, SA, ISA, Phi, phi_done, depth);
     }
     SampleLayout L = SampleLayout::of(N);
     size_t mark0 = ar.mark();
@@ -797,6 +1030,7 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     u32 *SAc = ar.alloc<u32>(L.m);
     u32 *ISAc = ar.alloc<u32>(L.m);
     u32 *d_scal = ar.alloc<u32>(8);
+    if (!SA) SA = ar.alloc<u32>(N);  // a streaming parent needs only the ranks
     SAIX_ARENA_OK(ar);
     Text<TT> T{text, N};
 
@@ -896,6 +1130,89 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     return SAIX_OK;
 }
 
+// Streaming level (see "streaming level" above).  SA / ISA / Phi nullable;
+// Phi is produced only when ISA is not requested (*phi_done tells).
+static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA, u32 *ISA, u32 *Phi,
+                            bool *phi_done, int depth) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    if (depth > c.max_depth) c.max_depth = depth;
+    SampleLayout L = SampleLayout::of(N);
+    const i64 m = L.m, k = L.k;
+    size_t mark0 = ar.mark();
+    u32 *tt = ar.alloc<u32>(m);
+    u32 *ISAc = ar.alloc<u32>(m);
+    u32 *d_scal = ar.alloc<u32>(8);
+    SAIX_ARENA_OK(ar);
+    Text<u8> T{text, N};
+    SAIX_TRY(sort_samples<u8>(c, T, L, sigma, tt, nullptr, ISAc, d_scal, depth, false));
+
+    // 1: sample records in rank order
+    uint4 *RS = ar.alloc<uint4>(m);
+    size_t mark1 = ar.mark();
+    PsPlan pr = PsPlan::of(m, 16);
+    pr.set_cursors(ar.alloc<u32>(pr.cursor_words()));
+    uint4 *stage1 = ar.alloc<uint4>(pr.stage1_items());
+    uint4 *stage2 = ar.alloc<uint4>(pr.stage2_items());
+    SAIX_ARENA_OK(ar);
+    SAIX_CUDA(cudaMemsetAsync(pr.a.cursor, 0, (size_t)pr.cursor_words() * 4, st));
+    {
+        Prof prof_("dc3.srec_emit", (double)N + 12.0 * m + 16.0 * m, st);
+        size_t smem = (size_t)2 * SR_TILE * 16 + 8 * (size_t)pr.a.buckets;
+        static bool attr = false;
+        if (!attr) {
+            SAIX_CUDA(cudaFuncSetAttribute(k_srec_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           2 * SR_TILE * 16 + 8 * PS_MAX_BUCKETS));
+            attr = true;
+        }
+        k_srec_emit<<<(unsigned)ceil_div(k, SR_TILE), SR_THREADS, smem, st>>>(T, L, ISAc, pr, stage1);
+    }
+    SAIX_LAUNCHED();
+    SAIX_TRY(ps_finish(stage1, stage2, pr, RsApply{RS}, st, "dc3.srec_apply", 48.0 * m));
+    ar.reset(mark1);
+
+    // 2: non-sample records in sorted order
+    uint4 *M0 = ar.alloc<uint4>(k);
+    size_t mark2 = ar.mark();
+    u32 *scratch = ar.alloc<u32>(os_scratch_words(m));
+    SAIX_ARENA_OK(ar);
+    SAIX_TRY(onesweep_partition<uint4>(Mod0RecSrc{RS}, m, Mod0HistSrc<u8>{T}, k, 0, M0, scratch, st,
+                                       "dc3.mod0_split", 16.0 * m + 16.0 * k + 1.0 * k));
+    ar.reset(mark2);
+
+    // 3: merge (the padding sample has rank 0 and is not a suffix)
+    i64 pad = L.pad ? 1 : 0;
+    i64 na = m - pad;
+    RecMergeView V{RS + pad, M0};
+    i64 total = na + k;
+    i64 ntiles = ceil_div(total, MT_TILE);
+    u32 *split = ar.alloc<u32>(merge_split_words(total));
+    int mode = ISA ? EMIT_ISA : (Phi ? EMIT_PHI : EMIT_NONE);
+    PsPlan pm = PsPlan::of(mode == EMIT_NONE ? 1 : total, 4);
+    pm.set_cursors(ar.alloc<u32>(pm.cursor_words()));
+    uint2 *pst1 = mode == EMIT_NONE ? nullptr : ar.alloc<uint2>(pm.stage1_items());
+    uint2 *pst2 = mode == EMIT_NONE ? nullptr : ar.alloc<uint2>(pm.stage2_items());
+    SAIX_ARENA_OK(ar);
+    SAIX_CUDA(cudaMemsetAsync(pm.a.cursor, 0, (size_t)pm.cursor_words() * 4, st));
+    {
+        Prof prof_("dc3.merge_partition", 32.0 * (ntiles + 1), st);
+        k_merge_partition_rec<<<grid_for((ntiles + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, split);
+    }
+    SAIX_LAUNCHED();
+    {
+        Prof prof_("dc3.merge_tile", 16.0 * total + (SA ? 4.0 * total : 0) + (mode ? 8.0 * total : 0), st);
+        if (mode == EMIT_ISA) SAIX_TRY(merge_rec_launch<EMIT_ISA>(V, na, k, split, SA, pm, pst1, st));
+        else if (mode == EMIT_PHI) SAIX_TRY(merge_rec_launch<EMIT_PHI>(V, na, k, split, SA, pm, pst1, st));
+        else SAIX_TRY(merge_rec_launch<EMIT_NONE>(V, na, k, split, SA, pm, pst1, st));
+    }
+    if (mode != EMIT_NONE)
+        SAIX_TRY(ps_finish(pst1, pst2, pm, U32Apply{mode == EMIT_ISA ? ISA : Phi}, st,
+                           mode == EMIT_ISA ? "dc3.isa_apply" : "dc3.phi_apply", 28.0 * total));
+    if (phi_done) *phi_done = mode == EMIT_PHI;
+    ar.reset(mark0);
+    return SAIX_OK;
+}
+
 // Upper bound of the workspace the driver carves (persistent arrays of every
 // level + the largest level's temporaries), see DESIGN.md "DC3 workspace".
 static size_t dc3_plan(i64 n) {
@@ -904,7 +1221,7 @@ static size_t dc3_plan(i64 n) {
     while (N > 1) {
         SampleLayout L = SampleLayout::of(N);
         i64 m = L.m, k = L.k;
-        persistent += (size_t)(3 * m + 8) * 4 + 4 * Arena::kAlign;
+        persistent += (size_t)(3 * m + 8) * 4 + (size_t)N * 4 + 5 * Arena::kAlign;
         i64 sw = os_scratch_words(m) > bs_scratch_words(N + 1) ? os_scratch_words(m) : bs_scratch_words(N + 1);
         size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
@@ -912,8 +1229,16 @@ static size_t dc3_plan(i64 n) {
         i64 bw = mod0_bitmap_words(7, m);
         size_t post_t = (size_t)k * 16 + (size_t)k * 32 + (size_t)k * 8 +
                         (size_t)(sw + merge_split_words(N) + 2 * bw + scan_tmp_words(bw)) * 4;
+        // streaming level: RS + (record stage | M0 + partition scratch | M0 + split + pair stage)
+        PsPlan pr = PsPlan::of(m, 16), pm = PsPlan::of(N, 4);
+        size_t s1 = (size_t)(pr.stage1_items() + pr.stage2_items()) * 16 + (size_t)pr.cursor_words() * 4;
+        size_t s2 = (size_t)k * 16 + (size_t)os_scratch_words(m) * 4;
+        size_t s3 = (size_t)k * 16 + (size_t)merge_split_words(N) * 4 +
+                    (size_t)(pm.stage1_items() + pm.stage2_items()) * 8 + (size_t)pm.cursor_words() * 4;
+        size_t stream_t = (size_t)m * 16 + (s1 > s2 ? (s1 > s3 ? s1 : s3) : (s2 > s3 ? s2 : s3));
         size_t t = sort_t > bm_t ? sort_t : bm_t;
         t = t > post_t ? t : post_t;
+        t = t > stream_t ? t : stream_t;
         t += 8 * Arena::kAlign;
         if (t > temps) temps = t;
         N = m;
@@ -937,7 +1262,8 @@ extern "C" int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sig
 
 namespace saix {
 int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, void *ws,
-                size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream) {
+                size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream, u32 *phi, bool *phi_done) {
+    if (phi_done) *phi_done = false;
     if (n < 0 || n > (int64_t)0xFFFFFFF0LL || (text_bytes != 1 && text_bytes != 4) || sigma < 1 ||
         (n > 0 && (!text || !sa))) {
         set_error("saix_dc3: invalid arguments (n=%lld, text_bytes=%d, sigma=%lld)", (long long)n,
@@ -983,7 +1309,7 @@ int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32
         return SAIX_OK;
     }
     int rc = text_bytes == 1
-                 ? dc3_level<u8>(c, (const u8 *)text, n, (u64)sigma, sa, isa, probe, 0)
+                 ? dc3_level<u8>(c, (const u8 *)text, n, (u64)sigma, sa, isa, probe, 0, phi, phi_done)
                  : dc3_level<u32>(c, (const u32 *)text, n, (u64)sigma, sa, isa, probe, 0);
     if (rc) return rc;
     if (probe) probe->depth = c.max_depth;

@@ -122,15 +122,17 @@ static __global__ void __launch_bounds__(OS_RADIX) k_os_scan(const u32 *__restri
     }
 }
 
-template <typename K, class Src, int ITEMS>
+// V: payload type (u32 sample index, or a 16 B DC3 record); keys_out may be
+// null when only the payloads are wanted (single-pass stable partitions).
+template <typename K, class Src, int ITEMS, typename V = u32>
 __global__ void __launch_bounds__(OS_THREADS, 2)
 k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restrict__ status, u32 *__restrict__ ticket,
-          K *__restrict__ keys_out, u32 *__restrict__ vals_out) {
+          K *__restrict__ keys_out, V *__restrict__ vals_out) {
     constexpr int TILE = OS_THREADS * ITEMS;
     extern __shared__ __align__(16) unsigned char smem[];
-    K *sk = reinterpret_cast<K *>(smem);
-    u32 *sv = reinterpret_cast<u32 *>(sk + TILE);
-    u32(*cnt)[OS_RADIX] = reinterpret_cast<u32(*)[OS_RADIX]>(sv + TILE);
+    V *sv = reinterpret_cast<V *>(smem);
+    K *sk = reinterpret_cast<K *>(sv + TILE);
+    u32(*cnt)[OS_RADIX] = reinterpret_cast<u32(*)[OS_RADIX]>(sk + TILE);
     u32 *tile_excl = &cnt[OS_WARPS][0];
     u32 *gbase = tile_excl + OS_RADIX;
     __shared__ u32 sh_tile, sh_warp[OS_WARPS + 1];
@@ -142,7 +144,8 @@ k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restri
     const u32 tile = sh_tile;
     i64 seg = (i64)tile * TILE + (i64)w * (32 * ITEMS);
     K k[ITEMS];
-    u32 v[ITEMS], rank[ITEMS], dig[ITEMS];
+    V v[ITEMS];
+    u32 rank[ITEMS], dig[ITEMS];
     u32 lt = lanemask_lt();
     // all loads first (16 in flight per thread), then the ranking rounds
 #pragma unroll
@@ -243,14 +246,14 @@ k_os_pass(Src src, i64 n, int shift, const u32 *__restrict__ offs, u32 *__restri
         K kk = sk[x];
         u32 d = (u32)(kk >> shift) & (OS_RADIX - 1);
         u32 dst = gbase[d] + (x - tile_excl[d]);
-        keys_out[dst] = kk;
+        if (keys_out) keys_out[dst] = kk;
         vals_out[dst] = sv[x];
     }
 }
 
-template <typename K, int ITEMS>
+template <typename K, int ITEMS, typename V = u32>
 constexpr size_t os_pass_smem() {
-    return (size_t)OS_THREADS * ITEMS * (sizeof(K) + 4) + (size_t)(OS_WARPS + 2) * OS_RADIX * 4;
+    return (size_t)OS_THREADS * ITEMS * (sizeof(K) + sizeof(V)) + (size_t)(OS_WARPS + 2) * OS_RADIX * 4;
 }
 
 inline int os_items_choice() {
@@ -262,19 +265,20 @@ inline int os_items_choice() {
     return v;
 }
 
-template <typename K, class Src, int ITEMS>
-static int os_launch_pass(Src src, i64 np, int shift, const u32 *offs, u32 *status, u32 *ticket, K *dk, u32 *dv,
+template <typename K, class Src, int ITEMS, typename V = u32>
+static int os_launch_pass(Src src, i64 np, int shift, const u32 *offs, u32 *status, u32 *ticket, K *dk, V *dv,
                           cudaStream_t st) {
     static bool attr = false;
+    constexpr size_t smem = os_pass_smem<K, ITEMS, V>();
     if (!attr) {
-        SAIX_CUDA(cudaFuncSetAttribute(k_os_pass<K, Src, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)os_pass_smem<K, ITEMS>()));
+        SAIX_CUDA(cudaFuncSetAttribute(k_os_pass<K, Src, ITEMS, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
         attr = true;
     }
     i64 ntiles = os_tiles(np, ITEMS);
     SAIX_CUDA(cudaMemsetAsync(status, 0, (size_t)ntiles * OS_RADIX * 4, st));
-    k_os_pass<K, Src, ITEMS><<<(unsigned)ntiles, OS_THREADS, os_pass_smem<K, ITEMS>(), st>>>(src, np, shift, offs,
-                                                                                             status, ticket, dk, dv);
+    k_os_pass<K, Src, ITEMS, V><<<(unsigned)ntiles, OS_THREADS, smem, st>>>(src, np, shift, offs, status, ticket, dk,
+                                                                            dv);
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
@@ -335,6 +339,33 @@ int onesweep_sort(Src src, i64 n, HSrc hsrc, i64 n_h, i64 n_out, int shift0, int
     out_k = ok;
     out_v = ov;
     return SAIX_OK;
+}
+
+// Single-pass stable partition of `src`'s valid items by an 8-bit key
+// (bits [shift, shift+8)), payloads only: out receives the n_out valid
+// payloads grouped by key, input order kept within a key.  `hsrc` enumerates
+// the same key multiset (see onesweep_sort).
+template <typename V, class Src, class HSrc>
+int onesweep_partition(Src src, i64 n, HSrc hsrc, i64 n_h, int shift, V *out, u32 *scratch, cudaStream_t st,
+                       const char *prof, double bytes) {
+    if (n >= ((i64)1 << 30)) {
+        set_error("onesweep_partition: n=%lld too large", (long long)n);
+        return SAIX_EINVAL;
+    }
+    Prof prof_(prof, bytes, st);
+    if (n <= 0) return SAIX_OK;
+    u32 *hist = scratch;
+    u32 *offs = hist + OS_MAX_PASSES * OS_RADIX;
+    u32 *ticket = offs + OS_MAX_PASSES * OS_RADIX;
+    u32 *status = ticket + 64;
+    SAIX_CUDA(cudaMemsetAsync(hist, 0, (size_t)OS_RADIX * 4, st));
+    SAIX_CUDA(cudaMemsetAsync(ticket, 0, 64 * 4, st));
+    k_os_hist<u32, HSrc><<<grid_for(n_h, OS_THREADS, kNumSMs * 8), OS_THREADS, 0, st>>>(hsrc, n_h, shift, 1, hist);
+    SAIX_LAUNCHED();
+    k_os_scan<<<1, OS_RADIX, 0, st>>>(hist, 1, offs, nullptr);
+    SAIX_LAUNCHED();
+    constexpr int kItems = sizeof(V) > 4 ? 8 : 16;  // 16 B payloads: keep the tile in registers
+    return os_launch_pass<u32, Src, kItems, V>(src, n, shift, offs, status, ticket, (u32 *)nullptr, out, st);
 }
 
 }  // namespace saix

@@ -73,8 +73,9 @@ def test_workspace_planners_monotone(n):
     a = L.saix_dc3_workspace_bytes(n, 1)
     b = L.saix_dc3_workspace_bytes(n + 1000, 1)
     assert 0 < a <= b
-    # persistent per-level arrays ~ 3 * 4 * sum(m_l) ~ 24 n, plus one level of temps
-    assert a < 64 * max(n, 1) + (1 << 24)
+    # worst-case recursion: persistent per-level arrays (tt, SAc, ISAc, child SA)
+    # ~ 12 * sum(N_l) = 36 n, plus the largest level's temps (records: ~ 32 m)
+    assert a < 80 * max(n, 1) + (1 << 24)
     assert L.saix_lcp_workspace_bytes(n) > 0
     assert L.saix_overlap_workspace_bytes(n) > 0
     assert L.saix_longest_overlap_workspace_bytes(n // 2, n - n // 2) >= a
