@@ -121,6 +121,15 @@ SAIX_API int saix_lcp(const void *text, int text_bytes, int64_t n, const uint32_
              const uint32_t *isa, uint32_t *lcp, void *ws, size_t ws_bytes,
              void *stream);
 
+/* build_lcp with the alphabet known (suffix_index.py:479-506, same output):
+ * sigma = largest rank (<= 0: unknown), separator = position of a unique
+ * separator rank 1 (generalized text, overlap.py:83-95) or -1.  Byte texts
+ * with <= 4 residue ranks (plus the separator) are compared 32 characters per
+ * word on a 2-bit packed copy; u8 text must be 16-byte aligned. */
+SAIX_API int saix_lcp_sigma(const void *text, int text_bytes, int64_t n, int64_t sigma,
+             int64_t separator, const uint32_t *sa, uint32_t *lcp, void *ws,
+             size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------- RMQ */
 
 #define SAIX_SPARSE_PACK32 0  /* entry = (value-bias) << ibits | index, u32 */

@@ -75,6 +75,7 @@ SIGNATURES = {
     "saix_dc3_merge": (_int, [_vp, _int, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
     "saix_lcp_workspace_bytes": (_c.c_size_t, [_i64]),
     "saix_lcp": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_lcp_sigma": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_minmax": (_int, [_vp, _int, _i64, _vp, _vp]),
     "saix_sparse_plan_make": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),
     "saix_sparse_build": (_int, [_c.POINTER(SparsePlan), _vp, _int, _vp, _vp]),

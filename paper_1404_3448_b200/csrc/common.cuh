@@ -142,8 +142,11 @@ inline int bits_for(u64 v) {  // bit width of v (>= 1), like int.bit_length()
 // the final permute kernel; boundary < 0 disables it.
 // phi_in (nullable): caller storage for Phi/PLCP; phi_ready says it already
 // holds Phi (Phi[sa[r]] = sa[r-1]).
+// sigma / sep (alphabet bound, unique separator position; -1 = unknown /
+// none) select the direct word-compare LCP when the text allows it.
 int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
-                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in = nullptr, bool phi_ready = false);
+                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in = nullptr, bool phi_ready = false,
+                i64 sigma = -1, i64 sep = -1);
 
 // PLCP (in place over Phi) for u8 text -- the batched-pairs path.
 size_t plcp_workspace_bytes(i64 n);

@@ -649,7 +649,7 @@ __device__ __forceinline__ bool recq_a_first(const uint4 &a, const uint4 &b) {
 }
 
 constexpr int SR_THREADS = 256;
-constexpr int SR_J = 8;                      // triplets per thread
+constexpr int SR_J = 4;                      // triplets per thread
 constexpr int SR_TILE = SR_THREADS * SR_J;   // 2048 triplets -> <= 4096 records
 
 // pass A of the record scatter: item {dest = 0-based sample rank, pos, nb, chars}
@@ -706,6 +706,151 @@ struct Mod0RecSrc {
         v = make_uint4(e.x - 1, (u32)r + 1u, e.y, cp | ((e.w & 0xFFu) << 8));
         return true;
     }
+};
+
+// Pass B of the record scatter, specialised: writes RS window w (4096 ranks)
+// and counts its mod-1 samples per cprev digit into hist[d * windows + w]
+// (digit-major, so one flat exclusive scan gives every (digit, window) its
+// output offset in the mod-0 order).
+constexpr int RW_SHIFT = 12;  // 4096 records = 64 KB window
+__global__ void __launch_bounds__(PS_THREADS)
+k_rs_window(const uint4 *__restrict__ stage2, PsPlan plan, uint4 *__restrict__ rs, u32 *__restrict__ hist, int D1) {
+    extern __shared__ __align__(16) unsigned char ps_smem[];
+    uint4 *win = reinterpret_cast<uint4 *>(ps_smem);
+    __shared__ u32 cnt[256];
+    const i64 w = blockIdx.x;
+    const i64 d0 = w << RW_SHIFT;
+    const i64 len = (d0 + (1 << RW_SHIFT) < plan.n_dest ? d0 + (1 << RW_SHIFT) : plan.n_dest) - d0;
+    const i64 n_in = plan.cursor2[w];
+    const uint4 *src = stage2 + d0;
+    RsApply ap{rs};
+    for (int d = threadIdx.x; d < 256; d += PS_THREADS) cnt[d] = 0;
+    __syncthreads();
+    const bool full = n_in == len;
+    for (i64 x = threadIdx.x; x < n_in; x += PS_THREADS) {
+        uint4 p = ld_stream(src + x);
+        uint4 e = ap.value(p);
+        if (full) win[(i64)p.x - d0] = e;
+        else rs[p.x] = e;
+    }
+    __syncthreads();
+    // count digits over the window's records (window order when full)
+    const i64 nc = full ? len : n_in;
+    for (i64 x0 = 0; x0 < nc; x0 += PS_THREADS) {
+        i64 x = x0 + threadIdx.x;
+        u32 d = 0xFFFFFFFFu;
+        if (x < nc) {
+            uint4 e;
+            if (full) {
+                e = win[x];
+                st_stream(rs + d0 + x, e);
+            } else {
+                e = ap.value(ld_stream(src + x));
+            }
+            if (e.x % 3 == 1) d = (e.w >> 16) & 0xFFu;
+        }
+        u32 peers = __match_any_sync(0xffffffffu, d);
+        if (d != 0xFFFFFFFFu && (peers & lanemask_lt()) == 0) atomicAdd(&cnt[d], (u32)__popc(peers));
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < D1; d += PS_THREADS) hist[(i64)d * plan.windows + w] = cnt[d];
+}
+
+// Mod-0 records of RS window w, stably partitioned by cprev: one tile of
+// 4096 ranks per CTA, warp-stable ranking (as in k_os_pass) with the global
+// per-(digit, window) offsets already known, so no look-back.
+constexpr int M0_ITEMS = 16;  // 256 threads x 16 = 4096 = 1 << RW_SHIFT
+__global__ void __launch_bounds__(256)
+k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__restrict__ offs, uint4 *__restrict__ M0) {
+    extern __shared__ __align__(16) unsigned char m0_smem[];
+    uint4 *sv = reinterpret_cast<uint4 *>(m0_smem);
+    __shared__ u32 cnt[8][256];
+    __shared__ u32 tile_excl[256], gbase[256], sh_warp[9];
+    const int wp = threadIdx.x >> 5, lane = lane_id();
+    for (int d = lane; d < 256; d += 32) cnt[wp][d] = 0;
+    __syncthreads();
+    const i64 w = blockIdx.x;
+    const i64 seg = (w << RW_SHIFT) + (i64)wp * (32 * M0_ITEMS);
+    u32 pos[M0_ITEMS], nb[M0_ITEMS], c0[M0_ITEMS], dig[M0_ITEMS], rank[M0_ITEMS];
+    const u32 lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < M0_ITEMS; r++) {
+        i64 i = seg + r * 32 + lane;
+        dig[r] = 256u;
+        if (i < m) {
+            uint4 e = __ldcs(rs + i);
+            if (e.x % 3 == 1) {
+                pos[r] = e.x;
+                nb[r] = e.y;
+                c0[r] = e.w & 0xFFu;
+                dig[r] = (e.w >> 16) & 0xFFu;
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < M0_ITEMS; r++) {
+        u32 d = dig[r];
+        bool ok = d < 256u;
+        u32 peers = __match_any_sync(0xffffffffu, d);
+        u32 before = __popc(peers & lt);
+        u32 cur = ok ? cnt[wp][d] : 0u;
+        __syncwarp();
+        if (ok && before == 0) cnt[wp][d] = cur + __popc(peers);
+        __syncwarp();
+        rank[r] = cur + before;
+    }
+    __syncthreads();
+    {
+        const int d = threadIdx.x;
+        u32 run = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            u32 c = cnt[q][d];
+            cnt[q][d] = run;
+            run += c;
+        }
+        gbase[d] = run ? offs[(i64)d * windows + w] : 0u;
+        u32 inc = run;
+        for (int o = 1; o < 32; o <<= 1) {
+            u32 y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) sh_warp[wp] = inc;
+        __syncthreads();
+        if (wp == 0) {
+            u32 x = lane < 8 ? sh_warp[lane] : 0u, xi = x;
+            for (int o = 1; o < 32; o <<= 1) {
+                u32 y = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += y;
+            }
+            if (lane < 8) sh_warp[lane] = xi - x;
+            if (lane == 7) sh_warp[8] = xi;
+        }
+        __syncthreads();
+        tile_excl[d] = sh_warp[wp] + inc - run;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < M0_ITEMS; r++) {
+        u32 d = dig[r];
+        if (d < 256u) {
+            u32 lp = tile_excl[d] + cnt[wp][d] + rank[r];
+            i64 rk = seg + r * 32 + lane;  // 0-based sample rank of 3j+1
+            sv[lp] = make_uint4(pos[r] - 1, (u32)rk + 1u, nb[r], d | (c0[r] << 8));
+        }
+    }
+    __syncthreads();
+    const u32 valid = sh_warp[8];
+    for (u32 x = threadIdx.x; x < valid; x += 256) {
+        uint4 v = sv[x];
+        u32 d = v.w & 0xFFu;
+        __stcs(M0 + gbase[d] + (x - tile_excl[d]), v);
+    }
+}
+
+struct HistIn {
+    const u32 *h;
+    __device__ u32 operator()(i64 i) const { return h[i]; }
 };
 
 struct RecMergeView {
@@ -1152,7 +1297,8 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     size_t mark1 = ar.mark();
     PsPlan pr = PsPlan::of(m, 16);
     pr.set_cursors(ar.alloc<u32>(pr.cursor_words()));
-    uint4 *stage1 = ar.alloc<uint4>(pr.stage1_items());
+    uint4 *stage1 = ar.alloc<uint4>(pr.stage1_items() > k ? pr.stage1_items() : k);  // later: M0
+    size_t mark_s1 = ar.mark();
     uint4 *stage2 = ar.alloc<uint4>(pr.stage2_items());
     SAIX_ARENA_OK(ar);
     SAIX_CUDA(cudaMemsetAsync(pr.a.cursor, 0, (size_t)pr.cursor_words() * 4, st));
@@ -1168,17 +1314,47 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
         k_srec_emit<<<(unsigned)ceil_div(k, SR_TILE), SR_THREADS, smem, st>>>(T, L, ISAc, pr, stage1);
     }
     SAIX_LAUNCHED();
-    SAIX_TRY(ps_finish(stage1, stage2, pr, RsApply{RS}, st, "dc3.srec_apply", 48.0 * m));
-    ar.reset(mark1);
-
-    // 2: non-sample records in sorted order
-    uint4 *M0 = ar.alloc<uint4>(k);
-    size_t mark2 = ar.mark();
-    u32 *scratch = ar.alloc<u32>(os_scratch_words(m));
+    // A2 + the specialised pass B (RS windows + per-window cprev histogram)
+    if (pr.windows > 1 && pr.s2 != RW_SHIFT) {
+        set_error("dc3: record window %d != %d", pr.s2, RW_SHIFT);
+        return SAIX_EINVAL;
+    }
+    const int D1 = (int)sigma + 1;
+    u32 *hist = ar.alloc<u32>((i64)D1 * pr.windows + 1);
+    u32 *hscan = ar.alloc<u32>(scan_tmp_words((i64)D1 * pr.windows));
     SAIX_ARENA_OK(ar);
-    SAIX_TRY(onesweep_partition<uint4>(Mod0RecSrc{RS}, m, Mod0HistSrc<u8>{T}, k, 0, M0, scratch, st,
-                                       "dc3.mod0_split", 16.0 * m + 16.0 * k + 1.0 * k));
-    ar.reset(mark2);
+    {
+        Prof prof_("dc3.srec_apply", 48.0 * m, st);
+        static bool attr = false;
+        if (!attr) {
+            SAIX_CUDA(cudaFuncSetAttribute(k_ps_refine<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(PS_REFINE_TILE * 16 + 8 * 256)));
+            SAIX_CUDA(cudaFuncSetAttribute(k_rs_window, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 << RW_SHIFT));
+            attr = true;
+        }
+        size_t smem = (size_t)PS_REFINE_TILE * 16 + 8 * ((size_t)1 << (pr.a.shift - pr.s2));
+        k_ps_refine<uint4><<<(unsigned)ceil_div(pr.stage1_items(), PS_REFINE_TILE), PS_THREADS, smem, st>>>(
+            stage1, pr, stage2);
+        SAIX_LAUNCHED();
+        k_rs_window<<<(unsigned)pr.windows, PS_THREADS, 16 << RW_SHIFT, st>>>(stage2, pr, RS, hist, D1);
+        SAIX_LAUNCHED();
+    }
+    // 2: non-sample records in sorted order: per-(digit, window) offsets,
+    // then one CTA per RS window
+    uint4 *M0 = (uint4 *)stage1;  // stage1 is free again and holds >= m records
+    SAIX_TRY(scan_transform(HistIn{hist}, StoreExcl{hist}, (i64)D1 * pr.windows, hscan, nullptr, st,
+                            "dc3.mod0_scan", 8.0 * D1 * pr.windows));
+    {
+        Prof prof_("dc3.mod0_split", 16.0 * m + 16.0 * k, st);
+        static bool attr = false;
+        if (!attr) {
+            SAIX_CUDA(cudaFuncSetAttribute(k_mod0_window, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 << RW_SHIFT));
+            attr = true;
+        }
+        k_mod0_window<<<(unsigned)pr.windows, 256, 16 << RW_SHIFT, st>>>(RS, m, pr.windows, hist, M0);
+    }
+    SAIX_LAUNCHED();
+    ar.reset(mark_s1);  // stage2, histogram and scan temps are dead
 
     // 3: merge (the padding sample has rank 0 and is not a suffix)
     i64 pad = L.pad ? 1 : 0;
@@ -1209,6 +1385,7 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
         SAIX_TRY(ps_finish(pst1, pst2, pm, U32Apply{mode == EMIT_ISA ? ISA : Phi}, st,
                            mode == EMIT_ISA ? "dc3.isa_apply" : "dc3.phi_apply", 28.0 * total));
     if (phi_done) *phi_done = mode == EMIT_PHI;
+    (void)mark1;
     ar.reset(mark0);
     return SAIX_OK;
 }

@@ -138,6 +138,152 @@ __global__ void k_lcp_permute(const u32 *__restrict__ sa, i64 n, const u32 *__re
     }
 }
 
+// ------------------------------------------------------------ direct LCP
+//
+// lcp[r] straight from the two suffixes' text, 32 characters per 64-bit word
+// compare on a 2-bit packed copy of the text (alphabet of <= 4 residues plus
+// at most one unique separator, whose position bounds every match: two
+// different suffixes can never both run through it), or 4 bytes per compare
+// on a byte text.  In SA order every suffix pair is an independent thread:
+// no Phi scatter, no PLCP walk, no permutation -- only random reads of the
+// packed text, which at <= 64 MB (2^28 residues) stays L2-resident.
+// Matches are capped at LCP_CAP characters; capped entries are listed and
+// extended exactly by one warp each, and when more than n/64 + 64 entries
+// hit the cap (highly repetitive text) the Kasai path above runs instead.
+constexpr u32 LCP_CAP = 256;
+
+__device__ __forceinline__ u64 load2(const u64 *__restrict__ W, i64 p) {
+    i64 q = p >> 5;
+    u32 o = (u32)(p & 31) * 2;
+    u64 lo = W[q];
+    return o ? (lo >> o) | (W[q + 1] << (64 - o)) : lo;
+}
+
+// chars [p, p+32) -> 2-bit codes (c - base) & 3, LSB first; zero tail words
+__global__ void k_pack2(const u8 *__restrict__ T, i64 n, u32 base, u64 *__restrict__ W, i64 nw) {
+    for (i64 w = (i64)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (i64)gridDim.x * blockDim.x) {
+        i64 p0 = w * 32;
+        u64 x = 0;
+        if (p0 + 32 <= n) {
+            const uint4 *T16 = reinterpret_cast<const uint4 *>(T + p0);
+            uint4 a = __ldcs(T16), b = __ldcs(T16 + 1);
+            u32 v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) x |= (u64)((((v[q] >> (8 * c)) & 0xFFu) - base) & 3u) << (2 * (4 * q + c));
+        } else {
+            for (i64 p = p0; p < n && p < p0 + 32; p++) x |= (u64)(((u32)T[p] - base) & 3u) << (2 * (p - p0));
+        }
+        W[w] = x;
+    }
+}
+
+struct Pack2Text {
+    const u64 *W;
+    __device__ __forceinline__ u32 match(i64 i, i64 j, u32 h, u32 stop) const {
+        while (h < stop) {
+            u64 d = load2(W, i + h) ^ load2(W, j + h);
+            if (d) return min(h + ((u32)(__ffsll((long long)d) - 1) >> 1), stop);
+            h += 32;
+        }
+        return stop;
+    }
+};
+struct ByteText {
+    const u8 *T;
+    i64 n;
+    __device__ __forceinline__ u32 match(i64 i, i64 j, u32 h, u32 stop) const {
+        const u32 *W = reinterpret_cast<const u32 *>(T);
+        while (h < stop) {
+            i64 a = i + h, b = j + h;
+            if (n - (a > b ? a : b) >= 8) {
+                i64 aw = a >> 2, bw = b >> 2;
+                u32 x = __funnelshift_r(W[aw], W[aw + 1], (u32)(a & 3) * 8);
+                u32 y = __funnelshift_r(W[bw], W[bw + 1], (u32)(b & 3) * 8);
+                u32 d = x ^ y;
+                if (d) return min(h + (u32)(__ffs(d) - 1) / 8, stop);
+                h += 4;
+            } else {
+                if (T[a] != T[b]) return h;
+                h++;
+            }
+        }
+        return stop;
+    }
+};
+
+__device__ __forceinline__ u32 match_limit(i64 n, i64 sep, i64 i, i64 j) {
+    i64 lim = n - (i > j ? i : j);
+    if (sep >= 0) {
+        if (i <= sep && sep - i < lim) lim = sep - i;
+        if (j <= sep && sep - j < lim) lim = sep - j;
+    }
+    return (u32)(lim < 0 ? 0 : (lim > 0x7FFFFFFF ? 0x7FFFFFFF : lim));
+}
+
+__device__ __forceinline__ bool cross_pair(u32 p, u32 q, u32 boundary) {
+    return p != boundary && q != boundary && ((p < boundary) != (q < boundary));
+}
+
+template <class Txt>
+__global__ void k_lcp_direct(Txt tx, i64 n, i64 sep, const u32 *__restrict__ sa, u32 *__restrict__ lcp,
+                             u32 *__restrict__ ncap, u32 *__restrict__ list, u32 list_cap, u32 boundary,
+                             u32 *best) {
+    u32 mx = 0;
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x) {
+        u32 j = __ldcs(sa + r), h = 0;
+        if (r > 0) {
+            u32 i = sa[r - 1];
+            u32 lim = match_limit(n, sep, i, j);
+            u32 stop = lim < LCP_CAP ? lim : LCP_CAP;
+            h = tx.match(i, j, 0, stop);
+            if (h == LCP_CAP && lim > LCP_CAP) {
+                u32 at = atomicAdd(ncap, 1u);
+                if (at < list_cap) list[at] = (u32)r;
+            }
+            if (best && cross_pair(i, j, boundary) && h > mx) mx = h;
+        }
+        __stcs(lcp + r, h);
+    }
+    if (best) {
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane_id() == 0 && mx) atomicMax(best, mx);
+    }
+}
+
+// one warp per capped entry: 32 windows of 32 characters (2-bit) per step
+template <class Txt>
+__global__ void k_lcp_extend(Txt tx, i64 n, i64 sep, const u32 *__restrict__ sa, u32 *__restrict__ lcp,
+                             const u32 *__restrict__ ncap, const u32 *__restrict__ list, u32 boundary, u32 *best) {
+    const u32 cnt = *ncap;
+    const int lane = lane_id();
+    for (u32 e = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < cnt; e += ((i64)gridDim.x * blockDim.x) >> 5) {
+        u32 r = list[e];
+        u32 i = sa[r - 1], j = sa[r];
+        u32 lim = match_limit(n, sep, i, j);
+        u32 h = LCP_CAP;
+        while (h < lim) {
+            u32 lo = h + 32u * lane;
+            u32 got = lo < lim ? tx.match(i, j, lo, min(lo + 32u, lim)) : lo;
+            u32 short_ = __ballot_sync(0xffffffffu, lo < lim && got < min(lo + 32u, lim));
+            if (short_) {
+                int l = __ffs(short_) - 1;
+                h = __shfl_sync(0xffffffffu, got, l);
+                break;
+            }
+            h = min(h + 32u * 32u, lim);
+        }
+        if (lane == 0) {
+            lcp[r] = h;
+            if (best && cross_pair(i, j, boundary)) atomicMax(best, h);
+        }
+    }
+}
+
+inline i64 lcp_list_cap(i64 n) { return n / 64 + 64; }
+inline i64 pack2_words(i64 n) { return ceil_div(n > 0 ? n : 1, 32) + 2; }
+
 static int lcp_run(const void *text, int tb, i64 n, const u32 *sa, u32 *lcp, u32 *phi, u32 *seeds, u8 *plcp8,
                    cudaStream_t st, i64 boundary, u32 *best, bool phi_ready) {
     i64 nchunks = ceil_div(n, LCP_CHUNK);
@@ -198,12 +344,57 @@ int plcp_from_phi(const u8 *text, i64 n, u32 *phi_plcp, void *ws, size_t ws_byte
 }
 
 int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp, void *ws, size_t ws_bytes,
-                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in, bool phi_ready) {
+                cudaStream_t st, i64 boundary, u32 *best, u32 *phi_in, bool phi_ready, i64 sigma, i64 sep) {
     Arena ar{(char *)ws, ws_bytes};
     u32 *phi = phi_in ? phi_in : ar.alloc<u32>(n);
     u32 *seeds = ar.alloc<u32>(ceil_div(n, LCP_CHUNK) + 1);
     u8 *plcp8 = ar.alloc<u8>(n);
+    u64 *W2 = ar.alloc<u64>(pack2_words(n));
+    u32 *ncap = ar.alloc<u32>(2);
+    u32 *list = ar.alloc<u32>(lcp_list_cap(n));
     SAIX_ARENA_OK(ar);
+    // packed path: residues 1..4 (no separator) or 2..5 around a unique
+    // separator 1 at `sep`; byte path for other small byte texts
+    bool pack = text_bytes == 1 && sigma >= 1 && ((sep < 0 && sigma <= 4) || (sep >= 0 && sigma <= 5));
+    bool bytes = !pack && text_bytes == 1 && n <= ((i64)48 << 20);
+    if (n > 1 && (pack || bytes) && !phi_ready) {
+        if (best) SAIX_CUDA(cudaMemsetAsync(best, 0, sizeof(u32), st));
+        SAIX_CUDA(cudaMemsetAsync(ncap, 0, sizeof(u32), st));
+        u32 lc = (u32)lcp_list_cap(n);
+        u32 bd = boundary >= 0 ? (u32)boundary : 0u;
+        u32 *bp = boundary >= 0 ? best : nullptr;
+        int g = grid_for(n, 256);
+        if (pack) {
+            i64 nw = pack2_words(n);
+            {
+                Prof prof_("lcp.pack2", (double)n + 8.0 * nw, st);
+                k_pack2<<<grid_for(nw, 256), 256, 0, st>>>((const u8 *)text, n, sep >= 0 ? 2u : 1u, W2, nw);
+            }
+            SAIX_LAUNCHED();
+            Prof prof_("lcp.direct", 12.0 * n + 2.0 * n / 4, st);
+            k_lcp_direct<Pack2Text><<<g, 256, 0, st>>>(Pack2Text{W2}, n, sep, sa, lcp, ncap, list, lc, bd, bp);
+        } else {
+            Prof prof_("lcp.direct", 12.0 * n + 2.0 * n, st);
+            k_lcp_direct<ByteText><<<g, 256, 0, st>>>(ByteText{(const u8 *)text, n}, n, sep, sa, lcp, ncap, list, lc,
+                                                      bd, bp);
+        }
+        SAIX_LAUNCHED();
+        u32 h = 0;
+        SAIX_CUDA(cudaMemcpyAsync(&h, ncap, sizeof(u32), cudaMemcpyDeviceToHost, st));
+        SAIX_CUDA(cudaStreamSynchronize(st));
+        if (h == 0) return SAIX_OK;
+        if (h <= lc) {
+            Prof prof_("lcp.extend", 0.0, st);
+            int ge = grid_for((i64)h * 32, 256);
+            if (pack) k_lcp_extend<Pack2Text><<<ge, 256, 0, st>>>(Pack2Text{W2}, n, sep, sa, lcp, ncap, list, bd, bp);
+            else k_lcp_extend<ByteText><<<ge, 256, 0, st>>>(ByteText{(const u8 *)text, n}, n, sep, sa, lcp, ncap, list,
+                                                           bd, bp);
+            SAIX_LAUNCHED();
+            return SAIX_OK;
+        }
+        // highly repetitive text: Kasai below
+        if (best) SAIX_CUDA(cudaMemsetAsync(best, 0, sizeof(u32), st));
+    }
     return lcp_run(text, text_bytes, n, sa, lcp, phi, seeds, plcp8, st, boundary, best, phi_ready);
 }
 
@@ -216,6 +407,9 @@ extern "C" size_t saix_lcp_workspace_bytes(int64_t n) {
     ar.alloc<u32>(n);
     ar.alloc<u32>(ceil_div(n > 0 ? n : 1, LCP_CHUNK) + 1);
     ar.alloc<u8>(n);
+    ar.alloc<u64>(pack2_words(n));
+    ar.alloc<u32>(2);
+    ar.alloc<u32>(lcp_list_cap(n));
     return ar.peak + Arena::kAlign;
 }
 
@@ -237,4 +431,23 @@ extern "C" int saix_lcp(const void *text, int text_bytes, int64_t n, const uint3
     }
     (void)isa;  // the Phi formulation needs only SA
     return lcp_compute(text, text_bytes, n, sa, lcp, ws, ws_bytes, (cudaStream_t)stream, -1, nullptr);
+}
+
+extern "C" int saix_lcp_sigma(const void *text, int text_bytes, int64_t n, int64_t sigma, int64_t separator,
+                              const uint32_t *sa, uint32_t *lcp, void *ws, size_t ws_bytes, void *stream) {
+    if (n < 0 || (text_bytes != 1 && text_bytes != 4) || (n > 0 && (!text || !sa || !lcp)) || separator >= n) {
+        set_error("saix_lcp_sigma: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    if (ws_bytes < saix_lcp_workspace_bytes(n)) {
+        set_error("saix_lcp_sigma: workspace too small");
+        return SAIX_ENOSPC;
+    }
+    if (n == 0) return SAIX_OK;
+    if (text_bytes == 1 && ((uintptr_t)text & 15)) {
+        set_error("saix_lcp_sigma: u8 text must be 16-byte aligned");
+        return SAIX_EINVAL;
+    }
+    return lcp_compute(text, text_bytes, n, sa, lcp, ws, ws_bytes, (cudaStream_t)stream, -1, nullptr, nullptr, false,
+                       sigma, separator);
 }

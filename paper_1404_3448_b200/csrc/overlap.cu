@@ -422,12 +422,12 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
     SAIX_ARENA_OK(ar);
     SAIX_TRY(saix_encode_gsa(a_ascii, na, b_ascii, nb, keep_n, w.gsa, bad_pos, stream));
     int sigma = (keep_n ? 5 : 4) + 1;  // max(sigma_A, sigma_B) + 1 (overlap.py:88)
-    // the pipeline never needs the top-level ISA (LCP runs on Phi/SA); the
-    // streaming level-0 merge emits Phi through the bucketed scatter
-    bool phi_done = false;
-    SAIX_TRY(dc3_compute(w.gsa, 1, n, sigma, w.sa, nullptr, w.rest, w.rest_bytes, nullptr, st, w.phi, &phi_done));
+    // the pipeline never needs the top-level ISA (LCP compares SA neighbours)
+    SAIX_TRY(dc3_compute(w.gsa, 1, n, sigma, w.sa, nullptr, w.rest, w.rest_bytes, nullptr, st));
     SAIX_CUDA(cudaMemsetAsync(w.ov.best, 0, sizeof(u32), st));
-    SAIX_TRY(lcp_compute(w.gsa, 1, n, w.sa, w.lcp, w.rest, w.rest_bytes, st, na, w.ov.best, w.phi, phi_done));
+    // direct word-compare LCP on the 2-bit packed GSA (separator at na);
+    // N residues (keep_n) fall back to the byte compare / Kasai
+    SAIX_TRY(lcp_compute(w.gsa, 1, n, w.sa, w.lcp, w.rest, w.rest_bytes, st, na, w.ov.best, w.phi, false, sigma, na));
     return overlap_scan(w.sa, w.lcp, n, na, out3, w.ov, st, true);
 }
 

@@ -182,9 +182,9 @@ def lcp_device(ix: DeviceIndex):
     n = ix.text.n
     lcp = _lib.empty(n, t.int32)
     ws = _lib.workspace(L.saix_lcp_workspace_bytes(n))
-    rc = L.saix_lcp(_lib.ptr(ix.text.t), ix.text.bytes, n, _lib.ptr(ix.sa), _lib.ptr(ix.isa),
-                    _lib.ptr(lcp), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
-    _lib.check(rc, "saix_lcp")
+    rc = L.saix_lcp_sigma(_lib.ptr(ix.text.t), ix.text.bytes, n, ix.text.sigma, -1, _lib.ptr(ix.sa),
+                          _lib.ptr(lcp), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+    _lib.check(rc, "saix_lcp_sigma")
     return lcp
 
 
@@ -323,8 +323,8 @@ class SuffixIndexer:
         s = _lib.stream_ptr()
         _lib.check(L.saix_dc3(_lib.ptr(self.t), self.bytes, self.n, self.sigma, _lib.ptr(self.sa),
                               _lib.ptr(self.isa), _lib.ptr(self.ws), self.ws.numel(), None, s), "saix_dc3")
-        _lib.check(L.saix_lcp(_lib.ptr(self.t), self.bytes, self.n, _lib.ptr(self.sa), None,
-                              _lib.ptr(self.lcp), _lib.ptr(self.ws), self.ws.numel(), s), "saix_lcp")
+        _lib.check(L.saix_lcp_sigma(_lib.ptr(self.t), self.bytes, self.n, self.sigma, -1, _lib.ptr(self.sa),
+                                    _lib.ptr(self.lcp), _lib.ptr(self.ws), self.ws.numel(), s), "saix_lcp_sigma")
 
     def run_staged(self) -> None:
         n = self.n
