@@ -281,3 +281,62 @@ class TestLargeAlphabets:
         sa, rank = oracle.dc3(r, sigma)
         assert np.array_equal(ix.sa, sa) and np.array_equal(ix.rank, rank)
         assert np.array_equal(sx.build_lcp(t, ix).lcp, oracle.lcp(r, sa, rank))
+
+
+class TestDirectLcp:
+    """Word-compare LCP (lcp.cu k_lcp_direct): 2-bit packed and byte texts,
+    the capped-entry extension, the separator clamp and the Kasai fallback."""
+
+    @pytest.mark.parametrize("n", [2, 3, 31, 32, 33, 63, 64, 65, 95, 96, 97, 1000, 4097])
+    def test_pack_tails(self, n):
+        t = encode(gen_random(n, 900 + n))
+        ix = sx.build_sa_dc3(t)
+        sa, rank = oracle.dc3(t.ranks, 4)
+        assert np.array_equal(sx.build_lcp(t, ix).lcp, oracle.lcp(t.ranks, sa, rank))
+
+    @pytest.mark.parametrize("rep", [257, 400, 1500])
+    def test_long_repeat_extension(self, rep):
+        s = list(gen_random(100_000, 5).residues)
+        s[60_000:60_000 + rep] = s[10_000:10_000 + rep]       # capped entries, < n/64 of them
+        t = text_of("".join(s))
+        ix = sx.build_sa_dc3(t)
+        sa, rank = oracle.dc3(t.ranks, 4)
+        assert np.array_equal(sx.build_lcp(t, ix).lcp, oracle.lcp(t.ranks, sa, rank))
+
+    @pytest.mark.parametrize("sigma", [5, 20, 255])
+    def test_byte_text(self, sigma):
+        rng = np.random.default_rng(sigma)
+        r = rng.integers(1, sigma + 1, size=50_000)
+        r[30_000:30_700] = r[1_000:1_700]
+        t = RankedText(r, sigma)
+        ix = sx.build_sa_dc3(t)
+        sa, rank = oracle.dc3(r, sigma)
+        assert np.array_equal(sx.build_lcp(t, ix).lcp, oracle.lcp(r, sa, rank))
+
+    @pytest.mark.parametrize("L", [300, 2000])
+    def test_overlap_long_block(self, L):
+        a = gen_random(100_000, 11).residues
+        b = list(gen_random(100_000, 12).residues)
+        b[50_000:50_000 + L] = a[7_000:7_000 + L]
+        b = "".join(b)
+        r = sx.longest_overlap(DnaSequence("a", a), DnaSequence("b", b))
+        assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a, b)
+        assert r.length >= L
+
+    def test_overlap_block_at_separator(self):
+        # A ends and B starts with the same block: matches run up to the separator
+        blk = gen_random(700, 3).residues
+        a = gen_random(5_000, 1).residues + blk
+        b = blk + gen_random(5_000, 2).residues
+        r = sx.longest_overlap(DnaSequence("a", a), DnaSequence("b", b))
+        assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a, b)
+
+    def test_overlap_keep_n_byte_path(self):
+        rng = random.Random(9)
+        a = "".join(rng.choice("ACGTN") for _ in range(20_000))
+        b = list("".join(rng.choice("ACGTN") for _ in range(20_000)))
+        b[9_000:9_500] = a[100:600]
+        b = "".join(b)
+        r = sx.longest_overlap(DnaSequence("a", a), DnaSequence("b", b), sx.NPolicy.KEEP)
+        assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a, b, keep_n=True)
+        assert r.length >= 500
