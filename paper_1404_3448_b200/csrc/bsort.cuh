@@ -1,36 +1,37 @@
-// bsort.cuh -- MSD bucket sort for large-alphabet keys.
+// bsort.cuh -- MSD bucket sort for wide keys (large-alphabet DC3 levels).
 //
-// Deep DC3 levels sort items whose leading key component ranges over a large
-// alphabet (level-2 names of DNA: ~2^18): LSD radix needs 7 passes of 8 bits
-// there, while an MSD split on the leading component leaves buckets of a few
-// dozen items.  Three streaming passes plus small in-shared-memory sorts:
-//   count    histogram of bucket ids (global atomics: buckets are many)
-//   scan     exclusive bucket starts
+// Deep DC3 levels sort items whose keys span a large range (level-2 triples
+// of DNA: 3 x 18-bit names); LSD radix needs 7 passes of 8 bits there.  Here
+// the key range is cut into ~n/8 equal buckets (bucket = key >> shift, a
+// monotone function of the key), so buckets hold a handful of items each:
+//   count    histogram of bucket ids (global atomics, L2-resident counters)
+//   scan     exclusive bucket starts; buckets of > 32 items are listed
 //   scatter  item -> its bucket's next slot (atomic cursor; order inside a
 //            bucket is arbitrary and fixed by the segment sort)
-//   segsort  warp-per-bucket bitonic sort in shared memory (<= 256 items),
-//            CTA-per-bucket bitonic (<= 4096); larger buckets are reported
-//            so the caller can fall back to a full LSD sort.
-// Sources: struct { __device__ void get(i64 i, u32 &bucket, u64 &key, u32 &val) const; }
-// with the bucket a monotone function of the key (e.g. its top component);
-// the result is sorted by key (ties in any order).
+//   segsort  <= 32 items: one warp, register bitonic via shuffles;
+//            <= 1024: one warp, bitonic in shared memory;
+//            <= 4096: one CTA; larger buckets are reported so the caller can
+//            fall back to a full LSD sort.
+// Sources: struct { __device__ void get(i64 i, u64 &key, u32 &val) const; }
+// with keys in [0, max_key]; the result is sorted by key (ties in any order).
 #pragma once
 
 #include "scan.cuh"
 
 namespace saix {
 
-constexpr int BS_SMALL = 256;   // warp-per-bucket limit
+constexpr int BS_TINY = 32;     // register bitonic limit
+constexpr int BS_SMALL = 1024;  // warp-per-bucket (shared memory) limit
 constexpr int BS_LARGE = 4096;  // CTA-per-bucket limit
+constexpr int BS_WARPS = 8;
 
 template <class Src>
-__global__ void k_bs_count(Src src, i64 n, u32 *__restrict__ cnt) {
+__global__ void k_bs_count(Src src, i64 n, int shift, u32 *__restrict__ cnt) {
     for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-        u32 b;
         u64 k;
         u32 v;
-        src.get(i, b, k, v);
-        atomicAdd(&cnt[b], 1u);
+        src.get(i, k, v);
+        atomicAdd(&cnt[k >> shift], 1u);
     }
 }
 
@@ -38,32 +39,82 @@ struct BsCntIn {
     const u32 *cnt;
     __device__ u32 operator()(i64 i) const { return cnt[i]; }
 };
-// bucket starts + cursor copy; buckets beyond BS_SMALL are listed for the
-// CTA-per-bucket pass and the largest size is recorded
+// bucket starts + cursor copy; buckets beyond BS_TINY are listed (medium /
+// large) and the largest size is recorded
 struct BsStartOut {
-    const u32 *cnt;
-    u32 *start, *cursor, *big_list, *big_count, *max_size;
+    u32 *start, *cursor, *mid_list, *big_list, *scal;  // scal: [0] mid count, [1] big count, [2] max size
     __device__ void operator()(i64 i, u32 excl, u32 v) const {
         start[i] = excl;
         cursor[i] = excl;
-        if (v > BS_SMALL) {
-            big_list[atomicAdd(big_count, 1u)] = (u32)i;
-            atomicMax(max_size, v);
+        if (v > BS_TINY) {
+            if (v <= BS_SMALL) mid_list[atomicAdd(&scal[0], 1u)] = (u32)i;
+            else big_list[atomicAdd(&scal[1], 1u)] = (u32)i;
+            atomicMax(&scal[2], v);
         }
     }
 };
 
 template <class Src>
-__global__ void k_bs_scatter(Src src, i64 n, u32 *__restrict__ cursor, u64 *__restrict__ keys,
+__global__ void k_bs_scatter(Src src, i64 n, int shift, u32 *__restrict__ cursor, u64 *__restrict__ keys,
                              u32 *__restrict__ vals) {
     for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-        u32 b;
         u64 k;
         u32 v;
-        src.get(i, b, k, v);
-        u32 at = atomicAdd(&cursor[b], 1u);
+        src.get(i, k, v);
+        u32 at = atomicAdd(&cursor[k >> shift], 1u);
         keys[at] = k;
         vals[at] = v;
+    }
+}
+
+// ascending bitonic sort of one (key, val) per lane across the warp
+__device__ __forceinline__ void warp_bitonic32(u64 &k, u32 &v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            u64 ok = __shfl_xor_sync(0xffffffffu, k, stride);
+            u32 ov = __shfl_xor_sync(0xffffffffu, v, stride);
+            bool up = (lane & size) == 0 || size == 32;
+            bool lower = (lane & stride) == 0;
+            bool take = (lower == up) ? (ok < k) : (ok > k);
+            if (take) {
+                k = ok;
+                v = ov;
+            }
+        }
+    }
+}
+
+// buckets of <= 32 items: a warp takes 32 consecutive buckets (coalesced
+// count/start reads) and sorts them one after another in registers
+__global__ void __launch_bounds__(256)
+k_bs_tiny(const u32 *__restrict__ start, const u32 *__restrict__ cnt, i64 nb, u64 *__restrict__ keys,
+          u32 *__restrict__ vals) {
+    const int lane = lane_id();
+    const i64 warps = ((i64)gridDim.x * blockDim.x) >> 5;
+    for (i64 b0 = (((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; b0 < nb; b0 += warps * 32) {
+        u32 my_len = b0 + lane < nb ? cnt[b0 + lane] : 0u;
+        u32 my_s0 = b0 + lane < nb ? start[b0 + lane] : 0u;
+        u32 todo = __ballot_sync(0xffffffffu, my_len > 1 && my_len <= BS_TINY);
+        while (todo) {
+            int q = __ffs(todo) - 1;
+            todo &= todo - 1;
+            u32 len = __shfl_sync(0xffffffffu, my_len, q);
+            u32 s0 = __shfl_sync(0xffffffffu, my_s0, q);
+            u64 k = ~0ull;
+            u32 v = 0xFFFFFFFFu;
+            if ((u32)lane < len) {
+                k = keys[s0 + lane];
+                v = vals[s0 + lane];
+            }
+            warp_bitonic32(k, v);
+            if ((u32)lane < len) {
+                keys[s0 + lane] = k;
+                vals[s0 + lane] = v;
+            }
+        }
     }
 }
 
@@ -99,32 +150,33 @@ __device__ __forceinline__ void bitonic_smem(u64 *sk, u32 *sv, int len, int tid,
     }
 }
 
-constexpr int BS_WARPS = 8;
-
-// one warp per bucket of <= BS_SMALL items
+// one warp per listed bucket of BS_TINY < size <= BS_SMALL items
 __global__ void __launch_bounds__(32 * BS_WARPS)
-k_bs_small(const u32 *__restrict__ start, const u32 *__restrict__ cnt, i64 nb, u64 *__restrict__ keys,
-           u32 *__restrict__ vals) {
-    __shared__ u64 sk[BS_WARPS][BS_SMALL];
-    __shared__ u32 sv[BS_WARPS][BS_SMALL];
+k_bs_small(const u32 *__restrict__ start, const u32 *__restrict__ cnt, const u32 *__restrict__ list,
+           const u32 *__restrict__ list_len, u64 *__restrict__ keys, u32 *__restrict__ vals) {
+    extern __shared__ __align__(16) unsigned char bs_small_smem[];
     int w = threadIdx.x >> 5, lane = lane_id();
-    for (i64 b = (i64)blockIdx.x * BS_WARPS + w; b < nb; b += (i64)gridDim.x * BS_WARPS) {
-        u32 len = cnt[b];
-        if (len <= 1 || len > BS_SMALL) continue;
-        u32 s0 = start[b];
+    u64 *sk = reinterpret_cast<u64 *>(bs_small_smem) + (size_t)w * BS_SMALL;
+    u32 *sv = reinterpret_cast<u32 *>(reinterpret_cast<u64 *>(bs_small_smem) + (size_t)BS_WARPS * BS_SMALL) +
+              (size_t)w * BS_SMALL;
+    const u32 nl = *list_len;
+    for (u32 q = blockIdx.x * BS_WARPS + w; q < nl; q += gridDim.x * BS_WARPS) {
+        u32 b = list[q];
+        u32 len = cnt[b], s0 = start[b];
         for (u32 x = lane; x < len; x += 32) {
-            sk[w][x] = keys[s0 + x];
-            sv[w][x] = vals[s0 + x];
+            sk[x] = keys[s0 + x];
+            sv[x] = vals[s0 + x];
         }
         __syncwarp();
-        bitonic_smem(sk[w], sv[w], (int)len, lane, 32, true);
+        bitonic_smem(sk, sv, (int)len, lane, 32, true);
         for (u32 x = lane; x < len; x += 32) {
-            keys[s0 + x] = sk[w][x];
-            vals[s0 + x] = sv[w][x];
+            keys[s0 + x] = sk[x];
+            vals[s0 + x] = sv[x];
         }
         __syncwarp();
     }
 }
+constexpr size_t BS_SMALL_SMEM = (size_t)BS_WARPS * BS_SMALL * 12;
 
 // one CTA per listed bucket of BS_SMALL < size <= BS_LARGE items
 __global__ void __launch_bounds__(256)
@@ -152,46 +204,74 @@ k_bs_large(const u32 *__restrict__ start, const u32 *__restrict__ cnt, const u32
     }
 }
 
-// scratch words: cnt, start, cursor (nb each), big list (nb), 3 scalars, scan tmp
-inline i64 bs_scratch_words(i64 nb) { return 4 * (nb + 1) + 8 + scan_tmp_words(nb) + 64; }
+// Bucket geometry: ~n/8 buckets (at most 2^23) over [0, max_key].
+struct BsGeom {
+    int shift;
+    i64 nb;
+};
+inline BsGeom bs_geom(u64 max_key, i64 n) {
+    i64 want = n / 8 > 1 ? n / 8 : 1;
+    if (want > ((i64)1 << 23)) want = (i64)1 << 23;
+    int shift = 0;
+    while ((i64)(max_key >> shift) + 1 > want) shift++;
+    return BsGeom{shift, (i64)(max_key >> shift) + 1};
+}
 
-// Returns false (after the count pass only) when some bucket exceeds
+// scratch words: cnt, start, cursor, mid list, big list (nb + 1 each), scalars, scan tmp
+inline i64 bs_scratch_words(i64 nb) { return 5 * (nb + 1) + 8 + scan_tmp_words(nb) + 64; }
+inline i64 bs_scratch_words_for(u64 max_key, i64 n) { return bs_scratch_words(bs_geom(max_key, n).nb); }
+
+// Returns ok = false (after the count pass only) when some bucket exceeds
 // BS_LARGE; the caller then sorts with onesweep instead.  One host sync.
 template <class Src>
-int bucket_sort(Src src, i64 n, i64 nb, u64 *keys, u32 *vals, u32 *scratch, bool &ok, cudaStream_t st,
+int bucket_sort(Src src, i64 n, u64 max_key, u64 *keys, u32 *vals, u32 *scratch, bool &ok, cudaStream_t st,
                 const char *prof = "bsort") {
     ok = true;
     if (n <= 0) return SAIX_OK;
+    BsGeom g = bs_geom(max_key, n);
+    const i64 nb = g.nb;
     Prof prof_(prof, 24.0 * n + 16.0 * nb, st);
-    u32 *cnt = scratch, *start = cnt + (nb + 1), *cursor = start + (nb + 1), *list = cursor + (nb + 1);
-    u32 *scal = list + (nb + 1);  // [0] big count, [1] max size
+    u32 *cnt = scratch, *start = cnt + (nb + 1), *cursor = start + (nb + 1), *mid = cursor + (nb + 1);
+    u32 *big = mid + (nb + 1);
+    u32 *scal = big + (nb + 1);  // [0] mid count, [1] big count, [2] max size
     u32 *tmp = scal + 8;
     SAIX_CUDA(cudaMemsetAsync(cnt, 0, (size_t)(nb + 1) * 4, st));
     SAIX_CUDA(cudaMemsetAsync(scal, 0, 8 * 4, st));
-    int g = grid_for(n, 256);
-    k_bs_count<Src><<<g, 256, 0, st>>>(src, n, cnt);
+    int gr = grid_for(n, 256);
+    k_bs_count<Src><<<gr, 256, 0, st>>>(src, n, g.shift, cnt);
     SAIX_LAUNCHED();
-    SAIX_TRY(scan_transform(BsCntIn{cnt}, BsStartOut{cnt, start, cursor, list, scal, scal + 1}, nb, tmp, nullptr, st,
+    SAIX_TRY(scan_transform(BsCntIn{cnt}, BsStartOut{start, cursor, mid, big, scal}, nb, tmp, nullptr, st,
                             "bsort.scan", 16.0 * nb));
-    u32 h[2];
-    SAIX_CUDA(cudaMemcpyAsync(h, scal, 8, cudaMemcpyDeviceToHost, st));
+    u32 h[3];
+    SAIX_CUDA(cudaMemcpyAsync(h, scal, 12, cudaMemcpyDeviceToHost, st));
     SAIX_CUDA(cudaStreamSynchronize(st));
-    if (h[1] > (u32)BS_LARGE) {
+    if (h[2] > (u32)BS_LARGE) {
         ok = false;
         return SAIX_OK;
     }
-    k_bs_scatter<Src><<<g, 256, 0, st>>>(src, n, cursor, keys, vals);
+    k_bs_scatter<Src><<<gr, 256, 0, st>>>(src, n, g.shift, cursor, keys, vals);
     SAIX_LAUNCHED();
-    k_bs_small<<<grid_for(nb, 32 * BS_WARPS, kNumSMs * 64), 32 * BS_WARPS, 0, st>>>(start, cnt, nb, keys, vals);
+    k_bs_tiny<<<grid_for(ceil_div(nb, 32) * 32, 256, kNumSMs * 16), 256, 0, st>>>(start, cnt, nb, keys, vals);
     SAIX_LAUNCHED();
     if (h[0]) {
+        static bool attr = false;
+        if (!attr) {
+            SAIX_CUDA(cudaFuncSetAttribute(k_bs_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BS_SMALL_SMEM));
+            attr = true;
+        }
+        u32 blocks = (h[0] + BS_WARPS - 1) / BS_WARPS;
+        k_bs_small<<<blocks < 2 * kNumSMs ? blocks : 2 * kNumSMs, 32 * BS_WARPS, BS_SMALL_SMEM, st>>>(start, cnt, mid,
+                                                                                                   scal, keys, vals);
+        SAIX_LAUNCHED();
+    }
+    if (h[1]) {
         static bool attr = false;
         size_t smem = (size_t)BS_LARGE * 12;
         if (!attr) {
             SAIX_CUDA(cudaFuncSetAttribute(k_bs_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr = true;
         }
-        k_bs_large<<<h[0] < 4 * kNumSMs ? h[0] : 4 * kNumSMs, 256, smem, st>>>(start, cnt, list, scal, keys, vals);
+        k_bs_large<<<h[1] < 4 * kNumSMs ? h[1] : 4 * kNumSMs, 256, smem, st>>>(start, cnt, big, scal + 1, keys, vals);
         SAIX_LAUNCHED();
     }
     return SAIX_OK;

@@ -162,37 +162,33 @@ struct Mod0HistSrc {
     }
 };
 
-// bucket-sort sources (large alphabets, bsort.cuh): bucket = leading char
+// bucket-sort sources (wide keys, bsort.cuh): mixed-radix keys, bucketed by
+// their top bits
 template <typename TT>
 struct TripleBucketSrc {
     Text<TT> T;
     SampleLayout L;
     u64 s1;
-    __device__ __forceinline__ void get(i64 s, u32 &b, u64 &k, u32 &v) const {
+    __device__ __forceinline__ void get(i64 s, u64 &k, u32 &v) const {
         i64 p = L.pos(s);
-        u32 c0 = T(p);
-        b = c0;
-        k = ((u64)c0 * s1 + T(p + 1)) * s1 + T(p + 2);
+        k = ((u64)T(p) * s1 + T(p + 1)) * s1 + T(p + 2);
         v = (u32)s;
     }
 };
-// mod-0 suffix 3j keyed by (T(3j), R(3j+1)); streamed in text order
+// mod-0 suffix 3j keyed by (T(3j), R(3j+1)) = T(3j) * (m+1) + ISAc[j] + 1;
+// streamed in text order (the keys are distinct)
 template <typename TT>
 struct Mod0BucketSrc {
     Text<TT> T;
     const u32 *isac;
-    __device__ __forceinline__ void get(i64 j, u32 &b, u64 &k, u32 &v) const {
-        u32 c = T(3 * j);
-        b = c;
-        k = ((u64)c << 32) | (__ldcs(isac + j) + 1u);
+    u64 m1;  // m + 1
+    __device__ __forceinline__ void get(i64 j, u64 &k, u32 &v) const {
+        k = (u64)T(3 * j) * m1 + (__ldcs(isac + j) + 1u);
         v = (u32)j;
     }
 };
-// bucket sort pays off when the leading alphabet is large and buckets small;
-// the bucket arrays are sized by the item count (scratch: bs_scratch_words(N+1))
-static bool use_bsort(u64 sigma, i64 n) {
-    return sigma + 1 >= 4096 && (i64)(sigma + 1) <= n && n / (i64)(sigma + 1) <= 512;
-}
+// bucket sort replaces LSD radix when the keys are wide
+static bool use_bsort(u64 max_key, i64 n) { return n >= 4096 && bits_for(max_key) > 24; }
 
 // wide-alphabet naming sources (3 bits(sigma) > 64)
 template <typename TT>
@@ -980,6 +976,31 @@ __global__ void k_isa_from_names(const u32 *__restrict__ tt, i64 m, u32 *__restr
         isac[s] = __ldcs(tt + s) - 1u;
 }
 
+// all names distinct after a sort: SAc = the sorted sample order (streamed
+// copy) and ISAc through the bucketed scatter (pass A here)
+constexpr int UE_ITEMS = 8;
+__global__ void __launch_bounds__(256)
+k_unique_emit(const u32 *__restrict__ vals, i64 m, u32 *__restrict__ sac, PsPlan plan, uint2 *__restrict__ stage) {
+    extern __shared__ __align__(16) unsigned char ue_smem[];
+    uint2 *sh_items = reinterpret_cast<uint2 *>(ue_smem);
+    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_items + 256 * UE_ITEMS);
+    u32 *sh_base = sh_cnt + plan.a.buckets;
+    const i64 r0 = (i64)blockIdx.x * (256 * UE_ITEMS);
+    uint2 it[UE_ITEMS];
+    bool ok[UE_ITEMS];
+#pragma unroll
+    for (int q = 0; q < UE_ITEMS; q++) {
+        i64 r = r0 + q * 256 + threadIdx.x;
+        ok[q] = r < m;
+        if (ok[q]) {
+            u32 sidx = __ldcs(vals + r);
+            if (sac) __stcs(sac + r, sidx);
+            it[q] = make_uint2(sidx, (u32)r);
+        }
+    }
+    ps_block_emit<uint2, 256, UE_ITEMS>(it, ok, plan.a, stage, sh_items, sh_cnt, sh_base);
+}
+
 inline bool stream_level_ok(int text_bytes, u64 sigma, i64 N, const saix_dc3_probe *probe) {
     return text_bytes == 1 && sigma + 1 <= 256 && probe == nullptr && N < ((i64)3 << 29);
 }
@@ -1083,8 +1104,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         int b = bits_for(sigma);
         u64 *k0 = ar.alloc<u64>(m), *k1 = ar.alloc<u64>(m);
         u32 *v0 = ar.alloc<u32>(m), *v1 = ar.alloc<u32>(m);
-        u32 *scratch = ar.alloc<u32>(os_scratch_words(m) > bs_scratch_words(L.n + 1) ? os_scratch_words(m)
-                                                                                  : bs_scratch_words(L.n + 1));
+        u32 *scratch = ar.alloc<u32>(os_scratch_words(m) > bs_scratch_words(L.n / 8 + 2) ? os_scratch_words(m)
+                                                                                  : bs_scratch_words(L.n / 8 + 2));
         u32 *tmp = ar.alloc<u32>(scan_tmp_words(m));
         SAIX_ARENA_OK(ar);
         u64 *keys = k0;
@@ -1095,8 +1116,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             int passes = (kb + OS_BITS - 1) / OS_BITS;
             TripleSrc<TT> src{T, L, s1};
             bool done = false;
-            if (use_bsort(sigma, m)) {
-                SAIX_TRY(bucket_sort(TripleBucketSrc<TT>{T, L, s1}, m, (i64)s1, k0, v0, scratch, done, st,
+            if (use_bsort(s1 * s1 * s1 - 1, m)) {
+                SAIX_TRY(bucket_sort(TripleBucketSrc<TT>{T, L, s1}, m, s1 * s1 * s1 - 1, k0, v0, scratch, done, st,
                                      "dc3.triple_sort"));
                 keys = k0;
                 vals = v0;
@@ -1138,11 +1159,32 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         sorted_vals = vals;
     }
     if ((i64)D == m) {
-        Prof prof_("dc3.unique_ranks", 12.0 * m, st);
-        if (sorted_vals) k_unique_from_sorted<<<g, K_THREADS, 0, st>>>(sorted_vals, m, SAc, ISAc);
-        else if (SAc) k_unique_from_names<<<g, K_THREADS, 0, st>>>(tt, m, SAc, ISAc);
-        else k_isa_from_names<<<g, K_THREADS, 0, st>>>(tt, m, ISAc);
-        SAIX_LAUNCHED();
+        if (sorted_vals && m > ((i64)1 << 20)) {
+            PsPlan pu = PsPlan::of(m, 4);
+            pu.set_cursors(ar.alloc<u32>(pu.cursor_words()));
+            uint2 *s1 = ar.alloc<uint2>(pu.stage1_items()), *s2 = ar.alloc<uint2>(pu.stage2_items());
+            SAIX_ARENA_OK(ar);
+            SAIX_CUDA(cudaMemsetAsync(pu.a.cursor, 0, (size_t)pu.cursor_words() * 4, st));
+            {
+                Prof prof_("dc3.unique_ranks", (SAc ? 16.0 : 12.0) * m, st);
+                static bool attr = false;
+                if (!attr) {
+                    SAIX_CUDA(cudaFuncSetAttribute(k_unique_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   256 * UE_ITEMS * 8 + 8 * PS_MAX_BUCKETS));
+                    attr = true;
+                }
+                size_t smem = (size_t)256 * UE_ITEMS * 8 + 8 * (size_t)pu.a.buckets;
+                k_unique_emit<<<(unsigned)ceil_div(m, 256 * UE_ITEMS), 256, smem, st>>>(sorted_vals, m, SAc, pu, s1);
+            }
+            SAIX_LAUNCHED();
+            SAIX_TRY(ps_finish(s1, s2, pu, U32Apply{ISAc}, st, "dc3.unique_isa", 28.0 * m));
+        } else {
+            Prof prof_("dc3.unique_ranks", 12.0 * m, st);
+            if (sorted_vals) k_unique_from_sorted<<<g, K_THREADS, 0, st>>>(sorted_vals, m, SAc, ISAc);
+            else if (SAc) k_unique_from_names<<<g, K_THREADS, 0, st>>>(tt, m, SAc, ISAc);
+            else k_isa_from_names<<<g, K_THREADS, 0, st>>>(tt, m, ISAc);
+            SAIX_LAUNCHED();
+        }
         ar.reset(mark);
     } else {
         ar.reset(mark);
@@ -1187,8 +1229,8 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     i64 k = L.k;
     u32 *k0 = ar.alloc<u32>(k), *k1 = ar.alloc<u32>(k);
     u32 *v0 = ar.alloc<u32>(k), *v1 = ar.alloc<u32>(k);
-    u32 *scratch = ar.alloc<u32>(os_scratch_words(L.m) > bs_scratch_words(N + 1) ? os_scratch_words(L.m)
-                                                                                  : bs_scratch_words(N + 1));
+    u32 *scratch = ar.alloc<u32>(os_scratch_words(L.m) > bs_scratch_words(N / 8 + 2) ? os_scratch_words(L.m)
+                                                                                  : bs_scratch_words(N / 8 + 2));
     u32 *split = ar.alloc<u32>(merge_split_words(N));
     SAIX_ARENA_OK(ar);
     u32 *keys = k0, *vals = v0;
@@ -1208,12 +1250,13 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
         SAIX_LAUNCHED();
     } else {
         bool done = false;
-        if (use_bsort(sigma, k)) {
+        u64 mk = (u64)sigma * (u64)(L.m + 1) + (u64)L.m;
+        if (sigma + 1 > 256 && use_bsort(mk, k)) {
             // the (char, rank) keys are distinct, so an unstable bucket split
             // followed by in-bucket sorts gives the exact order
             u64 *k64 = ar.alloc<u64>(k);
             SAIX_ARENA_OK(ar);
-            SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc}, k, (i64)sigma + 1, k64, v0, scratch, done, st,
+            SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc, (u64)L.m + 1}, k, mk, k64, v0, scratch, done, st,
                                  "dc3.mod0_split"));
             vals = v0;
         }
@@ -1399,8 +1442,11 @@ static size_t dc3_plan(i64 n) {
         SampleLayout L = SampleLayout::of(N);
         i64 m = L.m, k = L.k;
         persistent += (size_t)(3 * m + 8) * 4 + (size_t)N * 4 + 5 * Arena::kAlign;
-        i64 sw = os_scratch_words(m) > bs_scratch_words(N + 1) ? os_scratch_words(m) : bs_scratch_words(N + 1);
-        size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4;
+        i64 sw = os_scratch_words(m) > bs_scratch_words(N / 8 + 2) ? os_scratch_words(m) : bs_scratch_words(N / 8 + 2);
+        PsPlan pu = PsPlan::of(m, 4);
+        size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4 +
+                        (size_t)(pu.stage1_items() + pu.stage2_items()) * 8 + (size_t)pu.cursor_words() * 4 +
+                        4 * Arena::kAlign;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
         i64 bw = mod0_bitmap_words(7, m);
