@@ -16,6 +16,7 @@
 // with keys in [0, max_key]; the result is sorted by key (ties in any order).
 #pragma once
 
+#include "pscatter.cuh"
 #include "scan.cuh"
 
 namespace saix {
@@ -65,6 +66,70 @@ __global__ void k_bs_scatter(Src src, i64 n, int shift, u32 *__restrict__ cursor
         keys[at] = k;
         vals[at] = v;
     }
+}
+
+// Large inputs: the same scatter, its writes through the bucketed scatter
+// (pscatter.cuh) instead of random 12 B stores -- pass A item
+// {slot, val, key lo, key hi}; pass B writes keys/vals windows as full lines.
+constexpr int BSE_ITEMS = 8;
+template <class Src>
+__global__ void __launch_bounds__(256)
+k_bs_scatter_emit(Src src, i64 n, int shift, u32 *__restrict__ cursor, PsPlan plan, uint4 *__restrict__ stage) {
+    extern __shared__ __align__(16) unsigned char bse_smem[];
+    uint4 *sh_items = reinterpret_cast<uint4 *>(bse_smem);
+    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_items + 256 * BSE_ITEMS);
+    u32 *sh_base = sh_cnt + plan.a.buckets;
+    const i64 i0 = (i64)blockIdx.x * (256 * BSE_ITEMS);
+    uint4 it[BSE_ITEMS];
+    bool ok[BSE_ITEMS];
+#pragma unroll
+    for (int q = 0; q < BSE_ITEMS; q++) {
+        i64 i = i0 + q * 256 + threadIdx.x;
+        ok[q] = i < n;
+        if (ok[q]) {
+            u64 k;
+            u32 v;
+            src.get(i, k, v);
+            u32 at = atomicAdd(&cursor[k >> shift], 1u);
+            it[q] = make_uint4(at, v, (u32)k, (u32)(k >> 32));
+        }
+    }
+    ps_block_emit<uint4, 256, BSE_ITEMS>(it, ok, plan.a, stage, sh_items, sh_cnt, sh_base);
+}
+
+__global__ void __launch_bounds__(PS_THREADS)
+k_bs_window(const uint4 *__restrict__ stage2, PsPlan plan, u64 *__restrict__ keys, u32 *__restrict__ vals) {
+    extern __shared__ __align__(16) unsigned char ps_smem[];
+    uint4 *win = reinterpret_cast<uint4 *>(ps_smem);
+    const i64 w = blockIdx.x;
+    const i64 d0 = w << plan.s2;
+    const i64 len = (d0 + ((i64)1 << plan.s2) < plan.n_dest ? d0 + ((i64)1 << plan.s2) : plan.n_dest) - d0;
+    const i64 cnt = plan.cursor2[w];
+    const uint4 *src = stage2 + d0;
+    if (cnt == len) {
+        for (i64 x = threadIdx.x; x < cnt; x += PS_THREADS) {
+            uint4 v = ld_stream(src + x);
+            win[(i64)v.x - d0] = v;
+        }
+        __syncthreads();
+        for (i64 x = threadIdx.x; x < len; x += PS_THREADS) {
+            uint4 v = win[x];
+            keys[d0 + x] = ((u64)v.w << 32) | v.z;
+            vals[d0 + x] = v.y;
+        }
+    } else {
+        for (i64 x = threadIdx.x; x < cnt; x += PS_THREADS) {
+            uint4 v = ld_stream(src + x);
+            keys[v.x] = ((u64)v.w << 32) | v.z;
+            vals[v.x] = v.y;
+        }
+    }
+}
+// bytes of arena space bucket_sort takes for the bucketed scatter
+inline size_t bs_ps_bytes(i64 n) {
+    if (n < ((i64)1 << 20)) return 0;
+    PsPlan p = PsPlan::of(n, 16);
+    return (size_t)(p.stage1_items() + p.stage2_items()) * 16 + (size_t)p.cursor_words() * 4 + 4 * Arena::kAlign;
 }
 
 // ascending bitonic sort of one (key, val) per lane across the warp
@@ -225,7 +290,7 @@ inline i64 bs_scratch_words_for(u64 max_key, i64 n) { return bs_scratch_words(bs
 // BS_LARGE; the caller then sorts with onesweep instead.  One host sync.
 template <class Src>
 int bucket_sort(Src src, i64 n, u64 max_key, u64 *keys, u32 *vals, u32 *scratch, bool &ok, cudaStream_t st,
-                const char *prof = "bsort") {
+                const char *prof = "bsort", Arena *ar = nullptr) {
     ok = true;
     if (n <= 0) return SAIX_OK;
     BsGeom g = bs_geom(max_key, n);
@@ -249,8 +314,37 @@ int bucket_sort(Src src, i64 n, u64 max_key, u64 *keys, u32 *vals, u32 *scratch,
         ok = false;
         return SAIX_OK;
     }
-    k_bs_scatter<Src><<<gr, 256, 0, st>>>(src, n, g.shift, cursor, keys, vals);
-    SAIX_LAUNCHED();
+    if (ar && bs_ps_bytes(n)) {
+        size_t mark = ar->mark();
+        PsPlan pp = PsPlan::of(n, 16);
+        pp.set_cursors(ar->alloc<u32>(pp.cursor_words()));
+        uint4 *s1 = ar->alloc<uint4>(pp.stage1_items()), *s2 = ar->alloc<uint4>(pp.stage2_items());
+        SAIX_ARENA_OK(*ar);
+        SAIX_CUDA(cudaMemsetAsync(pp.a.cursor, 0, (size_t)pp.cursor_words() * 4, st));
+        static bool attr = false;
+        if (!attr) {
+            SAIX_CUDA(cudaFuncSetAttribute(k_bs_scatter_emit<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           256 * BSE_ITEMS * 16 + 8 * PS_MAX_BUCKETS));
+            SAIX_CUDA(cudaFuncSetAttribute(k_ps_refine<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(PS_REFINE_TILE * 16 + 8 * 256)));
+            SAIX_CUDA(cudaFuncSetAttribute(k_bs_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)PS_WINDOW_BYTES));
+            attr = true;
+        }
+        size_t smem = (size_t)256 * BSE_ITEMS * 16 + 8 * (size_t)pp.a.buckets;
+        k_bs_scatter_emit<Src><<<(unsigned)ceil_div(n, 256 * BSE_ITEMS), 256, smem, st>>>(src, n, g.shift, cursor, pp,
+                                                                                          s1);
+        SAIX_LAUNCHED();
+        size_t smem2 = (size_t)PS_REFINE_TILE * 16 + 8 * ((size_t)1 << (pp.a.shift - pp.s2));
+        k_ps_refine<uint4><<<(unsigned)ceil_div(pp.stage1_items(), PS_REFINE_TILE), PS_THREADS, smem2, st>>>(s1, pp, s2);
+        SAIX_LAUNCHED();
+        k_bs_window<<<(unsigned)pp.windows, PS_THREADS, (size_t)16 << pp.s2, st>>>(s2, pp, keys, vals);
+        SAIX_LAUNCHED();
+        ar->reset(mark);
+    } else {
+        k_bs_scatter<Src><<<gr, 256, 0, st>>>(src, n, g.shift, cursor, keys, vals);
+        SAIX_LAUNCHED();
+    }
     k_bs_tiny<<<grid_for(ceil_div(nb, 32) * 32, 256, kNumSMs * 16), 256, 0, st>>>(start, cnt, nb, keys, vals);
     SAIX_LAUNCHED();
     if (h[0]) {

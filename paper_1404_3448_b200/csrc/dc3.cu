@@ -1118,7 +1118,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             bool done = false;
             if (use_bsort(s1 * s1 * s1 - 1, m)) {
                 SAIX_TRY(bucket_sort(TripleBucketSrc<TT>{T, L, s1}, m, s1 * s1 * s1 - 1, k0, v0, scratch, done, st,
-                                     "dc3.triple_sort"));
+                                     "dc3.triple_sort", &ar));
                 keys = k0;
                 vals = v0;
             }
@@ -1257,7 +1257,7 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
             u64 *k64 = ar.alloc<u64>(k);
             SAIX_ARENA_OK(ar);
             SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc, (u64)L.m + 1}, k, mk, k64, v0, scratch, done, st,
-                                 "dc3.mod0_split"));
+                                 "dc3.mod0_split", &ar));
             vals = v0;
         }
         if (!done) {
@@ -1446,11 +1446,11 @@ static size_t dc3_plan(i64 n) {
         PsPlan pu = PsPlan::of(m, 4);
         size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4 +
                         (size_t)(pu.stage1_items() + pu.stage2_items()) * 8 + (size_t)pu.cursor_words() * 4 +
-                        4 * Arena::kAlign;
+                        4 * Arena::kAlign + bs_ps_bytes(m);
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
         i64 bw = mod0_bitmap_words(7, m);
-        size_t post_t = (size_t)k * 16 + (size_t)k * 32 + (size_t)k * 8 +
+        size_t post_t = (size_t)k * 16 + (size_t)k * 32 + (size_t)k * 8 + bs_ps_bytes(k) +
                         (size_t)(sw + merge_split_words(N) + 2 * bw + scan_tmp_words(bw)) * 4;
         // streaming level: RS + (record stage | M0 + partition scratch | M0 + split + pair stage)
         PsPlan pr = PsPlan::of(m, 16), pm = PsPlan::of(N, 4);
