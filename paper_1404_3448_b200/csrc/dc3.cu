@@ -753,39 +753,42 @@ k_rs_window(const uint4 *__restrict__ stage2, PsPlan plan, uint4 *__restrict__ r
 }
 
 // Mod-0 records of RS window w, stably partitioned by cprev: one tile of
-// 4096 ranks per CTA, warp-stable ranking (as in k_os_pass) with the global
-// per-(digit, window) offsets already known, so no look-back.
-constexpr int M0_ITEMS = 16;  // 256 threads x 16 = 4096 = 1 << RW_SHIFT
-__global__ void __launch_bounds__(256)
+// 4096 ranks per CTA (512 threads x 8), warp-stable ranking (as in
+// k_os_pass) with the global per-(digit, window) offsets already known, so
+// no look-back; the tile is staged digit-sorted in shared memory and written
+// as runs.
+constexpr int M0_THREADS = 512, M0_WARPS = M0_THREADS / 32;
+constexpr int M0_ITEMS = 8;  // 512 x 8 = 4096 = 1 << RW_SHIFT
+__global__ void __launch_bounds__(M0_THREADS)
 k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__restrict__ offs, uint4 *__restrict__ M0) {
     extern __shared__ __align__(16) unsigned char m0_smem[];
     uint4 *sv = reinterpret_cast<uint4 *>(m0_smem);
-    __shared__ u32 cnt[8][256];
+    u32(*cnt)[256] = reinterpret_cast<u32(*)[256]>(sv + (1 << RW_SHIFT));
     __shared__ u32 tile_excl[256], gbase[256], sh_warp[9];
     const int wp = threadIdx.x >> 5, lane = lane_id();
     for (int d = lane; d < 256; d += 32) cnt[wp][d] = 0;
     __syncthreads();
     const i64 w = blockIdx.x;
     const i64 seg = (w << RW_SHIFT) + (i64)wp * (32 * M0_ITEMS);
-    u32 pos[M0_ITEMS], nb[M0_ITEMS], c0[M0_ITEMS], dig[M0_ITEMS], rank[M0_ITEMS];
+    // per item: pos, nb, and c0 | digit << 8 | rank-in-digit << 17
+    u32 pos[M0_ITEMS], nb[M0_ITEMS], pk[M0_ITEMS];
     const u32 lt = lanemask_lt();
 #pragma unroll
     for (int r = 0; r < M0_ITEMS; r++) {
         i64 i = seg + r * 32 + lane;
-        dig[r] = 256u;
+        pk[r] = 256u << 8;
         if (i < m) {
             uint4 e = __ldcs(rs + i);
             if (e.x % 3 == 1) {
                 pos[r] = e.x;
                 nb[r] = e.y;
-                c0[r] = e.w & 0xFFu;
-                dig[r] = (e.w >> 16) & 0xFFu;
+                pk[r] = (e.w & 0xFFu) | (((e.w >> 16) & 0xFFu) << 8);
             }
         }
     }
 #pragma unroll
     for (int r = 0; r < M0_ITEMS; r++) {
-        u32 d = dig[r];
+        u32 d = (pk[r] >> 8) & 0x1FFu;
         bool ok = d < 256u;
         u32 peers = __match_any_sync(0xffffffffu, d);
         u32 before = __popc(peers & lt);
@@ -793,56 +796,58 @@ k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__res
         __syncwarp();
         if (ok && before == 0) cnt[wp][d] = cur + __popc(peers);
         __syncwarp();
-        rank[r] = cur + before;
+        pk[r] |= (cur + before) << 17;
     }
     __syncthreads();
-    {
-        const int d = threadIdx.x;
-        u32 run = 0;
+    // threads 0..255 own one digit each: warp-exclusive prefixes, tile counts
+    u32 run = 0, inc = 0;
+    const int d = threadIdx.x;
+    if (d < 256) {
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
+        for (int q = 0; q < M0_WARPS; q++) {
             u32 c = cnt[q][d];
             cnt[q][d] = run;
             run += c;
         }
         gbase[d] = run ? offs[(i64)d * windows + w] : 0u;
-        u32 inc = run;
+        inc = run;
         for (int o = 1; o < 32; o <<= 1) {
             u32 y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
         if (lane == 31) sh_warp[wp] = inc;
-        __syncthreads();
-        if (wp == 0) {
-            u32 x = lane < 8 ? sh_warp[lane] : 0u, xi = x;
-            for (int o = 1; o < 32; o <<= 1) {
-                u32 y = __shfl_up_sync(0xffffffffu, xi, o);
-                if (lane >= o) xi += y;
-            }
-            if (lane < 8) sh_warp[lane] = xi - x;
-            if (lane == 7) sh_warp[8] = xi;
-        }
-        __syncthreads();
-        tile_excl[d] = sh_warp[wp] + inc - run;
     }
+    __syncthreads();
+    if (wp == 0) {
+        u32 x = lane < 8 ? sh_warp[lane] : 0u, xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            u32 y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        if (lane < 8) sh_warp[lane] = xi - x;
+        if (lane == 7) sh_warp[8] = xi;
+    }
+    __syncthreads();
+    if (d < 256) tile_excl[d] = sh_warp[wp] + inc - run;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < M0_ITEMS; r++) {
-        u32 d = dig[r];
-        if (d < 256u) {
-            u32 lp = tile_excl[d] + cnt[wp][d] + rank[r];
+        u32 dg = (pk[r] >> 8) & 0x1FFu;
+        if (dg < 256u) {
+            u32 lp = tile_excl[dg] + cnt[wp][dg] + (pk[r] >> 17);
             i64 rk = seg + r * 32 + lane;  // 0-based sample rank of 3j+1
-            sv[lp] = make_uint4(pos[r] - 1, (u32)rk + 1u, nb[r], d | (c0[r] << 8));
+            sv[lp] = make_uint4(pos[r] - 1, (u32)rk + 1u, nb[r], dg | ((pk[r] & 0xFFu) << 8));
         }
     }
     __syncthreads();
     const u32 valid = sh_warp[8];
-    for (u32 x = threadIdx.x; x < valid; x += 256) {
+    for (u32 x = threadIdx.x; x < valid; x += M0_THREADS) {
         uint4 v = sv[x];
-        u32 d = v.w & 0xFFu;
-        __stcs(M0 + gbase[d] + (x - tile_excl[d]), v);
+        u32 dg = v.w & 0xFFu;
+        __stcs(M0 + gbase[dg] + (x - tile_excl[dg]), v);
     }
 }
+constexpr size_t M0_SMEM = ((size_t)16 << RW_SHIFT) + (size_t)M0_WARPS * 256 * 4;
 
 struct HistIn {
     const u32 *h;
@@ -876,6 +881,25 @@ __global__ void k_merge_partition_rec(RecMergeView v, i64 na, i64 nb, i64 ntiles
     }
 }
 
+// Comparison keys of the record merge (byte text): a non-sample b gets
+//   K1 = c0 << 32 | R(b+1)            (against mod-1 samples)
+//   K2 = (c0 << 8 | c1) << 32 | R(b+2) (against mod-2 samples)
+// and a sample its own form, mod-2 samples flagged in bit 63; then
+// recq_a_first(a, b) == keys_a_first(key(a), K1(b), K2(b)).
+constexpr u64 kMod2Flag = 1ull << 63;
+__device__ __forceinline__ u64 merge_key1(const uint4 &e) { return ((u64)(e.w & 0xFFu) << 32) | e.y; }
+__device__ __forceinline__ u64 merge_key2(const uint4 &e) {
+    return ((u64)(((e.w & 0xFFu) << 8) | ((e.w >> 8) & 0xFFu)) << 32) | e.z;
+}
+__device__ __forceinline__ u64 merge_key_sample(const uint4 &e) {
+    if (e.x % 3 == 1) return ((u64)(e.w & 0xFFu) << 32) | e.y;
+    u32 c01 = ((e.w & 0xFFu) << 8) | ((e.w >> 8) & 0xFFu);
+    return kMod2Flag | ((u64)c01 << 32) | e.z;
+}
+__device__ __forceinline__ bool keys_a_first(u64 ka, const u64 *B1, const u64 *B2, int j) {
+    return (ka & kMod2Flag) ? (ka & ~kMod2Flag) < B2[j] : ka < B1[j];
+}
+
 enum { EMIT_NONE = 0, EMIT_ISA = 1, EMIT_PHI = 2 };
 constexpr u32 kNoPred = 0xFFFFFFFFu;
 
@@ -886,9 +910,13 @@ template <int MODE>
 __global__ void __launch_bounds__(MT_THREADS)
 k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
                  uint2 *__restrict__ stage) {
+    // shared tile as comparison keys (merge_key_*) + positions: one 8 B key
+    // pair per comparison instead of two 16 B records
     extern __shared__ __align__(16) unsigned char smem[];
-    uint4 *sh = reinterpret_cast<uint4 *>(smem);
-    u32 *out = reinterpret_cast<u32 *>(sh + MT_TILE);
+    u64 *k1 = reinterpret_cast<u64 *>(smem);
+    u64 *k2 = k1 + MT_TILE;
+    u32 *pos = reinterpret_cast<u32 *>(k2 + MT_TILE);
+    u32 *out = pos + MT_TILE;
     u32 *sh_cnt = out + MT_TILE;
     u32 *sh_base = sh_cnt + plan.a.buckets;
     __shared__ u32 sh_pred;
@@ -901,7 +929,18 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
 #pragma unroll
     for (int q = 0; q < MT_ITEMS; q++) {
         int x = threadIdx.x + q * MT_THREADS;
-        if (x < cnt) sh[x] = x < nat ? v.ra(i0 + x) : v.rb(j0 + (x - nat));
+        if (x < cnt) {
+            if (x < nat) {
+                uint4 e = v.ra(i0 + x);
+                k1[x] = merge_key_sample(e);
+                pos[x] = e.x;
+            } else {
+                uint4 e = v.rb(j0 + (x - nat));
+                k1[x] = merge_key1(e);
+                k2[x] = merge_key2(e);
+                pos[x] = e.x;
+            }
+        }
     }
     if (MODE == EMIT_PHI && threadIdx.x == 0) {
         // the suffix at rank d0-1 is the larger of the two run predecessors
@@ -917,21 +956,21 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
         sh_pred = pr;
     }
     __syncthreads();
-    const uint4 *A = sh, *B = sh + nat;
+    const u64 *B1 = k1 + nat, *B2 = k2 + nat;
     int dt = threadIdx.x * MT_ITEMS;
     if (dt < cnt) {
         int lo = dt > nbt ? dt - nbt : 0, hi = dt < nat ? dt : nat;
         while (lo < hi) {
             int mid = (lo + hi) >> 1;
-            if (recq_a_first(A[mid], B[dt - 1 - mid])) lo = mid + 1;
+            if (keys_a_first(k1[mid], B1, B2, dt - 1 - mid)) lo = mid + 1;
             else hi = mid;
         }
         int i = lo, j = dt - lo;
 #pragma unroll
         for (int r = 0; r < MT_ITEMS; r++) {
             if (dt + r >= cnt) break;
-            bool takeA = j >= nbt || (i < nat && recq_a_first(A[i], B[j]));
-            out[dt + r] = takeA ? A[i++].x : B[j++].x;
+            bool takeA = j >= nbt || (i < nat && keys_a_first(k1[i], B1, B2, j));
+            out[dt + r] = takeA ? pos[i++] : pos[nat + j++];
         }
     }
     __syncthreads();
@@ -949,7 +988,7 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
                 else it[q] = make_uint2(out[x], x > 0 ? out[x - 1] : sh_pred);
             }
         }
-        ps_block_emit<uint2, MT_THREADS, MT_ITEMS>(it, ok, plan.a, stage, reinterpret_cast<uint2 *>(sh), sh_cnt,
+        ps_block_emit<uint2, MT_THREADS, MT_ITEMS>(it, ok, plan.a, stage, reinterpret_cast<uint2 *>(k1), sh_cnt,
                                                    sh_base);
     }
 }
@@ -958,12 +997,12 @@ template <int MODE>
 static int merge_rec_launch(RecMergeView v, i64 na, i64 nb, const u32 *split, u32 *sa, const PsPlan &plan,
                             uint2 *stage, cudaStream_t st) {
     static bool attr = false;
-    size_t smem = (size_t)MT_TILE * 20 + 8 * (size_t)PS_MAX_BUCKETS;
+    size_t smem = (size_t)MT_TILE * 24 + 8 * (size_t)PS_MAX_BUCKETS;
     if (!attr) {
         SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_rec<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    size_t use = (size_t)MT_TILE * 20 + 8 * (size_t)(MODE == EMIT_NONE ? 1 : plan.a.buckets);
+    size_t use = (size_t)MT_TILE * 24 + 8 * (size_t)(MODE == EMIT_NONE ? 1 : plan.a.buckets);
     k_merge_tile_rec<MODE><<<(unsigned)ceil_div(na + nb, MT_TILE), MT_THREADS, use, st>>>(v, na, nb, split, sa, plan,
                                                                                          stage);
     SAIX_LAUNCHED();
@@ -1391,10 +1430,10 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
         Prof prof_("dc3.mod0_split", 16.0 * m + 16.0 * k, st);
         static bool attr = false;
         if (!attr) {
-            SAIX_CUDA(cudaFuncSetAttribute(k_mod0_window, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 << RW_SHIFT));
+            SAIX_CUDA(cudaFuncSetAttribute(k_mod0_window, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M0_SMEM));
             attr = true;
         }
-        k_mod0_window<<<(unsigned)pr.windows, 256, 16 << RW_SHIFT, st>>>(RS, m, pr.windows, hist, M0);
+        k_mod0_window<<<(unsigned)pr.windows, M0_THREADS, M0_SMEM, st>>>(RS, m, pr.windows, hist, M0);
     }
     SAIX_LAUNCHED();
     ar.reset(mark_s1);  // stage2, histogram and scan temps are dead
