@@ -165,25 +165,25 @@ struct Mod0HistSrc {
 // bucket-sort sources (wide keys, bsort.cuh): mixed-radix keys, bucketed by
 // their top bits
 template <typename TT>
-struct TripleBucketSrc {
+struct TripleBucketSrc {  // key = c0 << 2b | c1 << b | c2 (b = bits(sigma))
     Text<TT> T;
     SampleLayout L;
-    u64 s1;
+    int b;
     __device__ __forceinline__ void get(i64 s, u64 &k, u32 &v) const {
         i64 p = L.pos(s);
-        k = ((u64)T(p) * s1 + T(p + 1)) * s1 + T(p + 2);
+        k = ((u64)T(p) << (2 * b)) | ((u64)T(p + 1) << b) | T(p + 2);
         v = (u32)s;
     }
 };
-// mod-0 suffix 3j keyed by (T(3j), R(3j+1)) = T(3j) * (m+1) + ISAc[j] + 1;
+// mod-0 suffix 3j keyed by (T(3j), R(3j+1)) = T(3j) << rb | ISAc[j] + 1;
 // streamed in text order (the keys are distinct)
 template <typename TT>
 struct Mod0BucketSrc {
     Text<TT> T;
     const u32 *isac;
-    u64 m1;  // m + 1
+    int rb;  // bits(m)
     __device__ __forceinline__ void get(i64 j, u64 &k, u32 &v) const {
-        k = (u64)T(3 * j) * m1 + (__ldcs(isac + j) + 1u);
+        k = ((u64)T(3 * j) << rb) | (__ldcs(isac + j) + 1u);
         v = (u32)j;
     }
 };
@@ -1097,13 +1097,216 @@ template <typename TT>
 static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *ISA,
                      saix_dc3_probe *probe, int depth, u32 *Phi = nullptr, bool *phi_done = nullptr);
 
+// ------------------------------------------------------------ wide-level finish
+//
+// A u32 level whose sample triples are all distinct (the deepest level of
+// DNA-like texts) gets its merge inputs as records built in sorted order,
+// with one random read per item instead of the merge's per-element gathers:
+//   RA[r] = {pos, R(pos+1) | R(pos+2), c0, c1} of the sample at rank r, from
+//           the bucket-sorted triple keys (chars) and one ISAc read;
+//   RB[q] = {3j, R(3j+1), R(3j+2), c0} (+ c1) of the q-th non-sample, from
+//           the bucket-sorted (T(3j), R(3j+1)) keys and RA[R(3j+1) - 1] --
+//           the mod-1 sample 3j+1, whose record holds R(3j+2) and T(3j+1).
+__global__ void k_arec(const u64 *__restrict__ keys, const u32 *__restrict__ vals, SampleLayout L, int b,
+                       const u32 *__restrict__ isac, uint4 *__restrict__ ra) {
+    const u64 cm = ((u64)1 << b) - 1;
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < L.m; r += (i64)gridDim.x * blockDim.x) {
+        u64 key = __ldcs(keys + r);
+        u32 sidx = __ldcs(vals + r);
+        u32 nb;
+        i64 pos;
+        if (sidx < L.m1) {  // mod-1 sample 3s+1: R(3s+2)
+            pos = 3 * (i64)sidx + 1;
+            nb = sidx < L.m2 ? isac[L.m1 + sidx] + 1u : 0u;
+        } else {  // mod-2 sample 3j+2: R(3j+4)
+            i64 j = sidx - L.m1;
+            pos = 3 * j + 2;
+            nb = j + 1 < L.m1 ? isac[j + 1] + 1u : 0u;
+        }
+        __stcs(ra + r, make_uint4((u32)pos, nb, (u32)(key >> (2 * b)), (u32)((key >> b) & cm)));
+    }
+}
+
+__global__ void k_brec(const u64 *__restrict__ keys, const u32 *__restrict__ vals, i64 k, int rb,
+                       const uint4 *__restrict__ ra, uint4 *__restrict__ rb4, u32 *__restrict__ rbc1) {
+    const u64 rm = ((u64)1 << rb) - 1;
+    for (i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x; q < k; q += (i64)gridDim.x * blockDim.x) {
+        u64 key = __ldcs(keys + q);
+        u32 j = __ldcs(vals + q);
+        u32 r1 = (u32)(key & rm);
+        uint4 e = ra[r1 - 1];  // mod-1 sample 3j+1
+        __stcs(rb4 + q, make_uint4(3u * j, r1, e.y, (u32)(key >> rb)));
+        __stcs(rbc1 + q, e.z);
+    }
+}
+
+struct MergeRA {
+    const uint4 *A, *B;
+    const u32 *Bc1;
+    __device__ __forceinline__ MRec reca(i64 i) const {
+        uint4 e = A[i];
+        MRec m;
+        m.pos = e.x;
+        m.c0 = e.z;
+        if (e.x % 3 == 1) {
+            m.c1 = 0;
+            m.r1 = e.y;
+            m.r2 = 0;
+        } else {
+            m.c1 = e.w;
+            m.r1 = 0;
+            m.r2 = e.y;
+        }
+        return m;
+    }
+    __device__ __forceinline__ MRec recb(i64 j) const {
+        uint4 e = B[j];
+        MRec m;
+        m.pos = e.x;
+        m.c0 = e.w;
+        m.c1 = Bc1[j];
+        m.r1 = e.y;
+        m.r2 = e.z;
+        return m;
+    }
+};
+
+// merge of record runs (MRec form) with the bucketed ISA side output
+template <int MODE, class V>
+__global__ void __launch_bounds__(MT_THREADS)
+k_merge_tile_m(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
+               uint2 *__restrict__ stage) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    MRec *sh = reinterpret_cast<MRec *>(smem);
+    u32 *out = reinterpret_cast<u32 *>(sh + MT_TILE);
+    u32 *sh_cnt = out + MT_TILE;
+    u32 *sh_base = sh_cnt + plan.a.buckets;
+    i64 total = na + nb;
+    i64 d0 = (i64)blockIdx.x * MT_TILE;
+    i64 d1 = d0 + MT_TILE < total ? d0 + MT_TILE : total;
+    i64 i0 = split[blockIdx.x], i1 = split[blockIdx.x + 1];
+    i64 j0 = d0 - i0;
+    int nat = (int)(i1 - i0), cnt = (int)(d1 - d0), nbt = cnt - nat;
+#pragma unroll
+    for (int q = 0; q < MT_ITEMS; q++) {
+        int x = threadIdx.x + q * MT_THREADS;
+        if (x < cnt) sh[x] = x < nat ? v.reca(i0 + x) : v.recb(j0 + (x - nat));
+    }
+    __syncthreads();
+    const MRec *A = sh, *B = sh + nat;
+    int dt = threadIdx.x * MT_ITEMS;
+    if (dt < cnt) {
+        int lo = dt > nbt ? dt - nbt : 0, hi = dt < nat ? dt : nat;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (rec_a_first(A[mid], B[dt - 1 - mid])) lo = mid + 1;
+            else hi = mid;
+        }
+        int i = lo, j = dt - lo;
+#pragma unroll
+        for (int r = 0; r < MT_ITEMS; r++) {
+            if (dt + r >= cnt) break;
+            bool takeA = j >= nbt || (i < nat && rec_a_first(A[i], B[j]));
+            out[dt + r] = takeA ? A[i++].pos : B[j++].pos;
+        }
+    }
+    __syncthreads();
+    if (sa)
+        for (int x = threadIdx.x; x < cnt; x += MT_THREADS) __stcs(sa + d0 + x, out[x]);
+    if (MODE == EMIT_ISA) {
+        uint2 it[MT_ITEMS];
+        bool ok[MT_ITEMS];
+#pragma unroll
+        for (int q = 0; q < MT_ITEMS; q++) {
+            int x = threadIdx.x + q * MT_THREADS;
+            ok[q] = x < cnt;
+            if (ok[q]) it[q] = make_uint2(out[x], (u32)(d0 + x));
+        }
+        ps_block_emit<uint2, MT_THREADS, MT_ITEMS>(it, ok, plan.a, stage, reinterpret_cast<uint2 *>(sh), sh_cnt,
+                                                   sh_base);
+    }
+}
+
+template <typename TT>
+static int dc3_wide_finish(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma, const u32 *ISAc,
+                           const uint4 *RA, u32 *SA, u32 *ISA, bool &fin) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    fin = false;
+    const i64 m = L.m, k = L.k, N = L.n;
+    size_t mark = ar.mark();
+    int rbm = bits_for((u64)m);
+    u64 mk = ((u64)sigma << rbm) | (u64)m;
+    if (bits_for(sigma) + rbm > 64) return SAIX_OK;
+    // mod-0 order: bucket sort of (T(3j), R(3j+1))
+    uint4 *RB = ar.alloc<uint4>(k);
+    u32 *RBc1 = ar.alloc<u32>(k);
+    size_t mark_b = ar.mark();
+    u64 *k64 = ar.alloc<u64>(k);
+    u32 *v0 = ar.alloc<u32>(k);
+    u32 *scratch = ar.alloc<u32>(bs_scratch_words(N / 8 + 2));
+    SAIX_ARENA_OK(ar);
+    bool ok = false;
+    SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc, rbm}, k, mk, k64, v0, scratch, ok, st, "dc3.mod0_split", &ar));
+    if (!ok) {
+        ar.reset(mark);
+        return SAIX_OK;
+    }
+    {
+        Prof prof_("dc3.brec", 12.0 * k + 16.0 * k + 20.0 * k, st);
+        k_brec<<<grid_for(k, 256), 256, 0, st>>>(k64, v0, k, rbm, RA, RB, RBc1);
+    }
+    SAIX_LAUNCHED();
+    ar.reset(mark_b);
+    // merge
+    i64 pad = L.pad ? 1 : 0;
+    i64 na = m - pad, total = na + k;
+    MergeRA V{RA + pad, RB, RBc1};
+    i64 ntiles = ceil_div(total, MT_TILE);
+    u32 *split = ar.alloc<u32>(merge_split_words(total));
+    PsPlan pm = PsPlan::of(ISA ? total : 1, 4);
+    pm.set_cursors(ar.alloc<u32>(pm.cursor_words()));
+    uint2 *pst1 = ISA ? ar.alloc<uint2>(pm.stage1_items()) : nullptr;
+    uint2 *pst2 = ISA ? ar.alloc<uint2>(pm.stage2_items()) : nullptr;
+    SAIX_ARENA_OK(ar);
+    SAIX_CUDA(cudaMemsetAsync(pm.a.cursor, 0, (size_t)pm.cursor_words() * 4, st));
+    {
+        Prof prof_("dc3.merge_partition", 32.0 * (ntiles + 1), st);
+        k_merge_partition<MergeRA><<<grid_for((ntiles + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, split);
+    }
+    SAIX_LAUNCHED();
+    {
+        Prof prof_("dc3.merge_tile", 16.0 * na + 20.0 * k + (SA ? 4.0 * total : 0) + (ISA ? 8.0 * total : 0), st);
+        static bool attr = false;
+        size_t smax = (size_t)MT_TILE * 24 + 8 * (size_t)PS_MAX_BUCKETS;
+        if (!attr) {
+            SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_m<EMIT_ISA, MergeRA>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+            SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_m<EMIT_NONE, MergeRA>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+            attr = true;
+        }
+        size_t smem = (size_t)MT_TILE * 24 + 8 * (size_t)(ISA ? pm.a.buckets : 1);
+        if (ISA)
+            k_merge_tile_m<EMIT_ISA, MergeRA><<<(unsigned)ntiles, MT_THREADS, smem, st>>>(V, na, k, split, SA, pm, pst1);
+        else
+            k_merge_tile_m<EMIT_NONE, MergeRA><<<(unsigned)ntiles, MT_THREADS, smem, st>>>(V, na, k, split, SA, pm,
+                                                                                           pst1);
+    }
+    SAIX_LAUNCHED();
+    if (ISA) SAIX_TRY(ps_finish(pst1, pst2, pm, U32Apply{ISA}, st, "dc3.isa_apply", 28.0 * total));
+    ar.reset(mark);
+    fin = true;
+    return SAIX_OK;
+}
+
 static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA, u32 *ISA, u32 *Phi,
                             bool *phi_done, int depth);
 
 // Steps 1-2: names of the sample triples, then SAc/ISAc (recursing if needed).
 template <typename TT>
 static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma, u32 *tt,
-                        u32 *SAc, u32 *ISAc, u32 *d_scal, int depth, bool keep_u32) {
+                        u32 *SAc, u32 *ISAc, u32 *d_scal, int depth, bool keep_u32, uint4 **RA_out) {
     Arena &ar = *c.ar;
     cudaStream_t st = c.st;
     size_t mark = ar.mark();
@@ -1112,6 +1315,11 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
     u32 D = 0;
     bool narrow = false;  // recursion string stored as u8
     u32 *sorted_vals = nullptr;
+    u64 *sorted_keys = nullptr;
+    bool bsorted = false;  // keys are shift-packed triples (bucket sort)
+    int kbits = 0;
+    bool keep_arena = false;  // RA built: the caller releases the sort temps
+    if (RA_out) *RA_out = nullptr;
     if (use_bitmap(sigma, m)) {
         u64 s1 = sigma + 1;
         u64 codes = s1 * s1 * s1;
@@ -1155,9 +1363,11 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             int passes = (kb + OS_BITS - 1) / OS_BITS;
             TripleSrc<TT> src{T, L, s1};
             bool done = false;
-            if (use_bsort(s1 * s1 * s1 - 1, m)) {
-                SAIX_TRY(bucket_sort(TripleBucketSrc<TT>{T, L, s1}, m, s1 * s1 * s1 - 1, k0, v0, scratch, done, st,
+            u64 bmax = (sigma << (2 * b)) | (sigma << b) | sigma;
+            if (use_bsort(bmax, m)) {
+                SAIX_TRY(bucket_sort(TripleBucketSrc<TT>{T, L, b}, m, bmax, k0, v0, scratch, done, st,
                                      "dc3.triple_sort", &ar));
+                bsorted = done;
                 keys = k0;
                 vals = v0;
             }
@@ -1196,6 +1406,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             SAIX_TRY(read_u32(d_scal, &D, st));
         }
         sorted_vals = vals;
+        sorted_keys = keys;
+        kbits = b;
     }
     if ((i64)D == m) {
         if (sorted_vals && m > ((i64)1 << 20)) {
@@ -1217,6 +1429,17 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             }
             SAIX_LAUNCHED();
             SAIX_TRY(ps_finish(s1, s2, pu, U32Apply{ISAc}, st, "dc3.unique_isa", 28.0 * m));
+            if (RA_out && bsorted) {
+                // the wide-level finish (dc3_wide_finish) merges from sample
+                // records in rank order: build them while the keys are alive
+                uint4 *RA = ar.alloc<uint4>(m);
+                SAIX_ARENA_OK(ar);
+                Prof prof_("dc3.arec", 36.0 * m, st);
+                k_arec<<<grid_for(m, 256), 256, 0, st>>>(sorted_keys, sorted_vals, L, kbits, ISAc, RA);
+                SAIX_LAUNCHED();
+                *RA_out = RA;
+                keep_arena = true;
+            }
         } else {
             Prof prof_("dc3.unique_ranks", 12.0 * m, st);
             if (sorted_vals) k_unique_from_sorted<<<g, K_THREADS, 0, st>>>(sorted_vals, m, SAc, ISAc);
@@ -1224,7 +1447,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             else k_isa_from_names<<<g, K_THREADS, 0, st>>>(tt, m, ISAc);
             SAIX_LAUNCHED();
         }
-        ar.reset(mark);
+        if (!keep_arena) ar.reset(mark);
     } else {
         ar.reset(mark);
         if (narrow) SAIX_TRY(dc3_level<u8>(c, (const u8 *)tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
@@ -1260,7 +1483,21 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     SAIX_ARENA_OK(ar);
     Text<TT> T{text, N};
 
-    SAIX_TRY(sort_samples<TT>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth, probe != nullptr));
+    // wide levels whose names all differ take the record finish below
+    uint4 *RA = nullptr;
+    size_t mark_s = ar.mark();
+    bool want_ra = sizeof(TT) == 4 && probe == nullptr && L.m >= 4096;
+    SAIX_TRY(sort_samples<TT>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth, probe != nullptr,
+                              want_ra ? &RA : nullptr));
+    if (RA) {
+        bool fin = false;
+        SAIX_TRY(dc3_wide_finish<TT>(c, T, L, sigma, ISAc, RA, SA, ISA, fin));
+        if (fin) {
+            ar.reset(mark0);
+            return SAIX_OK;
+        }
+        ar.reset(mark_s);  // sort temps + RA
+    }
 
     // step 3: mod-0 suffixes = mod-1 samples in rank order, minus one,
     // stably split by their first character
@@ -1289,13 +1526,14 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
         SAIX_LAUNCHED();
     } else {
         bool done = false;
-        u64 mk = (u64)sigma * (u64)(L.m + 1) + (u64)L.m;
-        if (sigma + 1 > 256 && use_bsort(mk, k)) {
+        int rbm = bits_for((u64)L.m);
+        u64 mk = ((u64)sigma << rbm) | (u64)L.m;
+        if (sigma + 1 > 256 && bits_for(sigma) + rbm <= 64 && use_bsort(mk, k)) {
             // the (char, rank) keys are distinct, so an unstable bucket split
             // followed by in-bucket sorts gives the exact order
             u64 *k64 = ar.alloc<u64>(k);
             SAIX_ARENA_OK(ar);
-            SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc, (u64)L.m + 1}, k, mk, k64, v0, scratch, done, st,
+            SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc, rbm}, k, mk, k64, v0, scratch, done, st,
                                  "dc3.mod0_split", &ar));
             vals = v0;
         }
@@ -1372,7 +1610,7 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     u32 *d_scal = ar.alloc<u32>(8);
     SAIX_ARENA_OK(ar);
     Text<u8> T{text, N};
-    SAIX_TRY(sort_samples<u8>(c, T, L, sigma, tt, nullptr, ISAc, d_scal, depth, false));
+    SAIX_TRY(sort_samples<u8>(c, T, L, sigma, tt, nullptr, ISAc, d_scal, depth, false, nullptr));
 
     // 1: sample records in rank order
     uint4 *RS = ar.alloc<uint4>(m);
@@ -1474,7 +1712,7 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
 
 // Upper bound of the workspace the driver carves (persistent arrays of every
 // level + the largest level's temporaries), see DESIGN.md "DC3 workspace".
-static size_t dc3_plan(i64 n) {
+static size_t dc3_plan(i64 n, int text_bytes = 4) {
     size_t persistent = 0, temps = 0;
     i64 N = n;
     while (N > 1) {
@@ -1498,7 +1736,13 @@ static size_t dc3_plan(i64 n) {
         size_t s3 = (size_t)k * 16 + (size_t)merge_split_words(N) * 4 +
                     (size_t)(pm.stage1_items() + pm.stage2_items()) * 8 + (size_t)pm.cursor_words() * 4;
         size_t stream_t = (size_t)m * 16 + (s1 > s2 ? (s1 > s3 ? s1 : s3) : (s2 > s3 ? s2 : s3));
+        // wide-level finish: RB + (mod-0 bucket sort | merge split + ISA staging)
+        size_t wf1 = (size_t)k * 12 + (size_t)bs_scratch_words(N / 8 + 2) * 4 + bs_ps_bytes(k);
+        size_t wf2 = (size_t)merge_split_words(N) * 4 + (size_t)(pm.stage1_items() + pm.stage2_items()) * 8 +
+                     (size_t)pm.cursor_words() * 4;
+        size_t wide_t = sort_t + (size_t)m * 16 + (size_t)k * 20 + (wf1 > wf2 ? wf1 : wf2) + 8 * Arena::kAlign;
         size_t t = sort_t > bm_t ? sort_t : bm_t;
+        if (!(N == n && text_bytes == 1)) t = t > wide_t ? t : wide_t;  // byte top levels stream
         t = t > post_t ? t : post_t;
         t = t > stream_t ? t : stream_t;
         t += 8 * Arena::kAlign;
@@ -1513,8 +1757,7 @@ static size_t dc3_plan(i64 n) {
 using namespace saix;
 
 extern "C" size_t saix_dc3_workspace_bytes(int64_t n, int text_bytes) {
-    (void)text_bytes;
-    return dc3_plan(n);
+    return dc3_plan(n, text_bytes);
 }
 
 extern "C" int saix_dc3(const void *text, int text_bytes, int64_t n, int64_t sigma, uint32_t *sa,
@@ -1536,8 +1779,8 @@ int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32
         set_error("saix_dc3: sigma %lld does not fit u8 text", (long long)sigma);
         return SAIX_EINVAL;
     }
-    if (ws_bytes < dc3_plan(n)) {
-        set_error("saix_dc3: workspace %zu < %zu bytes", ws_bytes, dc3_plan(n));
+    if (ws_bytes < dc3_plan(n, text_bytes)) {
+        set_error("saix_dc3: workspace %zu < %zu bytes", ws_bytes, dc3_plan(n, text_bytes));
         return SAIX_ENOSPC;
     }
     Arena ar;
