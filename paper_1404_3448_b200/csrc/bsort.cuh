@@ -12,8 +12,11 @@
 //            <= 1024: one warp, bitonic in shared memory;
 //            <= 4096: one CTA; larger buckets are reported so the caller can
 //            fall back to a full LSD sort.
-// Sources: struct { __device__ void get(i64 i, u64 &key, u32 &val) const; }
-// with keys in [0, max_key]; the result is sorted by key (ties in any order).
+// Sources: struct { __device__ void get(i64 i, u64 &key, u32 &val) const;
+//                   __device__ u64 dense(u64 key) const; }
+// where dense() is a monotone map of the keys onto [0, span] that spreads
+// them evenly (e.g. the mixed-radix value of the leading key fields); the
+// result is sorted by key (ties in any order).
 #pragma once
 
 #include "pscatter.cuh"
@@ -32,7 +35,7 @@ __global__ void k_bs_count(Src src, i64 n, int shift, u32 *__restrict__ cnt) {
         u64 k;
         u32 v;
         src.get(i, k, v);
-        atomicAdd(&cnt[k >> shift], 1u);
+        atomicAdd(&cnt[src.dense(k) >> shift], 1u);
     }
 }
 
@@ -62,7 +65,7 @@ __global__ void k_bs_scatter(Src src, i64 n, int shift, u32 *__restrict__ cursor
         u64 k;
         u32 v;
         src.get(i, k, v);
-        u32 at = atomicAdd(&cursor[k >> shift], 1u);
+        u32 at = atomicAdd(&cursor[src.dense(k) >> shift], 1u);
         keys[at] = k;
         vals[at] = v;
     }
@@ -90,7 +93,7 @@ k_bs_scatter_emit(Src src, i64 n, int shift, u32 *__restrict__ cursor, PsPlan pl
             u64 k;
             u32 v;
             src.get(i, k, v);
-            u32 at = atomicAdd(&cursor[k >> shift], 1u);
+            u32 at = atomicAdd(&cursor[src.dense(k) >> shift], 1u);
             it[q] = make_uint4(at, v, (u32)k, (u32)(k >> 32));
         }
     }
@@ -289,11 +292,11 @@ inline i64 bs_scratch_words_for(u64 max_key, i64 n) { return bs_scratch_words(bs
 // Returns ok = false (after the count pass only) when some bucket exceeds
 // BS_LARGE; the caller then sorts with onesweep instead.  One host sync.
 template <class Src>
-int bucket_sort(Src src, i64 n, u64 max_key, u64 *keys, u32 *vals, u32 *scratch, bool &ok, cudaStream_t st,
+int bucket_sort(Src src, i64 n, u64 span, u64 *keys, u32 *vals, u32 *scratch, bool &ok, cudaStream_t st,
                 const char *prof = "bsort", Arena *ar = nullptr) {
     ok = true;
     if (n <= 0) return SAIX_OK;
-    BsGeom g = bs_geom(max_key, n);
+    BsGeom g = bs_geom(span, n);
     const i64 nb = g.nb;
     Prof prof_(prof, 24.0 * n + 16.0 * nb, st);
     u32 *cnt = scratch, *start = cnt + (nb + 1), *cursor = start + (nb + 1), *mid = cursor + (nb + 1);

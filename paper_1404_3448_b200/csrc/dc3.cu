@@ -165,14 +165,18 @@ struct Mod0HistSrc {
 // bucket-sort sources (wide keys, bsort.cuh): mixed-radix keys, bucketed by
 // their top bits
 template <typename TT>
-struct TripleBucketSrc {  // key = c0 << 2b | c1 << b | c2 (b = bits(sigma))
+struct TripleBucketSrc {  // key = c0 << 2b | c1 << b | c2 (b = bits(sigma)); dense = c0 * s1 + c1
     Text<TT> T;
     SampleLayout L;
     int b;
+    u64 s1;
     __device__ __forceinline__ void get(i64 s, u64 &k, u32 &v) const {
         i64 p = L.pos(s);
         k = ((u64)T(p) << (2 * b)) | ((u64)T(p + 1) << b) | T(p + 2);
         v = (u32)s;
+    }
+    __device__ __forceinline__ u64 dense(u64 k) const {
+        return (k >> (2 * b)) * s1 + ((k >> b) & (((u64)1 << b) - 1));
     }
 };
 // mod-0 suffix 3j keyed by (T(3j), R(3j+1)) = T(3j) << rb | ISAc[j] + 1;
@@ -182,10 +186,12 @@ struct Mod0BucketSrc {
     Text<TT> T;
     const u32 *isac;
     int rb;  // bits(m)
+    u64 m1;  // m + 1
     __device__ __forceinline__ void get(i64 j, u64 &k, u32 &v) const {
         k = ((u64)T(3 * j) << rb) | (__ldcs(isac + j) + 1u);
         v = (u32)j;
     }
+    __device__ __forceinline__ u64 dense(u64 k) const { return (k >> rb) * m1 + (k & (((u64)1 << rb) - 1)); }
 };
 // bucket sort replaces LSD radix when the keys are wide
 static bool use_bsort(u64 max_key, i64 n) { return n >= 4096 && bits_for(max_key) > 24; }
@@ -1247,7 +1253,8 @@ static int dc3_wide_finish(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sig
     u32 *scratch = ar.alloc<u32>(bs_scratch_words(N / 8 + 2));
     SAIX_ARENA_OK(ar);
     bool ok = false;
-    SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc, rbm}, k, mk, k64, v0, scratch, ok, st, "dc3.mod0_split", &ar));
+    SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc, rbm, (u64)m + 1}, k, sigma * ((u64)m + 1) + m, k64, v0, scratch,
+                         ok, st, "dc3.mod0_split", &ar));
     if (!ok) {
         ar.reset(mark);
         return SAIX_OK;
@@ -1365,8 +1372,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             bool done = false;
             u64 bmax = (sigma << (2 * b)) | (sigma << b) | sigma;
             if (use_bsort(bmax, m)) {
-                SAIX_TRY(bucket_sort(TripleBucketSrc<TT>{T, L, b}, m, bmax, k0, v0, scratch, done, st,
-                                     "dc3.triple_sort", &ar));
+                SAIX_TRY(bucket_sort(TripleBucketSrc<TT>{T, L, b, s1}, m, sigma * s1 + sigma, k0, v0, scratch, done,
+                                     st, "dc3.triple_sort", &ar));
                 bsorted = done;
                 keys = k0;
                 vals = v0;
@@ -1533,8 +1540,8 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
             // followed by in-bucket sorts gives the exact order
             u64 *k64 = ar.alloc<u64>(k);
             SAIX_ARENA_OK(ar);
-            SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc, rbm}, k, mk, k64, v0, scratch, done, st,
-                                 "dc3.mod0_split", &ar));
+            SAIX_TRY(bucket_sort(Mod0BucketSrc<TT>{T, ISAc, rbm, (u64)L.m + 1}, k, sigma * ((u64)L.m + 1) + L.m,
+                                 k64, v0, scratch, done, st, "dc3.mod0_split", &ar));
             vals = v0;
         }
         if (!done) {
