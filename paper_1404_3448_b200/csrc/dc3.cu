@@ -1083,6 +1083,15 @@ struct Dc3Ctx {
     int max_depth;
 };
 
+// SAIX_TRACE=1: one stderr line per level (development aid)
+static bool trace_on() {
+    static int v = [] {
+        const char *e = getenv("SAIX_TRACE");
+        return e && *e == '1' ? 1 : 0;
+    }();
+    return v != 0;
+}
+
 static bool use_bitmap(u64 sigma, i64 m) {
     u64 s1 = sigma + 1;
     if (s1 >= ((u64)1 << 21)) return false;
@@ -1113,6 +1122,142 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
 //   RB[q] = {3j, R(3j+1), R(3j+2), c0} (+ c1) of the q-th non-sample, from
 //           the bucket-sorted (T(3j), R(3j+1)) keys and RA[R(3j+1) - 1] --
 //           the mod-1 sample 3j+1, whose record holds R(3j+2) and T(3j+1).
+// generic pass A of a u32 scatter dst[idx[i]] = val[i] (val == nullptr: i)
+constexpr int PE_ITEMS = 8;
+__global__ void __launch_bounds__(256)
+k_pairs_emit(const u32 *__restrict__ idx, const u32 *__restrict__ val, i64 n, PsPlan plan, uint2 *__restrict__ stage) {
+    extern __shared__ __align__(16) unsigned char pe_smem[];
+    uint2 *sh_items = reinterpret_cast<uint2 *>(pe_smem);
+    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_items + 256 * PE_ITEMS);
+    u32 *sh_base = sh_cnt + plan.a.buckets;
+    const i64 i0 = (i64)blockIdx.x * (256 * PE_ITEMS);
+    uint2 it[PE_ITEMS];
+    bool ok[PE_ITEMS];
+#pragma unroll
+    for (int q = 0; q < PE_ITEMS; q++) {
+        i64 i = i0 + q * 256 + threadIdx.x;
+        ok[q] = i < n;
+        if (ok[q]) it[q] = make_uint2(__ldcs(idx + i), val ? __ldcs(val + i) : (u32)i);
+    }
+    ps_block_emit<uint2, 256, PE_ITEMS>(it, ok, plan.a, stage, sh_items, sh_cnt, sh_base);
+}
+
+// dst[idx[i]] = val[i] for a permutation-like idx, through the bucketed
+// scatter (small n: direct)
+__global__ void k_scatter_direct(const u32 *__restrict__ idx, const u32 *__restrict__ val, i64 n, u32 *__restrict__ dst) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        dst[idx[i]] = val ? val[i] : (u32)i;
+}
+static int scatter_u32(Arena &ar, const u32 *idx, const u32 *val, i64 n, i64 n_dest, u32 *dst, cudaStream_t st,
+                       const char *prof) {
+    if (n <= 0) return SAIX_OK;
+    if (n < ((i64)1 << 20)) {
+        Prof prof_(prof, 12.0 * n, st);
+        k_scatter_direct<<<grid_for(n, 256), 256, 0, st>>>(idx, val, n, dst);
+        SAIX_LAUNCHED();
+        return SAIX_OK;
+    }
+    size_t mark = ar.mark();
+    PsPlan pp = PsPlan::of(n_dest, 4);
+    pp.set_cursors(ar.alloc<u32>(pp.cursor_words()));
+    uint2 *s1 = ar.alloc<uint2>(pp.stage1_items()), *s2 = ar.alloc<uint2>(pp.stage2_items());
+    SAIX_ARENA_OK(ar);
+    SAIX_CUDA(cudaMemsetAsync(pp.a.cursor, 0, (size_t)pp.cursor_words() * 4, st));
+    {
+        Prof prof_(prof, 16.0 * n, st);
+        static bool attr = false;
+        if (!attr) {
+            SAIX_CUDA(cudaFuncSetAttribute(k_pairs_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           256 * PE_ITEMS * 8 + 8 * PS_MAX_BUCKETS));
+            attr = true;
+        }
+        size_t smem = (size_t)256 * PE_ITEMS * 8 + 8 * (size_t)pp.a.buckets;
+        k_pairs_emit<<<(unsigned)ceil_div(n, 256 * PE_ITEMS), 256, smem, st>>>(idx, val, n, pp, s1);
+    }
+    SAIX_LAUNCHED();
+    SAIX_TRY(ps_finish(s1, s2, pp, U32Apply{dst}, st, prof, 28.0 * n));
+    ar.reset(mark);
+    return SAIX_OK;
+}
+inline size_t scatter_u32_bytes(i64 n_dest) {
+    PsPlan pp = PsPlan::of(n_dest, 4);
+    return (size_t)(pp.stage1_items() + pp.stage2_items()) * 8 + (size_t)pp.cursor_words() * 4 + 4 * Arena::kAlign;
+}
+
+// RA from a sample order (recursion case / wide naming): chars and the
+// neighbour rank by two random reads per sample
+template <typename TT>
+__global__ void k_arec_sa(const u32 *__restrict__ sac, Text<TT> T, SampleLayout L, const u32 *__restrict__ isac,
+                          uint4 *__restrict__ ra) {
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < L.m; r += (i64)gridDim.x * blockDim.x) {
+        u32 sidx = __ldcs(sac + r);
+        u32 nb;
+        i64 pos;
+        if (sidx < L.m1) {
+            pos = 3 * (i64)sidx + 1;
+            nb = sidx < L.m2 ? isac[L.m1 + sidx] + 1u : 0u;
+        } else {
+            i64 j = sidx - L.m1;
+            pos = 3 * j + 2;
+            nb = j + 1 < L.m1 ? isac[j + 1] + 1u : 0u;
+        }
+        __stcs(ra + r, make_uint4((u32)pos, nb, T(pos), T(pos + 1)));
+    }
+}
+
+// Wide naming (3 bits(sigma) > 64): bucket sort by the dense pair
+// c0 * s1 + c1, then every run of equal pairs (rare: repeats) is ordered by
+// c2 in place; runs longer than FR_MAX are reported (caller falls back).
+template <typename TT>
+struct PairDenseSrc {
+    Text<TT> T;
+    SampleLayout L;
+    u64 s1;
+    __device__ __forceinline__ void get(i64 s, u64 &k, u32 &v) const {
+        i64 p = L.pos(s);
+        k = (u64)T(p) * s1 + T(p + 1);
+        v = (u32)s;
+    }
+    __device__ __forceinline__ u64 dense(u64 k) const { return k; }
+};
+constexpr int FR_MAX = 64;
+template <typename TT>
+__global__ void k_fix_runs(const u64 *__restrict__ keys, u32 *__restrict__ vals, i64 m, Text<TT> T, SampleLayout L,
+                           u32 *__restrict__ overflow) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < m; i += (i64)gridDim.x * blockDim.x) {
+        u64 k = keys[i];
+        if (keys[i + 1] != k || (i > 0 && keys[i - 1] == k)) continue;  // not a run head
+        i64 e = i + 2;
+        while (e < m && keys[e] == k && e - i <= FR_MAX) e++;
+        if (e - i > FR_MAX) {
+            atomicMax(overflow, 1u);
+            continue;
+        }
+        u32 v[FR_MAX], c[FR_MAX];
+        int len = (int)(e - i);
+        for (int x = 0; x < len; x++) {
+            v[x] = vals[i + x];
+            c[x] = T(L.pos(v[x]) + 2);
+        }
+        for (int x = 1; x < len; x++) {  // insertion sort by c2
+            u32 cv = c[x], vv = v[x];
+            int y = x - 1;
+            while (y >= 0 && c[y] > cv) {
+                c[y + 1] = c[y];
+                v[y + 1] = v[y];
+                y--;
+            }
+            c[y + 1] = cv;
+            v[y + 1] = vv;
+        }
+        for (int x = 0; x < len; x++) vals[i + x] = v[x];
+    }
+}
+struct StoreName {
+    u32 *names;
+    __device__ void operator()(i64 i, u32 excl, u32 v) const { names[i] = excl + v; }
+};
+
 __global__ void k_arec(const u64 *__restrict__ keys, const u32 *__restrict__ vals, SampleLayout L, int b,
                        const u32 *__restrict__ isac, uint4 *__restrict__ ra) {
     const u64 cm = ((u64)1 << b) - 1;
@@ -1391,31 +1536,62 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             }
             SAIX_LAUNCHED();
             SAIX_TRY(read_u32(d_scal, &D, st));
-            if ((i64)D < m || keep_u32)
-                SAIX_TRY(scan_transform(FlagPacked{keys}, ScatterName{vals, tt}, m, tmp, nullptr, st,
-                                        "dc3.name_scan", 16.0 * m));
+            if ((i64)D < m || keep_u32) {
+                u32 *names = reinterpret_cast<u32 *>(keys == k0 ? k1 : k0);
+                SAIX_TRY(scan_transform(FlagPacked{keys}, StoreName{names}, m, tmp, nullptr, st, "dc3.name_scan",
+                                        16.0 * m));
+                SAIX_TRY(scatter_u32(ar, vals, names, m, m, tt, st, "dc3.name_scatter"));
+            }
         } else {
-            // wide alphabet: stable sort by the third character, then stably
-            // by the mixed-radix pair of the first two (LSD over components)
+            // wide alphabet: bucket sort by (c0, c1), repeats ordered by c2
             u64 s1 = sigma + 1;
-            ThirdSrc<TT> src1{T, L};
-            SAIX_TRY(onesweep_sort<u64>(src1, m, src1, m, m, 0, (b + OS_BITS - 1) / OS_BITS, k0, v0, k1, v1,
-                                        scratch, keys, vals, nullptr, st, "dc3.triple_sort"));
-            PairGatherSrc<TT> src2{T, L, vals, s1};
-            PairStreamSrc<TT> hsrc2{T, L, s1};
-            int kb2 = bits_for(s1 * s1 - 1);
-            u64 *ok0 = keys == k0 ? k1 : k0;   // pass 0 must not overwrite its source
-            u32 *ov0 = vals == v0 ? v1 : v0;
-            SAIX_TRY(onesweep_sort<u64>(src2, m, hsrc2, m, m, 0, (kb2 + OS_BITS - 1) / OS_BITS, ok0, ov0, keys, vals,
-                                        scratch, keys, vals, nullptr, st, "dc3.triple_sort"));
-            SAIX_TRY(scan_transform(FlagWide<TT>{T, L, keys, vals}, ScatterName{vals, tt}, m, tmp, d_scal, st,
+            bool done = false;
+            if (sigma < ((u64)1 << 32) && m >= 4096) {
+                SAIX_TRY(bucket_sort(PairDenseSrc<TT>{T, L, s1}, m, sigma * s1 + sigma, k0, v0, scratch, done, st,
+                                     "dc3.triple_sort", &ar));
+                if (done) {
+                    SAIX_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(u32), st));
+                    {
+                        Prof prof_("dc3.fix_runs", 12.0 * m, st);
+                        k_fix_runs<TT><<<grid_for(m, 256), 256, 0, st>>>(k0, v0, m, T, L, d_scal);
+                    }
+                    SAIX_LAUNCHED();
+                    u32 of = 0;
+                    SAIX_TRY(read_u32(d_scal, &of, st));
+                    done = of == 0;
+                    keys = k0;
+                    vals = v0;
+                }
+            }
+            if (!done) {
+                // LSD over components: stably by the third character, then by
+                // the mixed-radix pair of the first two
+                ThirdSrc<TT> src1{T, L};
+                SAIX_TRY(onesweep_sort<u64>(src1, m, src1, m, m, 0, (b + OS_BITS - 1) / OS_BITS, k0, v0, k1, v1,
+                                            scratch, keys, vals, nullptr, st, "dc3.triple_sort"));
+                PairGatherSrc<TT> src2{T, L, vals, s1};
+                PairStreamSrc<TT> hsrc2{T, L, s1};
+                int kb2 = bits_for(s1 * s1 - 1);
+                u64 *ok0 = keys == k0 ? k1 : k0;  // pass 0 must not overwrite its source
+                u32 *ov0 = vals == v0 ? v1 : v0;
+                SAIX_TRY(onesweep_sort<u64>(src2, m, hsrc2, m, m, 0, (kb2 + OS_BITS - 1) / OS_BITS, ok0, ov0, keys,
+                                            vals, scratch, keys, vals, nullptr, st, "dc3.triple_sort"));
+            }
+            // names in sorted order (into the free key buffer), then scattered
+            u32 *names = reinterpret_cast<u32 *>(keys == k0 ? k1 : k0);
+            SAIX_TRY(scan_transform(FlagWide<TT>{T, L, keys, vals}, StoreName{names}, m, tmp, d_scal, st,
                                     "dc3.name_scan", 24.0 * m));
             SAIX_TRY(read_u32(d_scal, &D, st));
+            if ((i64)D < m || keep_u32) SAIX_TRY(scatter_u32(ar, vals, names, m, m, tt, st, "dc3.name_scatter"));
         }
         sorted_vals = vals;
         sorted_keys = keys;
         kbits = b;
     }
+    if (trace_on())
+        fprintf(stderr, "[saix dc3] depth %d: N=%lld text=u%d sigma=%llu m=%lld names=%u naming=%s%s\n", depth,
+                (long long)L.n, (int)sizeof(TT) * 8, (unsigned long long)sigma, (long long)m, D,
+                sorted_vals ? (bsorted ? "bucket-sort" : "radix") : "bitmap", (i64)D == m ? " (unique)" : "");
     if ((i64)D == m) {
         if (sorted_vals && m > ((i64)1 << 20)) {
             PsPlan pu = PsPlan::of(m, 4);
@@ -1496,6 +1672,14 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
     bool want_ra = sizeof(TT) == 4 && probe == nullptr && L.m >= 4096;
     SAIX_TRY(sort_samples<TT>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth, probe != nullptr,
                               want_ra ? &RA : nullptr));
+    if (!RA && want_ra) {
+        // recursion case: sample records from the child's order
+        RA = ar.alloc<uint4>(L.m);
+        SAIX_ARENA_OK(ar);
+        Prof prof_("dc3.arec", 36.0 * L.m, st);
+        k_arec_sa<TT><<<grid_for(L.m, 256), 256, 0, st>>>(SAc, T, L, ISAc, RA);
+        SAIX_LAUNCHED();
+    }
     if (RA) {
         bool fin = false;
         SAIX_TRY(dc3_wide_finish<TT>(c, T, L, sigma, ISAc, RA, SA, ISA, fin));
@@ -1728,9 +1912,11 @@ static size_t dc3_plan(i64 n, int text_bytes = 4) {
         persistent += (size_t)(3 * m + 8) * 4 + (size_t)N * 4 + 5 * Arena::kAlign;
         i64 sw = os_scratch_words(m) > bs_scratch_words(N / 8 + 2) ? os_scratch_words(m) : bs_scratch_words(N / 8 + 2);
         PsPlan pu = PsPlan::of(m, 4);
-        size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4 +
-                        (size_t)(pu.stage1_items() + pu.stage2_items()) * 8 + (size_t)pu.cursor_words() * 4 +
-                        4 * Arena::kAlign + bs_ps_bytes(m);
+        // sort buffers + the largest of the (sequential) bucketed scatters
+        size_t ps_u = (size_t)(pu.stage1_items() + pu.stage2_items()) * 8 + (size_t)pu.cursor_words() * 4;
+        size_t ps_max = bs_ps_bytes(m) > scatter_u32_bytes(m) ? bs_ps_bytes(m) : scatter_u32_bytes(m);
+        ps_max = ps_max > ps_u ? ps_max : ps_u;
+        size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4 + 4 * Arena::kAlign + ps_max;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
         i64 bw = mod0_bitmap_words(7, m);

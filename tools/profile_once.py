@@ -7,7 +7,14 @@ from paper_1404_3448_b200.sequence import gen_random, RankedText
 from paper_1404_3448_b200.suffix_index import DeviceText, dc3_device, lcp_device
 
 what = sys.argv[1] if len(sys.argv) > 1 else "c2"
-if what == "c2":
+if what == "c4":
+    from paper_1404_3448_b200.workloads import c4_pairs
+    seqs, offs = c4_pairs(0, 6700)      # one wave of <= 2^27 residues
+    ob = sx.OverlapBatch(seqs, offs)
+    ob.run_device(); ob.run_device()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start(); ob.run_device(); torch.cuda.synchronize(); torch.cuda.profiler.stop()
+elif what == "c2":
     a, b = gen_random(10_000_000, 11), gen_random(10_000_000, 12)
     ha = np.frombuffer(a.residues.encode(), np.uint8); hb = np.frombuffer(b.residues.encode(), np.uint8)
     p = sx.OverlapPipeline(len(ha), len(hb))
