@@ -135,16 +135,18 @@ inline size_t bs_ps_bytes(i64 n) {
     return (size_t)(p.stage1_items() + p.stage2_items()) * 16 + (size_t)p.cursor_words() * 4 + 4 * Arena::kAlign;
 }
 
-// ascending bitonic sort of one (key, val) per lane across the warp
-__device__ __forceinline__ void warp_bitonic32(u64 &k, u32 &v) {
+// ascending bitonic sort of one (key, val) per lane inside aligned segments
+// of W lanes (W = 8, 16, 32)
+template <int W>
+__device__ __forceinline__ void seg_bitonic(u64 &k, u32 &v) {
     const int lane = lane_id();
 #pragma unroll
-    for (int size = 2; size <= 32; size <<= 1) {
+    for (int size = 2; size <= W; size <<= 1) {
 #pragma unroll
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             u64 ok = __shfl_xor_sync(0xffffffffu, k, stride);
             u32 ov = __shfl_xor_sync(0xffffffffu, v, stride);
-            bool up = (lane & size) == 0 || size == 32;
+            bool up = (lane & size) == 0 || size == W;
             bool lower = (lane & stride) == 0;
             bool take = (lower == up) ? (ok < k) : (ok > k);
             if (take) {
@@ -155,8 +157,42 @@ __device__ __forceinline__ void warp_bitonic32(u64 &k, u32 &v) {
     }
 }
 
+// sort the buckets flagged in `todo` (lane q of the warp holds bucket q's
+// length / start), 32/W buckets per round, one W-lane segment each
+template <int W>
+__device__ __forceinline__ void tiny_round(u32 todo, u32 my_len, u32 my_s0, u64 *__restrict__ keys,
+                                           u32 *__restrict__ vals) {
+    const int lane = lane_id();
+    const int g = lane / W, sl = lane & (W - 1);
+    while (todo) {
+        // the g-th set bit of todo belongs to segment g
+        u32 t = todo;
+        int q = -1;
+        for (int x = 0; x < 32 / W; x++) {
+            int f = t ? __ffs(t) - 1 : -1;
+            if (x == g) q = f;
+            if (t) t &= t - 1;
+        }
+        todo = t;
+        u32 len = __shfl_sync(0xffffffffu, my_len, q < 0 ? 0 : q);
+        u32 s0 = __shfl_sync(0xffffffffu, my_s0, q < 0 ? 0 : q);
+        if (q < 0) len = 0;
+        u64 k = ~0ull;
+        u32 v = 0xFFFFFFFFu;
+        if ((u32)sl < len) {
+            k = keys[s0 + sl];
+            v = vals[s0 + sl];
+        }
+        seg_bitonic<W>(k, v);
+        if ((u32)sl < len) {
+            keys[s0 + sl] = k;
+            vals[s0 + sl] = v;
+        }
+    }
+}
+
 // buckets of <= 32 items: a warp takes 32 consecutive buckets (coalesced
-// count/start reads) and sorts them one after another in registers
+// count/start reads) and sorts them in register segments of 8/16/32 lanes
 __global__ void __launch_bounds__(256)
 k_bs_tiny(const u32 *__restrict__ start, const u32 *__restrict__ cnt, i64 nb, u64 *__restrict__ keys,
           u32 *__restrict__ vals) {
@@ -165,24 +201,9 @@ k_bs_tiny(const u32 *__restrict__ start, const u32 *__restrict__ cnt, i64 nb, u6
     for (i64 b0 = (((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; b0 < nb; b0 += warps * 32) {
         u32 my_len = b0 + lane < nb ? cnt[b0 + lane] : 0u;
         u32 my_s0 = b0 + lane < nb ? start[b0 + lane] : 0u;
-        u32 todo = __ballot_sync(0xffffffffu, my_len > 1 && my_len <= BS_TINY);
-        while (todo) {
-            int q = __ffs(todo) - 1;
-            todo &= todo - 1;
-            u32 len = __shfl_sync(0xffffffffu, my_len, q);
-            u32 s0 = __shfl_sync(0xffffffffu, my_s0, q);
-            u64 k = ~0ull;
-            u32 v = 0xFFFFFFFFu;
-            if ((u32)lane < len) {
-                k = keys[s0 + lane];
-                v = vals[s0 + lane];
-            }
-            warp_bitonic32(k, v);
-            if ((u32)lane < len) {
-                keys[s0 + lane] = k;
-                vals[s0 + lane] = v;
-            }
-        }
+        tiny_round<8>(__ballot_sync(0xffffffffu, my_len > 1 && my_len <= 8), my_len, my_s0, keys, vals);
+        tiny_round<16>(__ballot_sync(0xffffffffu, my_len > 8 && my_len <= 16), my_len, my_s0, keys, vals);
+        tiny_round<32>(__ballot_sync(0xffffffffu, my_len > 16 && my_len <= BS_TINY), my_len, my_s0, keys, vals);
     }
 }
 

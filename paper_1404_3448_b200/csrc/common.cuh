@@ -17,6 +17,7 @@
 namespace saix {
 
 using u8 = uint8_t;
+using u16 = uint16_t;
 using u32 = uint32_t;
 using u64 = uint64_t;
 using i64 = int64_t;
@@ -130,6 +131,20 @@ __device__ __forceinline__ u32 lanemask_lt() {
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Peer mask of lanes holding the same 8-bit digit: eight ballots + ANDs
+// (cheaper than __match_any_sync on sm_100).  Lanes with d == OS_RADIX (no
+// item) differ from every valid digit in bit 8 via the `valid` ballot.
+__device__ __forceinline__ u32 digit_peers(u32 d) {
+    u32 peers = __ballot_sync(0xffffffffu, d < 256u);
+    if (d >= 256u) peers = ~peers;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        u32 m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? m : ~m;
+    }
+    return peers;
+}
 
 inline int bits_for(u64 v) {  // bit width of v (>= 1), like int.bit_length()
     int b = 1;

@@ -751,7 +751,7 @@ k_rs_window(const uint4 *__restrict__ stage2, PsPlan plan, uint4 *__restrict__ r
             }
             if (e.x % 3 == 1) d = (e.w >> 16) & 0xFFu;
         }
-        u32 peers = __match_any_sync(0xffffffffu, d);
+        u32 peers = digit_peers(d);
         if (d != 0xFFFFFFFFu && (peers & lanemask_lt()) == 0) atomicAdd(&cnt[d], (u32)__popc(peers));
     }
     __syncthreads();
@@ -796,7 +796,7 @@ k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__res
     for (int r = 0; r < M0_ITEMS; r++) {
         u32 d = (pk[r] >> 8) & 0x1FFu;
         bool ok = d < 256u;
-        u32 peers = __match_any_sync(0xffffffffu, d);
+        u32 peers = digit_peers(d);
         u32 before = __popc(peers & lt);
         u32 cur = ok ? cnt[wp][d] : 0u;
         __syncwarp();

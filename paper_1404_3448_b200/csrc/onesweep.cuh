@@ -36,20 +36,6 @@ constexpr int OS_MAX_PASSES = 8;
 constexpr u32 OS_FLAG_AGG = 1u << 30, OS_FLAG_PRE = 2u << 30, OS_MASK = (1u << 30) - 1;
 static_assert(OS_THREADS == OS_RADIX, "one thread per digit in the look-back phase");
 
-// Peer mask of lanes holding the same 8-bit digit: eight ballots + ANDs
-// (cheaper than __match_any_sync on sm_100).  Lanes with d == OS_RADIX (no
-// item) differ from every valid digit in bit 8 via the `valid` ballot.
-__device__ __forceinline__ u32 digit_peers(u32 d) {
-    u32 peers = __ballot_sync(0xffffffffu, d < OS_RADIX);
-    if (d >= OS_RADIX) peers = ~peers;
-#pragma unroll
-    for (int b = 0; b < OS_BITS; b++) {
-        u32 m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        peers &= ((d >> b) & 1u) ? m : ~m;
-    }
-    return peers;
-}
-
 template <typename K>
 struct ArraySrc {
     const K *keys;

@@ -12,6 +12,8 @@
 //           choice is a u64 atomicMin of (minA << 32 | minB) at run ends.
 #include <vector>
 
+#include "lcp_direct.cuh"
+#include "lsd.cuh"
 #include "onesweep.cuh"
 #include "scan.cuh"
 
@@ -447,7 +449,13 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
 namespace saix {
 
 __device__ __forceinline__ u32 pair_of(const i64 *__restrict__ xoff, i64 P, i64 stride, i64 g) {
-    if (stride > 0) return (u32)(g / stride);
+    if (stride > 0) {
+        // g < 2^30, stride < 2^30: double quotient, corrected to the exact floor
+        u32 q = (u32)((double)g * (1.0 / (double)stride));
+        if ((i64)(q + 1) * stride <= g) q++;
+        else if ((i64)q * stride > g) q--;
+        return q;
+    }
     i64 lo = 0, hi = P - 1;  // largest p with xoff[p] <= g
     while (lo < hi) {
         i64 mid = (lo + hi + 1) >> 1;
@@ -486,6 +494,12 @@ __global__ void k_batch_build_x(const u8 *__restrict__ seqs, const i64 *__restri
     if (local_bad != INT64_MAX) atomicMin((unsigned long long *)bad, (unsigned long long)local_bad);
 }
 
+struct PairKey {
+    const i64 *xoff;
+    i64 P, stride;
+    __device__ __forceinline__ u32 operator()(u32 v) const { return pair_of(xoff, P, stride, v); }
+};
+
 struct PairSrc {
     const u32 *sa;
     const i64 *xoff;
@@ -508,9 +522,70 @@ __global__ void k_batch_phi(const u32 *__restrict__ sap, i64 nx, const i64 *__re
     }
 }
 
+// Direct LCP inside each pair block of the partitioned SA: lcp[r] of the
+// adjacent suffixes sap[r-1], sap[r] (same pair) by word compares on the
+// 2-bit packed wave text.  The pair's separator xs and terminator xt are
+// unique inside the pair, so a match stops at the nearer of them for either
+// suffix (the packed codes of those two symbols are never trusted).
+struct PairClamp {
+    const i64 *xoff, *offs;
+    i64 P, stride;
+    __device__ __forceinline__ u32 lim(u32 g, u32 i, u32 j) const {
+        i64 x0 = xoff[g];
+        i64 xs = x0 + (offs[2 * g + 1] - offs[2 * g]), xt = xoff[g + 1] - 1;
+        i64 li = (i <= xs ? xs : xt) - (i64)i, lj = (j <= xs ? xs : xt) - (i64)j;
+        return (u32)(li < lj ? li : lj);
+    }
+};
+
+template <class Txt>
+__global__ void k_batch_lcp(Txt tx, const u32 *__restrict__ sap, i64 nx, PairClamp pc, u32 *__restrict__ lcp,
+                            u32 *__restrict__ ncap, u32 *__restrict__ list, u32 list_cap) {
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < nx; r += (i64)gridDim.x * blockDim.x) {
+        u32 g = pair_of(pc.xoff, pc.P, pc.stride, r);
+        u32 h = 0;
+        if (r > pc.xoff[g] + 1) {  // the terminator entry and the first real suffix have no predecessor
+            u32 i = sap[r - 1], j = __ldcs(sap + r);
+            u32 lim = pc.lim(g, i, j);
+            u32 stop = lim < LCP_CAP ? lim : LCP_CAP;
+            h = tx.match(i, j, 0, stop);
+            if (h == LCP_CAP && lim > LCP_CAP) {
+                u32 at = atomicAdd(ncap, 1u);
+                if (at < list_cap) list[at] = (u32)r;
+            }
+        }
+        __stcs(lcp + r, h);
+    }
+}
+
+template <class Txt>
+__global__ void k_batch_lcp_extend(Txt tx, const u32 *__restrict__ sap, PairClamp pc, u32 *__restrict__ lcp,
+                                   const u32 *__restrict__ ncap, const u32 *__restrict__ list) {
+    const u32 cnt = *ncap;
+    const int lane = lane_id();
+    for (u32 e = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < cnt; e += ((i64)gridDim.x * blockDim.x) >> 5) {
+        u32 r = list[e];
+        u32 i = sap[r - 1], j = sap[r];
+        u32 lim = pc.lim(pair_of(pc.xoff, pc.P, pc.stride, r), i, j);
+        u32 h = LCP_CAP;
+        while (h < lim) {
+            u32 lo = h + 32u * lane;
+            u32 hi = min(lo + 32u, lim);
+            u32 got = lo < lim ? tx.match(i, j, lo, hi) : lo;
+            u32 short_ = __ballot_sync(0xffffffffu, lo < lim && got < hi);
+            if (short_) {
+                h = __shfl_sync(0xffffffffu, got, __ffs(short_) - 1);
+                break;
+            }
+            h = min(h + 32u * 32u, lim);
+        }
+        if (lane == 0) lcp[r] = h;
+    }
+}
+
 __global__ void __launch_bounds__(OV_THREADS)
 k_batch_overlap(const u32 *__restrict__ sap, const u32 *__restrict__ plcp, const i64 *__restrict__ xoff,
-                const i64 *__restrict__ offs, i64 P, i64 *__restrict__ out) {
+                const i64 *__restrict__ offs, i64 P, i64 *__restrict__ out, int by_rank) {
     __shared__ u32 sh_red[OV_THREADS / 32];
     __shared__ unsigned long long sh_win[OV_THREADS / 32];
     for (i64 p = blockIdx.x; p < P; p += gridDim.x) {
@@ -526,7 +601,7 @@ k_batch_overlap(const u32 *__restrict__ sap, const u32 *__restrict__ plcp, const
         for (i64 r = s0 + 1 + threadIdx.x; r < x1; r += OV_THREADS) {
             u32 ga = (u32)(sap[r - 1] - x0), gb = (u32)(sap[r] - x0);
             bool cross = ga != la && gb != la && ((ga < la) != (gb < la));
-            if (cross) mx = max(mx, plcp[sap[r]]);
+            if (cross) mx = max(mx, plcp[by_rank ? (u32)r : sap[r]]);
         }
         for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane_id() == 0) sh_red[threadIdx.x >> 5] = mx;
@@ -548,11 +623,11 @@ k_batch_overlap(const u32 *__restrict__ sap, const u32 *__restrict__ plcp, const
             bool end = false;
             if (live) {
                 u32 g = sap[r], loc = g - (u32)x0;
-                u32 l = r == s0 ? 0u : plcp[g];
+                u32 l = r == s0 ? 0u : plcp[by_rank ? (u32)r : g];
                 e.f = (r == s0 || l < best) ? 1u : 0u;
                 e.a = loc < la ? loc : kInf;
                 e.b = loc > la ? loc : kInf;
-                end = (r + 1 >= x1) || plcp[sap[r + 1]] < best;
+                end = (r + 1 >= x1) || plcp[by_rank ? (u32)(r + 1) : sap[r + 1]] < best;
             }
             Seg tot;
             Seg ex = block_seg_exclusive(e, tot);
@@ -613,6 +688,8 @@ struct BatchWs {
     u32 *k0, *v0, *k1, *v1, *scratch;
     void *plcp_ws;
     size_t plcp_bytes;
+    u64 *W2;
+    u32 *ncap, *list;
 };
 
 static size_t batch_ws(Arena &ar, i64 P, i64 nx, BatchWs *w) {
@@ -630,9 +707,12 @@ static size_t batch_ws(Arena &ar, i64 P, i64 nx, BatchWs *w) {
     t.v0 = ar.alloc<u32>(nx);
     t.k1 = ar.alloc<u32>(nx);
     t.v1 = ar.alloc<u32>(nx);
-    t.scratch = ar.alloc<u32>(os_scratch_words(nx));
+    t.scratch = ar.alloc<u32>(lsd_scratch_words(nx) > os_scratch_words(nx) ? lsd_scratch_words(nx) : os_scratch_words(nx));
     t.plcp_bytes = plcp_workspace_bytes(nx);
     t.plcp_ws = ar.alloc<char>((i64)t.plcp_bytes);
+    t.W2 = ar.alloc<u64>(pack2_words(nx));
+    t.ncap = ar.alloc<u32>(2);
+    t.list = ar.alloc<u32>(lcp_list_cap(nx));
     if (ar.mark() < peak_dc3) ar.reset(peak_dc3);
     if (w) *w = t;
     return ar.peak;
@@ -672,29 +752,65 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
     }
     SAIX_LAUNCHED();
     if (nx == 0) {
-        k_batch_overlap<<<1, OV_THREADS, 0, st>>>(nullptr, nullptr, w.xoff, w.offs, P, out);
+        k_batch_overlap<<<1, OV_THREADS, 0, st>>>(nullptr, nullptr, w.xoff, w.offs, P, out, 0);
         SAIX_LAUNCHED();
         return SAIX_OK;
     }
     int sigma = keep_n ? 7 : 6;  // terminator 1, separator 2, residues 3..6 (N 7)
     SAIX_TRY(dc3_compute(w.X, 1, nx, sigma, w.sa, nullptr, w.dc3, w.dc3_bytes, nullptr, st));
     // stable partition by pair id: each pair's suffixes keep their order
-    u32 *keys = w.k0, *sap = w.v0;
-    int passes = (bits_for((u64)(P > 1 ? P - 1 : 1)) + OS_BITS - 1) / OS_BITS;
-    PairSrc src{w.sa, w.xoff, P, b.stride};
-    SAIX_TRY(onesweep_sort<u32>(src, nx, src, nx, nx, 0, passes, w.k0, w.v0, w.k1, w.v1, w.scratch, keys, sap,
-                                nullptr, st, "batch.partition"));
-    u32 *phi = w.sa;  // SA(X) is no longer needed
+    u32 *sap = nullptr;
+    int passes = (bits_for((u64)(P > 1 ? P - 1 : 1)) + 7) / 8;
+    SAIX_TRY(lsd_partition(PairKey{w.xoff, P, b.stride}, w.sa, w.v0, nx, passes, w.scratch, sap, st,
+                           "batch.partition"));
+    // LCP inside each pair block: direct word compares (2-bit packed wave
+    // text: residues 3..6; N residues -> byte compares), capped entries
+    // extended by one warp each; highly repetitive pairs -> Phi / PLCP walk
+    u32 *lcp = sap == w.sa ? w.v0 : w.sa;  // SA(X) is no longer needed
+    PairClamp pc{w.xoff, w.offs, P, b.stride};
+    bool pack = !keep_n;
+    u32 lc = (u32)lcp_list_cap(nx);
+    SAIX_CUDA(cudaMemsetAsync(w.ncap, 0, sizeof(u32), st));
+    if (pack) {
+        i64 nw = pack2_words(nx);
+        {
+            Prof prof_("lcp.pack2", (double)nx + 8.0 * nw, st);
+            k_pack2<<<grid_for(nw, 256), 256, 0, st>>>(w.X, nx, 3u, w.W2, nw);
+        }
+        SAIX_LAUNCHED();
+    }
     {
-        Prof prof_("batch.phi", 12.0 * nx, st);
-        k_batch_phi<<<grid_for(nx, 256), 256, 0, st>>>(sap, nx, w.xoff, P, b.stride, phi);
+        Prof prof_("batch.lcp", 12.0 * nx + nx / 2.0, st);
+        if (pack) k_batch_lcp<Pack2Text><<<grid_for(nx, 256), 256, 0, st>>>(Pack2Text{w.W2}, sap, nx, pc, lcp, w.ncap,
+                                                                           w.list, lc);
+        else k_batch_lcp<ByteText><<<grid_for(nx, 256), 256, 0, st>>>(ByteText{w.X, nx}, sap, nx, pc, lcp, w.ncap,
+                                                                     w.list, lc);
     }
     SAIX_LAUNCHED();
-    SAIX_TRY(plcp_from_phi(w.X, nx, phi, w.plcp_ws, w.plcp_bytes, st));
+    u32 hc = 0;
+    SAIX_CUDA(cudaMemcpyAsync(&hc, w.ncap, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    SAIX_CUDA(cudaStreamSynchronize(st));
+    int by_rank = 1;
+    if (hc > 0 && hc <= lc) {
+        Prof prof_("batch.lcp_extend", 0.0, st);
+        int ge = grid_for((i64)hc * 32, 256);
+        if (pack) k_batch_lcp_extend<Pack2Text><<<ge, 256, 0, st>>>(Pack2Text{w.W2}, sap, pc, lcp, w.ncap, w.list);
+        else k_batch_lcp_extend<ByteText><<<ge, 256, 0, st>>>(ByteText{w.X, nx}, sap, pc, lcp, w.ncap, w.list);
+        SAIX_LAUNCHED();
+    } else if (hc > lc) {
+        u32 *phi = lcp;
+        {
+            Prof prof_("batch.phi", 12.0 * nx, st);
+            k_batch_phi<<<grid_for(nx, 256), 256, 0, st>>>(sap, nx, w.xoff, P, b.stride, phi);
+        }
+        SAIX_LAUNCHED();
+        SAIX_TRY(plcp_from_phi(w.X, nx, phi, w.plcp_ws, w.plcp_bytes, st));
+        by_rank = 0;
+    }
     {
-        Prof prof_("batch.overlap", 12.0 * nx, st);
-        k_batch_overlap<<<(unsigned)(P < 65535 ? P : 65535), OV_THREADS, 0, st>>>(sap, phi, w.xoff, w.offs, P,
-                                                                                   out);
+        Prof prof_("batch.overlap", 8.0 * nx, st);
+        k_batch_overlap<<<(unsigned)(P < 65535 ? P : 65535), OV_THREADS, 0, st>>>(sap, lcp, w.xoff, w.offs, P, out,
+                                                                                   by_rank);
     }
     SAIX_LAUNCHED();
     return SAIX_OK;

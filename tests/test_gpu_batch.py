@@ -64,3 +64,36 @@ def test_first_bad_pair_raises_like_reference():
         sx.longest_overlap_batch(pairs)
     ok = sx.longest_overlap_batch([(DnaSequence("a", ""), DnaSequence("b", "XYZ"))])
     assert ok == [sx.OverlapResult(0, 0, 0)]
+
+
+def test_many_short_pairs_two_partition_passes():
+    """> 256 pairs per wave: the pair-id partition takes two LSD passes."""
+    seqs, offs = c4_pairs(0, 1500, length=300)
+    want = oracle.overlap_batch(seqs, offs, threads=4)
+    ob = sx.OverlapBatch(seqs, offs)
+    ob.run_device()
+    assert np.array_equal(ob.results(), want)
+
+
+def test_keep_n_pairs_byte_compare():
+    rng = np.random.default_rng(5)
+    pairs = []
+    for _ in range(40):
+        a = "".join(rng.choice(list("ACGTN"), size=1500))
+        b = list("".join(rng.choice(list("ACGTN"), size=1500)))
+        b[300:700] = a[900:1300]
+        pairs.append((DnaSequence("a", a), DnaSequence("b", "".join(b))))
+    got = sx.longest_overlap_batch(pairs, sx.NPolicy.KEEP)
+    for (a, b), r in zip(pairs, got):
+        assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a.residues, b.residues, keep_n=True)
+        assert r.length >= 400
+
+
+def test_repetitive_pairs_kasai_fallback():
+    """Most adjacent LCPs exceed the direct-compare cap: the Phi/PLCP path."""
+    pairs = [(DnaSequence("a", "A" * 3000), DnaSequence("b", "A" * 2000 + "C")),
+             (DnaSequence("a", "ACG" * 900), DnaSequence("b", "CGA" * 700)),
+             (DnaSequence("a", "AC" * 10), DnaSequence("b", "GT" * 10))]
+    got = sx.longest_overlap_batch(pairs)
+    for (a, b), r in zip(pairs, got):
+        assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a.residues, b.residues)

@@ -340,3 +340,34 @@ class TestDirectLcp:
         r = sx.longest_overlap(DnaSequence("a", a), DnaSequence("b", b), sx.NPolicy.KEEP)
         assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a, b, keep_n=True)
         assert r.length >= 500
+
+
+class TestDeepLevels:
+    """Recursing u32 levels (wide-level finish from the child's order), wide
+    naming by (c0, c1) bucket sort with in-run c2 fix-up, and its fallback."""
+
+    def test_repeated_blocks_deep_recursion(self):
+        rng = np.random.default_rng(11)
+        blocks = [rng.integers(1, 5, size=int(rng.integers(50, 400))) for _ in range(40)]
+        parts = [blocks[int(rng.integers(0, 40))] for _ in range(3000)]
+        r = np.concatenate(parts)[: 1 << 20]
+        t = RankedText(r, 4)
+        ws = sx.prepare_dc3_workspace(t)
+        assert ws.depth >= 4
+        ix = sx.build_sa_dc3(t)
+        sa, rank = oracle.dc3(r, 4)
+        assert np.array_equal(ix.sa, sa) and np.array_equal(ix.rank, rank)
+        assert np.array_equal(sx.build_lcp(t, ix).lcp, oracle.lcp(r, sa, rank))
+
+    @pytest.mark.parametrize("hot", [0, 40, 200])
+    def test_wide_alphabet_repeats(self, hot):
+        rng = np.random.default_rng(12 + hot)
+        sigma = 1 << 22
+        r = rng.integers(1, sigma + 1, size=120_000)
+        r[50_000:52_000] = r[10_000:12_000]                  # equal (c0, c1, c2) runs
+        for k in range(hot):                                  # one (c0, c1) pair `hot` times
+            r[70_000 + 3 * k: 70_000 + 3 * k + 2] = (7, 9)
+        t = RankedText(r, sigma)
+        ix = sx.build_sa_dc3(t)
+        sa, rank = oracle.dc3(r, sigma)
+        assert np.array_equal(ix.sa, sa) and np.array_equal(ix.rank, rank)
