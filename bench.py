@@ -131,15 +131,34 @@ def count_our_launches(fn) -> int:
     return n
 
 
-def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch of `kernel` from a committed
-    `ncu --set full` capture summary (profiles/ncu_traffic.json), if any."""
+def ncu_traffic(workload: str, scope: str):
+    """DRAM read+write bytes per invocation of the prof scope `scope` from the
+    committed ncu launch-list summary (profiles/ncu_traffic.json, written by
+    tools/make_traffic.py from `ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum,...` of one step of the same workload), if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(kernel)
+            return json.load(f).get(workload, {}).get(scope)
     except Exception:
         return None
+
+
+def dc3_model_bytes(trace, isa: bool = False) -> float:
+    """SURVEY.md section 8(d) contract: algorithmic DC3 bytes over the level
+    trace (N, sigma, m, names) -- per level (k = ceil(N/3), r = recurses,
+    w = 1 at level 0 and 4 below): (wN + 8m) + 72m + 16m + 8m r + (4m + (12+w)k)
+    + (4m + 4k + (2w+8)N), plus 8n for a top-level ISA."""
+    total = 0.0
+    for lvl, (n_l, _sigma, m, names) in enumerate(trace):
+        w = 1 if lvl == 0 else 4
+        k = (n_l + 2) // 3
+        r = 1 if names < m else 0
+        total += (w * n_l + 8 * m) + 72 * m + 16 * m + 8 * m * r + (4 * m + (12 + w) * k) \
+            + (4 * m + 4 * k + (2 * w + 8) * n_l)
+    if isa and trace:
+        total += 8 * trace[0][0]
+    return total
 
 
 def encode_ascii(residues: str, shift: int = 0) -> np.ndarray:
@@ -355,6 +374,7 @@ class C4:
                                    "shared block (paper_1404_3448_b200/workloads.py), batched waves of <= 2^27 "
                                    "residues, results all-gathered over NCCL",
                        "pairs": self.TOTAL, "pairs_this_rank": self.P, "waves_this_rank": len(self.ob.waves)}
+        self.dc3_calls_per_step = len(self.ob.waves)
 
     def _gather(self):
         if self.dist is None:
@@ -465,12 +485,18 @@ def bench(args, rank, world, dist):
 
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
-    _lib.prof_enable(not args.no_prof)
     ms_dev = timed(wl.step_device, args.steps)    # value: inputs resident in HBM
-    prof = _lib.prof_collect()
-    _lib.prof_enable(False)
     ms_e2e = timed(wl.step_e2e, args.steps)       # e2e: pinned host in, results out
     clk = clocks.stop()
+    # per-kernel CUDA events (launching stream) in a separate pass of the same
+    # K steps, so the timed value carries no event overhead
+    prof = []
+    if not args.no_prof:
+        _lib.prof_enable(True)
+        ms_prof = timed(wl.step_device, args.steps)
+        prof = _lib.prof_collect()
+        _lib.prof_enable(False)
+    trace = _lib.dc3_trace()
 
     launches_per_step = count_our_launches(wl.step_device)
     peak, peak_kind = measured_peak_gbs()
@@ -482,10 +508,22 @@ def bench(args, rank, world, dist):
         ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": dom["name"], "achieved": round(ach, 1), "peak": peak,
                 "peak_source": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": ncu_traffic(dom["name"]),
+                "traffic": ncu_traffic(args.workload, dom["name"]),
                 "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                 "share_of_step": round(dom["ms"] / ms_dev, 4) if ms_dev else None}
     stage = {e["name"]: round(e["ms"] / args.steps, 4) for e in sorted(prof, key=lambda e: -e["ms"])}
+    # whole-DC3 roofline against the section 8(d) contract bytes of the last
+    # DC3 level trace (per DC3 call; C4 runs one DC3 per wave)
+    dc3_roof = None
+    dc3_ms = sum(e["ms"] for e in prof if e["name"].startswith("dc3.")) / args.steps
+    if trace and dc3_ms > 0:
+        calls = getattr(wl, "dc3_calls_per_step", 1)
+        mb = dc3_model_bytes(trace) * calls
+        ach = mb / (dc3_ms * 1e-3) / 1e9
+        dc3_roof = {"model_bytes_per_step": mb, "dc3_ms_per_step": round(dc3_ms, 4),
+                    "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                    "levels": [list(t) for t in trace],
+                    "note": "SURVEY.md 8(d) textbook stage model; level trace of the last DC3 call"}
 
     scale = 1e6 if wl.unit == "Mbases/s" else 1.0
     total = getattr(wl, "units_total", wl.units * world)
@@ -516,7 +554,7 @@ def bench(args, rank, world, dist):
             "e2e": {"value": round(e2e_value, 2), "unit": wl.unit, "h2d_bytes_per_step": wl.h2d,
                     "d2h_bytes_per_step": wl.d2h, "ms_per_step": round(ms_e2e / args.steps, 4)},
             "gpu_launches": launches_per_step * args.steps,
-            "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+            "roofline": roof, "dc3_roofline": dc3_roof, "cpu_baseline": cpu, "clocks": clk,
             "stage_ms_per_step": stage,
         }
         if results is not None:

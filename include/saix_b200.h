@@ -111,6 +111,11 @@ SAIX_API int saix_dc3_merge(const void *text, int text_bytes, int64_t n,
                    int64_t ms, const uint32_t *sorted_nonsamples, int64_t k,
                    uint32_t *sa, void *ws, size_t ws_bytes, void *stream);
 
+/* Level trace of the last saix_dc3 call on this host thread: per recursion
+ * level (top first) {N, sigma, samples m, distinct triple names}; returns
+ * the number of levels (at most max_levels are written to out[4*i..]). */
+SAIX_API int saix_dc3_trace(int64_t *out, int max_levels);
+
 /* ------------------------------------------------------------------- LCP */
 
 SAIX_API size_t saix_lcp_workspace_bytes(int64_t n);

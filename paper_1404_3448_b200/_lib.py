@@ -76,6 +76,7 @@ SIGNATURES = {
     "saix_lcp_workspace_bytes": (_c.c_size_t, [_i64]),
     "saix_lcp": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_lcp_sigma": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_dc3_trace": (_int, [_vp, _int]),
     "saix_minmax": (_int, [_vp, _int, _i64, _vp, _vp]),
     "saix_sparse_plan_make": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),
     "saix_sparse_build": (_int, [_c.POINTER(SparsePlan), _vp, _int, _vp, _vp]),
@@ -207,3 +208,11 @@ def prof_collect() -> list[dict]:
     n = L.saix_prof_collect(buf, 256)
     return [{"name": buf[i].name.decode(), "launches": int(buf[i].launches),
              "ms": float(buf[i].total_ms), "bytes": float(buf[i].bytes)} for i in range(min(n, 256))]
+
+
+def dc3_trace() -> list[tuple[int, int, int, int]]:
+    """(N, sigma, m, distinct names) per level of the last DC3 on this thread."""
+    import numpy as np
+    out = np.zeros(4 * 64, np.int64)
+    k = load().saix_dc3_trace(out.ctypes.data, 64)
+    return [tuple(int(x) for x in out[4 * i: 4 * i + 4]) for i in range(min(k, 64))]

@@ -20,6 +20,8 @@
 //             position left, stably split by first character.
 //   4 merge   (_merge_walk 173-218): merge-path partition with the DC3
 //             comparator, ISA scattered in the same kernel.
+#include <vector>
+
 #include "bsort.cuh"
 #include "onesweep.cuh"
 #include "pscatter.cuh"
@@ -1083,6 +1085,13 @@ struct Dc3Ctx {
     int max_depth;
 };
 
+// Level trace of the last saix_dc3 / dc3_compute on this host thread
+// (saix_dc3_trace): (N, sigma, m, distinct names) per level, top first.
+struct LevelRec {
+    i64 n, sigma, m, names;
+};
+static thread_local std::vector<LevelRec> g_trace;
+
 // SAIX_TRACE=1: one stderr line per level (development aid)
 static bool trace_on() {
     static int v = [] {
@@ -1588,6 +1597,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         sorted_keys = keys;
         kbits = b;
     }
+    if ((size_t)depth >= g_trace.size()) g_trace.resize((size_t)depth + 1);
+    g_trace[(size_t)depth] = LevelRec{L.n, (i64)sigma, m, (i64)D};
     if (trace_on())
         fprintf(stderr, "[saix dc3] depth %d: N=%lld text=u%d sigma=%llu m=%lld names=%u naming=%s%s\n", depth,
                 (long long)L.n, (int)sizeof(TT) * 8, (unsigned long long)sigma, (long long)m, D,
@@ -1980,6 +1991,7 @@ int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32
     ar.base = (char *)ws;
     ar.cap = ws_bytes;
     Dc3Ctx c{&ar, (cudaStream_t)stream, 0};
+    g_trace.clear();
     if (probe) {
         probe->depth = 0;
         probe->n_samples = probe->n_sorted_samples = 0;
@@ -2043,4 +2055,15 @@ extern "C" int saix_dc3_merge(const void *text, int text_bytes, int64_t n, const
         rc = merge_run(V, ms, k, split, sa, nullptr, st);
     }
     return rc;
+}
+
+extern "C" int saix_dc3_trace(int64_t *out, int max_levels) {
+    int n = (int)g_trace.size();
+    for (int i = 0; i < n && i < max_levels; i++) {
+        out[4 * i + 0] = g_trace[i].n;
+        out[4 * i + 1] = g_trace[i].sigma;
+        out[4 * i + 2] = g_trace[i].m;
+        out[4 * i + 3] = g_trace[i].names;
+    }
+    return n;
 }

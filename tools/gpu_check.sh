@@ -12,8 +12,10 @@ for what in "$@"; do
     c2|c3|c4|c5) timeout 900 python bench.py --workload $what > $O/bench_$what.json 2> $O/bench_$what.err; tail -c 600 $O/bench_$what.json; tail -3 $O/bench_$what.err ;;
     ref) timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err; cat $O/bench_ref.json ;;
     ncu_c2) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/c2_launches.csv python tools/profile_once.py c2 > $O/ncu_c2.log 2>&1; python tools/ncu_summary.py $O/c2_launches.csv > $O/c2_launches.txt; head -30 $O/c2_launches.txt ;;
+    ncu_c4|ncu_c5) W=${what#ncu_}; timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/${W}_launches.csv python tools/profile_once.py $W > $O/ncu_$W.log 2>&1; python tools/ncu_summary.py $O/${W}_launches.csv 40 > $O/${W}_launches.txt; head -25 $O/${W}_launches.txt ;;
     ncu_c3) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/c3_launches.csv python tools/profile_once.py 268435456 > $O/ncu_c3.log 2>&1; python tools/ncu_summary.py $O/c3_launches.csv > $O/c3_launches.txt; head -30 $O/c3_launches.txt ;;
     c3full_*) K=${what#c3full_}; timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:$K -c 1 -o $O/c3full_$K python tools/profile_once.py 268435456 > $O/ncu_c3full_$K.log 2>&1; tail -2 $O/ncu_c3full_$K.log ;;
+    c2full_*) K=${what#c2full_}; timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:$K -c 1 -o $O/c2full_$K python tools/profile_once.py c2 > $O/ncu_c2full_$K.log 2>&1; tail -2 $O/ncu_c2full_$K.log ;;
     full_*) K=${what#full_}; timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:$K -c 1 -o $O/full_$K python tools/profile_once.py c2 > $O/ncu_full_$K.log 2>&1; tail -3 $O/ncu_full_$K.log ;;
   esac
 done

@@ -7,7 +7,13 @@ from paper_1404_3448_b200.sequence import gen_random, RankedText
 from paper_1404_3448_b200.suffix_index import DeviceText, dc3_device, lcp_device
 
 what = sys.argv[1] if len(sys.argv) > 1 else "c2"
-if what == "c4":
+if what == "c5":
+    import bench
+    wl = bench.C5(0)
+    wl.step_device(); wl.step_device()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start(); wl.step_device(); torch.cuda.synchronize(); torch.cuda.profiler.stop()
+elif what == "c4":
     from paper_1404_3448_b200.workloads import c4_pairs
     seqs, offs = c4_pairs(0, 6700)      # one wave of <= 2^27 residues
     ob = sx.OverlapBatch(seqs, offs)
