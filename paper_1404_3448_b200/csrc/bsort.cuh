@@ -359,9 +359,7 @@ int bucket_sort(Src src, i64 n, u64 span, u64 *keys, u32 *vals, u32 *scratch, bo
         k_bs_scatter_emit<Src><<<(unsigned)ceil_div(n, 256 * BSE_ITEMS), 256, smem, st>>>(src, n, g.shift, cursor, pp,
                                                                                           s1);
         SAIX_LAUNCHED();
-        size_t smem2 = (size_t)PS_REFINE_TILE * 16 + 8 * ((size_t)1 << (pp.a.shift - pp.s2));
-        k_ps_refine<uint4><<<(unsigned)ceil_div(pp.stage1_items(), PS_REFINE_TILE), PS_THREADS, smem2, st>>>(s1, pp, s2);
-        SAIX_LAUNCHED();
+        SAIX_TRY(ps_refine_launch(s1, pp, s2, st));
         k_bs_window<<<(unsigned)pp.windows, PS_THREADS, (size_t)16 << pp.s2, st>>>(s2, pp, keys, vals);
         SAIX_LAUNCHED();
         ar->reset(mark);

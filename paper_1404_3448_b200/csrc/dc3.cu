@@ -38,6 +38,35 @@ struct Text {
 };
 
 // ------------------------------------------------------------ naming
+// A tile of a byte text staged in shared memory with aligned 4-byte loads
+// (coalesced; the per-character loads of the triple kernels hit shared
+// memory instead of issuing one global byte load each).  Covers absolute
+// positions [b0, b0 + len); positions >= n read as the virtual zero padding.
+struct SmemText {
+    const u8 *sh;  // sh[p - a0]
+    i64 a0;
+    __device__ __forceinline__ u32 operator()(i64 p) const { return sh[p - a0]; }
+};
+__device__ __forceinline__ SmemText stage_text(const u8 *__restrict__ T, i64 n, i64 b0, int len, u32 *sh_words,
+                                               int nthreads) {
+    i64 a0 = b0 & ~(i64)3;
+    int nw = (int)((b0 - a0 + len + 3) >> 2);
+    const u32 *W = reinterpret_cast<const u32 *>(T);
+    for (int w = threadIdx.x; w < nw; w += nthreads) {
+        i64 q = a0 + 4 * (i64)w;
+        u32 x = 0;
+        if (q + 4 <= n) x = __ldg(W + (q >> 2));
+        else
+            for (int c = 0; c < 4; c++)
+                if (q + c < n) x |= (u32)T[q + c] << (8 * c);
+        sh_words[w] = x;
+    }
+    __syncthreads();
+    return SmemText{reinterpret_cast<const u8 *>(sh_words), a0};
+}
+constexpr int TT_TILE = 2048;  // triplets per CTA in the staged byte-text kernels
+constexpr int TT_WORDS = (3 * TT_TILE + 8) / 4 + 2;
+
 
 template <typename TT>
 __global__ void k_bitmap_set(Text<TT> T, SampleLayout L, u64 s1, u32 *__restrict__ bm,
@@ -58,6 +87,63 @@ __global__ void k_bitmap_set(Text<TT> T, SampleLayout L, u64 s1, u32 *__restrict
         __syncthreads();
         for (u32 w = threadIdx.x; w < nwords; w += blockDim.x)
             if (shb[w]) atomicOr(&bm[w], shb[w]);
+    }
+}
+
+// Byte-text versions: one CTA per TT_TILE triplets j, samples 3j+1 (mod-1,
+// s = j) and 3j+2 (mod-2, s = m1 + j) read from the staged tile.
+__global__ void __launch_bounds__(256)
+k_bitmap_set_u8(const u8 *__restrict__ T, SampleLayout L, u64 s1, u32 *__restrict__ bm, u32 nwords, int use_smem) {
+    extern __shared__ u32 shb[];
+    __shared__ u32 shw[TT_WORDS];
+    if (use_smem) {
+        for (u32 w = threadIdx.x; w < nwords; w += blockDim.x) shb[w] = 0;
+    }
+    const i64 j0 = (i64)blockIdx.x * TT_TILE;
+    SmemText t = stage_text(T, L.n, 3 * j0, 3 * TT_TILE + 4, shw, 256);
+    u32 *dst = use_smem ? shb : bm;
+    for (int x = threadIdx.x; x < TT_TILE; x += 256) {
+        i64 j = j0 + x;
+        if (j >= L.m1) break;
+        i64 p = 3 * j;
+        u32 c1 = t(p + 1), c2 = t(p + 2), c3 = t(p + 3), c4 = t(p + 4);
+        u64 code = ((u64)c1 * s1 + c2) * s1 + c3;
+        u32 w = (u32)(code >> 5), bit = 1u << (code & 31);
+        if (!(dst[w] & bit)) atomicOr(&dst[w], bit);
+        if (j < L.m2) {
+            code = ((u64)c2 * s1 + c3) * s1 + c4;
+            w = (u32)(code >> 5);
+            bit = 1u << (code & 31);
+            if (!(dst[w] & bit)) atomicOr(&dst[w], bit);
+        }
+    }
+    if (use_smem) {
+        __syncthreads();
+        for (u32 w = threadIdx.x; w < nwords; w += blockDim.x)
+            if (shb[w]) atomicOr(&bm[w], shb[w]);
+    }
+}
+
+template <typename OT>
+__global__ void __launch_bounds__(256)
+k_bitmap_name_u8(const u8 *__restrict__ T, SampleLayout L, u64 s1, const u32 *__restrict__ bm,
+                 const u32 *__restrict__ wp, OT *__restrict__ tt) {
+    __shared__ u32 shw[TT_WORDS];
+    const i64 j0 = (i64)blockIdx.x * TT_TILE;
+    SmemText t = stage_text(T, L.n, 3 * j0, 3 * TT_TILE + 4, shw, 256);
+    for (int x = threadIdx.x; x < TT_TILE; x += 256) {
+        i64 j = j0 + x;
+        if (j >= L.m1) break;
+        i64 p = 3 * j;
+        u32 c1 = t(p + 1), c2 = t(p + 2), c3 = t(p + 3), c4 = t(p + 4);
+        u64 code = ((u64)c1 * s1 + c2) * s1 + c3;
+        u32 w = (u32)(code >> 5);
+        tt[j] = (OT)(wp[w] + __popc(bm[w] & ((1u << (code & 31)) - 1u)) + 1u);
+        if (j < L.m2) {
+            code = ((u64)c2 * s1 + c3) * s1 + c4;
+            w = (u32)(code >> 5);
+            tt[L.m1 + j] = (OT)(wp[w] + __popc(bm[w] & ((1u << (code & 31)) - 1u)) + 1u);
+        }
     }
 }
 
@@ -663,7 +749,9 @@ k_srec_emit(Text<u8> T, SampleLayout L, const u32 *__restrict__ isac, PsPlan pla
     uint4 *sh_items = reinterpret_cast<uint4 *>(smem);
     u32 *sh_cnt = reinterpret_cast<u32 *>(sh_items + 2 * SR_TILE);
     u32 *sh_base = sh_cnt + plan.a.buckets;
+    __shared__ u32 shw[(3 * SR_TILE + 8) / 4 + 2];
     const i64 j0 = (i64)blockIdx.x * SR_TILE;
+    SmemText t = stage_text(T.t, T.n, 3 * j0, 3 * SR_TILE + 4, shw, SR_THREADS);
     uint4 it[2 * SR_J];
     bool ok[2 * SR_J];
 #pragma unroll
@@ -673,7 +761,7 @@ k_srec_emit(Text<u8> T, SampleLayout L, const u32 *__restrict__ isac, PsPlan pla
         ok[2 * r + 1] = j < L.m2;
         if (ok[2 * r]) {
             i64 p = 3 * j;
-            u32 cp = T(p), c0 = T(p + 1), c1 = T(p + 2), c2 = T(p + 3);
+            u32 cp = t(p), c0 = t(p + 1), c1 = t(p + 2), c2 = t(p + 3);
             u32 r1 = isac[j];
             u32 r2 = j < L.m2 ? isac[L.m1 + j] : 0xFFFFFFFFu;
             u32 r4 = j + 1 < L.m1 ? isac[j + 1] + 1u : 0u;
@@ -1496,7 +1584,13 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         int gs = (use_smem && nwords > 1024) ? (g < 2 * kNumSMs ? g : 2 * kNumSMs) : g;
         {
             Prof prof_("dc3.bitmap_set", (double)sizeof(TT) * L.n, st);
-            k_bitmap_set<TT><<<gs, K_THREADS, use_smem ? nwords * 4 : 0, st>>>(T, L, s1, bm, nwords, use_smem);
+            if (sizeof(TT) == 1 && ((uintptr_t)T.t & 3) == 0) {
+                unsigned gt = (unsigned)ceil_div(L.m1 > 0 ? L.m1 : 1, TT_TILE);
+                k_bitmap_set_u8<<<gt, 256, use_smem ? nwords * 4 : 0, st>>>((const u8 *)T.t, L, s1, bm, nwords,
+                                                                          use_smem);
+            } else {
+                k_bitmap_set<TT><<<gs, K_THREADS, use_smem ? nwords * 4 : 0, st>>>(T, L, s1, bm, nwords, use_smem);
+            }
         }
         SAIX_LAUNCHED();
         SAIX_TRY(scan_transform(PopcIn{bm}, StoreExcl{wp}, nwords, tmp, d_scal, st, "dc3.bitmap_scan", 8.0 * nwords));
@@ -1504,8 +1598,15 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         narrow = !keep_u32 && D <= 255 && (i64)D < m;
         {
             Prof prof_("dc3.bitmap_name", (double)sizeof(TT) * L.n + (narrow ? 1.0 : 4.0) * m, st);
-            if (narrow) k_bitmap_name<TT, u8><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, (u8 *)tt);
-            else k_bitmap_name<TT, u32><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, tt);
+            if (sizeof(TT) == 1 && ((uintptr_t)T.t & 3) == 0) {
+                unsigned gt = (unsigned)ceil_div(L.m1 > 0 ? L.m1 : 1, TT_TILE);
+                if (narrow) k_bitmap_name_u8<u8><<<gt, 256, 0, st>>>((const u8 *)T.t, L, s1, bm, wp, (u8 *)tt);
+                else k_bitmap_name_u8<u32><<<gt, 256, 0, st>>>((const u8 *)T.t, L, s1, bm, wp, tt);
+            } else if (narrow) {
+                k_bitmap_name<TT, u8><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, (u8 *)tt);
+            } else {
+                k_bitmap_name<TT, u32><<<g, K_THREADS, 0, st>>>(T, L, s1, bm, wp, tt);
+            }
         }
         SAIX_LAUNCHED();
     } else {
@@ -1665,7 +1766,8 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
         return SAIX_OK;
     }
     if constexpr (sizeof(TT) == 1) {
-        if (stream_level_ok(1, sigma, N, probe)) return dc3_level_stream(c, text, N, sigma, SA, ISA, Phi, phi_done, depth);
+        if (stream_level_ok(1, sigma, N, probe) && ((uintptr_t)text & 3) == 0)
+            return dc3_level_stream(c, text, N, sigma, SA, ISA, Phi, phi_done, depth);
     }
     SampleLayout L = SampleLayout::of(N);
     size_t mark0 = ar.mark();
@@ -1854,10 +1956,7 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
             SAIX_CUDA(cudaFuncSetAttribute(k_rs_window, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 << RW_SHIFT));
             attr = true;
         }
-        size_t smem = (size_t)PS_REFINE_TILE * 16 + 8 * ((size_t)1 << (pr.a.shift - pr.s2));
-        k_ps_refine<uint4><<<(unsigned)ceil_div(pr.stage1_items(), PS_REFINE_TILE), PS_THREADS, smem, st>>>(
-            stage1, pr, stage2);
-        SAIX_LAUNCHED();
+        SAIX_TRY(ps_refine_launch(stage1, pr, stage2, st));
         k_rs_window<<<(unsigned)pr.windows, PS_THREADS, 16 << RW_SHIFT, st>>>(stage2, pr, RS, hist, D1);
         SAIX_LAUNCHED();
     }
