@@ -30,8 +30,9 @@ namespace saix {
 
 constexpr int PS_MAX_BUCKETS = 4096;
 constexpr int PS_THREADS = 256;
-constexpr int PS_REFINE_ITEMS = 16;                            // pass A2 tile: 4096 items
-constexpr int PS_REFINE_TILE = PS_THREADS * PS_REFINE_ITEMS;
+constexpr int PS_REFINE_THREADS = 512;
+constexpr int PS_REFINE_ITEMS = 8;                             // pass A2 tile: 4096 items
+constexpr int PS_REFINE_TILE = PS_REFINE_THREADS * PS_REFINE_ITEMS;
 constexpr i64 PS_WINDOW_BYTES = 64 << 10;                      // pass B window in shared memory
 
 // staging traffic streams past L2 (evict-first)
@@ -150,7 +151,7 @@ __device__ __forceinline__ void ps_block_emit(const P (&it)[ITEMS], const bool (
 
 // Pass A2: tile t covers stage1[t*TILE, (t+1)*TILE) inside one coarse region.
 template <class P>
-__global__ void __launch_bounds__(PS_THREADS)
+__global__ void __launch_bounds__(PS_REFINE_THREADS)
 k_ps_refine(const P *__restrict__ stage1, PsPlan plan, P *__restrict__ stage2) {
     extern __shared__ __align__(16) unsigned char ps_smem[];
     P *sh_items = reinterpret_cast<P *>(ps_smem);
@@ -171,12 +172,27 @@ k_ps_refine(const P *__restrict__ stage1, PsPlan plan, P *__restrict__ stage2) {
     bool ok[PS_REFINE_ITEMS];
 #pragma unroll
     for (int r = 0; r < PS_REFINE_ITEMS; r++) {
-        i64 x = off + r * PS_THREADS + threadIdx.x;
+        i64 x = off + r * PS_REFINE_THREADS + threadIdx.x;
         ok[r] = x < fill;
         if (ok[r]) it[r] = ld_stream(stage1 + (b << plan.a.shift) + x);
     }
-    ps_block_emit<P, PS_THREADS, PS_REFINE_ITEMS>(it, ok, lv, stage2 + ((i64)lv.base << plan.s2), sh_items, sh_cnt,
-                                                 sh_base);
+    ps_block_emit<P, PS_REFINE_THREADS, PS_REFINE_ITEMS>(it, ok, lv, stage2 + ((i64)lv.base << plan.s2), sh_items,
+                                                        sh_cnt, sh_base);
+}
+
+template <class P>
+int ps_refine_launch(const P *stage1, const PsPlan &plan, P *stage2, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        SAIX_CUDA(cudaFuncSetAttribute(k_ps_refine<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(PS_REFINE_TILE * sizeof(P) + 8 * 256)));
+        attr = true;
+    }
+    size_t smem = (size_t)PS_REFINE_TILE * sizeof(P) + 8 * ((size_t)1 << (plan.a.shift - plan.s2));
+    i64 tiles = ceil_div(plan.stage1_items(), PS_REFINE_TILE);
+    k_ps_refine<P><<<(unsigned)tiles, PS_REFINE_THREADS, smem, st>>>(stage1, plan, stage2);
+    SAIX_LAUNCHED();
+    return SAIX_OK;
 }
 
 // Pass B: one CTA per window.  Apply provides `using Out = ...;`, the
@@ -214,18 +230,7 @@ int ps_finish(const P *stage1, P *stage2, const PsPlan &plan, Apply ap, cudaStre
               double bytes) {
     using Out = typename Apply::Out;
     Prof prof_(prof, bytes, st);
-    {
-        static bool attr = false;
-        if (!attr) {
-            SAIX_CUDA(cudaFuncSetAttribute(k_ps_refine<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(PS_REFINE_TILE * sizeof(P) + 8 * 256)));
-            attr = true;
-        }
-        size_t smem = (size_t)PS_REFINE_TILE * sizeof(P) + 8 * ((size_t)1 << (plan.a.shift - plan.s2));
-        i64 tiles = ceil_div(plan.stage1_items(), PS_REFINE_TILE);
-        k_ps_refine<P><<<(unsigned)tiles, PS_THREADS, smem, st>>>(stage1, plan, stage2);
-        SAIX_LAUNCHED();
-    }
+    SAIX_TRY(ps_refine_launch(stage1, plan, stage2, st));
     {
         static bool attr = false;
         if (!attr) {
