@@ -146,6 +146,40 @@ __device__ __forceinline__ u32 digit_peers(u32 d) {
     return peers;
 }
 
+// u32 division by a runtime-constant divisor d >= 1 (Granlund-Montgomery,
+// exact for every 32-bit dividend): q = (t + ((x - t) >> 1)) >> (l - 1),
+// t = umulhi(m, x), l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1.
+struct U32Div {
+    u32 m = 0, d = 1;
+    int l = 0;
+    static U32Div of(u32 d) {
+        U32Div r;
+        r.d = d;
+        int l = 0;
+        while (((u64)1 << l) < d) l++;
+        r.l = l;
+        r.m = (u32)((((u64)1 << 32) * (((u64)1 << l) - d)) / d + 1);
+        return r;
+    }
+    __device__ __forceinline__ u32 div(u32 x) const {
+        if (l == 0) return x;
+        u32 t = __umulhi(m, x);
+        return (t + ((x - t) >> 1)) >> (l - 1);
+    }
+};
+
+// digit_peers for digits in [0, mask] (mask = 2^w - 1), 256 = no item:
+// w + 1 ballots instead of 9
+__device__ __forceinline__ u32 digit_peers_w(u32 d, u32 mask) {
+    u32 peers = __ballot_sync(0xffffffffu, d < 256u);
+    if (d >= 256u) peers = ~peers;
+    for (u32 b = 0; (1u << b) <= mask; b++) {
+        u32 m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? m : ~m;
+    }
+    return peers;
+}
+
 inline int bits_for(u64 v) {  // bit width of v (>= 1), like int.bit_length()
     int b = 1;
     while (b < 64 && (v >> b)) b++;

@@ -1552,6 +1552,196 @@ static int dc3_wide_finish(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sig
 static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA, u32 *ISA, u32 *Phi,
                             bool *phi_done, int depth);
 
+// ------------------------------------------------------------ tie resolution
+//
+// When a level's sample names are almost all distinct (m - names <= m/32;
+// e.g. the deep levels of DNA pairs with planted repeats), the recursion
+// would re-run a full DC3 level only to order the few samples that share a
+// name.  Those ties are resolved instead by prefix doubling on the recursion
+// string R = tt (whose suffix order is exactly what the recursion returns,
+// suffix_index.py:256-271): G[s] = head of s's group in the sorted order;
+// each round sorts every tied group by G[s + h] (0 past the end) and splits
+// it, h doubling, until all groups are singletons -- then G = ISAc and the
+// sorted order = SAc.  Work is proportional to the tied samples only.
+struct EqPacked {
+    const u64 *keys;
+    __device__ __forceinline__ bool operator()(i64 a, i64 b) const { return keys[a] == keys[b]; }
+};
+template <typename TT>
+struct EqWide {  // (c0, c1) dense key + third character
+    Text<TT> T;
+    SampleLayout L;
+    const u64 *keys;
+    const u32 *vals;
+    __device__ __forceinline__ bool operator()(i64 a, i64 b) const {
+        return keys[a] == keys[b] && T(L.pos(vals[a]) + 2) == T(L.pos(vals[b]) + 2);
+    }
+};
+constexpr i64 TIE_MAX_RUN = 4096;
+
+template <class Eq>
+__global__ void k_tie_init(Eq eq, i64 m, u32 *__restrict__ head, u32 *__restrict__ rs, u32 *__restrict__ rl,
+                           u32 *__restrict__ nruns, u32 cap, u32 *__restrict__ overflow) {
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (i64)gridDim.x * blockDim.x) {
+        i64 h = r;
+        while (h > 0 && r - h <= TIE_MAX_RUN && eq(h - 1, h)) h--;
+        if (r - h > TIE_MAX_RUN) {
+            atomicMax(overflow, 1u);
+            h = r;
+        }
+        head[r] = (u32)h;
+        if (h == r && r + 1 < m && eq(r, r + 1)) {  // head of a tied group
+            i64 e = r + 2;
+            while (e < m && e - r <= TIE_MAX_RUN && eq(r, e)) e++;
+            u32 at = atomicAdd(nruns, 1u);
+            if (at < cap) {
+                rs[at] = (u32)r;
+                rl[at] = (u32)(e - r);
+            } else {
+                atomicMax(overflow, 1u);
+            }
+        }
+    }
+}
+
+// one thread per run: doubling key of every member (G read only)
+__global__ void k_tie_keys(const u32 *__restrict__ rs, const u32 *__restrict__ rl, const u32 *__restrict__ nruns,
+                           const u32 *__restrict__ S, const u32 *__restrict__ G, i64 m, i64 h, u64 *__restrict__ kk) {
+    const u32 nr = *nruns;
+    for (u32 q = (u32)((i64)blockIdx.x * blockDim.x + threadIdx.x); q < nr; q += gridDim.x * blockDim.x) {
+        u32 s0 = rs[q], len = rl[q];
+        for (u32 x = s0; x < s0 + len; x++) {
+            i64 sidx = (i64)S[x] + h;
+            kk[x] = sidx < m ? (u64)G[sidx] + 1u : 0ull;
+        }
+    }
+}
+
+// runs of 33..4096 members for the shared-memory sorts
+__global__ void k_tie_lists(const u32 *__restrict__ rl, const u32 *__restrict__ nruns, u32 *__restrict__ mid,
+                            u32 *__restrict__ big, u32 *__restrict__ scal) {
+    const u32 nr = *nruns;
+    for (u32 q = (u32)((i64)blockIdx.x * blockDim.x + threadIdx.x); q < nr; q += gridDim.x * blockDim.x) {
+        u32 len = rl[q];
+        if (len > BS_SMALL) big[atomicAdd(&scal[1], 1u)] = q;
+        else if (len > BS_TINY) mid[atomicAdd(&scal[0], 1u)] = q;
+    }
+}
+
+// split every sorted run where the key changes: members get their sub-run's
+// head as group id; sub-runs of > 1 member go to the next round's list
+__global__ void k_tie_split(const u32 *__restrict__ rs, const u32 *__restrict__ rl, const u32 *__restrict__ nruns,
+                            const u32 *__restrict__ S, const u64 *__restrict__ kk, u32 *__restrict__ G,
+                            u32 *__restrict__ rs2, u32 *__restrict__ rl2, u32 *__restrict__ nruns2) {
+    const u32 nr = *nruns;
+    for (u32 q = (u32)((i64)blockIdx.x * blockDim.x + threadIdx.x); q < nr; q += gridDim.x * blockDim.x) {
+        u32 s0 = rs[q], e = s0 + rl[q];
+        u32 sub = s0;
+        for (u32 x = s0; x < e; x++) {
+            if (x > s0 && kk[x] != kk[x - 1]) {
+                if (x - sub > 1) {
+                    u32 at = atomicAdd(nruns2, 1u);
+                    rs2[at] = sub;
+                    rl2[at] = x - sub;
+                }
+                sub = x;
+            }
+            G[S[x]] = sub;
+        }
+        if (e - sub > 1) {
+            u32 at = atomicAdd(nruns2, 1u);
+            rs2[at] = sub;
+            rl2[at] = e - sub;
+        }
+    }
+}
+
+// Resolve the tied groups of the sorted samples (keys/S from the naming sort)
+// into ISAc (and SAc when asked).  ok = false: too many / too long ties, the
+// caller recurses instead (nothing has been written to ISAc / SAc then).
+template <class Eq>
+static int resolve_ties(Dc3Ctx &c, Eq eq, i64 m, i64 ties, u32 *S, u64 *kk, u32 *SAc, u32 *ISAc, bool &ok) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    ok = false;
+    size_t mark = ar.mark();
+    u32 cap = (u32)(ties + 64);
+    u32 *head = ar.alloc<u32>(m);
+    u32 *rsA = ar.alloc<u32>(cap), *rlA = ar.alloc<u32>(cap), *rsB = ar.alloc<u32>(cap), *rlB = ar.alloc<u32>(cap);
+    u32 *mid = ar.alloc<u32>(cap), *big = ar.alloc<u32>(cap);
+    u32 *scal = ar.alloc<u32>(16);  // [0] mid, [1] big, [2] runs A, [3] runs B, [4] overflow
+    SAIX_ARENA_OK(ar);
+    Prof prof_("dc3.tie_resolve", 8.0 * m + 24.0 * ties, st);
+    SAIX_CUDA(cudaMemsetAsync(scal, 0, 16 * 4, st));
+    k_tie_init<Eq><<<grid_for(m, 256), 256, 0, st>>>(eq, m, head, rsA, rlA, scal + 2, cap, scal + 4);
+    SAIX_LAUNCHED();
+    u32 h2[3];
+    SAIX_CUDA(cudaMemcpyAsync(h2, scal + 2, 12, cudaMemcpyDeviceToHost, st));
+    SAIX_CUDA(cudaStreamSynchronize(st));
+    if (h2[2]) {
+        ar.reset(mark);
+        return SAIX_OK;
+    }
+    // G[S[r]] = head(r): the (mostly unique) group ids through the bucketed scatter
+    SAIX_TRY(scatter_u32(ar, S, head, m, m, ISAc, st, "dc3.tie_scatter"));
+    u32 nr = h2[0];
+    u32 *rs = rsA, *rl = rlA, *rs2 = rsB, *rl2 = rlB;
+    u32 *cnt_cur = scal + 2, *cnt_next = scal + 3;
+    for (i64 h = 1; nr > 0; h <<= 1) {
+        if (h > 2 * m) {
+            set_error("dc3: tie resolution did not converge");
+            return SAIX_EINVAL;
+        }
+        int g = grid_for(nr, 128);
+        k_tie_keys<<<g, 128, 0, st>>>(rs, rl, cnt_cur, S, ISAc, m, h, kk);
+        SAIX_LAUNCHED();
+        // sort every run by its key (runs are buckets for the bucket-sort kernels)
+        k_bs_tiny<<<grid_for(ceil_div(nr, 32) * 32, 256, kNumSMs * 16), 256, 0, st>>>(rs, rl, nr, kk, S);
+        SAIX_LAUNCHED();
+        SAIX_CUDA(cudaMemsetAsync(scal, 0, 8, st));
+        k_tie_lists<<<g, 128, 0, st>>>(rl, cnt_cur, mid, big, scal);
+        SAIX_LAUNCHED();
+        u32 hl[2];
+        SAIX_CUDA(cudaMemcpyAsync(hl, scal, 8, cudaMemcpyDeviceToHost, st));
+        SAIX_CUDA(cudaStreamSynchronize(st));
+        if (hl[0]) {
+            static bool attr = false;
+            if (!attr) {
+                SAIX_CUDA(cudaFuncSetAttribute(k_bs_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)BS_SMALL_SMEM));
+                attr = true;
+            }
+            u32 blocks = (hl[0] + BS_WARPS - 1) / BS_WARPS;
+            k_bs_small<<<blocks < 2 * kNumSMs ? blocks : 2 * kNumSMs, 32 * BS_WARPS, BS_SMALL_SMEM, st>>>(
+                rs, rl, mid, scal, kk, S);
+            SAIX_LAUNCHED();
+        }
+        if (hl[1]) {
+            static bool attr = false;
+            size_t smem = (size_t)BS_LARGE * 12;
+            if (!attr) {
+                SAIX_CUDA(cudaFuncSetAttribute(k_bs_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                attr = true;
+            }
+            k_bs_large<<<hl[1] < 4 * kNumSMs ? hl[1] : 4 * kNumSMs, 256, smem, st>>>(rs, rl, big, scal + 1, kk, S);
+            SAIX_LAUNCHED();
+        }
+        SAIX_CUDA(cudaMemsetAsync(cnt_next, 0, 4, st));
+        k_tie_split<<<g, 128, 0, st>>>(rs, rl, cnt_cur, S, kk, ISAc, rs2, rl2, cnt_next);
+        SAIX_LAUNCHED();
+        SAIX_CUDA(cudaMemcpyAsync(&nr, cnt_next, 4, cudaMemcpyDeviceToHost, st));
+        SAIX_CUDA(cudaStreamSynchronize(st));
+        u32 *t;
+        t = rs; rs = rs2; rs2 = t;
+        t = rl; rl = rl2; rl2 = t;
+        t = cnt_cur; cnt_cur = cnt_next; cnt_next = t;
+    }
+    if (SAc) SAIX_CUDA(cudaMemcpyAsync(SAc, S, (size_t)m * 4, cudaMemcpyDeviceToDevice, st));
+    ar.reset(mark);
+    ok = true;
+    return SAIX_OK;
+}
+
 // Steps 1-2: names of the sample triples, then SAc/ISAc (recursing if needed).
 template <typename TT>
 static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma, u32 *tt,
@@ -1567,6 +1757,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
     u64 *sorted_keys = nullptr;
     bool bsorted = false;  // keys are shift-packed triples (bucket sort)
     int kbits = 0;
+    bool wide_names = false;                        // keys hold (c0, c1) only; c2 from the text
+    u64 *k0_keep = nullptr, *k1_keep = nullptr;     // the sort's key buffers (tie resolution scratch)
     bool keep_arena = false;  // RA built: the caller releases the sort temps
     if (RA_out) *RA_out = nullptr;
     if (use_bitmap(sigma, m)) {
@@ -1619,6 +1811,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         SAIX_ARENA_OK(ar);
         u64 *keys = k0;
         u32 *vals = v0;
+        k0_keep = k0;
+        k1_keep = k1;
         if (3 * b <= 64) {
             u64 s1 = sigma + 1;
             int kb = bits_for(s1 * s1 * s1 - 1);
@@ -1654,6 +1848,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             }
         } else {
             // wide alphabet: bucket sort by (c0, c1), repeats ordered by c2
+            wide_names = true;
             u64 s1 = sigma + 1;
             bool done = false;
             if (sigma < ((u64)1 << 32) && m >= 4096) {
@@ -1744,9 +1939,22 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         }
         if (!keep_arena) ar.reset(mark);
     } else {
+        bool resolved = false;
+        if (sorted_vals && !keep_u32 && m >= 4096 && (i64)(m - D) <= m / 32) {
+            // almost all names distinct: order the tied samples by prefix
+            // doubling instead of a full recursion level
+            u64 *kk = sorted_keys == k0_keep ? k1_keep : k0_keep;
+            if (wide_names)
+                SAIX_TRY(resolve_ties(c, EqWide<TT>{T, L, sorted_keys, sorted_vals}, m, m - D, sorted_vals, kk, SAc,
+                                      ISAc, resolved));
+            else
+                SAIX_TRY(resolve_ties(c, EqPacked{sorted_keys}, m, m - D, sorted_vals, kk, SAc, ISAc, resolved));
+        }
         ar.reset(mark);
-        if (narrow) SAIX_TRY(dc3_level<u8>(c, (const u8 *)tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
-        else SAIX_TRY(dc3_level<u32>(c, tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
+        if (!resolved) {
+            if (narrow) SAIX_TRY(dc3_level<u8>(c, (const u8 *)tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
+            else SAIX_TRY(dc3_level<u32>(c, tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
+        }
     }
     return SAIX_OK;
 }
@@ -2026,7 +2234,9 @@ static size_t dc3_plan(i64 n, int text_bytes = 4) {
         size_t ps_u = (size_t)(pu.stage1_items() + pu.stage2_items()) * 8 + (size_t)pu.cursor_words() * 4;
         size_t ps_max = bs_ps_bytes(m) > scatter_u32_bytes(m) ? bs_ps_bytes(m) : scatter_u32_bytes(m);
         ps_max = ps_max > ps_u ? ps_max : ps_u;
-        size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4 + 4 * Arena::kAlign + ps_max;
+        // (+ tie resolution: group heads and run lists next to the sort buffers)
+        size_t sort_t = (size_t)m * 24 + (size_t)(sw + scan_tmp_words(m)) * 4 + 4 * Arena::kAlign + ps_max +
+                        (size_t)m * 4 + (size_t)(m / 32 + 64) * 24 + 8 * Arena::kAlign;
         i64 words = (2 * m > (1 << 16) ? 2 * m : (1 << 16)) + 1;
         size_t bm_t = (size_t)(2 * words + scan_tmp_words(words)) * 4;
         i64 bw = mod0_bitmap_words(7, m);

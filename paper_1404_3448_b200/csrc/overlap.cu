@@ -449,13 +449,7 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
 namespace saix {
 
 __device__ __forceinline__ u32 pair_of(const i64 *__restrict__ xoff, i64 P, i64 stride, i64 g) {
-    if (stride > 0) {
-        // g < 2^30, stride < 2^30: double quotient, corrected to the exact floor
-        u32 q = (u32)((double)g * (1.0 / (double)stride));
-        if ((i64)(q + 1) * stride <= g) q++;
-        else if ((i64)q * stride > g) q--;
-        return q;
-    }
+    if (stride > 0) return (u32)g / (u32)stride;  // waves hold < 2^30 residues: 32-bit division
     i64 lo = 0, hi = P - 1;  // largest p with xoff[p] <= g
     while (lo < hi) {
         i64 mid = (lo + hi + 1) >> 1;
@@ -497,7 +491,10 @@ __global__ void k_batch_build_x(const u8 *__restrict__ seqs, const i64 *__restri
 struct PairKey {
     const i64 *xoff;
     i64 P, stride;
-    __device__ __forceinline__ u32 operator()(u32 v) const { return pair_of(xoff, P, stride, v); }
+    U32Div dv;  // fixed-length pairs: v / stride by multiply-high
+    __device__ __forceinline__ u32 operator()(u32 v) const {
+        return stride > 0 ? dv.div(v) : pair_of(xoff, P, stride, v);
+    }
 };
 
 struct PairSrc {
@@ -583,6 +580,7 @@ __global__ void k_batch_lcp_extend(Txt tx, const u32 *__restrict__ sap, PairClam
     }
 }
 
+constexpr int BO_ITEMS = 16;
 __global__ void __launch_bounds__(OV_THREADS)
 k_batch_overlap(const u32 *__restrict__ sap, const u32 *__restrict__ plcp, const i64 *__restrict__ xoff,
                 const i64 *__restrict__ offs, i64 P, i64 *__restrict__ out, int by_rank) {
@@ -613,27 +611,40 @@ k_batch_overlap(const u32 *__restrict__ sap, const u32 *__restrict__ plcp, const
             if (threadIdx.x == 0) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0;
             continue;
         }
-        // pass 2: runs of lcp >= best, per-run min A / B position (138-152)
+        // pass 2: runs of lcp >= best, per-run min A / B position (138-152):
+        // each thread folds BO_ITEMS consecutive elements, one block scan of
+        // the per-thread aggregates per chunk, then the same elements again
+        // with the carry-in to close runs
         Seg carry{0u, kInf, kInf};
         unsigned long long win = ~0ull;
-        for (i64 c = s0; c < x1; c += OV_THREADS) {
-            i64 r = c + threadIdx.x;
-            bool live = r < x1;
-            Seg e{0u, kInf, kInf};
-            bool end = false;
-            if (live) {
-                u32 g = sap[r], loc = g - (u32)x0;
-                u32 l = r == s0 ? 0u : plcp[by_rank ? (u32)r : g];
-                e.f = (r == s0 || l < best) ? 1u : 0u;
-                e.a = loc < la ? loc : kInf;
-                e.b = loc > la ? loc : kInf;
-                end = (r + 1 >= x1) || plcp[by_rank ? (u32)(r + 1) : sap[r + 1]] < best;
+        for (i64 c = s0; c < x1; c += (i64)OV_THREADS * BO_ITEMS) {
+            const i64 r0 = c + (i64)threadIdx.x * BO_ITEMS;
+            u32 lv[BO_ITEMS + 1], gv[BO_ITEMS];
+#pragma unroll
+            for (int q = 0; q <= BO_ITEMS; q++) {
+                i64 r = r0 + q;
+                lv[q] = r < x1 ? (r == s0 ? 0u : plcp[by_rank ? (u32)r : sap[r]]) : 0u;
+                if (q < BO_ITEMS) gv[q] = r < x1 ? sap[r] - (u32)x0 : 0u;
+            }
+            Seg agg{0u, kInf, kInf};
+#pragma unroll
+            for (int q = 0; q < BO_ITEMS; q++) {
+                i64 r = r0 + q;
+                if (r >= x1) break;
+                Seg e{(r == s0 || lv[q] < best) ? 1u : 0u, gv[q] < la ? gv[q] : kInf, gv[q] > la ? gv[q] : kInf};
+                agg = seg_combine(agg, e);
             }
             Seg tot;
-            Seg ex = block_seg_exclusive(e, tot);
-            Seg run = seg_combine(seg_combine(carry, ex), e);
-            if (live && end && run.a != kInf && run.b != kInf)
-                win = min(win, ((unsigned long long)run.a << 32) | run.b);
+            Seg run = seg_combine(carry, block_seg_exclusive(agg, tot));
+#pragma unroll
+            for (int q = 0; q < BO_ITEMS; q++) {
+                i64 r = r0 + q;
+                if (r >= x1) break;
+                Seg e{(r == s0 || lv[q] < best) ? 1u : 0u, gv[q] < la ? gv[q] : kInf, gv[q] > la ? gv[q] : kInf};
+                run = seg_combine(run, e);
+                bool end = (r + 1 >= x1) || lv[q + 1] < best;
+                if (end && run.a != kInf && run.b != kInf) win = min(win, ((unsigned long long)run.a << 32) | run.b);
+            }
             carry = seg_combine(carry, tot);
         }
         for (int o = 16; o; o >>= 1) win = min(win, __shfl_xor_sync(0xffffffffu, win, o));
@@ -646,6 +657,97 @@ k_batch_overlap(const u32 *__restrict__ sap, const u32 *__restrict__ plcp, const
             out[3 * p + 2] = (i64)(win & 0xFFFFFFFFull) - (i64)la - 1;
         }
         __syncthreads();
+    }
+}
+
+// One warp per pair: pass 1 (best cross-sequence adjacent LCP) and pass 2
+// (runs of lcp >= best, per-run min A / B, overlap.py:129-152) as lane-strided
+// streams over the pair block; pass 2 folds 16 consecutive elements per lane
+// and closes runs with a warp segmented scan per 512-element chunk.  Many
+// pairs in flight per SM hide the latency the CTA-per-pair form exposed.
+constexpr int BW_ITEMS = 16;
+__global__ void __launch_bounds__(256)
+k_batch_overlap_warp(const u32 *__restrict__ sap, const u32 *__restrict__ lcp, const i64 *__restrict__ xoff,
+                     const i64 *__restrict__ offs, i64 P, i64 *__restrict__ out) {
+    const int lane = lane_id();
+    const i64 warps = ((i64)gridDim.x * blockDim.x) >> 5;
+    for (i64 p = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P; p += warps) {
+        const i64 x0 = xoff[p], x1 = xoff[p + 1];
+        if (x1 == x0) {
+            if (lane == 0) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0;
+            continue;
+        }
+        const u32 la = (u32)(offs[2 * p + 1] - offs[2 * p]);
+        const i64 s0 = x0 + 1;  // first real suffix (the terminator sorts first)
+        u32 mx = 0;
+        for (i64 c = s0; c < x1; c += 32 * BW_ITEMS) {  // 16 consecutive pairs per lane, loads in flight together
+            const i64 r0 = c + (i64)lane * BW_ITEMS;
+            u32 gv[BW_ITEMS + 1], lv[BW_ITEMS];
+#pragma unroll
+            for (int q = 0; q <= BW_ITEMS; q++) {
+                i64 r = r0 + q - 1;
+                gv[q] = (r >= s0 && r < x1) ? __ldg(sap + r) - (u32)x0 : la;
+                if (q < BW_ITEMS) lv[q] = r + 1 < x1 ? __ldg(lcp + r + 1) : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < BW_ITEMS; q++) {
+                u32 ga = gv[q], gb = gv[q + 1];  // suffixes r0+q-1, r0+q
+                bool cross = ga != la && gb != la && ((ga < la) != (gb < la));
+                if (cross && lv[q] > mx) mx = lv[q];
+            }
+        }
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const u32 best = mx;
+        if (best == 0) {
+            if (lane == 0) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0;
+            continue;
+        }
+        Seg carry{0u, kInf, kInf};
+        unsigned long long win = ~0ull;
+        for (i64 c = s0; c < x1; c += 32 * BW_ITEMS) {
+            const i64 r0 = c + (i64)lane * BW_ITEMS;
+            u32 lv[BW_ITEMS + 1], gv[BW_ITEMS];
+#pragma unroll
+            for (int q = 0; q <= BW_ITEMS; q++) {
+                i64 r = r0 + q;
+                lv[q] = r < x1 ? (r == s0 ? 0u : __ldg(lcp + r)) : 0u;
+                if (q < BW_ITEMS) gv[q] = r < x1 ? __ldg(sap + r) - (u32)x0 : 0u;
+            }
+            Seg agg{0u, kInf, kInf};
+#pragma unroll
+            for (int q = 0; q < BW_ITEMS; q++) {
+                if (r0 + q >= x1) break;
+                Seg e{(r0 + q == s0 || lv[q] < best) ? 1u : 0u, gv[q] < la ? gv[q] : kInf, gv[q] > la ? gv[q] : kInf};
+                agg = seg_combine(agg, e);
+            }
+            // warp exclusive segmented scan of the lane aggregates
+            Seg inc = agg;
+            for (int o = 1; o < 32; o <<= 1) {
+                Seg y = seg_shfl_up(inc, o);
+                if (lane >= o) inc = seg_combine(y, inc);
+            }
+            Seg ex = seg_shfl_up(inc, 1);
+            if (lane == 0) ex = Seg{0u, kInf, kInf};
+            Seg run = seg_combine(carry, ex);
+#pragma unroll
+            for (int q = 0; q < BW_ITEMS; q++) {
+                i64 r = r0 + q;
+                if (r >= x1) break;
+                Seg e{(r == s0 || lv[q] < best) ? 1u : 0u, gv[q] < la ? gv[q] : kInf, gv[q] > la ? gv[q] : kInf};
+                run = seg_combine(run, e);
+                bool end = (r + 1 >= x1) || lv[q + 1] < best;
+                if (end && run.a != kInf && run.b != kInf) win = min(win, ((unsigned long long)run.a << 32) | run.b);
+            }
+            Seg tot{__shfl_sync(0xffffffffu, inc.f, 31), __shfl_sync(0xffffffffu, inc.a, 31),
+                    __shfl_sync(0xffffffffu, inc.b, 31)};
+            carry = seg_combine(carry, tot);
+        }
+        for (int o = 16; o; o >>= 1) win = min(win, __shfl_xor_sync(0xffffffffu, win, o));
+        if (lane == 0) {
+            out[3 * p] = best;
+            out[3 * p + 1] = (i64)(win >> 32);
+            out[3 * p + 2] = (i64)(win & 0xFFFFFFFFull) - (i64)la - 1;
+        }
     }
 }
 
@@ -760,8 +862,9 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
     SAIX_TRY(dc3_compute(w.X, 1, nx, sigma, w.sa, nullptr, w.dc3, w.dc3_bytes, nullptr, st));
     // stable partition by pair id: each pair's suffixes keep their order
     u32 *sap = nullptr;
-    int passes = (bits_for((u64)(P > 1 ? P - 1 : 1)) + 7) / 8;
-    SAIX_TRY(lsd_partition(PairKey{w.xoff, P, b.stride}, w.sa, w.v0, nx, passes, w.scratch, sap, st,
+    int pbits = P > 1 ? bits_for((u64)(P - 1)) : 0;
+    SAIX_TRY(lsd_partition(PairKey{w.xoff, P, b.stride, U32Div::of(b.stride > 0 ? (u32)b.stride : 1u)}, w.sa,
+                           w.v0, nx, pbits, w.scratch, sap, st,
                            "batch.partition"));
     // LCP inside each pair block: direct word compares (2-bit packed wave
     // text: residues 3..6; N residues -> byte compares), capped entries
@@ -809,8 +912,11 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
     }
     {
         Prof prof_("batch.overlap", 8.0 * nx, st);
-        k_batch_overlap<<<(unsigned)(P < 65535 ? P : 65535), OV_THREADS, 0, st>>>(sap, lcp, w.xoff, w.offs, P, out,
-                                                                                   by_rank);
+        if (by_rank)
+            k_batch_overlap_warp<<<grid_for(P * 32, 256), 256, 0, st>>>(sap, lcp, w.xoff, w.offs, P, out);
+        else
+            k_batch_overlap<<<(unsigned)(P < 65535 ? P : 65535), OV_THREADS, 0, st>>>(sap, lcp, w.xoff, w.offs, P,
+                                                                                       out, by_rank);
     }
     SAIX_LAUNCHED();
     return SAIX_OK;

@@ -371,3 +371,49 @@ class TestDeepLevels:
         ix = sx.build_sa_dc3(t)
         sa, rank = oracle.dc3(r, sigma)
         assert np.array_equal(ix.sa, sa) and np.array_equal(ix.rank, rank)
+
+
+class TestTieResolution:
+    """Levels whose names are almost all distinct resolve the few tied samples
+    by prefix doubling on the recursion string instead of recursing."""
+
+    @pytest.mark.parametrize("reps", [(300,), (257, 1200, 40), (2000, 2000)])
+    def test_sparse_repeats(self, reps):
+        rng = np.random.default_rng(sum(reps))
+        r = rng.integers(1, 5, size=1 << 20)
+        for k, L in enumerate(reps):                     # copies of earlier stretches
+            src, dst = 1000 + 7919 * k, 600_000 + 50_000 * k
+            r[dst:dst + L] = r[src:src + L]
+        t = RankedText(r, 4)
+        ix = sx.build_sa_dc3(t)
+        from paper_1404_3448_b200 import _lib
+        trace = _lib.dc3_trace()
+        assert trace[-1][3] < trace[-1][2], trace      # deepest level had ties: resolved, not recursed
+        sa, rank = oracle.dc3(r, 4)
+        assert np.array_equal(ix.sa, sa) and np.array_equal(ix.rank, rank)
+        assert np.array_equal(sx.build_lcp(t, ix).lcp, oracle.lcp(r, sa, rank))
+
+    def test_many_copies_of_one_block(self):
+        """One block repeated 40 times: long tied groups (the doubling still
+        converges; > 4096 copies would fall back to recursion)."""
+        rng = np.random.default_rng(3)
+        r = rng.integers(1, 5, size=1 << 19)
+        blk = r[:500].copy()
+        for k in range(40):
+            r[100_000 + 9000 * k: 100_000 + 9000 * k + 500] = blk
+        t = RankedText(r, 4)
+        ix = sx.build_sa_dc3(t)
+        sa, rank = oracle.dc3(r, 4)
+        assert np.array_equal(ix.sa, sa) and np.array_equal(ix.rank, rank)
+
+    def test_overlap_pairs_with_ties(self):
+        seqs, offs = c4_pairs_local(200, 4000)
+        want = oracle.overlap_batch(seqs, offs, threads=4)
+        ob = sx.OverlapBatch(seqs, offs)
+        ob.run_device()
+        assert np.array_equal(ob.results(), want)
+
+
+def c4_pairs_local(n, length):
+    from paper_1404_3448_b200.workloads import c4_pairs
+    return c4_pairs(0, n, length=length)
