@@ -848,6 +848,54 @@ k_rs_window(const uint4 *__restrict__ stage2, PsPlan plan, uint4 *__restrict__ r
     for (int d = threadIdx.x; d < D1; d += PS_THREADS) hist[(i64)d * plan.windows + w] = cnt[d];
 }
 
+// Small levels (text + ISAc <= ~48 MB, L2-resident for random reads): RS by
+// gathers in rank order from the child's SAc instead of the bucketed
+// scatter -- one CTA per 4096-rank window, also counting the window's mod-1
+// samples per cprev digit (as k_rs_window does).
+constexpr i64 RS_GATHER_BYTES = (i64)48 << 20;
+constexpr int RG_THREADS = 512, RG_ITEMS = 8;  // 4096 = 1 << RW_SHIFT
+__global__ void __launch_bounds__(RG_THREADS)
+k_rs_gather(const u32 *__restrict__ sac, Text<u8> T, SampleLayout L, const u32 *__restrict__ isac,
+            uint4 *__restrict__ rs, u32 *__restrict__ hist, int D1, u32 dmask, i64 windows) {
+    __shared__ u32 cnt[256];
+    for (int d = threadIdx.x; d < 256; d += RG_THREADS) cnt[d] = 0;
+    __syncthreads();
+    const i64 w = blockIdx.x;
+    const i64 r0 = w << RW_SHIFT;
+    u32 sv[RG_ITEMS];
+#pragma unroll
+    for (int q = 0; q < RG_ITEMS; q++) {
+        i64 r = r0 + q * RG_THREADS + threadIdx.x;
+        sv[q] = r < L.m ? __ldcs(sac + r) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < RG_ITEMS; q++) {
+        i64 r = r0 + q * RG_THREADS + threadIdx.x;
+        u32 d = 256u;
+        if (r < L.m) {
+            u32 sidx = sv[q];
+            uint4 e;
+            if (sidx < L.m1) {  // mod-1 sample 3s+1: {pos, R(pos+1), 0, c0 | c1 << 8 | cprev << 16}
+                i64 p = 3 * (i64)sidx + 1;
+                u32 nb = sidx < L.m2 ? isac[L.m1 + sidx] + 1u : 0u;
+                u32 cp = T(p - 1);
+                e = make_uint4((u32)p, nb, 0u, T(p) | (T(p + 1) << 8) | (cp << 16));
+                d = cp;
+            } else {  // mod-2 sample 3j+2: {pos, 0, R(pos+2), c0 | c1 << 8}
+                i64 j = sidx - L.m1;
+                i64 p = 3 * j + 2;
+                u32 nb = j + 1 < L.m1 ? isac[j + 1] + 1u : 0u;
+                e = make_uint4((u32)p, 0u, nb, T(p) | (T(p + 1) << 8));
+            }
+            __stcs(rs + r, e);
+        }
+        u32 peers = digit_peers_w(d, dmask);
+        if (d < 256u && (peers & lanemask_lt()) == 0) atomicAdd(&cnt[d], (u32)__popc(peers));
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < D1; d += RG_THREADS) hist[(i64)d * windows + w] = cnt[d];
+}
+
 // Mod-0 records of RS window w, stably partitioned by cprev: one tile of
 // 4096 ranks per CTA (512 threads x 8), warp-stable ranking (as in
 // k_os_pass) with the global per-(digit, window) offsets already known, so
@@ -2122,15 +2170,40 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     u32 *d_scal = ar.alloc<u32>(8);
     SAIX_ARENA_OK(ar);
     Text<u8> T{text, N};
-    SAIX_TRY(sort_samples<u8>(c, T, L, sigma, tt, nullptr, ISAc, d_scal, depth, false, nullptr));
+    // small level: the child also returns its order, and RS is gathered
+    const bool gather = N + 4 * m <= RS_GATHER_BYTES;
+    u32 *SAc = gather ? ar.alloc<u32>(m) : nullptr;
+    SAIX_ARENA_OK(ar);
+    SAIX_TRY(sort_samples<u8>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth, false, nullptr));
 
     // 1: sample records in rank order
     uint4 *RS = ar.alloc<uint4>(m);
     size_t mark1 = ar.mark();
     PsPlan pr = PsPlan::of(m, 16);
+    const int D1 = (int)sigma + 1;
+    if (pr.windows > 1 && pr.s2 != RW_SHIFT) {
+        set_error("dc3: record window %d != %d", pr.s2, RW_SHIFT);
+        return SAIX_EINVAL;
+    }
+    u32 *hist = nullptr, *hscan = nullptr;
+    uint4 *stage1 = nullptr;
+    size_t mark_s1 = 0;
+    if (gather) {
+        stage1 = ar.alloc<uint4>(k);  // M0
+        mark_s1 = ar.mark();
+        hist = ar.alloc<u32>((i64)D1 * pr.windows + 1);
+        hscan = ar.alloc<u32>(scan_tmp_words((i64)D1 * pr.windows));
+        SAIX_ARENA_OK(ar);
+        u32 dmask = 1;
+        while (dmask < (u32)D1 - 1) dmask = dmask * 2 + 1;
+        Prof prof_("dc3.srec_gather", 4.0 * m + 2.0 * 32 * m + 16.0 * m, st);
+        k_rs_gather<<<(unsigned)pr.windows, RG_THREADS, 0, st>>>(SAc, T, L, ISAc, RS, hist, D1, dmask, pr.windows);
+        SAIX_LAUNCHED();
+    } else {
+
     pr.set_cursors(ar.alloc<u32>(pr.cursor_words()));
-    uint4 *stage1 = ar.alloc<uint4>(pr.stage1_items() > k ? pr.stage1_items() : k);  // later: M0
-    size_t mark_s1 = ar.mark();
+    stage1 = ar.alloc<uint4>(pr.stage1_items() > k ? pr.stage1_items() : k);  // later: M0
+    mark_s1 = ar.mark();
     uint4 *stage2 = ar.alloc<uint4>(pr.stage2_items());
     SAIX_ARENA_OK(ar);
     SAIX_CUDA(cudaMemsetAsync(pr.a.cursor, 0, (size_t)pr.cursor_words() * 4, st));
@@ -2147,13 +2220,8 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     }
     SAIX_LAUNCHED();
     // A2 + the specialised pass B (RS windows + per-window cprev histogram)
-    if (pr.windows > 1 && pr.s2 != RW_SHIFT) {
-        set_error("dc3: record window %d != %d", pr.s2, RW_SHIFT);
-        return SAIX_EINVAL;
-    }
-    const int D1 = (int)sigma + 1;
-    u32 *hist = ar.alloc<u32>((i64)D1 * pr.windows + 1);
-    u32 *hscan = ar.alloc<u32>(scan_tmp_words((i64)D1 * pr.windows));
+    hist = ar.alloc<u32>((i64)D1 * pr.windows + 1);
+    hscan = ar.alloc<u32>(scan_tmp_words((i64)D1 * pr.windows));
     SAIX_ARENA_OK(ar);
     {
         Prof prof_("dc3.srec_apply", 48.0 * m, st);
@@ -2168,6 +2236,7 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
         k_rs_window<<<(unsigned)pr.windows, PS_THREADS, 16 << RW_SHIFT, st>>>(stage2, pr, RS, hist, D1);
         SAIX_LAUNCHED();
     }
+    }  // scatter path
     // 2: non-sample records in sorted order: per-(digit, window) offsets,
     // then one CTA per RS window
     uint4 *M0 = (uint4 *)stage1;  // stage1 is free again and holds >= m records
@@ -2248,7 +2317,7 @@ static size_t dc3_plan(i64 n, int text_bytes = 4) {
         size_t s2 = (size_t)k * 16 + (size_t)os_scratch_words(m) * 4;
         size_t s3 = (size_t)k * 16 + (size_t)merge_split_words(N) * 4 +
                     (size_t)(pm.stage1_items() + pm.stage2_items()) * 8 + (size_t)pm.cursor_words() * 4;
-        size_t stream_t = (size_t)m * 16 + (s1 > s2 ? (s1 > s3 ? s1 : s3) : (s2 > s3 ? s2 : s3));
+        size_t stream_t = (size_t)m * 20 + (s1 > s2 ? (s1 > s3 ? s1 : s3) : (s2 > s3 ? s2 : s3));
         // wide-level finish: RB + (mod-0 bucket sort | merge split + ISA staging)
         size_t wf1 = (size_t)k * 12 + (size_t)bs_scratch_words(N / 8 + 2) * 4 + bs_ps_bytes(k);
         size_t wf2 = (size_t)merge_split_words(N) * 4 + (size_t)(pm.stage1_items() + pm.stage2_items()) * 8 +
