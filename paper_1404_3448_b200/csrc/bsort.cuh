@@ -130,7 +130,7 @@ k_bs_window(const uint4 *__restrict__ stage2, PsPlan plan, u64 *__restrict__ key
 }
 // bytes of arena space bucket_sort takes for the bucketed scatter
 inline size_t bs_ps_bytes(i64 n) {
-    if (n < ((i64)1 << 20)) return 0;
+    if (n < kDirectScatterItems) return 0;
     PsPlan p = PsPlan::of(n, 16);
     return (size_t)(p.stage1_items() + p.stage2_items()) * 16 + (size_t)p.cursor_words() * 4 + 4 * Arena::kAlign;
 }

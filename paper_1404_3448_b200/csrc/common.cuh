@@ -24,6 +24,10 @@ using i64 = int64_t;
 
 constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
 
+// Below this many items a permutation's random 4-12 B writes stay in L2 and
+// beat the three streaming passes of the bucketed scatter (pscatter.cuh).
+constexpr i64 kDirectScatterItems = (i64)1 << 23;
+
 // ---------------------------------------------------------------- errors
 
 void set_error(const char *fmt, ...);

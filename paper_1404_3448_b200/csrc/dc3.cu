@@ -1297,7 +1297,7 @@ __global__ void k_scatter_direct(const u32 *__restrict__ idx, const u32 *__restr
 static int scatter_u32(Arena &ar, const u32 *idx, const u32 *val, i64 n, i64 n_dest, u32 *dst, cudaStream_t st,
                        const char *prof) {
     if (n <= 0) return SAIX_OK;
-    if (n < ((i64)1 << 20)) {
+    if (n < kDirectScatterItems) {
         Prof prof_(prof, 12.0 * n, st);
         k_scatter_direct<<<grid_for(n, 256), 256, 0, st>>>(idx, val, n, dst);
         SAIX_LAUNCHED();
@@ -1949,7 +1949,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
                 (long long)L.n, (int)sizeof(TT) * 8, (unsigned long long)sigma, (long long)m, D,
                 sorted_vals ? (bsorted ? "bucket-sort" : "radix") : "bitmap", (i64)D == m ? " (unique)" : "");
     if ((i64)D == m) {
-        if (sorted_vals && m > ((i64)1 << 20)) {
+        if (sorted_vals && m >= kDirectScatterItems) {
             PsPlan pu = PsPlan::of(m, 4);
             pu.set_cursors(ar.alloc<u32>(pu.cursor_words()));
             uint2 *s1 = ar.alloc<uint2>(pu.stage1_items()), *s2 = ar.alloc<uint2>(pu.stage2_items());
