@@ -1054,7 +1054,7 @@ constexpr u32 kNoPred = 0xFFFFFFFFu;
 template <int MODE>
 __global__ void __launch_bounds__(MT_THREADS)
 k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
-                 uint2 *__restrict__ stage) {
+                 uint2 *__restrict__ stage, u32 *__restrict__ isa_direct) {
     // shared tile as comparison keys (merge_key_*) + positions: one 8 B key
     // pair per comparison instead of two 16 B records
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1121,6 +1121,8 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
     __syncthreads();
     if (sa)
         for (int x = threadIdx.x; x < cnt; x += MT_THREADS) __stcs(sa + d0 + x, out[x]);
+    if (isa_direct)  // small levels: the ISA target is L2-resident
+        for (int x = threadIdx.x; x < cnt; x += MT_THREADS) isa_direct[out[x]] = (u32)(d0 + x);
     if (MODE != EMIT_NONE) {
         uint2 it[MT_ITEMS];
         bool ok[MT_ITEMS];
@@ -1140,7 +1142,7 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
 
 template <int MODE>
 static int merge_rec_launch(RecMergeView v, i64 na, i64 nb, const u32 *split, u32 *sa, const PsPlan &plan,
-                            uint2 *stage, cudaStream_t st) {
+                            uint2 *stage, cudaStream_t st, u32 *isa_direct = nullptr) {
     static bool attr = false;
     size_t smem = (size_t)MT_TILE * 24 + 8 * (size_t)PS_MAX_BUCKETS;
     if (!attr) {
@@ -1149,7 +1151,7 @@ static int merge_rec_launch(RecMergeView v, i64 na, i64 nb, const u32 *split, u3
     }
     size_t use = (size_t)MT_TILE * 24 + 8 * (size_t)(MODE == EMIT_NONE ? 1 : plan.a.buckets);
     k_merge_tile_rec<MODE><<<(unsigned)ceil_div(na + nb, MT_TILE), MT_THREADS, use, st>>>(v, na, nb, split, sa, plan,
-                                                                                         stage);
+                                                                                         stage, isa_direct);
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
@@ -1472,7 +1474,7 @@ struct MergeRA {
 template <int MODE, class V>
 __global__ void __launch_bounds__(MT_THREADS)
 k_merge_tile_m(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
-               uint2 *__restrict__ stage) {
+               uint2 *__restrict__ stage, u32 *__restrict__ isa_direct) {
     extern __shared__ __align__(16) unsigned char smem[];
     MRec *sh = reinterpret_cast<MRec *>(smem);
     u32 *out = reinterpret_cast<u32 *>(sh + MT_TILE);
@@ -1510,6 +1512,8 @@ k_merge_tile_m(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restri
     __syncthreads();
     if (sa)
         for (int x = threadIdx.x; x < cnt; x += MT_THREADS) __stcs(sa + d0 + x, out[x]);
+    if (isa_direct)
+        for (int x = threadIdx.x; x < cnt; x += MT_THREADS) isa_direct[out[x]] = (u32)(d0 + x);
     if (MODE == EMIT_ISA) {
         uint2 it[MT_ITEMS];
         bool ok[MT_ITEMS];
@@ -1562,6 +1566,8 @@ static int dc3_wide_finish(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sig
     MergeRA V{RA + pad, RB, RBc1};
     i64 ntiles = ceil_div(total, MT_TILE);
     u32 *split = ar.alloc<u32>(merge_split_words(total));
+    u32 *isa_direct = (ISA && total < 2 * kDirectScatterItems) ? ISA : nullptr;
+    if (isa_direct) ISA = nullptr;  // written by the tiles directly
     PsPlan pm = PsPlan::of(ISA ? total : 1, 4);
     pm.set_cursors(ar.alloc<u32>(pm.cursor_words()));
     uint2 *pst1 = ISA ? ar.alloc<uint2>(pm.stage1_items()) : nullptr;
@@ -1586,10 +1592,11 @@ static int dc3_wide_finish(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sig
         }
         size_t smem = (size_t)MT_TILE * 24 + 8 * (size_t)(ISA ? pm.a.buckets : 1);
         if (ISA)
-            k_merge_tile_m<EMIT_ISA, MergeRA><<<(unsigned)ntiles, MT_THREADS, smem, st>>>(V, na, k, split, SA, pm, pst1);
+            k_merge_tile_m<EMIT_ISA, MergeRA><<<(unsigned)ntiles, MT_THREADS, smem, st>>>(V, na, k, split, SA, pm, pst1,
+                                                                                          nullptr);
         else
             k_merge_tile_m<EMIT_NONE, MergeRA><<<(unsigned)ntiles, MT_THREADS, smem, st>>>(V, na, k, split, SA, pm,
-                                                                                           pst1);
+                                                                                           pst1, isa_direct);
     }
     SAIX_LAUNCHED();
     if (ISA) SAIX_TRY(ps_finish(pst1, pst2, pm, U32Apply{ISA}, st, "dc3.isa_apply", 28.0 * total));
@@ -2262,7 +2269,8 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     i64 total = na + k;
     i64 ntiles = ceil_div(total, MT_TILE);
     u32 *split = ar.alloc<u32>(merge_split_words(total));
-    int mode = ISA ? EMIT_ISA : (Phi ? EMIT_PHI : EMIT_NONE);
+    const bool isa_direct = ISA && total < 2 * kDirectScatterItems;
+    int mode = (ISA && !isa_direct) ? EMIT_ISA : (ISA ? EMIT_NONE : (Phi ? EMIT_PHI : EMIT_NONE));
     PsPlan pm = PsPlan::of(mode == EMIT_NONE ? 1 : total, 4);
     pm.set_cursors(ar.alloc<u32>(pm.cursor_words()));
     uint2 *pst1 = mode == EMIT_NONE ? nullptr : ar.alloc<uint2>(pm.stage1_items());
@@ -2278,7 +2286,7 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
         Prof prof_("dc3.merge_tile", 16.0 * total + (SA ? 4.0 * total : 0) + (mode ? 8.0 * total : 0), st);
         if (mode == EMIT_ISA) SAIX_TRY(merge_rec_launch<EMIT_ISA>(V, na, k, split, SA, pm, pst1, st));
         else if (mode == EMIT_PHI) SAIX_TRY(merge_rec_launch<EMIT_PHI>(V, na, k, split, SA, pm, pst1, st));
-        else SAIX_TRY(merge_rec_launch<EMIT_NONE>(V, na, k, split, SA, pm, pst1, st));
+        else SAIX_TRY(merge_rec_launch<EMIT_NONE>(V, na, k, split, SA, pm, pst1, st, isa_direct ? ISA : nullptr));
     }
     if (mode != EMIT_NONE)
         SAIX_TRY(ps_finish(pst1, pst2, pm, U32Apply{mode == EMIT_ISA ? ISA : Phi}, st,
