@@ -1005,13 +1005,31 @@ struct RecMergeView {
     __device__ __forceinline__ uint4 rb(i64 j) const { return B[j]; }
 };
 
-__global__ void k_merge_partition_rec(RecMergeView v, i64 na, i64 nb, i64 ntiles, u32 *__restrict__ split) {
+// record merge tile: 4096 outputs per CTA (one merge-path search per 16
+// outputs); shared keys + positions 24 B per output
+constexpr int RM_THREADS = 256, RM_ITEMS = 4, RM_TILE = RM_THREADS * RM_ITEMS;
+
+// Split search at every `stride`-th tile boundary (stride = 1: every tile).
+// With `coarse` (splits at RM_COARSE x coarser boundaries) each search starts
+// inside its coarse window: ~half the probe rounds, and the probes of
+// neighbouring tiles share the window's lines.
+constexpr int RM_COARSE = 32;
+__global__ void k_merge_partition_rec(RecMergeView v, i64 na, i64 nb, i64 ntiles, u32 *__restrict__ split,
+                                      i64 stride, const u32 *__restrict__ coarse) {
     i64 total = na + nb;
     int lane = lane_id();
     i64 warps = ((i64)gridDim.x * blockDim.x) >> 5;
-    for (i64 t = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t <= ntiles; t += warps) {
-        i64 d = t * MT_TILE < total ? t * MT_TILE : total;
+    i64 nsplit = ceil_div(ntiles, stride);  // boundaries 0 .. nsplit (the last = total)
+    for (i64 t = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t <= nsplit; t += warps) {
+        i64 d = t * stride * RM_TILE < total ? t * stride * RM_TILE : total;
         i64 lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+        if (coarse) {
+            i64 c = t / RM_COARSE;
+            i64 clo = coarse[c], chi = coarse[c + 1 <= ceil_div(ntiles, RM_COARSE) ? c + 1 : c];
+            if (clo > lo) lo = clo;
+            if (chi < hi && t % RM_COARSE) hi = chi;
+            if (t % RM_COARSE == 0) lo = hi = clo;  // a coarse boundary: already known
+        }
         while (lo < hi) {
             i64 span = hi - lo;
             i64 x = lo + (span * (lane + 1)) / 33;
@@ -1052,28 +1070,28 @@ constexpr u32 kNoPred = 0xFFFFFFFFu;
 //   EMIT_ISA  {pos, rank}           -> ISA[pos] = rank
 //   EMIT_PHI  {pos, pos of rank-1}  -> Phi[pos]  (kNoPred at rank 0)
 template <int MODE>
-__global__ void __launch_bounds__(MT_THREADS)
+__global__ void __launch_bounds__(RM_THREADS)
 k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
                  uint2 *__restrict__ stage, u32 *__restrict__ isa_direct) {
     // shared tile as comparison keys (merge_key_*) + positions: one 8 B key
     // pair per comparison instead of two 16 B records
     extern __shared__ __align__(16) unsigned char smem[];
     u64 *k1 = reinterpret_cast<u64 *>(smem);
-    u64 *k2 = k1 + MT_TILE;
-    u32 *pos = reinterpret_cast<u32 *>(k2 + MT_TILE);
-    u32 *out = pos + MT_TILE;
-    u32 *sh_cnt = out + MT_TILE;
+    u64 *k2 = k1 + RM_TILE;
+    u32 *pos = reinterpret_cast<u32 *>(k2 + RM_TILE);
+    u32 *out = pos + RM_TILE;
+    u32 *sh_cnt = out + RM_TILE;
     u32 *sh_base = sh_cnt + plan.a.buckets;
     __shared__ u32 sh_pred;
     i64 total = na + nb;
-    i64 d0 = (i64)blockIdx.x * MT_TILE;
-    i64 d1 = d0 + MT_TILE < total ? d0 + MT_TILE : total;
+    i64 d0 = (i64)blockIdx.x * RM_TILE;
+    i64 d1 = d0 + RM_TILE < total ? d0 + RM_TILE : total;
     i64 i0 = split[blockIdx.x], i1 = split[blockIdx.x + 1];
     i64 j0 = d0 - i0;
     int nat = (int)(i1 - i0), cnt = (int)(d1 - d0), nbt = cnt - nat;
 #pragma unroll
-    for (int q = 0; q < MT_ITEMS; q++) {
-        int x = threadIdx.x + q * MT_THREADS;
+    for (int q = 0; q < RM_ITEMS; q++) {
+        int x = threadIdx.x + q * RM_THREADS;
         if (x < cnt) {
             if (x < nat) {
                 uint4 e = v.ra(i0 + x);
@@ -1102,7 +1120,7 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
     }
     __syncthreads();
     const u64 *B1 = k1 + nat, *B2 = k2 + nat;
-    int dt = threadIdx.x * MT_ITEMS;
+    int dt = threadIdx.x * RM_ITEMS;
     if (dt < cnt) {
         int lo = dt > nbt ? dt - nbt : 0, hi = dt < nat ? dt : nat;
         while (lo < hi) {
@@ -1112,7 +1130,7 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
         }
         int i = lo, j = dt - lo;
 #pragma unroll
-        for (int r = 0; r < MT_ITEMS; r++) {
+        for (int r = 0; r < RM_ITEMS; r++) {
             if (dt + r >= cnt) break;
             bool takeA = j >= nbt || (i < nat && keys_a_first(k1[i], B1, B2, j));
             out[dt + r] = takeA ? pos[i++] : pos[nat + j++];
@@ -1120,22 +1138,22 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
     }
     __syncthreads();
     if (sa)
-        for (int x = threadIdx.x; x < cnt; x += MT_THREADS) __stcs(sa + d0 + x, out[x]);
+        for (int x = threadIdx.x; x < cnt; x += RM_THREADS) __stcs(sa + d0 + x, out[x]);
     if (isa_direct)  // small levels: the ISA target is L2-resident
-        for (int x = threadIdx.x; x < cnt; x += MT_THREADS) isa_direct[out[x]] = (u32)(d0 + x);
+        for (int x = threadIdx.x; x < cnt; x += RM_THREADS) isa_direct[out[x]] = (u32)(d0 + x);
     if (MODE != EMIT_NONE) {
-        uint2 it[MT_ITEMS];
-        bool ok[MT_ITEMS];
+        uint2 it[RM_ITEMS];
+        bool ok[RM_ITEMS];
 #pragma unroll
-        for (int q = 0; q < MT_ITEMS; q++) {
-            int x = threadIdx.x + q * MT_THREADS;
+        for (int q = 0; q < RM_ITEMS; q++) {
+            int x = threadIdx.x + q * RM_THREADS;
             ok[q] = x < cnt;
             if (ok[q]) {
                 if (MODE == EMIT_ISA) it[q] = make_uint2(out[x], (u32)(d0 + x));
                 else it[q] = make_uint2(out[x], x > 0 ? out[x - 1] : sh_pred);
             }
         }
-        ps_block_emit<uint2, MT_THREADS, MT_ITEMS>(it, ok, plan.a, stage, reinterpret_cast<uint2 *>(k1), sh_cnt,
+        ps_block_emit<uint2, RM_THREADS, RM_ITEMS>(it, ok, plan.a, stage, reinterpret_cast<uint2 *>(k1), sh_cnt,
                                                    sh_base);
     }
 }
@@ -1144,13 +1162,13 @@ template <int MODE>
 static int merge_rec_launch(RecMergeView v, i64 na, i64 nb, const u32 *split, u32 *sa, const PsPlan &plan,
                             uint2 *stage, cudaStream_t st, u32 *isa_direct = nullptr) {
     static bool attr = false;
-    size_t smem = (size_t)MT_TILE * 24 + 8 * (size_t)PS_MAX_BUCKETS;
+    size_t smem = (size_t)RM_TILE * 24 + 8 * (size_t)PS_MAX_BUCKETS;
     if (!attr) {
         SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_rec<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    size_t use = (size_t)MT_TILE * 24 + 8 * (size_t)(MODE == EMIT_NONE ? 1 : plan.a.buckets);
-    k_merge_tile_rec<MODE><<<(unsigned)ceil_div(na + nb, MT_TILE), MT_THREADS, use, st>>>(v, na, nb, split, sa, plan,
+    size_t use = (size_t)RM_TILE * 24 + 8 * (size_t)(MODE == EMIT_NONE ? 1 : plan.a.buckets);
+    k_merge_tile_rec<MODE><<<(unsigned)ceil_div(na + nb, RM_TILE), RM_THREADS, use, st>>>(v, na, nb, split, sa, plan,
                                                                                          stage, isa_direct);
     SAIX_LAUNCHED();
     return SAIX_OK;
@@ -2267,8 +2285,8 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     i64 na = m - pad;
     RecMergeView V{RS + pad, M0};
     i64 total = na + k;
-    i64 ntiles = ceil_div(total, MT_TILE);
-    u32 *split = ar.alloc<u32>(merge_split_words(total));
+    i64 ntiles = ceil_div(total, RM_TILE);
+    u32 *split = ar.alloc<u32>(ceil_div(total, RM_TILE) + 2);
     const bool isa_direct = ISA && total < 2 * kDirectScatterItems;
     int mode = (ISA && !isa_direct) ? EMIT_ISA : (ISA ? EMIT_NONE : (Phi ? EMIT_PHI : EMIT_NONE));
     PsPlan pm = PsPlan::of(mode == EMIT_NONE ? 1 : total, 4);
@@ -2279,7 +2297,13 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     SAIX_CUDA(cudaMemsetAsync(pm.a.cursor, 0, (size_t)pm.cursor_words() * 4, st));
     {
         Prof prof_("dc3.merge_partition", 32.0 * (ntiles + 1), st);
-        k_merge_partition_rec<<<grid_for((ntiles + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, split);
+        i64 nc = ceil_div(ntiles, RM_COARSE);
+        u32 *coarse = ar.alloc<u32>(nc + 2);
+        SAIX_ARENA_OK(ar);
+        k_merge_partition_rec<<<grid_for((nc + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, coarse, RM_COARSE,
+                                                                            nullptr);
+        SAIX_LAUNCHED();
+        k_merge_partition_rec<<<grid_for((ntiles + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, split, 1, coarse);
     }
     SAIX_LAUNCHED();
     {
