@@ -1993,23 +1993,23 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             }
             SAIX_LAUNCHED();
             SAIX_TRY(ps_finish(s1, s2, pu, U32Apply{ISAc}, st, "dc3.unique_isa", 28.0 * m));
-            if (RA_out && bsorted) {
-                // the wide-level finish (dc3_wide_finish) merges from sample
-                // records in rank order: build them while the keys are alive
-                uint4 *RA = ar.alloc<uint4>(m);
-                SAIX_ARENA_OK(ar);
-                Prof prof_("dc3.arec", 36.0 * m, st);
-                k_arec<<<grid_for(m, 256), 256, 0, st>>>(sorted_keys, sorted_vals, L, kbits, ISAc, RA);
-                SAIX_LAUNCHED();
-                *RA_out = RA;
-                keep_arena = true;
-            }
         } else {
             Prof prof_("dc3.unique_ranks", 12.0 * m, st);
             if (sorted_vals) k_unique_from_sorted<<<g, K_THREADS, 0, st>>>(sorted_vals, m, SAc, ISAc);
             else if (SAc) k_unique_from_names<<<g, K_THREADS, 0, st>>>(tt, m, SAc, ISAc);
             else k_isa_from_names<<<g, K_THREADS, 0, st>>>(tt, m, ISAc);
             SAIX_LAUNCHED();
+        }
+        if (RA_out && bsorted) {
+            // the wide-level finish (dc3_wide_finish) merges from sample
+            // records in rank order: build them while the keys are alive
+            uint4 *RA = ar.alloc<uint4>(m);
+            SAIX_ARENA_OK(ar);
+            Prof prof_("dc3.arec", 36.0 * m, st);
+            k_arec<<<grid_for(m, 256), 256, 0, st>>>(sorted_keys, sorted_vals, L, kbits, ISAc, RA);
+            SAIX_LAUNCHED();
+            *RA_out = RA;
+            keep_arena = true;
         }
         if (!keep_arena) ar.reset(mark);
     } else {
