@@ -2024,7 +2024,18 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             else
                 SAIX_TRY(resolve_ties(c, EqPacked{sorted_keys}, m, m - D, sorted_vals, kk, SAc, ISAc, resolved));
         }
-        ar.reset(mark);
+        if (resolved && RA_out && bsorted) {
+            // the keys still describe the (tie-reordered) sorted samples: RA
+            // for the wide-level finish without text gathers
+            uint4 *RA = ar.alloc<uint4>(m);
+            SAIX_ARENA_OK(ar);
+            Prof prof_("dc3.arec", 36.0 * m, st);
+            k_arec<<<grid_for(m, 256), 256, 0, st>>>(sorted_keys, sorted_vals, L, kbits, ISAc, RA);
+            SAIX_LAUNCHED();
+            *RA_out = RA;
+        } else {
+            ar.reset(mark);
+        }
         if (!resolved) {
             if (narrow) SAIX_TRY(dc3_level<u8>(c, (const u8 *)tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));
             else SAIX_TRY(dc3_level<u32>(c, tt, m, (u64)D, SAc, ISAc, nullptr, depth + 1));

@@ -189,6 +189,57 @@ __global__ void k_lcp_direct(Txt tx, i64 n, i64 sep, const u32 *__restrict__ sa,
     }
 }
 
+// Packed-text direct LCP with instruction-level parallelism: every thread
+// takes LD_ILP adjacent-suffix pairs of its CTA's chunk at once, so the SA
+// loads and the first 32-character word compare of all of them are in flight
+// together (the first word decides almost every pair of a DNA-like text).
+constexpr int LD_ILP = 4;
+__global__ void __launch_bounds__(256)
+k_lcp_direct_p2(Pack2Text tx, i64 n, i64 sep, const u32 *__restrict__ sa, u32 *__restrict__ lcp,
+                u32 *__restrict__ ncap, u32 *__restrict__ list, u32 list_cap, u32 boundary, u32 *best) {
+    u32 mx = 0;
+    const i64 step = (i64)gridDim.x * 256 * LD_ILP;
+    for (i64 base = (i64)blockIdx.x * 256 * LD_ILP; base < n; base += step) {
+        u32 iv[LD_ILP], jv[LD_ILP];
+        u64 wi[LD_ILP], wj[LD_ILP];
+#pragma unroll
+        for (int q = 0; q < LD_ILP; q++) {
+            i64 r = base + q * 256 + threadIdx.x;
+            jv[q] = r < n ? __ldcs(sa + r) : 0u;
+            iv[q] = (r > 0 && r < n) ? sa[r - 1] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < LD_ILP; q++) {
+            wi[q] = load2(tx.W, iv[q]);
+            wj[q] = load2(tx.W, jv[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < LD_ILP; q++) {
+            i64 r = base + q * 256 + threadIdx.x;
+            if (r >= n) continue;
+            u32 h = 0;
+            if (r > 0) {
+                u32 i = iv[q], j = jv[q];
+                u32 lim = match_limit(n, sep, i, j);
+                u32 stop = lim < LCP_CAP ? lim : LCP_CAP;
+                u64 d = wi[q] ^ wj[q];
+                if (d) h = min((u32)(__ffsll((long long)d) - 1) >> 1, stop);
+                else h = tx.match(i, j, 32u < stop ? 32u : stop, stop);
+                if (h == LCP_CAP && lim > LCP_CAP) {
+                    u32 at = atomicAdd(ncap, 1u);
+                    if (at < list_cap) list[at] = (u32)r;
+                }
+                if (best && cross_pair(i, j, boundary) && h > mx) mx = h;
+            }
+            __stcs(lcp + r, h);
+        }
+    }
+    if (best) {
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane_id() == 0 && mx) atomicMax(best, mx);
+    }
+}
+
 // one warp per capped entry: 32 windows of 32 characters (2-bit) per step
 template <class Txt>
 __global__ void k_lcp_extend(Txt tx, i64 n, i64 sep, const u32 *__restrict__ sa, u32 *__restrict__ lcp,
@@ -307,7 +358,8 @@ int lcp_compute(const void *text, int text_bytes, i64 n, const u32 *sa, u32 *lcp
             }
             SAIX_LAUNCHED();
             Prof prof_("lcp.direct", 12.0 * n + 2.0 * n / 4, st);
-            k_lcp_direct<Pack2Text><<<g, 256, 0, st>>>(Pack2Text{W2}, n, sep, sa, lcp, ncap, list, lc, bd, bp);
+            k_lcp_direct_p2<<<grid_for(ceil_div(n, LD_ILP), 256), 256, 0, st>>>(Pack2Text{W2}, n, sep, sa, lcp, ncap,
+                                                                                list, lc, bd, bp);
         } else {
             Prof prof_("lcp.direct", 12.0 * n + 2.0 * n, st);
             k_lcp_direct<ByteText><<<g, 256, 0, st>>>(ByteText{(const u8 *)text, n}, n, sep, sa, lcp, ncap, list, lc,

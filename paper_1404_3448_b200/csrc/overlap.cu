@@ -555,6 +555,56 @@ __global__ void k_batch_lcp(Txt tx, const u32 *__restrict__ sap, i64 nx, PairCla
     }
 }
 
+// packed-text variant with LD_ILP pairs per thread in flight (see lcp.cu)
+constexpr int BL_ILP = 4;
+__global__ void __launch_bounds__(256)
+k_batch_lcp_p2(Pack2Text tx, const u32 *__restrict__ sap, i64 nx, PairClamp pc, U32Div dv, u32 *__restrict__ lcp,
+               u32 *__restrict__ ncap, u32 *__restrict__ list, u32 list_cap) {
+    const i64 step = (i64)gridDim.x * 256 * BL_ILP;
+    for (i64 base = (i64)blockIdx.x * 256 * BL_ILP; base < nx; base += step) {
+        u32 iv[BL_ILP], jv[BL_ILP], gv[BL_ILP];
+        u64 wi[BL_ILP], wj[BL_ILP];
+#pragma unroll
+        for (int q = 0; q < BL_ILP; q++) {
+            i64 r = base + q * 256 + threadIdx.x;
+            gv[q] = 0xFFFFFFFFu;
+            jv[q] = iv[q] = 0u;
+            if (r < nx) {
+                u32 g = pc.stride > 0 ? dv.div((u32)r) : pair_of(pc.xoff, pc.P, pc.stride, r);
+                if (r > pc.xoff[g] + 1) {  // the terminator entry and the first real suffix have no predecessor
+                    gv[q] = g;
+                    jv[q] = __ldcs(sap + r);
+                    iv[q] = sap[r - 1];
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < BL_ILP; q++) {
+            wi[q] = load2(tx.W, iv[q]);
+            wj[q] = load2(tx.W, jv[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < BL_ILP; q++) {
+            i64 r = base + q * 256 + threadIdx.x;
+            if (r >= nx) continue;
+            u32 h = 0;
+            if (gv[q] != 0xFFFFFFFFu) {
+                u32 i = iv[q], j = jv[q];
+                u32 lim = pc.lim(gv[q], i, j);
+                u32 stop = lim < LCP_CAP ? lim : LCP_CAP;
+                u64 d = wi[q] ^ wj[q];
+                if (d) h = min((u32)(__ffsll((long long)d) - 1) >> 1, stop);
+                else h = tx.match(i, j, 32u < stop ? 32u : stop, stop);
+                if (h == LCP_CAP && lim > LCP_CAP) {
+                    u32 at = atomicAdd(ncap, 1u);
+                    if (at < list_cap) list[at] = (u32)r;
+                }
+            }
+            __stcs(lcp + r, h);
+        }
+    }
+}
+
 template <class Txt>
 __global__ void k_batch_lcp_extend(Txt tx, const u32 *__restrict__ sap, PairClamp pc, u32 *__restrict__ lcp,
                                    const u32 *__restrict__ ncap, const u32 *__restrict__ list) {
@@ -884,8 +934,9 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
     }
     {
         Prof prof_("batch.lcp", 12.0 * nx + nx / 2.0, st);
-        if (pack) k_batch_lcp<Pack2Text><<<grid_for(nx, 256), 256, 0, st>>>(Pack2Text{w.W2}, sap, nx, pc, lcp, w.ncap,
-                                                                           w.list, lc);
+        if (pack)
+            k_batch_lcp_p2<<<grid_for(ceil_div(nx, BL_ILP), 256), 256, 0, st>>>(
+                Pack2Text{w.W2}, sap, nx, pc, U32Div::of(b.stride > 0 ? (u32)b.stride : 1u), lcp, w.ncap, w.list, lc);
         else k_batch_lcp<ByteText><<<grid_for(nx, 256), 256, 0, st>>>(ByteText{w.X, nx}, sap, nx, pc, lcp, w.ncap,
                                                                      w.list, lc);
     }
