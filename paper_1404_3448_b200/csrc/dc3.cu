@@ -99,23 +99,28 @@ k_bitmap_set_u8(const u8 *__restrict__ T, SampleLayout L, u64 s1, u32 *__restric
     if (use_smem) {
         for (u32 w = threadIdx.x; w < nwords; w += blockDim.x) shb[w] = 0;
     }
-    const i64 j0 = (i64)blockIdx.x * TT_TILE;
-    SmemText t = stage_text(T, L.n, 3 * j0, 3 * TT_TILE + 4, shw, 256);
     u32 *dst = use_smem ? shb : bm;
-    for (int x = threadIdx.x; x < TT_TILE; x += 256) {
-        i64 j = j0 + x;
-        if (j >= L.m1) break;
-        i64 p = 3 * j;
-        u32 c1 = t(p + 1), c2 = t(p + 2), c3 = t(p + 3), c4 = t(p + 4);
-        u64 code = ((u64)c1 * s1 + c2) * s1 + c3;
-        u32 w = (u32)(code >> 5), bit = 1u << (code & 31);
-        if (!(dst[w] & bit)) atomicOr(&dst[w], bit);
-        if (j < L.m2) {
-            code = ((u64)c2 * s1 + c3) * s1 + c4;
-            w = (u32)(code >> 5);
-            bit = 1u << (code & 31);
+    const i64 ntiles = ceil_div(L.m1 > 0 ? L.m1 : 1, TT_TILE);
+    // grid-stride over tiles: a large private bitmap is merged once per CTA
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const i64 j0 = tile * TT_TILE;
+        SmemText t = stage_text(T, L.n, 3 * j0, 3 * TT_TILE + 4, shw, 256);
+        for (int x = threadIdx.x; x < TT_TILE; x += 256) {
+            i64 j = j0 + x;
+            if (j >= L.m1) break;
+            i64 p = 3 * j;
+            u32 c1 = t(p + 1), c2 = t(p + 2), c3 = t(p + 3), c4 = t(p + 4);
+            u64 code = ((u64)c1 * s1 + c2) * s1 + c3;
+            u32 w = (u32)(code >> 5), bit = 1u << (code & 31);
             if (!(dst[w] & bit)) atomicOr(&dst[w], bit);
+            if (j < L.m2) {
+                code = ((u64)c2 * s1 + c3) * s1 + c4;
+                w = (u32)(code >> 5);
+                bit = 1u << (code & 31);
+                if (!(dst[w] & bit)) atomicOr(&dst[w], bit);
+            }
         }
+        __syncthreads();  // the staged tile is reused by the next iteration
     }
     if (use_smem) {
         __syncthreads();
@@ -1851,9 +1856,10 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         {
             Prof prof_("dc3.bitmap_set", (double)sizeof(TT) * L.n, st);
             if (sizeof(TT) == 1 && ((uintptr_t)T.t & 3) == 0) {
-                unsigned gt = (unsigned)ceil_div(L.m1 > 0 ? L.m1 : 1, TT_TILE);
-                k_bitmap_set_u8<<<gt, 256, use_smem ? nwords * 4 : 0, st>>>((const u8 *)T.t, L, s1, bm, nwords,
-                                                                          use_smem);
+                i64 gt = ceil_div(L.m1 > 0 ? L.m1 : 1, TT_TILE);
+                if (use_smem && nwords > 1024 && gt > 2 * kNumSMs) gt = 2 * kNumSMs;
+                k_bitmap_set_u8<<<(unsigned)gt, 256, use_smem ? nwords * 4 : 0, st>>>((const u8 *)T.t, L, s1, bm,
+                                                                                     nwords, use_smem);
             } else {
                 k_bitmap_set<TT><<<gs, K_THREADS, use_smem ? nwords * 4 : 0, st>>>(T, L, s1, bm, nwords, use_smem);
             }

@@ -29,7 +29,10 @@ elif what == "c2":
     torch.cuda.profiler.start(); p.run_device(); torch.cuda.synchronize(); torch.cuda.profiler.stop()
     print(p.res.cpu())
 else:
+    # the C3 bench path: SuffixIndexer (SA + LCP, no ISA)
+    from paper_1404_3448_b200.suffix_index import SuffixIndexer
     n = int(what)
-    dt = DeviceText(RankedText(np.random.default_rng(1).integers(1, 5, size=n), 4))
-    ix = dc3_device(dt); lcp_device(ix); torch.cuda.synchronize()
-    torch.cuda.profiler.start(); ix = dc3_device(dt); lcp_device(ix); torch.cuda.synchronize(); torch.cuda.profiler.stop()
+    ix = SuffixIndexer(n, 4)
+    ix.stage(np.random.default_rng(1).integers(1, 5, size=n).astype(np.uint8))
+    ix.run_staged(); ix.run_device(); torch.cuda.synchronize()
+    torch.cuda.profiler.start(); ix.run_device(); torch.cuda.synchronize(); torch.cuda.profiler.stop()
