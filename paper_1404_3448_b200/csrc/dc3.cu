@@ -805,11 +805,11 @@ struct Mod0RecSrc {
     }
 };
 
-// Pass B of the record scatter, specialised: writes RS window w (4096 ranks)
+// Pass B of the record scatter, specialised: writes RS window w (2048 ranks)
 // and counts its mod-1 samples per cprev digit into hist[d * windows + w]
 // (digit-major, so one flat exclusive scan gives every (digit, window) its
 // output offset in the mod-0 order).
-constexpr int RW_SHIFT = 12;  // 4096 records = 64 KB window
+constexpr int RW_SHIFT = 11;  // 2048 records = 32 KB window
 __global__ void __launch_bounds__(PS_THREADS)
 k_rs_window(const uint4 *__restrict__ stage2, PsPlan plan, uint4 *__restrict__ rs, u32 *__restrict__ hist, int D1) {
     extern __shared__ __align__(16) unsigned char ps_smem[];
@@ -856,10 +856,10 @@ k_rs_window(const uint4 *__restrict__ stage2, PsPlan plan, uint4 *__restrict__ r
 // Small levels (text + ISAc <= 128 MB: random reads mostly L2 hits; C2 level
 // 0 at 73 MB measured 0.17 ms vs 0.36 ms for the scatter passes): RS by
 // gathers in rank order from the child's SAc instead of the bucketed
-// scatter -- one CTA per 4096-rank window, also counting the window's mod-1
+// scatter -- one CTA per 2048-rank window, also counting the window's mod-1
 // samples per cprev digit (as k_rs_window does).
 constexpr i64 RS_GATHER_BYTES = (i64)128 << 20;
-constexpr int RG_THREADS = 512, RG_ITEMS = 8;  // 4096 = 1 << RW_SHIFT
+constexpr int RG_THREADS = 256, RG_ITEMS = 8;  // 2048 = 1 << RW_SHIFT
 __global__ void __launch_bounds__(RG_THREADS)
 k_rs_gather(const u32 *__restrict__ sac, Text<u8> T, SampleLayout L, const u32 *__restrict__ isac,
             uint4 *__restrict__ rs, u32 *__restrict__ hist, int D1, u32 dmask, i64 windows) {
@@ -903,12 +903,12 @@ k_rs_gather(const u32 *__restrict__ sac, Text<u8> T, SampleLayout L, const u32 *
 }
 
 // Mod-0 records of RS window w, stably partitioned by cprev: one tile of
-// 4096 ranks per CTA (512 threads x 8), warp-stable ranking (as in
+// 2048 ranks per CTA (256 threads x 8), warp-stable ranking (as in
 // k_os_pass) with the global per-(digit, window) offsets already known, so
 // no look-back; the tile is staged digit-sorted in shared memory and written
 // as runs.
-constexpr int M0_THREADS = 512, M0_WARPS = M0_THREADS / 32;
-constexpr int M0_ITEMS = 8;  // 512 x 8 = 4096 = 1 << RW_SHIFT
+constexpr int M0_THREADS = 256, M0_WARPS = M0_THREADS / 32;
+constexpr int M0_ITEMS = 8;  // 256 x 8 = 2048 = 1 << RW_SHIFT
 __global__ void __launch_bounds__(M0_THREADS)
 k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__restrict__ offs, uint4 *__restrict__ M0) {
     extern __shared__ __align__(16) unsigned char m0_smem[];
@@ -2222,7 +2222,7 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     // 1: sample records in rank order
     uint4 *RS = ar.alloc<uint4>(m);
     size_t mark1 = ar.mark();
-    PsPlan pr = PsPlan::of(m, 16);
+    PsPlan pr = PsPlan::of(m, 16, (i64)16 << RW_SHIFT);
     const int D1 = (int)sigma + 1;
     if (pr.windows > 1 && pr.s2 != RW_SHIFT) {
         set_error("dc3: record window %d != %d", pr.s2, RW_SHIFT);
@@ -2362,7 +2362,7 @@ static size_t dc3_plan(i64 n, int text_bytes = 4) {
         size_t post_t = (size_t)k * 16 + (size_t)k * 32 + (size_t)k * 8 + bs_ps_bytes(k) +
                         (size_t)(sw + merge_split_words(N) + 2 * bw + scan_tmp_words(bw)) * 4;
         // streaming level: RS + (record stage | M0 + partition scratch | M0 + split + pair stage)
-        PsPlan pr = PsPlan::of(m, 16), pm = PsPlan::of(N, 4);
+        PsPlan pr = PsPlan::of(m, 16, (i64)16 << 11), pm = PsPlan::of(N, 4);
         size_t s1 = (size_t)(pr.stage1_items() + pr.stage2_items()) * 16 + (size_t)pr.cursor_words() * 4;
         size_t s2 = (size_t)k * 16 + (size_t)os_scratch_words(m) * 4;
         size_t s3 = (size_t)k * 16 + (size_t)merge_split_words(N) * 4 +

@@ -60,11 +60,11 @@ struct PsPlan {
 
     // payload of `out_bytes` per destination; coarse regions of <= 256
     // windows, at most PS_MAX_BUCKETS of them
-    static PsPlan of(i64 n_dest, int out_bytes) {
+    static PsPlan of(i64 n_dest, int out_bytes, i64 window_bytes = PS_WINDOW_BYTES) {
         PsPlan p;
         p.n_dest = n_dest > 0 ? n_dest : 1;
         int s2 = 6;
-        while (((i64)out_bytes << (s2 + 1)) <= PS_WINDOW_BYTES && ((i64)1 << s2) < p.n_dest) s2++;
+        while (((i64)out_bytes << (s2 + 1)) <= window_bytes && ((i64)1 << s2) < p.n_dest) s2++;
         int s1 = s2;
         while (s1 < s2 + 8 && ((i64)1 << s1) < p.n_dest) s1++;
         while (ceil_div(p.n_dest, (i64)1 << s1) > PS_MAX_BUCKETS) s1++;
