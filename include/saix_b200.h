@@ -116,6 +116,28 @@ SAIX_API int saix_dc3_merge(const void *text, int text_bytes, int64_t n,
  * the number of levels (at most max_levels are written to out[4*i..]). */
 SAIX_API int saix_dc3_trace(int64_t *out, int max_levels);
 
+/* ------------------------------------------------- parallel sort engine */
+/* The reference's split-kernel engine (parallel_sort.py:110-293) on the
+ * device scan and radix sort. Keys are int64 (nonnegative for the sort). */
+
+SAIX_API size_t saix_psort_workspace_bytes(int64_t n);
+
+/* exclusive_scan (parallel_sort.py:110-131): out[0] = 0, out[i] = sum(in[<i]). */
+SAIX_API int saix_exclusive_scan_i64(const int64_t *in, int64_t n, int64_t *out,
+             void *ws, size_t ws_bytes, void *stream);
+
+/* split_by_bit (parallel_sort.py:150-163): stable zero-then-one partition by
+ * bit `bit`; bits, zero_flags, dest nullable; scanned = exclusive scan of the
+ * zero flags; *zero_total (device) = number of zero bits. */
+SAIX_API int saix_split_by_bit(const int64_t *keys, int64_t n, int bit, int64_t *out,
+             int64_t *bits, int64_t *zero_flags, int64_t *scanned, int64_t *dest,
+             int64_t *zero_total, void *ws, size_t ws_bytes, void *stream);
+
+/* radix_sort / chunked_sort (parallel_sort.py:195-254): ascending stable sort
+ * of nonnegative keys < 2^total_bits (the caller checks the width). */
+SAIX_API int saix_radix_sort_i64(const int64_t *keys, int64_t n, int total_bits,
+             int64_t *out, void *ws, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------- LCP */
 
 SAIX_API size_t saix_lcp_workspace_bytes(int64_t n);

@@ -9,6 +9,8 @@ include/saix_b200.h); PyTorch provides device memory and streams only.
 from .overlap import (GeneralizedText, LcpQueryEngine, OverlapBatch, OverlapPipeline, OverlapResult,
                       lcp_query, lcp_query_batch, longest_overlap, longest_overlap_batch,
                       overlap_report, pack_pairs, parse_overlap_record)
+from .parallel_sort import (ChunkPlan, SortConfig, SplitState, chunked_sort, exclusive_scan,
+                            parallel_build_sa, plan_chunks, radix_sort, split_by_bit)
 from .rmq import SparseTable, build_sparse, query_sparse, query_sparse_batch
 from .sequence import (DnaSequence, NPolicy, RankedText, SequenceError, decode, encode,
                        gen_random, parse_fasta, write_fasta)
@@ -19,6 +21,8 @@ from .suffix_index import (Dc3Workspace, LcpArray, SuffixArray, build_lcp, build
 __version__ = "0.1.0"
 
 __all__ = [
+    "ChunkPlan", "SortConfig", "SplitState", "chunked_sort", "exclusive_scan", "parallel_build_sa",
+    "plan_chunks", "radix_sort", "split_by_bit",
     "Dc3Workspace", "DnaSequence", "GeneralizedText", "LcpArray", "LcpQueryEngine",
     "NPolicy", "OverlapBatch", "OverlapPipeline", "OverlapResult", "RankedText", "SequenceError",
     "SparseTable", "SuffixArray", "build_lcp", "build_sa_dc3", "build_sa_oracle",

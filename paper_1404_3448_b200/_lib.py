@@ -77,6 +77,10 @@ SIGNATURES = {
     "saix_lcp": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_lcp_sigma": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_dc3_trace": (_int, [_vp, _int]),
+    "saix_psort_workspace_bytes": (_c.c_size_t, [_i64]),
+    "saix_exclusive_scan_i64": (_int, [_vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_split_by_bit": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_radix_sort_i64": (_int, [_vp, _i64, _int, _vp, _vp, _c.c_size_t, _vp]),
     "saix_minmax": (_int, [_vp, _int, _i64, _vp, _vp]),
     "saix_sparse_plan_make": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),
     "saix_sparse_build": (_int, [_c.POINTER(SparsePlan), _vp, _int, _vp, _vp]),
