@@ -748,7 +748,7 @@ constexpr int SR_J = 4;                      // triplets per thread
 constexpr int SR_TILE = SR_THREADS * SR_J;   // 2048 triplets -> <= 4096 records
 
 // pass A of the record scatter: item {dest = 0-based sample rank, pos, nb, chars}
-__global__ void __launch_bounds__(SR_THREADS)
+__global__ void __launch_bounds__(SR_THREADS, 4)
 k_srec_emit(Text<u8> T, SampleLayout L, const u32 *__restrict__ isac, PsPlan plan, uint4 *__restrict__ stage) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint4 *sh_items = reinterpret_cast<uint4 *>(smem);
@@ -814,14 +814,14 @@ __global__ void __launch_bounds__(PS_THREADS)
 k_rs_window(const uint4 *__restrict__ stage2, PsPlan plan, uint4 *__restrict__ rs, u32 *__restrict__ hist, int D1) {
     extern __shared__ __align__(16) unsigned char ps_smem[];
     uint4 *win = reinterpret_cast<uint4 *>(ps_smem);
-    __shared__ u32 cnt[256];
+    __shared__ u32 cnt[PS_THREADS / 32][256];  // warp-private digit counters (plain shared atomics)
     const i64 w = blockIdx.x;
     const i64 d0 = w << RW_SHIFT;
     const i64 len = (d0 + (1 << RW_SHIFT) < plan.n_dest ? d0 + (1 << RW_SHIFT) : plan.n_dest) - d0;
     const i64 n_in = plan.cursor2[w];
     const uint4 *src = stage2 + d0;
     RsApply ap{rs};
-    for (int d = threadIdx.x; d < 256; d += PS_THREADS) cnt[d] = 0;
+    for (int d = threadIdx.x; d < (PS_THREADS / 32) * 256; d += PS_THREADS) (&cnt[0][0])[d] = 0;
     __syncthreads();
     const bool full = n_in == len;
     for (i64 x = threadIdx.x; x < n_in; x += PS_THREADS) {
@@ -846,11 +846,15 @@ k_rs_window(const uint4 *__restrict__ stage2, PsPlan plan, uint4 *__restrict__ r
             }
             if (e.x % 3 == 1) d = (e.w >> 16) & 0xFFu;
         }
-        u32 peers = digit_peers(d);
-        if (d != 0xFFFFFFFFu && (peers & lanemask_lt()) == 0) atomicAdd(&cnt[d], (u32)__popc(peers));
+        if (d != 0xFFFFFFFFu) atomicAdd(&cnt[threadIdx.x >> 5][d], 1u);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < D1; d += PS_THREADS) hist[(i64)d * plan.windows + w] = cnt[d];
+    for (int d = threadIdx.x; d < D1; d += PS_THREADS) {
+        u32 c = 0;
+#pragma unroll
+        for (int q = 0; q < PS_THREADS / 32; q++) c += cnt[q][d];
+        hist[(i64)d * plan.windows + w] = c;
+    }
 }
 
 // Small levels (text + ISAc <= 128 MB: random reads mostly L2 hits; C2 level
@@ -910,7 +914,8 @@ k_rs_gather(const u32 *__restrict__ sac, Text<u8> T, SampleLayout L, const u32 *
 constexpr int M0_THREADS = 256, M0_WARPS = M0_THREADS / 32;
 constexpr int M0_ITEMS = 8;  // 256 x 8 = 2048 = 1 << RW_SHIFT
 __global__ void __launch_bounds__(M0_THREADS)
-k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__restrict__ offs, uint4 *__restrict__ M0) {
+k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__restrict__ offs, uint4 *__restrict__ M0,
+              u32 dmask) {
     extern __shared__ __align__(16) unsigned char m0_smem[];
     uint4 *sv = reinterpret_cast<uint4 *>(m0_smem);
     u32(*cnt)[256] = reinterpret_cast<u32(*)[256]>(sv + (1 << RW_SHIFT));
@@ -940,7 +945,7 @@ k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__res
     for (int r = 0; r < M0_ITEMS; r++) {
         u32 d = (pk[r] >> 8) & 0x1FFu;
         bool ok = d < 256u;
-        u32 peers = digit_peers(d);
+        u32 peers = digit_peers_w(d, dmask);
         u32 before = __popc(peers & lt);
         u32 cur = ok ? cnt[wp][d] : 0u;
         __syncwarp();
@@ -2292,7 +2297,9 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
             SAIX_CUDA(cudaFuncSetAttribute(k_mod0_window, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M0_SMEM));
             attr = true;
         }
-        k_mod0_window<<<(unsigned)pr.windows, M0_THREADS, M0_SMEM, st>>>(RS, m, pr.windows, hist, M0);
+        u32 dmask = 1;
+        while (dmask < (u32)D1 - 1) dmask = dmask * 2 + 1;
+        k_mod0_window<<<(unsigned)pr.windows, M0_THREADS, M0_SMEM, st>>>(RS, m, pr.windows, hist, M0, dmask);
     }
     SAIX_LAUNCHED();
     ar.reset(mark_s1);  // stage2, histogram and scan temps are dead
