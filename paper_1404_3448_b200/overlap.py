@@ -204,7 +204,10 @@ class OverlapBatch:
     ``wave_residues`` residues (one generalized text per wave)."""
 
     def __init__(self, seqs: np.ndarray, offs: np.ndarray, policy: NPolicy = NPolicy.REJECT,
-                 wave_residues: int = 1 << 27):
+                 wave_residues: int | None = None):
+        if wave_residues is None:
+            import os
+            wave_residues = int(os.environ.get("SAIX_WAVE_RESIDUES", 1 << 27))
         t = _lib.torch()
         L = _lib.load()
         dev = _lib.device()
