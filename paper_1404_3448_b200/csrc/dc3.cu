@@ -611,16 +611,25 @@ constexpr int MT_TILE = MT_THREADS * MT_ITEMS;  // 2048 outputs per CTA
 
 // One warp per tile boundary: a 33-ary search (each lane probes one split
 // candidate per round) so a split costs ~log_32(n) dependent gather rounds.
-template <class V>
-__global__ void k_merge_partition(V v, i64 na, i64 nb, i64 ntiles, u32 *__restrict__ split) {
+template <class V, int TILE = MT_TILE>
+__global__ void k_merge_partition(V v, i64 na, i64 nb, i64 ntiles, u32 *__restrict__ split, i64 stride = 1,
+                                  const u32 *__restrict__ coarse = nullptr) {
     i64 total = na + nb;
     int lane = lane_id();
     i64 warps = ((i64)gridDim.x * blockDim.x) >> 5;
-    for (i64 t = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t <= ntiles; t += warps) {
-        i64 d = t * MT_TILE < total ? t * MT_TILE : total;
+    i64 nsplit = ceil_div(ntiles, stride);
+    for (i64 t = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t <= nsplit; t += warps) {
+        i64 d = t * stride * TILE < total ? t * stride * TILE : total;
         // invariant: answer in [lo, hi]; P(x) = a_first(A[x], B[d-1-x]) is
         // true for x < answer and false from answer on
         i64 lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+        if (coarse) {  // inside the coarse window (see k_merge_partition_rec)
+            i64 c = t / 32;
+            i64 clo = coarse[c], chi = coarse[c + 1 <= ceil_div(ntiles, 32) ? c + 1 : c];
+            if (clo > lo) lo = clo;
+            if (chi < hi && t % 32) hi = chi;
+            if (t % 32 == 0) lo = hi = clo;
+        }
         while (lo < hi) {
             i64 span = hi - lo;
             i64 x = lo + (span * (lane + 1)) / 33;  // candidates in [lo, hi)
@@ -1498,60 +1507,90 @@ struct MergeRA {
     }
 };
 
-// merge of record runs (MRec form) with the bucketed ISA side output
-template <int MODE, class V>
-__global__ void __launch_bounds__(MT_THREADS)
-k_merge_tile_m(V v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
+// Wide merge tile on comparison keys (as k_merge_tile_rec): a non-sample b
+// holds K1 = c0 << 32 | R(b+1), K2 = c0 << 32 | c1 and R(b+2); a mod-1
+// sample its K1 form, a mod-2 sample its K2 form + R(a+2).  1024 outputs per
+// CTA, 28 B of shared memory per output.
+constexpr int WT_THREADS = 256, WT_ITEMS = 4, WT_TILE = WT_THREADS * WT_ITEMS;
+template <int MODE>
+__global__ void __launch_bounds__(WT_THREADS)
+k_merge_tile_w(MergeRA v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
                uint2 *__restrict__ stage, u32 *__restrict__ isa_direct) {
     extern __shared__ __align__(16) unsigned char smem[];
-    MRec *sh = reinterpret_cast<MRec *>(smem);
-    u32 *out = reinterpret_cast<u32 *>(sh + MT_TILE);
-    u32 *sh_cnt = out + MT_TILE;
+    u64 *ka = reinterpret_cast<u64 *>(smem);
+    u64 *kb = ka + WT_TILE;
+    u32 *rr = reinterpret_cast<u32 *>(kb + WT_TILE);
+    u32 *pos = rr + WT_TILE;
+    u32 *out = pos + WT_TILE;
+    u32 *sh_cnt = out + WT_TILE;
     u32 *sh_base = sh_cnt + plan.a.buckets;
     i64 total = na + nb;
-    i64 d0 = (i64)blockIdx.x * MT_TILE;
-    i64 d1 = d0 + MT_TILE < total ? d0 + MT_TILE : total;
+    i64 d0 = (i64)blockIdx.x * WT_TILE;
+    i64 d1 = d0 + WT_TILE < total ? d0 + WT_TILE : total;
     i64 i0 = split[blockIdx.x], i1 = split[blockIdx.x + 1];
     i64 j0 = d0 - i0;
     int nat = (int)(i1 - i0), cnt = (int)(d1 - d0), nbt = cnt - nat;
 #pragma unroll
-    for (int q = 0; q < MT_ITEMS; q++) {
-        int x = threadIdx.x + q * MT_THREADS;
-        if (x < cnt) sh[x] = x < nat ? v.reca(i0 + x) : v.recb(j0 + (x - nat));
+    for (int q = 0; q < WT_ITEMS; q++) {
+        int x = threadIdx.x + q * WT_THREADS;
+        if (x < cnt) {
+            if (x < nat) {  // RA: {pos, nb, c0, c1}
+                uint4 e = v.A[i0 + x];
+                pos[x] = e.x;
+                if (e.x % 3 == 1) {
+                    ka[x] = ((u64)e.z << 32) | e.y;
+                } else {
+                    ka[x] = ((u64)e.z << 32) | e.w;
+                    rr[x] = e.y;
+                }
+            } else {  // RB: {3j, r1, r2, c0} + c1
+                i64 jj = j0 + (x - nat);
+                uint4 e = v.B[jj];
+                pos[x] = e.x;
+                ka[x] = ((u64)e.w << 32) | e.y;
+                kb[x] = ((u64)e.w << 32) | v.Bc1[jj];
+                rr[x] = e.z;
+            }
+        }
     }
     __syncthreads();
-    const MRec *A = sh, *B = sh + nat;
-    int dt = threadIdx.x * MT_ITEMS;
+    auto a_first = [&](int i, int j) -> bool {  // sample i vs non-sample nat + j
+        int b = nat + j;
+        if (pos[i] % 3 == 1) return ka[i] < ka[b];
+        u64 x = ka[i], y = kb[b];
+        return x < y || (x == y && rr[i] < rr[b]);
+    };
+    int dt = threadIdx.x * WT_ITEMS;
     if (dt < cnt) {
         int lo = dt > nbt ? dt - nbt : 0, hi = dt < nat ? dt : nat;
         while (lo < hi) {
             int mid = (lo + hi) >> 1;
-            if (rec_a_first(A[mid], B[dt - 1 - mid])) lo = mid + 1;
+            if (a_first(mid, dt - 1 - mid)) lo = mid + 1;
             else hi = mid;
         }
         int i = lo, j = dt - lo;
 #pragma unroll
-        for (int r = 0; r < MT_ITEMS; r++) {
+        for (int r = 0; r < WT_ITEMS; r++) {
             if (dt + r >= cnt) break;
-            bool takeA = j >= nbt || (i < nat && rec_a_first(A[i], B[j]));
-            out[dt + r] = takeA ? A[i++].pos : B[j++].pos;
+            bool takeA = j >= nbt || (i < nat && a_first(i, j));
+            out[dt + r] = takeA ? pos[i++] : pos[nat + j++];
         }
     }
     __syncthreads();
     if (sa)
-        for (int x = threadIdx.x; x < cnt; x += MT_THREADS) __stcs(sa + d0 + x, out[x]);
+        for (int x = threadIdx.x; x < cnt; x += WT_THREADS) __stcs(sa + d0 + x, out[x]);
     if (isa_direct)
-        for (int x = threadIdx.x; x < cnt; x += MT_THREADS) isa_direct[out[x]] = (u32)(d0 + x);
+        for (int x = threadIdx.x; x < cnt; x += WT_THREADS) isa_direct[out[x]] = (u32)(d0 + x);
     if (MODE == EMIT_ISA) {
-        uint2 it[MT_ITEMS];
-        bool ok[MT_ITEMS];
+        uint2 it[WT_ITEMS];
+        bool ok[WT_ITEMS];
 #pragma unroll
-        for (int q = 0; q < MT_ITEMS; q++) {
-            int x = threadIdx.x + q * MT_THREADS;
+        for (int q = 0; q < WT_ITEMS; q++) {
+            int x = threadIdx.x + q * WT_THREADS;
             ok[q] = x < cnt;
             if (ok[q]) it[q] = make_uint2(out[x], (u32)(d0 + x));
         }
-        ps_block_emit<uint2, MT_THREADS, MT_ITEMS>(it, ok, plan.a, stage, reinterpret_cast<uint2 *>(sh), sh_cnt,
+        ps_block_emit<uint2, WT_THREADS, WT_ITEMS>(it, ok, plan.a, stage, reinterpret_cast<uint2 *>(ka), sh_cnt,
                                                    sh_base);
     }
 }
@@ -1592,8 +1631,9 @@ static int dc3_wide_finish(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sig
     i64 pad = L.pad ? 1 : 0;
     i64 na = m - pad, total = na + k;
     MergeRA V{RA + pad, RB, RBc1};
-    i64 ntiles = ceil_div(total, MT_TILE);
-    u32 *split = ar.alloc<u32>(merge_split_words(total));
+    i64 ntiles = ceil_div(total, WT_TILE);
+    u32 *split = ar.alloc<u32>(ntiles + 2);
+    u32 *coarse = ar.alloc<u32>(ceil_div(ntiles, 32) + 2);
     u32 *isa_direct = (ISA && total < 2 * kDirectScatterItems) ? ISA : nullptr;
     if (isa_direct) ISA = nullptr;  // written by the tiles directly
     PsPlan pm = PsPlan::of(ISA ? total : 1, 4);
@@ -1604,27 +1644,31 @@ static int dc3_wide_finish(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sig
     SAIX_CUDA(cudaMemsetAsync(pm.a.cursor, 0, (size_t)pm.cursor_words() * 4, st));
     {
         Prof prof_("dc3.merge_partition", 32.0 * (ntiles + 1), st);
-        k_merge_partition<MergeRA><<<grid_for((ntiles + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, split);
+        i64 nc = ceil_div(ntiles, 32);
+        k_merge_partition<MergeRA, WT_TILE><<<grid_for((nc + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, coarse, 32,
+                                                                                          nullptr);
+        SAIX_LAUNCHED();
+        k_merge_partition<MergeRA, WT_TILE><<<grid_for((ntiles + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, split,
+                                                                                             1, coarse);
     }
     SAIX_LAUNCHED();
     {
         Prof prof_("dc3.merge_tile", 16.0 * na + 20.0 * k + (SA ? 4.0 * total : 0) + (ISA ? 8.0 * total : 0), st);
         static bool attr = false;
-        size_t smax = (size_t)MT_TILE * 24 + 8 * (size_t)PS_MAX_BUCKETS;
+        size_t smax = (size_t)WT_TILE * 28 + 8 * (size_t)PS_MAX_BUCKETS;
         if (!attr) {
-            SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_m<EMIT_ISA, MergeRA>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
-            SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_m<EMIT_NONE, MergeRA>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+            SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_w<EMIT_ISA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smax));
+            SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_w<EMIT_NONE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smax));
             attr = true;
         }
-        size_t smem = (size_t)MT_TILE * 24 + 8 * (size_t)(ISA ? pm.a.buckets : 1);
+        size_t smem = (size_t)WT_TILE * 28 + 8 * (size_t)(ISA ? pm.a.buckets : 1);
         if (ISA)
-            k_merge_tile_m<EMIT_ISA, MergeRA><<<(unsigned)ntiles, MT_THREADS, smem, st>>>(V, na, k, split, SA, pm, pst1,
-                                                                                          nullptr);
+            k_merge_tile_w<EMIT_ISA><<<(unsigned)ntiles, WT_THREADS, smem, st>>>(V, na, k, split, SA, pm, pst1, nullptr);
         else
-            k_merge_tile_m<EMIT_NONE, MergeRA><<<(unsigned)ntiles, MT_THREADS, smem, st>>>(V, na, k, split, SA, pm,
-                                                                                           pst1, isa_direct);
+            k_merge_tile_w<EMIT_NONE><<<(unsigned)ntiles, WT_THREADS, smem, st>>>(V, na, k, split, SA, pm, pst1,
+                                                                                  isa_direct);
     }
     SAIX_LAUNCHED();
     if (ISA) SAIX_TRY(ps_finish(pst1, pst2, pm, U32Apply{ISA}, st, "dc3.isa_apply", 28.0 * total));

@@ -16,7 +16,7 @@ from ncu_summary import load  # noqa: E402
 
 # scope -> (kernel regex that marks one invocation, regex of all its kernels)
 SCOPES = {
-    "dc3.merge_tile": (r"^k_merge_tile", r"^k_merge_tile"),
+    "dc3.merge_tile": (r"^k_merge_tile", r"^k_merge_tile"),  # _rec, _w (wide) and the probe-path tile
     "dc3.merge_partition": (r"^k_merge_partition", r"^k_merge_partition"),
     "dc3.srec_emit": (r"^k_srec_emit", r"^k_srec_emit"),
     "dc3.srec_apply": (r"^k_rs_window", r"^k_rs_window|^k_ps_refine<uint4>$"),
