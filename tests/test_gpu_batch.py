@@ -97,3 +97,19 @@ def test_repetitive_pairs_kasai_fallback():
     got = sx.longest_overlap_batch(pairs)
     for (a, b), r in zip(pairs, got):
         assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a.residues, b.residues)
+
+
+def test_full_wave_c4_scale():
+    """One full 2^27-residue wave of C4 pairs (byte levels on the bucketed
+    scatter, planted repeats -> tie resolution at the wide level); a spread
+    subset of pairs against the oracle."""
+    seqs, offs = c4_pairs(0, 6700)
+    ob = sx.OverlapBatch(seqs, offs)
+    assert len(ob.waves) == 1
+    ob.run_device()
+    got = ob.results()
+    idx = list(range(0, 6700, 23))
+    for p in idx:
+        a = seqs[offs[2 * p]:offs[2 * p + 1]].tobytes()
+        b = seqs[offs[2 * p + 1]:offs[2 * p + 2]].tobytes()
+        assert tuple(int(x) for x in got[p]) == oracle.longest_overlap(a, b), p

@@ -44,8 +44,11 @@ def test_c2_pair_full_pipeline_vs_oracle():
     assert (r.length, r.pos_a, r.pos_b) == oracle.longest_overlap(a.residues, b.residues)
 
 
-@pytest.mark.parametrize("n", [1 << 24])
+@pytest.mark.parametrize("n", [1 << 24, 1 << 26])
 def test_large_random_sa_properties(n):
+    """2^24: the byte levels gather their records (text + ranks <= 128 MB);
+    2^26: both byte levels take the bucketed-scatter path (k_srec_emit ->
+    refine -> window) and the top level is too large for direct scatters."""
     t = encode(gen_random(n, 1))
     ix = sx.build_sa_dc3(t)
     assert sa_is_correct(t.ranks, ix.sa, ix.rank)
