@@ -1906,7 +1906,8 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             Prof prof_("dc3.bitmap_set", (double)sizeof(TT) * L.n, st);
             if (sizeof(TT) == 1 && ((uintptr_t)T.t & 3) == 0) {
                 i64 gt = ceil_div(L.m1 > 0 ? L.m1 : 1, TT_TILE);
-                if (use_smem && nwords > 1024 && gt > 2 * kNumSMs) gt = 2 * kNumSMs;
+                i64 gcap = (use_smem && nwords > 1024) ? 2 * kNumSMs : 8 * kNumSMs;  // few long-lived CTAs
+                if (gt > gcap) gt = gcap;
                 k_bitmap_set_u8<<<(unsigned)gt, 256, use_smem ? nwords * 4 : 0, st>>>((const u8 *)T.t, L, s1, bm,
                                                                                      nwords, use_smem);
             } else {

@@ -46,23 +46,49 @@ __device__ __forceinline__ u32 encode_at(const u8 *__restrict__ a, i64 na, const
     return r + shift;
 }
 
-// Four output ranks per thread, stored as one u32 word (out must be 4-byte
-// aligned; the ABI entry points check and fall back to bytes otherwise).
+// Sixteen output ranks per thread, stored as one 16-byte word (out must be
+// 16-byte aligned; the ABI entry points check and fall back to bytes).
 __global__ void k_encode_gsa(const u8 *__restrict__ a, i64 na, const u8 *__restrict__ b, i64 nb, int keep_n,
                              int shift, u8 *__restrict__ out, i64 *__restrict__ bad, int words) {
     i64 n = na + nb + (b ? 1 : 0);
     i64 local_bad = INT64_MAX;
     i64 stride = (i64)gridDim.x * blockDim.x;
     if (words) {
-        u32 *out32 = reinterpret_cast<u32 *>(out);
-        i64 nw = n / 4;
-        for (i64 w = (i64)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride) {
-            u32 word = 0;
+        // 16 output ranks per thread, stored as one 16-byte word (out 16-byte
+        // aligned); runs that lie inside A or inside B skip the side test
+        uint4 *out16 = reinterpret_cast<uint4 *>(out);
+        i64 nv = n / 16;
+        for (i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+            const i64 p0 = 16 * v;
+            u32 w[4] = {0, 0, 0, 0};
+            if (p0 + 16 <= na) {
 #pragma unroll
-            for (int j = 0; j < 4; j++) word |= encode_at(a, na, b, 4 * w + j, keep_n, shift, local_bad) << (8 * j);
-            out32[w] = word;
+                for (int j = 0; j < 16; j++) {
+                    u32 r = rank_of_ascii(a[p0 + j], keep_n);
+                    if (r == 0) {
+                        if (p0 + j < local_bad) local_bad = p0 + j;
+                        r = 1;
+                    }
+                    w[j >> 2] |= (r + shift) << (8 * (j & 3));
+                }
+            } else if (p0 > na) {
+                const u8 *bb = b + (p0 - na - 1);
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    u32 r = rank_of_ascii(bb[j], keep_n);
+                    if (r == 0) {
+                        if (p0 + j < local_bad) local_bad = p0 + j;
+                        r = 1;
+                    }
+                    w[j >> 2] |= (r + shift) << (8 * (j & 3));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; j++) w[j >> 2] |= encode_at(a, na, b, p0 + j, keep_n, shift, local_bad) << (8 * (j & 3));
+            }
+            out16[v] = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        for (i64 i = 4 * nw + (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        for (i64 i = 16 * nv + (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
             out[i] = (u8)encode_at(a, na, b, i, keep_n, shift, local_bad);
     } else {
         for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -332,9 +358,9 @@ extern "C" int saix_encode_gsa(const uint8_t *a_ascii, int64_t na, const uint8_t
     cudaStream_t st = (cudaStream_t)stream;
     i64 n = na + nb + 1;
     Prof prof_("encode.gsa", 2.0 * n, st);
-    int words = ((uintptr_t)gsa & 3) == 0;
-    k_encode_gsa<<<grid_for(words ? n / 4 + 1 : n, 256), 256, 0, st>>>(a_ascii, na, b_ascii ? b_ascii : a_ascii, nb,
-                                                                      keep_n, 1, gsa, bad_pos, words);
+    int words = ((uintptr_t)gsa & 15) == 0;
+    k_encode_gsa<<<grid_for(words ? n / 16 + 1 : n, 256), 256, 0, st>>>(a_ascii, na, b_ascii ? b_ascii : a_ascii,
+                                                                       nb, keep_n, 1, gsa, bad_pos, words);
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
@@ -347,9 +373,9 @@ extern "C" int saix_encode(const uint8_t *ascii, int64_t n, int keep_n, uint8_t 
     }
     if (n == 0) return SAIX_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    int words = ((uintptr_t)ranks & 3) == 0;
-    k_encode_gsa<<<grid_for(words ? n / 4 + 1 : n, 256), 256, 0, st>>>(ascii, n, nullptr, 0, keep_n, 0, ranks,
-                                                                      bad_pos, words);
+    int words = ((uintptr_t)ranks & 15) == 0;
+    k_encode_gsa<<<grid_for(words ? n / 16 + 1 : n, 256), 256, 0, st>>>(ascii, n, nullptr, 0, keep_n, 0, ranks,
+                                                                       bad_pos, words);
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
