@@ -1463,6 +1463,28 @@ __global__ void k_arec(const u64 *__restrict__ keys, const u32 *__restrict__ val
     }
 }
 
+// Large wide levels: the neighbour ranks reach rank order by the bucketed
+// scatter instead of a random ISAc gather per sample -- nbv[s] (sample order,
+// streamed reads of ISAc) is scattered to NB[ISAc[s]].
+__global__ void k_nb_by_sample(SampleLayout L, const u32 *__restrict__ isac, u32 *__restrict__ nbv) {
+    for (i64 sidx = (i64)blockIdx.x * blockDim.x + threadIdx.x; sidx < L.m; sidx += (i64)gridDim.x * blockDim.x) {
+        u32 nb;
+        if (sidx < L.m1) nb = sidx < L.m2 ? isac[L.m1 + sidx] + 1u : 0u;  // R(3s+2)
+        else nb = sidx - L.m1 + 1 < L.m1 ? isac[sidx - L.m1 + 1] + 1u : 0u;  // R(3j+4)
+        __stcs(nbv + sidx, nb);
+    }
+}
+__global__ void k_arec_nb(const u64 *__restrict__ keys, const u32 *__restrict__ vals, SampleLayout L, int b,
+                          const u32 *__restrict__ nb_by_rank, uint4 *__restrict__ ra) {
+    const u64 cm = ((u64)1 << b) - 1;
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < L.m; r += (i64)gridDim.x * blockDim.x) {
+        u64 key = __ldcs(keys + r);
+        u32 sidx = __ldcs(vals + r);
+        i64 pos = sidx < L.m1 ? 3 * (i64)sidx + 1 : 3 * (i64)(sidx - L.m1) + 2;
+        __stcs(ra + r, make_uint4((u32)pos, __ldcs(nb_by_rank + r), (u32)(key >> (2 * b)), (u32)((key >> b) & cm)));
+    }
+}
+
 __global__ void k_brec(const u64 *__restrict__ keys, const u32 *__restrict__ vals, i64 k, int rb,
                        const uint4 *__restrict__ ra, uint4 *__restrict__ rb4, u32 *__restrict__ rbc1) {
     const u64 rm = ((u64)1 << rb) - 1;
@@ -1799,9 +1821,11 @@ static int resolve_ties(Dc3Ctx &c, Eq eq, i64 m, i64 ties, u32 *S, u64 *kk, u32 
     u32 *mid = ar.alloc<u32>(cap), *big = ar.alloc<u32>(cap);
     u32 *scal = ar.alloc<u32>(16);  // [0] mid, [1] big, [2] runs A, [3] runs B, [4] overflow
     SAIX_ARENA_OK(ar);
-    Prof prof_("dc3.tie_resolve", 8.0 * m + 24.0 * ties, st);
     SAIX_CUDA(cudaMemsetAsync(scal, 0, 16 * 4, st));
-    k_tie_init<Eq><<<grid_for(m, 256), 256, 0, st>>>(eq, m, head, rsA, rlA, scal + 2, cap, scal + 4);
+    {
+        Prof prof_("dc3.tie_resolve", 8.0 * m, st);
+        k_tie_init<Eq><<<grid_for(m, 256), 256, 0, st>>>(eq, m, head, rsA, rlA, scal + 2, cap, scal + 4);
+    }
     SAIX_LAUNCHED();
     u32 h2[3];
     SAIX_CUDA(cudaMemcpyAsync(h2, scal + 2, 12, cudaMemcpyDeviceToHost, st));
@@ -1815,6 +1839,7 @@ static int resolve_ties(Dc3Ctx &c, Eq eq, i64 m, i64 ties, u32 *S, u64 *kk, u32 
     u32 nr = h2[0];
     u32 *rs = rsA, *rl = rlA, *rs2 = rsB, *rl2 = rlB;
     u32 *cnt_cur = scal + 2, *cnt_next = scal + 3;
+    Prof prof_("dc3.tie_resolve", 24.0 * ties, st);
     for (i64 h = 1; nr > 0; h <<= 1) {
         if (h > 2 * m) {
             set_error("dc3: tie resolution did not converge");
@@ -1867,6 +1892,37 @@ static int resolve_ties(Dc3Ctx &c, Eq eq, i64 m, i64 ties, u32 *S, u64 *kk, u32 
     if (SAc) SAIX_CUDA(cudaMemcpyAsync(SAc, S, (size_t)m * 4, cudaMemcpyDeviceToDevice, st));
     ar.reset(mark);
     ok = true;
+    return SAIX_OK;
+}
+
+// RA (sample records in rank order) from the sorted triple keys: neighbour
+// ranks gathered (small levels) or scattered to rank order (large levels)
+static int build_ra(Dc3Ctx &c, const u64 *keys, const u32 *vals, const SampleLayout &L, int kbits, const u32 *ISAc,
+                    uint4 *RA) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    const i64 m = L.m;
+    if (m < kDirectScatterItems) {
+        Prof prof_("dc3.arec", 36.0 * m, st);
+        k_arec<<<grid_for(m, 256), 256, 0, st>>>(keys, vals, L, kbits, ISAc, RA);
+        SAIX_LAUNCHED();
+        return SAIX_OK;
+    }
+    size_t mark = ar.mark();
+    u32 *nbv = ar.alloc<u32>(m), *nbr = ar.alloc<u32>(m);
+    SAIX_ARENA_OK(ar);
+    {
+        Prof prof_("dc3.arec", 16.0 * m, st);
+        k_nb_by_sample<<<grid_for(m, 256), 256, 0, st>>>(L, ISAc, nbv);
+    }
+    SAIX_LAUNCHED();
+    SAIX_TRY(scatter_u32(ar, ISAc, nbv, m, m, nbr, st, "dc3.nb_scatter"));
+    {
+        Prof prof_("dc3.arec", 32.0 * m, st);
+        k_arec_nb<<<grid_for(m, 256), 256, 0, st>>>(keys, vals, L, kbits, nbr, RA);
+    }
+    SAIX_LAUNCHED();
+    ar.reset(mark);
     return SAIX_OK;
 }
 
@@ -2061,9 +2117,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             // records in rank order: build them while the keys are alive
             uint4 *RA = ar.alloc<uint4>(m);
             SAIX_ARENA_OK(ar);
-            Prof prof_("dc3.arec", 36.0 * m, st);
-            k_arec<<<grid_for(m, 256), 256, 0, st>>>(sorted_keys, sorted_vals, L, kbits, ISAc, RA);
-            SAIX_LAUNCHED();
+            SAIX_TRY(build_ra(c, sorted_keys, sorted_vals, L, kbits, ISAc, RA));
             *RA_out = RA;
             keep_arena = true;
         }
@@ -2085,9 +2139,7 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             // for the wide-level finish without text gathers
             uint4 *RA = ar.alloc<uint4>(m);
             SAIX_ARENA_OK(ar);
-            Prof prof_("dc3.arec", 36.0 * m, st);
-            k_arec<<<grid_for(m, 256), 256, 0, st>>>(sorted_keys, sorted_vals, L, kbits, ISAc, RA);
-            SAIX_LAUNCHED();
+            SAIX_TRY(build_ra(c, sorted_keys, sorted_vals, L, kbits, ISAc, RA));
             *RA_out = RA;
         } else {
             ar.reset(mark);
@@ -2424,7 +2476,10 @@ static size_t dc3_plan(i64 n, int text_bytes = 4) {
         size_t wf1 = (size_t)k * 12 + (size_t)bs_scratch_words(N / 8 + 2) * 4 + bs_ps_bytes(k);
         size_t wf2 = (size_t)merge_split_words(N) * 4 + (size_t)(pm.stage1_items() + pm.stage2_items()) * 8 +
                      (size_t)pm.cursor_words() * 4;
-        size_t wide_t = sort_t + (size_t)m * 16 + (size_t)k * 20 + (wf1 > wf2 ? wf1 : wf2) + 8 * Arena::kAlign;
+        size_t ra_t = (size_t)m * 8 + scatter_u32_bytes(m);
+        size_t wf = wf1 > wf2 ? wf1 : wf2;
+        wf = wf > ra_t ? wf : ra_t;
+        size_t wide_t = sort_t + (size_t)m * 16 + (size_t)k * 20 + wf + 8 * Arena::kAlign;
         size_t t = sort_t > bm_t ? sort_t : bm_t;
         if (!(N == n && text_bytes == 1)) t = t > wide_t ? t : wide_t;  // byte top levels stream
         t = t > post_t ? t : post_t;
