@@ -242,6 +242,36 @@ SAIX_API int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, i
                                 int keep_n, int64_t *out, int64_t *bad, void *ws,
                                 size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------ .saix index files */
+/* save_index / load_index (index_store.py:65-134) fed from device buffers.
+ * Layout (index_store.py:1-14): "SAIX1\0\0\0", u64 version=1, flags, n,
+ * sigma; text (n rank bytes); sa (n x u64); lcp (n x u64); u64 zlib crc32 of
+ * everything above. All integers little-endian. */
+
+SAIX_API size_t saix_crc32_workspace_bytes(int64_t nbytes);
+
+/* zlib.crc32(data[0:nbytes]) of a device buffer into *crc_out (device). */
+SAIX_API int saix_crc32(const void *data, int64_t nbytes, uint32_t *crc_out,
+             void *ws, size_t ws_bytes, void *stream);
+
+/* Size of a .saix file for n positions: 40 + 17n + 8. */
+SAIX_API int64_t saix_index_bytes(int64_t n);
+
+/* Writes the whole file image (saix_index_bytes(n) bytes) into device `out`
+ * (16-byte aligned) from device text ranks / SA / LCP (sigma <= 255; ws >=
+ * saix_crc32_workspace_bytes(0)); the CRC is computed as the image is written. */
+SAIX_API int saix_index_pack(const uint8_t *text, const uint32_t *sa, const uint32_t *lcp,
+             int64_t n, int64_t sigma, int64_t flags, uint8_t *out,
+             void *ws, size_t ws_bytes, void *stream);
+
+/* Verifies the CRC of a device file image whose header (magic, version,
+ * length) the caller has checked; then unpacks text, sa, lcp and the ISA
+ * (isa[sa[i]] = i). SAIX_EINVAL with "checksum mismatch" on a bad CRC, or
+ * "out of range" if an SA/LCP entry does not fit. */
+SAIX_API size_t saix_index_unpack_workspace_bytes(int64_t n);
+SAIX_API int saix_index_unpack(const uint8_t *blob, int64_t n, uint8_t *text, uint32_t *sa,
+             uint32_t *lcp, uint32_t *isa, void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,6 +6,8 @@ Compute runs in libsaix_b200.so (hand-written CUDA, C ABI in
 include/saix_b200.h); PyTorch provides device memory and streams only.
 """
 
+from .index_store import (BadMagicError, ChecksumError, IndexFileError, TruncatedFileError,
+                          UnsupportedVersionError, load_index, save_index)
 from .overlap import (GeneralizedText, LcpQueryEngine, OverlapBatch, OverlapPipeline, OverlapResult,
                       lcp_query, lcp_query_batch, longest_overlap, longest_overlap_batch,
                       overlap_report, pack_pairs, parse_overlap_record)
@@ -21,6 +23,8 @@ from .suffix_index import (Dc3Workspace, LcpArray, SuffixArray, build_lcp, build
 __version__ = "0.1.0"
 
 __all__ = [
+    "BadMagicError", "ChecksumError", "IndexFileError", "TruncatedFileError", "UnsupportedVersionError",
+    "load_index", "save_index",
     "ChunkPlan", "SortConfig", "SplitState", "chunked_sort", "exclusive_scan", "parallel_build_sa",
     "plan_chunks", "radix_sort", "split_by_bit",
     "Dc3Workspace", "DnaSequence", "GeneralizedText", "LcpArray", "LcpQueryEngine",

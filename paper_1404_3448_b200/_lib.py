@@ -82,6 +82,12 @@ SIGNATURES = {
     "saix_split_by_bit": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_radix_sort_i64": (_int, [_vp, _i64, _int, _vp, _vp, _c.c_size_t, _vp]),
     "saix_minmax": (_int, [_vp, _int, _i64, _vp, _vp]),
+    "saix_crc32_workspace_bytes": (_c.c_size_t, [_i64]),
+    "saix_crc32": (_int, [_vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_index_bytes": (_i64, [_i64]),
+    "saix_index_pack": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_index_unpack_workspace_bytes": (_c.c_size_t, [_i64]),
+    "saix_index_unpack": (_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_sparse_plan_make": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),
     "saix_sparse_build": (_int, [_c.POINTER(SparsePlan), _vp, _int, _vp, _vp]),
     "saix_sparse_query": (_int, [_c.POINTER(SparsePlan), _vp, _vp, _int, _vp, _vp, _i64,

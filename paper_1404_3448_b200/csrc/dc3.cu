@@ -794,11 +794,6 @@ struct RsApply {
         return (p.y % 3 == 1) ? make_uint4(p.y, p.z, 0u, p.w) : make_uint4(p.y, 0u, p.z, p.w);
     }
 };
-struct U32Apply {
-    using Out = u32;
-    u32 *out;
-    __device__ __forceinline__ u32 value(const uint2 &p) const { return p.y; }
-};
 
 // mod-0 split source: RS in rank order; mod-1 sample 3j+1 at rank r gives
 // non-sample 3j = {3j, r+1, R(3j+2), T(3j) | T(3j+1) << 8} keyed by T(3j)
@@ -1307,68 +1302,6 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
 //   RB[q] = {3j, R(3j+1), R(3j+2), c0} (+ c1) of the q-th non-sample, from
 //           the bucket-sorted (T(3j), R(3j+1)) keys and RA[R(3j+1) - 1] --
 //           the mod-1 sample 3j+1, whose record holds R(3j+2) and T(3j+1).
-// generic pass A of a u32 scatter dst[idx[i]] = val[i] (val == nullptr: i)
-constexpr int PE_ITEMS = 8;
-__global__ void __launch_bounds__(256)
-k_pairs_emit(const u32 *__restrict__ idx, const u32 *__restrict__ val, i64 n, PsPlan plan, uint2 *__restrict__ stage) {
-    extern __shared__ __align__(16) unsigned char pe_smem[];
-    uint2 *sh_items = reinterpret_cast<uint2 *>(pe_smem);
-    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_items + 256 * PE_ITEMS);
-    u32 *sh_base = sh_cnt + plan.a.buckets;
-    const i64 i0 = (i64)blockIdx.x * (256 * PE_ITEMS);
-    uint2 it[PE_ITEMS];
-    bool ok[PE_ITEMS];
-#pragma unroll
-    for (int q = 0; q < PE_ITEMS; q++) {
-        i64 i = i0 + q * 256 + threadIdx.x;
-        ok[q] = i < n;
-        if (ok[q]) it[q] = make_uint2(__ldcs(idx + i), val ? __ldcs(val + i) : (u32)i);
-    }
-    ps_block_emit<uint2, 256, PE_ITEMS>(it, ok, plan.a, stage, sh_items, sh_cnt, sh_base);
-}
-
-// dst[idx[i]] = val[i] for a permutation-like idx, through the bucketed
-// scatter (small n: direct)
-__global__ void k_scatter_direct(const u32 *__restrict__ idx, const u32 *__restrict__ val, i64 n, u32 *__restrict__ dst) {
-    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
-        dst[idx[i]] = val ? val[i] : (u32)i;
-}
-static int scatter_u32(Arena &ar, const u32 *idx, const u32 *val, i64 n, i64 n_dest, u32 *dst, cudaStream_t st,
-                       const char *prof) {
-    if (n <= 0) return SAIX_OK;
-    if (n < kDirectScatterItems) {
-        Prof prof_(prof, 12.0 * n, st);
-        k_scatter_direct<<<grid_for(n, 256), 256, 0, st>>>(idx, val, n, dst);
-        SAIX_LAUNCHED();
-        return SAIX_OK;
-    }
-    size_t mark = ar.mark();
-    PsPlan pp = PsPlan::of(n_dest, 4);
-    pp.set_cursors(ar.alloc<u32>(pp.cursor_words()));
-    uint2 *s1 = ar.alloc<uint2>(pp.stage1_items()), *s2 = ar.alloc<uint2>(pp.stage2_items());
-    SAIX_ARENA_OK(ar);
-    SAIX_CUDA(cudaMemsetAsync(pp.a.cursor, 0, (size_t)pp.cursor_words() * 4, st));
-    {
-        Prof prof_(prof, 16.0 * n, st);
-        static bool attr = false;
-        if (!attr) {
-            SAIX_CUDA(cudaFuncSetAttribute(k_pairs_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           256 * PE_ITEMS * 8 + 8 * PS_MAX_BUCKETS));
-            attr = true;
-        }
-        size_t smem = (size_t)256 * PE_ITEMS * 8 + 8 * (size_t)pp.a.buckets;
-        k_pairs_emit<<<(unsigned)ceil_div(n, 256 * PE_ITEMS), 256, smem, st>>>(idx, val, n, pp, s1);
-    }
-    SAIX_LAUNCHED();
-    SAIX_TRY(ps_finish(s1, s2, pp, U32Apply{dst}, st, prof, 28.0 * n));
-    ar.reset(mark);
-    return SAIX_OK;
-}
-inline size_t scatter_u32_bytes(i64 n_dest) {
-    PsPlan pp = PsPlan::of(n_dest, 4);
-    return (size_t)(pp.stage1_items() + pp.stage2_items()) * 8 + (size_t)pp.cursor_words() * 4 + 4 * Arena::kAlign;
-}
-
 // RA from a sample order (recursion case / wide naming): chars and the
 // neighbour rank by two random reads per sample
 template <typename TT>

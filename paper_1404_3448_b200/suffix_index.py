@@ -96,6 +96,17 @@ class DeviceText:
             self.bytes = 4
             self.t = _lib.to_device(text.ranks.astype(np.uint32).view(np.int32))
 
+    @classmethod
+    def resident(cls, text: RankedText, t) -> "DeviceText":
+        """Wrap ranks already on the device (u8 when sigma <= 255, else u32)."""
+        self = cls.__new__(cls)
+        self.n = text.n
+        self.sigma = int(text.sigma)
+        self.source = text.ranks
+        self.bytes = 1 if self.sigma <= 255 else 4
+        self.t = t
+        return self
+
 
 def device_text(text: RankedText, cache: Any = None) -> DeviceText:
     if cache is not None and getattr(cache, "text", None) is not None \

@@ -22,3 +22,16 @@ for what in "$@"; do
 done
 # extra: full ncu capture of one launch of kernel K on the C3-size run: tools/gpu_check.sh TAG c3full_K
 # c4full_K: full ncu capture of one launch of kernel K in one C4 wave
+# store: .saix pack / crc / unpack timing at 2^27
+for what in "$@"; do
+  case $what in
+    store) timeout 600 python tools/store_probe.py $((1<<27)) > $O/store.json 2> $O/store.err; cat $O/store.json; tail -3 $O/store.err ;;
+    storetests) timeout 900 python -m pytest tests/test_gpu_index_store.py -x -q > $O/storetests.log 2>&1; tail -15 $O/storetests.log ;;
+    ncu_store) timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/store_launches.csv python tools/store_probe.py $((1<<26)) > $O/ncu_store.log 2>&1; python tools/ncu_summary.py $O/store_launches.csv 20 > $O/store_launches.txt; head -20 $O/store_launches.txt ;;
+  esac
+done
+for what in "$@"; do
+  case $what in
+    storefull_*) K=${what#storefull_}; timeout 600 ncu --set full --import-source on --clock-control none -k regex:$K -c 2 -o $O/storefull_$K python tools/store_probe.py $((1<<26)) > $O/ncu_storefull_$K.log 2>&1; tail -2 $O/ncu_storefull_$K.log ;;
+  esac
+done
