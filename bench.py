@@ -455,7 +455,80 @@ class C4:
                           "GPU answers matched on all of them"}
 
 
-WORKLOADS = {"c2": C2, "c3": C3, "c4": C4, "c5": C5}
+class Store:
+    """.saix save + load round trip (index_store.py:
+    65-134) of a 2^26-base index -- device step: fused pack + CRC-32 of the
+    file image, then CRC check + decode + ISA rebuild from the image; e2e:
+    save_index into a BytesIO and load_index back (host bytes, RMQ rebuild and
+    the reference's int64 host arrays included)."""
+    name = "store"
+    unit = "Mbases/s"
+    N = 1 << 26
+
+    def __init__(self, rank: int):
+        import torch
+        from paper_1404_3448_b200 import _lib, index_store
+        from paper_1404_3448_b200.overlap import LcpQueryEngine
+        from paper_1404_3448_b200.sequence import encode, gen_random
+        from paper_1404_3448_b200.suffix_index import _device_index_of
+        n = self.N
+        self.ist = index_store
+        self.eng = LcpQueryEngine.build(encode(gen_random(n, 21 + rank)))
+        self.L = L = _lib.load()
+        self.ix = _device_index_of(self.eng.text, self.eng.sa)
+        self.lcp = self.eng.lcp._dev[1]
+        total = int(L.saix_index_bytes(n))
+        self.blob = _lib.empty(total, torch.uint8)
+        self.text_d = _lib.empty(n, torch.uint8)
+        self.sa_d, self.lcp_d, self.isa_d = (_lib.empty(n, torch.int32) for _ in range(3))
+        self.ws = _lib.workspace(max(L.saix_crc32_workspace_bytes(total), L.saix_index_unpack_workspace_bytes(n)))
+        self.units = n
+        self.h2d = total
+        self.d2h = total + 13 * n
+        self.step_device()
+        assert bytes(self.blob[-8:].cpu().numpy()) == bytes(self.ist.pack_index(self.eng)[-8:].cpu().numpy())
+        self.result = None
+        self.config = {"workload": "store: .saix save + load of the index of a 2^26-base random ACGT text "
+                                   "(gen_random seed 21 + rank); file image 17n+48 bytes",
+                       "bases": n, "file_bytes": total}
+
+    def step_device(self):
+        from paper_1404_3448_b200 import _lib
+        L, n, s = self.L, self.N, _lib.stream_ptr()
+        _lib.check(L.saix_index_pack(_lib.ptr(self.ix.text.t), _lib.ptr(self.ix.sa), _lib.ptr(self.lcp), n, 4, 0,
+                                     _lib.ptr(self.blob), _lib.ptr(self.ws), self.ws.numel(), s), "saix_index_pack")
+        _lib.check(L.saix_index_unpack(_lib.ptr(self.blob), n, _lib.ptr(self.text_d), _lib.ptr(self.sa_d),
+                                       _lib.ptr(self.lcp_d), _lib.ptr(self.isa_d), _lib.ptr(self.ws),
+                                       self.ws.numel(), s), "saix_index_unpack")
+
+    def step_e2e(self):
+        import io
+        sink = io.BytesIO()
+        self.ist.save_index(self.eng, sink)
+        sink.seek(0)
+        self.loaded = self.ist.load_index(sink)
+
+    def extra(self, ms_dev, steps, world):
+        return {}
+
+    def cpu_baseline(self):
+        import oracle
+        n = 1 << 24
+        text = self.eng.text.ranks[:n]
+        sa, rank = oracle.dc3(text, 4)
+        lcp = oracle.lcp(text, sa, rank)
+        t0 = time.perf_counter()
+        blob = oracle.index_file(text, 4, sa, lcp)
+        _, _, sa2, _, lcp2 = oracle.index_load(blob)
+        oracle.sparse_build(lcp2)
+        dt = time.perf_counter() - t0
+        assert np.array_equal(sa2, sa)
+        return {"value": n / dt / 1e6, "unit": self.unit, "cores": 1, "kind": "port",
+                "sample": f"save (numpy + zlib.crc32) + load (crc check, int64 arrays, rank scatter, sparse-table "
+                          f"RMQ rebuild) of a 2^24-base index, single thread ({dt:.1f} s)"}
+
+
+WORKLOADS = {"c2": C2, "c3": C3, "c4": C4, "c5": C5, "store": Store}
 
 
 def run_reference(args, rank):

@@ -178,6 +178,11 @@ typedef struct saix_sparse_plan {
  * LCP array) be planned without copying it to the host. */
 SAIX_API int saix_minmax(const void *values, int value_bytes, int64_t n, int64_t *out2, void *stream);
 
+/* dst[i] = (int64)src[i] for a u8 (src_bytes 1) or u32 (4) device array: the
+ * reference API's int64 host arrays are widened on the device before the
+ * download. */
+SAIX_API int saix_widen_i64(const void *src, int src_bytes, int64_t n, int64_t *dst, void *stream);
+
 /* Choose the table layout for n values in [vmin, vmax]. */
 SAIX_API int saix_sparse_plan_make(int64_t n, int64_t vmin, int64_t vmax,
                           saix_sparse_plan *plan);

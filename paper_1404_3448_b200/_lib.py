@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import warnings
 
 import numpy as np
 
@@ -82,6 +83,7 @@ SIGNATURES = {
     "saix_split_by_bit": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_radix_sort_i64": (_int, [_vp, _i64, _int, _vp, _vp, _c.c_size_t, _vp]),
     "saix_minmax": (_int, [_vp, _int, _i64, _vp, _vp]),
+    "saix_widen_i64": (_int, [_vp, _int, _i64, _vp, _vp]),
     "saix_crc32_workspace_bytes": (_c.c_size_t, [_i64]),
     "saix_crc32": (_int, [_vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
     "saix_index_bytes": (_i64, [_i64]),
@@ -184,7 +186,13 @@ def workspace(nbytes: int):
 def to_device(arr: np.ndarray, dev=None):
     """Host numpy -> device tensor (pinned staging for large arrays)."""
     t = torch()
-    h = t.from_numpy(np.ascontiguousarray(arr))
+    arr = np.ascontiguousarray(arr)
+    if not arr.flags.writeable:   # read-only host data (e.g. file bytes): only ever copied from
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            h = t.from_numpy(arr)
+    else:
+        h = t.from_numpy(arr)
     if h.numel() == 0:
         return t.empty(1, dtype=h.dtype, device=dev or device())
     return h.to(dev or device(), non_blocking=False)
@@ -200,11 +208,40 @@ def to_host(t_dev, n: int | None = None, dtype=np.int64) -> np.ndarray:
     return a.astype(dtype, copy=False) if a.dtype != dtype else a
 
 
-def u32_to_i64_host(t_dev, n: int) -> np.ndarray:
-    """u32 device array (stored in an int32 tensor) -> host int64."""
+def widen_i64_host(t_dev, n: int) -> np.ndarray:
+    """u8 / u32 device array (uint8 / int32 tensor) -> host int64, widened on
+    the device (saix_widen_i64) so the download is the only host work."""
     if n == 0:
         return np.zeros(0, np.int64)
-    return t_dev[:n].cpu().numpy().view(np.uint32).astype(np.int64)
+    t = torch()
+    src_bytes = 1 if t_dev.dtype == t.uint8 else 4
+    out = t.empty(n, dtype=t.int64, device=t_dev.device)
+    check(load().saix_widen_i64(ptr(t_dev), src_bytes, n, ptr(out), stream_ptr()), "saix_widen_i64")
+    host = t.empty(n, dtype=t.int64, pin_memory=True)   # torch caches pinned blocks across calls
+    host.copy_(out)
+    return host.numpy()
+
+
+_staging = {}
+
+
+def staging(nbytes: int):
+    """A reusable pinned host uint8 buffer of at least nbytes (grown in powers
+    of two): file images pass through it at full PCIe / C2C speed instead of
+    page-faulting into fresh pageable memory."""
+    t = torch()
+    buf = _staging.get("b")
+    if buf is None or buf.numel() < nbytes:
+        size = 1 << max(20, (int(nbytes) - 1).bit_length())
+        _staging.pop("b", None)
+        buf = t.empty(size, dtype=t.uint8, pin_memory=True)
+        _staging["b"] = buf
+    return buf
+
+
+def u32_to_i64_host(t_dev, n: int) -> np.ndarray:
+    """u32 device array (stored in an int32 tensor) -> host int64."""
+    return widen_i64_host(t_dev, n)
 
 
 def prof_enable(on: bool = True) -> None:

@@ -153,19 +153,49 @@ __global__ void k_minmax(Vals<V> val, i64 n, i64 *out2) {
     }
 }
 
+// u8 / u32 device arrays -> int64 (the reference API's host array dtype),
+// four items per thread with 128-bit stores
+template <typename V>
+__global__ void k_widen_i64(const V *__restrict__ src, i64 n, i64 *__restrict__ dst) {
+    for (i64 i = 4 * ((i64)blockIdx.x * blockDim.x + threadIdx.x); i < n; i += 4 * (i64)gridDim.x * blockDim.x) {
+        if (i + 4 <= n && ((reinterpret_cast<uintptr_t>(dst + i) & 15) == 0)) {
+            i64 a = (i64)src[i], b = (i64)src[i + 1], c = (i64)src[i + 2], d = (i64)src[i + 3];
+            __stcs(reinterpret_cast<longlong2 *>(dst + i), make_longlong2(a, b));
+            __stcs(reinterpret_cast<longlong2 *>(dst + i + 2), make_longlong2(c, d));
+        } else {
+            for (i64 k = i; k < n && k < i + 4; k++) dst[k] = (i64)src[k];
+        }
+    }
+}
+
 }  // namespace saix
 
 using namespace saix;
 
+extern "C" int saix_widen_i64(const void *src, int src_bytes, int64_t n, int64_t *dst, void *stream) {
+    if (n < 0 || (n > 0 && (!src || !dst)) || (src_bytes != 1 && src_bytes != 4)) {
+        set_error("saix_widen_i64: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    if (n == 0) return SAIX_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int g = grid_for(ceil_div(n, 4), 256);
+    if (src_bytes == 1) k_widen_i64<u8><<<g, 256, 0, st>>>((const u8 *)src, n, dst);
+    else k_widen_i64<u32><<<g, 256, 0, st>>>((const u32 *)src, n, dst);
+    SAIX_LAUNCHED();
+    return SAIX_OK;
+}
+
 extern "C" int saix_minmax(const void *values, int value_bytes, int64_t n, int64_t *out2, void *stream) {
-    if (!values || !out2 || n <= 0 || (value_bytes != 4 && value_bytes != 8)) {
+    if (!values || !out2 || n <= 0 || (value_bytes != 1 && value_bytes != 4 && value_bytes != 8)) {
         set_error("saix_minmax: invalid arguments");
         return SAIX_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;
     k_minmax_init<<<1, 1, 0, st>>>(out2);
     int g = grid_for(n, 256, kNumSMs * 8);
-    if (value_bytes == 4) k_minmax<u32><<<g, 256, 0, st>>>(Vals<u32>{(const u32 *)values}, n, out2);
+    if (value_bytes == 1) k_minmax<u8><<<g, 256, 0, st>>>(Vals<u8>{(const u8 *)values}, n, out2);
+    else if (value_bytes == 4) k_minmax<u32><<<g, 256, 0, st>>>(Vals<u32>{(const u32 *)values}, n, out2);
     else k_minmax<i64><<<g, 256, 0, st>>>(Vals<i64>{(const i64 *)values}, n, out2);
     SAIX_LAUNCHED();
     return SAIX_OK;

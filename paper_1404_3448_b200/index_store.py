@@ -99,30 +99,73 @@ def pack_index(engine: LcpQueryEngine):
 def save_index(engine: LcpQueryEngine, destination: str | Path | BinaryIO) -> int:
     """Write an engine's text, suffix array, and lcp array; returns bytes
     written (index_store.py:65-88)."""
-    blob = pack_index(engine).cpu().numpy().tobytes()
+    image_d = pack_index(engine)
+    total = int(image_d.shape[0])
+    host = _lib.staging(total)
+    host[:total].copy_(image_d)
     sink, owned = _open_sink(destination)
     try:
-        sink.write(blob)
+        sink.write(memoryview(host.numpy())[:total])
     finally:
         if owned:
             sink.close()
-    return len(blob)
+    return total
 
 
-def _check_header(blob: bytes) -> int:
-    """index_store.py:99-116: the reference's header checks, in its order;
-    returns n."""
-    if len(blob) < _HEADER + _U64.size:
-        raise TruncatedFileError(f"file is {len(blob)} bytes; shorter than any valid index")
-    if blob[:len(MAGIC)] != MAGIC:
-        raise BadMagicError(f"bad magic {blob[:len(MAGIC)]!r}")
-    version, _flags, n, _sigma = (_U64.unpack_from(blob, len(MAGIC) + k * _U64.size)[0] for k in range(4))
+def _check_prefix(head) -> int:
+    """index_store.py:99-112: the reference's checks on the first 48 bytes
+    (length, magic, version), in its order; returns n."""
+    if len(head) < _HEADER + _U64.size:
+        raise TruncatedFileError(f"file is {len(head)} bytes; shorter than any valid index")
+    if bytes(head[:len(MAGIC)]) != MAGIC:
+        raise BadMagicError(f"bad magic {bytes(head[:len(MAGIC)])!r}")
+    version, _flags, n, _sigma = (_U64.unpack_from(head, len(MAGIC) + k * _U64.size)[0] for k in range(4))
     if version != VERSION:
         raise UnsupportedVersionError(f"unsupported version {version}")
+    return int(n)
+
+
+def _check_header(blob) -> int:
+    """index_store.py:99-116: prefix checks, then the length n implies."""
+    n = _check_prefix(blob)
     expected = _HEADER + n + 2 * 8 * n + _U64.size
     if len(blob) < expected:
         raise TruncatedFileError(f"file is {len(blob)} bytes; need {expected} for n={n}")
-    return int(n)
+    return n
+
+
+def _read_image(fh):
+    """The file image from a binary stream -- read straight into the pinned
+    staging buffer when the stream supports readinto (else fh.read()), with
+    the reference's checks on what was read.  Returns a bytes-like image of
+    exactly the checked length."""
+    seekable = hasattr(fh, "readinto") and hasattr(fh, "seekable") and fh.seekable()
+    if not seekable:
+        blob = fh.read()
+        n = _check_header(blob)
+        return memoryview(blob)[:_HEADER + 17 * n + _U64.size]
+    head = fh.read(_HEADER + _U64.size)
+    n = _check_prefix(head)
+    total = _HEADER + 17 * n + _U64.size
+    here = fh.tell()
+    size = fh.seek(0, 2) - here + len(head)
+    fh.seek(here)
+    if size < total:  # checked before any buffer is sized from the header's n
+        fh.read()
+        raise TruncatedFileError(f"file is {size} bytes; need {total} for n={n}")
+    buf = _lib.staging(total)
+    view = memoryview(buf.numpy())[:total]
+    view[:len(head)] = head
+    got = len(head)
+    while got < total:
+        k = fh.readinto(view[got:])
+        if not k:
+            break
+        got += k
+    if got < total:
+        raise TruncatedFileError(f"file is {got} bytes; need {total} for n={n}")
+    fh.read()  # the reference consumes the whole stream; trailing bytes are ignored
+    return view
 
 
 def unpack_index(blob, rmq_kind: RmqKind = "sparse") -> LcpQueryEngine:
@@ -133,8 +176,7 @@ def unpack_index(blob, rmq_kind: RmqKind = "sparse") -> LcpQueryEngine:
     t = _lib.torch()
     L = _lib.load()
     payload = _HEADER + 17 * n
-    host = np.frombuffer(blob, dtype=np.uint8, count=payload + _U64.size)
-    dev_blob = _lib.to_device(host)
+    dev_blob = _lib.to_device(np.frombuffer(blob, dtype=np.uint8, count=payload + _U64.size))
     text_d = _lib.empty(n, t.uint8)
     sa_d, lcp_d, isa_d = (_lib.empty(n, t.int32) for _ in range(3))
     ws = _ws(L.saix_index_unpack_workspace_bytes(n))
@@ -147,14 +189,20 @@ def unpack_index(blob, rmq_kind: RmqKind = "sparse") -> LcpQueryEngine:
         if "out of range" in msg:
             raise IndexError(f"index entries out of range for n={n}")
         _lib.check(rc, "saix_index_unpack")
-    ranks = text_d[:n].cpu().numpy().astype(np.int64) if n else np.zeros(0, np.int64)
-    text = RankedText(ranks=ranks, sigma=int(sigma))
+    if n:
+        # RankedText's 1..sigma check (sequence.py:55-62), on the device
+        mm = t.empty(2, dtype=t.int64, device=text_d.device)
+        _lib.check(L.saix_minmax(_lib.ptr(text_d), 1, n, _lib.ptr(mm), _lib.stream_ptr()), "saix_minmax")
+        lo, hi = (int(x) for x in mm.cpu().tolist())
+        if lo < 1 or hi > sigma:
+            raise ValueError("ranks must lie in 1..sigma")
+    text = RankedText._checked(_lib.widen_i64_host(text_d, n), int(sigma))
     dt = DeviceText.resident(text, text_d)
     ix = DeviceIndex(dt, sa_d, isa_d)
-    sa = _lib.u32_to_i64_host(sa_d, n)
-    rank = _lib.u32_to_i64_host(isa_d, n) if n else sa.copy()
+    sa = _lib.widen_i64_host(sa_d, n)
+    rank = _lib.widen_i64_host(isa_d, n) if n else sa.copy()
     sa_struct = SuffixArray(n=n, sa=sa, rank=rank, _dev=ix)
-    lcp = LcpArray(_lib.u32_to_i64_host(lcp_d, n), _dev=(ix, lcp_d))
+    lcp = LcpArray(_lib.widen_i64_host(lcp_d, n), _dev=(ix, lcp_d))
     return LcpQueryEngine.from_parts(text, sa_struct, lcp, rmq_kind)
 
 
@@ -163,7 +211,7 @@ def load_index(source: str | Path | BinaryIO, rmq_kind: RmqKind = "sparse") -> L
     (index_store.py:91-134)."""
     if isinstance(source, (str, Path)):
         with open(source, "rb") as fh:
-            blob = fh.read()
+            image = _read_image(fh)
     else:
-        blob = source.read()
-    return unpack_index(blob, rmq_kind)
+        image = _read_image(source)
+    return unpack_index(image, rmq_kind)

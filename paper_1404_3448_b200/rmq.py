@@ -33,9 +33,16 @@ class SparseTable:
         self.values = values
         n = int(values.shape[0])
         L = _lib.load()
+        if _device_values is not None:          # plan from a device min / max, no host pass
+            t = _lib.torch()
+            mm = t.empty(2, dtype=t.int64, device=_device_values[0].device)
+            _lib.check(L.saix_minmax(_lib.ptr(_device_values[0]), _device_values[1], n, _lib.ptr(mm),
+                                     _lib.stream_ptr()), "saix_minmax")
+            vmin, vmax = (int(x) for x in mm.cpu().tolist())
+        else:
+            vmin, vmax = int(values.min()), int(values.max())
         plan = _lib.SparsePlan()
-        _lib.check(L.saix_sparse_plan_make(n, int(values.min()), int(values.max()),
-                                           ctypes.byref(plan)), "saix_sparse_plan_make")
+        _lib.check(L.saix_sparse_plan_make(n, vmin, vmax, ctypes.byref(plan)), "saix_sparse_plan_make")
         self.plan = plan
         _lib.device()
         t = _lib.torch()

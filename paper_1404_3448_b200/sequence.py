@@ -60,6 +60,17 @@ class RankedText:
         if r.shape[0] and (int(r.min()) < 1 or int(r.max()) > self.sigma):
             raise ValueError("ranks must lie in 1..sigma")
 
+    @classmethod
+    def _checked(cls, ranks: np.ndarray, sigma: int) -> "RankedText":
+        """Construct from int64 ranks already range-checked (on the device)."""
+        self = cls.__new__(cls)
+        r = np.asarray(ranks, dtype=np.int64)
+        r.flags.writeable = False
+        object.__setattr__(self, "ranks", r)
+        object.__setattr__(self, "sigma", int(sigma))
+        object.__setattr__(self, "n", int(r.shape[0]))
+        return self
+
     def __len__(self) -> int:
         return self.n
 

@@ -209,3 +209,32 @@ def test_large_roundtrip(n):
     assert np.array_equal(loaded.sa.rank, eng.sa.rank)
     assert np.array_equal(loaded.lcp.lcp, eng.lcp.lcp)
     assert np.array_equal(np.frombuffer(blob, "<u8", n, 40 + 9 * n).astype(np.int64), eng.lcp.lcp)
+
+
+def _recrc(blob: bytearray) -> bytes:
+    blob[-8:] = zlib.crc32(bytes(blob[:-8])).to_bytes(8, "little")
+    return bytes(blob)
+
+
+def test_crafted_bad_rank_rejected():
+    blob = bytearray(saved_bytes(engine_for("ACGTACGT")))
+    blob[41] = 0  # rank 0 with a valid checksum
+    with pytest.raises(ValueError):
+        index_store.load_index(io.BytesIO(_recrc(blob)))
+
+
+def test_crafted_sa_out_of_range_rejected():
+    blob = bytearray(saved_bytes(engine_for("ACGTACGT")))
+    blob[48:56] = (99).to_bytes(8, "little")  # sa[0] = 99 >= n
+    with pytest.raises(IndexError):
+        index_store.load_index(io.BytesIO(_recrc(blob)))
+
+
+def test_widen_matches_host():
+    t = _lib.torch()
+    rng = np.random.default_rng(5)
+    for n in (1, 3, 4, 5, 1000, 1 << 20):
+        a = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        assert np.array_equal(_lib.widen_i64_host(_lib.to_device(a.view(np.int32)), n), a.astype(np.int64))
+        b = rng.integers(0, 256, n, dtype=np.uint8)
+        assert np.array_equal(_lib.widen_i64_host(_lib.to_device(b), n), b.astype(np.int64))

@@ -100,3 +100,16 @@ def test_path_errors(tmp_path, blobs):
     p.write_bytes(b"SAIX0" + bytes(50))
     with pytest.raises(index_store.BadMagicError):
         index_store.load_index(p)
+
+
+def test_oracle_index_load_roundtrip(blobs):
+    for s, keep, blob in blobs:
+        ranks, sigma, sa, rank, lcp = oracle.index_load(blob)
+        assert ranks.tolist() == oracle.dna_ranks(s, keep).tolist()
+        assert oracle.index_file(ranks, sigma, sa, lcp) == blob
+        if len(s):
+            assert rank[sa].tolist() == list(range(len(s)))
+    bad = bytearray(blobs[3][2])
+    bad[45] ^= 4
+    with pytest.raises(ValueError):
+        oracle.index_load(bytes(bad))
