@@ -528,7 +528,69 @@ class Store:
                           f"RMQ rebuild) of a 2^24-base index, single thread ({dt:.1f} s)"}
 
 
-WORKLOADS = {"c2": C2, "c3": C3, "c4": C4, "c5": C5, "store": Store}
+class Fasta:
+    """FASTA ingest (sequence.py:77-157 parse_fasta +
+    encode) of a 2^28-base synthetic FASTA (60-column lines, mixed case,
+    ~256 records) -- device step: line split, strip, classify, validate,
+    concatenate and rank-encode the file bytes resident in HBM; e2e:
+    ingest_fasta(bytes) from host memory (H2D of the file inside)."""
+    name = "fasta"
+    unit = "Mbases/s"
+    N = 1 << 28
+
+    def __init__(self, rank: int):
+        import torch
+        from paper_1404_3448_b200 import _lib
+        from paper_1404_3448_b200.fasta import ingest_fasta
+        rng = np.random.default_rng(31 + rank)
+        lut = np.frombuffer(b"ACGTacgt", np.uint8)
+        recs, left, k = [], self.N, 0
+        while left > 0:
+            m = min(left, 1 << 20)
+            seq = lut[rng.integers(0, 8, m)]
+            lines = seq[: (m // 60) * 60].reshape(-1, 60)
+            body = np.concatenate([lines, np.full((lines.shape[0], 1), 10, np.uint8)], axis=1).ravel().tobytes()
+            tail = seq[(m // 60) * 60:].tobytes()
+            recs.append(b">chr%d synthetic record %d\n" % (k, k) + body + (tail + b"\n" if tail else b""))
+            left -= m
+            k += 1
+        self.data = b"".join(recs)
+        self.dev = _lib.to_device(np.frombuffer(self.data, np.uint8))
+        self.ingest = ingest_fasta
+        fi = ingest_fasta(self.dev)
+        assert fi.total_residues == self.N and len(fi) == k
+        self.result = None
+        self.units = self.N
+        self.h2d = len(self.data)
+        self.d2h = 8 * (k + 1) * 2 + sum(len(b">chr%d synthetic record %d" % (i, i)) for i in range(k))
+        self.config = {"workload": f"fasta: 2^28-base synthetic FASTA ({len(self.data)} bytes, {k} records, "
+                                   "60-column lines, 50% lower case; seed 31 + rank), parse + validate + "
+                                   "rank-encode per step", "bases": self.N, "file_bytes": len(self.data)}
+
+    def step_device(self):
+        self.ingest(self.dev)
+
+    def step_e2e(self):
+        self.ingest(self.data)
+
+    def extra(self, ms_dev, steps, world):
+        return {"file_GBps": round(len(self.data) * steps / (ms_dev * 1e-3) / 1e9, 1)}
+
+    def cpu_baseline(self):
+        import oracle
+        sample = self.data[: 1 << 26]
+        sample = sample[: sample.rfind(b"\n") + 1]
+        t0 = time.perf_counter()
+        recs, err = oracle.fasta(sample, as_ranks=True)
+        dt = time.perf_counter() - t0
+        assert err is None
+        nb = sum(len(r[1]) for r in recs)
+        return {"value": nb / dt / 1e6, "unit": self.unit, "cores": 1, "kind": "port",
+                "sample": f"first 64 MiB of the file ({nb} bases), oracle_fasta (C restatement of parse_fasta + "
+                          f"encode), single thread ({dt:.2f} s)"}
+
+
+WORKLOADS = {"c2": C2, "c3": C3, "c4": C4, "c5": C5, "store": Store, "fasta": Fasta}
 
 
 def run_reference(args, rank):

@@ -247,6 +247,24 @@ SAIX_API int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, i
                                 int keep_n, int64_t *out, int64_t *bad, void *ws,
                                 size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------ FASTA ingest */
+/* parse_fasta (sequence.py:77-125) + encode (sequence.py:144-157) over raw
+ * FASTA bytes in device memory (inputs < 4 GiB), with the reference's
+ * semantics for a str source: lines end at '\n', each line str.strip()-ed,
+ * blank lines skipped, '>' lines open records (header stripped again),
+ * sequence lines upper-cased and validated against ACGT (+N when keep_n).
+ * Three calls: saix_fasta_lines (line count, sizes the workspace),
+ * saix_fasta_scan (line table + counts; the workspace carries it), and
+ * saix_fasta_emit (residues, record starts, header texts, first error). */
+SAIX_API int saix_fasta_lines(const uint8_t *data, int64_t nbytes, int64_t *lines_host, void *ws,
+             size_t ws_bytes, void *stream);
+SAIX_API size_t saix_fasta_workspace_bytes(int64_t nbytes, int64_t lines);
+SAIX_API int saix_fasta_scan(const uint8_t *data, int64_t nbytes, int64_t lines, int64_t *counts_host,
+             void *ws, size_t ws_bytes, void *stream);
+SAIX_API int saix_fasta_emit(const uint8_t *data, int64_t nbytes, int64_t lines, int keep_n, int as_ranks,
+             uint8_t *res, uint32_t *rec_start, uint8_t *hdr, uint32_t *hdr_off, int64_t *err_host,
+             void *ws, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------ .saix index files */
 /* save_index / load_index (index_store.py:65-134) fed from device buffers.
  * Layout (index_store.py:1-14): "SAIX1\0\0\0", u64 version=1, flags, n,

@@ -465,3 +465,69 @@ EXPORT int64_t oracle_overlap_batch(const uint8_t *seqs, const int64_t *offs,
     }
     return st;
 }
+
+/* ------------------------------------------------------------------ FASTA */
+/* parse_fasta (sequence.py:77-125) for a str source, followed by encode
+ * (sequence.py:144-157) when as_ranks: io.StringIO yields lines ending at
+ * '\n'; each line is str.strip()-ed (ASCII whitespace \t\n\v\f\r, \x1c-\x1f,
+ * space); blank lines skipped; '>' opens a record (header = rest, stripped);
+ * other lines need a header first, are upper-cased and every char must be in
+ * ACGT (+N).  The loop stops at the first error like the reference's raise.
+ * Outputs: res (residues, <= B bytes), rec_start[r] (residue offset of record
+ * r; rec_start[nrec] = total), hdr_start / hdr_len (header text in d),
+ * counts = {residues, records}; err = {pos, line (0-based), kind (1 empty
+ * header, 2 sequence line), line start, headers before} or err[0] = -1. */
+static int fa_ws(uint8_t c) { return c == 32 || (c >= 9 && c <= 13) || (c >= 28 && c <= 31); }
+
+EXPORT int oracle_fasta(const uint8_t *d, int64_t B, int keep_n, int as_ranks, uint8_t *res,
+                        int64_t *rec_start, int64_t *hdr_start, int64_t *hdr_len, int64_t *counts,
+                        int64_t *err) {
+    int64_t nres = 0, nrec = 0, line = 0, s = 0;
+    err[0] = -1;
+    while (s < B) {
+        int64_t e = s;
+        while (e < B && d[e] != '\n') e++;
+        int64_t next = e < B ? e + 1 : B;
+        int64_t a = s, z = e;
+        while (a < z && fa_ws(d[a])) a++;
+        while (z > a && fa_ws(d[z - 1])) z--;
+        if (a < z) {
+            if (d[a] == '>') {
+                int64_t h = a + 1;
+                while (h < z && fa_ws(d[h])) h++;
+                if (h == z) {
+                    err[0] = a; err[1] = line; err[2] = 1; err[3] = a; err[4] = nrec;
+                    break;
+                }
+                rec_start[nrec] = nres;
+                hdr_start[nrec] = h;
+                hdr_len[nrec] = z - h;
+                nrec++;
+            } else {
+                if (nrec == 0) {
+                    err[0] = a; err[1] = line; err[2] = 2; err[3] = a; err[4] = 0;
+                    break;
+                }
+                int bad = 0;
+                for (int64_t j = a; j < z; j++) {
+                    uint8_t u = d[j];
+                    if (u >= 'a' && u <= 'z') u -= 32;
+                    int r = u == 'A' ? 1 : u == 'C' ? 2 : u == 'G' ? 3 : u == 'T' ? 4 : (u == 'N' && keep_n) ? 5 : 0;
+                    if (!r) {
+                        err[0] = j; err[1] = line; err[2] = 2; err[3] = a; err[4] = nrec;
+                        bad = 1;
+                        break;
+                    }
+                    res[nres++] = as_ranks ? (uint8_t)r : u;
+                }
+                if (bad) break;
+            }
+        }
+        line++;
+        s = next;
+    }
+    rec_start[nrec] = nres;
+    counts[0] = nres;
+    counts[1] = nrec;
+    return err[0] >= 0;
+}

@@ -6,6 +6,7 @@ Compute runs in libsaix_b200.so (hand-written CUDA, C ABI in
 include/saix_b200.h); PyTorch provides device memory and streams only.
 """
 
+from .fasta import FastaIngest, ingest_fasta
 from .index_store import (BadMagicError, ChecksumError, IndexFileError, TruncatedFileError,
                           UnsupportedVersionError, load_index, save_index)
 from .overlap import (GeneralizedText, LcpQueryEngine, OverlapBatch, OverlapPipeline, OverlapResult,
@@ -24,7 +25,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BadMagicError", "ChecksumError", "IndexFileError", "TruncatedFileError", "UnsupportedVersionError",
-    "load_index", "save_index",
+    "load_index", "save_index", "FastaIngest", "ingest_fasta",
     "ChunkPlan", "SortConfig", "SplitState", "chunked_sort", "exclusive_scan", "parallel_build_sa",
     "plan_chunks", "radix_sort", "split_by_bit",
     "Dc3Workspace", "DnaSequence", "GeneralizedText", "LcpArray", "LcpQueryEngine",

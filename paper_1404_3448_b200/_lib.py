@@ -84,6 +84,10 @@ SIGNATURES = {
     "saix_radix_sort_i64": (_int, [_vp, _i64, _int, _vp, _vp, _c.c_size_t, _vp]),
     "saix_minmax": (_int, [_vp, _int, _i64, _vp, _vp]),
     "saix_widen_i64": (_int, [_vp, _int, _i64, _vp, _vp]),
+    "saix_fasta_lines": (_int, [_vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_fasta_workspace_bytes": (_c.c_size_t, [_i64, _i64]),
+    "saix_fasta_scan": (_int, [_vp, _i64, _i64, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_fasta_emit": (_int, [_vp, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_crc32_workspace_bytes": (_c.c_size_t, [_i64]),
     "saix_crc32": (_int, [_vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
     "saix_index_bytes": (_i64, [_i64]),

@@ -198,6 +198,7 @@ def unpack_index(blob, rmq_kind: RmqKind = "sparse") -> LcpQueryEngine:
             raise ValueError("ranks must lie in 1..sigma")
     text = RankedText._checked(_lib.widen_i64_host(text_d, n), int(sigma))
     dt = DeviceText.resident(text, text_d)
+    object.__setattr__(text, "_dev", dt)
     ix = DeviceIndex(dt, sa_d, isa_d)
     sa = _lib.widen_i64_host(sa_d, n)
     rank = _lib.widen_i64_host(isa_d, n) if n else sa.copy()

@@ -50,6 +50,7 @@ class RankedText:
     ranks: np.ndarray
     sigma: int
     n: int = field(default=-1)
+    _dev: object = field(default=None, repr=False, compare=False)  # resident DeviceText, if any
 
     def __post_init__(self):
         r = np.asarray(self.ranks, dtype=np.int64)
@@ -69,6 +70,7 @@ class RankedText:
         object.__setattr__(self, "ranks", r)
         object.__setattr__(self, "sigma", int(sigma))
         object.__setattr__(self, "n", int(r.shape[0]))
+        object.__setattr__(self, "_dev", None)
         return self
 
     def __len__(self) -> int:
@@ -138,7 +140,15 @@ def gen_random(n: int, seed: int,
 
 def parse_fasta(source: str | IO[str] | Iterable[str],
                 policy: NPolicy = NPolicy.REJECT) -> list[DnaSequence]:
-    """FASTA -> records with residue validation (sequence.py:77-125)."""
+    """FASTA -> records with residue validation (sequence.py:77-125).
+
+    An ASCII ``str`` source is parsed on the device (``fasta.ingest_fasta``:
+    line split, strip, classify, upper-case, validate, concatenate); text
+    streams and line iterables keep the reference's line-by-line loop here
+    (their universal-newline line splitting is the stream's own)."""
+    if isinstance(source, str) and source.isascii():
+        from .fasta import ingest_fasta
+        return ingest_fasta(source, policy, as_ranks=False).records()
     lines = io.StringIO(source) if isinstance(source, str) else source
     ok = set(alphabet(policy))
     out: list[DnaSequence] = []

@@ -109,6 +109,9 @@ class DeviceText:
 
 
 def device_text(text: RankedText, cache: Any = None) -> DeviceText:
+    resident = getattr(text, "_dev", None)
+    if resident is not None and resident.source is text.ranks:
+        return resident
     if cache is not None and getattr(cache, "text", None) is not None \
             and cache.text.source is text.ranks:
         return cache.text
@@ -172,7 +175,7 @@ def build_sa_dc3(text: RankedText, sort_by_keys: SortByKeys | None = None) -> Su
     if n == 0:
         return SuffixArray(n=0, sa=np.zeros(0, np.int64), rank=np.zeros(0, np.int64))
     _lib.device()
-    ix = dc3_device(DeviceText(text))
+    ix = dc3_device(device_text(text))
     return SuffixArray(n=n, sa=_lib.u32_to_i64_host(ix.sa, n),
                        rank=_lib.u32_to_i64_host(ix.isa, n), _dev=ix)
 
@@ -224,7 +227,7 @@ def _probe_run(text: RankedText):
     }
     probe = _lib.Dc3Probe(*[_lib.ptr(bufs[k_]) for k_ in
                             ("triple_text", "sample_rank", "sorted_samples", "sorted_nonsamples")])
-    ix = dc3_device(DeviceText(text), probe)
+    ix = dc3_device(device_text(text), probe)
 
     def host(name, count):
         if count == 0:
@@ -289,7 +292,7 @@ def merge_sample_nonsample(workspace: Dc3Workspace, text: RankedText) -> SuffixA
     _lib.device()
     t = _lib.torch()
     L = _lib.load()
-    dt = DeviceText(text)
+    dt = device_text(text)
     rank = _lib.to_device(np.asarray(workspace.sample_rank).astype(np.uint32).view(np.int32))
     a = _lib.to_device(ss.astype(np.uint32).view(np.int32))
     b = _lib.to_device(sn.astype(np.uint32).view(np.int32))
