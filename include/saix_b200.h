@@ -247,6 +247,38 @@ SAIX_API int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, i
                                 int keep_n, int64_t *out, int64_t *bad, void *ws,
                                 size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------ Cartesian tree / ±1 RMQ */
+/* build_cartesian + euler_tour (rmq.py:91-152) on the device: parent, left,
+ * right (-1 = none), the 2n-1 tour nodes / depths and first_visit (int32),
+ * *root_host = the leftmost minimum.  values: n entries of value_bytes 4
+ * (u32) or 8 (int64), n < 2^30. */
+SAIX_API size_t saix_cartesian_workspace_bytes(int64_t n);
+SAIX_API int saix_cartesian_build(const void *values, int value_bytes, int64_t n, int32_t *parent,
+             int32_t *left, int32_t *right, int32_t *tour_nodes, int32_t *tour_depths,
+             int32_t *first_visit, int64_t *root_host, void *ws, size_t ws_bytes, void *stream);
+
+/* PlusMinusOneRmq.__init__ (rmq.py:167-197) minus the block-minimum sparse
+ * table (built with saix_sparse_build over bmin): block size b (1..16),
+ * nblocks = ceil(m/b) leftmost argmins / minima / step codes, the in-block
+ * tables tab[code][i][j] (u8, 2^(b-1) codes) of the codes present; present
+ * holds ceil(2^(b-1)/32) + 1 words; *bad_host = 1 on a non-unit step. */
+SAIX_API int saix_pm1_build(const int32_t *depths, int64_t m, int b, int32_t *bargmin, int32_t *bmin,
+             int32_t *types, uint32_t *present, uint8_t *tab, int32_t *bad_host, void *stream);
+
+/* PlusMinusOneRmq.query / CartesianRmq.query (rmq.py:219-251), batched in two
+ * halves around a saix_sparse_query over the block minima:
+ * begin -> (mid_lo, mid_hi) block ranges ((0, 0) when unused) and three ints
+ * per query in cand (left candidate, right candidate or -1, has-middle);
+ * saix_sparse_query(mid_lo, mid_hi) -> mid_blk; end -> out[t] (tour
+ * position, or the node when `nodes` is given; `first` maps array positions
+ * to tour positions). */
+SAIX_API int saix_pm1_query_begin(int b, const int32_t *types, const uint8_t *tab, const int32_t *first,
+             const int64_t *qi, const int64_t *qj, int64_t q, int64_t *mid_lo, int64_t *mid_hi,
+             int32_t *cand, void *stream);
+SAIX_API int saix_pm1_query_end(const int32_t *depths, int b, const int32_t *bargmin,
+             const int64_t *mid_blk, const int32_t *cand, const int32_t *nodes, int64_t q,
+             int64_t *out, void *stream);
+
 /* ------------------------------------------------------------ FASTA ingest */
 /* parse_fasta (sequence.py:77-125) + encode (sequence.py:144-157) over raw
  * FASTA bytes in device memory (inputs < 4 GiB), with the reference's

@@ -531,3 +531,61 @@ EXPORT int oracle_fasta(const uint8_t *d, int64_t B, int keep_n, int as_ranks, u
     counts[1] = nrec;
     return err[0] >= 0;
 }
+
+/* --------------------------------------------------- Cartesian tree / tour */
+/* build_cartesian (rmq.py:91-117: rightmost-spine stack, pop while the top is
+ * greater) and euler_tour (rmq.py:120-152: iterative DFS emitting a node on
+ * entry and after each child returns). */
+EXPORT int oracle_cartesian(const int64_t *v, int64_t n, int64_t *parent, int64_t *left, int64_t *right,
+                            int64_t *root, int64_t *nodes, int64_t *depths, int64_t *first) {
+    if (n <= 0) return -1;
+    int64_t *stack = (int64_t *)xcalloc((size_t)n, sizeof(int64_t));
+    int64_t top = 0;
+    for (int64_t i = 0; i < n; i++) {
+        parent[i] = left[i] = right[i] = -1;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        int64_t last = -1;
+        while (top > 0 && v[stack[top - 1]] > v[i]) last = stack[--top];
+        if (last != -1) {
+            left[i] = last;
+            parent[last] = i;
+        }
+        if (top > 0) {
+            right[stack[top - 1]] = i;
+            parent[i] = stack[top - 1];
+        }
+        stack[top++] = i;
+    }
+    *root = stack[0];
+    /* DFS: (node, depth, phase) */
+    int64_t *sn = (int64_t *)xcalloc((size_t)(2 * n + 2), sizeof(int64_t));
+    int64_t *sd = (int64_t *)xcalloc((size_t)(2 * n + 2), sizeof(int64_t));
+    int8_t *sp = (int8_t *)xcalloc((size_t)(2 * n + 2), 1);
+    for (int64_t i = 0; i < n; i++) first[i] = -1;
+    int64_t sz = 0, pos = 0;
+    sn[sz] = *root; sd[sz] = 0; sp[sz] = 0; sz++;
+    while (sz > 0) {
+        sz--;
+        int64_t node = sn[sz], depth = sd[sz];
+        int phase = sp[sz];
+        nodes[pos] = node;
+        depths[pos] = depth;
+        if (first[node] < 0) first[node] = pos;
+        pos++;
+        if (phase == 0) {
+            if (left[node] >= 0) {
+                sn[sz] = node; sd[sz] = depth; sp[sz] = 1; sz++;
+                sn[sz] = left[node]; sd[sz] = depth + 1; sp[sz] = 0; sz++;
+                continue;
+            }
+            phase = 1;
+        }
+        if (phase == 1 && right[node] >= 0) {
+            sn[sz] = node; sd[sz] = depth; sp[sz] = 2; sz++;
+            sn[sz] = right[node]; sd[sz] = depth + 1; sp[sz] = 0; sz++;
+        }
+    }
+    free(stack); free(sn); free(sd); free(sp);
+    return pos == 2 * n - 1 ? 0 : -2;
+}

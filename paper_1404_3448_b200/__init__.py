@@ -14,7 +14,8 @@ from .overlap import (GeneralizedText, LcpQueryEngine, OverlapBatch, OverlapPipe
                       overlap_report, pack_pairs, parse_overlap_record)
 from .parallel_sort import (ChunkPlan, SortConfig, SplitState, chunked_sort, exclusive_scan,
                             parallel_build_sa, plan_chunks, radix_sort, split_by_bit)
-from .rmq import SparseTable, build_sparse, query_sparse, query_sparse_batch
+from .rmq import (CartesianRmq, CartesianTree, EulerTour, PlusMinusOneRmq, SparseTable, build_cartesian,
+                  build_pm1, build_sparse, euler_tour, query_pm1, query_sparse, query_sparse_batch, rmq_via_lca)
 from .sequence import (DnaSequence, NPolicy, RankedText, SequenceError, decode, encode,
                        gen_random, parse_fasta, write_fasta)
 from .suffix_index import (Dc3Workspace, LcpArray, SuffixArray, build_lcp, build_sa_dc3,
@@ -26,6 +27,8 @@ __version__ = "0.1.0"
 __all__ = [
     "BadMagicError", "ChecksumError", "IndexFileError", "TruncatedFileError", "UnsupportedVersionError",
     "load_index", "save_index", "FastaIngest", "ingest_fasta",
+    "CartesianRmq", "CartesianTree", "EulerTour", "PlusMinusOneRmq", "build_cartesian", "build_pm1",
+    "euler_tour", "query_pm1", "rmq_via_lca",
     "ChunkPlan", "SortConfig", "SplitState", "chunked_sort", "exclusive_scan", "parallel_build_sa",
     "plan_chunks", "radix_sort", "split_by_bit",
     "Dc3Workspace", "DnaSequence", "GeneralizedText", "LcpArray", "LcpQueryEngine",

@@ -84,6 +84,11 @@ SIGNATURES = {
     "saix_radix_sort_i64": (_int, [_vp, _i64, _int, _vp, _vp, _c.c_size_t, _vp]),
     "saix_minmax": (_int, [_vp, _int, _i64, _vp, _vp]),
     "saix_widen_i64": (_int, [_vp, _int, _i64, _vp, _vp]),
+    "saix_cartesian_workspace_bytes": (_c.c_size_t, [_i64]),
+    "saix_cartesian_build": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_pm1_build": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "saix_pm1_query_begin": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "saix_pm1_query_end": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "saix_fasta_lines": (_int, [_vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
     "saix_fasta_workspace_bytes": (_c.c_size_t, [_i64, _i64]),
     "saix_fasta_scan": (_int, [_vp, _i64, _i64, _vp, _vp, _c.c_size_t, _vp]),

@@ -17,7 +17,7 @@ from typing import Any, Literal
 import numpy as np
 
 from . import _lib
-from .rmq import SparseTable
+from .rmq import CartesianRmq, SparseTable
 from .sequence import (DnaSequence, NPolicy, RankedText, SequenceError, alphabet, encode,
                        residue_error)
 from .suffix_index import (LcpArray, SuffixArray, _device_index_of, build_lcp, build_sa_dc3)
@@ -35,7 +35,7 @@ class LcpQueryEngine:
     text: RankedText
     sa: SuffixArray
     lcp: LcpArray
-    rmq: SparseTable | None
+    rmq: SparseTable | CartesianRmq | None
     _isa_dev: Any = field(default=None, repr=False, compare=False)
 
     @classmethod
@@ -52,8 +52,8 @@ class LcpQueryEngine:
             raise ValueError(f"unknown rmq kind {rmq_kind!r}")
         if text.n == 0:
             return cls(text=text, sa=sa, lcp=lcp, rmq=None)
-        # both engines answer leftmost-argmin identically (rmq.py:1-15); the
-        # device sparse table serves either kind
+        if rmq_kind == "cartesian":  # the reference's parity engine (rmq.py:239-251), on the device
+            return cls(text=text, sa=sa, lcp=lcp, rmq=CartesianRmq(lcp.lcp))
         dev_vals = (lcp._dev[1], 4) if lcp._dev is not None else None
         rmq = SparseTable(lcp.lcp, _device_values=dev_vals)
         isa = _device_index_of(text, sa).isa
@@ -73,6 +73,16 @@ def lcp_query_batch(engine: LcpQueryEngine, i, j) -> np.ndarray:
         raise IndexError(f"positions ({int(qi.ravel()[0])}, {int(qj.ravel()[0])}) "
                          f"out of bounds for length 0")
     st = engine.rmq
+    if isinstance(st, CartesianRmq):  # overlap.py:58-69 through the Cartesian engine
+        fi, fj = qi.ravel(), qj.ravel()
+        bad = np.flatnonzero((fi < 0) | (fi >= n) | (fj < 0) | (fj >= n))
+        if bad.size:
+            raise IndexError(f"positions ({int(fi[bad[0]])}, {int(fj[bad[0]])}) out of bounds for length {n}")
+        ri, rj = engine.sa.rank[fi], engine.sa.rank[fj]
+        lo, hi = np.minimum(ri, rj), np.maximum(ri, rj)
+        same = fi == fj
+        k = st.query_batch(np.where(same, 0, lo + 1), np.where(same, 0, hi))
+        return np.where(same, n - fi, engine.lcp.lcp[k]).reshape(qi.shape)
     t = _lib.torch()
     L = _lib.load()
     di, dj = _lib.to_device(qi.ravel()), _lib.to_device(qj.ravel())

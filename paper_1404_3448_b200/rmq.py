@@ -1,5 +1,6 @@
-"""Sparse-table range-minimum queries on the B200 -- drop-in for the
-``SparseTable`` half of ``saix.rmq`` (rmq.py:24-58, 254-259).
+"""Range-minimum queries on the B200 -- drop-in for ``saix.rmq``: the
+``SparseTable`` engine (rmq.py:24-58, 254-259) and the Cartesian-tree /
+Euler-tour / ±1 engine (rmq.py:61-251, end of this file).
 
 The table lives on the device as packed (value, index) entries (u32 when
 value range + index bits fit 32, else u64).  ``query`` keeps
@@ -11,6 +12,8 @@ the throughput path: one kernel over arrays of queries.
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass, field
+from typing import Any
 
 import numpy as np
 
@@ -165,3 +168,210 @@ def query_sparse(st: SparseTable, i: int, j: int) -> int:
 def query_sparse_batch(st: SparseTable, i, j) -> np.ndarray:
     """Equals ``[query_sparse(st, a, b) for a, b in zip(i, j)]``."""
     return st.query_batch(i, j)
+
+
+# ------------------------------------------------------- Cartesian pipeline
+# The reference's second RMQ engine (rmq.py:61-251): Cartesian tree -> Euler
+# tour -> ±1 RMQ, built on the device (csrc/cartesian.cu); same classes,
+# fields, values and query answers.
+
+
+@dataclass
+class CartesianTree:
+    """Min-heap binary tree whose in-order traversal is 0..n-1; ties break so
+    the leftmost minimum becomes the ancestor (rmq.py:61-72)."""
+
+    values: np.ndarray
+    parent: np.ndarray
+    left: np.ndarray
+    right: np.ndarray
+    root: int
+    _tour: Any = field(default=None, repr=False, compare=False)
+
+
+@dataclass
+class EulerTour:
+    """Depth-first tour (node on entry and after each child; rmq.py:75-88)."""
+
+    tour_nodes: np.ndarray
+    tour_depths: np.ndarray
+    first_visit: np.ndarray
+    _dev: Any = field(default=None, repr=False, compare=False)  # (nodes, depths, first) int32 tensors
+
+
+def _cartesian_device(values: np.ndarray):
+    t = _lib.torch()
+    L = _lib.load()
+    n = int(values.shape[0])
+    _lib.device()
+    vals = _lib.to_device(values)
+    parent, left, right, first = (_lib.empty(n, t.int32) for _ in range(4))
+    nodes, depths = (_lib.empty(2 * n - 1, t.int32) for _ in range(2))
+    root = np.zeros(1, np.int64)
+    ws = _lib.workspace(L.saix_cartesian_workspace_bytes(n))
+    _lib.check(L.saix_cartesian_build(_lib.ptr(vals), 8, n, _lib.ptr(parent), _lib.ptr(left), _lib.ptr(right),
+                                      _lib.ptr(nodes), _lib.ptr(depths), _lib.ptr(first), root.ctypes.data,
+                                      _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "saix_cartesian_build")
+    i32 = lambda x, k: x[:k].cpu().numpy().astype(np.int64)  # noqa: E731  (signed: -1 = none)
+    tour = EulerTour(tour_nodes=i32(nodes, 2 * n - 1), tour_depths=i32(depths, 2 * n - 1),
+                     first_visit=i32(first, n), _dev=(nodes, depths, first))
+    tree = CartesianTree(values=values, parent=i32(parent, n), left=i32(left, n), right=i32(right, n),
+                         root=int(root[0]), _tour=tour)
+    return tree
+
+
+def build_cartesian(values) -> CartesianTree:
+    """Cartesian tree of ``values`` (rmq.py:91-117) on the device."""
+    values = np.asarray(values, dtype=np.int64)
+    if len(values) == 0:
+        raise ValueError("cannot build a Cartesian tree over an empty array")
+    return _cartesian_device(values)
+
+
+def euler_tour(tree: CartesianTree) -> EulerTour:
+    """Euler tour of a Cartesian tree (rmq.py:120-152); the device builds it
+    with the tree, from the same nearest-value links."""
+    if tree._tour is None:
+        tree._tour = _cartesian_device(np.asarray(tree.values, dtype=np.int64))._tour
+    return tree._tour
+
+
+class PlusMinusOneRmq:
+    """O(1) RMQ over an array whose adjacent entries differ by exactly 1
+    (rmq.py:155-236): blocks of b = max(1, floor(log2 m / 2)), per-block
+    leftmost argmin / min / step-pattern type, one in-block table per present
+    type, a sparse table over block minima -- all built on the device."""
+
+    def __init__(self, depths, _device_depths=None):
+        depths = np.asarray(depths, dtype=np.int64)
+        m = len(depths)
+        if m == 0:
+            raise ValueError("cannot build over an empty array")
+        t = _lib.torch()
+        L = _lib.load()
+        _lib.device()
+        self.depths = depths
+        self.block = b = max(1, (m.bit_length() - 1) // 2)
+        if b > 16:
+            raise ValueError("array too large for the ±1 engine")
+        nblocks = (m + b - 1) // b
+        d0 = int(depths[0])
+        if _device_depths is not None and d0 == 0:
+            dd = _device_depths
+        else:  # argmin is shift-invariant: store depths - depths[0] (|.| < m) as int32
+            dd = _lib.to_device((depths - d0).astype(np.int32))
+        self._d = dd
+        bargmin, bmin, types = (_lib.empty(nblocks, t.int32) for _ in range(3))
+        ncodes = 1 << (b - 1)
+        present = _lib.empty((ncodes + 31) // 32 + 1, t.int32)
+        tab = _lib.empty(ncodes * b * b, t.uint8)
+        bad = np.zeros(1, np.int32)
+        _lib.check(L.saix_pm1_build(_lib.ptr(dd), m, b, _lib.ptr(bargmin), _lib.ptr(bmin), _lib.ptr(types),
+                                    _lib.ptr(present), _lib.ptr(tab), bad.ctypes.data, _lib.stream_ptr()),
+                   "saix_pm1_build")
+        if bad[0]:
+            raise ValueError("adjacent entries must differ by exactly 1")
+        self._bargmin, self._types, self._tab = bargmin, types, tab
+        self.block_argmin = bargmin[:nblocks].cpu().numpy().astype(np.int64)
+        self.block_min = bmin[:nblocks].cpu().numpy().astype(np.int64) + d0
+        self.block_sparse = SparseTable(self.block_min)
+        self.types = types[:nblocks].cpu().numpy().astype(np.int64)
+        bits = present[:(ncodes + 31) // 32].cpu().numpy().view(np.uint32)
+        tabs = tab[:ncodes * b * b].cpu().numpy().reshape(ncodes, b, b)
+        self.inblock: dict[int, np.ndarray] = {}
+        for code in range(ncodes):
+            if (int(bits[code >> 5]) >> (code & 31)) & 1:
+                self.inblock[code] = tabs[code].astype(np.int64)
+
+    @staticmethod
+    def _table_for(code: int, b: int) -> np.ndarray:
+        """argmin table over the simulated walk for one step pattern (rmq.py:199-213)."""
+        walk = [0]
+        for k in range(b - 1):
+            walk.append(walk[-1] + (-1 if (code >> k) & 1 else 1))
+        table = np.zeros((b, b), dtype=np.int64)
+        for i in range(b):
+            best = i
+            table[i, i] = i
+            for j in range(i + 1, b):
+                if walk[j] < walk[best]:
+                    best = j
+                table[i, j] = best
+        return table
+
+    def _inblock_query(self, blk: int, lo: int, hi: int) -> int:
+        return blk * self.block + int(self.inblock[int(self.types[blk])][lo, hi])
+
+    def _query_device(self, qi, qj, first=None, nodes=None) -> np.ndarray:
+        t = _lib.torch()
+        L = _lib.load()
+        q = int(qi.shape[0])
+        di, dj = _lib.to_device(qi), _lib.to_device(qj)
+        lo, hi = _lib.empty(q, t.int64), _lib.empty(q, t.int64)
+        cand = _lib.empty(3 * q, t.int32)
+        st = _lib.stream_ptr()
+        _lib.check(L.saix_pm1_query_begin(self.block, _lib.ptr(self._types), _lib.ptr(self._tab),
+                                          _lib.ptr(first) if first is not None else None, _lib.ptr(di),
+                                          _lib.ptr(dj), q, _lib.ptr(lo), _lib.ptr(hi), _lib.ptr(cand), st),
+                   "saix_pm1_query_begin")
+        mid, _ = self.block_sparse.query_device(lo[:q], hi[:q])
+        out = _lib.empty(q, t.int64)
+        _lib.check(L.saix_pm1_query_end(_lib.ptr(self._d), self.block, _lib.ptr(self._bargmin), _lib.ptr(mid),
+                                        _lib.ptr(cand), _lib.ptr(nodes) if nodes is not None else None, q,
+                                        _lib.ptr(out), st), "saix_pm1_query_end")
+        return out[:q].cpu().numpy()
+
+    def query_batch(self, i, j) -> np.ndarray:
+        qi = np.ascontiguousarray(i, dtype=np.int64).ravel()
+        qj = np.ascontiguousarray(j, dtype=np.int64).ravel()
+        m = len(self.depths)
+        if qi.size and (qi.min() < 0 or qi.max() >= m or qj.min() < 0 or qj.max() >= m):
+            bad = np.flatnonzero((qi < 0) | (qi >= m) | (qj < 0) | (qj >= m))[0]
+            raise IndexError(f"query ({int(qi[bad])}, {int(qj[bad])}) out of bounds for length {m}")
+        if qi.size == 0:
+            return np.zeros(0, np.int64)
+        return self._query_device(qi, qj)
+
+    def query(self, i: int, j: int) -> int:
+        i, j = _check_range(len(self.depths), int(i), int(j))
+        return int(self.query_batch(np.array([i]), np.array([j]))[0])
+
+
+class CartesianRmq:
+    """Range minima answered as LCAs: tree + tour + ±1 RMQ, built once on the
+    device (rmq.py:239-251)."""
+
+    def __init__(self, values):
+        self.values = np.asarray(values, dtype=np.int64)
+        self.tree = build_cartesian(self.values)
+        self.tour = euler_tour(self.tree)
+        self.pm1 = PlusMinusOneRmq(self.tour.tour_depths, _device_depths=self.tour._dev[1])
+
+    def query_batch(self, i, j) -> np.ndarray:
+        qi = np.ascontiguousarray(i, dtype=np.int64).ravel()
+        qj = np.ascontiguousarray(j, dtype=np.int64).ravel()
+        n = len(self.values)
+        if qi.size and (qi.min() < 0 or qi.max() >= n or qj.min() < 0 or qj.max() >= n):
+            bad = np.flatnonzero((qi < 0) | (qi >= n) | (qj < 0) | (qj >= n))[0]
+            raise IndexError(f"query ({int(qi[bad])}, {int(qj[bad])}) out of bounds for length {n}")
+        if qi.size == 0:
+            return np.zeros(0, np.int64)
+        nodes, _, first = self.tour._dev
+        return self.pm1._query_device(qi, qj, first=first, nodes=nodes)
+
+    def query(self, i: int, j: int) -> int:
+        i, j = _check_range(len(self.values), int(i), int(j))
+        return int(self.query_batch(np.array([i]), np.array([j]))[0])
+
+
+def build_pm1(depths) -> PlusMinusOneRmq:
+    return PlusMinusOneRmq(depths)
+
+
+def query_pm1(structure: PlusMinusOneRmq, i: int, j: int) -> int:
+    return structure.query(i, j)
+
+
+def rmq_via_lca(values, i: int, j: int) -> int:
+    """One-shot build-and-query through the Cartesian pipeline (rmq.py:266-268)."""
+    return CartesianRmq(values).query(i, j)

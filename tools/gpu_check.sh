@@ -45,3 +45,8 @@ for what in "$@"; do
     fastafull_*) K=${what#fastafull_}; timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K -c 1 -o $O/fastafull_$K python bench.py --workload fasta --steps 3 --warmup 3 --no-cpu-baseline --no-prof > $O/ncu_fastafull_$K.log 2>&1; tail -2 $O/ncu_fastafull_$K.log ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    carttests) timeout 900 python -m pytest tests/test_gpu_cartesian.py -x -q > $O/carttests.log 2>&1; tail -25 $O/carttests.log ;;
+  esac
+done
