@@ -261,9 +261,10 @@ SAIX_API int saix_cartesian_build(const void *values, int value_bytes, int64_t n
  * table (built with saix_sparse_build over bmin): block size b (1..16),
  * nblocks = ceil(m/b) leftmost argmins / minima / step codes, the in-block
  * tables tab[code][i][j] (u8, 2^(b-1) codes) of the codes present; present
- * holds ceil(2^(b-1)/32) + 1 words; *bad_host = 1 on a non-unit step. */
+ * (one flag byte per code) holds round_up(2^(b-1), 4) + 4 bytes; *bad_host =
+ * 1 on a non-unit step. */
 SAIX_API int saix_pm1_build(const int32_t *depths, int64_t m, int b, int32_t *bargmin, int32_t *bmin,
-             int32_t *types, uint32_t *present, uint8_t *tab, int32_t *bad_host, void *stream);
+             int32_t *types, uint8_t *present, uint8_t *tab, int32_t *bad_host, void *stream);
 
 /* PlusMinusOneRmq.query / CartesianRmq.query (rmq.py:219-251), batched in two
  * halves around a saix_sparse_query over the block minima:

@@ -49,71 +49,105 @@ template <typename V>
 __global__ void __launch_bounds__(CT_THREADS)
 k_ct_tile(const V *__restrict__ val, i64 n, int *__restrict__ Lo, int *__restrict__ Ro, V *__restrict__ pmin,
           V *__restrict__ smin, V *__restrict__ tmin) {
-    __shared__ V sv[CT_TILE];
-    __shared__ short sl[CT_TILE], sr[CT_TILE];
+    // one pad slot per 32 (4-byte V) / 16 (8-byte V) elements: a warp's
+    // threads walk their 8-element segments in lockstep without bank conflicts
+    constexpr int PSH = sizeof(V) == 4 ? 5 : 4;
+    __shared__ V sv_[CT_TILE + (CT_TILE >> PSH)];
+    __shared__ short sl_[CT_TILE + (CT_TILE >> 4)], sr_[CT_TILE + (CT_TILE >> 4)];
     __shared__ V wred[2][CT_THREADS / 32];
+    auto sv = [&](int k) -> V & { return sv_[k + (k >> PSH)]; };
+    auto sl = [&](int k) -> short & { return sl_[k + (k >> 4)]; };
+    auto sr = [&](int k) -> short & { return sr_[k + (k >> 4)]; };
     const i64 t0 = (i64)blockIdx.x * CT_TILE;
     const int cnt = n - t0 < CT_TILE ? (int)(n - t0) : CT_TILE;
-    for (int k = threadIdx.x; k < cnt; k += CT_THREADS) sv[k] = val[t0 + k];
+    for (int k = threadIdx.x; k < cnt; k += CT_THREADS) sv(k) = val[t0 + k];
     __syncthreads();
     const int s0 = threadIdx.x * CT_SEG;
     const int s1 = s0 + CT_SEG < cnt ? s0 + CT_SEG : cnt;
     // phase a: inside the segment
     for (int i = s0; i < s1; i++) {
         int j = i - 1;
-        const V x = sv[i];
-        while (j >= s0 && sv[j] > x) j = sl[j] >= 0 ? sl[j] : s0 - 1;
-        sl[i] = j >= s0 ? (short)j : (short)CT_OPEN;
+        const V x = sv(i);
+        while (j >= s0 && sv(j) > x) j = sl(j) >= 0 ? sl(j) : s0 - 1;
+        sl(i) = (short)(j >= s0 ? j : CT_OPEN);
     }
     for (int i = s1 - 1; i >= s0; i--) {
         int j = i + 1;
-        const V x = sv[i];
-        while (j < s1 && sv[j] >= x) j = sr[j] >= 0 ? sr[j] : s1;
-        sr[i] = j < s1 ? (short)j : (short)CT_OPEN;
+        const V x = sv(i);
+        while (j < s1 && sv(j) >= x) j = sr(j) >= 0 ? sr(j) : s1;
+        sr(i) = (short)(j < s1 ? j : CT_OPEN);
     }
     __syncthreads();
-    // phase b: across earlier / later segments (reads phase-a links only)
+    // phase b: elements whose answer lies in another segment.  A sparse
+    // table over the 256 segment minima (smem) finds the nearest qualifying
+    // segment by binary lifting; the element inside it by a <= 8-step walk.
+    constexpr int NSEG = CT_THREADS, SLV = 9;  // 2^8 = 256 segments
+    __shared__ V segt[SLV][NSEG];
+    {
+        V m0 = s0 < s1 ? sv(s0) : V(0);
+        for (int i = s0 + 1; i < s1; i++) m0 = ct_min(m0, sv(i));
+        segt[0][threadIdx.x] = m0;
+    }
+    const int nseg = (cnt + CT_SEG - 1) / CT_SEG;
+    __syncthreads();
+    for (int k = 1; k < SLV; k++) {
+        const int h = 1 << (k - 1);
+        const int u = threadIdx.x;
+        if (u < nseg) segt[k][u] = u + h < nseg ? ct_min(segt[k - 1][u], segt[k - 1][u + h]) : segt[k - 1][u];
+        __syncthreads();
+    }
+    const int myseg = threadIdx.x;
     int Lr[CT_SEG], Rr[CT_SEG];
 #pragma unroll
     for (int q = 0; q < CT_SEG; q++) {
         const int i = s0 + q;
         Lr[q] = Rr[q] = CT_OPEN;
         if (i >= s1) continue;
-        const V x = sv[i];
-        int j = sl[i];
+        const V x = sv(i);
+        int j = sl(i);
         if (j == CT_OPEN) {
-            j = s0 - 1;
-            while (j >= 0 && sv[j] > x) {
-                const int seg = j / CT_SEG * CT_SEG;
-                j = sl[j] >= 0 ? sl[j] : seg - 1;
+            int pos = myseg;  // segments [pos, myseg) all have min > x
+            for (int k = SLV - 1; k >= 0; k--) {
+                const int w = 1 << k;
+                if (pos - w >= 0 && segt[k][pos - w] > x) pos -= w;
             }
-            j = j >= 0 ? j : CT_OPEN;
+            if (pos >= 1) {
+                j = pos * CT_SEG - 1;  // last element of segment pos-1, walked left by phase-a links
+                while (sv(j) > x) j = sl(j);
+            } else {
+                j = CT_OPEN;
+            }
         }
         Lr[q] = j;
-        j = sr[i];
+        j = sr(i);
         if (j == CT_OPEN) {
-            j = s1;
-            while (j < cnt && sv[j] >= x) {
-                const int seg_end = (j / CT_SEG + 1) * CT_SEG < cnt ? (j / CT_SEG + 1) * CT_SEG : cnt;
-                j = sr[j] >= 0 ? sr[j] : seg_end;
+            int pos = myseg + 1;  // segments (myseg, pos) all have min >= x
+            for (int k = SLV - 1; k >= 0; k--) {
+                const int w = 1 << k;
+                if (pos + w <= nseg && segt[k][pos] >= x) pos += w;
             }
-            j = j < cnt ? j : CT_OPEN;
+            if (pos < nseg) {
+                j = pos * CT_SEG;  // first element of segment pos, walked right by phase-a links
+                while (sv(j) >= x) j = sr(j);
+            } else {
+                j = CT_OPEN;
+            }
         }
         Rr[q] = j;
     }
     // prefix / suffix minima of the tile (sequential in the segment, then a
     // warp + block combine)
     V pre[CT_SEG], suf[CT_SEG];
-    V run = s0 < s1 ? sv[s0] : V(0);
+    V run = s0 < s1 ? sv(s0) : V(0);
 #pragma unroll
     for (int q = 0; q < CT_SEG; q++) {
-        if (s0 + q < s1) run = ct_min(run, sv[s0 + q]);
+        if (s0 + q < s1) run = ct_min(run, sv(s0 + q));
         pre[q] = run;
     }
-    V run2 = s1 > s0 ? sv[s1 - 1] : V(0);
+    V run2 = s1 > s0 ? sv(s1 - 1) : V(0);
 #pragma unroll
     for (int q = CT_SEG - 1; q >= 0; q--) {
-        if (s0 + q < s1) run2 = ct_min(run2, sv[s0 + q]);
+        if (s0 + q < s1) run2 = ct_min(run2, sv(s0 + q));
         suf[q] = run2;
     }
     const bool has = s0 < s1;
@@ -192,7 +226,7 @@ k_ct_tile(const V *__restrict__ val, i64 n, int *__restrict__ Lo, int *__restric
         smin[g] = cr_has ? ct_min(cr, suf[q]) : suf[q];
     }
     if (threadIdx.x == 0) {
-        V m = sv[0];
+        V m = sv(0);
         for (int u = 0; u < CT_THREADS / 32; u++)
             if (whas[0][u]) m = ct_min(m, wred[0][u]);
         tmin[blockIdx.x] = m;
@@ -323,7 +357,7 @@ __global__ void k_ct_tour(i64 n, const int *__restrict__ Lo, const int *__restri
 // per block: leftmost argmin and min over the padded block, step code; flags
 // a non-unit step
 __global__ void k_pm1_blocks(const int *__restrict__ d, i64 m, int b, i64 nblocks, int *__restrict__ bargmin,
-                             int *__restrict__ bmin, int *__restrict__ types, u32 *__restrict__ present,
+                             int *__restrict__ bmin, int *__restrict__ types, u8 *__restrict__ present,
                              int *__restrict__ bad) {
     for (i64 k = (i64)blockIdx.x * blockDim.x + threadIdx.x; k < nblocks; k += (i64)gridDim.x * blockDim.x) {
         const i64 lo = k * b;
@@ -334,7 +368,7 @@ __global__ void k_pm1_blocks(const int *__restrict__ d, i64 m, int b, i64 nblock
             const i64 i = lo + q;
             const int x = i < m ? d[i] : last + 1 + (int)(i - m);
             const int step = x - prev;
-            if (i < m && step != 1 && step != -1) atomicOr(bad, 1);
+            if (i < m && step != 1 && step != -1) *bad = 1;
             if (step < 0) code |= 1u << (q - 1);
             if (x < bestv) {
                 bestv = x;
@@ -344,21 +378,21 @@ __global__ void k_pm1_blocks(const int *__restrict__ d, i64 m, int b, i64 nblock
         }
         if (k + 1 < nblocks) {  // the step into the next block
             const int nx = d[lo + b];
-            if (nx - prev != 1 && nx - prev != -1) atomicOr(bad, 1);
+            if (nx - prev != 1 && nx - prev != -1) *bad = 1;
         }
         bargmin[k] = best;
         bmin[k] = bestv;
         types[k] = (int)code;
-        atomicOr(present + (code >> 5), 1u << (code & 31));
+        if (!present[code]) present[code] = 1;  // plain racing stores of the same value
     }
 }
 
 // in-block answer tables of every present code: tab[code][i][j] (u8)
-__global__ void k_pm1_tables(int b, u32 ncodes, const u32 *__restrict__ present, u8 *__restrict__ tab) {
+__global__ void k_pm1_tables(int b, u32 ncodes, const u8 *__restrict__ present, u8 *__restrict__ tab) {
     for (i64 x = (i64)blockIdx.x * blockDim.x + threadIdx.x; x < (i64)ncodes * b; x += (i64)gridDim.x * blockDim.x) {
         const u32 code = (u32)(x / b);
         const int i = (int)(x % b);
-        if (!((present[code >> 5] >> (code & 31)) & 1u)) continue;
+        if (!present[code]) continue;
         int walk[32];
         walk[0] = 0;
         for (int k = 0; k + 1 < b; k++) walk[k + 1] = walk[k] + (((code >> k) & 1u) ? -1 : 1);
@@ -530,7 +564,7 @@ extern "C" int saix_cartesian_build(const void *values, int value_bytes, int64_t
 // codes' in-block tables (tab: (2^(b-1)) x b x b bytes); *bad_host = 1 if
 // some adjacent depths differ by other than 1.
 extern "C" int saix_pm1_build(const int32_t *depths, int64_t m, int b, int32_t *bargmin, int32_t *bmin,
-                              int32_t *types, uint32_t *present, uint8_t *tab, int32_t *bad_host, void *stream) {
+                              int32_t *types, uint8_t *present, uint8_t *tab, int32_t *bad_host, void *stream) {
     if (!depths || m <= 0 || b < 1 || b > 16 || !bargmin || !bmin || !types || !present || !tab || !bad_host) {
         set_error("saix_pm1_build: invalid arguments");
         return SAIX_EINVAL;
@@ -538,8 +572,8 @@ extern "C" int saix_pm1_build(const int32_t *depths, int64_t m, int b, int32_t *
     cudaStream_t st = (cudaStream_t)stream;
     const i64 nblocks = ceil_div(m, b);
     const u32 ncodes = 1u << (b - 1);
-    int *bad = reinterpret_cast<int *>(present + ceil_div(ncodes, 32));  // caller sized present + 1 word
-    SAIX_CUDA(cudaMemsetAsync(present, 0, (size_t)(ceil_div(ncodes, 32) + 1) * 4, st));
+    int *bad = reinterpret_cast<int *>(present + ((ncodes + 3) & ~3u));  // caller sized present + 4 bytes
+    SAIX_CUDA(cudaMemsetAsync(present, 0, (size_t)((ncodes + 3) & ~3u) + 4, st));
     {
         Prof prof_("pm1.blocks", (double)m * 4 + nblocks * 12.0, st);
         k_pm1_blocks<<<grid_for(nblocks, 256), 256, 0, st>>>(depths, m, b, nblocks, bargmin, bmin, types, present,

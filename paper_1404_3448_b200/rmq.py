@@ -263,7 +263,7 @@ class PlusMinusOneRmq:
         self._d = dd
         bargmin, bmin, types = (_lib.empty(nblocks, t.int32) for _ in range(3))
         ncodes = 1 << (b - 1)
-        present = _lib.empty((ncodes + 31) // 32 + 1, t.int32)
+        present = _lib.empty(((ncodes + 3) & ~3) + 4, t.uint8)
         tab = _lib.empty(ncodes * b * b, t.uint8)
         bad = np.zeros(1, np.int32)
         _lib.check(L.saix_pm1_build(_lib.ptr(dd), m, b, _lib.ptr(bargmin), _lib.ptr(bmin), _lib.ptr(types),
@@ -276,12 +276,9 @@ class PlusMinusOneRmq:
         self.block_min = bmin[:nblocks].cpu().numpy().astype(np.int64) + d0
         self.block_sparse = SparseTable(self.block_min)
         self.types = types[:nblocks].cpu().numpy().astype(np.int64)
-        bits = present[:(ncodes + 31) // 32].cpu().numpy().view(np.uint32)
+        flags = present[:ncodes].cpu().numpy()
         tabs = tab[:ncodes * b * b].cpu().numpy().reshape(ncodes, b, b)
-        self.inblock: dict[int, np.ndarray] = {}
-        for code in range(ncodes):
-            if (int(bits[code >> 5]) >> (code & 31)) & 1:
-                self.inblock[code] = tabs[code].astype(np.int64)
+        self.inblock: dict[int, np.ndarray] = {int(c): tabs[c].astype(np.int64) for c in np.flatnonzero(flags)}
 
     @staticmethod
     def _table_for(code: int, b: int) -> np.ndarray:

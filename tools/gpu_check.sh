@@ -9,7 +9,7 @@ for what in "$@"; do
   case $what in
     tests) timeout 1500 python -m pytest tests -m gpu -x -q > $O/tests.log 2>&1; tail -3 $O/tests.log ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -2 $O/smoke.log ;;
-    c2|c3|c4|c5|store|fasta) timeout 900 python bench.py --workload $what > $O/bench_$what.json 2> $O/bench_$what.err; tail -c 600 $O/bench_$what.json; tail -3 $O/bench_$what.err ;;
+    c2|c3|c4|c5|store|fasta|cartesian) timeout 900 python bench.py --workload $what > $O/bench_$what.json 2> $O/bench_$what.err; tail -c 600 $O/bench_$what.json; tail -3 $O/bench_$what.err ;;
     ref) timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err; cat $O/bench_ref.json ;;
     ncu_c2) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/c2_launches.csv python tools/profile_once.py c2 > $O/ncu_c2.log 2>&1; python tools/ncu_summary.py $O/c2_launches.csv > $O/c2_launches.txt; head -30 $O/c2_launches.txt ;;
     ncu_c4|ncu_c5) W=${what#ncu_}; timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/${W}_launches.csv python tools/profile_once.py $W > $O/ncu_$W.log 2>&1; python tools/ncu_summary.py $O/${W}_launches.csv 40 > $O/${W}_launches.txt; head -25 $O/${W}_launches.txt ;;
@@ -48,5 +48,15 @@ done
 for what in "$@"; do
   case $what in
     carttests) timeout 900 python -m pytest tests/test_gpu_cartesian.py -x -q > $O/carttests.log 2>&1; tail -25 $O/carttests.log ;;
+  esac
+done
+for what in "$@"; do
+  case $what in
+    ncu_cart) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_ct_|k_pm1|k_sparse|k_scan" --csv --log-file $O/cart_launches.csv python bench.py --workload cartesian --steps 1 --warmup 3 --no-cpu-baseline --no-prof > $O/ncu_cart.log 2>&1; python tools/ncu_summary.py $O/cart_launches.csv 20 > $O/cart_launches.txt; head -20 $O/cart_launches.txt ;;
+  esac
+done
+for what in "$@"; do
+  case $what in
+    cartfull_*) K=${what#cartfull_}; timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K -c 1 -o $O/cartfull_$K python bench.py --workload cartesian --steps 1 --warmup 3 --no-cpu-baseline --no-prof > $O/ncu_cartfull_$K.log 2>&1; tail -2 $O/ncu_cartfull_$K.log ;;
   esac
 done
