@@ -60,3 +60,9 @@ for what in "$@"; do
     cartfull_*) K=${what#cartfull_}; timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K -c 1 -o $O/cartfull_$K python bench.py --workload cartesian --steps 1 --warmup 3 --no-cpu-baseline --no-prof > $O/ncu_cartfull_$K.log 2>&1; tail -2 $O/ncu_cartfull_$K.log ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    ncu_fasta) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_fa_|k_scan" --csv --log-file $O/fasta_launches.csv python bench.py --workload fasta --steps 1 --warmup 3 --no-cpu-baseline --no-prof > $O/ncu_fasta.log 2>&1; python tools/ncu_summary.py $O/fasta_launches.csv 20 > $O/fasta_launches.txt; head -12 $O/fasta_launches.txt ;;
+    ncu_store2) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_crc|k_unpack|k_put|k_ps_|k_pairs" --csv --log-file $O/store_launches.csv python bench.py --workload store --steps 1 --warmup 3 --no-cpu-baseline --no-prof > $O/ncu_store.log 2>&1; python tools/ncu_summary.py $O/store_launches.csv 20 > $O/store_launches.txt; head -12 $O/store_launches.txt ;;
+  esac
+done
