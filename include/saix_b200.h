@@ -116,6 +116,12 @@ SAIX_API int saix_dc3_merge(const void *text, int text_bytes, int64_t n,
  * the number of levels (at most max_levels are written to out[4*i..]). */
 SAIX_API int saix_dc3_trace(int64_t *out, int max_levels);
 
+/* Level-0 window naming (byte texts, sigma <= 7): samples named by their
+ * 21-character windows, ties ordered by prefix doubling, no recursion below
+ * level 0 (same SA / ISA).  on = 0 runs the reference recursion instead.
+ * Returns the previous setting (default on; env SAIX_WINDOW_NAMING=0). */
+SAIX_API int saix_dc3_set_window_naming(int on);
+
 /* ------------------------------------------------- parallel sort engine */
 /* The reference's split-kernel engine (parallel_sort.py:110-293) on the
  * device scan and radix sort. Keys are int64 (nonnegative for the sort). */

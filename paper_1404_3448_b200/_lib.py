@@ -93,6 +93,7 @@ SIGNATURES = {
     "saix_fasta_workspace_bytes": (_c.c_size_t, [_i64, _i64]),
     "saix_fasta_scan": (_int, [_vp, _i64, _i64, _vp, _vp, _c.c_size_t, _vp]),
     "saix_fasta_emit": (_int, [_vp, _i64, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_dc3_set_window_naming": (_int, [_int]),
     "saix_crc32_workspace_bytes": (_c.c_size_t, [_i64]),
     "saix_crc32": (_int, [_vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
     "saix_index_bytes": (_i64, [_i64]),

@@ -29,13 +29,21 @@ constexpr int BS_SMALL = 1024;  // warp-per-bucket (shared memory) limit
 constexpr int BS_LARGE = 4096;  // CTA-per-bucket limit
 constexpr int BS_WARPS = 8;
 
+// key, value and dense bucket coordinate of item i; sources that can derive
+// the dense value more cheaply than from the key overload this (ADL)
+template <class Src>
+__device__ __forceinline__ u64 bs_get(const Src &src, i64 i, u64 &k, u32 &v) {
+    src.get(i, k, v);
+    return src.dense(k);
+}
+
 template <class Src>
 __global__ void k_bs_count(Src src, i64 n, int shift, u32 *__restrict__ cnt) {
     for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
         u64 k;
         u32 v;
-        src.get(i, k, v);
-        atomicAdd(&cnt[src.dense(k) >> shift], 1u);
+        const u64 d = bs_get(src, i, k, v);
+        atomicAdd(&cnt[d >> shift], 1u);
     }
 }
 
@@ -64,8 +72,8 @@ __global__ void k_bs_scatter(Src src, i64 n, int shift, u32 *__restrict__ cursor
     for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
         u64 k;
         u32 v;
-        src.get(i, k, v);
-        u32 at = atomicAdd(&cursor[src.dense(k) >> shift], 1u);
+        const u64 d = bs_get(src, i, k, v);
+        u32 at = atomicAdd(&cursor[d >> shift], 1u);
         keys[at] = k;
         vals[at] = v;
     }
@@ -76,7 +84,7 @@ __global__ void k_bs_scatter(Src src, i64 n, int shift, u32 *__restrict__ cursor
 // {slot, val, key lo, key hi}; pass B writes keys/vals windows as full lines.
 constexpr int BSE_ITEMS = 8;
 template <class Src>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 k_bs_scatter_emit(Src src, i64 n, int shift, u32 *__restrict__ cursor, PsPlan plan, uint4 *__restrict__ stage) {
     extern __shared__ __align__(16) unsigned char bse_smem[];
     uint4 *sh_items = reinterpret_cast<uint4 *>(bse_smem);
@@ -92,8 +100,8 @@ k_bs_scatter_emit(Src src, i64 n, int shift, u32 *__restrict__ cursor, PsPlan pl
         if (ok[q]) {
             u64 k;
             u32 v;
-            src.get(i, k, v);
-            u32 at = atomicAdd(&cursor[src.dense(k) >> shift], 1u);
+            const u64 d = bs_get(src, i, k, v);
+            u32 at = atomicAdd(&cursor[d >> shift], 1u);
             it[q] = make_uint4(at, v, (u32)k, (u32)(k >> 32));
         }
     }
@@ -298,9 +306,9 @@ struct BsGeom {
     int shift;
     i64 nb;
 };
-inline BsGeom bs_geom(u64 max_key, i64 n) {
-    i64 want = n / 8 > 1 ? n / 8 : 1;
-    if (want > ((i64)1 << 23)) want = (i64)1 << 23;
+inline BsGeom bs_geom(u64 max_key, i64 n, int per_bucket = 8, int max_bits = 23) {
+    i64 want = n / per_bucket > 1 ? n / per_bucket : 1;
+    if (want > ((i64)1 << max_bits)) want = (i64)1 << max_bits;
     int shift = 0;
     while ((i64)(max_key >> shift) + 1 > want) shift++;
     return BsGeom{shift, (i64)(max_key >> shift) + 1};
@@ -314,10 +322,10 @@ inline i64 bs_scratch_words_for(u64 max_key, i64 n) { return bs_scratch_words(bs
 // BS_LARGE; the caller then sorts with onesweep instead.  One host sync.
 template <class Src>
 int bucket_sort(Src src, i64 n, u64 span, u64 *keys, u32 *vals, u32 *scratch, bool &ok, cudaStream_t st,
-                const char *prof = "bsort", Arena *ar = nullptr) {
+                const char *prof = "bsort", Arena *ar = nullptr, int per_bucket = 8, int max_bits = 23) {
     ok = true;
     if (n <= 0) return SAIX_OK;
-    BsGeom g = bs_geom(span, n);
+    BsGeom g = bs_geom(span, n, per_bucket, max_bits);
     const i64 nb = g.nb;
     Prof prof_(prof, 24.0 * n + 16.0 * nb, st);
     u32 *cnt = scratch, *start = cnt + (nb + 1), *cursor = start + (nb + 1), *mid = cursor + (nb + 1);

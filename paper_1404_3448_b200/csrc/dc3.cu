@@ -1263,6 +1263,18 @@ struct LevelRec {
 };
 static thread_local std::vector<LevelRec> g_trace;
 
+// Level-0 window naming switch: SAIX_WINDOW_NAMING=0 or saix_dc3_set_window_naming(0)
+// turns it off (the reference recursion runs; A/B measurement and the
+// reference level trace for the section 8(d) model)
+static int g_window_naming = -1;
+static bool window_naming_on() {
+    if (g_window_naming < 0) {
+        const char *e = getenv("SAIX_WINDOW_NAMING");
+        g_window_naming = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_window_naming != 0;
+}
+
 // SAIX_TRACE=1: one stderr line per level (development aid)
 static bool trace_on() {
     static int v = [] {
@@ -2235,6 +2247,186 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
 
 // Streaming level (see "streaming level" above).  SA / ISA / Phi nullable;
 // Phi is produced only when ISA is not requested (*phi_done tells).
+// ------------------------------------------------ level-0 window naming
+// Byte levels with sigma <= 7: name every sample by its 21-character window
+// (3 bits per character, u64 key, 0 past the end) instead of its triple.  The
+// reduced string's suffix order is unchanged -- equal names mean equal 21
+// characters, a comparison continued at the next name (3 characters on)
+// re-reads what is already equal, and windows reaching past the end hold the
+// sentinel at distinct offsets, so they are unique and no comparison runs
+// across the end of a sample block (the same property DC3's padding triples
+// give).  On non-repetitive text almost all windows are distinct: the tied
+// samples are ordered by the prefix doubling of resolve_ties and the
+// recursion below this level disappears.  Too many ties -> the caller runs
+// the triple naming + recursion as before.
+constexpr int WN_CHARS = 21;
+struct WindowSrc {
+    const u8 *t;
+    i64 N;
+    SampleLayout L;
+    u32 lo, r;  // dense digits: c - lo in [0, r) for c >= lo
+    int j;      // leading characters in the dense map
+    int rb;     // log2(r) when r is a power of two, else 0
+    __device__ __forceinline__ void get(i64 s, u64 &k, u32 &v) const {
+        const i64 p = L.pos(s);
+        u64 key = 0;
+        const i64 a = p & ~(i64)3;
+        if (a + 28 <= N) {
+            const u32 *w = reinterpret_cast<const u32 *>(t + a);
+            const int sh = 8 * (int)(p - a);
+            u32 x[7];
+#pragma unroll
+            for (int q = 0; q < 7; q++) x[q] = __ldg(w + q);
+            u32 y[6];
+#pragma unroll
+            for (int q = 0; q < 6; q++) y[q] = __funnelshift_r(x[q], x[q + 1], sh);
+#pragma unroll
+            for (int q = 0; q < WN_CHARS; q++) key = (key << 3) | ((y[q >> 2] >> (8 * (q & 3))) & 7u);
+        } else {
+            for (int q = 0; q < WN_CHARS; q++) key = (key << 3) | (p + q < N ? (u64)(t[p + q] & 7u) : 0ull);
+        }
+        k = key;
+        v = (u32)s;
+    }
+    // monotone: mixed radix of the leading j characters; a character below lo
+    // (sentinel / separator) zeroes itself and everything after it
+    __device__ __forceinline__ u64 dense(u64 k) const {
+        u64 d = 0;
+        bool low = false;
+        for (int q = 0; q < j; q++) {
+            const u32 c = (u32)(k >> (3 * (WN_CHARS - 1 - q))) & 7u;
+            low = low || c < lo;
+            d = d * r + (low ? 0u : c - lo);
+        }
+        return d;
+    }
+};
+
+// key + dense value from the same loaded bytes (bucket-sort hook, bs_get)
+__device__ __forceinline__ u64 bs_get(const WindowSrc &w, i64 s, u64 &k, u32 &v) {
+    const i64 p = w.L.pos(s);
+    u64 key = 0, d = 0;
+    bool low = false;
+    const i64 a = p & ~(i64)3;
+    if (a + 28 <= w.N) {
+        const u32 *wp = reinterpret_cast<const u32 *>(w.t + a);
+        const int sh = 8 * (int)(p - a);
+        u32 x[7];
+#pragma unroll
+        for (int q = 0; q < 7; q++) x[q] = __ldg(wp + q);
+        u32 y[6];
+#pragma unroll
+        for (int q = 0; q < 6; q++) y[q] = __funnelshift_r(x[q], x[q + 1], sh);
+#pragma unroll
+        for (int q = 0; q < WN_CHARS; q++) {
+            const u32 c = (y[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+            key = (key << 3) | (c & 7u);
+            if (q < w.j) {
+                low = low || c < w.lo;
+                const u32 dig = low ? 0u : c - w.lo;
+                d = w.rb ? ((d << w.rb) | dig) : d * w.r + dig;
+            }
+        }
+    } else {
+        for (int q = 0; q < WN_CHARS; q++) {
+            const u32 c = p + q < w.N ? (u32)w.t[p + q] : 0u;
+            key = (key << 3) | (c & 7u);
+            if (q < w.j) {
+                low = low || c < w.lo;
+                const u32 dig = low ? 0u : c - w.lo;
+                d = w.rb ? ((d << w.rb) | dig) : d * w.r + dig;
+            }
+        }
+    }
+    k = key;
+    v = (u32)s;
+    return d;
+}
+
+static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const SampleLayout &L, u32 *SAc, u32 *ISAc,
+                       u32 *d_scal, int depth, bool &handled) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    handled = false;
+    const i64 m = L.m;
+    const size_t mark = ar.mark();
+    if (ar.cap - mark < (size_t)m * 96 + ((size_t)64 << 20)) return SAIX_OK;  // no room: recurse instead
+    WindowSrc src;
+    src.t = text;
+    src.N = N;
+    src.L = L;
+    src.lo = sigma <= 4 ? 1u : 2u;
+    src.r = (u32)sigma - src.lo + 1u;
+    src.j = 0;
+    src.rb = (src.r & (src.r - 1)) == 0 ? __builtin_ctz(src.r) : 0;
+    u64 span = 1;
+    while (src.j < WN_CHARS && span * src.r <= ((u64)1 << 28)) {
+        span *= src.r;
+        src.j++;
+    }
+    constexpr int WN_PER_BUCKET = 6, WN_MAX_BITS = 24;  // counters stay L2-resident (64 MB)
+    const BsGeom g = bs_geom(span - 1, m, WN_PER_BUCKET, WN_MAX_BITS);
+    u64 *k0 = ar.alloc<u64>(m), *k1 = ar.alloc<u64>(m);
+    u32 *v0 = ar.alloc<u32>(m);
+    u32 *scratch = ar.alloc<u32>(bs_scratch_words(g.nb));
+    SAIX_ARENA_OK(ar);
+    bool done = false;
+    SAIX_TRY(bucket_sort(src, m, span - 1, k0, v0, scratch, done, st, "dc3.window_sort", &ar, WN_PER_BUCKET,
+                         WN_MAX_BITS));
+    if (!done) {
+        ar.reset(mark);
+        return SAIX_OK;
+    }
+    SAIX_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(u32), st));
+    {
+        Prof prof_("dc3.count_names", 8.0 * m, st);
+        k_count_distinct<<<grid_for(m, K_THREADS, kNumSMs * 8), K_THREADS, 0, st>>>(k0, m, d_scal);
+    }
+    SAIX_LAUNCHED();
+    u32 D = 0;
+    SAIX_TRY(read_u32(d_scal, &D, st));
+    if ((i64)D == m) {
+        if (m >= kDirectScatterItems) {
+            PsPlan pu = PsPlan::of(m, 4);
+            pu.set_cursors(ar.alloc<u32>(pu.cursor_words()));
+            uint2 *s1 = ar.alloc<uint2>(pu.stage1_items()), *s2 = ar.alloc<uint2>(pu.stage2_items());
+            SAIX_ARENA_OK(ar);
+            SAIX_CUDA(cudaMemsetAsync(pu.a.cursor, 0, (size_t)pu.cursor_words() * 4, st));
+            {
+                Prof prof_("dc3.unique_ranks", (SAc ? 16.0 : 12.0) * m, st);
+                static bool attr = false;
+                if (!attr) {
+                    SAIX_CUDA(cudaFuncSetAttribute(k_unique_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   256 * UE_ITEMS * 8 + 8 * PS_MAX_BUCKETS));
+                    attr = true;
+                }
+                size_t smem = (size_t)256 * UE_ITEMS * 8 + 8 * (size_t)pu.a.buckets;
+                k_unique_emit<<<(unsigned)ceil_div(m, 256 * UE_ITEMS), 256, smem, st>>>(v0, m, SAc, pu, s1);
+            }
+            SAIX_LAUNCHED();
+            SAIX_TRY(ps_finish(s1, s2, pu, U32Apply{ISAc}, st, "dc3.unique_isa", 28.0 * m));
+        } else {
+            Prof prof_("dc3.unique_ranks", 12.0 * m, st);
+            k_unique_from_sorted<<<grid_for(m, K_THREADS), K_THREADS, 0, st>>>(v0, m, SAc, ISAc);
+            SAIX_LAUNCHED();
+        }
+        handled = true;
+    } else if ((i64)(m - D) <= m / 32) {
+        SAIX_TRY(resolve_ties(c, EqPacked{k0}, m, m - D, v0, k1, SAc, ISAc, handled));
+    }
+    if (handled) {
+        if ((size_t)depth >= g_trace.size()) g_trace.resize((size_t)depth + 1);
+        g_trace[(size_t)depth] = LevelRec{L.n, (i64)sigma, m, (i64)D};
+        g_trace.resize((size_t)depth + 1);
+        if (trace_on())
+            fprintf(stderr, "[saix dc3] depth %d: N=%lld text=u8 sigma=%llu m=%lld names=%u naming=window%d%s\n",
+                    depth, (long long)L.n, (unsigned long long)sigma, (long long)m, D, WN_CHARS,
+                    (i64)D == m ? " (unique)" : " (ties resolved)");
+    }
+    ar.reset(mark);
+    return SAIX_OK;
+}
+
 static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA, u32 *ISA, u32 *Phi,
                             bool *phi_done, int depth) {
     Arena &ar = *c.ar;
@@ -2252,7 +2444,10 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     const bool gather = N + 4 * m <= RS_GATHER_BYTES;
     u32 *SAc = gather ? ar.alloc<u32>(m) : nullptr;
     SAIX_ARENA_OK(ar);
-    SAIX_TRY(sort_samples<u8>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth, false, nullptr));
+    bool windowed = false;
+    if (sigma <= 7 && m >= 4096 && window_naming_on())
+        SAIX_TRY(window_rank(c, text, N, sigma, L, SAc, ISAc, d_scal, depth, windowed));
+    if (!windowed) SAIX_TRY(sort_samples<u8>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth, false, nullptr));
 
     // 1: sample records in rank order
     uint4 *RS = ar.alloc<uint4>(m);
@@ -2534,4 +2729,11 @@ extern "C" int saix_dc3_trace(int64_t *out, int max_levels) {
         out[4 * i + 3] = g_trace[i].names;
     }
     return n;
+}
+
+extern "C" int saix_dc3_set_window_naming(int on) {
+    window_naming_on();
+    const int old = g_window_naming;
+    g_window_naming = on ? 1 : 0;
+    return old;
 }

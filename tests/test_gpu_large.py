@@ -78,3 +78,31 @@ def test_long_repeat_text():
     sa, rank = oracle.dc3(t.ranks, 4)
     assert np.array_equal(ix.sa, sa)
     assert np.array_equal(sx.build_lcp(t, ix).lcp, oracle.lcp(t.ranks, sa, rank))
+
+
+@pytest.mark.parametrize("n,copies,seglen", [(300_000, 1500, 40), (120_000, 300, 25), (60_000, 40, 80)])
+def test_window_naming_with_planted_repeats(n, copies, seglen):
+    """Level-0 window naming with a few percent of tied 21-character windows:
+    the ties go through prefix doubling (resolve_ties), the result must equal
+    the oracle's DC3 exactly."""
+    rng = np.random.default_rng(n + copies)
+    t = rng.integers(1, 5, n)
+    seg = rng.integers(1, 5, seglen)
+    for p in rng.integers(0, n - seglen, copies):
+        t[p:p + seglen] = seg
+    text = sx.RankedText(ranks=t, sigma=4)
+    got = sx.build_sa_dc3(text)
+    sa, rank = oracle.dc3(t, 4)
+    assert np.array_equal(got.sa, sa)
+    assert np.array_equal(got.rank, rank)
+    assert np.array_equal(sx.build_lcp(text, got).lcp, oracle.lcp(t, sa, rank))
+
+
+@pytest.mark.parametrize("sigma", [5, 6, 7])
+def test_window_naming_wider_alphabets(sigma):
+    rng = np.random.default_rng(sigma)
+    t = rng.integers(1, sigma + 1, 200_000)
+    t[rng.integers(0, len(t), 50)] = 1  # a rare low character (separator-like)
+    text = sx.RankedText(ranks=t, sigma=sigma)
+    sa, rank = oracle.dc3(t, sigma)
+    assert np.array_equal(sx.build_sa_dc3(text).sa, sa)

@@ -66,3 +66,10 @@ for what in "$@"; do
     ncu_store2) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_crc|k_unpack|k_put|k_ps_|k_pairs" --csv --log-file $O/store_launches.csv python bench.py --workload store --steps 1 --warmup 3 --no-cpu-baseline --no-prof > $O/ncu_store.log 2>&1; python tools/ncu_summary.py $O/store_launches.csv 20 > $O/store_launches.txt; head -12 $O/store_launches.txt ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    c2nowin) SAIX_WINDOW_NAMING=0 timeout 900 python bench.py --workload c2 --no-cpu-baseline > $O/bench_c2nowin.json 2> $O/bench_c2nowin.err; tail -c 300 $O/bench_c2nowin.json ;;
+    largetests) timeout 1500 python -m pytest tests/test_gpu_large.py tests/test_gpu_parity.py tests/test_gpu_batch.py -x -q > $O/largetests.log 2>&1; tail -15 $O/largetests.log ;;
+    traces) for w in c2 c3; do SAIX_TRACE=1 timeout 600 python tools/profile_once.py $( [ $w = c3 ] && echo 268435456 || echo c2 ) 2>&1 | grep "saix dc3" | sort | uniq -c > $O/trace_$w.txt; cat $O/trace_$w.txt; done ;;
+  esac
+done
