@@ -212,6 +212,10 @@ int plcp_from_phi(const u8 *text, i64 n, u32 *phi_plcp, void *ws, size_t ws_byte
 int dc3_compute(const void *text, int text_bytes, i64 n, i64 sigma, u32 *sa, u32 *isa, void *ws,
                 size_t ws_bytes, saix_dc3_probe *probe, cudaStream_t stream, u32 *phi = nullptr,
                 bool *phi_done = nullptr);
+// Per-thread override of the level-0 window naming (-1: the global setting);
+// returns the previous override.  The batched-pairs path turns it off: its
+// planted pair overlaps leave long tied runs that the recursion handles better.
+int dc3_window_naming_override(int v);
 
 // L2 eviction-priority hints (sm_80+ createpolicy / L2::cache_hint): random
 // gather targets that should stay on chip are loaded / stored evict_last,

@@ -1267,7 +1267,14 @@ static thread_local std::vector<LevelRec> g_trace;
 // turns it off (the reference recursion runs; A/B measurement and the
 // reference level trace for the section 8(d) model)
 static int g_window_naming = -1;
+static thread_local int g_window_override = -1;
+int dc3_window_naming_override(int v) {
+    const int old = g_window_override;
+    g_window_override = v;
+    return old;
+}
 static bool window_naming_on() {
+    if (g_window_override >= 0) return g_window_override != 0;
     if (g_window_naming < 0) {
         const char *e = getenv("SAIX_WINDOW_NAMING");
         g_window_naming = (e && e[0] == '0') ? 0 : 1;
@@ -2732,7 +2739,10 @@ extern "C" int saix_dc3_trace(int64_t *out, int max_levels) {
 }
 
 extern "C" int saix_dc3_set_window_naming(int on) {
-    window_naming_on();
+    if (g_window_naming < 0) {
+        const char *e = getenv("SAIX_WINDOW_NAMING");
+        g_window_naming = (e && e[0] == '0') ? 0 : 1;
+    }
     const int old = g_window_naming;
     g_window_naming = on ? 1 : 0;
     return old;

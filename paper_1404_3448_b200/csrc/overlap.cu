@@ -935,7 +935,12 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
         return SAIX_OK;
     }
     int sigma = keep_n ? 7 : 6;  // terminator 1, separator 2, residues 3..6 (N 7)
-    SAIX_TRY(dc3_compute(w.X, 1, nx, sigma, w.sa, nullptr, w.dc3, w.dc3_bytes, nullptr, st));
+    {
+        const int prev = dc3_window_naming_override(0);
+        const int rc = dc3_compute(w.X, 1, nx, sigma, w.sa, nullptr, w.dc3, w.dc3_bytes, nullptr, st);
+        dc3_window_naming_override(prev);
+        SAIX_TRY(rc);
+    }
     // stable partition by pair id: each pair's suffixes keep their order
     u32 *sap = nullptr;
     int pbits = P > 1 ? bits_for((u64)(P - 1)) : 0;
