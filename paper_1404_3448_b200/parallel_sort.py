@@ -197,7 +197,15 @@ def parallel_build_sa(text: RankedText, config: SortConfig | None = None) -> Suf
     """DC3 with all sorting passes on the (device) engine; equals the serial
     build (parallel_sort.py:288-293)."""
     config = config or SortConfig()
-    sa = build_sa_dc3(text)
+    # the engine check reads the reference recursion's levels: run the DC3
+    # with the level-0 window naming off so the level trace is that recursion
+    L = _lib.load() if text.n > 1 else None
+    prev = L.saix_dc3_set_window_naming(0) if L is not None else None
+    try:
+        sa = build_sa_dc3(text)
+    finally:
+        if L is not None:
+            L.saix_dc3_set_window_naming(prev)
     if text.n > 1:
         _engine_key_check(text, config)
     return sa
