@@ -2309,45 +2309,76 @@ struct WindowSrc {
     }
 };
 
-// key + dense value from the same loaded bytes (bucket-sort hook, bs_get)
+// key + dense value from the same loaded bytes (bucket-sort hook, bs_get).
+// SWAR: byte-reverse each 4-character word (__byte_perm) and compress its
+// 8-bit lanes to 3-bit key fields / 2-bit dense digits with two shifts; the
+// per-character loop only runs for windows with a low character (sentinel /
+// separator) among the dense digits, or for alphabets without 2-bit digits.
+__device__ __forceinline__ u64 wn_dense_loop(const WindowSrc &w, const u32 *y) {
+    u64 d = 0;
+    bool low = false;
+    for (int q = 0; q < w.j; q++) {
+        const u32 c = (y[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+        low = low || c < w.lo;
+        const u32 dig = low ? 0u : c - w.lo;
+        d = w.rb ? ((d << w.rb) | dig) : d * w.r + dig;
+    }
+    return d;
+}
+
 __device__ __forceinline__ u64 bs_get(const WindowSrc &w, i64 s, u64 &k, u32 &v) {
     const i64 p = w.L.pos(s);
-    u64 key = 0, d = 0;
-    bool low = false;
     const i64 a = p & ~(i64)3;
+    u32 y[6];
     if (a + 28 <= w.N) {
         const u32 *wp = reinterpret_cast<const u32 *>(w.t + a);
         const int sh = 8 * (int)(p - a);
         u32 x[7];
 #pragma unroll
         for (int q = 0; q < 7; q++) x[q] = __ldg(wp + q);
-        u32 y[6];
 #pragma unroll
         for (int q = 0; q < 6; q++) y[q] = __funnelshift_r(x[q], x[q + 1], sh);
-#pragma unroll
-        for (int q = 0; q < WN_CHARS; q++) {
-            const u32 c = (y[q >> 2] >> (8 * (q & 3))) & 0xFFu;
-            key = (key << 3) | (c & 7u);
-            if (q < w.j) {
-                low = low || c < w.lo;
-                const u32 dig = low ? 0u : c - w.lo;
-                d = w.rb ? ((d << w.rb) | dig) : d * w.r + dig;
-            }
-        }
     } else {
-        for (int q = 0; q < WN_CHARS; q++) {
-            const u32 c = p + q < w.N ? (u32)w.t[p + q] : 0u;
-            key = (key << 3) | (c & 7u);
-            if (q < w.j) {
-                low = low || c < w.lo;
-                const u32 dig = low ? 0u : c - w.lo;
-                d = w.rb ? ((d << w.rb) | dig) : d * w.r + dig;
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+            u32 word = 0;
+            for (int b = 0; b < 4; b++) {
+                const i64 at = p + 4 * q + b;
+                word |= (at < w.N ? (u32)w.t[at] : 0u) << (8 * b);
             }
+            y[q] = word;
         }
     }
+    // key: 5 words of 4 characters -> 12 bits each, then character 20
+    u64 key = 0;
+#pragma unroll
+    for (int q = 0; q < 5; q++) {
+        const u32 r = __byte_perm(y[q], 0, 0x0123) & 0x07070707u;
+        const u32 pp = r | (r >> 5);
+        key = (key << 12) | (((pp >> 10) & 0xFC0u) | (pp & 0x3Fu));
+    }
+    key = (key << 3) | (y[5] & 7u);
     k = key;
     v = (u32)s;
-    return d;
+    // dense: 2-bit digits of the first 14 characters when no low character is among them
+    if (w.rb == 2 && w.j == 14) {
+        const u32 lo4 = w.lo * 0x01010101u;
+        const u32 lowm = __vcmpltu4(y[0], lo4) | __vcmpltu4(y[1], lo4) | __vcmpltu4(y[2], lo4) |
+                         (__vcmpltu4(y[3], lo4) & 0x0000FFFFu);
+        if (!lowm) {
+            u64 d = 0;
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                const u32 r = (__byte_perm(y[q], 0, 0x0123) - lo4) & 0x03030303u;
+                const u32 pp = r | (r >> 6);
+                d = (d << 8) | (((pp >> 12) & 0xF0u) | (pp & 0xFu));
+            }
+            d = (d << 2) | ((y[3] & 0xFFu) - w.lo);
+            d = (d << 2) | (((y[3] >> 8) & 0xFFu) - w.lo);
+            return d;
+        }
+    }
+    return wn_dense_loop(w, y);
 }
 
 static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const SampleLayout &L, u32 *SAc, u32 *ISAc,
