@@ -1758,37 +1758,51 @@ __global__ void k_tie_split(const u32 *__restrict__ rs, const u32 *__restrict__ 
     }
 }
 
-// Resolve the tied groups of the sorted samples (keys/S from the naming sort)
-// into ISAc (and SAc when asked).  ok = false: too many / too long ties, the
-// caller recurses instead (nothing has been written to ISAc / SAc then).
-template <class Eq>
-static int resolve_ties(Dc3Ctx &c, Eq eq, i64 m, i64 ties, u32 *S, u64 *kk, u32 *SAc, u32 *ISAc, bool &ok) {
-    Arena &ar = *c.ar;
+// One pass over sorted keys: distinct count and the tied runs (head, length)
+// of <= TIE_MAX_RUN members (longer runs or more than cap -> overflow)
+__global__ void k_count_runs(const u64 *__restrict__ keys, i64 m, u32 *__restrict__ count, u32 *__restrict__ rs,
+                             u32 *__restrict__ rl, u32 *__restrict__ nruns, u32 cap, u32 *__restrict__ overflow) {
+    u32 c = 0;
+    for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (i64)gridDim.x * blockDim.x) {
+        const u64 k = keys[r];
+        const bool head = r == 0 || keys[r - 1] != k;
+        c += head;
+        if (head && r + 1 < m && keys[r + 1] == k) {
+            i64 e = r + 2;
+            while (e < m && e - r <= TIE_MAX_RUN && keys[e] == k) e++;
+            if (e - r > TIE_MAX_RUN) {
+                atomicMax(overflow, 1u);
+                continue;
+            }
+            const u32 at = atomicAdd(nruns, 1u);
+            if (at < cap) {
+                rs[at] = (u32)r;
+                rl[at] = (u32)(e - r);
+            } else {
+                atomicMax(overflow, 1u);
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane_id() == 0 && c) atomicAdd(count, c);
+}
+// members of every tied run take the run head as group id
+__global__ void k_tie_groups(const u32 *__restrict__ rs, const u32 *__restrict__ rl, const u32 *__restrict__ nruns,
+                             const u32 *__restrict__ S, u32 *__restrict__ G) {
+    const u32 nr = *nruns;
+    for (u32 q = (u32)((i64)blockIdx.x * blockDim.x + threadIdx.x); q < nr; q += gridDim.x * blockDim.x) {
+        const u32 s0 = rs[q], len = rl[q];
+        for (u32 x = s0 + 1; x < s0 + len; x++) G[S[x]] = s0;
+    }
+}
+
+// Prefix-doubling rounds over the tied runs (rsA/rlA, nr0 of them; G holds
+// every sample's group id = its run head or its own rank): each round keys
+// the members by G[s + h], sorts every run, and splits it where keys change.
+static int tie_rounds(Dc3Ctx &c, i64 m, i64 ties, u32 *S, u64 *kk, u32 *ISAc, u32 *rsA, u32 *rlA, u32 *rsB,
+                      u32 *rlB, u32 *mid, u32 *big, u32 *scal, u32 nr0) {
     cudaStream_t st = c.st;
-    ok = false;
-    size_t mark = ar.mark();
-    u32 cap = (u32)(ties + 64);
-    u32 *head = ar.alloc<u32>(m);
-    u32 *rsA = ar.alloc<u32>(cap), *rlA = ar.alloc<u32>(cap), *rsB = ar.alloc<u32>(cap), *rlB = ar.alloc<u32>(cap);
-    u32 *mid = ar.alloc<u32>(cap), *big = ar.alloc<u32>(cap);
-    u32 *scal = ar.alloc<u32>(16);  // [0] mid, [1] big, [2] runs A, [3] runs B, [4] overflow
-    SAIX_ARENA_OK(ar);
-    SAIX_CUDA(cudaMemsetAsync(scal, 0, 16 * 4, st));
-    {
-        Prof prof_("dc3.tie_resolve", 8.0 * m, st);
-        k_tie_init<Eq><<<grid_for(m, 256), 256, 0, st>>>(eq, m, head, rsA, rlA, scal + 2, cap, scal + 4);
-    }
-    SAIX_LAUNCHED();
-    u32 h2[3];
-    SAIX_CUDA(cudaMemcpyAsync(h2, scal + 2, 12, cudaMemcpyDeviceToHost, st));
-    SAIX_CUDA(cudaStreamSynchronize(st));
-    if (h2[2]) {
-        ar.reset(mark);
-        return SAIX_OK;
-    }
-    // G[S[r]] = head(r): the (mostly unique) group ids through the bucketed scatter
-    SAIX_TRY(scatter_u32(ar, S, head, m, m, ISAc, st, "dc3.tie_scatter"));
-    u32 nr = h2[0];
+    u32 nr = nr0;
     u32 *rs = rsA, *rl = rlA, *rs2 = rsB, *rl2 = rlB;
     u32 *cnt_cur = scal + 2, *cnt_next = scal + 3;
     Prof prof_("dc3.tie_resolve", 24.0 * ties, st);
@@ -1841,6 +1855,40 @@ static int resolve_ties(Dc3Ctx &c, Eq eq, i64 m, i64 ties, u32 *S, u64 *kk, u32 
         t = rl; rl = rl2; rl2 = t;
         t = cnt_cur; cnt_cur = cnt_next; cnt_next = t;
     }
+    return SAIX_OK;
+}
+
+// Resolve the tied groups of the sorted samples (keys/S from the naming sort)
+// into ISAc (and SAc when asked).  ok = false: too many / too long ties, the
+// caller recurses instead (nothing has been written to ISAc / SAc then).
+template <class Eq>
+static int resolve_ties(Dc3Ctx &c, Eq eq, i64 m, i64 ties, u32 *S, u64 *kk, u32 *SAc, u32 *ISAc, bool &ok) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    ok = false;
+    size_t mark = ar.mark();
+    u32 cap = (u32)(ties + 64);
+    u32 *head = ar.alloc<u32>(m);
+    u32 *rsA = ar.alloc<u32>(cap), *rlA = ar.alloc<u32>(cap), *rsB = ar.alloc<u32>(cap), *rlB = ar.alloc<u32>(cap);
+    u32 *mid = ar.alloc<u32>(cap), *big = ar.alloc<u32>(cap);
+    u32 *scal = ar.alloc<u32>(16);  // [0] mid, [1] big, [2] runs A, [3] runs B, [4] overflow
+    SAIX_ARENA_OK(ar);
+    SAIX_CUDA(cudaMemsetAsync(scal, 0, 16 * 4, st));
+    {
+        Prof prof_("dc3.tie_resolve", 8.0 * m, st);
+        k_tie_init<Eq><<<grid_for(m, 256), 256, 0, st>>>(eq, m, head, rsA, rlA, scal + 2, cap, scal + 4);
+    }
+    SAIX_LAUNCHED();
+    u32 h2[3];
+    SAIX_CUDA(cudaMemcpyAsync(h2, scal + 2, 12, cudaMemcpyDeviceToHost, st));
+    SAIX_CUDA(cudaStreamSynchronize(st));
+    if (h2[2]) {
+        ar.reset(mark);
+        return SAIX_OK;
+    }
+    // G[S[r]] = head(r): the (mostly unique) group ids through the bucketed scatter
+    SAIX_TRY(scatter_u32(ar, S, head, m, m, ISAc, st, "dc3.tie_scatter"));
+    SAIX_TRY(tie_rounds(c, m, ties, S, kk, ISAc, rsA, rlA, rsB, rlB, mid, big, scal, h2[0]));
     if (SAc) SAIX_CUDA(cudaMemcpyAsync(SAc, S, (size_t)m * 4, cudaMemcpyDeviceToDevice, st));
     ar.reset(mark);
     ok = true;
@@ -2415,15 +2463,26 @@ static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const Sample
         ar.reset(mark);
         return SAIX_OK;
     }
-    SAIX_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(u32), st));
+    // distinct windows and the tied runs in one pass
+    const u32 cap = (u32)(m / 32 + 64);
+    u32 *rsA = ar.alloc<u32>(cap), *rlA = ar.alloc<u32>(cap), *rsB = ar.alloc<u32>(cap), *rlB = ar.alloc<u32>(cap);
+    u32 *mid = ar.alloc<u32>(cap), *big = ar.alloc<u32>(cap);
+    u32 *scal = ar.alloc<u32>(16);  // [0] mid, [1] big, [2] runs A, [3] runs B, [4] overflow, [5] distinct
+    SAIX_ARENA_OK(ar);
+    SAIX_CUDA(cudaMemsetAsync(scal, 0, 16 * 4, st));
     {
         Prof prof_("dc3.count_names", 8.0 * m, st);
-        k_count_distinct<<<grid_for(m, K_THREADS, kNumSMs * 8), K_THREADS, 0, st>>>(k0, m, d_scal);
+        k_count_runs<<<grid_for(m, K_THREADS, kNumSMs * 8), K_THREADS, 0, st>>>(k0, m, scal + 5, rsA, rlA, scal + 2,
+                                                                               cap, scal + 4);
     }
     SAIX_LAUNCHED();
-    u32 D = 0;
-    SAIX_TRY(read_u32(d_scal, &D, st));
-    if ((i64)D == m) {
+    u32 h6[6];
+    SAIX_CUDA(cudaMemcpyAsync(h6, scal, 24, cudaMemcpyDeviceToHost, st));
+    SAIX_CUDA(cudaStreamSynchronize(st));
+    const u32 D = h6[5];
+    const bool tie_ok = (i64)D < m && (i64)(m - D) <= m / 32 && !h6[4];
+    if ((i64)D == m || tie_ok) {
+        // ranks = sorted positions (the ties' order is fixed below)
         if (m >= kDirectScatterItems) {
             PsPlan pu = PsPlan::of(m, 4);
             pu.set_cursors(ar.alloc<u32>(pu.cursor_words()));
@@ -2448,9 +2507,16 @@ static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const Sample
             k_unique_from_sorted<<<grid_for(m, K_THREADS), K_THREADS, 0, st>>>(v0, m, SAc, ISAc);
             SAIX_LAUNCHED();
         }
+        if (tie_ok) {
+            {
+                Prof prof_("dc3.tie_resolve", 12.0 * (m - D), st);
+                k_tie_groups<<<grid_for(h6[2], 128), 128, 0, st>>>(rsA, rlA, scal + 2, v0, ISAc);
+            }
+            SAIX_LAUNCHED();
+            SAIX_TRY(tie_rounds(c, m, m - D, v0, k1, ISAc, rsA, rlA, rsB, rlB, mid, big, scal, h6[2]));
+            if (SAc) SAIX_CUDA(cudaMemcpyAsync(SAc, v0, (size_t)m * 4, cudaMemcpyDeviceToDevice, st));
+        }
         handled = true;
-    } else if ((i64)(m - D) <= m / 32) {
-        SAIX_TRY(resolve_ties(c, EqPacked{k0}, m, m - D, v0, k1, SAc, ISAc, handled));
     }
     if (handled) {
         if ((size_t)depth >= g_trace.size()) g_trace.resize((size_t)depth + 1);
