@@ -79,3 +79,8 @@ for what in "$@"; do
     c2direct) SAIX_WN_DIRECT=1 timeout 900 python bench.py --workload c2 --no-cpu-baseline > $O/bench_c2direct.json 2> $O/bench_c2direct.err; tail -c 200 $O/bench_c2direct.json ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    c2dm) SAIX_WN_DIRECT_MAX=20000000 timeout 900 python bench.py --workload c2 --no-cpu-baseline > $O/bench_c2dm.json 2> $O/bench_c2dm.err; tail -c 200 $O/bench_c2dm.json ;;
+  esac
+done
