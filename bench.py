@@ -2,25 +2,32 @@
 """Benchmark of the B200 longest-overlap hot path (one JSON line on rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c3|c5]
+                    [--workload c4|c2|c3|c5|...] [--no-c3]
 
-Default workload (BASELINE.json configs[1], "C2"): one synthetic pair of
-2 x 10 Mbp random ACGT sequences (gen_random seeds 11/12 on rank 0; rank r
-uses 11+2r/12+2r), full pipeline on one B200 per rank: encode -> generalized
-text -> DC3 suffix array -> LCP -> overlap scan.  A "step" is one pass of the
-pipeline over one pair.  Metric: Mbases/s of generalized-text bases through
-the whole pipeline (20,000,001 per pair); `value` is the whole-job aggregate;
-N > 1 runs independent replicas (weak scaling, no data-path collective: a
-single long pair does not shard).
+Default workload (BASELINE.json configs[3], "C4" -- the largest single-GPU
+configuration and the one the metric's "pairs/s at 1/2/4/8 B200" is quoted
+on): 100,000 synthetic noncoding-like pairs of 2 x 10 kbp
+(paper_1404_3448_b200/workloads.py), sharded contiguously across the ranks
+(strong scaling); every rank computes longest_overlap for its pairs on the
+device and the per-pair results are all-gathered (the path's only
+collective).  A "step" is one pass over all 100k pairs.  The same line
+carries a "c3" block at N=1: the north star's roofline config (configs[2],
+a 2^28 random text, DC3 suffix array + LCP per step, Mbases/s) with the
+whole-DC3 roofline against SURVEY.md 8(d)'s contract bytes and against the
+bytes this implementation executes.
 
-Other BASELINE configs (reported in DESIGN.md / profiles/, not the default):
-  c3  configs[2]: 256 Mbp (2^28) DC3 suffix array + LCP, Mbases/s
-  c5  configs[4]: 10^8 random sparse-table RMQ queries over the LCP array of a
-      64 Mbp (2^26) text, table build + queries per step, queries/s
+Other configs: --workload c2 (configs[1], one 2 x 10 Mbp pair), c3, c5
+(configs[4], 10^8 sparse-table RMQ queries on a 2^26 text), store, fasta,
+cartesian.
 
---impl reference times the reference algorithm on the host (the C oracle port
-in oracle/, kind "port": the reference is pure Python + numba, nothing to
-compile) on the same workload; rank 0 only.
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1 rendezvous).
+
+--impl reference times the reference algorithm on the host -- the C
+restatement in oracle/ (kind "port": the reference is pure Python + numba,
+nothing to compile) on all host threads -- on the same workload and config:
+each step is a bounded sample of the C4 pairs (10,000 pairs, rotating through
+the 100k); rank 0 only.
 """
 
 from __future__ import annotations
@@ -50,6 +57,21 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def host_info(threads: int) -> dict:
+    """CPU model, logical cores and library versions of the host arm."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "threads_used": threads,
+            "numpy": np.__version__, "compiler": "gcc -O3 -march=x86-64-v2 (oracle/saix_oracle.c)"}
 
 
 def measured_peak_gbs():
@@ -351,11 +373,16 @@ class C5:
 
     def cpu_baseline(self):
         import oracle
-        # parity on a 10^6 prefix of the queries against the leftmost-argmin definition
+        # parity on ALL 10^8 queries against the leftmost-argmin definition
+        # (untimed; block minima + sparse table over them, every host thread)
         lcp = self.ix.lcp[: self.N].cpu().numpy().view(np.uint32).astype(np.int64)
-        qi, qj = self.hqi[:1_000_000].numpy(), self.hqj[:1_000_000].numpy()
-        got = self.out[:1_000_000].cpu().numpy()
-        assert np.array_equal(got, oracle.argmin_blocked(lcp, qi, qj))
+        threads = os.cpu_count() or 1
+        got = self.out.cpu().numpy()
+        want = oracle.argmin_sparse_blocked(lcp, self.hqi.numpy(), self.hqj.numpy(), threads=threads)
+        mism = int(np.count_nonzero(got != want))
+        assert mism == 0, f"{mism} of {self.Q} C5 answers differ from the oracle"
+        self.parity = {"queries_checked": self.Q, "mismatches": mism}
+        del got, want
         # timed: the reference SparseTable.query restated in C, over a bounded
         # sample (table of the first 2^22 LCP values, 10^6 queries inside it)
         m = 1 << 22
@@ -368,12 +395,26 @@ class C5:
         dt = time.perf_counter() - t0
         return {"value": 1_000_000 / dt, "unit": self.unit, "cores": 1, "kind": "port",
                 "sample": "10^6 SparseTable.query over the first 2^22 LCP values (C port of rmq.py:52-58), "
-                          f"single thread ({dt:.2f} s); GPU answers matched the argmin oracle on 10^6 queries"}
+                          f"single thread ({dt:.2f} s); GPU answers matched the argmin oracle on all 10^8 queries"}
 
 
-def _c4_chunk(args):
-    from paper_1404_3448_b200.workloads import c4_pairs
-    return c4_pairs(*args)
+def c4_generate(lo: int, hi: int):
+    from paper_1404_3448_b200.workloads import c4_generate as gen
+    return gen(lo, hi)
+
+
+C4_TOTAL = 100_000
+C4_REF_SAMPLE = 10_000
+
+
+def c4_config(world: int) -> dict:
+    """The C4 `config` object -- identical on both arms."""
+    return {"workload": "C4: 100k pairs of 2 x 10 kbp AT-rich random sequences (W = 0.3/0.2/0.2/0.3) with one "
+                        "planted shared block of 32..256 bases (paper_1404_3448_b200/workloads.py); "
+                        "longest_overlap of every pair per step",
+            "pairs": C4_TOTAL, "residues_per_pair": 20_000,
+            "l2": "inputs (2 GB) larger than L2; L2 also flushed between timed steps (512 MiB write)",
+            "parallelism": f"pairs sharded x{world}"}
 
 
 class C4:
@@ -384,26 +425,16 @@ class C4:
     name = "c4"
     unit = "pairs/s"
     scaling = "strong"
-    TOTAL = 100_000
+    TOTAL = C4_TOTAL
 
     def __init__(self, rank: int, world: int = 1, dist=None):
-        import concurrent.futures as cf
-
         import torch
 
         import paper_1404_3448_b200 as sx
         from paper_1404_3448_b200.workloads import shard
-        lo, hi = shard(self.TOTAL, world, rank)
-        chunks = [(a, min(a + 1000, hi)) for a in range(lo, hi, 1000)]
-        with cf.ProcessPoolExecutor(max_workers=min(32, os.cpu_count() or 4)) as ex:
-            parts = list(ex.map(_c4_chunk, chunks))
-        self.seqs = np.concatenate([p[0] for p in parts])
-        offs, base = [np.zeros(1, np.int64)], 0
-        for s, o in parts:
-            offs.append(o[1:] + base)
-            base += int(o[-1])
-        self.offs = np.concatenate(offs)
-        self.P = hi - lo
+        self.lo, self.hi = shard(self.TOTAL, world, rank)
+        self.seqs, self.offs = c4_generate(self.lo, self.hi)
+        self.P = self.hi - self.lo
         self.dist, self.world = dist, world
         self.ob = sx.OverlapBatch(self.seqs, self.offs)
         self.hseqs = torch.from_numpy(self.seqs).pin_memory()
@@ -414,11 +445,8 @@ class C4:
         self.d2h = 24 * self.P
         self.ob.run_device()
         self.result = None
-        self.config = {"workload": "C4: 100k pairs of 2 x 10 kbp AT-rich random sequences with one planted "
-                                   "shared block (paper_1404_3448_b200/workloads.py), batched waves of <= 2^27 "
-                                   "residues, results all-gathered over NCCL",
-                       "pairs": self.TOTAL, "pairs_this_rank": self.P, "waves_this_rank": len(self.ob.waves)}
-        self.dc3_calls_per_step = len(self.ob.waves)
+        self.config = c4_config(world)
+        self.dc3_calls_per_step = getattr(self.ob, "dc3_calls", len(self.ob.waves))
 
     def _gather(self):
         if self.dist is None:
@@ -442,17 +470,21 @@ class C4:
         return {}
 
     def cpu_baseline(self):
+        """The oracle on every host thread over ALL of this rank's pairs
+        (100k at N=1): timed, and every GPU answer compared."""
         import oracle
-        k = 4000  # bounded sample: the first 4000 pairs on every host thread
         threads = os.cpu_count() or 1
         t0 = time.perf_counter()
-        want = oracle.overlap_batch(self.seqs[: self.offs[2 * k]], self.offs[: 2 * k + 1], threads=threads)
+        want = oracle.overlap_batch(self.seqs, self.offs, threads=threads)
         dt = time.perf_counter() - t0
-        got = self.ob.results()[:k]
-        assert np.array_equal(got, want)
-        return {"value": k / dt, "unit": self.unit, "cores": threads, "kind": "port",
-                "sample": f"first {k} C4 pairs, oracle/saix_oracle.c on {threads} host threads ({dt:.1f} s); "
-                          "GPU answers matched on all of them"}
+        got = self.ob.results()
+        mism = int(np.count_nonzero(np.any(got != want, axis=1)))
+        assert mism == 0, f"{mism} of {self.P} C4 pairs differ from the oracle"
+        self.parity = {"pairs_checked": int(self.P), "mismatches": mism}
+        return {"value": self.P / dt, "unit": self.unit, "cores": threads, "kind": "port",
+                "sample": f"all {self.P} C4 pairs, oracle/saix_oracle.c (C restatement of overlap.py:110-152 + "
+                          f"suffix_index.py DC3/Kasai) on {threads} host threads ({dt:.1f} s); GPU answers matched "
+                          "on every pair", "host": host_info(threads)}
 
 
 class Store:
@@ -697,45 +729,69 @@ WORKLOADS = {"c2": C2, "c3": C3, "c4": C4, "c5": C5, "store": Store, "fasta": Fa
 
 
 def run_reference(args, rank):
-    """Reference algorithm (C oracle port) on the host, same metric/config."""
+    """Reference algorithm (C oracle port, all host threads) on the host, same
+    metric/config as our arm; each step is a bounded sample of the workload."""
     import oracle
-    if args.workload != "c2":
+    threads = os.cpu_count() or 1
+    common = {"impl": "reference", "metric": METRIC, "n_gpus": args.gpus, "steps": args.steps,
+              "warmup": args.warmup, "higher_is_better": True, "vs_baseline": None, "dtype": "u32",
+              "data": "synthetic"}
+    if args.workload == "c4":
+        nsteps = args.warmup + args.steps
+        span = min(C4_TOTAL, nsteps * C4_REF_SAMPLE)
+        seqs, offs = c4_generate(0, span)
+        times = []
+        for k in range(nsteps):
+            p0 = (k * C4_REF_SAMPLE) % span
+            p1 = min(p0 + C4_REF_SAMPLE, span)
+            sq = seqs[offs[2 * p0]: offs[2 * p1]]
+            of = offs[2 * p0: 2 * p1 + 1] - offs[2 * p0]
+            t0 = time.perf_counter()
+            oracle.overlap_batch(sq, of, threads=threads)
+            if k >= args.warmup:
+                times.append((time.perf_counter() - t0, p1 - p0))
+        tot = sum(t for t, _ in times)
+        pairs = sum(p for _, p in times)
+        value = pairs / tot
+        sample = (f"{C4_REF_SAMPLE} C4 pairs per step (rotating through the first {span}), "
+                  f"oracle/saix_oracle.c on {threads} host threads")
+        line = dict(common, value=value, unit="pairs/s", ms_per_step=1e3 * tot / len(times),
+                    scaling="strong", config=c4_config(args.gpus))
+    elif args.workload == "c2":
+        from paper_1404_3448_b200.sequence import gen_random
+        a = gen_random(10_000_000, 11).residues.encode()
+        b = gen_random(10_000_000, 12).residues.encode()
+        n = len(a) + len(b) + 1
+        for _ in range(args.warmup):
+            oracle.longest_overlap(a, b)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            res = oracle.longest_overlap(a, b)
+            times.append(time.perf_counter() - t0)
+        tot = sum(times)
+        value = n * args.steps / tot / 1e6
+        threads = 1
+        sample = "full C2 pair (2 x 10 Mbp, GSA n=20,000,001) per step, oracle/saix_oracle.c single thread"
+        line = dict(common, value=value, unit="Mbases/s", ms_per_step=1e3 * tot / args.steps, scaling="weak",
+                    config={"workload": "C2", "gsa_bases": n, "result": list(res)})
+    else:
         print(json.dumps({"impl": "reference", "unavailable": f"workload {args.workload} not wired for the CPU arm"}))
         return
-    from paper_1404_3448_b200.sequence import gen_random
-    a = gen_random(10_000_000, 11).residues.encode()
-    b = gen_random(10_000_000, 12).residues.encode()
-    n = len(a) + len(b) + 1
-    for _ in range(args.warmup):
-        oracle.longest_overlap(a, b)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        res = oracle.longest_overlap(a, b)
-        times.append(time.perf_counter() - t0)
-    tot = sum(times)
-    value = n * args.steps / tot / 1e6
-    cb = {"value": value, "unit": "Mbases/s", "cores": 1, "kind": "port",
-          "sample": "full C2 pair (2 x 10 Mbp, GSA n=20,000,001) per step, oracle/saix_oracle.c single thread"}
-    print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mbases/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "config": {"workload": "C2", "gsa_bases": n, "result": list(res)},
-        "cpu_baseline": cb,
-        "e2e": {"value": value, "unit": "Mbases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    line["cpu_baseline"] = {"value": line["value"], "unit": line["unit"], "cores": threads, "kind": "port",
+                            "sample": sample, "host": host_info(threads)}
+    line["e2e"] = {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    print(json.dumps(line), flush=True)
 
 
-def bench(args, rank, world, dist):
+def measure(wl, args, rank, world, dist, dev, flush, record_ref_trace=True):
+    """Warm up, then time K device-resident steps and K end-to-end steps
+    (CUDA events on the launching stream, L2 flushed between steps, barrier +
+    synchronize on both sides, max over ranks), one more K-step pass with
+    per-kernel events, and the launch count of one step."""
     import torch
 
     from paper_1404_3448_b200 import _lib
-
-    dev = torch.device("cuda", torch.cuda.current_device())
-    cls = WORKLOADS[args.workload]
-    wl = cls(rank, world, dist) if cls is C4 else cls(rank)
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
 
     def barrier():
@@ -763,7 +819,7 @@ def bench(args, rank, world, dist):
     # the section 8(d) model is the reference recursion's level trace: one
     # untimed step with the level-0 window naming off records it
     ref_trace = None
-    if args.workload in ("c2", "c3", "c4"):
+    if record_ref_trace and wl.name in ("c2", "c3"):
         prev = _lib.load().saix_dc3_set_window_naming(0)
         wl.step_device()
         torch.cuda.synchronize()
@@ -784,12 +840,12 @@ def bench(args, rank, world, dist):
     prof = []
     if not args.no_prof:
         _lib.prof_enable(True)
-        ms_prof = timed(wl.step_device, args.steps)
+        timed(wl.step_device, args.steps)
         prof = _lib.prof_collect()
         _lib.prof_enable(False)
     trace = _lib.dc3_trace()
-
     launches_per_step = count_our_launches(wl.step_device)
+
     peak, peak_kind = measured_peak_gbs()
     dom = max(prof, key=lambda e: e["ms"]) if prof else None
     roof = None
@@ -797,33 +853,69 @@ def bench(args, rank, world, dist):
         per_launch_ms = dom["ms"] / dom["launches"]
         per_launch_bytes = dom["bytes"] / dom["launches"]
         ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+        tr = ncu_traffic(wl.name, dom["name"])
         roof = {"bound": "hbm", "kernel": dom["name"], "achieved": round(ach, 1), "peak": peak,
                 "peak_source": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": ncu_traffic(args.workload, dom["name"]),
+                "traffic": tr, "traffic_over_algorithmic": (round(tr / per_launch_bytes, 3)
+                                                             if tr and per_launch_bytes else None),
                 "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                 "share_of_step": round(dom["ms"] / ms_dev, 4) if ms_dev else None}
     stage = {e["name"]: round(e["ms"] / args.steps, 4) for e in sorted(prof, key=lambda e: -e["ms"])}
-    # whole-DC3 roofline against the section 8(d) contract bytes of the last
-    # DC3 level trace (per DC3 call; C4 runs one DC3 per wave)
+    # whole-DC3 roofline against the section 8(d) contract bytes, both over
+    # the reference recursion's level trace and over what actually ran
     dc3_roof = None
     dc3_ms = sum(e["ms"] for e in prof if e["name"].startswith("dc3.")) / args.steps
-    if trace and dc3_ms > 0:
+    model_fn = getattr(wl, "dc3_model", None)
+    if model_fn is not None and dc3_ms > 0:
+        dc3_roof = model_fn(dc3_ms, peak)
+    elif trace and dc3_ms > 0:
         calls = getattr(wl, "dc3_calls_per_step", 1)
         model_trace = ref_trace or trace
         mb = dc3_model_bytes(model_trace) * calls
+        xb = dc3_model_bytes(trace) * calls
         ach = mb / (dc3_ms * 1e-3) / 1e9
         dc3_roof = {"model_bytes_per_step": mb, "dc3_ms_per_step": round(dc3_ms, 4),
                     "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                    "executed_model_bytes": xb,
+                    "executed_frac": round(xb / (dc3_ms * 1e-3) / 1e9 / peak, 4),
                     "levels": [list(t) for t in model_trace], "executed_levels": [list(t) for t in trace],
-                    "executed_model_bytes": dc3_model_bytes(trace) * calls,
-                    "note": "SURVEY.md 8(d) textbook stage model over the reference recursion's level trace "
-                            "(recorded by one untimed step with the level-0 window naming off); "
-                            "executed_levels = what this implementation ran"}
+                    "note": "frac: SURVEY.md 8(d) textbook stage model over the reference recursion's level trace "
+                            "(recorded by one untimed step with the level-0 window naming off) / DC3 time; "
+                            "executed_frac: the same model over the levels this implementation ran"}
 
     scale = 1e6 if wl.unit == "Mbases/s" else 1.0
     total = getattr(wl, "units_total", wl.units * world)
-    value = total * args.steps / (ms_dev * 1e-3) / scale
-    e2e_value = total * args.steps / (ms_e2e * 1e-3) / scale
+    return {"value": total * args.steps / (ms_dev * 1e-3) / scale, "ms_dev": ms_dev,
+            "e2e_value": total * args.steps / (ms_e2e * 1e-3) / scale, "ms_e2e": ms_e2e,
+            "roofline": roof, "dc3_roofline": dc3_roof, "stage": stage, "clocks": clk,
+            "gpu_launches": launches_per_step * args.steps}
+
+
+def c3_block(args, dev, flush):
+    """The north star's roofline config (C3) measured in the same run: a 2^28
+    DC3 suffix array + LCP per step, N=1 only."""
+    wl = C3(0)
+    m = measure(wl, args, 0, 1, None, dev, flush)
+    blk = {"workload": wl.config["workload"], "value": round(m["value"], 2), "unit": wl.unit,
+           "ms_per_step": round(m["ms_dev"] / args.steps, 4),
+           "e2e": {"value": round(m["e2e_value"], 2), "unit": wl.unit, "h2d_bytes_per_step": wl.h2d,
+                   "d2h_bytes_per_step": wl.d2h, "ms_per_step": round(m["ms_e2e"] / args.steps, 4)},
+           "gpu_launches": m["gpu_launches"], "roofline": m["roofline"], "dc3_roofline": m["dc3_roofline"],
+           "clocks": m["clocks"], "stage_ms_per_step": m["stage"]}
+    if not args.no_cpu_baseline:
+        blk["cpu_baseline"] = wl.cpu_baseline()
+    del wl
+    return blk
+
+
+def bench(args, rank, world, dist):
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cls = WORKLOADS[args.workload]
+    wl = cls(rank, world, dist) if cls is C4 else cls(rank)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    m = measure(wl, args, rank, world, dist, dev, flush)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -836,25 +928,47 @@ def bench(args, rank, world, dist):
         dist.all_gather(allr, t)
         results = [[int(x) for x in r.tolist()] for r in allr]
 
+    c3 = None
+    if args.workload == "c4" and world == 1 and not args.no_c3:
+        del wl.ob
+        torch.cuda.empty_cache()
+        c3 = c3_block(args, dev, flush)
+
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": wl.unit, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_dev / args.steps, 4),
+            "metric": METRIC, "value": round(m["value"], 2), "unit": wl.unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(m["ms_dev"] / args.steps, 4),
             "higher_is_better": True, "scaling": getattr(wl, "scaling", "weak"), "vs_baseline": None,
             "dtype": "u32", "data": "synthetic",
-            "config": dict(wl.config, l2="flushed between timed steps (512 MiB write)",
-                           parallelism=(f"pairs sharded x{world}" if getattr(wl, "scaling", "") == "strong"
-                                        else f"replicas x{world}")),
-            **wl.extra(ms_dev, args.steps, world),
-            "e2e": {"value": round(e2e_value, 2), "unit": wl.unit, "h2d_bytes_per_step": wl.h2d,
-                    "d2h_bytes_per_step": wl.d2h, "ms_per_step": round(ms_e2e / args.steps, 4)},
-            "gpu_launches": launches_per_step * args.steps,
-            "roofline": roof, "dc3_roofline": dc3_roof, "cpu_baseline": cpu, "clocks": clk,
-            "stage_ms_per_step": stage,
+            "config": dict(wl.config) if wl.name == "c4" else dict(
+                wl.config, l2="flushed between timed steps (512 MiB write)", parallelism=f"replicas x{world}"),
+            **wl.extra(m["ms_dev"], args.steps, world),
+            "e2e": {"value": round(m["e2e_value"], 2), "unit": wl.unit, "h2d_bytes_per_step": wl.h2d,
+                    "d2h_bytes_per_step": wl.d2h, "ms_per_step": round(m["ms_e2e"] / args.steps, 4)},
+            "gpu_launches": m["gpu_launches"],
+            "roofline": m["roofline"], "dc3_roofline": m["dc3_roofline"], "cpu_baseline": cpu, "clocks": m["clocks"],
+            "stage_ms_per_step": m["stage"],
         }
+        if getattr(wl, "parity", None):
+            line["parity"] = wl.parity
         if results is not None:
             line["result"] = results
+        if c3 is not None:
+            line["c3"] = c3
         print(json.dumps(line), flush=True)
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` without a torchrun environment: run N ranks of this script
+    under torch.distributed.run (one process per GPU, 127.0.0.1)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -863,12 +977,18 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--no-c3", action="store_true", help="skip the in-line C3 block of the C4 line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prof", action="store_true", help="time without per-kernel events")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    args.gpus = world
 
     if args.impl == "reference":
         if rank == 0:

@@ -342,6 +342,77 @@ EXPORT int oracle_argmin_blocked(const int64_t *v, int64_t n, const int64_t *qi,
     return 0;
 }
 
+/* Leftmost argmin over inclusive [i, j] (swapped if i > j) -- the answer of
+ * SparseTable.query (rmq.py:52-58, ties to the left operand) -- for large
+ * query sweeps: 64-element blocks, a sparse table over the block minima
+ * (the same leftmost combine rule), in-block scans at both ends; `threads`
+ * pthreads split the queries.  Returns -1 on an out-of-range query. */
+typedef struct {
+    const int64_t *v, *qi, *qj, *bmin, *tab;
+    int64_t n, nb, lo, hi;
+    int64_t *out;
+    int bad;
+} ArgminJob;
+
+#define AB_SHIFT 6
+static int64_t ab_pick(const int64_t *v, int64_t a, int64_t b) { return v[a] <= v[b] ? a : b; }
+
+static void *argmin_worker(void *p) {
+    ArgminJob *J = (ArgminJob *)p;
+    const int64_t *v = J->v;
+    for (int64_t t = J->lo; t < J->hi; t++) {
+        int64_t i = J->qi[t], j = J->qj[t];
+        if (i < 0 || i >= J->n || j < 0 || j >= J->n) { J->bad = 1; return NULL; }
+        if (i > j) { int64_t x = i; i = j; j = x; }
+        int64_t bi = i >> AB_SHIFT, bj = j >> AB_SHIFT, best = i;
+        if (bi == bj) {
+            for (int64_t x = i + 1; x <= j; x++) if (v[x] < v[best]) best = x;
+        } else {
+            int64_t end = (bi + 1) << AB_SHIFT;
+            for (int64_t x = i + 1; x < end; x++) if (v[x] < v[best]) best = x;
+            if (bi + 1 <= bj - 1) {
+                int64_t l = bi + 1, r = bj - 1, len = r - l + 1, k = 63 - __builtin_clzll((uint64_t)len);
+                int64_t m = ab_pick(v, J->tab[k * J->nb + l], J->tab[k * J->nb + r - ((int64_t)1 << k) + 1]);
+                if (v[m] < v[best]) best = m;
+            }
+            for (int64_t x = bj << AB_SHIFT; x <= j; x++) if (v[x] < v[best]) best = x;
+        }
+        J->out[t] = best;
+    }
+    return NULL;
+}
+
+EXPORT int oracle_argmin_sparse_blocked(const int64_t *v, int64_t n, const int64_t *qi, const int64_t *qj,
+                                        int64_t q, int64_t *out, int threads) {
+    if (n <= 0) return q ? -1 : 0;
+    int64_t nb = ((n - 1) >> AB_SHIFT) + 1, levels = 1;
+    while (((int64_t)1 << levels) <= nb) levels++;
+    int64_t *tab = xcalloc((size_t)(nb * levels), sizeof(int64_t));
+    for (int64_t b = 0; b < nb; b++) {
+        int64_t best = b << AB_SHIFT;
+        for (int64_t x = best + 1; x < n && x < ((b + 1) << AB_SHIFT); x++) if (v[x] < v[best]) best = x;
+        tab[b] = best;
+    }
+    for (int64_t k = 1; k < levels; k++)
+        for (int64_t b = 0; b + ((int64_t)1 << k) <= nb; b++)
+            tab[k * nb + b] = ab_pick(v, tab[(k - 1) * nb + b], tab[(k - 1) * nb + b + ((int64_t)1 << (k - 1))]);
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t th[256];
+    ArgminJob jobs[256];
+    for (int w = 0; w < threads; w++) {
+        jobs[w] = (ArgminJob){v, qi, qj, NULL, tab, n, nb, q * w / threads, q * (w + 1) / threads, out, 0};
+        pthread_create(&th[w], NULL, argmin_worker, &jobs[w]);
+    }
+    int bad = 0;
+    for (int w = 0; w < threads; w++) {
+        pthread_join(th[w], NULL);
+        bad |= jobs[w].bad;
+    }
+    free(tab);
+    return bad ? -1 : 0;
+}
+
 /* ------------------------------------------------------------------ */
 /* Longest overlap via the generalized suffix array (overlap.py:72-152) */
 /* ------------------------------------------------------------------ */

@@ -353,15 +353,15 @@ int bucket_sort(Src src, i64 n, u64 span, u64 *keys, u32 *vals, u32 *scratch, bo
         uint4 *s1 = ar->alloc<uint4>(pp.stage1_items()), *s2 = ar->alloc<uint4>(pp.stage2_items());
         SAIX_ARENA_OK(*ar);
         SAIX_CUDA(cudaMemsetAsync(pp.a.cursor, 0, (size_t)pp.cursor_words() * 4, st));
-        static bool attr = false;
-        if (!attr) {
+        static DeviceFlags attr;
+        if (attr.need()) {
             SAIX_CUDA(cudaFuncSetAttribute(k_bs_scatter_emit<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            256 * BSE_ITEMS * 16 + 8 * PS_MAX_BUCKETS));
             SAIX_CUDA(cudaFuncSetAttribute(k_ps_refine<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(PS_REFINE_TILE * 16 + 8 * 256)));
             SAIX_CUDA(cudaFuncSetAttribute(k_bs_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)PS_WINDOW_BYTES));
-            attr = true;
+            attr.set();
         }
         size_t smem = (size_t)256 * BSE_ITEMS * 16 + 8 * (size_t)pp.a.buckets;
         k_bs_scatter_emit<Src><<<(unsigned)ceil_div(n, 256 * BSE_ITEMS), 256, smem, st>>>(src, n, g.shift, cursor, pp,
@@ -378,10 +378,10 @@ int bucket_sort(Src src, i64 n, u64 span, u64 *keys, u32 *vals, u32 *scratch, bo
     k_bs_tiny<<<grid_for(ceil_div(nb, 32) * 32, 256, kNumSMs * 16), 256, 0, st>>>(start, cnt, nb, keys, vals);
     SAIX_LAUNCHED();
     if (h[0]) {
-        static bool attr = false;
-        if (!attr) {
+        static DeviceFlags attr;
+        if (attr.need()) {
             SAIX_CUDA(cudaFuncSetAttribute(k_bs_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BS_SMALL_SMEM));
-            attr = true;
+            attr.set();
         }
         u32 blocks = (h[0] + BS_WARPS - 1) / BS_WARPS;
         k_bs_small<<<blocks < 2 * kNumSMs ? blocks : 2 * kNumSMs, 32 * BS_WARPS, BS_SMALL_SMEM, st>>>(start, cnt, mid,
@@ -389,11 +389,11 @@ int bucket_sort(Src src, i64 n, u64 span, u64 *keys, u32 *vals, u32 *scratch, bo
         SAIX_LAUNCHED();
     }
     if (h[1]) {
-        static bool attr = false;
+        static DeviceFlags attr;
         size_t smem = (size_t)BS_LARGE * 12;
-        if (!attr) {
+        if (attr.need()) {
             SAIX_CUDA(cudaFuncSetAttribute(k_bs_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
+            attr.set();
         }
         k_bs_large<<<h[1] < 4 * kNumSMs ? h[1] : 4 * kNumSMs, 256, smem, st>>>(start, cnt, big, scal + 1, keys, vals);
         SAIX_LAUNCHED();

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
 #include <string>
 
@@ -57,6 +58,21 @@ void set_error(const char *fmt, ...);
         int rc_ = (expr);                                                      \
         if (rc_ != SAIX_OK) return rc_;                                        \
     } while (0)
+
+// Per-device "done" bits for one-time kernel attributes
+// (cudaFuncSetAttribute applies per device context): need() is true until
+// set() ran on the current device.  Two host threads may both run the
+// (idempotent) attribute call; the bits themselves are atomic.
+struct DeviceFlags {
+    std::atomic<unsigned long long> bits{0};
+    static unsigned long long bit() {
+        int d = 0;
+        if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+        return 1ull << (d & 63);
+    }
+    bool need() const { return (bits.load(std::memory_order_acquire) & bit()) == 0; }
+    void set() { bits.fetch_or(bit(), std::memory_order_release); }
+};
 
 // ------------------------------------------------------------- profiling
 

@@ -1175,11 +1175,11 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
 template <int MODE>
 static int merge_rec_launch(RecMergeView v, i64 na, i64 nb, const u32 *split, u32 *sa, const PsPlan &plan,
                             uint2 *stage, cudaStream_t st, u32 *isa_direct = nullptr) {
-    static bool attr = false;
+    static DeviceFlags attr;
     size_t smem = (size_t)RM_TILE * 24 + 8 * (size_t)PS_MAX_BUCKETS;
-    if (!attr) {
+    if (attr.need()) {
         SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_rec<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        attr.set();
     }
     size_t use = (size_t)RM_TILE * 24 + 8 * (size_t)(MODE == EMIT_NONE ? 1 : plan.a.buckets);
     k_merge_tile_rec<MODE><<<(unsigned)ceil_div(na + nb, RM_TILE), RM_THREADS, use, st>>>(v, na, nb, split, sa, plan,
@@ -1628,14 +1628,14 @@ static int dc3_wide_finish(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sig
     SAIX_LAUNCHED();
     {
         Prof prof_("dc3.merge_tile", 16.0 * na + 20.0 * k + (SA ? 4.0 * total : 0) + (ISA ? 8.0 * total : 0), st);
-        static bool attr = false;
+        static DeviceFlags attr;
         size_t smax = (size_t)WT_TILE * 28 + 8 * (size_t)PS_MAX_BUCKETS;
-        if (!attr) {
+        if (attr.need()) {
             SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_w<EMIT_ISA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smax));
             SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_w<EMIT_NONE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smax));
-            attr = true;
+            attr.set();
         }
         size_t smem = (size_t)WT_TILE * 28 + 8 * (size_t)(ISA ? pm.a.buckets : 1);
         if (ISA)
@@ -1824,11 +1824,11 @@ static int tie_rounds(Dc3Ctx &c, i64 m, i64 ties, u32 *S, u64 *kk, u32 *ISAc, u3
         SAIX_CUDA(cudaMemcpyAsync(hl, scal, 8, cudaMemcpyDeviceToHost, st));
         SAIX_CUDA(cudaStreamSynchronize(st));
         if (hl[0]) {
-            static bool attr = false;
-            if (!attr) {
+            static DeviceFlags attr;
+            if (attr.need()) {
                 SAIX_CUDA(cudaFuncSetAttribute(k_bs_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)BS_SMALL_SMEM));
-                attr = true;
+                attr.set();
             }
             u32 blocks = (hl[0] + BS_WARPS - 1) / BS_WARPS;
             k_bs_small<<<blocks < 2 * kNumSMs ? blocks : 2 * kNumSMs, 32 * BS_WARPS, BS_SMALL_SMEM, st>>>(
@@ -1836,11 +1836,11 @@ static int tie_rounds(Dc3Ctx &c, i64 m, i64 ties, u32 *S, u64 *kk, u32 *ISAc, u3
             SAIX_LAUNCHED();
         }
         if (hl[1]) {
-            static bool attr = false;
+            static DeviceFlags attr;
             size_t smem = (size_t)BS_LARGE * 12;
-            if (!attr) {
+            if (attr.need()) {
                 SAIX_CUDA(cudaFuncSetAttribute(k_bs_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                attr = true;
+                attr.set();
             }
             k_bs_large<<<hl[1] < 4 * kNumSMs ? hl[1] : 4 * kNumSMs, 256, smem, st>>>(rs, rl, big, scal + 1, kk, S);
             SAIX_LAUNCHED();
@@ -2094,11 +2094,11 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
             SAIX_CUDA(cudaMemsetAsync(pu.a.cursor, 0, (size_t)pu.cursor_words() * 4, st));
             {
                 Prof prof_("dc3.unique_ranks", (SAc ? 16.0 : 12.0) * m, st);
-                static bool attr = false;
-                if (!attr) {
+                static DeviceFlags attr;
+                if (attr.need()) {
                     SAIX_CUDA(cudaFuncSetAttribute(k_unique_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    256 * UE_ITEMS * 8 + 8 * PS_MAX_BUCKETS));
-                    attr = true;
+                    attr.set();
                 }
                 size_t smem = (size_t)256 * UE_ITEMS * 8 + 8 * (size_t)pu.a.buckets;
                 k_unique_emit<<<(unsigned)ceil_div(m, 256 * UE_ITEMS), 256, smem, st>>>(sorted_vals, m, SAc, pu, s1);
@@ -2491,11 +2491,11 @@ static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const Sample
             SAIX_CUDA(cudaMemsetAsync(pu.a.cursor, 0, (size_t)pu.cursor_words() * 4, st));
             {
                 Prof prof_("dc3.unique_ranks", (SAc ? 16.0 : 12.0) * m, st);
-                static bool attr = false;
-                if (!attr) {
+                static DeviceFlags attr;
+                if (attr.need()) {
                     SAIX_CUDA(cudaFuncSetAttribute(k_unique_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    256 * UE_ITEMS * 8 + 8 * PS_MAX_BUCKETS));
-                    attr = true;
+                    attr.set();
                 }
                 size_t smem = (size_t)256 * UE_ITEMS * 8 + 8 * (size_t)pu.a.buckets;
                 k_unique_emit<<<(unsigned)ceil_div(m, 256 * UE_ITEMS), 256, smem, st>>>(v0, m, SAc, pu, s1);
@@ -2587,11 +2587,11 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     {
         Prof prof_("dc3.srec_emit", (double)N + 12.0 * m + 16.0 * m, st);
         size_t smem = (size_t)2 * SR_TILE * 16 + 8 * (size_t)pr.a.buckets;
-        static bool attr = false;
-        if (!attr) {
+        static DeviceFlags attr;
+        if (attr.need()) {
             SAIX_CUDA(cudaFuncSetAttribute(k_srec_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            2 * SR_TILE * 16 + 8 * PS_MAX_BUCKETS));
-            attr = true;
+            attr.set();
         }
         k_srec_emit<<<(unsigned)ceil_div(k, SR_TILE), SR_THREADS, smem, st>>>(T, L, ISAc, pr, stage1);
     }
@@ -2602,12 +2602,12 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     SAIX_ARENA_OK(ar);
     {
         Prof prof_("dc3.srec_apply", 48.0 * m, st);
-        static bool attr = false;
-        if (!attr) {
+        static DeviceFlags attr;
+        if (attr.need()) {
             SAIX_CUDA(cudaFuncSetAttribute(k_ps_refine<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(PS_REFINE_TILE * 16 + 8 * 256)));
             SAIX_CUDA(cudaFuncSetAttribute(k_rs_window, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 << RW_SHIFT));
-            attr = true;
+            attr.set();
         }
         SAIX_TRY(ps_refine_launch(stage1, pr, stage2, st));
         k_rs_window<<<(unsigned)pr.windows, PS_THREADS, 16 << RW_SHIFT, st>>>(stage2, pr, RS, hist, D1);
@@ -2621,10 +2621,10 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
                             "dc3.mod0_scan", 8.0 * D1 * pr.windows));
     {
         Prof prof_("dc3.mod0_split", 16.0 * m + 16.0 * k, st);
-        static bool attr = false;
-        if (!attr) {
+        static DeviceFlags attr;
+        if (attr.need()) {
             SAIX_CUDA(cudaFuncSetAttribute(k_mod0_window, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M0_SMEM));
-            attr = true;
+            attr.set();
         }
         u32 dmask = 1;
         while (dmask < (u32)D1 - 1) dmask = dmask * 2 + 1;

@@ -254,12 +254,12 @@ inline int os_items_choice() {
 template <typename K, class Src, int ITEMS, typename V = u32>
 static int os_launch_pass(Src src, i64 np, int shift, const u32 *offs, u32 *status, u32 *ticket, K *dk, V *dv,
                           cudaStream_t st) {
-    static bool attr = false;
+    static DeviceFlags attr;
     constexpr size_t smem = os_pass_smem<K, ITEMS, V>();
-    if (!attr) {
+    if (attr.need()) {
         SAIX_CUDA(cudaFuncSetAttribute(k_os_pass<K, Src, ITEMS, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-        attr = true;
+        attr.set();
     }
     i64 ntiles = os_tiles(np, ITEMS);
     SAIX_CUDA(cudaMemsetAsync(status, 0, (size_t)ntiles * OS_RADIX * 4, st));

@@ -182,11 +182,11 @@ k_ps_refine(const P *__restrict__ stage1, PsPlan plan, P *__restrict__ stage2) {
 
 template <class P>
 int ps_refine_launch(const P *stage1, const PsPlan &plan, P *stage2, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static DeviceFlags attr;
+    if (attr.need()) {
         SAIX_CUDA(cudaFuncSetAttribute(k_ps_refine<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(PS_REFINE_TILE * sizeof(P) + 8 * 256)));
-        attr = true;
+        attr.set();
     }
     size_t smem = (size_t)PS_REFINE_TILE * sizeof(P) + 8 * ((size_t)1 << (plan.a.shift - plan.s2));
     i64 tiles = ceil_div(plan.stage1_items(), PS_REFINE_TILE);
@@ -232,11 +232,11 @@ int ps_finish(const P *stage1, P *stage2, const PsPlan &plan, Apply ap, cudaStre
     Prof prof_(prof, bytes, st);
     SAIX_TRY(ps_refine_launch(stage1, plan, stage2, st));
     {
-        static bool attr = false;
-        if (!attr) {
+        static DeviceFlags attr;
+        if (attr.need()) {
             SAIX_CUDA(cudaFuncSetAttribute(k_ps_window<P, Apply>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)PS_WINDOW_BYTES));
-            attr = true;
+            attr.set();
         }
         size_t smem = (size_t)sizeof(Out) << plan.s2;
         k_ps_window<P, Apply><<<(unsigned)plan.windows, PS_THREADS, smem, st>>>(stage2, plan, ap);
@@ -298,11 +298,11 @@ static inline int scatter_u32(Arena &ar, const u32 *idx, const u32 *val, i64 n, 
     SAIX_CUDA(cudaMemsetAsync(pp.a.cursor, 0, (size_t)pp.cursor_words() * 4, st));
     {
         Prof prof_(prof, 16.0 * n, st);
-        static bool attr = false;
-        if (!attr) {
+        static DeviceFlags attr;
+        if (attr.need()) {
             SAIX_CUDA(cudaFuncSetAttribute(k_pairs_emit<>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            256 * PE_ITEMS * 8 + 8 * PS_MAX_BUCKETS));
-            attr = true;
+            attr.set();
         }
         size_t smem = (size_t)256 * PE_ITEMS * 8 + 8 * (size_t)pp.a.buckets;
         k_pairs_emit<><<<(unsigned)ceil_div(n, 256 * PE_ITEMS), 256, smem, st>>>(idx, val, n, pp, s1);

@@ -284,12 +284,16 @@ template <class Src>
 static int crc_stream(const Src &src, i64 L, u32 *crc, cudaStream_t st, const char *prof, double bytes) {
     SAIX_CUDA(cudaMemsetAsync(crc, 0, 4, st));
     if (L <= 0) return SAIX_OK;  // zlib.crc32(b"") == 0
-    static int per_sm = 0;
-    if (!per_sm) {
+    static DeviceFlags attr;
+    static std::atomic<int> per_sm_cached{1};
+    if (attr.need()) {
+        int per_sm = 0;
         SAIX_CUDA(cudaFuncSetAttribute(k_crc_stream<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SC_SMEM));
         SAIX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_crc_stream<Src>, SC_THREADS, SC_SMEM));
-        if (per_sm < 1) per_sm = 1;
+        per_sm_cached.store(per_sm < 1 ? 1 : per_sm);  // same on every B200
+        attr.set();
     }
+    const int per_sm = per_sm_cached.load();
     const i64 J = ceil_div(L, SC_BLOCK);
     i64 grid = (i64)kNumSMs * per_sm;
     if (grid > J) grid = J;
@@ -323,11 +327,15 @@ __global__ void k_unpack_index(const u8 *__restrict__ blob, i64 n, u8 *__restric
         u64 a = load_entry(blob, ss, i), b = load_entry(blob, ls, i);
         text[i] = blob[kHeader + i];
         const bool oob = a >= (u64)n;  // never scatter out of range (a crafted file)
-        nbad |= oob | (b > (u64)n);
+        // sa >= n: the reference's rank[sa] = arange(n) raises IndexError.  Any
+        // lcp value loads there; the device keeps u32 LCPs, so only values
+        // >= 2^32 (impossible for n < 2^32, i.e. a crafted file) are refused.
+        nbad |= (oob ? 1u : 0u) | ((b >> 32) ? 2u : 0u);
         sa[i] = oob ? 0u : (u32)a;
         lcp[i] = (u32)b;
     }
-    if (__any_sync(0xffffffffu, nbad) && lane_id() == 0) atomicOr(bad, 1u);
+    nbad = __reduce_or_sync(0xffffffffu, nbad);
+    if (nbad && lane_id() == 0) atomicOr(bad, nbad);
 }
 
 }  // namespace saix
@@ -432,8 +440,12 @@ extern "C" int saix_index_unpack(const uint8_t *blob, int64_t n, uint8_t *text, 
         set_error("checksum mismatch; file is corrupt");
         return SAIX_EINVAL;
     }
-    if (host[1]) {
+    if (host[1] & 1u) {
         set_error("index entries out of range");
+        return SAIX_EINVAL;
+    }
+    if (host[1] & 2u) {
+        set_error("lcp entries beyond 2^32-1 do not fit the device's u32 LCP layout");
         return SAIX_EINVAL;
     }
     return SAIX_OK;

@@ -197,7 +197,10 @@ def unpack_index(blob, rmq_kind: RmqKind = "sparse") -> LcpQueryEngine:
         if lo < 1 or hi > sigma:
             raise ValueError("ranks must lie in 1..sigma")
     text = RankedText._checked(_lib.widen_i64_host(text_d, n), int(sigma))
-    dt = DeviceText.resident(text, text_d)
+    # the file stores one byte per rank whatever the header's sigma (the
+    # reference loads sigma > 255 files too); device texts with sigma > 255
+    # are u32, so widen on the device
+    dt = DeviceText.resident(text, text_d if int(sigma) <= 255 else text_d.to(t.int32))
     object.__setattr__(text, "_dev", dt)
     ix = DeviceIndex(dt, sa_d, isa_d)
     sa = _lib.widen_i64_host(sa_d, n)

@@ -39,4 +39,28 @@ def c4_pairs(p0: int, p1: int, length: int = C4_LEN) -> tuple[np.ndarray, np.nda
     offs = np.arange(2 * n + 1, dtype=np.int64) * length
     return seqs, offs
 
+def _chunk(args):
+    return c4_pairs(*args)
+
+
+def c4_generate(lo: int, hi: int, length: int = C4_LEN, workers: int | None = None):
+    """Pairs [lo, hi) packed like c4_pairs, generated in 1000-pair chunks on
+    the host's cores (process pool)."""
+    import concurrent.futures as cf
+    import os
+    chunks = [(a, min(a + 1000, hi), length) for a in range(lo, hi, 1000)]
+    if not chunks:
+        return np.zeros(0, np.uint8), np.zeros(1, np.int64)
+    if len(chunks) == 1:
+        return c4_pairs(*chunks[0])
+    with cf.ProcessPoolExecutor(max_workers=workers or min(32, os.cpu_count() or 4)) as ex:
+        parts = list(ex.map(_chunk, chunks))
+    seqs = np.concatenate([p[0] for p in parts])
+    offs, base = [np.zeros(1, np.int64)], 0
+    for _s, o in parts:
+        offs.append(o[1:] + base)
+        base += int(o[-1])
+    return seqs, np.concatenate(offs)
+
+
 from .distributed import shard  # noqa: E402,F401  (re-exported for bench.py)

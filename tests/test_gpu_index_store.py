@@ -230,6 +230,27 @@ def test_crafted_sa_out_of_range_rejected():
         index_store.load_index(io.BytesIO(_recrc(blob)))
 
 
+def test_crafted_large_lcp_loads_like_reference():
+    # the reference loads any lcp value (index_store.py:128-131); so do we
+    blob = bytearray(saved_bytes(engine_for("ACGTACGT")))
+    n = 8
+    blob[40 + 9 * n + 8: 40 + 9 * n + 16] = (1000).to_bytes(8, "little")  # lcp[1] = 1000 > n
+    loaded = index_store.load_index(io.BytesIO(_recrc(blob)))
+    assert int(loaded.lcp.lcp[1]) == 1000
+
+
+def test_sigma_above_255_header_loads_like_reference():
+    # one byte per rank in the file whatever sigma says; the reference keeps
+    # the header's sigma (index_store.py:126) and so does the device text
+    blob = bytearray(saved_bytes(engine_for("ACGTACGT")))
+    blob[32:40] = (300).to_bytes(8, "little")
+    loaded = index_store.load_index(io.BytesIO(_recrc(blob)))
+    assert loaded.text.sigma == 300
+    ref = engine_for("ACGTACGT")
+    assert loaded.sa.sa.tolist() == ref.sa.sa.tolist()
+    assert lcp_query(loaded, 3, 3) == 5 and lcp_query(loaded, 6, 0) == 1
+
+
 def test_widen_matches_host():
     t = _lib.torch()
     rng = np.random.default_rng(5)

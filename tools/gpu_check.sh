@@ -73,14 +73,3 @@ for what in "$@"; do
     traces) for w in c2 c3; do SAIX_TRACE=1 timeout 600 python tools/profile_once.py $( [ $w = c3 ] && echo 268435456 || echo c2 ) 2>&1 | grep "saix dc3" | sort | uniq -c > $O/trace_$w.txt; cat $O/trace_$w.txt; done ;;
   esac
 done
-for what in "$@"; do
-  case $what in
-    c3direct) SAIX_WN_DIRECT=1 timeout 900 python bench.py --workload c3 --no-cpu-baseline > $O/bench_c3direct.json 2> $O/bench_c3direct.err; tail -c 200 $O/bench_c3direct.json ;;
-    c2direct) SAIX_WN_DIRECT=1 timeout 900 python bench.py --workload c2 --no-cpu-baseline > $O/bench_c2direct.json 2> $O/bench_c2direct.err; tail -c 200 $O/bench_c2direct.json ;;
-  esac
-done
-for what in "$@"; do
-  case $what in
-    c2dm) SAIX_WN_DIRECT_MAX=20000000 timeout 900 python bench.py --workload c2 --no-cpu-baseline > $O/bench_c2dm.json 2> $O/bench_c2dm.err; tail -c 200 $O/bench_c2dm.json ;;
-  esac
-done
