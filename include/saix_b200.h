@@ -240,18 +240,28 @@ SAIX_API int saix_longest_overlap(const uint8_t *a_ascii, int64_t na,
 /* ------------------------------------------------------- batched pairs */
 
 /* Batched longest_overlap over P independent pairs (BASELINE config C4):
- * equals [longest_overlap(A_p, B_p) for p] (overlap.py:110-152).
+ * equals [longest_overlap(A_p, B_p) for p] (overlap.py:110-152, the
+ * reference's per-pair entry point mapped over the batch).
  * seqs: device ASCII of all pairs; offs_host: HOST int64[2P+1], pair p is
  * A = seqs[offs[2p], offs[2p+1]), B = seqs[offs[2p+1], offs[2p+2]).
  * out: device int64[3P] (length, pos_a, pos_b per pair); *bad (device int64)
  * receives the smallest seqs offset of an illegal residue (INT64_MAX if
  * none; pairs with an empty side are not validated, like the reference).
- * All pairs of one call share one generalized text, so callers bound a call
- * to ~2^27 total residues and loop over waves. */
+ * Every pair with |A|+|B|+1 <= 20480 runs its whole DC3 + LCP + overlap scan
+ * in one CTA's shared memory (csrc/pairdc3.cu); longer pairs and pairs over
+ * the on-chip work bounds go through the wave-global DC3 (one generalized
+ * text per wave of <= 2^24 residues).  No limit on the call's total size.
+ * The call synchronizes the stream once (the fallback count). */
 SAIX_API size_t saix_overlap_batch_workspace_bytes(const int64_t *offs_host, int64_t npairs);
 SAIX_API int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, int64_t npairs,
                                 int keep_n, int64_t *out, int64_t *bad, void *ws,
                                 size_t ws_bytes, void *stream);
+/* 0: route every pair through the wave-global path (A/B and tests); returns
+ * the previous setting. */
+SAIX_API int saix_overlap_batch_set_onchip(int on);
+/* Pairs of this thread's last saix_overlap_batch call that took the
+ * wave-global path. */
+SAIX_API int64_t saix_overlap_batch_last_fallbacks(void);
 
 /* ------------------------------------------------ Cartesian tree / ±1 RMQ */
 /* build_cartesian + euler_tour (rmq.py:91-152) on the device: parent, left,

@@ -898,20 +898,24 @@ static size_t batch_ws(Arena &ar, i64 P, i64 nx, BatchWs *w) {
 
 }  // namespace saix
 
-extern "C" size_t saix_overlap_batch_workspace_bytes(const int64_t *offs_host, int64_t npairs) {
+namespace saix {
+
+// The wave-global batched path: all pairs of a call share one generalized
+// text (< 2^30 residues).  saix_overlap_batch (pairdc3.cu) runs every pair
+// that fits on chip in its own CTA and sends the rest here.
+size_t overlap_batch_global_ws(const i64 *offs_host, i64 npairs) {
     BatchLayout b;
     if (npairs < 0 || (npairs > 0 && !offs_host) || batch_layout(offs_host, npairs, b)) return 0;
     Arena ar;
     return batch_ws(ar, npairs, b.nx, nullptr) + Arena::kAlign;
 }
 
-extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, int64_t npairs, int keep_n,
-                                  int64_t *out, int64_t *bad, void *ws, size_t ws_bytes, void *stream) {
+int overlap_batch_global(const u8 *seqs, const i64 *offs_host, i64 npairs, int keep_n, i64 *out, i64 *bad,
+                         void *ws, size_t ws_bytes, cudaStream_t st) {
     if (npairs < 0 || (npairs > 0 && (!offs_host || !out)) || !bad) {
         set_error("saix_overlap_batch: invalid arguments");
         return SAIX_EINVAL;
     }
-    cudaStream_t st = (cudaStream_t)stream;
     k_pipeline_init<<<1, 1, 0, st>>>(out, bad);  // out[0..2] zero, bad = INT64_MAX
     SAIX_LAUNCHED();
     if (npairs == 0) return SAIX_OK;
@@ -1003,3 +1007,5 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
+
+}  // namespace saix

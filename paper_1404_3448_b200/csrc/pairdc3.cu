@@ -1,0 +1,800 @@
+// pairdc3.cu -- batched longest_overlap (overlap.py:110-152 mapped over
+// independent pairs, BASELINE config C4) with every pair's whole pipeline on
+// chip: one CTA per pair, the pair's generalized text, suffix array and DC3
+// rank table live in shared memory from the first residue load to the
+// three-int64 answer.  Nothing but the pair's ASCII (in) and its answer (out)
+// touches HBM.
+//
+// Per pair (n = |A| + |B| + 1 <= PD_NMAX, GSA codes: pad 0, separator 1,
+// A..T 2..5, N 6 under NPolicy.KEEP -- GeneralizedText.build, overlap.py:83-95
+// with encode's ranks shifted by one):
+//
+//  1. load + encode A, sep, B into T (u8) and validate every residue
+//     (sequence.py:144-157; REJECT: the smallest bad offset is reported);
+//  2. DC3 sample sort (suffix_index.py:221-271).  The samples -- positions
+//     p % 3 != 0 below limit = n+1 if n%3==1 else n (suffix_index.py:
+//     143-153), the all-padding sample n included -- are counting-sorted by
+//     their first 7 characters (14-bit bucket, a monotone 2-bit map), then
+//     each bucket is sorted by exact suffix comparison on T (8 characters per
+//     64-bit word).  This replaces the triple naming + recursion: with the
+//     whole text on chip, comparing the (rare) samples that share 7
+//     characters directly costs less than renaming and recursing, and the
+//     order is the same one the recursion returns (sample suffixes are
+//     distinct, so their order is unique);
+//  3. rank_of[sample] = 1-based rank (suffix_index.py:256-271; rank 0 for
+//     positions >= limit);
+//  4. non-samples i % 3 == 0 ordered by (T[i], rank_of[i+1]) -- the
+//     reference's _sort_nonsamples (suffix_index.py:274-290): the class-1
+//     samples in rank order give the successor order, one stable counting
+//     pass by T[i] (block scan of per-character counts);
+//  5. merge (suffix_index.py:173-218): merge path over the sample run
+//     (pad sample dropped) and the non-sample run with the DC3 comparator
+//     (char, then rank_of[+1] for mod-1, or char, char, rank_of[+2] for
+//     mod-2); outputs are held in registers and written back over the two
+//     runs, giving SA in shared memory;
+//  6. longest_overlap's two passes (overlap.py:129-152): pass 1 = max LCP
+//     over adjacent cross-sequence pairs (word compares on T), pass 2 = runs
+//     of lcp >= best as a segmented (head flag, min A, min B) block scan, the
+//     answer being the lexicographically smallest (min A, min B) of a run
+//     holding both sequences.
+//
+// Pairs longer than PD_NMAX, and pairs whose sample buckets or comparisons
+// exceed the on-chip work bounds (long exact repeats, e.g. poly-A runs), are
+// appended to a fallback list; saix_overlap_batch runs those through the
+// wave-global DC3 path of overlap.cu.  Both paths are exact, so the split
+// only moves time.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace saix {
+
+int overlap_batch_global(const u8 *seqs, const i64 *offs_host, i64 P, int keep_n, i64 *out, i64 *bad, void *ws,
+                         size_t ws_bytes, cudaStream_t st);
+size_t overlap_batch_global_ws(const i64 *offs_host, i64 P);
+
+namespace pd {
+
+constexpr int THREADS = 512;
+constexpr int WARPS = THREADS / 32;
+constexpr int NMAX = 20480;            // GSA residues per pair on chip
+constexpr int ITEMS = NMAX / THREADS;  // merge outputs / scan items per thread (40)
+constexpr int NB = 1 << 14;            // sample buckets: 7 characters x 2 bits
+constexpr int TPAD = 64;               // zero bytes after T (word loads past n)
+constexpr int MMAX = 2 * ((NMAX + 2) / 3) + 2;
+constexpr int KMAX = (NMAX + 2) / 3 + 1;
+constexpr int RKMAX = 2 * ((NMAX + 2) / 3 + 1) + 2;  // rank slots of positions 0..n+2
+constexpr int SMALL = 32;      // buckets up to this size: one thread, insertion sort
+constexpr int MAXBIG = 16;     // larger buckets per pair: whole CTA, rank counting
+constexpr u32 WORK_MAX = 1u << 16;  // per-thread word compares in the sample sort
+
+__host__ __device__ constexpr int al16(int x) { return (x + 15) & ~15; }
+constexpr int OFF_T = 0;
+constexpr int OFF_SS = al16(NMAX + TPAD);
+constexpr int OFF_S0 = OFF_SS + al16(2 * MMAX);
+constexpr int OFF_RK = OFF_S0 + al16(2 * KMAX);
+constexpr int OFF_MISC = OFF_RK + al16(2 * RKMAX);
+constexpr int BIG_CAP = (OFF_MISC - OFF_S0 - 2 * NB) / 2;  // u16 scratch after the counters
+constexpr int SMEM = OFF_MISC + 1024;
+static_assert(2 * NB <= OFF_MISC - OFF_S0, "bucket counters must fit the S0 + RK region");
+static_assert(BIG_CAP >= 1024, "big-bucket scratch");
+static_assert(MMAX + KMAX >= NMAX + 1, "SA is written over the sample + non-sample runs");
+static_assert(SMEM <= 113 * 1024, "two CTAs per SM");
+
+struct Misc {
+    unsigned long long scan64[2][WARPS + 1];
+    u32 scan32[WARPS + 1];
+    u32 pair;
+    u32 fail;
+    u32 nbig;
+    u32 big[MAXBIG][2];
+    u32 red32[WARPS];
+    unsigned long long red64[WARPS];
+    u32 seg[WARPS + 1][3];
+};
+static_assert(sizeof(Misc) <= 1024, "misc");
+
+// 8 characters at T[off..off+8) (little endian: byte k = T[off + k])
+__device__ __forceinline__ u64 ld8(const u8 *T, u32 off) {
+    const u64 *w = reinterpret_cast<const u64 *>(T + (off & ~7u));
+    const u64 lo = w[0], hi = w[1];
+    const u32 sh = (off & 7u) * 8u;
+    return (lo >> sh) | ((hi << 1) << (63u - sh));
+}
+
+// suffix i < suffix j (i != j); `work` counts 8-character steps.  Distinct
+// suffixes differ before the shorter reaches the zero padding.
+__device__ __forceinline__ bool suf_less(const u8 *T, u32 i, u32 j, u32 &work) {
+    for (u32 h = 0;; h += 8) {
+        const u64 a = ld8(T, i + h), b = ld8(T, j + h);
+        if (a != b) {
+            const int s = (__ffsll((long long)(a ^ b)) - 1) & ~7;
+            return ((a >> s) & 0xFFu) < ((b >> s) & 0xFFu);
+        }
+        work++;
+    }
+}
+
+// exact LCP of suffixes i != j (bounded by the separator / end: both unique)
+__device__ __forceinline__ u32 suf_lcp(const u8 *T, u32 i, u32 j) {
+    for (u32 h = 0;; h += 8) {
+        const u64 x = ld8(T, i + h) ^ ld8(T, j + h);
+        if (x) return h + ((u32)(__ffsll((long long)x) - 1) >> 3);
+    }
+}
+
+// lcp(i, j) >= need ?
+__device__ __forceinline__ bool lcp_at_least(const u8 *T, u32 i, u32 j, u32 need) {
+    for (u32 h = 0; h < need; h += 8) {
+        const u64 x = ld8(T, i + h) ^ ld8(T, j + h);
+        if (x) return h + ((u32)(__ffsll((long long)x) - 1) >> 3) >= need;
+    }
+    return true;
+}
+
+// Bucket of the suffix at s from its first 7 codes, monotone in suffix order:
+// A..T -> 0..3; pad / separator -> 0 and every later digit 0; N -> 3 and
+// every later digit 3.  (Equal digits with different codes: the smaller code
+// is pad/sep, whose zero fill keeps it <=, or the larger is N, whose 3-fill
+// keeps it >=.)
+__device__ __forceinline__ u32 bucket_of(const u8 *T, u32 s) {
+    const u64 w = ld8(T, s);
+    u32 b = 0, mode = 0;  // 0 normal, 1 zero fill, 2 three fill
+#pragma unroll
+    for (int k = 0; k < 7; k++) {
+        const u32 c = (u32)(w >> (8 * k)) & 0xFFu;
+        u32 d;
+        if (mode == 1) d = 0;
+        else if (mode == 2) d = 3;
+        else if (c <= 1) {
+            d = 0;
+            mode = 1;
+        } else if (c >= 6) {
+            d = 3;
+            mode = 2;
+        } else d = c - 2;
+        b = (b << 2) | d;
+    }
+    return b;
+}
+
+// rank slot of a sample-class position p (p % 3 != 0)
+__device__ __forceinline__ u32 slot(u32 p) { return 2u * (p / 3u) + (p % 3u) - 1u; }
+
+// DC3 merge comparator (suffix_index.py:192-202): sample a < non-sample b ?
+__device__ __forceinline__ bool sample_less(const u8 *T, const u16 *RK, u32 a, u32 b) {
+    const u32 ca = T[a], cb = T[b];
+    if (ca != cb) return ca < cb;
+    if (a % 3u == 1u) return RK[slot(a + 1)] < RK[slot(b + 1)];
+    const u32 ca1 = T[a + 1], cb1 = T[b + 1];
+    if (ca1 != cb1) return ca1 < cb1;
+    return RK[slot(a + 2)] < RK[slot(b + 2)];
+}
+
+// GSA code of one ASCII residue (rank + 1; 0 = illegal)
+__device__ __forceinline__ u32 code_of(u32 c, int keep_n) {
+    switch (c) {
+        case 'A': return 2;
+        case 'C': return 3;
+        case 'G': return 4;
+        case 'T': return 5;
+        case 'N': return keep_n ? 6u : 0u;
+        default: return 0;
+    }
+}
+
+// T[dst + i] = code(src[i]) for i < len; returns the smallest bad i (or len)
+__device__ __forceinline__ i64 load_codes(const u8 *__restrict__ src, i64 len, u8 *T, u32 dst, int keep_n) {
+    i64 bad = len;
+    const uintptr_t a0 = (uintptr_t)src;
+    const i64 head = (i64)((16 - (a0 & 15)) & 15) < len ? (i64)((16 - (a0 & 15)) & 15) : len;
+    for (i64 i = threadIdx.x; i < head; i += THREADS) {
+        u32 c = code_of(src[i], keep_n);
+        if (!c) {
+            bad = i < bad ? i : bad;
+            c = 2;
+        }
+        T[dst + i] = (u8)c;
+    }
+    const uint4 *v = reinterpret_cast<const uint4 *>(src + head);
+    const i64 nv = (len - head) >> 4;
+    for (i64 q = threadIdx.x; q < nv; q += THREADS) {
+        const uint4 x = __ldg(v + q);
+        const u32 w[4] = {x.x, x.y, x.z, x.w};
+        const i64 base = head + 16 * q;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            u32 c = code_of((w[k >> 2] >> (8 * (k & 3))) & 0xFFu, keep_n);
+            if (!c) {
+                bad = base + k < bad ? base + k : bad;
+                c = 2;
+            }
+            T[dst + base + k] = (u8)c;
+        }
+    }
+    for (i64 i = head + 16 * nv + threadIdx.x; i < len; i += THREADS) {
+        u32 c = code_of(src[i], keep_n);
+        if (!c) {
+            bad = i < bad ? i : bad;
+            c = 2;
+        }
+        T[dst + i] = (u8)c;
+    }
+    return bad;
+}
+
+// validation only (pairs that do not fit on chip)
+__device__ __forceinline__ i64 check_codes(const u8 *__restrict__ src, i64 len, int keep_n) {
+    i64 bad = len;
+    for (i64 i = threadIdx.x; i < len; i += THREADS)
+        if (!code_of(src[i], keep_n) && i < bad) bad = i;
+    return bad;
+}
+
+template <class V>
+__device__ __forceinline__ V warp_incl_add(V v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        V y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    return v;
+}
+
+// block exclusive sum (all THREADS threads); sh holds WARPS+1 entries
+template <class V>
+__device__ __forceinline__ V block_exsum(V v, V &total, V *sh) {
+    const int w = threadIdx.x >> 5, lane = lane_id();
+    V inc = warp_incl_add(v);
+    if (lane == 31) sh[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        V x = lane < WARPS ? sh[lane] : V(0);
+        V xi = warp_incl_add(x);
+        if (lane < WARPS) sh[lane] = xi - x;
+        if (lane == WARPS - 1) sh[WARPS] = xi;
+    }
+    __syncthreads();
+    V ex = sh[w] + inc - v;
+    total = sh[WARPS];
+    __syncthreads();
+    return ex;
+}
+
+struct Seg {  // segmented-min state: head flag + min A / min B position
+    u32 f, a, b;
+};
+constexpr u32 kInf = 0xFFFFFFFFu;
+__device__ __forceinline__ Seg seg_combine(Seg l, Seg r) {
+    if (r.f) return r;
+    return Seg{l.f, min(l.a, r.a), min(l.b, r.b)};
+}
+__device__ __forceinline__ Seg seg_shfl_up(Seg s, int o) {
+    return Seg{__shfl_up_sync(0xffffffffu, s.f, o), __shfl_up_sync(0xffffffffu, s.a, o),
+               __shfl_up_sync(0xffffffffu, s.b, o)};
+}
+
+__device__ __forceinline__ Seg block_seg_exclusive(Seg v, Misc &ms) {
+    const int w = threadIdx.x >> 5, lane = lane_id();
+    Seg inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        Seg y = seg_shfl_up(inc, o);
+        if (lane >= o) inc = seg_combine(y, inc);
+    }
+    if (lane == 31) {
+        ms.seg[w][0] = inc.f;
+        ms.seg[w][1] = inc.a;
+        ms.seg[w][2] = inc.b;
+    }
+    __syncthreads();
+    if (w == 0) {
+        Seg x = lane < WARPS ? Seg{ms.seg[lane][0], ms.seg[lane][1], ms.seg[lane][2]} : Seg{0u, kInf, kInf};
+        Seg xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            Seg y = seg_shfl_up(xi, o);
+            if (lane >= o) xi = seg_combine(y, xi);
+        }
+        Seg ex = seg_shfl_up(xi, 1);
+        if (lane == 0) ex = Seg{0u, kInf, kInf};
+        if (lane < WARPS) {
+            ms.seg[lane][0] = ex.f;
+            ms.seg[lane][1] = ex.a;
+            ms.seg[lane][2] = ex.b;
+        }
+    }
+    __syncthreads();
+    Seg prev = seg_shfl_up(inc, 1);
+    Seg carry{ms.seg[w][0], ms.seg[w][1], ms.seg[w][2]};
+    if (lane > 0) carry = seg_combine(carry, prev);
+    __syncthreads();
+    return carry;
+}
+
+__global__ void __launch_bounds__(THREADS, 2)
+k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int keep_n, i64 *__restrict__ out,
+           i64 *__restrict__ bad, u32 *__restrict__ next_pair, u32 *__restrict__ nfb, u32 *__restrict__ fb,
+           int nmax) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    u8 *T = smem + OFF_T;
+    u16 *SS = reinterpret_cast<u16 *>(smem + OFF_SS);
+    u16 *SA = SS;  // written over SS + S0 by the merge
+    u16 *S0 = reinterpret_cast<u16 *>(smem + OFF_S0);
+    u16 *RK = reinterpret_cast<u16 *>(smem + OFF_RK);
+    u32 *CNT = reinterpret_cast<u32 *>(smem + OFF_S0);  // NB u16 counters, two per word
+    u16 *BIGS = reinterpret_cast<u16 *>(smem + OFF_S0 + 2 * NB);
+    Misc &ms = *reinterpret_cast<Misc *>(smem + OFF_MISC);
+    const u32 tid = threadIdx.x;
+
+    for (;;) {
+        __syncthreads();  // every shared read of the previous pair is done
+        if (tid == 0) {
+            ms.pair = atomicAdd(next_pair, 1u);
+            ms.fail = 0;
+            ms.nbig = 0;
+        }
+        __syncthreads();
+        const i64 p = ms.pair;
+        if (p >= P) break;
+        const i64 a0 = offs[2 * p], b0 = offs[2 * p + 1], b1 = offs[2 * p + 2];
+        const i64 la = b0 - a0, lb = b1 - b0;
+        if (la == 0 || lb == 0) {  // overlap.py:120-121: (0, 0, 0) before any validation
+            if (tid == 0) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0;
+            continue;
+        }
+        const i64 nl = la + lb + 1;
+        if (nl > nmax) {  // validate here (bad offsets are relative to this call's seqs), solve elsewhere
+            i64 ba = check_codes(seqs + a0, la, keep_n), bb = check_codes(seqs + b0, lb, keep_n);
+            i64 mine = ba < la ? a0 + ba : (bb < lb ? b0 + bb : INT64_MAX);
+            if (mine != INT64_MAX) atomicMin((unsigned long long *)bad, (unsigned long long)mine);
+            if (tid == 0) fb[atomicAdd(nfb, 1u)] = (u32)p;
+            continue;
+        }
+        const u32 n = (u32)nl, nA = (u32)la;
+
+        // ---- 1. text + zeroed counters
+        {
+            i64 ba = load_codes(seqs + a0, la, T, 0, keep_n);
+            i64 bb = load_codes(seqs + b0, lb, T, nA + 1, keep_n);
+            i64 mine = ba < la ? a0 + ba : (bb < lb ? b0 + bb : INT64_MAX);
+            if (mine != INT64_MAX) atomicMin((unsigned long long *)bad, (unsigned long long)mine);
+            if (tid == 0) T[nA] = 1;  // separator (overlap.py:25)
+            for (u32 i = tid; i < TPAD; i += THREADS) T[n + i] = 0;
+            for (u32 i = tid; i < NB / 2; i += THREADS) CNT[i] = 0;
+        }
+        __syncthreads();
+
+        // ---- 2. sample buckets: sample q <-> position 3(q/2) + 1 + (q&1)
+        const u32 limit = (n % 3u == 1u) ? n + 1 : n;
+        const u32 qmax = 2u * ((limit + 2u) / 3u);
+        for (u32 q = tid; q < qmax; q += THREADS) {
+            const u32 s = 3u * (q >> 1) + 1u + (q & 1u);
+            if (s < limit) {
+                const u32 b = bucket_of(T, s);
+                atomicAdd(&CNT[b >> 1], 1u << (16 * (b & 1)));
+            }
+        }
+        __syncthreads();
+        // exclusive scan of the 2^14 u16 counts (32 per thread)
+        {
+            constexpr int W = NB / 2 / THREADS;  // 16 words per thread
+            u32 loc[W], sum = 0;
+#pragma unroll
+            for (int k = 0; k < W; k++) {
+                loc[k] = CNT[tid * W + k];
+                sum += (loc[k] & 0xFFFFu) + (loc[k] >> 16);
+            }
+            u32 tot;
+            u32 run = block_exsum<u32>(sum, tot, ms.scan32);
+#pragma unroll
+            for (int k = 0; k < W; k++) {
+                const u32 lo = run, hi = run + (loc[k] & 0xFFFFu);
+                run = hi + (loc[k] >> 16);
+                CNT[tid * W + k] = lo | (hi << 16);
+            }
+        }
+        __syncthreads();
+        for (u32 q = tid; q < qmax; q += THREADS) {
+            const u32 s = 3u * (q >> 1) + 1u + (q & 1u);
+            if (s < limit) {
+                const u32 b = bucket_of(T, s), sh = 16 * (b & 1);
+                const u32 at = (atomicAdd(&CNT[b >> 1], 1u << sh) >> sh) & 0xFFFFu;
+                SS[at] = (u16)s;
+            }
+        }
+        __syncthreads();
+        const u32 m = (CNT[NB / 2 - 1] >> 16);  // end of the last bucket = number of samples
+
+        // ---- in-bucket exact sort (counters now hold bucket ends)
+        {
+            u32 work = 0;
+            const u16 *C16 = reinterpret_cast<const u16 *>(CNT);
+            constexpr int BPT = NB / THREADS;  // 32 buckets per thread
+            u32 start = tid ? C16[tid * BPT - 1] : 0u;
+            for (int k = 0; k < BPT; k++) {
+                const u32 end = C16[tid * BPT + k];
+                const u32 sz = end - start;
+                if (sz >= 2) {
+                    if (sz <= SMALL) {
+                        for (u32 i = start + 1; i < end; i++) {
+                            const u32 x = SS[i];
+                            u32 j = i;
+                            while (j > start && suf_less(T, x, SS[j - 1], work)) {
+                                SS[j] = SS[j - 1];
+                                j--;
+                            }
+                            SS[j] = (u16)x;
+                            if (work > WORK_MAX) break;
+                        }
+                    } else {
+                        const u32 at = atomicAdd(&ms.nbig, 1u);
+                        if (at < MAXBIG) {
+                            ms.big[at][0] = start;
+                            ms.big[at][1] = end;
+                        } else ms.fail = 1;
+                    }
+                }
+                if (work > WORK_MAX) {
+                    ms.fail = 1;
+                    break;
+                }
+                start = end;
+            }
+        }
+        __syncthreads();
+        // big buckets (rare): rank counting over the whole CTA, through scratch
+        {
+            const u32 nbig = ms.nbig < MAXBIG ? ms.nbig : MAXBIG;
+            for (u32 g = 0; g < nbig && !ms.fail; g++) {
+                const u32 st = ms.big[g][0], sz = ms.big[g][1] - st;
+                if (sz > (u32)BIG_CAP) {
+                    ms.fail = 1;  // uniform: every thread reads the same sz
+                    break;
+                }
+                u32 work = 0;
+                for (u32 i = tid; i < sz; i += THREADS) {
+                    const u32 x = SS[st + i];
+                    u32 r = 0;
+                    for (u32 j = 0; j < sz && work <= 8 * WORK_MAX; j++)
+                        if (j != i && suf_less(T, SS[st + j], x, work)) r++;
+                    if (work > 8 * WORK_MAX) ms.fail = 1;
+                    else BIGS[r] = (u16)x;
+                }
+                __syncthreads();
+                for (u32 i = tid; i < sz; i += THREADS) SS[st + i] = BIGS[i];
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+        if (ms.fail) {
+            if (tid == 0) fb[atomicAdd(nfb, 1u)] = (u32)p;
+            continue;
+        }
+
+        // ---- 3. rank_of (1-based; 0 for positions >= limit)
+        const u32 rkn = 2u * ((n + 2u) / 3u + 1u) + 2u;
+        for (u32 i = tid; i < (rkn + 1) / 2; i += THREADS) reinterpret_cast<u32 *>(RK)[i] = 0;
+        __syncthreads();
+        for (u32 r = tid; r < m; r += THREADS) RK[slot(SS[r])] = (u16)(r + 1);
+        __syncthreads();
+
+        // ---- 4. non-samples: class-1 samples in rank order -> i = s-1,
+        //         stable by T[i] (codes 1..6; 16-bit lanes, codes 1-4 / 5-6)
+        {
+            const u32 per = (m + THREADS - 1) / THREADS;
+            const u32 r0 = tid * per, r1 = min(m, r0 + per);
+            unsigned long long c0 = 0, c1 = 0;
+            for (u32 r = r0; r < r1; r++) {
+                const u32 s = SS[r];
+                if (s % 3u == 1u) {
+                    const u32 c = T[s - 1];
+                    if (c <= 4) c0 += 1ull << (16 * (c - 1));
+                    else c1 += 1ull << (16 * (c - 5));
+                }
+            }
+            unsigned long long t0, t1;
+            unsigned long long e0 = block_exsum<unsigned long long>(c0, t0, ms.scan64[0]);
+            unsigned long long e1 = block_exsum<unsigned long long>(c1, t1, ms.scan64[1]);
+            u32 base[7];
+            u32 acc = 0;
+#pragma unroll
+            for (int c = 1; c <= 6; c++) {
+                base[c] = acc;
+                acc += (u32)(((c <= 4 ? t0 : t1) >> (16 * (c <= 4 ? c - 1 : c - 5))) & 0xFFFFu);
+            }
+#pragma unroll
+            for (int c = 1; c <= 6; c++)
+                base[c] += (u32)(((c <= 4 ? e0 : e1) >> (16 * (c <= 4 ? c - 1 : c - 5))) & 0xFFFFu);
+            for (u32 r = r0; r < r1; r++) {
+                const u32 s = SS[r];
+                if (s % 3u == 1u) {
+                    const u32 c = T[s - 1];
+                    u32 at = 0;
+#pragma unroll
+                    for (int cc = 1; cc <= 6; cc++)
+                        if (c == (u32)cc) at = base[cc]++;
+                    S0[at] = (u16)(s - 1);
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- 5. merge path: samples (pad sample dropped) with non-samples
+        {
+            const u32 pad = (n % 3u == 1u) ? 1u : 0u;
+            const u16 *A = SS + pad;
+            const u32 ma = m - pad, mb = (n + 2u) / 3u;
+            const u32 d0 = tid * ITEMS;
+            u32 outw[ITEMS / 2];
+            if (d0 < n) {
+                u32 lo = d0 > mb ? d0 - mb : 0u, hi = d0 < ma ? d0 : ma;
+                while (lo < hi) {  // number of samples among the first d0 outputs
+                    const u32 mid = (lo + hi) >> 1;
+                    if (sample_less(T, RK, A[mid], S0[d0 - mid - 1])) lo = mid + 1;
+                    else hi = mid;
+                }
+                u32 ia = lo, ib = d0 - lo;
+                u32 ha = ia < ma ? A[ia] : 0u, hb = ib < mb ? S0[ib] : 0u;
+#pragma unroll
+                for (int q = 0; q < ITEMS; q++) {
+                    u32 v = 0;
+                    if (d0 + q < n) {
+                        const bool ta = ib >= mb || (ia < ma && sample_less(T, RK, ha, hb));
+                        if (ta) {
+                            v = ha;
+                            ia++;
+                            ha = ia < ma ? A[ia] : 0u;
+                        } else {
+                            v = hb;
+                            ib++;
+                            hb = ib < mb ? S0[ib] : 0u;
+                        }
+                    }
+                    if (q & 1) outw[q >> 1] |= v << 16;
+                    else outw[q >> 1] = v;
+                }
+            }
+            __syncthreads();
+            if (d0 < n) {
+#pragma unroll
+                for (int q = 0; q < ITEMS / 2; q++)
+                    if (d0 + 2 * q < n) reinterpret_cast<u32 *>(SA)[(d0 >> 1) + q] = outw[q];
+            }
+        }
+        __syncthreads();
+
+        // ---- 6a. best = max LCP over adjacent cross-sequence pairs
+        const u32 r0 = tid * ITEMS;
+        u32 mx = 0;
+        {
+            u32 prev = (r0 > 0 && r0 < n) ? SA[r0 - 1] : 0u;
+            for (u32 q = 0; q < ITEMS && r0 + q < n; q++) {
+                const u32 cur = SA[r0 + q];
+                if (r0 + q > 0) {
+                    const bool cross = prev != nA && cur != nA && ((prev < nA) != (cur < nA));
+                    if (cross) mx = max(mx, suf_lcp(T, prev, cur));
+                }
+                prev = cur;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (lane_id() == 0) ms.red32[tid >> 5] = mx;
+            __syncthreads();
+            mx = 0;
+#pragma unroll
+            for (int w = 0; w < WARPS; w++) mx = max(mx, ms.red32[w]);
+        }
+        const u32 best = mx;
+        if (best == 0) {
+            if (tid == 0) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0;
+            __syncthreads();
+            continue;
+        }
+        // ---- 6b. runs of lcp >= best; smallest (min A, min B) of a run with both sides
+        {
+            unsigned long long head = 0;  // bit q: element r0+q starts a run; bit ITEMS: element r0+ITEMS
+            u32 prev = (r0 > 0 && r0 < n) ? SA[r0 - 1] : 0u;
+            for (u32 q = 0; q <= ITEMS && r0 + q < n; q++) {
+                const u32 cur = SA[r0 + q];
+                const bool h = (r0 + q == 0) || !lcp_at_least(T, prev, cur, best);
+                if (h) head |= 1ull << q;
+                prev = cur;
+            }
+            if (r0 + ITEMS >= n) head |= 1ull << (n > r0 ? n - r0 : 0);  // end of the array closes a run
+            Seg agg{0u, kInf, kInf};
+            for (u32 q = 0; q < ITEMS && r0 + q < n; q++) {
+                const u32 x = SA[r0 + q];
+                agg = seg_combine(agg, Seg{(u32)((head >> q) & 1ull), x < nA ? x : kInf, x > nA ? x : kInf});
+            }
+            Seg run = block_seg_exclusive(agg, ms);
+            unsigned long long win = ~0ull;
+            for (u32 q = 0; q < ITEMS && r0 + q < n; q++) {
+                const u32 x = SA[r0 + q];
+                run = seg_combine(run, Seg{(u32)((head >> q) & 1ull), x < nA ? x : kInf, x > nA ? x : kInf});
+                if (((head >> (q + 1)) & 1ull) && run.a != kInf && run.b != kInf)
+                    win = min(win, ((unsigned long long)run.a << 32) | run.b);
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) win = min(win, __shfl_xor_sync(0xffffffffu, win, o));
+            if (lane_id() == 0) ms.red64[tid >> 5] = win;
+            __syncthreads();
+            if (tid == 0) {
+#pragma unroll
+                for (int w = 1; w < WARPS; w++) win = min(win, ms.red64[w]);
+                out[3 * p] = best;
+                out[3 * p + 1] = (i64)(win >> 32);
+                out[3 * p + 2] = (i64)(win & 0xFFFFFFFFull) - (i64)nA - 1;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_fb_scatter(const u32 *__restrict__ list, i64 cnt, const i64 *__restrict__ sub, i64 *__restrict__ out) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (i64)gridDim.x * blockDim.x) {
+        const i64 p = list[i];
+        out[3 * p] = sub[3 * i];
+        out[3 * p + 1] = sub[3 * i + 1];
+        out[3 * p + 2] = sub[3 * i + 2];
+    }
+}
+
+__global__ void k_pd_init(i64 *__restrict__ out3, i64 *__restrict__ bad, u32 *__restrict__ ctr) {
+    out3[0] = out3[1] = out3[2] = 0;
+    *bad = INT64_MAX;
+    ctr[0] = ctr[1] = 0;
+}
+
+}  // namespace pd
+
+// Fallback capacity: the wave-global path re-runs the listed pairs in waves
+// of at most kFbResidues residues (or one pair, if a pair is longer).
+constexpr i64 kFbResidues = (i64)1 << 24;
+
+struct PairsWs {
+    i64 *offs;     // device copy of the caller's offsets
+    u32 *ctr;      // [0] next pair, [1] fallback count
+    u32 *fb;       // fallback pair list
+    i64 *dummy_bad;
+    u8 *fseqs;     // compacted fallback residues
+    i64 *fout;     // fallback results
+    void *gws;     // wave-global workspace
+    size_t gws_bytes;
+    i64 cap;       // residues per fallback wave
+};
+
+static i64 fb_capacity(const i64 *offs, i64 P) {
+    i64 cap = 0, total = 0;
+    for (i64 p = 0; p < P; p++) {
+        i64 la = offs[2 * p + 1] - offs[2 * p], lb = offs[2 * p + 2] - offs[2 * p + 1];
+        i64 len = (la && lb) ? la + lb : 0;
+        total += len;
+        if (len > cap) cap = len;
+    }
+    if (cap < kFbResidues) cap = kFbResidues;
+    if (cap > total) cap = total;
+    return cap;
+}
+
+static size_t pairs_ws(Arena &ar, const i64 *offs, i64 P, PairsWs *w) {
+    PairsWs t;
+    t.offs = ar.alloc<i64>(2 * P + 1);
+    t.ctr = ar.alloc<u32>(4);
+    t.fb = ar.alloc<u32>(P);
+    t.dummy_bad = ar.alloc<i64>(1);
+    t.cap = fb_capacity(offs, P);
+    t.fseqs = ar.alloc<u8>(t.cap + 16);
+    i64 pmax = t.cap / 2 + 1;  // pairs per fallback wave (each non-empty pair has >= 2 residues)
+    if (pmax > P) pmax = P;
+    t.fout = ar.alloc<i64>(3 * pmax + 3);
+    // worst-case wave-global workspace for a wave of <= cap residues over pmax pairs
+    std::vector<i64> probe(2 * pmax + 1);
+    for (i64 q = 0; q <= 2 * pmax; q++) probe[q] = q * (t.cap / (2 * pmax > 0 ? 2 * pmax : 1));
+    t.gws_bytes = t.cap > 0 ? overlap_batch_global_ws(probe.data(), pmax) : 0;
+    // a wave with fewer, longer pairs needs at most the single-pair workspace
+    if (t.cap > 0) {
+        i64 one[3] = {0, t.cap / 2, t.cap};
+        size_t s1 = overlap_batch_global_ws(one, 1);
+        if (s1 > t.gws_bytes) t.gws_bytes = s1;
+    }
+    t.gws = ar.alloc<char>((i64)t.gws_bytes);
+    if (w) *w = t;
+    return ar.peak;
+}
+
+}  // namespace saix
+
+using namespace saix;
+
+// Largest pair (GSA residues) the on-chip kernel takes; 0 sends every pair to
+// the wave-global path (A/B runs and tests of the fallback).
+static std::atomic<int> g_onchip_nmax{pd::NMAX};
+
+static thread_local long long g_last_fallbacks = 0;
+
+extern "C" int64_t saix_overlap_batch_last_fallbacks(void) { return g_last_fallbacks; }
+
+extern "C" int saix_overlap_batch_set_onchip(int on) {
+    return g_onchip_nmax.exchange(on ? pd::NMAX : 0) != 0;
+}
+
+extern "C" size_t saix_overlap_batch_workspace_bytes(const int64_t *offs_host, int64_t npairs) {
+    if (npairs < 0 || (npairs > 0 && !offs_host)) return 0;
+    for (i64 p = 0; p < 2 * npairs; p++)
+        if (offs_host[p + 1] < offs_host[p]) return 0;
+    Arena ar;
+    return pairs_ws(ar, offs_host, npairs, nullptr) + Arena::kAlign;
+}
+
+extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, int64_t npairs, int keep_n,
+                                  int64_t *out, int64_t *bad, void *ws, size_t ws_bytes, void *stream) {
+    if (npairs < 0 || (npairs > 0 && (!offs_host || !out)) || !bad) {
+        set_error("saix_overlap_batch: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    for (i64 p = 0; p < 2 * npairs; p++)
+        if (offs_host[p + 1] < offs_host[p]) {
+            set_error("saix_overlap_batch: offsets must be non-decreasing");
+            return SAIX_EINVAL;
+        }
+    cudaStream_t st = (cudaStream_t)stream;
+    const i64 P = npairs;
+    Arena ar{(char *)ws, ws_bytes};
+    PairsWs w;
+    pairs_ws(ar, offs_host, P, &w);
+    SAIX_ARENA_OK(ar);
+    g_last_fallbacks = 0;
+    pd::k_pd_init<<<1, 1, 0, st>>>(out, bad, w.ctr);  // out[0..2] zero, bad = INT64_MAX
+    SAIX_LAUNCHED();
+    if (P == 0) return SAIX_OK;
+    SAIX_CUDA(cudaMemcpyAsync(w.offs, offs_host, (size_t)(2 * P + 1) * 8, cudaMemcpyHostToDevice, st));
+    {
+        static DeviceFlags attr;
+        if (attr.need()) {
+            SAIX_CUDA(cudaFuncSetAttribute(pd::k_pair_dc3, cudaFuncAttributeMaxDynamicSharedMemorySize, pd::SMEM));
+            attr.set();
+        }
+        // C4 algorithmic bytes: 4,791,288 B per 20,001-residue pair (DC3 model + LCP + scan)
+        Prof prof_("pairs.dc3_onchip", 239.56 * (double)(offs_host[2 * P] - offs_host[0]), st);
+        const i64 grid = P < 2 * kNumSMs ? P : 2 * kNumSMs;
+        pd::k_pair_dc3<<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(seqs, w.offs, P, keep_n, out, bad, w.ctr,
+                                                                     w.ctr + 1, w.fb, g_onchip_nmax.load());
+    }
+    SAIX_LAUNCHED();
+    u32 nfb = 0;
+    SAIX_CUDA(cudaMemcpyAsync(&nfb, w.ctr + 1, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    SAIX_CUDA(cudaStreamSynchronize(st));
+    g_last_fallbacks = nfb;
+    if (nfb == 0) return SAIX_OK;
+    // fallback pairs: compact their residues and run the wave-global path
+    std::vector<u32> list(nfb);
+    SAIX_CUDA(cudaMemcpyAsync(list.data(), w.fb, (size_t)nfb * 4, cudaMemcpyDeviceToHost, st));
+    SAIX_CUDA(cudaStreamSynchronize(st));
+    std::sort(list.begin(), list.end());
+    u32 *dlist = w.fb;
+    SAIX_CUDA(cudaMemcpyAsync(dlist, list.data(), (size_t)nfb * 4, cudaMemcpyHostToDevice, st));
+    for (size_t i = 0; i < list.size();) {
+        std::vector<i64> sub{0};
+        size_t j = i;
+        i64 used = 0;
+        while (j < list.size()) {
+            const i64 p = list[j];
+            const i64 a0 = offs_host[2 * p], b0 = offs_host[2 * p + 1], b1 = offs_host[2 * p + 2];
+            if (j > i && used + (b1 - a0) > w.cap) break;
+            SAIX_CUDA(cudaMemcpyAsync(w.fseqs + used, seqs + a0, (size_t)(b1 - a0), cudaMemcpyDeviceToDevice, st));
+            sub.push_back(used + (b0 - a0));
+            used += b1 - a0;
+            sub.push_back(used);
+            j++;
+        }
+        SAIX_TRY(overlap_batch_global(w.fseqs, sub.data(), (i64)(j - i), keep_n, w.fout, w.dummy_bad, w.gws,
+                                      w.gws_bytes, st));
+        pd::k_fb_scatter<<<grid_for((i64)(j - i), 256), 256, 0, st>>>(dlist + i, (i64)(j - i), w.fout, out);
+        SAIX_LAUNCHED();
+        i = j;
+    }
+    return SAIX_OK;
+}

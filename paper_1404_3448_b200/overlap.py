@@ -210,14 +210,16 @@ class OverlapBatch:
     """Batched ``longest_overlap`` over many independent pairs on the device
     (saix_overlap_batch).  Pairs are packed as ASCII into ``seqs`` with
     ``offs`` (int64[2P+1]: pair p is A = seqs[offs[2p]:offs[2p+1]], B =
-    seqs[offs[2p+1]:offs[2p+2]]) and processed in waves of at most
-    ``wave_residues`` residues (one generalized text per wave)."""
+    seqs[offs[2p+1]:offs[2p+2]]).  Every pair of up to 20,480 GSA residues
+    runs its whole pipeline in one CTA's shared memory; one call covers all
+    pairs unless ``wave_residues`` (or SAIX_WAVE_RESIDUES) splits the batch
+    into calls of at most that many residues."""
 
     def __init__(self, seqs: np.ndarray, offs: np.ndarray, policy: NPolicy = NPolicy.REJECT,
                  wave_residues: int | None = None):
         if wave_residues is None:
             import os
-            wave_residues = int(os.environ.get("SAIX_WAVE_RESIDUES", 1 << 27))
+            wave_residues = int(os.environ.get("SAIX_WAVE_RESIDUES", 1 << 62))
         t = _lib.torch()
         L = _lib.load()
         dev = _lib.device()

@@ -113,3 +113,102 @@ def test_full_wave_c4_scale():
         a = seqs[offs[2 * p]:offs[2 * p + 1]].tobytes()
         b = seqs[offs[2 * p + 1]:offs[2 * p + 2]].tobytes()
         assert tuple(int(x) for x in got[p]) == oracle.longest_overlap(a, b), p
+
+
+# ---------------------------------------------------------------- on-chip path
+# saix_overlap_batch runs every pair of <= 20,480 GSA residues in one CTA
+# (csrc/pairdc3.cu) and sends longer / over-budget pairs to the wave-global
+# DC3; both must give the reference's answer (overlap.py:110-152).
+
+def _rnd(rng, k, alpha=b"ACGT"):
+    return np.frombuffer(alpha, np.uint8)[rng.integers(0, len(alpha), k)].tobytes()
+
+
+def _batch(pairs_bytes, keep=False):
+    seqs = np.frombuffer(b"".join(a + b for a, b in pairs_bytes), np.uint8)
+    offs = [0]
+    for a, b in pairs_bytes:
+        offs += [offs[-1] + len(a), offs[-1] + len(a) + len(b)]
+    return seqs, np.asarray(offs, np.int64)
+
+
+def _run(seqs, offs, keep=False, onchip=True):
+    from paper_1404_3448_b200 import _lib
+    L = _lib.load()
+    prev = L.saix_overlap_batch_set_onchip(int(onchip))
+    try:
+        ob = sx.OverlapBatch(seqs, offs, sx.NPolicy.KEEP if keep else sx.NPolicy.REJECT)
+        ob.run_device()
+        return ob.results()
+    finally:
+        L.saix_overlap_batch_set_onchip(prev)
+
+
+def test_onchip_equals_wave_global_and_oracle():
+    seqs, offs = c4_pairs(0, 3000)
+    want = oracle.overlap_batch(seqs, offs, threads=8)
+    assert np.array_equal(_run(seqs, offs, onchip=True), want)
+    from paper_1404_3448_b200 import _lib
+    assert _lib.load().saix_overlap_batch_last_fallbacks() == 0   # all C4 pairs stayed on chip
+    assert np.array_equal(_run(seqs[: offs[600]], offs[:601], onchip=False), want[:300])
+    assert _lib.load().saix_overlap_batch_last_fallbacks() == 300
+
+
+def test_onchip_small_pairs_every_length_mod3():
+    rng = np.random.default_rng(11)
+    pairs = []
+    for la in range(1, 25):
+        for lb in range(1, 25):
+            a = _rnd(rng, la)
+            b = _rnd(rng, lb, b"AC")
+            pairs.append((a, b))
+    seqs, offs = _batch(pairs)
+    want = oracle.overlap_batch(seqs, offs, threads=8)
+    assert np.array_equal(_run(seqs, offs), want)
+
+
+def test_onchip_mixed_with_fallback_pairs():
+    """Poly-A and tandem-repeat pairs (buckets / comparisons over the on-chip
+    bounds), pairs longer than 20,480 residues, pairs right at the limit,
+    empty sides and ordinary pairs in one call."""
+    rng = np.random.default_rng(12)
+
+    def rnd(k, alpha=b"ACGT"):
+        return _rnd(rng, k, alpha)
+
+    pairs = [
+        (b"A" * 9000, b"A" * 8000 + b"C"),                      # one huge bucket
+        (b"ACGT" * 2500, b"TACG" * 2400),                       # long periodic repeats
+        (rnd(15000), rnd(12000)),                                # longer than the on-chip limit
+        (rnd(10239), rnd(10240)),                                # n = 20480 exactly
+        (rnd(10240), rnd(10240)),                                # n = 20481
+        (b"", rnd(50)), (rnd(50), b""),
+        (rnd(5000), rnd(5000)),
+        (b"AT" * 300 + rnd(3000), rnd(2000) + b"AT" * 280),       # bucket of ~200 samples
+        (rnd(10000, b"AT"), rnd(10000, b"AT")),                   # two-letter text: big buckets, long LCPs
+    ]
+    a, b = rnd(10000), bytearray(rnd(10000))
+    b[4000:4256] = a[1234:1490]                                   # planted block of 256
+    pairs.append((a, bytes(b)))
+    seqs, offs = _batch(pairs)
+    want = oracle.overlap_batch(seqs, offs, threads=8)
+    got = _run(seqs, offs)
+    assert np.array_equal(got, want), np.flatnonzero(np.any(got != want, axis=1))
+    assert tuple(got[-1]) >= (256,)
+
+
+def test_onchip_keep_n_and_reject():
+    rng = np.random.default_rng(13)
+    pairs = []
+    for _ in range(30):
+        a = _rnd(rng, 4000, b"ACGTN")
+        b = bytearray(_rnd(rng, 3000, b"ACGTN"))
+        b[100:400] = a[2000:2300]
+        pairs.append((a, bytes(b)))
+    seqs, offs = _batch(pairs)
+    want = oracle.overlap_batch(seqs, offs, keep_n=True, threads=8)
+    assert np.array_equal(_run(seqs, offs, keep=True), want)
+    ob = sx.OverlapBatch(seqs, offs)                             # REJECT: the first N in the batch
+    ob.run_device()
+    first = int(np.flatnonzero(seqs == ord("N"))[0])
+    assert int(ob.bad[0].item()) == first

@@ -239,16 +239,23 @@ def test_crafted_large_lcp_loads_like_reference():
     assert int(loaded.lcp.lcp[1]) == 1000
 
 
+def sx_build_lcp(eng):
+    from paper_1404_3448_b200.suffix_index import build_lcp
+    return build_lcp(eng.text, eng.sa).lcp
+
+
 def test_sigma_above_255_header_loads_like_reference():
     # one byte per rank in the file whatever sigma says; the reference keeps
     # the header's sigma (index_store.py:126) and so does the device text
-    blob = bytearray(saved_bytes(engine_for("ACGTACGT")))
+    blob = bytearray(saved_bytes(engine_for("ATTGCTAC")))
     blob[32:40] = (300).to_bytes(8, "little")
     loaded = index_store.load_index(io.BytesIO(_recrc(blob)))
     assert loaded.text.sigma == 300
-    ref = engine_for("ACGTACGT")
+    ref = engine_for("ATTGCTAC")
     assert loaded.sa.sa.tolist() == ref.sa.sa.tolist()
+    # test_overlap.py:22-26 answers on ATTGCTAC
     assert lcp_query(loaded, 3, 3) == 5 and lcp_query(loaded, 6, 0) == 1
+    assert sx_build_lcp(loaded).tolist() == ref.lcp.lcp.tolist()
 
 
 def test_widen_matches_host():
