@@ -262,6 +262,8 @@ SAIX_API int saix_overlap_batch_set_onchip(int on);
 /* Pairs of this thread's last saix_overlap_batch call that took the
  * wave-global path. */
 SAIX_API int64_t saix_overlap_batch_last_fallbacks(void);
+/* Diagnostics: per-phase SM cycles of the last call with SAIX_PD_CLOCKS=1. */
+SAIX_API int saix_overlap_batch_phase_clocks(int64_t *out, int max_phases);
 
 /* ------------------------------------------------ Cartesian tree / ±1 RMQ */
 /* build_cartesian + euler_tour (rmq.py:91-152) on the device: parent, left,

@@ -74,14 +74,17 @@ constexpr int OFF_T = 0;
 constexpr int OFF_SS = al16(NMAX + TPAD);
 constexpr int OFF_S0 = OFF_SS + al16(2 * MMAX);
 constexpr int OFF_RK = OFF_S0 + al16(2 * KMAX);
-constexpr int OFF_MISC = OFF_RK + al16(2 * RKMAX);
-constexpr int BIG_CAP = (OFF_MISC - OFF_S0 - 2 * NB) / 2;  // u16 scratch after the counters
+constexpr int QCAP = 8 * 32;  // per-warp queue of small buckets (one round: 8 per lane)
+constexpr int OFF_Q = OFF_RK + al16(2 * RKMAX);
+constexpr int OFF_MISC = OFF_Q + al16(2 * QCAP * WARPS);
+constexpr int BIG_CAP = (OFF_Q - OFF_S0 - 2 * NB) / 2;  // u16 scratch after the counters
 constexpr int SMEM = OFF_MISC + 1024;
-static_assert(2 * NB <= OFF_MISC - OFF_S0, "bucket counters must fit the S0 + RK region");
+static_assert(2 * NB <= OFF_Q - OFF_S0, "bucket counters must fit the S0 + RK region");
 static_assert(BIG_CAP >= 1024, "big-bucket scratch");
 static_assert(MMAX + KMAX >= NMAX + 1, "SA is written over the sample + non-sample runs");
 static_assert(SMEM <= 113 * 1024, "two CTAs per SM");
 
+constexpr int NPHASE = 12;  // phase clocks (SAIX_PD_CLOCKS=1): see PD_MARK uses
 struct Misc {
     unsigned long long scan64[2][WARPS + 1];
     u32 scan32[WARPS + 1];
@@ -92,15 +95,30 @@ struct Misc {
     u32 red32[WARPS];
     unsigned long long red64[WARPS];
     u32 seg[WARPS + 1][3];
+    long long t_prev;
+    long long acc[NPHASE];
+    long long tmax, tsum, acc2[2];
 };
 static_assert(sizeof(Misc) <= 1024, "misc");
 
-// 8 characters at T[off..off+8) (little endian: byte k = T[off + k])
+// thread 0's clock since the previous mark, charged to phase k (after a barrier,
+// so a phase's time includes waiting for its slowest thread)
+#define PD_MARK(k)                                         \
+    do {                                                   \
+        if (CLK && threadIdx.x == 0) {                     \
+            const long long t_ = clock64();                \
+            ms.acc[k] += t_ - ms.t_prev;                   \
+            ms.t_prev = t_;                                \
+        }                                                  \
+    } while (0)
+
+// 8 characters at T[off..off+8) (little endian: byte k = T[off + k]): three
+// aligned 32-bit shared loads and two byte permutes
 __device__ __forceinline__ u64 ld8(const u8 *T, u32 off) {
-    const u64 *w = reinterpret_cast<const u64 *>(T + (off & ~7u));
-    const u64 lo = w[0], hi = w[1];
-    const u32 sh = (off & 7u) * 8u;
-    return (lo >> sh) | ((hi << 1) << (63u - sh));
+    const u32 *w = reinterpret_cast<const u32 *>(T + (off & ~3u));
+    const u32 a = w[0], b = w[1], c = w[2];
+    const u32 sel = 0x3210u + (off & 3u) * 0x1111u;
+    return ((u64)__byte_perm(b, c, sel) << 32) | __byte_perm(a, b, sel);
 }
 
 // suffix i < suffix j (i != j); `work` counts 8-character steps.  Distinct
@@ -140,6 +158,21 @@ __device__ __forceinline__ bool lcp_at_least(const u8 *T, u32 i, u32 j, u32 need
 // keeps it >=.)
 __device__ __forceinline__ u32 bucket_of(const u8 *T, u32 s) {
     const u64 w = ld8(T, s);
+    const u64 w7 = w & 0x00FFFFFFFFFFFFFFull;
+    // fast path (no pad / separator / N among the 7): digit = code - 2, all
+    // bytes at once; codes < 128, so byte-wise adds never carry
+    const bool ge2 = ((w7 + 0x007E7E7E7E7E7E7Eull) & 0x0080808080808080ull) == 0x0080808080808080ull;
+    const bool ge6 = ((w7 + 0x007A7A7A7A7A7A7Aull) & 0x0080808080808080ull) != 0;
+    if (ge2 && !ge6) {
+        // byte k holds digit k (<= 3); pack with character 0 most significant
+        u64 d = w7 - 0x0002020202020202ull;
+        const u32 lo = (u32)d, hi = (u32)(d >> 32);
+        const u32 r = __byte_perm(lo, 0u, 0x0123);               // bytes 3..0 = c0 c1 c2 c3
+        const u32 q = __byte_perm(hi, 0u, 0x4012);               // bytes 2..0 = c4 c5 c6
+        const u32 r4 = (r | (r >> 6)) & 0x000F000Fu, r8 = (r4 | (r4 >> 12)) & 0xFFu;  // 8 bits: c0..c3
+        const u32 q4 = (q | (q >> 6)) & 0x000F000Fu, q6 = (q4 >> 16 << 4) | (q4 & 0xFu);   // 6 bits: c4..c6
+        return (r8 << 6) | q6;
+    }
     u32 b = 0, mode = 0;  // 0 normal, 1 zero fill, 2 three fill
 #pragma unroll
     for (int k = 0; k < 7; k++) {
@@ -170,6 +203,21 @@ __device__ __forceinline__ bool sample_less(const u8 *T, const u16 *RK, u32 a, u
     const u32 ca1 = T[a + 1], cb1 = T[b + 1];
     if (ca1 != cb1) return ca1 < cb1;
     return RK[slot(a + 2)] < RK[slot(b + 2)];
+}
+
+// The same comparator as 32-bit keys (codes < 8, ranks < 2^16):
+// K1(x) = T[x] << 16 | R(x+1), K2(x) = T[x] << 24 | T[x+1] << 16 | R(x+2);
+// a mod-1 sample compares by K1, a mod-2 sample by K2.
+__device__ __forceinline__ u32 key1s(const u8 *T, const u16 *RK, u32 a) {  // a % 3 == 1: slot(a+1) = 2(a/3)+1
+    return ((u32)T[a] << 16) | RK[2u * (a / 3u) + 1u];
+}
+__device__ __forceinline__ u32 key2s(const u8 *T, const u16 *RK, u32 a) {  // a % 3 == 2: slot(a+2) = 2(a/3+1)
+    return ((u32)T[a] << 24) | ((u32)T[a + 1] << 16) | RK[2u * (a / 3u) + 2u];
+}
+__device__ __forceinline__ void key12n(const u8 *T, const u16 *RK, u32 b, u32 &k1, u32 &k2) {  // b % 3 == 0
+    const u32 q = 2u * (b / 3u), c0 = T[b], c1 = T[b + 1];
+    k1 = (c0 << 16) | RK[q];
+    k2 = (c0 << 24) | (c1 << 16) | RK[q + 1];
 }
 
 // GSA code of one ASCII residue (rank + 1; 0 = illegal)
@@ -314,10 +362,11 @@ __device__ __forceinline__ Seg block_seg_exclusive(Seg v, Misc &ms) {
     return carry;
 }
 
+template <bool CLK>
 __global__ void __launch_bounds__(THREADS, 2)
 k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int keep_n, i64 *__restrict__ out,
            i64 *__restrict__ bad, u32 *__restrict__ next_pair, u32 *__restrict__ nfb, u32 *__restrict__ fb,
-           int nmax) {
+           int nmax, unsigned long long *__restrict__ clk) {
     extern __shared__ __align__(16) unsigned char smem[];
     u8 *T = smem + OFF_T;
     u16 *SS = reinterpret_cast<u16 *>(smem + OFF_SS);
@@ -326,8 +375,14 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
     u16 *RK = reinterpret_cast<u16 *>(smem + OFF_RK);
     u32 *CNT = reinterpret_cast<u32 *>(smem + OFF_S0);  // NB u16 counters, two per word
     u16 *BIGS = reinterpret_cast<u16 *>(smem + OFF_S0 + 2 * NB);
+    u16 *QW = reinterpret_cast<u16 *>(smem + OFF_Q);
     Misc &ms = *reinterpret_cast<Misc *>(smem + OFF_MISC);
     const u32 tid = threadIdx.x;
+    if (CLK && tid == 0) {
+        ms.t_prev = clock64();
+        for (int k = 0; k < NPHASE; k++) ms.acc[k] = 0;
+        ms.tmax = ms.tsum = ms.acc2[0] = ms.acc2[1] = 0;
+    }
 
     for (;;) {
         __syncthreads();  // every shared read of the previous pair is done
@@ -337,6 +392,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             ms.nbig = 0;
         }
         __syncthreads();
+        PD_MARK(11);
         const i64 p = ms.pair;
         if (p >= P) break;
         const i64 a0 = offs[2 * p], b0 = offs[2 * p + 1], b1 = offs[2 * p + 2];
@@ -366,6 +422,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             for (u32 i = tid; i < NB / 2; i += THREADS) CNT[i] = 0;
         }
         __syncthreads();
+        PD_MARK(0);
 
         // ---- 2. sample buckets: sample q <-> position 3(q/2) + 1 + (q&1)
         const u32 limit = (n % 3u == 1u) ? n + 1 : n;
@@ -378,6 +435,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             }
         }
         __syncthreads();
+        PD_MARK(1);
         // exclusive scan of the 2^14 u16 counts (32 per thread)
         {
             constexpr int W = NB / 2 / THREADS;  // 16 words per thread
@@ -397,6 +455,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             }
         }
         __syncthreads();
+        PD_MARK(2);
         for (u32 q = tid; q < qmax; q += THREADS) {
             const u32 s = 3u * (q >> 1) + 1u + (q & 1u);
             if (s < limit) {
@@ -406,45 +465,112 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             }
         }
         __syncthreads();
+        PD_MARK(3);
         const u32 m = (CNT[NB / 2 - 1] >> 16);  // end of the last bucket = number of samples
 
         // ---- in-bucket exact sort (counters now hold bucket ends)
         {
+            const long long t_in = CLK ? clock64() : 0;
             u32 work = 0;
             const u16 *C16 = reinterpret_cast<const u16 *>(CNT);
-            constexpr int BPT = NB / THREADS;  // 32 buckets per thread
-            u32 start = tid ? C16[tid * BPT - 1] : 0u;
-            for (int k = 0; k < BPT; k++) {
-                const u32 end = C16[tid * BPT + k];
-                const u32 sz = end - start;
-                if (sz >= 2) {
-                    if (sz <= SMALL) {
-                        for (u32 i = start + 1; i < end; i++) {
-                            const u32 x = SS[i];
-                            u32 j = i;
-                            while (j > start && suf_less(T, x, SS[j - 1], work)) {
-                                SS[j] = SS[j - 1];
-                                j--;
-                            }
-                            SS[j] = (u16)x;
-                            if (work > WORK_MAX) break;
-                        }
-                    } else {
+            // Insertion sort of every bucket of 2..SMALL samples, one 8-character
+            // word compare per step.  Buckets are collected into a per-warp queue
+            // (a round of 8 buckets per lane) and the warp's lanes pull buckets
+            // from it as they finish, so the lanes run in lock step with balanced
+            // work (a per-lane loop over its own buckets serialises the lanes).
+            constexpr int BPT = NB / THREADS;  // 32 buckets per lane, strided: the heavy
+                                               // (A/T-rich) prefixes spread over all lanes
+            u16 *Q = QW + (tid >> 5) * QCAP;
+            const u32 lane = lane_id(), lt = lanemask_lt();
+            for (int round = 0; round < BPT / 8; round++) {
+                u32 qn = 0;
+#pragma unroll
+                for (int kk = 0; kk < 8; kk++) {
+                    const u32 b = tid + (u32)(round * 8 + kk) * THREADS;
+                    const u32 st = b ? C16[b - 1] : 0u, sz = C16[b] - st;
+                    if (sz > (u32)SMALL) {
                         const u32 at = atomicAdd(&ms.nbig, 1u);
                         if (at < MAXBIG) {
-                            ms.big[at][0] = start;
-                            ms.big[at][1] = end;
+                            ms.big[at][0] = st;
+                            ms.big[at][1] = st + sz;
                         } else ms.fail = 1;
                     }
+                    const bool want = sz >= 2 && sz <= (u32)SMALL;
+                    const u32 mask = __ballot_sync(0xffffffffu, want);
+                    if (want) Q[qn + __popc(mask & lt)] = (u16)b;
+                    qn += __popc(mask);
                 }
-                if (work > WORK_MAX) {
-                    ms.fail = 1;
-                    break;
+                __syncwarp();
+                u32 taken = min(qn, 32u);  // tasks handed out so far (warp-uniform)
+                u32 start = 0, end = 0, i = 0, j = 0, x = 0, h = 0;
+                bool live = lane < qn;
+                if (live) {
+                    const u32 b = Q[lane];
+                    start = b ? C16[b - 1] : 0u;
+                    end = C16[b];
+                    i = j = start + 1;
+                    x = SS[i];
                 }
-                start = end;
+                while (__any_sync(0xffffffffu, live)) {
+                    bool done = false;
+                    if (live) {
+                        const u32 y = SS[j - 1];
+                        const u64 wa = ld8(T, x + h), wb = ld8(T, y + h);
+                        if (wa == wb) {
+                            h += 8;
+                            if (++work > WORK_MAX) {
+                                ms.fail = 1;
+                                live = false;
+                            }
+                        } else {
+                            const int sh = (__ffsll((long long)(wa ^ wb)) - 1) & ~7;
+                            const bool less = ((wa >> sh) & 0xFFu) < ((wb >> sh) & 0xFFu);
+                            h = 0;
+                            if (less) {
+                                SS[j] = (u16)y;
+                                j--;
+                            }
+                            if (!less || j == start) {
+                                SS[j] = (u16)x;
+                                if (++i < end) {
+                                    x = SS[i];
+                                    j = i;
+                                } else {
+                                    done = true;
+                                }
+                            }
+                        }
+                    }
+                    // lanes that finished a bucket take the next queued ones
+                    const u32 dm = __ballot_sync(0xffffffffu, done);
+                    if (done) {
+                        const u32 t = taken + __popc(dm & lt);
+                        live = t < qn;
+                        if (live) {
+                            const u32 b = Q[t];
+                            start = b ? C16[b - 1] : 0u;
+                            end = C16[b];
+                            i = j = start + 1;
+                            x = SS[i];
+                        }
+                    }
+                    taken += __popc(dm);
+                }
+                __syncwarp();
+            }
+            if (CLK) {
+                atomicMax((unsigned long long *)&ms.tmax, (unsigned long long)(clock64() - t_in));
+                atomicAdd((unsigned long long *)&ms.tsum, (unsigned long long)(clock64() - t_in));
             }
         }
         __syncthreads();
+        PD_MARK(4);
+        if (CLK && tid == 0) {
+            ms.acc2[0] += ms.tmax;
+            ms.acc2[1] += ms.tsum / THREADS;
+            ms.tmax = 0;
+            ms.tsum = 0;
+        }
         // big buckets (rare): rank counting over the whole CTA, through scratch
         {
             const u32 nbig = ms.nbig < MAXBIG ? ms.nbig : MAXBIG;
@@ -469,6 +595,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             }
         }
         __syncthreads();
+        PD_MARK(5);
         if (ms.fail) {
             if (tid == 0) fb[atomicAdd(nfb, 1u)] = (u32)p;
             continue;
@@ -480,6 +607,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
         __syncthreads();
         for (u32 r = tid; r < m; r += THREADS) RK[slot(SS[r])] = (u16)(r + 1);
         __syncthreads();
+        PD_MARK(6);
 
         // ---- 4. non-samples: class-1 samples in rank order -> i = s-1,
         //         stable by T[i] (codes 1..6; 16-bit lanes, codes 1-4 / 5-6)
@@ -521,6 +649,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             }
         }
         __syncthreads();
+        PD_MARK(7);
 
         // ---- 5. merge path: samples (pad sample dropped) with non-samples
         {
@@ -536,21 +665,45 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                     if (sample_less(T, RK, A[mid], S0[d0 - mid - 1])) lo = mid + 1;
                     else hi = mid;
                 }
+                // the comparator's keys of the two run heads, recomputed only
+                // when a head advances: sample a -> its own key (K1 for mod 1,
+                // K2 for mod 2); non-sample b -> both K1(b) and K2(b).  One
+                // branch-free head update per output (either side).
                 u32 ia = lo, ib = d0 - lo;
-                u32 ha = ia < ma ? A[ia] : 0u, hb = ib < mb ? S0[ib] : 0u;
+                u32 ha = 0, hb = 0, ka = 0, kb1 = 0, kb2 = 0;
+                bool a1 = true;
+                if (ia < ma) {
+                    ha = A[ia];
+                    a1 = ha % 3u == 1u;
+                    ka = a1 ? key1s(T, RK, ha) : key2s(T, RK, ha);
+                }
+                if (ib < mb) {
+                    hb = S0[ib];
+                    key12n(T, RK, hb, kb1, kb2);
+                }
 #pragma unroll
                 for (int q = 0; q < ITEMS; q++) {
                     u32 v = 0;
                     if (d0 + q < n) {
-                        const bool ta = ib >= mb || (ia < ma && sample_less(T, RK, ha, hb));
+                        const bool ta = ib >= mb || (ia < ma && (a1 ? ka < kb1 : ka < kb2));
+                        v = ta ? ha : hb;
+                        ia += ta;
+                        ib += !ta;
+                        const bool more = ta ? ia < ma : ib < mb;
+                        const u32 p = more ? (ta ? A[ia] : S0[ib]) : 0u;
+                        const u32 q3 = p / 3u, pm = p - 3u * q3;
+                        const u32 o1 = ta ? (pm == 1u ? 1u : 2u) : 0u, o2 = ta ? o1 : 1u;
+                        const u32 c0 = T[p], c1 = T[p + 1];
+                        const u32 k1 = (c0 << 16) | RK[2u * q3 + o1];
+                        const u32 k2 = (c0 << 24) | (c1 << 16) | RK[2u * q3 + o2];
                         if (ta) {
-                            v = ha;
-                            ia++;
-                            ha = ia < ma ? A[ia] : 0u;
+                            ha = p;
+                            a1 = pm == 1u;
+                            ka = a1 ? k1 : k2;
                         } else {
-                            v = hb;
-                            ib++;
-                            hb = ib < mb ? S0[ib] : 0u;
+                            hb = p;
+                            kb1 = k1;
+                            kb2 = k2;
                         }
                     }
                     if (q & 1) outw[q >> 1] |= v << 16;
@@ -565,24 +718,47 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             }
         }
         __syncthreads();
+        PD_MARK(8);
 
-        // ---- 6a. best = max LCP over adjacent cross-sequence pairs
+        // ---- 6a. lcp of every adjacent pair (saturated to a byte, in the
+        //          rank table's place) and best = max over cross-sequence pairs
+        u8 *LC = reinterpret_cast<u8 *>(RK);
         const u32 r0 = tid * ITEMS;
         u32 mx = 0;
         {
-            u32 prev = (r0 > 0 && r0 < n) ? SA[r0 - 1] : 0u;
-            for (u32 q = 0; q < ITEMS && r0 + q < n; q++) {
-                const u32 cur = SA[r0 + q];
-                if (r0 + q > 0) {
-                    const bool cross = prev != nA && cur != nA && ((prev < nA) != (cur < nA));
-                    if (cross) mx = max(mx, suf_lcp(T, prev, cur));
+            // one 8-character word compare per step, lanes in lock step (see
+            // the in-bucket sort); rank 0 has no predecessor (lcp 0)
+            u32 q = 0, h = 0, prev = 0, cur = 0;
+            bool live = r0 < n;
+            if (live) {
+                cur = SA[r0];
+                prev = r0 ? SA[r0 - 1] : cur;
+            }
+            while (__any_sync(0xffffffffu, live)) {
+                if (live) {
+                    const u64 x = (r0 + q == 0) ? 1ull : (ld8(T, prev + h) ^ ld8(T, cur + h));
+                    if (!x) {
+                        h += 8;
+                    } else {
+                        const u32 l = (r0 + q == 0) ? 0u : h + ((u32)(__ffsll((long long)x) - 1) >> 3);
+                        const bool cross = prev != nA && cur != nA && ((prev < nA) != (cur < nA));
+                        if (cross) mx = max(mx, l);
+                        LC[r0 + q] = (u8)min(l, 255u);
+                        h = 0;
+                        if (++q < (u32)ITEMS && r0 + q < n) {
+                            prev = cur;
+                            cur = SA[r0 + q];
+                        } else {
+                            live = false;
+                        }
+                    }
                 }
-                prev = cur;
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             if (lane_id() == 0) ms.red32[tid >> 5] = mx;
             __syncthreads();
+            PD_MARK(9);
             mx = 0;
 #pragma unroll
             for (int w = 0; w < WARPS; w++) mx = max(mx, ms.red32[w]);
@@ -590,18 +766,17 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
         const u32 best = mx;
         if (best == 0) {
             if (tid == 0) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0;
-            __syncthreads();
             continue;
         }
         // ---- 6b. runs of lcp >= best; smallest (min A, min B) of a run with both sides
         {
             unsigned long long head = 0;  // bit q: element r0+q starts a run; bit ITEMS: element r0+ITEMS
-            u32 prev = (r0 > 0 && r0 < n) ? SA[r0 - 1] : 0u;
+            const u32 bcap = min(best, 255u);
             for (u32 q = 0; q <= ITEMS && r0 + q < n; q++) {
-                const u32 cur = SA[r0 + q];
-                const bool h = (r0 + q == 0) || !lcp_at_least(T, prev, cur, best);
+                const u32 r = r0 + q, l = LC[r];
+                bool h = (r == 0) || l < bcap;
+                if (!h && best > 255u) h = !lcp_at_least(T, SA[r - 1], SA[r], best);  // saturated entry
                 if (h) head |= 1ull << q;
-                prev = cur;
             }
             if (r0 + ITEMS >= n) head |= 1ull << (n > r0 ? n - r0 : 0);  // end of the array closes a run
             Seg agg{0u, kInf, kInf};
@@ -621,6 +796,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             for (int o = 16; o; o >>= 1) win = min(win, __shfl_xor_sync(0xffffffffu, win, o));
             if (lane_id() == 0) ms.red64[tid >> 5] = win;
             __syncthreads();
+            PD_MARK(10);
             if (tid == 0) {
 #pragma unroll
                 for (int w = 1; w < WARPS; w++) win = min(win, ms.red64[w]);
@@ -629,7 +805,11 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                 out[3 * p + 2] = (i64)(win & 0xFFFFFFFFull) - (i64)nA - 1;
             }
         }
-        __syncthreads();
+    }
+    if (CLK && tid == 0) {
+        for (int k = 0; k < NPHASE; k++) atomicAdd(clk + k, (unsigned long long)ms.acc[k]);
+        atomicAdd(clk + NPHASE, (unsigned long long)ms.acc2[0]);
+        atomicAdd(clk + NPHASE + 1, (unsigned long long)ms.acc2[1]);
     }
 }
 
@@ -658,6 +838,7 @@ struct PairsWs {
     i64 *offs;     // device copy of the caller's offsets
     u32 *ctr;      // [0] next pair, [1] fallback count
     u32 *fb;       // fallback pair list
+    unsigned long long *clk;  // phase clocks (SAIX_PD_CLOCKS=1)
     i64 *dummy_bad;
     u8 *fseqs;     // compacted fallback residues
     i64 *fout;     // fallback results
@@ -684,6 +865,7 @@ static size_t pairs_ws(Arena &ar, const i64 *offs, i64 P, PairsWs *w) {
     t.offs = ar.alloc<i64>(2 * P + 1);
     t.ctr = ar.alloc<u32>(4);
     t.fb = ar.alloc<u32>(P);
+    t.clk = ar.alloc<unsigned long long>(pd::NPHASE + 2);
     t.dummy_bad = ar.alloc<i64>(1);
     t.cap = fb_capacity(offs, P);
     t.fseqs = ar.alloc<u8>(t.cap + 16);
@@ -714,6 +896,24 @@ using namespace saix;
 static std::atomic<int> g_onchip_nmax{pd::NMAX};
 
 static thread_local long long g_last_fallbacks = 0;
+static unsigned long long g_phase_clk[pd::NPHASE + 2];
+
+static bool clocks_on() {
+    static const bool on = [] {
+        const char *e = getenv("SAIX_PD_CLOCKS");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// Per-phase SM cycles (summed over CTAs) of the last call when SAIX_PD_CLOCKS=1:
+// 0 load, 1 bucket counts, 2 scan, 3 scatter, 4 in-bucket sort, 5 big buckets,
+// 6 ranks, 7 non-samples, 8 merge, 9 LCP pass 1, 10 runs pass 2, 11 pair fetch.
+extern "C" int saix_overlap_batch_phase_clocks(int64_t *out, int max) {
+    int k = 0;
+    for (; k < max && k < pd::NPHASE + 2; k++) out[k] = (int64_t)g_phase_clk[k];
+    return k;
+}
 
 extern "C" int64_t saix_overlap_batch_last_fallbacks(void) { return g_last_fallbacks; }
 
@@ -754,18 +954,29 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
     {
         static DeviceFlags attr;
         if (attr.need()) {
-            SAIX_CUDA(cudaFuncSetAttribute(pd::k_pair_dc3, cudaFuncAttributeMaxDynamicSharedMemorySize, pd::SMEM));
+            SAIX_CUDA(cudaFuncSetAttribute(pd::k_pair_dc3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           pd::SMEM));
+            SAIX_CUDA(cudaFuncSetAttribute(pd::k_pair_dc3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           pd::SMEM));
             attr.set();
         }
         // C4 algorithmic bytes: 4,791,288 B per 20,001-residue pair (DC3 model + LCP + scan)
         Prof prof_("pairs.dc3_onchip", 239.56 * (double)(offs_host[2 * P] - offs_host[0]), st);
         const i64 grid = P < 2 * kNumSMs ? P : 2 * kNumSMs;
-        pd::k_pair_dc3<<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(seqs, w.offs, P, keep_n, out, bad, w.ctr,
-                                                                     w.ctr + 1, w.fb, g_onchip_nmax.load());
+        if (clocks_on()) {
+            SAIX_CUDA(cudaMemsetAsync(w.clk, 0, sizeof(unsigned long long) * (pd::NPHASE + 2), st));
+            pd::k_pair_dc3<true><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
+                seqs, w.offs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk);
+        } else {
+            pd::k_pair_dc3<false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
+                seqs, w.offs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr);
+        }
     }
     SAIX_LAUNCHED();
     u32 nfb = 0;
     SAIX_CUDA(cudaMemcpyAsync(&nfb, w.ctr + 1, sizeof(u32), cudaMemcpyDeviceToHost, st));
+    if (clocks_on())
+        SAIX_CUDA(cudaMemcpyAsync(g_phase_clk, w.clk, sizeof(g_phase_clk), cudaMemcpyDeviceToHost, st));
     SAIX_CUDA(cudaStreamSynchronize(st));
     g_last_fallbacks = nfb;
     if (nfb == 0) return SAIX_OK;
