@@ -460,8 +460,7 @@ class C4:
 
     def step_e2e(self):
         import torch
-        self.ob.seqs_dev[: self.seqs.shape[0]].copy_(self.hseqs, non_blocking=True)
-        self.ob.run_device()
+        self.ob.run_from_host(self.hseqs)     # chunked H2D overlapped with the chunks' pairs
         self._gather()
         self.hout.copy_(self.ob.out[: 3 * self.P], non_blocking=True)
         torch.cuda.current_stream().synchronize()

@@ -256,6 +256,13 @@ SAIX_API size_t saix_overlap_batch_workspace_bytes(const int64_t *offs_host, int
 SAIX_API int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, int64_t npairs,
                                 int keep_n, int64_t *out, int64_t *bad, void *ws,
                                 size_t ws_bytes, void *stream);
+/* The same with the offsets also resident on the device (offs_dev, equal to
+ * offs_host): no H2D inside the call, so it can run while bulk host-to-device
+ * copies are in flight on the copy engine (chunked e2e pipelines). */
+SAIX_API int saix_overlap_batch_dev(const uint8_t *seqs, const int64_t *offs_host,
+                                    const int64_t *offs_dev, int64_t npairs, int keep_n,
+                                    int64_t *out, int64_t *bad, void *ws, size_t ws_bytes,
+                                    void *stream);
 /* 0: route every pair through the wave-global path (A/B and tests); returns
  * the previous setting. */
 SAIX_API int saix_overlap_batch_set_onchip(int on);

@@ -74,9 +74,12 @@ constexpr int OFF_T = 0;
 constexpr int OFF_SS = al16(NMAX + TPAD);
 constexpr int OFF_S0 = OFF_SS + al16(2 * MMAX);
 constexpr int OFF_RK = OFF_S0 + al16(2 * KMAX);
-constexpr int QCAP = 8 * 32;  // per-warp queue of small buckets (one round: 8 per lane)
+constexpr int QROUND = 16;            // buckets per lane per queue round
+constexpr int QCAP = QROUND * 32;     // per-warp queue of small buckets
 constexpr int OFF_Q = OFF_RK + al16(2 * RKMAX);
-constexpr int OFF_MISC = OFF_Q + al16(2 * QCAP * WARPS);
+constexpr int P2W = NMAX / 32 + 2;    // 2-bit packed text words
+constexpr int OFF_P2 = OFF_Q + al16(2 * QCAP * WARPS);
+constexpr int OFF_MISC = OFF_P2 + 8 * P2W;
 constexpr int BIG_CAP = (OFF_Q - OFF_S0 - 2 * NB) / 2;  // u16 scratch after the counters
 constexpr int SMEM = OFF_MISC + 1024;
 static_assert(2 * NB <= OFF_Q - OFF_S0, "bucket counters must fit the S0 + RK region");
@@ -120,6 +123,58 @@ __device__ __forceinline__ u64 ld8(const u8 *T, u32 off) {
     const u32 sel = 0x3210u + (off & 3u) * 0x1111u;
     return ((u64)__byte_perm(b, c, sel) << 32) | __byte_perm(a, b, sel);
 }
+
+// The pair text for suffix comparisons.  Packed mode (no N): the residues
+// 2-bit packed, 32 characters per 64-bit word; the separator (position nA)
+// and the end (n) are unique, so a comparison runs over at most
+// L = min(lim(i), lim(j)) residues, and if those are equal the suffix that
+// reaches its special first is smaller (a special, code <= 1, is below every
+// residue), on equal distance the one reaching the end (pad 0) is below the
+// one reaching the separator (1).  Byte mode (NPolicy.KEEP): 8 codes per step
+// on T, where pad 0 < separator 1 < residues makes plain byte order exact.
+struct Txt {
+    const u8 *T;
+    const u64 *P2;
+    u32 nA, n;
+    bool packed;
+    __device__ __forceinline__ u32 step() const { return packed ? 32u : 8u; }
+    __device__ __forceinline__ u32 lim(u32 i) const { return i <= nA ? nA - i : n - i; }
+    __device__ __forceinline__ u64 ld32(u32 i) const {
+        const u32 w = i >> 5, sh = 2u * (i & 31u);
+        return (P2[w] >> sh) | ((P2[w + 1] << 1) << (63u - sh));
+    }
+    // One comparison step of suffixes i != j at offset h.  0: equal so far
+    // (continue at h + step()); 1: i < j; 2: i > j.  When decided, *lcp is
+    // their longest common prefix.
+    __device__ __forceinline__ int cmp(u32 i, u32 j, u32 h, u32 &lcp) const {
+        if (packed) {
+            const u32 li = lim(i), lj = lim(j), L = min(li, lj);
+            u32 d = L;
+            if (h < L) {
+                const u64 x = ld32(i + h) ^ ld32(j + h);
+                if (!x) {
+                    if (h + 32u < L) return 0;
+                } else {
+                    d = h + ((u32)(__ffsll((long long)x) - 1) >> 1);
+                }
+            }
+            if (d < L) {
+                lcp = d;
+                const u32 sh = 2u * ((i + d) & 31u), sj = 2u * ((j + d) & 31u);
+                const u32 ci = (u32)(P2[(i + d) >> 5] >> sh) & 3u, cj = (u32)(P2[(j + d) >> 5] >> sj) & 3u;
+                return ci < cj ? 1 : 2;
+            }
+            lcp = L;
+            if (li != lj) return li < lj ? 1 : 2;
+            return i > nA ? 1 : 2;  // equal distance: the end (pad) is below the separator
+        }
+        const u64 a = ld8(T, i + h), b = ld8(T, j + h);
+        if (a == b) return 0;
+        const u32 bit = (u32)(__ffsll((long long)(a ^ b)) - 1) & ~7u;
+        lcp = h + (bit >> 3);
+        return ((a >> bit) & 0xFFu) < ((b >> bit) & 0xFFu) ? 1 : 2;
+    }
+};
 
 // suffix i < suffix j (i != j); `work` counts 8-character steps.  Distinct
 // suffixes differ before the shorter reaches the zero padding.
@@ -376,6 +431,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
     u32 *CNT = reinterpret_cast<u32 *>(smem + OFF_S0);  // NB u16 counters, two per word
     u16 *BIGS = reinterpret_cast<u16 *>(smem + OFF_S0 + 2 * NB);
     u16 *QW = reinterpret_cast<u16 *>(smem + OFF_Q);
+    u64 *P2 = reinterpret_cast<u64 *>(smem + OFF_P2);
     Misc &ms = *reinterpret_cast<Misc *>(smem + OFF_MISC);
     const u32 tid = threadIdx.x;
     if (CLK && tid == 0) {
@@ -427,6 +483,21 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
         // ---- 2. sample buckets: sample q <-> position 3(q/2) + 1 + (q&1)
         const u32 limit = (n % 3u == 1u) ? n + 1 : n;
         const u32 qmax = 2u * ((limit + 2u) / 3u);
+        const Txt tx{T, P2, nA, n, keep_n == 0};
+        if (tx.packed) {  // 2-bit residues, 32 per word (specials: any value, never compared)
+            const u32 nw = (n + 31u) / 32u + 1u;
+            for (u32 w = tid; w < nw; w += THREADS) {
+                const u32 *src = reinterpret_cast<const u32 *>(T + 32u * w);
+                u64 acc = 0;
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const u32 v = ((src[k] | 0x80808080u) - 0x02020202u) & 0x03030303u;
+                    const u32 b = (v | (v >> 6) | (v >> 12) | (v >> 18)) & 0xFFu;
+                    acc |= (u64)b << (8 * k);
+                }
+                P2[w] = acc;
+            }
+        }
         for (u32 q = tid; q < qmax; q += THREADS) {
             const u32 s = 3u * (q >> 1) + 1u + (q & 1u);
             if (s < limit) {
@@ -482,11 +553,11 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                                                // (A/T-rich) prefixes spread over all lanes
             u16 *Q = QW + (tid >> 5) * QCAP;
             const u32 lane = lane_id(), lt = lanemask_lt();
-            for (int round = 0; round < BPT / 8; round++) {
+            for (int round = 0; round < BPT / QROUND; round++) {
                 u32 qn = 0;
-#pragma unroll
-                for (int kk = 0; kk < 8; kk++) {
-                    const u32 b = tid + (u32)(round * 8 + kk) * THREADS;
+#pragma unroll 4
+                for (int kk = 0; kk < QROUND; kk++) {
+                    const u32 b = tid + (u32)(round * QROUND + kk) * THREADS;
                     const u32 st = b ? C16[b - 1] : 0u, sz = C16[b] - st;
                     if (sz > (u32)SMALL) {
                         const u32 at = atomicAdd(&ms.nbig, 1u);
@@ -515,16 +586,16 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                     bool done = false;
                     if (live) {
                         const u32 y = SS[j - 1];
-                        const u64 wa = ld8(T, x + h), wb = ld8(T, y + h);
-                        if (wa == wb) {
-                            h += 8;
+                        u32 l_;
+                        const int c = tx.cmp(x, y, h, l_);
+                        if (c == 0) {
+                            h += tx.step();
                             if (++work > WORK_MAX) {
                                 ms.fail = 1;
                                 live = false;
                             }
                         } else {
-                            const int sh = (__ffsll((long long)(wa ^ wb)) - 1) & ~7;
-                            const bool less = ((wa >> sh) & 0xFFu) < ((wb >> sh) & 0xFFu);
+                            const bool less = c == 1;
                             h = 0;
                             if (less) {
                                 SS[j] = (u16)y;
@@ -534,7 +605,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                                 SS[j] = (u16)x;
                                 if (++i < end) {
                                     x = SS[i];
-                                    j = i;
+                                            j = i;
                                 } else {
                                     done = true;
                                 }
@@ -736,11 +807,11 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             }
             while (__any_sync(0xffffffffu, live)) {
                 if (live) {
-                    const u64 x = (r0 + q == 0) ? 1ull : (ld8(T, prev + h) ^ ld8(T, cur + h));
-                    if (!x) {
-                        h += 8;
+                    u32 l = 0;
+                    const int c = (r0 + q == 0) ? 1 : tx.cmp(prev, cur, h, l);
+                    if (c == 0) {
+                        h += tx.step();
                     } else {
-                        const u32 l = (r0 + q == 0) ? 0u : h + ((u32)(__ffsll((long long)x) - 1) >> 3);
                         const bool cross = prev != nA && cur != nA && ((prev < nA) != (cur < nA));
                         if (cross) mx = max(mx, l);
                         LC[r0 + q] = (u8)min(l, 255u);
@@ -931,6 +1002,12 @@ extern "C" size_t saix_overlap_batch_workspace_bytes(const int64_t *offs_host, i
 
 extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host, int64_t npairs, int keep_n,
                                   int64_t *out, int64_t *bad, void *ws, size_t ws_bytes, void *stream) {
+    return saix_overlap_batch_dev(seqs, offs_host, nullptr, npairs, keep_n, out, bad, ws, ws_bytes, stream);
+}
+
+extern "C" int saix_overlap_batch_dev(const uint8_t *seqs, const int64_t *offs_host, const int64_t *offs_dev,
+                                      int64_t npairs, int keep_n, int64_t *out, int64_t *bad, void *ws,
+                                      size_t ws_bytes, void *stream) {
     if (npairs < 0 || (npairs > 0 && (!offs_host || !out)) || !bad) {
         set_error("saix_overlap_batch: invalid arguments");
         return SAIX_EINVAL;
@@ -950,7 +1027,13 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
     pd::k_pd_init<<<1, 1, 0, st>>>(out, bad, w.ctr);  // out[0..2] zero, bad = INT64_MAX
     SAIX_LAUNCHED();
     if (P == 0) return SAIX_OK;
-    SAIX_CUDA(cudaMemcpyAsync(w.offs, offs_host, (size_t)(2 * P + 1) * 8, cudaMemcpyHostToDevice, st));
+    // offsets: the caller's device copy, or uploaded here (a pageable H2D copy
+    // queues behind any bulk H2D already in flight on the copy engine)
+    const i64 *doffs = offs_dev;
+    if (!doffs) {
+        SAIX_CUDA(cudaMemcpyAsync(w.offs, offs_host, (size_t)(2 * P + 1) * 8, cudaMemcpyHostToDevice, st));
+        doffs = w.offs;
+    }
     {
         static DeviceFlags attr;
         if (attr.need()) {
@@ -966,10 +1049,10 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
         if (clocks_on()) {
             SAIX_CUDA(cudaMemsetAsync(w.clk, 0, sizeof(unsigned long long) * (pd::NPHASE + 2), st));
             pd::k_pair_dc3<true><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
-                seqs, w.offs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk);
+                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk);
         } else {
             pd::k_pair_dc3<false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
-                seqs, w.offs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr);
+                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr);
         }
     }
     SAIX_LAUNCHED();

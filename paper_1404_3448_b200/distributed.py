@@ -63,12 +63,9 @@ class ShardedOverlapBatch:
         import torch
         from .overlap import INT64_MAX
         b = self.batch
-        bad = b.bad[: len(b.waves)].cpu().numpy()
         key = INT64_MAX
-        hit = np.flatnonzero(bad != INT64_MAX)
-        if hit.shape[0]:
-            w = int(hit[0])
-            pos = int(bad[w]) + int(b.offs[2 * b.waves[w][0]])       # offset in this rank's seqs
+        pos = b.first_bad()                                           # offset in this rank's seqs
+        if pos is not None:
             si = int(np.searchsorted(b.offs, pos, side="right") - 1)  # sequence 2p or 2p+1 of the shard
             key = ((2 * self.lo + si) << 40) | (pos - int(b.offs[si]))
         if self.dist is not None and self.world > 1:

@@ -213,10 +213,15 @@ class OverlapBatch:
     seqs[offs[2p+1]:offs[2p+2]]).  Every pair of up to 20,480 GSA residues
     runs its whole pipeline in one CTA's shared memory; one call covers all
     pairs unless ``wave_residues`` (or SAIX_WAVE_RESIDUES) splits the batch
-    into calls of at most that many residues."""
+    into calls of at most that many residues.
+
+    ``run_device`` works on the device-resident copy of ``seqs``;
+    ``run_from_host`` streams pinned host ASCII in chunks on a copy stream,
+    each chunk's pairs starting as soon as its bytes have landed (the H2D of
+    chunk k+1 overlaps the pairs of chunk k)."""
 
     def __init__(self, seqs: np.ndarray, offs: np.ndarray, policy: NPolicy = NPolicy.REJECT,
-                 wave_residues: int | None = None):
+                 wave_residues: int | None = None, chunks: int = 8):
         if wave_residues is None:
             import os
             wave_residues = int(os.environ.get("SAIX_WAVE_RESIDUES", 1 << 62))
@@ -227,39 +232,86 @@ class OverlapBatch:
         self.P = (len(self.offs) - 1) // 2
         self.keep_n = int(policy is NPolicy.KEEP)
         self.policy = policy
-        self.waves = []
-        p = 0
-        while p < self.P:
-            q = p + 1
-            while q < self.P and self.offs[2 * (q + 1)] - self.offs[2 * p] <= wave_residues:
-                q += 1
-            self.waves.append((p, q))
-            p = q
+        self.waves = self._split(lambda p, q: self.offs[2 * (q + 1)] - self.offs[2 * p] <= wave_residues)
+        per = max(1, -(-self.P // max(1, chunks)))
+        self.chunks = [(p, min(p + per, self.P)) for p in range(0, self.P, per)]
         self.seqs_dev = _lib.to_device(np.ascontiguousarray(seqs, dtype=np.uint8))
         self.out = t.zeros(max(3 * self.P, 3), dtype=t.int64, device=dev)
-        self.bad = t.zeros(max(len(self.waves), 1), dtype=t.int64, device=dev)
-        self.wave_offs = [np.ascontiguousarray(self.offs[2 * a: 2 * b + 1] - self.offs[2 * a]) for a, b in self.waves]
+        self.bad = t.zeros(max(len(self.waves), len(self.chunks), 1), dtype=t.int64, device=dev)
+        self._calls = {}
+        for kind, spans in (("waves", self.waves), ("chunks", self.chunks)):
+            calls = []
+            for a, b in spans:
+                o = np.ascontiguousarray(self.offs[2 * a: 2 * b + 1] - self.offs[2 * a])
+                calls.append((a, b, o, _lib.to_device(o)))   # host copy + resident device copy
+            self._calls[kind] = calls
         ws = max((L.saix_overlap_batch_workspace_bytes(o.ctypes.data, b - a)
-                  for o, (a, b) in zip(self.wave_offs, self.waves)), default=256)
+                  for calls in self._calls.values() for a, b, o, _d in calls), default=256)
         self.ws = _lib.workspace(ws)
         self.h2d_bytes = int(self.offs[-1])
+        self._last = "waves"
+        self._copy_stream = None
+
+    def _split(self, fits):
+        spans, p = [], 0
+        while p < self.P:
+            q = p + 1
+            while q < self.P and fits(p, q):
+                q += 1
+            spans.append((p, q))
+            p = q
+        return spans
+
+    def _call(self, k: int, a: int, b: int, o: np.ndarray, od, L, s) -> None:
+        rc = L.saix_overlap_batch_dev(_lib.ptr(self.seqs_dev) + int(self.offs[2 * a]), o.ctypes.data,
+                                      _lib.ptr(od), b - a, self.keep_n, _lib.ptr(self.out) + 24 * a,
+                                      _lib.ptr(self.bad) + 8 * k, _lib.ptr(self.ws), self.ws.numel(), s)
+        _lib.check(rc, "saix_overlap_batch")
 
     def run_device(self) -> None:
         """All waves on the device-resident ASCII (no host traffic)."""
         L = _lib.load()
         s = _lib.stream_ptr()
-        for w, ((a, b), o) in enumerate(zip(self.waves, self.wave_offs)):
-            rc = L.saix_overlap_batch(_lib.ptr(self.seqs_dev) + int(self.offs[2 * a]), o.ctypes.data, b - a,
-                                      self.keep_n, _lib.ptr(self.out) + 24 * a, _lib.ptr(self.bad) + 8 * w,
-                                      _lib.ptr(self.ws), self.ws.numel(), s)
-            _lib.check(rc, "saix_overlap_batch")
+        self._last = "waves"
+        for k, (a, b, o, od) in enumerate(self._calls["waves"]):
+            self._call(k, a, b, o, od, L, s)
+
+    def run_from_host(self, host_seqs) -> None:
+        """Copy pinned host ASCII (a uint8 torch tensor laid out like
+        ``seqs``) to the device chunk by chunk on a copy stream and run each
+        chunk's pairs as soon as its bytes are resident."""
+        t = _lib.torch()
+        L = _lib.load()
+        cur = t.cuda.current_stream()
+        if self._copy_stream is None:
+            self._copy_stream = t.cuda.Stream()
+        cs = self._copy_stream
+        cs.wait_stream(cur)  # the previous step's kernels are done with seqs_dev
+        events = []
+        with t.cuda.stream(cs):
+            for a, b, _o, _d in self._calls["chunks"]:
+                lo, hi = int(self.offs[2 * a]), int(self.offs[2 * b])
+                self.seqs_dev[lo:hi].copy_(host_seqs[lo:hi], non_blocking=True)
+                ev = t.cuda.Event()
+                ev.record(cs)
+                events.append(ev)
+        s = cur.cuda_stream
+        self._last = "chunks"
+        for k, ((a, b, o, od), ev) in enumerate(zip(self._calls["chunks"], events)):
+            cur.wait_event(ev)
+            self._call(k, a, b, o, od, L, s)
+
+    def first_bad(self) -> int | None:
+        """Smallest seqs offset of an illegal residue in the last run, or None."""
+        calls = self._calls[self._last]
+        bad = self.bad[: len(calls)].cpu().numpy()
+        hit = [int(v) + int(self.offs[2 * a]) for v, (a, _b, _o, _d) in zip(bad, calls) if v != INT64_MAX]
+        return min(hit) if hit else None
 
     def results(self) -> np.ndarray:
         """(P, 3) int64 host array; raises SequenceError like the reference."""
-        bad = self.bad.cpu().numpy()
-        hit = np.flatnonzero(bad[: len(self.waves)] != INT64_MAX)
-        if hit.shape[0]:
-            pos = int(bad[hit[0]])
+        pos = self.first_bad()
+        if pos is not None:
             raise SequenceError(f"illegal residue at packed offset {pos} "
                                 f"(policy={self.policy.value})")
         return self.out[: 3 * self.P].cpu().numpy().reshape(self.P, 3)
@@ -286,10 +338,8 @@ def longest_overlap_batch(pairs, policy: NPolicy = NPolicy.REJECT) -> list[Overl
     seqs, offs = pack_pairs(pairs)
     ob = OverlapBatch(seqs, offs, policy)
     ob.run_device()
-    bad = ob.bad.cpu().numpy()[: len(ob.waves)]
-    hit = np.flatnonzero(bad != INT64_MAX)
-    if hit.shape[0]:
-        pos = int(bad[hit[0]])
+    pos = ob.first_bad()
+    if pos is not None:
         pi = int(np.searchsorted(offs, pos, side="right") - 1)  # sequence index 2p or 2p+1
         seq = pairs[pi // 2][pi % 2]
         raise residue_error(seq, pos - int(offs[pi]), policy)

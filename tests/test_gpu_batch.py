@@ -211,4 +211,23 @@ def test_onchip_keep_n_and_reject():
     ob = sx.OverlapBatch(seqs, offs)                             # REJECT: the first N in the batch
     ob.run_device()
     first = int(np.flatnonzero(seqs == ord("N"))[0])
-    assert int(ob.bad[0].item()) == first
+    assert ob.first_bad() == first
+
+
+def test_run_from_host_chunks_match_device_run():
+    """Chunked H2D overlapped with the chunks' pairs (run_from_host) gives the
+    device-resident answers, and an illegal residue in a later chunk is
+    reported at its absolute packed offset."""
+    import torch
+    seqs, offs = c4_pairs(0, 700)
+    want = oracle.overlap_batch(seqs, offs, threads=8)
+    ob = sx.OverlapBatch(seqs, offs, chunks=5)
+    assert len(ob.chunks) == 5
+    host = torch.from_numpy(seqs.copy()).pin_memory()
+    ob.seqs_dev.zero_()
+    ob.run_from_host(host)
+    assert np.array_equal(ob.results(), want)
+    bad_at = int(offs[2 * 650 + 1]) + 17
+    host[bad_at] = ord("Q")
+    ob.run_from_host(host)
+    assert ob.first_bad() == bad_at
