@@ -116,6 +116,12 @@ SAIX_API int saix_dc3_merge(const void *text, int text_bytes, int64_t n,
  * the number of levels (at most max_levels are written to out[4*i..]). */
 SAIX_API int saix_dc3_trace(int64_t *out, int max_levels);
 
+/* Level-0 naming path of the last byte-text DC3 level 0 on this host thread:
+ * 0 triple naming (+ recursion), 1 generic 21-character window sort, 2 the
+ * DNA window sort (ranks 1..4: MSD record sort, csrc/wsort.cuh).  Test and
+ * A/B aid; the SA / ISA are the same on every path. */
+SAIX_API int saix_dc3_naming(void);
+
 /* Level-0 window naming (byte texts, sigma <= 7): samples named by their
  * 21-character windows, ties ordered by prefix doubling, no recursion below
  * level 0 (same SA / ISA).  on = 0 runs the reference recursion instead.

@@ -78,6 +78,7 @@ SIGNATURES = {
     "saix_lcp": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_lcp_sigma": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_dc3_trace": (_int, [_vp, _int]),
+    "saix_dc3_naming": (_int, []),
     "saix_psort_workspace_bytes": (_c.c_size_t, [_i64]),
     "saix_exclusive_scan_i64": (_int, [_vp, _i64, _vp, _vp, _c.c_size_t, _vp]),
     "saix_split_by_bit": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
@@ -269,6 +270,12 @@ def prof_collect() -> list[dict]:
     n = L.saix_prof_collect(buf, 256)
     return [{"name": buf[i].name.decode(), "launches": int(buf[i].launches),
              "ms": float(buf[i].total_ms), "bytes": float(buf[i].bytes)} for i in range(min(n, 256))]
+
+
+def dc3_naming() -> int:
+    """Level-0 naming path of the last DC3 level 0 on this thread (0 triples,
+    1 generic window sort, 2 DNA window sort)."""
+    return int(load().saix_dc3_naming())
 
 
 def dc3_trace() -> list[tuple[int, int, int, int]]:

@@ -26,6 +26,7 @@
 #include "onesweep.cuh"
 #include "pscatter.cuh"
 #include "scan.cuh"
+#include "wsort.cuh"
 
 namespace saix {
 
@@ -1262,6 +1263,9 @@ struct LevelRec {
     i64 n, sigma, m, names;
 };
 static thread_local std::vector<LevelRec> g_trace;
+// level-0 naming of the last DC3 on this thread: 0 triples (+ recursion),
+// 1 generic window sort, 2 DNA window sort (wsort.cuh)
+static thread_local int g_naming = 0;
 
 // Level-0 window naming switch: SAIX_WINDOW_NAMING=0 or saix_dc3_set_window_naming(0)
 // turns it off (the reference recursion runs; A/B measurement and the
@@ -2429,8 +2433,8 @@ __device__ __forceinline__ u64 bs_get(const WindowSrc &w, i64 s, u64 &k, u32 &v)
     return wn_dense_loop(w, y);
 }
 
-static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const SampleLayout &L, u32 *SAc, u32 *ISAc,
-                       u32 *d_scal, int depth, bool &handled) {
+static int window_rank_generic(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const SampleLayout &L, u32 *SAc,
+                               u32 *ISAc, u32 *d_scal, int depth, bool &handled) {
     Arena &ar = *c.ar;
     cudaStream_t st = c.st;
     handled = false;
@@ -2519,6 +2523,7 @@ static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const Sample
         handled = true;
     }
     if (handled) {
+        if (depth == 0) g_naming = 1;
         if ((size_t)depth >= g_trace.size()) g_trace.resize((size_t)depth + 1);
         g_trace[(size_t)depth] = LevelRec{L.n, (i64)sigma, m, (i64)D};
         g_trace.resize((size_t)depth + 1);
@@ -2529,6 +2534,128 @@ static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const Sample
     }
     ar.reset(mark);
     return SAIX_OK;
+}
+
+// Level-0 window naming of DNA texts by the MSD record sort (wsort.cuh).
+// tried = false: preconditions not met (caller runs the generic window
+// sort); tried && !handled: too many ties -> the triple-naming recursion.
+static bool ws_dna_on() {
+    static int v = [] {
+        const char *e = getenv("SAIX_WS_DNA");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    return v != 0;
+}
+static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout &L, u32 *SAc, u32 *ISAc, int depth,
+                           bool &handled, bool &tried) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    handled = tried = false;
+    const i64 m = L.m;
+    PsPlan pu = PsPlan::of(m, 4);
+    i64 stage_items = m;
+    if (pu.stage1_items() > stage_items) stage_items = pu.stage1_items();
+    if (pu.stage2_items() > stage_items) stage_items = pu.stage2_items();
+    const u32 cap = (u32)(m / 32 + 64);
+    const size_t need = (size_t)stage_items * 16 + (SAc ? 0 : (size_t)m * 4) + (size_t)cap * 24 +
+                        (size_t)WS_FINE * 12 + ((size_t)16 << 20);
+    const size_t mark = ar.mark();
+    if (ar.cap - mark < need) return SAIX_OK;
+    u64 *SA_ = ar.alloc<u64>(stage_items), *SB = ar.alloc<u64>(stage_items);
+    u32 *sorted = SAc ? SAc : ar.alloc<u32>(m);
+    u32 *hist = ar.alloc<u32>(WS_FINE), *off = ar.alloc<u32>(WS_FINE + 1), *curF = ar.alloc<u32>(WS_FINE);
+    u32 *curC = ar.alloc<u32>(WS_COARSE), *tstart = ar.alloc<u32>(WS_COARSE + 1);
+    u32 *tmp = ar.alloc<u32>(scan_tmp_words(WS_FINE));
+    u32 *scal = ar.alloc<u32>(16);  // resolve_ties layout; [6] P1 overflow, [7] largest bucket
+    u32 *rsA = ar.alloc<u32>(cap), *rlA = ar.alloc<u32>(cap), *rsB = ar.alloc<u32>(cap), *rlB = ar.alloc<u32>(cap);
+    u32 *mid = ar.alloc<u32>(cap), *big = ar.alloc<u32>(cap);
+    pu.set_cursors(ar.alloc<u32>(pu.cursor_words()));
+    SAIX_ARENA_OK(ar);
+    const i64 ntiles = ceil_div(N + 1, (i64)WS_TP);
+    static DeviceFlags attr;
+    if (attr.need()) {
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_count, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_FINE * 2));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_part1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_P2_SMEM));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_part2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_P2_SMEM));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 << 10));
+        attr.set();
+    }
+    SAIX_CUDA(cudaMemsetAsync(hist, 0, (size_t)WS_FINE * 4, st));
+    SAIX_CUDA(cudaMemsetAsync(scal, 0, 16 * 4, st));
+    {
+        Prof prof_("dc3.ws_count", (double)N, st);
+        k_ws_count<<<kNumSMs, 1024, WS_FINE * 2, st>>>(text, L, ntiles, hist, scal + 6);
+        SAIX_LAUNCHED();
+    }
+    SAIX_TRY(scan_transform(WsHistIn{hist}, WsOffOut{off, curF, curC, scal + 7}, WS_FINE, tmp, off + WS_FINE, st,
+                            "dc3.ws_scan", 16.0 * WS_FINE));
+    k_ws_tiles<<<1, WS_COARSE, 0, st>>>(off, m, tstart);
+    SAIX_LAUNCHED();
+    u32 h[2];
+    SAIX_CUDA(cudaMemcpyAsync(h, scal + 6, 8, cudaMemcpyDeviceToHost, st));
+    SAIX_CUDA(cudaStreamSynchronize(st));
+    if (h[0] || h[1] > (u32)WS_CAP_MAX) {  // skewed text: the generic window sort
+        ar.reset(mark);
+        return SAIX_OK;
+    }
+    tried = true;
+    const int capA = (int)(h[1] <= (u32)WS_CAP_MIN ? WS_CAP_MIN : ceil_div((i64)h[1], (i64)256) * 256);
+    {
+        Prof prof_("dc3.ws_part1", (double)N + 8.0 * m, st);
+        k_ws_part1<<<(unsigned)ntiles, WS_PT, WS_P2_SMEM, st>>>(text, L, curC, SA_);
+        SAIX_LAUNCHED();
+    }
+    {
+        Prof prof_("dc3.ws_part2", 16.0 * m, st);
+        k_ws_part2<<<(unsigned)(ceil_div(m, (i64)WS_PTILE) + WS_COARSE), WS_PT, WS_P2_SMEM, st>>>(SA_, off, tstart, m,
+                                                                                                  curF, SB);
+        SAIX_LAUNCHED();
+    }
+    SAIX_CUDA(cudaMemsetAsync(pu.a.cursor, 0, (size_t)pu.cursor_words() * 4, st));
+    {
+        Prof prof_("dc3.ws_sort", 8.0 * m + 4.0 * m + 8.0 * m, st);
+        k_ws_sort<<<WS_FINE, WS_ST, ws_sort_smem(capA, pu), st>>>(SB, off, m, L.m1, capA, sorted, pu,
+                                                                 reinterpret_cast<uint2 *>(SA_), rsA, rlA, cap, scal);
+        SAIX_LAUNCHED();
+    }
+    u32 h6[6];
+    SAIX_CUDA(cudaMemcpyAsync(h6, scal, 24, cudaMemcpyDeviceToHost, st));
+    SAIX_CUDA(cudaStreamSynchronize(st));
+    const u32 D = h6[5];
+    const bool tie_ok = (i64)D < m && (i64)(m - D) <= m / 32 && !h6[4];
+    if ((i64)D == m || tie_ok) {
+        SAIX_TRY(ps_finish(reinterpret_cast<uint2 *>(SA_), reinterpret_cast<uint2 *>(SB), pu, U32Apply{ISAc}, st,
+                           "dc3.unique_isa", 28.0 * m));
+        if (tie_ok) {
+            {
+                Prof prof_("dc3.tie_resolve", 12.0 * (m - D), st);
+                k_tie_groups<<<grid_for(h6[2], 128), 128, 0, st>>>(rsA, rlA, scal + 2, sorted, ISAc);
+            }
+            SAIX_LAUNCHED();
+            SAIX_TRY(tie_rounds(c, m, m - D, sorted, SA_, ISAc, rsA, rlA, rsB, rlB, mid, big, scal, h6[2]));
+        }
+        handled = true;
+        if (depth == 0) g_naming = 2;
+        if ((size_t)depth >= g_trace.size()) g_trace.resize((size_t)depth + 1);
+        g_trace[(size_t)depth] = LevelRec{L.n, 4, m, (i64)D};
+        g_trace.resize((size_t)depth + 1);
+        if (trace_on())
+            fprintf(stderr, "[saix dc3] depth %d: N=%lld text=u8 sigma<=4 m=%lld names=%u naming=window21/msd%s\n",
+                    depth, (long long)L.n, (long long)m, D, (i64)D == m ? " (unique)" : " (ties resolved)");
+    }
+    ar.reset(mark);
+    return SAIX_OK;
+}
+
+static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const SampleLayout &L, u32 *SAc, u32 *ISAc,
+                       u32 *d_scal, int depth, bool &handled) {
+    if (sigma <= 4 && N + 1 < (i64)WS_POS_MASK && L.m >= ((i64)1 << 20) && ((uintptr_t)text & 15) == 0 &&
+        ws_dna_on()) {
+        bool tried = false;
+        SAIX_TRY(window_rank_dna(c, text, N, L, SAc, ISAc, depth, handled, tried));
+        if (tried) return SAIX_OK;
+    }
+    return window_rank_generic(c, text, N, sigma, L, SAc, ISAc, d_scal, depth, handled);
 }
 
 static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA, u32 *ISA, u32 *Phi,
@@ -2549,6 +2676,7 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     u32 *SAc = gather ? ar.alloc<u32>(m) : nullptr;
     SAIX_ARENA_OK(ar);
     bool windowed = false;
+    if (depth == 0) g_naming = 0;
     if (sigma <= 7 && m >= 4096 && window_naming_on())
         SAIX_TRY(window_rank(c, text, N, sigma, L, SAc, ISAc, d_scal, depth, windowed));
     if (!windowed) SAIX_TRY(sort_samples<u8>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth, false, nullptr));
@@ -2823,6 +2951,8 @@ extern "C" int saix_dc3_merge(const void *text, int text_bytes, int64_t n, const
     }
     return rc;
 }
+
+extern "C" int saix_dc3_naming(void) { return g_naming; }
 
 extern "C" int saix_dc3_trace(int64_t *out, int max_levels) {
     int n = (int)g_trace.size();

@@ -1,0 +1,411 @@
+// wsort.cuh -- level-0 window naming for DNA texts (ranks 1..4, N < 2^29):
+// an MSD sort of the samples' 21-character windows in streaming passes.
+//
+// The generic window sort (bsort.cuh over WindowSrc) builds 63-bit keys
+// twice from unaligned global words, moves 16 B staging records through two
+// HBM round trips and re-reads the sorted output to order 2^24 tiny buckets.
+// Here the text is staged per tile in shared memory as 2-bit packed words
+// (a 21-character window is three funnel shifts) and every sample becomes
+// ONE 8-byte record that carries the rest of its key:
+//
+//   rec = chars 5..21 (34 bits) | flag (1) | 2^29-1-pos (29)
+//
+// flag = 1 for a full window, 0 for a window that reaches past the end (at
+// most 20 of them).  Sorting records as u64 orders equal 0-filled windows
+// "end window first, then the shorter one", which is the suffix order, so
+// end windows stay unique names (the property DC3's padding triples give).
+//
+//   P1 k_ws_count   text tiles -> 2^16 fine bins (first 8 chars) in 16-bit
+//                   shared-memory counters, one flush per CTA
+//   (scan)          fine offsets: bucket f occupies [off[f], off[f+1]) in
+//                   both staging arrays and in the sorted order
+//   P2a k_ws_part1  text tiles -> records bucketed by the first 4 chars
+//                   (256 coarse regions; runs of ~32 records per tile)
+//   P2b k_ws_part2  each coarse region -> 256 fine buckets (chars 5..8)
+//   P3  k_ws_sort   one CTA per fine bucket: counting split by chars 9..13
+//                   in shared memory, per-thread insertion sort of the
+//                   ~3-record sub-buckets, then in the same pass: the sorted
+//                   sample indices (= SAc), distinct-name count, tied runs
+//                   for resolve_ties, and ISAc[s] = rank through pass A of
+//                   the bucketed scatter (pscatter.cuh).
+// Reference: suffix_index.py:221-253 (_name_triples), 256-271 (_sort_samples).
+#pragma once
+
+#include "pscatter.cuh"
+#include "scan.cuh"
+
+namespace saix {
+
+constexpr int WS_TP = 12288;              // text positions per tile (multiple of 48)
+constexpr int WS_TS = WS_TP / 3 * 2;      // samples per tile
+constexpr int WS_WORDS = WS_TP / 16 + 2;  // packed words per tile (+ 32 halo characters)
+constexpr int WS_FINE = 1 << 16;          // fine buckets: 8 leading characters
+constexpr int WS_COARSE = 256;            // coarse regions: 4 leading characters
+constexpr int WS_POS_BITS = 29;
+constexpr u64 WS_POS_MASK = (1ull << WS_POS_BITS) - 1;
+constexpr int WS_SUBS = 1024;             // P3 split: characters 9..13
+constexpr int WS_PT = 512;                // P2 threads
+constexpr int WS_PI = 16;                 // P2 items per thread
+constexpr int WS_PTILE = WS_PT * WS_PI;   // 8192 records
+constexpr int WS_ST = 256;                // P3 threads
+constexpr int WS_SI = 16;                 // P3 emit items per thread
+constexpr int WS_CAP_MIN = WS_ST * WS_SI; // 4096
+constexpr int WS_CAP_MAX = 12288;         // largest fine bucket P3 takes
+constexpr int WS_SMALL_SUB = 32;          // insertion-sort limit per sub-bucket
+constexpr int WS_MAX_RUN = 4096;          // longest tied run handed to resolve_ties
+
+// 16 ranks (bytes 1..4) -> one 32-bit word of 2-bit digits, first at the top
+__device__ __forceinline__ u32 ws_pack4(u32 x) {
+    const u32 r = __byte_perm(x - 0x01010101u, 0, 0x0123) & 0x03030303u;
+    const u32 pp = r | (r >> 6);
+    return ((pp >> 12) & 0xF0u) | (pp & 0xFu);
+}
+__device__ __forceinline__ u32 ws_pack16(uint4 v) {
+    return (ws_pack4(v.x) << 24) | (ws_pack4(v.y) << 16) | (ws_pack4(v.z) << 8) | ws_pack4(v.w);
+}
+
+// stage positions [p0, p0 + WS_TP + 32) as packed words; past the end reads
+// as digit 0 (the flag tells end windows apart)
+__device__ __forceinline__ void ws_stage(const u8 *__restrict__ t, i64 N, i64 p0, u32 *__restrict__ W,
+                                         int nthreads) {
+    for (int w = threadIdx.x; w < WS_WORDS; w += nthreads) {
+        const i64 q = p0 + 16 * (i64)w;
+        uint4 v;
+        if (q + 16 <= N) {
+            v = __ldg(reinterpret_cast<const uint4 *>(t + q));
+        } else {
+            u32 x[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                u32 word = 0;
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const i64 at = q + 4 * k + b;
+                    word |= (at < N ? (u32)t[at] : 1u) << (8 * b);
+                }
+                x[k] = word;
+            }
+            v = make_uint4(x[0], x[1], x[2], x[3]);
+        }
+        W[w] = ws_pack16(v);
+    }
+}
+
+// 21-character window at tile offset o: 42 bits, first character on top
+__device__ __forceinline__ u64 ws_key(const u32 *__restrict__ W, int o) {
+    const int w = o >> 4, sh = 2 * (o & 15);
+    const u32 w0 = W[w], w1 = W[w + 1], w2 = W[w + 2];
+    const u32 a = __funnelshift_l(w1, w0, sh);
+    const u32 b = __funnelshift_l(w2, w1, sh);
+    return ((u64)a << 10) | (b >> 22);
+}
+
+// local sample q of a tile: position, validity
+__device__ __forceinline__ int ws_off(int q) { return 3 * (q >> 1) + 1 + (q & 1); }
+__device__ __forceinline__ bool ws_valid(i64 p, const SampleLayout &L) { return p < L.n || (p == L.n && L.pad); }
+__device__ __forceinline__ u64 ws_rec(u64 key, i64 p, i64 N) {
+    const u64 flag = (p + 21 <= N) ? 1ull : 0ull;
+    return ((key & ((1ull << 34) - 1)) << 30) | (flag << 29) | (WS_POS_MASK - (u64)p);
+}
+__device__ __forceinline__ i64 ws_pos(u64 rec) { return (i64)(WS_POS_MASK - (rec & WS_POS_MASK)); }
+// equal names: same 21 characters and both full windows
+__device__ __forceinline__ bool ws_same(u64 a, u64 b) { return ((a ^ b) >> 29) == 0 && ((a >> 29) & 1); }
+
+// ---------------------------------------------------------------- P1
+__global__ void __launch_bounds__(1024, 1)
+k_ws_count(const u8 *__restrict__ t, SampleLayout L, i64 ntiles, u32 *__restrict__ hist, u32 *__restrict__ overflow) {
+    extern __shared__ __align__(16) u32 ws_h16[];  // WS_FINE 16-bit counters, two per word
+    __shared__ u32 W[WS_WORDS];
+    for (int i = threadIdx.x; i < WS_FINE / 2; i += 1024) ws_h16[i] = 0;
+    bool ovf = false;
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const i64 p0 = tile * WS_TP;
+        __syncthreads();
+        ws_stage(t, L.n, p0, W, 1024);
+        __syncthreads();
+#pragma unroll 4
+        for (int q = threadIdx.x; q < WS_TS; q += 1024) {
+            const int o = ws_off(q);
+            if (!ws_valid(p0 + o, L)) continue;
+            const u32 f = (u32)(ws_key(W, o) >> 26);
+            const int sh = 16 * (f & 1);
+            const u32 old = atomicAdd(&ws_h16[f >> 1], 1u << sh);
+            ovf |= ((old >> sh) & 0xFFFFu) == 0xFFFFu;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < WS_FINE / 2; i += 1024) {
+        const u32 v = ws_h16[i];
+        if (v & 0xFFFFu) atomicAdd(&hist[2 * i], v & 0xFFFFu);
+        if (v >> 16) atomicAdd(&hist[2 * i + 1], v >> 16);
+    }
+    if (ovf) atomicMax(overflow, 1u);
+}
+
+// fine offsets (exclusive), staging cursors and the largest bucket
+struct WsHistIn {
+    const u32 *hist;
+    __device__ u32 operator()(i64 i) const { return hist[i]; }
+};
+struct WsOffOut {
+    u32 *off, *cur_fine, *cur_coarse, *maxb;
+    __device__ void operator()(i64 i, u32 excl, u32 v) const {
+        off[i] = excl;
+        cur_fine[i] = excl;
+        if ((i & (WS_COARSE - 1)) == 0) cur_coarse[i / WS_COARSE] = excl;
+        const u32 mx = __reduce_max_sync(__activemask(), v);
+        if (lane_id() == __ffs(__activemask()) - 1 && mx) atomicMax(maxb, mx);
+    }
+};
+
+// P2b tile table: coarse region c owns tiles [tstart[c], tstart[c+1])
+__global__ void __launch_bounds__(WS_COARSE) k_ws_tiles(const u32 *__restrict__ off, i64 m, u32 *__restrict__ tstart) {
+    __shared__ u32 sh_warp[WS_COARSE / 32 + 1];
+    const int c = threadIdx.x;
+    const i64 lo = off[c * WS_COARSE];
+    const i64 hi = c + 1 < WS_COARSE ? (i64)off[(c + 1) * WS_COARSE] : m;
+    const u32 nt = (u32)ceil_div(hi - lo, (i64)WS_PTILE);
+    u32 excl;
+    const u32 tot = block_exclusive_scan<WS_COARSE>(nt, excl, sh_warp);
+    tstart[c] = excl;
+    if (c == 0) tstart[WS_COARSE] = tot;
+}
+
+// Block-level bucketed write of WS_PT*WS_PI records into runs reserved on
+// absolute cursors: item r goes to bucket bk[r] (< 256), cursor cur[bk].
+__device__ __forceinline__ void ws_block_emit(const u64 (&rec)[WS_PI], const u8 (&bk)[WS_PI], const bool (&ok)[WS_PI],
+                                              u32 *__restrict__ cur, u64 *__restrict__ out, u64 *__restrict__ sh_rec,
+                                              u8 *__restrict__ sh_bk, u32 *__restrict__ sh_cnt, u32 *__restrict__ sh_start,
+                                              u32 *__restrict__ sh_base) {
+    __shared__ u32 sh_warp[WS_PT / 32 + 1];
+    if (threadIdx.x < 256) sh_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    u32 slot[WS_PI];
+#pragma unroll
+    for (int r = 0; r < WS_PI; r++)
+        if (ok[r]) slot[r] = atomicAdd(&sh_cnt[bk[r]], 1u);
+    __syncthreads();
+    const u32 c = threadIdx.x < 256 ? sh_cnt[threadIdx.x] : 0u;
+    u32 excl;
+    const u32 tot = block_exclusive_scan<WS_PT>(c, excl, sh_warp);
+    if (threadIdx.x < 256) {
+        sh_start[threadIdx.x] = excl;
+        sh_base[threadIdx.x] = c ? atomicAdd(&cur[threadIdx.x], c) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < WS_PI; r++)
+        if (ok[r]) {
+            const u32 at = sh_start[bk[r]] + slot[r];
+            sh_rec[at] = rec[r];
+            sh_bk[at] = bk[r];
+        }
+    __syncthreads();
+    for (u32 x = threadIdx.x; x < tot; x += WS_PT) {
+        const u32 b = sh_bk[x];
+        __stcs(out + sh_base[b] + (x - sh_start[b]), sh_rec[x]);
+    }
+}
+constexpr size_t WS_P2_SMEM = (size_t)WS_PTILE * 9 + 3 * 256 * 4;
+
+// ---------------------------------------------------------------- P2a
+__global__ void __launch_bounds__(WS_PT, 2)
+k_ws_part1(const u8 *__restrict__ t, SampleLayout L, u32 *__restrict__ cur_coarse, u64 *__restrict__ stageA) {
+    extern __shared__ __align__(16) unsigned char ws_smem[];
+    u64 *sh_rec = reinterpret_cast<u64 *>(ws_smem);
+    u8 *sh_bk = ws_smem + (size_t)WS_PTILE * 8;
+    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_bk + WS_PTILE), *sh_start = sh_cnt + 256, *sh_base = sh_start + 256;
+    __shared__ u32 W[WS_WORDS];
+    const i64 p0 = (i64)blockIdx.x * WS_TP;
+    ws_stage(t, L.n, p0, W, WS_PT);
+    __syncthreads();
+    u64 rec[WS_PI];
+    u8 bk[WS_PI];
+    bool ok[WS_PI];
+#pragma unroll
+    for (int r = 0; r < WS_PI; r++) {
+        const int o = ws_off(r * WS_PT + threadIdx.x);
+        const i64 p = p0 + o;
+        ok[r] = ws_valid(p, L);
+        const u64 key = ws_key(W, o);
+        rec[r] = ws_rec(key, p, L.n);
+        bk[r] = (u8)(key >> 34);
+    }
+    ws_block_emit(rec, bk, ok, cur_coarse, stageA, sh_rec, sh_bk, sh_cnt, sh_start, sh_base);
+}
+
+// ---------------------------------------------------------------- P2b
+__global__ void __launch_bounds__(WS_PT, 2)
+k_ws_part2(const u64 *__restrict__ stageA, const u32 *__restrict__ off, const u32 *__restrict__ tstart, i64 m,
+           u32 *__restrict__ cur_fine, u64 *__restrict__ stageB) {
+    extern __shared__ __align__(16) unsigned char ws_smem[];
+    u64 *sh_rec = reinterpret_cast<u64 *>(ws_smem);
+    u8 *sh_bk = ws_smem + (size_t)WS_PTILE * 8;
+    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_bk + WS_PTILE), *sh_start = sh_cnt + 256, *sh_base = sh_start + 256;
+    const u32 b = blockIdx.x;
+    if (b >= tstart[WS_COARSE]) return;
+    int c = 0;  // largest region with tstart[c] <= b
+#pragma unroll
+    for (int s = 128; s; s >>= 1)
+        if (tstart[c + s] <= b) c += s;
+    const i64 lo = off[c * WS_COARSE] + (i64)(b - tstart[c]) * WS_PTILE;
+    const i64 hi_r = c + 1 < WS_COARSE ? (i64)off[(c + 1) * WS_COARSE] : m;
+    const i64 hi = lo + WS_PTILE < hi_r ? lo + WS_PTILE : hi_r;
+    u64 rec[WS_PI];
+    u8 bk[WS_PI];
+    bool ok[WS_PI];
+#pragma unroll
+    for (int r = 0; r < WS_PI; r++) {
+        const i64 x = lo + r * WS_PT + threadIdx.x;
+        ok[r] = x < hi;
+        rec[r] = ok[r] ? __ldcs(stageA + x) : 0ull;
+        bk[r] = (u8)(rec[r] >> 56);
+    }
+    ws_block_emit(rec, bk, ok, cur_fine + c * WS_COARSE, stageB, sh_rec, sh_bk, sh_cnt, sh_start, sh_base);
+}
+
+// ---------------------------------------------------------------- P3
+// scal (resolve_ties layout): [2] tied runs, [4] overflow, [5] distinct names
+__global__ void __launch_bounds__(WS_ST)
+k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i64 m1, int capA,
+          u32 *__restrict__ sorted, PsPlan plan, uint2 *__restrict__ stage1, u32 *__restrict__ rs,
+          u32 *__restrict__ rl, u32 cap_runs, u32 *__restrict__ scal) {
+    extern __shared__ __align__(16) unsigned char ws_smem[];
+    const u32 f = blockIdx.x;
+    const i64 lo = off[f];
+    const i64 hi = f + 1 < WS_FINE ? (i64)off[f + 1] : m;
+    const int L = (int)(hi - lo);
+    if (L <= 0) return;
+    u64 *A = reinterpret_cast<u64 *>(ws_smem);
+    u64 *B = A + capA;
+    u32 *scnt = reinterpret_cast<u32 *>(B + capA);
+    u32 *e_cnt = scnt + WS_SUBS, *e_base = e_cnt + plan.a.buckets;
+    __shared__ u32 sh_big[64];
+    __shared__ u32 sh_nbig, sh_d;
+    for (int i = threadIdx.x; i < WS_SUBS; i += WS_ST) scnt[i] = 0;
+    if (threadIdx.x == 0) {
+        sh_nbig = 0;
+        sh_d = 0;
+    }
+#pragma unroll 4
+    for (int x = threadIdx.x; x < L; x += WS_ST) A[x] = __ldcs(stageB + lo + x);
+    __syncthreads();
+    for (int x = threadIdx.x; x < L; x += WS_ST) atomicAdd(&scnt[(u32)(A[x] >> 46) & (WS_SUBS - 1)], 1u);
+    __syncthreads();
+    {  // exclusive scan of the sub-bucket counts, 4 per thread
+        __shared__ u32 sh_warp[WS_ST / 32 + 1];
+        u32 v[4], s = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            v[k] = scnt[threadIdx.x * 4 + k];
+            s += v[k];
+        }
+        u32 excl;
+        block_exclusive_scan<WS_ST>(s, excl, sh_warp);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            scnt[threadIdx.x * 4 + k] = excl;
+            excl += v[k];
+        }
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < L; x += WS_ST) {
+        const u64 r = A[x];
+        B[atomicAdd(&scnt[(u32)(r >> 46) & (WS_SUBS - 1)], 1u)] = r;
+    }
+    __syncthreads();
+    // scnt[k] = end of sub-bucket k; sort each (they share characters 1..13)
+    for (int k = threadIdx.x; k < WS_SUBS; k += WS_ST) {
+        const int s0 = k ? (int)scnt[k - 1] : 0, e = (int)scnt[k];
+        if (e - s0 <= 1) continue;
+        if (e - s0 > WS_SMALL_SUB) {
+            const u32 at = atomicAdd(&sh_nbig, 1u);
+            if (at < 64) sh_big[at] = (u32)k;
+            else atomicMax(&scal[4], 1u);
+            continue;
+        }
+        for (int i = s0 + 1; i < e; i++) {
+            const u64 v = B[i];
+            int j = i - 1;
+            while (j >= s0 && B[j] > v) {
+                B[j + 1] = B[j];
+                j--;
+            }
+            B[j + 1] = v;
+        }
+    }
+    __syncthreads();
+    const u32 nbig = sh_nbig < 64 ? sh_nbig : 64;
+    for (u32 q = 0; q < nbig; q++) {  // large sub-buckets: CTA bitonic in A
+        const int k = (int)sh_big[q];
+        const int s0 = k ? (int)scnt[k - 1] : 0, len = (int)scnt[k] - s0;
+        int p2 = 1;
+        while (p2 < len) p2 <<= 1;
+        if (p2 > capA) {
+            if (threadIdx.x == 0) atomicMax(&scal[4], 1u);
+            continue;
+        }
+        for (int x = threadIdx.x; x < p2; x += WS_ST) A[x] = x < len ? B[s0 + x] : ~0ull;
+        __syncthreads();
+        for (int size = 2; size <= p2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int tt = threadIdx.x; tt < (p2 >> 1); tt += WS_ST) {
+                    const int a = 2 * tt - (tt & (stride - 1)), bb = a + stride;
+                    const bool up = (a & size) == 0;
+                    const u64 x = A[a], y = A[bb];
+                    if ((x > y) == up) {
+                        A[a] = y;
+                        A[bb] = x;
+                    }
+                }
+                __syncthreads();
+            }
+        for (int x = threadIdx.x; x < len; x += WS_ST) B[s0 + x] = A[x];
+        __syncthreads();
+    }
+    // names, tied runs, sorted order and the ISA scatter's pass A
+    u32 d = 0;
+    for (int c0 = 0; c0 < L; c0 += WS_ST * WS_SI) {
+        uint2 it[WS_SI];
+        bool ok[WS_SI];
+#pragma unroll
+        for (int r = 0; r < WS_SI; r++) {
+            const int x = c0 + r * WS_ST + threadIdx.x;
+            ok[r] = x < L;
+            if (!ok[r]) continue;
+            const u64 v = B[x];
+            const bool head = x == 0 || !ws_same(B[x - 1], v);
+            d += head;
+            if (head && x + 1 < L && ws_same(v, B[x + 1])) {
+                int e = x + 2;
+                while (e < L && e - x <= WS_MAX_RUN && ws_same(v, B[e])) e++;
+                if (e - x > WS_MAX_RUN) {
+                    atomicMax(&scal[4], 1u);
+                } else {
+                    const u32 at = atomicAdd(&scal[2], 1u);
+                    if (at < cap_runs) {
+                        rs[at] = (u32)(lo + x);
+                        rl[at] = (u32)(e - x);
+                    } else {
+                        atomicMax(&scal[4], 1u);
+                    }
+                }
+            }
+            const i64 p = ws_pos(v);
+            const u32 s = (u32)(p % 3 == 1 ? p / 3 : m1 + p / 3);
+            __stcs(sorted + lo + x, s);
+            it[r] = make_uint2(s, (u32)(lo + x));
+        }
+        __syncthreads();  // A is the emit staging
+        ps_block_emit<uint2, WS_ST, WS_SI>(it, ok, plan.a, stage1, reinterpret_cast<uint2 *>(A), e_cnt, e_base);
+    }
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if (lane_id() == 0 && d) atomicAdd(&sh_d, d);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&scal[5], sh_d);
+}
+inline size_t ws_sort_smem(int capA, const PsPlan &plan) {
+    return (size_t)capA * 16 + (size_t)WS_SUBS * 4 + 8 * (size_t)plan.a.buckets;
+}
+
+}  // namespace saix

@@ -14,8 +14,8 @@ if what == "c5":
     torch.cuda.synchronize()
     torch.cuda.profiler.start(); wl.step_device(); torch.cuda.synchronize(); torch.cuda.profiler.stop()
 elif what == "c4":
-    from paper_1404_3448_b200.workloads import c4_pairs
-    seqs, offs = c4_pairs(0, 6700)      # one wave of <= 2^27 residues
+    from paper_1404_3448_b200.workloads import c4_generate
+    seqs, offs = c4_generate(0, 100_000)  # the whole C4 batch (on-chip pair DC3: one launch)
     ob = sx.OverlapBatch(seqs, offs)
     ob.run_device(); ob.run_device()
     torch.cuda.synchronize()
