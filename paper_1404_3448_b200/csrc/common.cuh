@@ -152,6 +152,35 @@ __device__ __forceinline__ u32 lanemask_lt() {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// ------------------------------------------- bulk copies (TMA) + mbarriers
+// One-dimensional cp.async.bulk global -> shared completing on an mbarrier
+// (sm_90+ async proxy; on sm_100a the copy engine behind UBLKCP).  src/dst
+// 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64 *bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// make the barrier init (and prior generic-proxy smem writes) visible to the async proxy
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(u64 *bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, u32 bytes, u64 *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *bar, u32 parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // Peer mask of lanes holding the same 8-bit digit: eight ballots + ANDs
 // (cheaper than __match_any_sync on sm_100).  Lanes with d == OS_RADIX (no
 // item) differ from every valid digit in bit 8 via the `valid` ballot.

@@ -1958,7 +1958,9 @@ static int sort_samples(Dc3Ctx &c, Text<TT> T, const SampleLayout &L, u64 sigma,
         u32 *tmp = ar.alloc<u32>(scan_tmp_words(nwords));
         SAIX_ARENA_OK(ar);
         SAIX_CUDA(cudaMemsetAsync(bm, 0, (size_t)nwords * 4, st));
-        int use_smem = nwords * 4 <= 48 * 1024;
+        // private bitmap in shared memory when it fits beside the kernels' 6 KB
+        // text tile under the default 48 KB dynamic + static limit
+        int use_smem = nwords * 4 <= 40 * 1024;
         // tiny bitmaps (level 0: <= 216 codes) merge cheaply from every CTA;
         // larger ones are privatised in fewer, longer-lived CTAs
         int gs = (use_smem && nwords > 1024) ? (g < 2 * kNumSMs ? g : 2 * kNumSMs) : g;
@@ -2577,7 +2579,7 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
         SAIX_CUDA(cudaFuncSetAttribute(k_ws_count, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_FINE * 2));
         SAIX_CUDA(cudaFuncSetAttribute(k_ws_part1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_P2_SMEM));
         SAIX_CUDA(cudaFuncSetAttribute(k_ws_part2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_P2_SMEM));
-        SAIX_CUDA(cudaFuncSetAttribute(k_ws_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 << 10));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 << 10));
         attr.set();
     }
     SAIX_CUDA(cudaMemsetAsync(hist, 0, (size_t)WS_FINE * 4, st));
@@ -2614,8 +2616,10 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     SAIX_CUDA(cudaMemsetAsync(pu.a.cursor, 0, (size_t)pu.cursor_words() * 4, st));
     {
         Prof prof_("dc3.ws_sort", 8.0 * m + 4.0 * m + 8.0 * m, st);
-        k_ws_sort<<<WS_FINE, WS_ST, ws_sort_smem(capA, pu), st>>>(SB, off, m, L.m1, capA, sorted, pu,
-                                                                 reinterpret_cast<uint2 *>(SA_), rsA, rlA, cap, scal);
+        const size_t smem = ws_sort_smem(capA, pu);
+        const int per_sm = smem <= (110u << 10) ? 2 : 1;
+        k_ws_sort<<<kNumSMs * per_sm, WS_ST, smem, st>>>(SB, off, m, L.m1, capA, sorted, pu,
+                                                          reinterpret_cast<uint2 *>(SA_), rsA, rlA, cap, scal);
         SAIX_LAUNCHED();
     }
     u32 h6[6];

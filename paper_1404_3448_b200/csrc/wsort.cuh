@@ -22,9 +22,10 @@
 //   P2a k_ws_part1  text tiles -> records bucketed by the first 4 chars
 //                   (256 coarse regions; runs of ~32 records per tile)
 //   P2b k_ws_part2  each coarse region -> 256 fine buckets (chars 5..8)
-//   P3  k_ws_sort   one CTA per fine bucket: counting split by chars 9..13
-//                   in shared memory, per-thread insertion sort of the
-//                   ~3-record sub-buckets, then in the same pass: the sorted
+//   P3  k_ws_sort   persistent CTAs, one fine bucket at a time (bulk-copy
+//                   prefetch of the next): counting split by the next 11
+//                   bits in shared memory, rank by counting inside the
+//                   ~1.3-record sub-buckets, then in the same pass: the sorted
 //                   sample indices (= SAc), distinct-name count, tied runs
 //                   for resolve_ties, and ISAc[s] = rank through pass A of
 //                   the bucketed scatter (pscatter.cuh).
@@ -43,14 +44,14 @@ constexpr int WS_FINE = 1 << 16;          // fine buckets: 8 leading characters
 constexpr int WS_COARSE = 256;            // coarse regions: 4 leading characters
 constexpr int WS_POS_BITS = 29;
 constexpr u64 WS_POS_MASK = (1ull << WS_POS_BITS) - 1;
-constexpr int WS_SUBS = 1024;             // P3 split: characters 9..13
+constexpr int WS_SUBS = 2048;             // P3 split: the next 11 bits (characters 9..14)
 constexpr int WS_PT = 512;                // P2 threads
 constexpr int WS_PI = 16;                 // P2 items per thread
 constexpr int WS_PTILE = WS_PT * WS_PI;   // 8192 records
-constexpr int WS_ST = 256;                // P3 threads
-constexpr int WS_SI = 16;                 // P3 emit items per thread
+constexpr int WS_ST = 512;                // P3 threads
+constexpr int WS_SI = 8;                  // P3 emit items per thread
 constexpr int WS_CAP_MIN = WS_ST * WS_SI; // 4096
-constexpr int WS_CAP_MAX = 12288;         // largest fine bucket P3 takes
+constexpr int WS_CAP_MAX = 8960;          // largest fine bucket P3 takes (3 buffers <= 227 KB)
 constexpr int WS_SMALL_SUB = 32;          // insertion-sort limit per sub-bucket
 constexpr int WS_MAX_RUN = 4096;          // longest tied run handed to resolve_ties
 
@@ -265,147 +266,190 @@ k_ws_part2(const u64 *__restrict__ stageA, const u32 *__restrict__ off, const u3
 }
 
 // ---------------------------------------------------------------- P3
+// Persistent: CTA b sorts fine buckets b, b + grid, ...  The next bucket's
+// records arrive by a bulk copy (TMA, cp.async.bulk) into IN while the
+// current one is ranked and written.  Per bucket (L records, all sharing
+// characters 1..8):
+//   split   IN -> S by the next 11 bits (2048 sub-buckets, ~1.3 records
+//           each on random text) with shared-memory atomics
+//   rank    every record counts the smaller records of its sub-bucket and
+//           lands at that rank in R (sub-buckets of > 32: CTA bitonic)
+//   emit    names / tied runs / sorted sample indices / ISA pass A
 // scal (resolve_ties layout): [2] tied runs, [4] overflow, [5] distinct names
-__global__ void __launch_bounds__(WS_ST)
+constexpr int WS_SUB_SHIFT = 45;
+__device__ __forceinline__ u32 ws_sub(u64 r) { return (u32)(r >> WS_SUB_SHIFT) & (WS_SUBS - 1); }
+
+__global__ void __launch_bounds__(WS_ST, 2)
 k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i64 m1, int capA,
           u32 *__restrict__ sorted, PsPlan plan, uint2 *__restrict__ stage1, u32 *__restrict__ rs,
           u32 *__restrict__ rl, u32 cap_runs, u32 *__restrict__ scal) {
     extern __shared__ __align__(16) unsigned char ws_smem[];
-    const u32 f = blockIdx.x;
-    const i64 lo = off[f];
-    const i64 hi = f + 1 < WS_FINE ? (i64)off[f + 1] : m;
-    const int L = (int)(hi - lo);
-    if (L <= 0) return;
-    u64 *A = reinterpret_cast<u64 *>(ws_smem);
-    u64 *B = A + capA;
-    u32 *scnt = reinterpret_cast<u32 *>(B + capA);
+    u64 *IN = reinterpret_cast<u64 *>(ws_smem);
+    u64 *S = IN + capA + 2;
+    u64 *R = S + capA;
+    u32 *scnt = reinterpret_cast<u32 *>(R + capA);
     u32 *e_cnt = scnt + WS_SUBS, *e_base = e_cnt + plan.a.buckets;
+    __shared__ __align__(8) u64 bar;
     __shared__ u32 sh_big[64];
     __shared__ u32 sh_nbig, sh_d;
-    for (int i = threadIdx.x; i < WS_SUBS; i += WS_ST) scnt[i] = 0;
-    if (threadIdx.x == 0) {
-        sh_nbig = 0;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
         sh_d = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_async_smem();
     }
-#pragma unroll 4
-    for (int x = threadIdx.x; x < L; x += WS_ST) A[x] = __ldcs(stageB + lo + x);
     __syncthreads();
-    for (int x = threadIdx.x; x < L; x += WS_ST) atomicAdd(&scnt[(u32)(A[x] >> 46) & (WS_SUBS - 1)], 1u);
-    __syncthreads();
-    {  // exclusive scan of the sub-bucket counts, 4 per thread
-        __shared__ u32 sh_warp[WS_ST / 32 + 1];
-        u32 v[4], s = 0;
+    auto span = [&](u32 f, i64 &lo, int &L) {
+        lo = off[f];
+        L = (int)((f + 1 < WS_FINE ? (i64)off[f + 1] : m) - lo);
+    };
+    auto issue = [&](i64 lo, int L) {  // one thread: the bucket's 16 B-aligned cover
+        const i64 a0 = lo & ~(i64)1, a1 = (lo + L + 1) & ~(i64)1;
+        const u32 bytes = (u32)((a1 - a0) * 8);
+        mbar_expect_tx(&bar, bytes);
+        bulk_g2s(IN, stageB + a0, bytes, &bar);
+    };
+    u32 f = blockIdx.x, parity = 0, d = 0;
+    i64 lo = 0;
+    int L = 0;
+    if (f < WS_FINE) span(f, lo, L);
+    if (tid == 0 && f < WS_FINE && L > 0) issue(lo, L);
+    for (; f < WS_FINE; f += gridDim.x) {
+        const u32 fn = f + gridDim.x;
+        i64 lo_n = 0;
+        int L_n = 0;
+        if (fn < WS_FINE) span(fn, lo_n, L_n);
+        if (L > 0) {
+            for (int i = tid; i < WS_SUBS; i += WS_ST) scnt[i] = 0;
+            if (tid == 0) sh_nbig = 0;
+            mbar_wait(&bar, parity);
+            parity ^= 1;
+            const u64 *in = IN + (lo & 1);
+            __syncthreads();
+            for (int x = tid; x < L; x += WS_ST) atomicAdd(&scnt[ws_sub(in[x])], 1u);
+            __syncthreads();
+            {  // exclusive scan of the sub-bucket counts, 4 per thread
+                __shared__ u32 sh_warp[WS_ST / 32 + 1];
+                u32 v[4], sum = 0;
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            v[k] = scnt[threadIdx.x * 4 + k];
-            s += v[k];
-        }
-        u32 excl;
-        block_exclusive_scan<WS_ST>(s, excl, sh_warp);
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            scnt[threadIdx.x * 4 + k] = excl;
-            excl += v[k];
-        }
-    }
-    __syncthreads();
-    for (int x = threadIdx.x; x < L; x += WS_ST) {
-        const u64 r = A[x];
-        B[atomicAdd(&scnt[(u32)(r >> 46) & (WS_SUBS - 1)], 1u)] = r;
-    }
-    __syncthreads();
-    // scnt[k] = end of sub-bucket k; sort each (they share characters 1..13)
-    for (int k = threadIdx.x; k < WS_SUBS; k += WS_ST) {
-        const int s0 = k ? (int)scnt[k - 1] : 0, e = (int)scnt[k];
-        if (e - s0 <= 1) continue;
-        if (e - s0 > WS_SMALL_SUB) {
-            const u32 at = atomicAdd(&sh_nbig, 1u);
-            if (at < 64) sh_big[at] = (u32)k;
-            else atomicMax(&scal[4], 1u);
-            continue;
-        }
-        for (int i = s0 + 1; i < e; i++) {
-            const u64 v = B[i];
-            int j = i - 1;
-            while (j >= s0 && B[j] > v) {
-                B[j + 1] = B[j];
-                j--;
-            }
-            B[j + 1] = v;
-        }
-    }
-    __syncthreads();
-    const u32 nbig = sh_nbig < 64 ? sh_nbig : 64;
-    for (u32 q = 0; q < nbig; q++) {  // large sub-buckets: CTA bitonic in A
-        const int k = (int)sh_big[q];
-        const int s0 = k ? (int)scnt[k - 1] : 0, len = (int)scnt[k] - s0;
-        int p2 = 1;
-        while (p2 < len) p2 <<= 1;
-        if (p2 > capA) {
-            if (threadIdx.x == 0) atomicMax(&scal[4], 1u);
-            continue;
-        }
-        for (int x = threadIdx.x; x < p2; x += WS_ST) A[x] = x < len ? B[s0 + x] : ~0ull;
-        __syncthreads();
-        for (int size = 2; size <= p2; size <<= 1)
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                for (int tt = threadIdx.x; tt < (p2 >> 1); tt += WS_ST) {
-                    const int a = 2 * tt - (tt & (stride - 1)), bb = a + stride;
-                    const bool up = (a & size) == 0;
-                    const u64 x = A[a], y = A[bb];
-                    if ((x > y) == up) {
-                        A[a] = y;
-                        A[bb] = x;
-                    }
+                for (int k = 0; k < 4; k++) {
+                    v[k] = scnt[tid * 4 + k];
+                    sum += v[k];
                 }
+                u32 excl;
+                block_exclusive_scan<WS_ST>(sum, excl, sh_warp);
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    scnt[tid * 4 + k] = excl;
+                    excl += v[k];
+                }
+            }
+            __syncthreads();
+            for (int x = tid; x < L; x += WS_ST) {
+                const u64 r = in[x];
+                S[atomicAdd(&scnt[ws_sub(r)], 1u)] = r;
+            }
+            __syncthreads();  // IN is free: the next bucket streams in behind the rest
+            if (tid == 0 && L_n > 0) {
+                fence_async_smem();
+                issue(lo_n, L_n);
+            }
+            // scnt[k] = end of sub-bucket k
+            for (int i = tid; i < L; i += WS_ST) {
+                const u64 v = S[i];
+                const u32 k = ws_sub(v);
+                const int s0 = k ? (int)scnt[k - 1] : 0, e = (int)scnt[k];
+                if (e - s0 > WS_SMALL_SUB) {
+                    R[i] = v;
+                    if (i == s0) {
+                        const u32 at = atomicAdd(&sh_nbig, 1u);
+                        if (at < 64) sh_big[at] = k;
+                        else atomicMax(&scal[4], 1u);
+                    }
+                    continue;
+                }
+                int r = s0;
+                for (int j = s0; j < e; j++) r += S[j] < v;
+                R[r] = v;
+            }
+            __syncthreads();
+            const u32 nbig = sh_nbig < 64 ? sh_nbig : 64;
+            for (u32 q = 0; q < nbig; q++) {  // large sub-buckets: CTA bitonic in S
+                const u32 k = sh_big[q];
+                const int s0 = k ? (int)scnt[k - 1] : 0, len = (int)scnt[k] - s0;
+                int p2 = 1;
+                while (p2 < len) p2 <<= 1;
+                if (p2 > capA) {
+                    if (tid == 0) atomicMax(&scal[4], 1u);
+                    continue;
+                }
+                for (int x = tid; x < p2; x += WS_ST) S[x] = x < len ? R[s0 + x] : ~0ull;
+                __syncthreads();
+                for (int size = 2; size <= p2; size <<= 1)
+                    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                        for (int t = tid; t < (p2 >> 1); t += WS_ST) {
+                            const int a = 2 * t - (t & (stride - 1)), b = a + stride;
+                            const bool up = (a & size) == 0;
+                            const u64 x = S[a], y = S[b];
+                            if ((x > y) == up) {
+                                S[a] = y;
+                                S[b] = x;
+                            }
+                        }
+                        __syncthreads();
+                    }
+                for (int x = tid; x < len; x += WS_ST) R[s0 + x] = S[x];
                 __syncthreads();
             }
-        for (int x = threadIdx.x; x < len; x += WS_ST) B[s0 + x] = A[x];
-        __syncthreads();
-    }
-    // names, tied runs, sorted order and the ISA scatter's pass A
-    u32 d = 0;
-    for (int c0 = 0; c0 < L; c0 += WS_ST * WS_SI) {
-        uint2 it[WS_SI];
-        bool ok[WS_SI];
+            // names, tied runs, sorted order and the ISA scatter's pass A
+            for (int c0 = 0; c0 < L; c0 += WS_ST * WS_SI) {
+                uint2 it[WS_SI];
+                bool ok[WS_SI];
 #pragma unroll
-        for (int r = 0; r < WS_SI; r++) {
-            const int x = c0 + r * WS_ST + threadIdx.x;
-            ok[r] = x < L;
-            if (!ok[r]) continue;
-            const u64 v = B[x];
-            const bool head = x == 0 || !ws_same(B[x - 1], v);
-            d += head;
-            if (head && x + 1 < L && ws_same(v, B[x + 1])) {
-                int e = x + 2;
-                while (e < L && e - x <= WS_MAX_RUN && ws_same(v, B[e])) e++;
-                if (e - x > WS_MAX_RUN) {
-                    atomicMax(&scal[4], 1u);
-                } else {
-                    const u32 at = atomicAdd(&scal[2], 1u);
-                    if (at < cap_runs) {
-                        rs[at] = (u32)(lo + x);
-                        rl[at] = (u32)(e - x);
-                    } else {
-                        atomicMax(&scal[4], 1u);
+                for (int r = 0; r < WS_SI; r++) {
+                    const int x = c0 + r * WS_ST + tid;
+                    ok[r] = x < L;
+                    if (!ok[r]) continue;
+                    const u64 v = R[x];
+                    const bool head = x == 0 || !ws_same(R[x - 1], v);
+                    d += head;
+                    if (head && x + 1 < L && ws_same(v, R[x + 1])) {
+                        int e = x + 2;
+                        while (e < L && e - x <= WS_MAX_RUN && ws_same(v, R[e])) e++;
+                        if (e - x > WS_MAX_RUN) {
+                            atomicMax(&scal[4], 1u);
+                        } else {
+                            const u32 at = atomicAdd(&scal[2], 1u);
+                            if (at < cap_runs) {
+                                rs[at] = (u32)(lo + x);
+                                rl[at] = (u32)(e - x);
+                            } else {
+                                atomicMax(&scal[4], 1u);
+                            }
+                        }
                     }
+                    const u32 p = (u32)ws_pos(v);
+                    const u32 sidx = (p % 3u == 1u) ? p / 3u : (u32)m1 + p / 3u;
+                    __stcs(sorted + lo + x, sidx);
+                    it[r] = make_uint2(sidx, (u32)(lo + x));
                 }
+                ps_block_emit<uint2, WS_ST, WS_SI>(it, ok, plan.a, stage1, reinterpret_cast<uint2 *>(S), e_cnt, e_base);
             }
-            const i64 p = ws_pos(v);
-            const u32 s = (u32)(p % 3 == 1 ? p / 3 : m1 + p / 3);
-            __stcs(sorted + lo + x, s);
-            it[r] = make_uint2(s, (u32)(lo + x));
+        } else if (tid == 0 && L_n > 0) {  // empty bucket: nothing in flight, IN is free
+            fence_async_smem();
+            issue(lo_n, L_n);
         }
-        __syncthreads();  // A is the emit staging
-        ps_block_emit<uint2, WS_ST, WS_SI>(it, ok, plan.a, stage1, reinterpret_cast<uint2 *>(A), e_cnt, e_base);
+        lo = lo_n;
+        L = L_n;
     }
     for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
     if (lane_id() == 0 && d) atomicAdd(&sh_d, d);
     __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(&scal[5], sh_d);
+    if (tid == 0 && sh_d) atomicAdd(&scal[5], sh_d);
 }
 inline size_t ws_sort_smem(int capA, const PsPlan &plan) {
-    return (size_t)capA * 16 + (size_t)WS_SUBS * 4 + 8 * (size_t)plan.a.buckets;
+    return (size_t)(3 * capA + 2) * 8 + (size_t)WS_SUBS * 4 + 8 * (size_t)plan.a.buckets;
 }
 
 }  // namespace saix

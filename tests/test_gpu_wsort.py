@@ -68,10 +68,18 @@ def test_small_alphabets(sigma):
     _check(_random(N0, 20 + sigma, tuple(range(1, sigma + 1))), sigma=sigma, naming=2 if sigma == 3 else None)
 
 
-def test_at_only_text_larger_buckets():
-    """Two of four digits: 2^8 of the 2^16 fine buckets, ~5.5k records each
-    (P3 capacity above its 4096 minimum)."""
-    _check(_random(N0, 31, (1, 4)))
+def test_skewed_text_larger_buckets():
+    """Weights (0.5, 0.2, 0.2, 0.1): the AAAAAAAA bucket holds ~5.5k records
+    (P3 capacity above its 4096 minimum, one CTA per SM) and its sub-buckets
+    reach past 32 records (the CTA bitonic)."""
+    rng = np.random.default_rng(31)
+    t = (rng.choice(4, size=N0, p=[0.5, 0.2, 0.2, 0.1]) + 1).astype(np.uint8)
+    _check(t)
+
+
+def test_two_letter_text_leaves_the_path():
+    """A/T only: 2^21 windows for 1.4M samples, mostly tied -> recursion."""
+    _check(_random(N0, 31, (1, 4)), naming=None)
 
 
 def test_planted_repeats_tie_rounds():
