@@ -2602,6 +2602,7 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     }
     tried = true;
     const int capA = (int)(h[1] <= (u32)WS_CAP_MIN ? WS_CAP_MIN : ceil_div((i64)h[1], (i64)256) * 256);
+    // (the largest bucket fits; emit staging reuses S)
     {
         Prof prof_("dc3.ws_part1", (double)N + 8.0 * m, st);
         k_ws_part1<<<(unsigned)ntiles, WS_PT, WS_P2_SMEM, st>>>(text, L, curC, SA_);
@@ -2617,14 +2618,19 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     {
         Prof prof_("dc3.ws_sort", 8.0 * m + 4.0 * m + 8.0 * m, st);
         const size_t smem = ws_sort_smem(capA, pu);
-        const int per_sm = smem <= (110u << 10) ? 2 : 1;
+        const int per_sm = smem <= (74u << 10) ? 3 : smem <= (112u << 10) ? 2 : 1;
         k_ws_sort<<<kNumSMs * per_sm, WS_ST, smem, st>>>(SB, off, m, L.m1, capA, sorted, pu,
                                                           reinterpret_cast<uint2 *>(SA_), rsA, rlA, cap, scal);
         SAIX_LAUNCHED();
     }
-    u32 h6[6];
-    SAIX_CUDA(cudaMemcpyAsync(h6, scal, 24, cudaMemcpyDeviceToHost, st));
+    u32 h6[9];
+    SAIX_CUDA(cudaMemcpyAsync(h6, scal, 36, cudaMemcpyDeviceToHost, st));
     SAIX_CUDA(cudaStreamSynchronize(st));
+    if (h6[8]) {  // low-complexity sub-bucket: the generic window sort
+        tried = false;
+        ar.reset(mark);
+        return SAIX_OK;
+    }
     const u32 D = h6[5];
     const bool tie_ok = (i64)D < m && (i64)(m - D) <= m / 32 && !h6[4];
     if ((i64)D == m || tie_ok) {

@@ -23,9 +23,9 @@
 //                   (256 coarse regions; runs of ~32 records per tile)
 //   P2b k_ws_part2  each coarse region -> 256 fine buckets (chars 5..8)
 //   P3  k_ws_sort   persistent CTAs, one fine bucket at a time (bulk-copy
-//                   prefetch of the next): counting split by the next 11
+//                   prefetch of the next): counting split by the next 12
 //                   bits in shared memory, rank by counting inside the
-//                   ~1.3-record sub-buckets, then in the same pass: the sorted
+//                   ~0.7-record sub-buckets, then in the same pass: the sorted
 //                   sample indices (= SAc), distinct-name count, tied runs
 //                   for resolve_ties, and ISAc[s] = rank through pass A of
 //                   the bucketed scatter (pscatter.cuh).
@@ -44,15 +44,13 @@ constexpr int WS_FINE = 1 << 16;          // fine buckets: 8 leading characters
 constexpr int WS_COARSE = 256;            // coarse regions: 4 leading characters
 constexpr int WS_POS_BITS = 29;
 constexpr u64 WS_POS_MASK = (1ull << WS_POS_BITS) - 1;
-constexpr int WS_SUBS = 2048;             // P3 split: the next 11 bits (characters 9..14)
+constexpr int WS_SUBS = 4096;             // P3 split: the next 12 bits (characters 9..14)
 constexpr int WS_PT = 512;                // P2 threads
 constexpr int WS_PI = 16;                 // P2 items per thread
 constexpr int WS_PTILE = WS_PT * WS_PI;   // 8192 records
 constexpr int WS_ST = 512;                // P3 threads
-constexpr int WS_SI = 8;                  // P3 emit items per thread
-constexpr int WS_CAP_MIN = WS_ST * WS_SI; // 4096
-constexpr int WS_CAP_MAX = 8960;          // largest fine bucket P3 takes (3 buffers <= 227 KB)
-constexpr int WS_SMALL_SUB = 32;          // insertion-sort limit per sub-bucket
+constexpr int WS_CAP_MIN = 1024;
+constexpr int WS_CAP_MAX = 10240;         // largest fine bucket P3 takes (shared memory <= 227 KB)
 constexpr int WS_MAX_RUN = 4096;          // longest tied run handed to resolve_ties
 
 // 16 ranks (bytes 1..4) -> one 32-bit word of 2-bit digits, first at the top
@@ -270,29 +268,37 @@ k_ws_part2(const u64 *__restrict__ stageA, const u32 *__restrict__ off, const u3
 // records arrive by a bulk copy (TMA, cp.async.bulk) into IN while the
 // current one is ranked and written.  Per bucket (L records, all sharing
 // characters 1..8):
-//   split   IN -> S by the next 11 bits (2048 sub-buckets, ~1.3 records
+//   split   IN -> S by the next 12 bits (4096 sub-buckets, ~0.7 records
 //           each on random text) with shared-memory atomics
-//   rank    every record counts the smaller records of its sub-bucket and
-//           lands at that rank in R (sub-buckets of > 32: CTA bitonic)
-//   emit    names / tied runs / sorted sample indices / ISA pass A
-// scal (resolve_ties layout): [2] tied runs, [4] overflow, [5] distinct names
-constexpr int WS_SUB_SHIFT = 45;
+//   rank    every record counts, inside its sub-bucket, the smaller records
+//           (its rank), the smaller records of the same name (0: it heads
+//           its name) and the records of its name (the tied run's length);
+//           the sample index lands at its rank in R (u32)
+//   emit    R streamed out as the sorted order; (sample, rank) pairs bucketed
+//           in shared memory and written as runs = pass A of the ISA scatter
+// Equal names share characters 1..14, hence a sub-bucket: no comparison
+// crosses one.  Sub-buckets over WS_BIG_SUB records (low-complexity text)
+// set the overflow flag and the caller takes the generic window sort.
+// scal (resolve_ties layout): [2] tied runs, [4] overflow, [5] distinct names;
+// [8] a sub-bucket over WS_BIG_SUB
+constexpr int WS_SUB_SHIFT = 44;
+constexpr int WS_BIG_SUB = 256;
 __device__ __forceinline__ u32 ws_sub(u64 r) { return (u32)(r >> WS_SUB_SHIFT) & (WS_SUBS - 1); }
 
-__global__ void __launch_bounds__(WS_ST, 2)
+__global__ void __launch_bounds__(WS_ST, 3)
 k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i64 m1, int capA,
           u32 *__restrict__ sorted, PsPlan plan, uint2 *__restrict__ stage1, u32 *__restrict__ rs,
           u32 *__restrict__ rl, u32 cap_runs, u32 *__restrict__ scal) {
     extern __shared__ __align__(16) unsigned char ws_smem[];
     u64 *IN = reinterpret_cast<u64 *>(ws_smem);
     u64 *S = IN + capA + 2;
-    u64 *R = S + capA;
-    u32 *scnt = reinterpret_cast<u32 *>(R + capA);
-    u32 *e_cnt = scnt + WS_SUBS, *e_base = e_cnt + plan.a.buckets;
+    u32 *R = reinterpret_cast<u32 *>(S + capA);
+    u32 *scnt = R + capA;  // WS_SUBS 16-bit counters, two per word
+    u32 *e_cnt = scnt + WS_SUBS / 2, *e_base = e_cnt + plan.a.buckets;
     __shared__ __align__(8) u64 bar;
-    __shared__ u32 sh_big[64];
-    __shared__ u32 sh_nbig, sh_d;
+    __shared__ u32 sh_d;
     const int tid = threadIdx.x;
+    const int nq = (int)plan.a.buckets;
     if (tid == 0) {
         mbar_init(&bar, 1);
         sh_d = 0;
@@ -321,34 +327,40 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
         int L_n = 0;
         if (fn < WS_FINE) span(fn, lo_n, L_n);
         if (L > 0) {
-            for (int i = tid; i < WS_SUBS; i += WS_ST) scnt[i] = 0;
-            if (tid == 0) sh_nbig = 0;
+            for (int i = tid; i < WS_SUBS / 2; i += WS_ST) scnt[i] = 0;
+            for (int i = tid; i < nq; i += WS_ST) e_cnt[i] = 0;
             mbar_wait(&bar, parity);
             parity ^= 1;
             const u64 *in = IN + (lo & 1);
             __syncthreads();
-            for (int x = tid; x < L; x += WS_ST) atomicAdd(&scnt[ws_sub(in[x])], 1u);
+            for (int x = tid; x < L; x += WS_ST) {
+                const u32 k = ws_sub(in[x]);
+                atomicAdd(&scnt[k >> 1], 1u << (16 * (k & 1)));
+            }
             __syncthreads();
-            {  // exclusive scan of the sub-bucket counts, 4 per thread
+            {  // exclusive scan of the sub-bucket counts (16-bit pairs)
+                constexpr int PER = WS_SUBS / 2 / WS_ST;
                 __shared__ u32 sh_warp[WS_ST / 32 + 1];
-                u32 v[4], sum = 0;
+                u32 v[PER], sum = 0;
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    v[k] = scnt[tid * 4 + k];
-                    sum += v[k];
+                for (int k = 0; k < PER; k++) {
+                    v[k] = scnt[tid * PER + k];
+                    sum += (v[k] & 0xFFFFu) + (v[k] >> 16);
                 }
                 u32 excl;
                 block_exclusive_scan<WS_ST>(sum, excl, sh_warp);
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    scnt[tid * 4 + k] = excl;
-                    excl += v[k];
+                for (int k = 0; k < PER; k++) {
+                    const u32 a = excl, b = excl + (v[k] & 0xFFFFu);
+                    scnt[tid * PER + k] = a | (b << 16);
+                    excl = b + (v[k] >> 16);
                 }
             }
             __syncthreads();
             for (int x = tid; x < L; x += WS_ST) {
                 const u64 r = in[x];
-                S[atomicAdd(&scnt[ws_sub(r)], 1u)] = r;
+                const u32 k = ws_sub(r), sh = 16 * (k & 1);
+                S[(atomicAdd(&scnt[k >> 1], 1u << sh) >> sh) & 0xFFFFu] = r;
             }
             __syncthreads();  // IN is free: the next bucket streams in behind the rest
             if (tid == 0 && L_n > 0) {
@@ -359,83 +371,70 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
             for (int i = tid; i < L; i += WS_ST) {
                 const u64 v = S[i];
                 const u32 k = ws_sub(v);
-                const int s0 = k ? (int)scnt[k - 1] : 0, e = (int)scnt[k];
-                if (e - s0 > WS_SMALL_SUB) {
-                    R[i] = v;
-                    if (i == s0) {
-                        const u32 at = atomicAdd(&sh_nbig, 1u);
-                        if (at < 64) sh_big[at] = k;
-                        else atomicMax(&scal[4], 1u);
+                const u32 wk = scnt[k >> 1];
+                const int e = (int)((k & 1) ? wk >> 16 : wk & 0xFFFFu);
+                const int s0 = (k & 1) ? (int)(wk & 0xFFFFu) : (k ? (int)(scnt[(k >> 1) - 1] >> 16) : 0);
+                int lt = 0, same_lt = 0, same = 0;
+                if (e - s0 > WS_BIG_SUB) {
+                    atomicMax(&scal[8], 1u);
+                } else if (e - s0 > 1) {
+                    // same name: equal characters and flag bits, v a full window
+                    const u64 vh = ((v >> 29) & 1) ? v >> 29 : ~0ull;
+                    for (int j = s0; j < e; j++) {
+                        const u64 o = S[j];
+                        const bool less = o < v, eq = (o >> 29) == vh;
+                        lt += less;
+                        same_lt += less && eq;
+                        same += eq;
                     }
-                    continue;
                 }
-                int r = s0;
-                for (int j = s0; j < e; j++) r += S[j] < v;
-                R[r] = v;
+                const int rank = s0 + lt;
+                if (same_lt == 0) {
+                    d++;
+                    if (same > 1) {
+                        const u32 at = atomicAdd(&scal[2], 1u);
+                        if (at < cap_runs) {
+                            rs[at] = (u32)(lo + rank);
+                            rl[at] = (u32)same;
+                        } else {
+                            atomicMax(&scal[4], 1u);
+                        }
+                    }
+                }
+                const u32 p = (u32)ws_pos(v);
+                const u32 sidx = (p % 3u == 1u) ? p / 3u : (u32)m1 + p / 3u;
+                R[rank] = sidx;
+                atomicAdd(&e_cnt[sidx >> plan.a.shift], 1u);
             }
             __syncthreads();
-            const u32 nbig = sh_nbig < 64 ? sh_nbig : 64;
-            for (u32 q = 0; q < nbig; q++) {  // large sub-buckets: CTA bitonic in S
-                const u32 k = sh_big[q];
-                const int s0 = k ? (int)scnt[k - 1] : 0, len = (int)scnt[k] - s0;
-                int p2 = 1;
-                while (p2 < len) p2 <<= 1;
-                if (p2 > capA) {
-                    if (tid == 0) atomicMax(&scal[4], 1u);
-                    continue;
-                }
-                for (int x = tid; x < p2; x += WS_ST) S[x] = x < len ? R[s0 + x] : ~0ull;
-                __syncthreads();
-                for (int size = 2; size <= p2; size <<= 1)
-                    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                        for (int t = tid; t < (p2 >> 1); t += WS_ST) {
-                            const int a = 2 * t - (t & (stride - 1)), b = a + stride;
-                            const bool up = (a & size) == 0;
-                            const u64 x = S[a], y = S[b];
-                            if ((x > y) == up) {
-                                S[a] = y;
-                                S[b] = x;
-                            }
-                        }
-                        __syncthreads();
+            if (tid < 32) {  // run reservation per coarse ISA bucket; local starts
+                u32 carry = 0;
+                for (int q0 = 0; q0 < nq; q0 += 32) {
+                    const int q = q0 + tid;
+                    const u32 c = q < nq ? e_cnt[q] : 0u;
+                    const u32 inc = warp_inclusive_scan(c);
+                    if (q < nq) {
+                        e_base[q] = (c ? atomicAdd(&plan.a.cursor[q], c) : 0u) - (carry + inc - c);
+                        e_cnt[q] = carry + inc - c;
                     }
-                for (int x = tid; x < len; x += WS_ST) R[s0 + x] = S[x];
-                __syncthreads();
-            }
-            // names, tied runs, sorted order and the ISA scatter's pass A
-            for (int c0 = 0; c0 < L; c0 += WS_ST * WS_SI) {
-                uint2 it[WS_SI];
-                bool ok[WS_SI];
-#pragma unroll
-                for (int r = 0; r < WS_SI; r++) {
-                    const int x = c0 + r * WS_ST + tid;
-                    ok[r] = x < L;
-                    if (!ok[r]) continue;
-                    const u64 v = R[x];
-                    const bool head = x == 0 || !ws_same(R[x - 1], v);
-                    d += head;
-                    if (head && x + 1 < L && ws_same(v, R[x + 1])) {
-                        int e = x + 2;
-                        while (e < L && e - x <= WS_MAX_RUN && ws_same(v, R[e])) e++;
-                        if (e - x > WS_MAX_RUN) {
-                            atomicMax(&scal[4], 1u);
-                        } else {
-                            const u32 at = atomicAdd(&scal[2], 1u);
-                            if (at < cap_runs) {
-                                rs[at] = (u32)(lo + x);
-                                rl[at] = (u32)(e - x);
-                            } else {
-                                atomicMax(&scal[4], 1u);
-                            }
-                        }
-                    }
-                    const u32 p = (u32)ws_pos(v);
-                    const u32 sidx = (p % 3u == 1u) ? p / 3u : (u32)m1 + p / 3u;
-                    __stcs(sorted + lo + x, sidx);
-                    it[r] = make_uint2(sidx, (u32)(lo + x));
+                    carry += __shfl_sync(0xffffffffu, inc, 31);
                 }
-                ps_block_emit<uint2, WS_ST, WS_SI>(it, ok, plan.a, stage1, reinterpret_cast<uint2 *>(S), e_cnt, e_base);
             }
+            __syncthreads();
+            uint2 *E = reinterpret_cast<uint2 *>(S);  // S is free: emit staging
+            for (int x = tid; x < L; x += WS_ST) {
+                const u32 sidx = R[x];
+                __stcs(sorted + lo + x, sidx);
+                E[atomicAdd(&e_cnt[sidx >> plan.a.shift], 1u)] = make_uint2(sidx, (u32)(lo + x));
+            }
+            __syncthreads();
+            // e_base[q] = q's run in its staging region minus its local start
+            for (int x = tid; x < L; x += WS_ST) {
+                const uint2 it = E[x];
+                const u32 q = it.x >> plan.a.shift;
+                st_stream(stage1 + ((i64)q << plan.a.shift) + (u32)(e_base[q] + (u32)x), it);
+            }
+            __syncthreads();
         } else if (tid == 0 && L_n > 0) {  // empty bucket: nothing in flight, IN is free
             fence_async_smem();
             issue(lo_n, L_n);
@@ -449,7 +448,7 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
     if (tid == 0 && sh_d) atomicAdd(&scal[5], sh_d);
 }
 inline size_t ws_sort_smem(int capA, const PsPlan &plan) {
-    return (size_t)(3 * capA + 2) * 8 + (size_t)WS_SUBS * 4 + 8 * (size_t)plan.a.buckets;
+    return (size_t)(2 * capA + 2) * 8 + (size_t)capA * 4 + (size_t)WS_SUBS * 2 + 8 * (size_t)plan.a.buckets;
 }
 
 }  // namespace saix
