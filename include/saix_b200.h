@@ -174,6 +174,9 @@ SAIX_API int saix_lcp_sigma(const void *text, int text_bytes, int64_t n, int64_t
 #define SAIX_SPARSE_PACK32 0  /* entry = (value-bias) << ibits | index, u32 */
 #define SAIX_SPARSE_PACK64 1  /* same packing in u64                        */
 #define SAIX_SPARSE_INDEX 2   /* entry = u32 index; values gathered (int64) */
+#define SAIX_SPARSE_BLOCKED 3 /* u8 values + 256-value blocks + sparse table
+                                 over block minima (L2-resident; queries scan
+                                 the two end blocks); values span <= 254    */
 
 typedef struct saix_sparse_plan {
     int64_t n;
@@ -197,6 +200,13 @@ SAIX_API int saix_widen_i64(const void *src, int src_bytes, int64_t n, int64_t *
 
 /* Choose the table layout for n values in [vmin, vmax]. */
 SAIX_API int saix_sparse_plan_make(int64_t n, int64_t vmin, int64_t vmax,
+                          saix_sparse_plan *plan);
+
+/* The query-optimised layout for the same SparseTable: SAIX_SPARSE_BLOCKED
+ * when vmax - vmin <= 254 (LCP arrays), else exactly saix_sparse_plan_make.
+ * Same answers (leftmost argmin); the per-level reference layout
+ * (SparseTable.table) then needs a saix_sparse_plan_make table. */
+SAIX_API int saix_sparse_plan_blocked(int64_t n, int64_t vmin, int64_t vmax,
                           saix_sparse_plan *plan);
 
 /* SparseTable.__init__ (rmq.py:33-50).  values: n entries of

@@ -27,7 +27,7 @@ SAIX_ENOSPC = -28
 SAIX_ECUDA = -100
 SAIX_ESEQ = -101
 
-SPARSE_PACK32, SPARSE_PACK64, SPARSE_INDEX = 0, 1, 2
+SPARSE_PACK32, SPARSE_PACK64, SPARSE_INDEX, SPARSE_BLOCKED = 0, 1, 2, 3
 
 
 class Dc3Probe(_c.Structure):
@@ -102,6 +102,7 @@ SIGNATURES = {
     "saix_index_unpack_workspace_bytes": (_c.c_size_t, [_i64]),
     "saix_index_unpack": (_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_sparse_plan_make": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),
+    "saix_sparse_plan_blocked": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),
     "saix_sparse_build": (_int, [_c.POINTER(SparsePlan), _vp, _int, _vp, _vp]),
     "saix_sparse_query": (_int, [_c.POINTER(SparsePlan), _vp, _vp, _int, _vp, _vp, _i64,
                                  _vp, _vp, _vp, _vp]),

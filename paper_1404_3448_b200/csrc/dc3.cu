@@ -2657,9 +2657,19 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     return SAIX_OK;
 }
 
+// smallest level the DNA window sort takes (below, the generic sort's few
+// launches win); SAIX_WS_MIN_M lowers it for compute-sanitizer runs on small
+// texts (tools/sanitize_run.py)
+static i64 ws_min_m() {
+    static i64 v = [] {
+        const char *e = getenv("SAIX_WS_MIN_M");
+        return e && *e ? (i64)atoll(e) : ((i64)1 << 20);
+    }();
+    return v;
+}
 static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const SampleLayout &L, u32 *SAc, u32 *ISAc,
                        u32 *d_scal, int depth, bool &handled) {
-    if (sigma <= 4 && N + 1 < (i64)WS_POS_MASK && L.m >= ((i64)1 << 20) && ((uintptr_t)text & 15) == 0 &&
+    if (sigma <= 4 && N + 1 < (i64)WS_POS_MASK && L.m >= ws_min_m() && ((uintptr_t)text & 15) == 0 &&
         ws_dna_on()) {
         bool tried = false;
         SAIX_TRY(window_rank_dna(c, text, N, L, SAc, ISAc, depth, handled, tried));

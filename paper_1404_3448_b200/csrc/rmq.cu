@@ -50,6 +50,168 @@ __global__ void k_sparse_idx_level(Vals<V> val, const u32 *__restrict__ prev, i6
 
 __device__ __forceinline__ int floor_log2(u64 x) { return 63 - __clzll((long long)x); }
 
+// ------------------------------------------------------------ blocked mode
+// SAIX_SPARSE_BLOCKED (values spanning <= 254 after the bias, e.g. LCP
+// arrays): an RMQ whose structures sit in L2 instead of a 6.7-13 GB table of
+// random HBM probes.  Blocks of 32 values, superblocks of 32 blocks (1024
+// values).  One table buffer holds
+//   vals8  n bytes: v - bias (0xFF past the end; 16 B slack)        64 MB at 2^26
+//   bpre   per block: leftmost min of [superblock start, block end]
+//   bsuf   per block: leftmost min of [block start, superblock end]
+//          both (v << 16 | offset in the superblock), u32          2 x 8 MB
+//   bmin   per block: (v << 8 | offset in the block), u16           4 MB
+//   stab   sparse table over superblock minima, (v << sbits | sb)    4 MB
+// A query [i, j] takes the leftmost minimum of: i's block scanned from i,
+// bsuf of the next block, stab over the superblocks strictly between, bpre
+// of the block before j's, j's block scanned up to j -- one 32 B sector of
+// vals8 per end plus four small L2 probes (same-superblock ranges scan bmin).
+// Candidates are combined as (value << 32 | position) keys, so equal values
+// keep the leftmost position (rmq.py:48-58).
+constexpr int BLK_SHIFT = 5, SB_SHIFT = 10;
+constexpr i64 BLK = (i64)1 << BLK_SHIFT, SBK = (i64)1 << SB_SHIFT;
+constexpr int BPS = (int)(SBK / BLK);  // blocks per superblock (32 = one warp)
+struct BlkLayout {
+    i64 n, nb, ns, n8, o_pre, o_suf, o_min, o_stab;
+    int sbits, slevels;
+    __host__ __device__ static BlkLayout of(i64 n) {
+        BlkLayout L;
+        L.n = n;
+        L.ns = (n + SBK - 1) >> SB_SHIFT;
+        L.nb = L.ns * BPS;  // whole superblocks (blocks past the end hold 0xFF)
+        L.n8 = L.nb * BLK + 16;
+        L.o_pre = L.n8;
+        L.o_suf = L.o_pre + 4 * L.nb;
+        L.o_min = L.o_suf + 4 * L.nb;
+        L.o_stab = L.o_min + ((2 * L.nb + 15) & ~(i64)15);
+        L.sbits = 0;
+        while (((i64)1 << L.sbits) < L.ns) L.sbits++;
+        L.slevels = 0;
+        while (L.slevels < 40 && ((i64)1 << L.slevels) <= L.ns) L.slevels++;
+        return L;
+    }
+    __host__ __device__ i64 bytes() const { return o_stab + 4 * level_off(ns, slevels); }
+};
+
+// one warp per superblock, lane l = block l: vals8, bmin, bpre / bsuf (warp
+// min-scans), stab level 0
+template <typename V>
+__global__ void k_blk_pack(Vals<V> val, BlkLayout L, i64 bias, u8 *__restrict__ tab) {
+    u32 *bpre = reinterpret_cast<u32 *>(tab + L.o_pre), *bsuf = reinterpret_cast<u32 *>(tab + L.o_suf);
+    u16 *bmin = reinterpret_cast<u16 *>(tab + L.o_min);
+    u32 *stab = reinterpret_cast<u32 *>(tab + L.o_stab);
+    const int lane = lane_id();
+    const i64 warps = ((i64)gridDim.x * blockDim.x) >> 5;
+    for (i64 sb = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sb < L.ns; sb += warps) {
+        const i64 b = sb * BPS + lane, p0 = b << BLK_SHIFT;
+        u32 w[8];
+        u32 best = 0xFFFFu;  // (v << 8 | offset in block)
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            u32 word = 0;
+#pragma unroll
+            for (int y = 0; y < 4; y++) {
+                const i64 p = p0 + 4 * q + y;
+                const u32 x = p < L.n ? (u32)((u64)val(p) - (u64)bias) : 0xFFu;
+                word |= x << (8 * y);
+                const u32 key = (x << 8) | (u32)(4 * q + y);
+                best = key < best ? key : best;
+            }
+            w[q] = word;
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(tab + p0);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        bmin[b] = (u16)best;
+        // (v << 16 | offset in superblock): min-scans over the warp's blocks
+        const u32 own = ((best >> 8) << 16) | (u32)(lane * BLK + (best & 0xFF));
+        u32 pre = own, suf = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 a = __shfl_up_sync(0xffffffffu, pre, o);
+            const u32 c = __shfl_down_sync(0xffffffffu, suf, o);
+            if (lane >= o) pre = a < pre ? a : pre;
+            if (lane + o < 32) suf = c < suf ? c : suf;
+        }
+        bpre[b] = pre;
+        bsuf[b] = suf;
+        if (lane == 0) stab[sb] = ((suf >> 16) << L.sbits) | (u32)sb;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 16) tab[L.n8 - 16 + threadIdx.x] = 0xFF;
+}
+
+// leftmost minimum of v8[a..b] inside one 32-value block, (v << 32 | position)
+__device__ __forceinline__ u64 blk_scan(const u8 *__restrict__ v8, i64 a, i64 b) {
+    const i64 c0 = a & ~(BLK - 1);
+    const uint4 q0 = __ldg(reinterpret_cast<const uint4 *>(v8 + c0));
+    const uint4 q1 = __ldg(reinterpret_cast<const uint4 *>(v8 + c0 + 16));
+    u32 w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    const int lo = (int)(a - c0), hi = (int)(b - c0);
+    u32 m = 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        // bytes outside [lo, hi] -> 0xFF (never a value: values are <= 254)
+        const int s = 4 * k;
+        u32 keep = 0xFFFFFFFFu;
+        if (s < lo) keep &= lo - s >= 4 ? 0u : (0xFFFFFFFFu << (8 * (lo - s)));
+        if (s + 3 > hi) keep &= hi - s < 0 ? 0u : (0xFFFFFFFFu >> (8 * (3 - (hi - s))));
+        w[k] |= ~keep;
+        m = __vminu4(m, w[k]);
+    }
+    m = __vminu4(m, m >> 16);
+    m = __vminu4(m, m >> 8) & 0xFFu;
+    const u32 pat = m * 0x01010101u;
+    int pos = 31;
+#pragma unroll
+    for (int k = 7; k >= 0; k--) {
+        const u32 e = __vcmpeq4(w[k], pat);
+        if (e) pos = 4 * k + ((__ffs(e) - 1) >> 3);
+    }
+    return ((u64)m << 32) | (u64)(c0 + pos);
+}
+
+__device__ __forceinline__ void blocked_query(const u8 *__restrict__ tab, i64 n, i64 bias, i64 i, i64 j, i64 &idx,
+                                              i64 &val) {
+    const BlkLayout L = BlkLayout::of(n);
+    const u32 *bpre = reinterpret_cast<const u32 *>(tab + L.o_pre), *bsuf = reinterpret_cast<const u32 *>(tab + L.o_suf);
+    const u16 *bmin = reinterpret_cast<const u16 *>(tab + L.o_min);
+    const u32 *stab = reinterpret_cast<const u32 *>(tab + L.o_stab);
+    const i64 bi = i >> BLK_SHIFT, bj = j >> BLK_SHIFT;
+    u64 best;
+    if (bi == bj) {
+        best = blk_scan(tab, i, j);
+    } else {
+        best = blk_scan(tab, i, ((bi + 1) << BLK_SHIFT) - 1);
+        const i64 si = i >> SB_SHIFT, sj = j >> SB_SHIFT;
+        auto cand = [&](u32 e, i64 sb) {  // (v << 16 | offset in superblock sb)
+            const u64 key = ((u64)(e >> 16) << 32) | (u64)((sb << SB_SHIFT) + (e & 0xFFFFu));
+            best = key < best ? key : best;
+        };
+        if (si == sj) {
+            for (i64 b = bi + 1; b < bj; b++) {  // rare: range inside one superblock
+                const u32 e = __ldg(bmin + b);
+                const u64 key = ((u64)(e >> 8) << 32) | (u64)((b << BLK_SHIFT) + (e & 0xFF));
+                best = key < best ? key : best;
+            }
+        } else {
+            if (bi + 1 < (si + 1) * BPS) cand(__ldg(bsuf + bi + 1), si);
+            if (si + 1 <= sj - 1) {
+                const i64 lo = si + 1, hi = sj - 1;
+                const int k = floor_log2((u64)(hi - lo + 1));
+                const u32 *lv = stab + level_off(L.ns, k);
+                const u32 a = __ldg(lv + lo), b = __ldg(lv + hi - ((i64)1 << k) + 1);
+                const u32 mn = a <= b ? a : b;
+                const i64 sb = (i64)(mn & ((1u << L.sbits) - 1));
+                cand(((mn >> L.sbits) << 16) | (__ldg(bsuf + sb * BPS) & 0xFFFFu), sb);
+            }
+            if (bj - 1 >= sj * BPS) cand(__ldg(bpre + bj - 1), sj);
+        }
+        const u64 r = blk_scan(tab, bj << BLK_SHIFT, j);
+        best = r < best ? r : best;
+    }
+    idx = (i64)(best & 0xFFFFFFFFull);
+    val = (i64)(best >> 32) + bias;
+}
+
 // One query: leftmost argmin index of [i, j] and its value.
 template <typename E>
 __device__ __forceinline__ void packed_query(const E *__restrict__ tab, i64 n, i64 bias, int ib, i64 i, i64 j,
@@ -81,7 +243,8 @@ struct PlanDev {
 template <typename V>
 __device__ __forceinline__ void any_query(const PlanDev &P, const void *tab, Vals<V> val, i64 i, i64 j,
                                           i64 &idx, i64 &v) {
-    if (P.mode == SAIX_SPARSE_PACK32) packed_query<u32>((const u32 *)tab, P.n, P.bias, P.ib, i, j, idx, v);
+    if (P.mode == SAIX_SPARSE_BLOCKED) blocked_query((const u8 *)tab, P.n, P.bias, i, j, idx, v);
+    else if (P.mode == SAIX_SPARSE_PACK32) packed_query<u32>((const u32 *)tab, P.n, P.bias, P.ib, i, j, idx, v);
     else if (P.mode == SAIX_SPARSE_PACK64) packed_query<u64>((const u64 *)tab, P.n, P.bias, P.ib, i, j, idx, v);
     else index_query<V>((const u32 *)tab, val, P.n, i, j, idx, v);
 }
@@ -223,6 +386,14 @@ extern "C" int saix_sparse_plan_make(int64_t n, int64_t vmin, int64_t vmax, saix
     return SAIX_OK;
 }
 
+extern "C" int saix_sparse_plan_blocked(int64_t n, int64_t vmin, int64_t vmax, saix_sparse_plan *plan) {
+    SAIX_TRY(saix_sparse_plan_make(n, vmin, vmax, plan));
+    if ((u64)vmax - (u64)vmin > 254 || n > ((int64_t)1 << 32) - 1) return SAIX_OK;  // keeps the full table
+    plan->mode = SAIX_SPARSE_BLOCKED;
+    plan->table_bytes = BlkLayout::of(n).bytes();
+    return SAIX_OK;
+}
+
 extern "C" int saix_sparse_build(const saix_sparse_plan *plan, const void *values, int value_bytes, void *table,
                                  void *stream) {
     if (!plan || !values || !table || (value_bytes != 4 && value_bytes != 8)) {
@@ -230,6 +401,28 @@ extern "C" int saix_sparse_build(const saix_sparse_plan *plan, const void *value
         return SAIX_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    if (plan->mode == SAIX_SPARSE_BLOCKED) {
+        const BlkLayout B = BlkLayout::of(plan->n);
+        u8 *tab = (u8 *)table;
+        u32 *bt = reinterpret_cast<u32 *>(tab + B.o_stab);
+        {
+            Prof prof_("rmq.block_pack", (double)(value_bytes + 1) * B.n + 10.0 * B.nb + 4.0 * B.ns, st);
+            const int g = grid_for(B.ns * 32, 256);
+            if (value_bytes == 4)
+                k_blk_pack<u32><<<g, 256, 0, st>>>(Vals<u32>{(const u32 *)values}, B, plan->value_bias, tab);
+            else
+                k_blk_pack<i64><<<g, 256, 0, st>>>(Vals<i64>{(const i64 *)values}, B, plan->value_bias, tab);
+            SAIX_LAUNCHED();
+        }
+        Prof prof_("rmq.block_levels", 12.0 * (double)level_off(B.ns, B.slevels), st);
+        for (int k = 1; k < B.slevels; k++) {
+            const i64 len = B.ns - ((i64)1 << k) + 1;
+            k_sparse_level<u32><<<grid_for(len, 256), 256, 0, st>>>(bt + level_off(B.ns, k - 1), len,
+                                                                    (i64)1 << (k - 1), bt + level_off(B.ns, k));
+            SAIX_LAUNCHED();
+        }
+        return SAIX_OK;
+    }
     i64 n = plan->n;
     int ib = plan->index_bits;
     for (int k = 0; k < plan->levels; k++) {
@@ -282,7 +475,8 @@ extern "C" int saix_sparse_query(const saix_sparse_plan *plan, const void *table
     int g = grid_for(q, 256);
     PlanDev P = dev_plan(plan);
     // 2 x int64 in, int64 out, two random table probes at one 32 B sector each
-    Prof prof_("rmq.query", 88.0 * q, st);
+    // (blocked mode: the probes are L2 hits; HBM sees the 24 B of queries)
+    Prof prof_("rmq.query", (plan->mode == SAIX_SPARSE_BLOCKED ? 24.0 : 88.0) * q, st);
     if (value_bytes == 4)
         k_sparse_query<u32><<<g, 256, 0, st>>>(P, table, Vals<u32>{(const u32 *)values}, qi, qj, q, out_index, out_value, err);
     else

@@ -45,8 +45,9 @@ class SparseTable:
         else:
             vmin, vmax = int(values.min()), int(values.max())
         plan = _lib.SparsePlan()
-        _lib.check(L.saix_sparse_plan_make(n, vmin, vmax, ctypes.byref(plan)), "saix_sparse_plan_make")
+        _lib.check(L.saix_sparse_plan_blocked(n, vmin, vmax, ctypes.byref(plan)), "saix_sparse_plan_blocked")
         self.plan = plan
+        self._vrange = (vmin, vmax)
         _lib.device()
         t = _lib.torch()
         if _device_values is not None:          # (tensor, value_bytes) already on device
@@ -64,17 +65,32 @@ class SparseTable:
     def n(self) -> int:
         return int(self.plan.n)
 
+    def _full_table(self):
+        """(plan, device table) in the per-level layout; a blocked query table
+        (SAIX_SPARSE_BLOCKED) gets a full one built on demand."""
+        if self.plan.mode != _lib.SPARSE_BLOCKED:
+            return self.plan, self._table
+        L = _lib.load()
+        plan = _lib.SparsePlan()
+        _lib.check(L.saix_sparse_plan_make(self.n, self._vrange[0], self._vrange[1], ctypes.byref(plan)),
+                   "saix_sparse_plan_make")
+        tab = _lib.workspace(plan.table_bytes)
+        _lib.check(L.saix_sparse_build(ctypes.byref(plan), _lib.ptr(self._vals), self._vbytes, _lib.ptr(tab),
+                                       _lib.stream_ptr()), "saix_sparse_build")
+        return plan, tab
+
     @property
     def table(self) -> list[np.ndarray]:
         """The reference layout: per level, int64 argmin indices."""
         if self._table_host is None:
-            raw = self._table.cpu().numpy()
-            n, ib = self.n, self.plan.index_bits
-            mode = self.plan.mode
+            plan, tab = self._full_table()
+            raw = tab.cpu().numpy()
+            n, ib = self.n, plan.index_bits
+            mode = plan.mode
             dt = np.uint64 if mode == _lib.SPARSE_PACK64 else np.uint32
-            flat = raw[: self.plan.table_bytes].view(dt)
+            flat = raw[: plan.table_bytes].view(dt)
             levels, off = [], 0
-            for k in range(self.plan.levels):
+            for k in range(plan.levels):
                 ln = n - (1 << k) + 1
                 e = flat[off: off + ln].astype(np.uint64)
                 idx = e if mode == _lib.SPARSE_INDEX else e & np.uint64((1 << ib) - 1)
@@ -134,8 +150,9 @@ class DeviceSparseTable(SparseTable):
                    "saix_minmax")
         vmin, vmax = (int(x) for x in mm.tolist())
         plan = _lib.SparsePlan()
-        _lib.check(L.saix_sparse_plan_make(n, vmin, vmax, ctypes.byref(plan)), "saix_sparse_plan_make")
+        _lib.check(L.saix_sparse_plan_blocked(n, vmin, vmax, ctypes.byref(plan)), "saix_sparse_plan_blocked")
         self.plan = plan
+        self._vrange = (vmin, vmax)
         self._vals, self._vbytes = values_dev, value_bytes
         self._table = _lib.workspace(plan.table_bytes)
         self._err = t.zeros(1, dtype=t.int32, device=values_dev.device)

@@ -70,6 +70,7 @@ for what in "$@"; do
   case $what in
     c2nowin) SAIX_WINDOW_NAMING=0 timeout 900 python bench.py --workload c2 --no-cpu-baseline > $O/bench_c2nowin.json 2> $O/bench_c2nowin.err; tail -c 300 $O/bench_c2nowin.json ;;
     largetests) timeout 1500 python -m pytest tests/test_gpu_large.py tests/test_gpu_parity.py tests/test_gpu_batch.py -x -q > $O/largetests.log 2>&1; tail -15 $O/largetests.log ;;
+    sanitize) for tool in memcheck racecheck synccheck; do SAIX_WS_MIN_M=4096 timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 30 --kernel-name kns=k_ python tools/sanitize_run.py > $O/san_$tool.log 2>&1; echo "$tool rc=$?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|all steps|MISMATCH" $O/san_$tool.log | tail -3; done ;;
     traces) for w in c2 c3; do SAIX_TRACE=1 timeout 600 python tools/profile_once.py $( [ $w = c3 ] && echo 268435456 || echo c2 ) 2>&1 | grep "saix dc3" | sort | uniq -c > $O/trace_$w.txt; cat $O/trace_$w.txt; done ;;
   esac
 done
