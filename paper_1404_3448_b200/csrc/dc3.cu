@@ -2560,7 +2560,8 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     if (pu.stage2_items() > stage_items) stage_items = pu.stage2_items();
     const u32 cap = (u32)(m / 32 + 64);
     const size_t need = (size_t)stage_items * 16 + (SAc ? 0 : (size_t)m * 4) + (size_t)cap * 24 +
-                        (size_t)WS_FINE * 12 + ((size_t)16 << 20);
+                        ((size_t)3 * WS_FINE + 2 * WS_COARSE + scan_tmp_words(WS_FINE) + pu.cursor_words() + 32) * 4 +
+                        24 * Arena::kAlign;
     const size_t mark = ar.mark();
     if (ar.cap - mark < need) return SAIX_OK;
     u64 *SA_ = ar.alloc<u64>(stage_items), *SB = ar.alloc<u64>(stage_items);

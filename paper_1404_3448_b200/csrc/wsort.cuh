@@ -376,7 +376,9 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
                 const int s0 = (k & 1) ? (int)(wk & 0xFFFFu) : (k ? (int)(scnt[(k >> 1) - 1] >> 16) : 0);
                 int lt = 0, same_lt = 0, same = 0;
                 if (e - s0 > WS_BIG_SUB) {
+                    // the caller discards this pass; keep R a permutation
                     atomicMax(&scal[8], 1u);
+                    lt = i - s0;
                 } else if (e - s0 > 1) {
                     // same name: equal characters and flag bits, v a full window
                     const u64 vh = ((v >> 29) & 1) ? v >> 29 : ~0ull;

@@ -117,3 +117,12 @@ def test_matches_lcp_and_overlap_pipeline():
     assert _lib.dc3_naming() == 2
     lcp = sx.build_lcp(rt, ix).lcp
     assert np.array_equal(lcp, oracle.lcp(t, ix.sa, ix.rank))
+
+
+def test_homopolymer_run_in_random_text():
+    """A 4000-base A run: its windows fill one fine bucket (within P3's
+    capacity) and one sub-bucket far past WS_BIG_SUB -> the pass is
+    discarded (generic window sort), and the answer stays exact."""
+    t = _random(N0, 61)
+    t[N0 // 3:N0 // 3 + 4000] = 1
+    _check(t, naming=1)
