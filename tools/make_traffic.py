@@ -28,9 +28,14 @@ SCOPES = {
     "dc3.triple_sort": (r"^k_bs_count<(Triple|PairDense)", r"^k_bs_count<(Triple|PairDense)|^k_bs_scatter_emit<(Triple|PairDense)|^k_bs_tiny|^k_bs_small|^k_bs_window|^k_bs_large"),
     "batch.partition": (r"^k_lsd_scatter", r"^k_lsd_"),
     "pairs.dc3_onchip": (r"^k_pair_dc3", r"^k_pair_dc3"),
+    "dc3.ws_count": (r"^k_ws_count", r"^k_ws_count"),
+    "dc3.ws_part1": (r"^k_ws_part1", r"^k_ws_part1"),
+    "dc3.ws_part2": (r"^k_ws_part2", r"^k_ws_part2"),
+    "dc3.ws_sort": (r"^k_ws_sort", r"^k_ws_sort"),
+    "dc3.unique_isa": (r"^k_ps_window<uint2", r"^k_ps_window<uint2|^k_ps_refine<uint2>$"),
+    "rmq.block_pack": (r"^k_blk_pack", r"^k_blk_pack"),
     "dc3.window_sort": (r"^k_bs_count<Window", r"^k_bs_count<Window|^k_bs_scatter_emit<Window|^k_bs_tiny|^k_bs_small|^k_bs_window|^k_bs_large|^k_ws_"),
     "dc3.unique_ranks": (r"^k_unique_ranks|^k_wn_ranks", r"^k_unique_ranks|^k_wn_ranks"),
-    "dc3.unique_isa": (r"^k_unique_isa|^k_wn_isa", r"^k_unique_isa|^k_wn_isa"),
     "dc3.tie_resolve": (r"^k_tie", r"^k_tie"),
 }
 
