@@ -449,10 +449,15 @@ class C4:
         self.dc3_calls_per_step = getattr(self.ob, "dc3_calls", len(self.ob.waves))
 
     def _gather(self):
-        if self.dist is None:
+        if self.dist is None or self.world == 1:
             return
-        from paper_1404_3448_b200.distributed import gather_results
-        self.full = gather_results(self.ob.out[: 3 * self.P], self.TOTAL, self.world, self.dist)
+        from paper_1404_3448_b200.distributed import NcclComm, gather_results, gather_results_nccl
+        if self.dist.get_backend() == "nccl":   # the library's own NCCL communicator
+            if getattr(self, "comm", None) is None:
+                self.comm = NcclComm(self.dist, self.world, self.dist.get_rank())
+            self.full = gather_results_nccl(self.ob.out[: 3 * self.P], self.TOTAL, self.world, self.comm)
+        else:
+            self.full = gather_results(self.ob.out[: 3 * self.P], self.TOTAL, self.world, self.dist)
 
     def step_device(self):
         self.ob.run_device()
@@ -948,6 +953,17 @@ def bench(args, rank, world, dist):
             "roofline": m["roofline"], "dc3_roofline": m["dc3_roofline"], "cpu_baseline": cpu, "clocks": m["clocks"],
             "stage_ms_per_step": m["stage"],
         }
+        roof = m["roofline"]
+        if wl.name == "c4" and roof and roof.get("kernel") == "pairs.dc3_onchip":
+            # the pair DC3 works out of shared memory (HBM moves only its input,
+            # roofline.traffic): the same model bytes against the aggregate
+            # shared-memory bandwidth, 128 B/clk per SM at the sampled SM clock
+            mhz = (m["clocks"] or {}).get("sm_mhz") or 1965.0
+            smem_peak = 128.0 * 148 * mhz * 1e6 / 1e9
+            line["onchip_roofline"] = {"bound": "smem", "kernel": roof["kernel"], "achieved": roof["achieved"],
+                                       "peak": round(smem_peak, 1), "unit": "GB/s",
+                                       "frac": round(roof["achieved"] / smem_peak, 4),
+                                       "peak_source": f"128 B/clk/SM x 148 SMs x {mhz:.0f} MHz"}
         if getattr(wl, "parity", None):
             line["parity"] = wl.parity
         if results is not None:

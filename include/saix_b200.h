@@ -39,6 +39,7 @@ extern "C" {
 #define SAIX_ENOSPC (-28)   /* workspace smaller than *_workspace_bytes()     */
 #define SAIX_ECUDA (-100)   /* CUDA runtime error (message has the details)   */
 #define SAIX_ESEQ (-101)    /* illegal residue: reference SequenceError       */
+#define SAIX_ENCCL (-102)   /* NCCL unavailable or failed (message: details)  */
 
 SAIX_API const char *saix_last_error(void);
 SAIX_API int saix_abi_version(void);
@@ -230,6 +231,24 @@ SAIX_API int saix_lcp_query(const saix_sparse_plan *plan, const void *table,
                    const void *lcp, int lcp_bytes, const uint32_t *isa,
                    const int64_t *qi, const int64_t *qj, int64_t q,
                    int64_t *out, int32_t *err, void *stream);
+
+/* ------------------------------------------------------- multi-GPU (8e) */
+/* Batched pairs shard across ranks (one process per GPU); the per-pair
+ * results are the only exchange.  NCCL is bound at run time (libnccl.so.2,
+ * shared with the process's NCCL if already loaded).  The 128-byte id from
+ * rank 0 reaches the other ranks through the caller's bootstrap (e.g. a
+ * torch.distributed broadcast), then every rank calls saix_comm_init with
+ * its own device.  Collectives are stream-ordered on `stream`.
+ * Reference: overlap.py:110-152 (the per-pair call being sharded). */
+SAIX_API int saix_comm_unique_id(uint8_t *out128);
+SAIX_API int saix_comm_init(void **comm, int nranks, const uint8_t *id128, int rank, int device);
+SAIX_API int saix_comm_destroy(void *comm);
+/* recv (device, nranks * count int64) = every rank's send (count int64), in
+ * rank order: the padded per-shard result blocks */
+SAIX_API int saix_comm_allgather_i64(void *comm, const int64_t *send, int64_t count, int64_t *recv, void *stream);
+/* recv = elementwise MIN over ranks (the first illegal residue of the job) */
+SAIX_API int saix_comm_allreduce_min_i64(void *comm, const int64_t *send, int64_t *recv, int64_t count,
+                                         void *stream);
 
 /* --------------------------------------------------------------- overlap */
 

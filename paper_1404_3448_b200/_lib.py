@@ -26,6 +26,7 @@ SAIX_ERANGE = -34
 SAIX_ENOSPC = -28
 SAIX_ECUDA = -100
 SAIX_ESEQ = -101
+SAIX_ENCCL = -102
 
 SPARSE_PACK32, SPARSE_PACK64, SPARSE_INDEX, SPARSE_BLOCKED = 0, 1, 2, 3
 
@@ -102,6 +103,11 @@ SIGNATURES = {
     "saix_index_unpack_workspace_bytes": (_c.c_size_t, [_i64]),
     "saix_index_unpack": (_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_sparse_plan_make": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),
+    "saix_comm_unique_id": (_int, [_vp]),
+    "saix_comm_init": (_int, [_c.POINTER(_vp), _int, _vp, _int, _int]),
+    "saix_comm_destroy": (_int, [_vp]),
+    "saix_comm_allgather_i64": (_int, [_vp, _vp, _i64, _vp, _vp]),
+    "saix_comm_allreduce_min_i64": (_int, [_vp, _vp, _vp, _i64, _vp]),
     "saix_sparse_plan_blocked": (_int, [_i64, _i64, _i64, _c.POINTER(SparsePlan)]),
     "saix_sparse_build": (_int, [_c.POINTER(SparsePlan), _vp, _int, _vp, _vp]),
     "saix_sparse_query": (_int, [_c.POINTER(SparsePlan), _vp, _vp, _int, _vp, _vp, _i64,

@@ -2,8 +2,10 @@
 
 Independent pairs shard contiguously across ranks (one process per GPU);
 every rank runs its shard through ``OverlapBatch`` and the per-pair results
-(3 x int64 per pair) are all-gathered -- the only collective of the path (NCCL
-over NVLink on GPUs; any torch.distributed backend works, the tests use gloo).
+(3 x int64 per pair) are all-gathered -- the only collective of the path: on
+GPUs by NCCL inside libsaix_b200.so (``NcclComm``, saix_comm_* in the C ABI),
+torch.distributed only bootstrapping the NCCL id; the CPU tests run the same
+gather over a gloo process group (``gather_results``).
 """
 
 from __future__ import annotations
@@ -35,6 +37,73 @@ def gather_results(local, total: int, world: int, dist, group=None):
     return full.to(local.device) if host else full
 
 
+class NcclComm:
+    """This rank's NCCL communicator held by libsaix_b200.so (saix_comm_*):
+    the result all-gather and the first-error MIN all-reduce run inside the
+    library on the current stream, PyTorch supplies device buffers only.
+    ``dist`` (any torch.distributed backend) is used once, to broadcast rank
+    0's 128-byte NCCL id (the bootstrap)."""
+
+    def __init__(self, dist, world: int, rank: int, device: int | None = None, group=None):
+        import ctypes
+
+        import torch
+
+        from . import _lib
+        L = _lib.load()
+        self.world, self.rank = world, rank
+        dev = torch.cuda.current_device() if device is None else device
+        idb = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            _lib.check(L.saix_comm_unique_id(idb), "saix_comm_unique_id")
+        box = [bytes(idb)]
+        if dist is not None and world > 1:
+            dist.broadcast_object_list(box, src=0, group=group)
+        idb = (ctypes.c_uint8 * 128).from_buffer_copy(box[0])
+        self._comm = ctypes.c_void_p()
+        _lib.check(L.saix_comm_init(ctypes.byref(self._comm), world, idb, rank, dev), "saix_comm_init")
+
+    def all_gather(self, send):
+        """(world * send.numel()) int64 device tensor: every rank's block in rank order."""
+        import torch
+
+        from . import _lib
+        out = torch.empty(self.world * send.numel(), dtype=torch.int64, device=send.device)
+        _lib.check(_lib.load().saix_comm_allgather_i64(self._comm, _lib.ptr(send), send.numel(), _lib.ptr(out),
+                                                       _lib.stream_ptr()), "saix_comm_allgather_i64")
+        return out
+
+    def all_reduce_min(self, t):
+        from . import _lib
+        out = t.clone()
+        _lib.check(_lib.load().saix_comm_allreduce_min_i64(self._comm, _lib.ptr(t), _lib.ptr(out), t.numel(),
+                                                           _lib.stream_ptr()), "saix_comm_allreduce_min_i64")
+        return out
+
+    def close(self):
+        from . import _lib
+        if self._comm:
+            _lib.check(_lib.load().saix_comm_destroy(self._comm), "saix_comm_destroy")
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def gather_results_nccl(local, total: int, world: int, comm: NcclComm):
+    """gather_results over the library's NCCL communicator (device tensors)."""
+    import torch
+    counts = [hi - lo for lo, hi in (shard(total, world, r) for r in range(world))]
+    width = 3 * max(counts)
+    mine = torch.zeros(width, dtype=torch.int64, device=local.device)
+    mine[: local.numel()].copy_(local.reshape(-1))
+    allr = comm.all_gather(mine).view(world, width)
+    return torch.cat([allr[r, : 3 * c] for r, c in enumerate(counts)]).reshape(total, 3)
+
+
 class ShardedOverlapBatch:
     """This rank's shard of a batched longest-overlap job plus the gather.
 
@@ -45,11 +114,11 @@ class ShardedOverlapBatch:
     gathered, so no rank returns overlaps computed past a bad residue."""
 
     def __init__(self, seqs, offs, total: int, world: int, rank: int, dist=None, group=None,
-                 policy=None):
+                 policy=None, comm: NcclComm | None = None):
         from .overlap import OverlapBatch
         from .sequence import NPolicy
         self.total, self.world, self.rank = total, world, rank
-        self.dist, self.group = dist, group
+        self.dist, self.group, self.comm = dist, group, comm
         self.lo, self.hi = shard(total, world, rank)
         self.policy = NPolicy.REJECT if policy is None else policy
         self.batch = OverlapBatch(seqs, offs, self.policy)
@@ -68,7 +137,9 @@ class ShardedOverlapBatch:
         if pos is not None:
             si = int(np.searchsorted(b.offs, pos, side="right") - 1)  # sequence 2p or 2p+1 of the shard
             key = ((2 * self.lo + si) << 40) | (pos - int(b.offs[si]))
-        if self.dist is not None and self.world > 1:
+        if self.comm is not None and self.world > 1:
+            key = int(self.comm.all_reduce_min(torch.tensor([key], dtype=torch.int64, device=b.bad.device)).item())
+        elif self.dist is not None and self.world > 1:
             on = "cpu" if self.dist.get_backend(self.group) == "gloo" else b.bad.device
             t = torch.tensor([key], dtype=torch.int64, device=on)
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
@@ -97,6 +168,8 @@ class ShardedOverlapBatch:
         self.batch.run_device()
         self.check(seq_of)
         local = self.batch.out[: 3 * self.batch.P]
-        if self.dist is None or self.world == 1:
+        if self.world == 1:
             return local.reshape(-1, 3)
+        if self.comm is not None:
+            return gather_results_nccl(local, self.total, self.world, self.comm)
         return gather_results(local, self.total, self.world, self.dist, self.group)

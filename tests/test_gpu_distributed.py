@@ -84,3 +84,25 @@ def test_sharded_batch_reject_raises_on_every_rank():
     msgs = {m for _, kind, m in out if kind == "err"}
     assert len(msgs) == 1 and all(kind == "err" for _, kind, _ in out)
     assert "pair 33 sequence B" in msgs.pop()
+
+
+def test_library_nccl_comm_single_rank():
+    """The C-ABI collective (saix_comm_*: NCCL bound inside libsaix_b200.so)
+    on one device: id, init, all-gather, MIN all-reduce, and a world-1
+    ShardedOverlapBatch gather through it against the oracle."""
+    import torch
+
+    import oracle
+    from paper_1404_3448_b200.distributed import NcclComm, ShardedOverlapBatch, gather_results_nccl
+    from paper_1404_3448_b200.workloads import c4_pairs
+    torch.cuda.set_device(0)
+    comm = NcclComm(None, 1, 0)
+    x = torch.arange(12, dtype=torch.int64, device="cuda")
+    assert torch.equal(comm.all_gather(x), x)
+    assert torch.equal(comm.all_reduce_min(x), x)
+    assert torch.equal(gather_results_nccl(x, 4, 1, comm), x.reshape(4, 3))
+    seqs, offs = c4_pairs(0, 30)
+    job = ShardedOverlapBatch(seqs, offs, 30, 1, 0, comm=comm)
+    got = job.run().cpu().numpy()
+    assert np.array_equal(got, oracle.overlap_batch(seqs, offs))
+    comm.close()
