@@ -68,6 +68,7 @@ constexpr int RKMAX = 2 * ((NMAX + 2) / 3 + 1) + 2;  // rank slots of positions 
 constexpr int SMALL = 32;      // buckets up to this size: one thread, insertion sort
 constexpr int MAXBIG = 16;     // larger buckets per pair: whole CTA, rank counting
 constexpr u32 WORK_MAX = 1u << 16;  // per-thread word compares in the sample sort
+constexpr int LIST_CAP = 64;        // run-joining ranks walked by one thread (else block scan)
 
 __host__ __device__ constexpr int al16(int x) { return (x + 15) & ~15; }
 constexpr int OFF_T = 0;
@@ -94,6 +95,7 @@ struct Misc {
     u32 pair;
     u32 fail;
     u32 nbig;
+    u32 nlist;
     u32 big[MAXBIG][2];
     u32 red32[WARPS];
     unsigned long long red64[WARPS];
@@ -839,10 +841,57 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             if (tid == 0) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0;
             continue;
         }
-        // ---- 6b. runs of lcp >= best; smallest (min A, min B) of a run with both sides
+        // ---- 6b. runs of lcp >= best; smallest (min A, min B) of a run with both sides.
+        //          A rank r joins the run of r - 1 iff lcp(r-1, r) >= best: such
+        //          ranks are few (the planted copies, the odd best-length match),
+        //          so they are listed (in the free queue region) and one thread
+        //          walks the runs; a long list (repetitive pairs) takes the
+        //          segmented block scan below.
+        const u32 bcap = min(best, 255u);
+        {
+            u16 *LST = QW;
+            if (tid == 0) ms.nlist = 0;
+            __syncthreads();
+            for (u32 q = 0; q < ITEMS && r0 + q < n; q++) {
+                const u32 r = r0 + q;
+                if (r == 0 || LC[r] < bcap) continue;
+                if (best > 255u && !lcp_at_least(T, SA[r - 1], SA[r], best)) continue;  // saturated entry
+                const u32 at = atomicAdd(&ms.nlist, 1u);
+                if (at < (u32)LIST_CAP) LST[at] = (u16)r;
+            }
+            __syncthreads();
+            const u32 nl = ms.nlist;
+            if (nl <= (u32)LIST_CAP) {
+                if (tid == 0) {
+                    for (u32 a = 1; a < nl; a++) {  // insertion sort (tiny list)
+                        const u16 v = LST[a];
+                        u32 b = a;
+                        for (; b > 0 && LST[b - 1] > v; b--) LST[b] = LST[b - 1];
+                        LST[b] = v;
+                    }
+                    unsigned long long win = ~0ull;
+                    for (u32 a = 0; a < nl;) {
+                        u32 e = a;  // run = ranks LST[a]-1 .. LST[e] (consecutive list entries)
+                        while (e + 1 < nl && LST[e + 1] == LST[e] + 1u) e++;
+                        u32 ma = kInf, mb = kInf;
+                        for (u32 r = LST[a] - 1u; r <= (u32)LST[e]; r++) {
+                            const u32 x = SA[r];
+                            if (x < nA) ma = min(ma, x);
+                            else if (x > nA) mb = min(mb, x);
+                        }
+                        if (ma != kInf && mb != kInf) win = min(win, ((unsigned long long)ma << 32) | mb);
+                        a = e + 1;
+                    }
+                    out[3 * p] = best;
+                    out[3 * p + 1] = win == ~0ull ? 0 : (i64)(win >> 32);
+                    out[3 * p + 2] = win == ~0ull ? 0 : (i64)(win & 0xFFFFFFFFull) - (i64)nA - 1;
+                }
+                PD_MARK(10);
+                continue;
+            }
+        }
         {
             unsigned long long head = 0;  // bit q: element r0+q starts a run; bit ITEMS: element r0+ITEMS
-            const u32 bcap = min(best, 255u);
             for (u32 q = 0; q <= ITEMS && r0 + q < n; q++) {
                 const u32 r = r0 + q, l = LC[r];
                 bool h = (r == 0) || l < bcap;
