@@ -798,7 +798,43 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
         u8 *LC = reinterpret_cast<u8 *>(RK);
         const u32 r0 = tid * ITEMS;
         u32 mx = 0;
-        {
+        if (tx.packed) {
+            // 2-bit text: one 32-character word compare decides almost every
+            // pair; the word of rank r's suffix is reused as rank r+1's
+            // predecessor word
+            if (r0 < n) {
+                u32 prev = r0 ? SA[r0 - 1] : 0u;
+                u64 wp = r0 ? tx.ld32(prev) : 0ull;
+                for (u32 q = 0; q < (u32)ITEMS && r0 + q < n; q++) {
+                    const u32 cur = SA[r0 + q];
+                    const u64 wc = tx.ld32(cur);
+                    u32 l = 0;
+                    if (r0 + q) {
+                        const u32 L = min(tx.lim(prev), tx.lim(cur));
+                        u64 x = wp ^ wc;
+                        u32 h = 0;
+                        while (!x && h + 32u < L) {
+                            h += 32u;
+                            x = tx.ld32(prev + h) ^ tx.ld32(cur + h);
+                        }
+                        l = x ? min(L, h + ((u32)(__ffsll((long long)x) - 1) >> 1)) : L;
+                        const bool cross = prev != nA && cur != nA && ((prev < nA) != (cur < nA));
+                        if (cross) mx = max(mx, l);
+                    }
+                    LC[r0 + q] = (u8)min(l, 255u);
+                    prev = cur;
+                    wp = wc;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (lane_id() == 0) ms.red32[tid >> 5] = mx;
+            __syncthreads();
+            PD_MARK(9);
+            mx = 0;
+#pragma unroll
+            for (int w = 0; w < WARPS; w++) mx = max(mx, ms.red32[w]);
+        } else {
             // one 8-character word compare per step, lanes in lock step (see
             // the in-bucket sort); rank 0 has no predecessor (lcp 0)
             u32 q = 0, h = 0, prev = 0, cur = 0;
