@@ -298,6 +298,18 @@ SAIX_API int saix_overlap_batch_dev(const uint8_t *seqs, const int64_t *offs_hos
                                     const int64_t *offs_dev, int64_t npairs, int keep_n,
                                     int64_t *out, int64_t *bad, void *ws, size_t ws_bytes,
                                     void *stream);
+
+/* saix_overlap_batch over a batch still on the host: one kernel launch over
+ * all pairs while the copy engine streams seqs_host (pinned) into seqs_dev on
+ * copy_stream (cudaStreamNonBlocking, != stream) in nchunks chunks, each
+ * followed by a 4-byte count the kernel's CTAs wait on before taking a pair
+ * of that chunk -- the H2D overlaps the pairs without a launch per chunk.
+ * Results and errors as saix_overlap_batch_dev; the caller keeps seqs_host
+ * alive and unmodified until the call returns (it synchronises stream). */
+SAIX_API int saix_overlap_batch_stream(const uint8_t *seqs_dev, const uint8_t *seqs_host,
+                                       const int64_t *offs_host, const int64_t *offs_dev, int64_t npairs,
+                                       int nchunks, int keep_n, int64_t *out, int64_t *bad, void *ws,
+                                       size_t ws_bytes, void *stream, void *copy_stream);
 /* 0: route every pair through the wave-global path (A/B and tests); returns
  * the previous setting. */
 SAIX_API int saix_overlap_batch_set_onchip(int on);

@@ -121,6 +121,8 @@ SIGNATURES = {
     "saix_overlap_batch_workspace_bytes": (_c.c_size_t, [_vp, _i64]),
     "saix_overlap_batch": (_int, [_vp, _vp, _i64, _int, _vp, _vp, _vp, _c.c_size_t, _vp]),
     "saix_overlap_batch_dev": (_int, [_vp, _vp, _vp, _i64, _int, _vp, _vp, _vp, _c.c_size_t, _vp]),
+    "saix_overlap_batch_stream": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _int, _vp, _vp, _vp, _c.c_size_t, _vp,
+                                         _vp]),
     "saix_overlap_batch_set_onchip": (_int, [_int]),
     "saix_overlap_batch_last_fallbacks": (_i64, []),
     "saix_overlap_batch_phase_clocks": (_int, [_vp, _int]),

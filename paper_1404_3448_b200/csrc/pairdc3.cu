@@ -44,6 +44,7 @@
 // wave-global DC3 path of overlap.cu.  Both paths are exact, so the split
 // only moves time.
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -289,13 +290,22 @@ __device__ __forceinline__ u32 code_of(u32 c, int keep_n) {
     }
 }
 
+// global loads of the pair's ASCII: streamed batches (the copy engine is
+// still writing other parts of the buffer) read at L2 only, so no line with
+// not-yet-copied bytes can sit stale in L1 / the non-coherent path
+template <bool STREAM>
+__device__ __forceinline__ uint4 ld_seq16(const uint4 *p) { return STREAM ? __ldcg(p) : __ldg(p); }
+template <bool STREAM>
+__device__ __forceinline__ u8 ld_seq1(const u8 *p) { return STREAM ? __ldcg(p) : __ldg(p); }
+
 // T[dst + i] = code(src[i]) for i < len; returns the smallest bad i (or len)
+template <bool STREAM>
 __device__ __forceinline__ i64 load_codes(const u8 *__restrict__ src, i64 len, u8 *T, u32 dst, int keep_n) {
     i64 bad = len;
     const uintptr_t a0 = (uintptr_t)src;
     const i64 head = (i64)((16 - (a0 & 15)) & 15) < len ? (i64)((16 - (a0 & 15)) & 15) : len;
     for (i64 i = threadIdx.x; i < head; i += THREADS) {
-        u32 c = code_of(src[i], keep_n);
+        u32 c = code_of(ld_seq1<STREAM>(src + i), keep_n);
         if (!c) {
             bad = i < bad ? i : bad;
             c = 2;
@@ -305,7 +315,7 @@ __device__ __forceinline__ i64 load_codes(const u8 *__restrict__ src, i64 len, u
     const uint4 *v = reinterpret_cast<const uint4 *>(src + head);
     const i64 nv = (len - head) >> 4;
     for (i64 q = threadIdx.x; q < nv; q += THREADS) {
-        const uint4 x = __ldg(v + q);
+        const uint4 x = ld_seq16<STREAM>(v + q);
         const u32 w[4] = {x.x, x.y, x.z, x.w};
         const i64 base = head + 16 * q;
 #pragma unroll
@@ -319,7 +329,7 @@ __device__ __forceinline__ i64 load_codes(const u8 *__restrict__ src, i64 len, u
         }
     }
     for (i64 i = head + 16 * nv + threadIdx.x; i < len; i += THREADS) {
-        u32 c = code_of(src[i], keep_n);
+        u32 c = code_of(ld_seq1<STREAM>(src + i), keep_n);
         if (!c) {
             bad = i < bad ? i : bad;
             c = 2;
@@ -330,10 +340,11 @@ __device__ __forceinline__ i64 load_codes(const u8 *__restrict__ src, i64 len, u
 }
 
 // validation only (pairs that do not fit on chip)
+template <bool STREAM>
 __device__ __forceinline__ i64 check_codes(const u8 *__restrict__ src, i64 len, int keep_n) {
     i64 bad = len;
     for (i64 i = threadIdx.x; i < len; i += THREADS)
-        if (!code_of(src[i], keep_n) && i < bad) bad = i;
+        if (!code_of(ld_seq1<STREAM>(src + i), keep_n) && i < bad) bad = i;
     return bad;
 }
 
@@ -419,11 +430,14 @@ __device__ __forceinline__ Seg block_seg_exclusive(Seg v, Misc &ms) {
     return carry;
 }
 
-template <bool CLK>
+// STREAM: the batch's ASCII is still arriving (saix_overlap_batch_stream):
+// the copy engine publishes chunk c of `per` pairs by writing c + 1 to
+// *ready after its bytes; a CTA takes pair p only once ready * per > p.
+template <bool CLK, bool STREAM>
 __global__ void __launch_bounds__(THREADS, 2)
 k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int keep_n, i64 *__restrict__ out,
            i64 *__restrict__ bad, u32 *__restrict__ next_pair, u32 *__restrict__ nfb, u32 *__restrict__ fb,
-           int nmax, unsigned long long *__restrict__ clk) {
+           int nmax, unsigned long long *__restrict__ clk, const u32 *ready, u32 per) {
     extern __shared__ __align__(16) unsigned char smem[];
     u8 *T = smem + OFF_T;
     u16 *SS = reinterpret_cast<u16 *>(smem + OFF_SS);
@@ -448,6 +462,14 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             ms.pair = atomicAdd(next_pair, 1u);
             ms.fail = 0;
             ms.nbig = 0;
+            if (STREAM && ms.pair < P) {
+                for (;;) {
+                    u32 c;
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ready) : "memory");
+                    if ((u64)c * per > (u64)ms.pair) break;
+                    __nanosleep(256);
+                }
+            }
         }
         __syncthreads();
         PD_MARK(11);
@@ -461,7 +483,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
         }
         const i64 nl = la + lb + 1;
         if (nl > nmax) {  // validate here (bad offsets are relative to this call's seqs), solve elsewhere
-            i64 ba = check_codes(seqs + a0, la, keep_n), bb = check_codes(seqs + b0, lb, keep_n);
+            i64 ba = check_codes<STREAM>(seqs + a0, la, keep_n), bb = check_codes<STREAM>(seqs + b0, lb, keep_n);
             i64 mine = ba < la ? a0 + ba : (bb < lb ? b0 + bb : INT64_MAX);
             if (mine != INT64_MAX) atomicMin((unsigned long long *)bad, (unsigned long long)mine);
             if (tid == 0) fb[atomicAdd(nfb, 1u)] = (u32)p;
@@ -471,8 +493,8 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
 
         // ---- 1. text + zeroed counters
         {
-            i64 ba = load_codes(seqs + a0, la, T, 0, keep_n);
-            i64 bb = load_codes(seqs + b0, lb, T, nA + 1, keep_n);
+            i64 ba = load_codes<STREAM>(seqs + a0, la, T, 0, keep_n);
+            i64 bb = load_codes<STREAM>(seqs + b0, lb, T, nA + 1, keep_n);
             i64 mine = ba < la ? a0 + ba : (bb < lb ? b0 + bb : INT64_MAX);
             if (mine != INT64_MAX) atomicMin((unsigned long long *)bad, (unsigned long long)mine);
             if (tid == 0) T[nA] = 1;  // separator (overlap.py:25)
@@ -981,7 +1003,7 @@ __global__ void k_fb_scatter(const u32 *__restrict__ list, i64 cnt, const i64 *_
 __global__ void k_pd_init(i64 *__restrict__ out3, i64 *__restrict__ bad, u32 *__restrict__ ctr) {
     out3[0] = out3[1] = out3[2] = 0;
     *bad = INT64_MAX;
-    ctr[0] = ctr[1] = 0;
+    ctr[0] = ctr[1] = ctr[2] = 0;
 }
 
 }  // namespace pd
@@ -1090,9 +1112,55 @@ extern "C" int saix_overlap_batch(const uint8_t *seqs, const int64_t *offs_host,
     return saix_overlap_batch_dev(seqs, offs_host, nullptr, npairs, keep_n, out, bad, ws, ws_bytes, stream);
 }
 
+static int overlap_batch_run(const uint8_t *seqs, const int64_t *offs_host, const int64_t *offs_dev, int64_t npairs,
+                             int keep_n, int64_t *out, int64_t *bad, void *ws, size_t ws_bytes, void *stream,
+                             const uint8_t *host_seqs, int nchunks, void *copy_stream);
+
 extern "C" int saix_overlap_batch_dev(const uint8_t *seqs, const int64_t *offs_host, const int64_t *offs_dev,
                                       int64_t npairs, int keep_n, int64_t *out, int64_t *bad, void *ws,
                                       size_t ws_bytes, void *stream) {
+    return overlap_batch_run(seqs, offs_host, offs_dev, npairs, keep_n, out, bad, ws, ws_bytes, stream, nullptr, 0,
+                             nullptr);
+}
+
+// chunk counts 1, 2, ... as pinned host words: the flag copies behind each
+// chunk's bytes read from here (constant, so calls in flight never race)
+static const u32 *ready_values() {
+    static u32 *vals = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        if (cudaMallocHost(&vals, 4097 * sizeof(u32)) != cudaSuccess) {
+            vals = nullptr;
+            return;
+        }
+        for (u32 k = 0; k <= 4096; k++) vals[k] = k;
+    });
+    return vals;
+}
+
+extern "C" int saix_overlap_batch_stream(const uint8_t *seqs_dev, const uint8_t *seqs_host, const int64_t *offs_host,
+                                         const int64_t *offs_dev, int64_t npairs, int nchunks, int keep_n,
+                                         int64_t *out, int64_t *bad, void *ws, size_t ws_bytes, void *stream,
+                                         void *copy_stream) {
+    if (!seqs_host || nchunks < 1 || nchunks > 4096 || !copy_stream || copy_stream == stream) {
+        set_error("saix_overlap_batch_stream: invalid arguments");
+        return SAIX_EINVAL;
+    }
+    // the kernel waits on the copies: the copy stream must not be ordered
+    // behind it by the legacy default stream's implicit synchronisation
+    unsigned flags = 0;
+    SAIX_CUDA(cudaStreamGetFlags((cudaStream_t)copy_stream, &flags));
+    if (!(flags & cudaStreamNonBlocking)) {
+        set_error("saix_overlap_batch_stream: copy_stream must be created with cudaStreamNonBlocking");
+        return SAIX_EINVAL;
+    }
+    return overlap_batch_run(seqs_dev, offs_host, offs_dev, npairs, keep_n, out, bad, ws, ws_bytes, stream,
+                             seqs_host, nchunks, copy_stream);
+}
+
+static int overlap_batch_run(const uint8_t *seqs, const int64_t *offs_host, const int64_t *offs_dev, int64_t npairs,
+                             int keep_n, int64_t *out, int64_t *bad, void *ws, size_t ws_bytes, void *stream,
+                             const uint8_t *host_seqs, int nchunks, void *copy_stream) {
     if (npairs < 0 || (npairs > 0 && (!offs_host || !out)) || !bad) {
         set_error("saix_overlap_batch: invalid arguments");
         return SAIX_EINVAL;
@@ -1122,22 +1190,55 @@ extern "C" int saix_overlap_batch_dev(const uint8_t *seqs, const int64_t *offs_h
     {
         static DeviceFlags attr;
         if (attr.need()) {
-            SAIX_CUDA(cudaFuncSetAttribute(pd::k_pair_dc3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            SAIX_CUDA(cudaFuncSetAttribute(pd::k_pair_dc3<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            pd::SMEM));
-            SAIX_CUDA(cudaFuncSetAttribute(pd::k_pair_dc3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            SAIX_CUDA(cudaFuncSetAttribute(pd::k_pair_dc3<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           pd::SMEM));
+            SAIX_CUDA(cudaFuncSetAttribute(pd::k_pair_dc3<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            pd::SMEM));
             attr.set();
         }
         // C4 algorithmic bytes: 4,791,288 B per 20,001-residue pair (DC3 model + LCP + scan)
         Prof prof_("pairs.dc3_onchip", 239.56 * (double)(offs_host[2 * P] - offs_host[0]), st);
         const i64 grid = P < 2 * kNumSMs ? P : 2 * kNumSMs;
-        if (clocks_on()) {
+        if (host_seqs) {
+            // one launch over the whole batch while the copy engine streams it in:
+            // chunk c's bytes, then the count c + 1 into ctr[2] (the kernel's gate)
+            const u32 *vals = ready_values();
+            if (!vals) {
+                set_error("saix_overlap_batch_stream: pinned flag buffer");
+                return SAIX_ECUDA;
+            }
+            cudaStream_t cs = (cudaStream_t)copy_stream;
+            const i64 per = (P + nchunks - 1) / nchunks;
+            cudaEvent_t e0, e1;
+            SAIX_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+            SAIX_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+            SAIX_CUDA(cudaEventRecord(e0, st));  // ready = 0 and earlier readers of the buffer are done
+            SAIX_CUDA(cudaStreamWaitEvent(cs, e0, 0));
+            pd::k_pair_dc3<false, true><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
+                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr, w.ctr + 2,
+                (u32)per);
+            SAIX_LAUNCHED();
+            for (i64 c = 0; c * per < P; c++) {
+                const i64 a = c * per, b = (c + 1) * per < P ? (c + 1) * per : P;
+                const i64 lo = offs_host[2 * a], hi = offs_host[2 * b];
+                if (hi > lo)
+                    SAIX_CUDA(cudaMemcpyAsync((void *)(seqs + lo), host_seqs + lo, (size_t)(hi - lo),
+                                              cudaMemcpyHostToDevice, cs));
+                SAIX_CUDA(cudaMemcpyAsync(w.ctr + 2, vals + c + 1, 4, cudaMemcpyHostToDevice, cs));
+            }
+            SAIX_CUDA(cudaEventRecord(e1, cs));
+            SAIX_CUDA(cudaStreamWaitEvent(st, e1, 0));  // later work on st sees the whole batch
+            SAIX_CUDA(cudaEventDestroy(e0));
+            SAIX_CUDA(cudaEventDestroy(e1));
+        } else if (clocks_on()) {
             SAIX_CUDA(cudaMemsetAsync(w.clk, 0, sizeof(unsigned long long) * (pd::NPHASE + 2), st));
-            pd::k_pair_dc3<true><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
-                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk);
+            pd::k_pair_dc3<true, false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
+                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk, nullptr, 0);
         } else {
-            pd::k_pair_dc3<false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
-                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr);
+            pd::k_pair_dc3<false, false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
+                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr, nullptr, 0);
         }
     }
     SAIX_LAUNCHED();

@@ -276,16 +276,30 @@ class OverlapBatch:
         for k, (a, b, o, od) in enumerate(self._calls["waves"]):
             self._call(k, a, b, o, od, L, s)
 
-    def run_from_host(self, host_seqs) -> None:
+    def run_from_host(self, host_seqs, stream_chunks: int = 32) -> None:
         """Copy pinned host ASCII (a uint8 torch tensor laid out like
-        ``seqs``) to the device chunk by chunk on a copy stream and run each
-        chunk's pairs as soon as its bytes are resident."""
+        ``seqs``) to the device and run the pairs as their bytes land: one
+        kernel launch per wave whose CTAs wait on the copy engine's per-chunk
+        counts (saix_overlap_batch_stream); ``stream_chunks=0`` uses one
+        launch per chunk instead."""
         t = _lib.torch()
         L = _lib.load()
         cur = t.cuda.current_stream()
         if self._copy_stream is None:
-            self._copy_stream = t.cuda.Stream()
+            self._copy_stream = t.cuda.Stream()   # a pool stream: cudaStreamNonBlocking
         cs = self._copy_stream
+        if stream_chunks:
+            self._last = "waves"
+            base = host_seqs.data_ptr()
+            for k, (a, b, o, od) in enumerate(self._calls["waves"]):
+                lo = int(self.offs[2 * a])
+                rc = L.saix_overlap_batch_stream(_lib.ptr(self.seqs_dev) + lo, base + lo, o.ctypes.data,
+                                                 _lib.ptr(od), b - a, int(stream_chunks), self.keep_n,
+                                                 _lib.ptr(self.out) + 24 * a, _lib.ptr(self.bad) + 8 * k,
+                                                 _lib.ptr(self.ws), self.ws.numel(), cur.cuda_stream,
+                                                 cs.cuda_stream)
+                _lib.check(rc, "saix_overlap_batch_stream")
+            return
         cs.wait_stream(cur)  # the previous step's kernels are done with seqs_dev
         events = []
         with t.cuda.stream(cs):

@@ -214,10 +214,12 @@ def test_onchip_keep_n_and_reject():
     assert ob.first_bad() == first
 
 
-def test_run_from_host_chunks_match_device_run():
-    """Chunked H2D overlapped with the chunks' pairs (run_from_host) gives the
-    device-resident answers, and an illegal residue in a later chunk is
-    reported at its absolute packed offset."""
+@pytest.mark.parametrize("stream_chunks", [0, 1, 7, 32, 700])
+def test_run_from_host_chunks_match_device_run(stream_chunks):
+    """H2D overlapped with the pairs (run_from_host): one launch gated on the
+    copy engine's per-chunk counts (saix_overlap_batch_stream, 1..700
+    chunks), or one launch per chunk (0) -- the device-resident answers, and
+    an illegal residue in a later chunk reported at its absolute offset."""
     import torch
     seqs, offs = c4_pairs(0, 700)
     want = oracle.overlap_batch(seqs, offs, threads=8)
@@ -225,9 +227,9 @@ def test_run_from_host_chunks_match_device_run():
     assert len(ob.chunks) == 5
     host = torch.from_numpy(seqs.copy()).pin_memory()
     ob.seqs_dev.zero_()
-    ob.run_from_host(host)
+    ob.run_from_host(host, stream_chunks=stream_chunks)
     assert np.array_equal(ob.results(), want)
     bad_at = int(offs[2 * 650 + 1]) + 17
     host[bad_at] = ord("Q")
-    ob.run_from_host(host)
+    ob.run_from_host(host, stream_chunks=stream_chunks)
     assert ob.first_bad() == bad_at
