@@ -918,9 +918,13 @@ k_rs_gather(const u32 *__restrict__ sac, Text<u8> T, SampleLayout L, const u32 *
 // as runs.
 constexpr int M0_THREADS = 256, M0_WARPS = M0_THREADS / 32;
 constexpr int M0_ITEMS = 8;  // 256 x 8 = 2048 = 1 << RW_SHIFT
+struct RsRecSrc {  // 16 B records RS[rank]
+    const uint4 *rs;
+    __device__ __forceinline__ uint4 operator()(i64 i) const { return __ldcs(rs + i); }
+};
+template <class Src>
 __global__ void __launch_bounds__(M0_THREADS)
-k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__restrict__ offs, uint4 *__restrict__ M0,
-              u32 dmask) {
+k_mod0_window(Src rs, i64 m, i64 windows, const u32 *__restrict__ offs, uint4 *__restrict__ M0, u32 dmask) {
     extern __shared__ __align__(16) unsigned char m0_smem[];
     uint4 *sv = reinterpret_cast<uint4 *>(m0_smem);
     u32(*cnt)[256] = reinterpret_cast<u32(*)[256]>(sv + (1 << RW_SHIFT));
@@ -938,7 +942,7 @@ k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__res
         i64 i = seg + r * 32 + lane;
         pk[r] = 256u << 8;
         if (i < m) {
-            uint4 e = __ldcs(rs + i);
+            uint4 e = rs(i);
             if (e.x % 3 == 1) {
                 pos[r] = e.x;
                 nb[r] = e.y;
@@ -1009,6 +1013,112 @@ k_mod0_window(const uint4 *__restrict__ rs, i64 m, i64 windows, const u32 *__res
 }
 constexpr size_t M0_SMEM = ((size_t)16 << RW_SHIFT) + (size_t)M0_WARPS * 256 * 4;
 
+// ---- compact byte-level records (levels named by the DNA window sort)
+// The window sort leaves the samples' rank order SR (= SAc, sample indices)
+// and their first two characters CH (c0 | c1 << 4, from the window key) in
+// rank order; only the rank of the next sample (+ cprev of mod-1 samples)
+// travels through the bucketed scatter, 8 B items instead of 16 B records:
+//   NX[rank] = R(next sample) (1-based, 0 past the end) | cprev << 29
+// (cprev field 7 marks a mod-2 sample).  The record of the mod-0 and merge
+// passes ({pos, R(pos+1), R(pos+2), c0 | c1 << 8 | cprev << 16}) is rebuilt
+// from (SR, NX, CH): 9 B read per rank instead of 16.
+constexpr u32 NX_MASK = (1u << 29) - 1;
+constexpr u32 NX_MOD2 = 7u;
+struct CompactRecSrc {
+    const u32 *sr, *nx;
+    const u8 *ch;
+    u32 m1;
+    __device__ __forceinline__ uint4 operator()(i64 i) const {
+        const u32 s = __ldcs(sr + i), x = __ldcs(nx + i), c = __ldcs(ch + i);
+        const u32 r = x & NX_MASK;
+        const u32 cc = (c & 15u) | ((c >> 4) << 8);
+        if (s < m1) return make_uint4(3u * s + 1u, r, 0u, cc | ((x >> 29) << 16));
+        return make_uint4(3u * (s - m1) + 2u, 0u, r, cc);
+    }
+};
+struct CompactMergeView {
+    CompactRecSrc a;
+    i64 off;  // the padding sample (rank 0) is not a suffix
+    const uint4 *B;
+    __device__ __forceinline__ uint4 ra(i64 i) const { return a(i + off); }
+    __device__ __forceinline__ uint4 rb(i64 j) const { return B[j]; }
+};
+
+// pass A of the NX scatter: triplet j -> mod-1 sample 3j+1 and mod-2 sample 3j+2
+constexpr int NX_THREADS = 256, NX_J = 4;
+__global__ void __launch_bounds__(NX_THREADS)
+k_nx_emit(const u8 *__restrict__ t, SampleLayout L, const u32 *__restrict__ isac, PsPlan plan,
+          uint2 *__restrict__ stage) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint2 *sh_items = reinterpret_cast<uint2 *>(smem);
+    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_items + 2 * NX_THREADS * NX_J);
+    u32 *sh_base = sh_cnt + plan.a.buckets;
+    const i64 j0 = (i64)blockIdx.x * (NX_THREADS * NX_J);
+    uint2 it[2 * NX_J];
+    bool ok[2 * NX_J];
+#pragma unroll
+    for (int r = 0; r < NX_J; r++) {
+        const i64 j = j0 + r * NX_THREADS + threadIdx.x;
+        ok[2 * r] = j < L.m1;
+        ok[2 * r + 1] = j < L.m2;
+        if (ok[2 * r]) {
+            const u32 r2 = j < L.m2 ? __ldcs(isac + L.m1 + j) + 1u : 0u;
+            it[2 * r] = make_uint2(__ldcs(isac + j), r2 | ((u32)__ldg(t + 3 * j) << 29));
+        }
+        if (ok[2 * r + 1]) {
+            const u32 r4 = j + 1 < L.m1 ? __ldg(isac + j + 1) + 1u : 0u;
+            it[2 * r + 1] = make_uint2(__ldg(isac + L.m1 + j), r4 | (NX_MOD2 << 29));
+        }
+    }
+    ps_block_emit<uint2, NX_THREADS, 2 * NX_J>(it, ok, plan.a, stage, sh_items, sh_cnt, sh_base);
+}
+constexpr size_t NX_EMIT_SMEM = (size_t)2 * NX_THREADS * NX_J * 8 + 8 * PS_MAX_BUCKETS;
+
+// pass B: NX window w (2048 ranks) + its mod-1 samples per cprev digit into
+// hist[d * windows + w] (the mod-0 offsets, as k_rs_window)
+__global__ void __launch_bounds__(PS_THREADS)
+k_nx_window(const uint2 *__restrict__ stage2, PsPlan plan, u32 *__restrict__ nx, u32 *__restrict__ hist, int D1) {
+    __shared__ u32 win[1 << RW_SHIFT];
+    __shared__ u32 cnt[8];
+    const i64 w = blockIdx.x;
+    const i64 d0 = w << RW_SHIFT;
+    const i64 len = (d0 + (1 << RW_SHIFT) < plan.n_dest ? d0 + (1 << RW_SHIFT) : plan.n_dest) - d0;
+    const i64 n_in = plan.cursor2[w];
+    const uint2 *src = stage2 + d0;
+    if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
+    const bool full = n_in == len;
+    for (i64 x = threadIdx.x; x < n_in; x += PS_THREADS) {
+        const uint2 v = ld_stream(src + x);
+        if (full) win[(i64)v.x - d0] = v.y;
+        else nx[v.x] = v.y;
+    }
+    __syncthreads();
+    const i64 nc = full ? len : n_in;
+    u32 c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (i64 x0 = 0; x0 < nc; x0 += PS_THREADS) {
+        const i64 x = x0 + threadIdx.x;
+        u32 dg = NX_MOD2;
+        if (x < nc) {
+            u32 e;
+            if (full) {
+                e = win[x];
+                st_stream(nx + d0 + x, e);
+            } else {
+                e = ld_stream(src + x).y;
+            }
+            dg = e >> 29;
+        }
+#pragma unroll
+        for (int d = 0; d < 7; d++) c[d] += __popc(__ballot_sync(0xffffffffu, dg == (u32)d));
+    }
+    if (lane_id() == 0)
+#pragma unroll
+        for (int d = 0; d < 7; d++)
+            if (c[d]) atomicAdd(&cnt[d], c[d]);
+    __syncthreads();
+    for (int d = threadIdx.x; d < D1; d += PS_THREADS) hist[(i64)d * plan.windows + w] = cnt[d];
+}
+
 struct HistIn {
     const u32 *h;
     __device__ u32 operator()(i64 i) const { return h[i]; }
@@ -1029,7 +1139,8 @@ constexpr int RM_THREADS = 256, RM_ITEMS = 4, RM_TILE = RM_THREADS * RM_ITEMS;
 // inside its coarse window: ~half the probe rounds, and the probes of
 // neighbouring tiles share the window's lines.
 constexpr int RM_COARSE = 32;
-__global__ void k_merge_partition_rec(RecMergeView v, i64 na, i64 nb, i64 ntiles, u32 *__restrict__ split,
+template <class View>
+__global__ void k_merge_partition_rec(View v, i64 na, i64 nb, i64 ntiles, u32 *__restrict__ split,
                                       i64 stride, const u32 *__restrict__ coarse) {
     i64 total = na + nb;
     int lane = lane_id();
@@ -1084,9 +1195,9 @@ constexpr u32 kNoPred = 0xFFFFFFFFu;
 // Merge of record runs; MODE selects the bucketed side output:
 //   EMIT_ISA  {pos, rank}           -> ISA[pos] = rank
 //   EMIT_PHI  {pos, pos of rank-1}  -> Phi[pos]  (kNoPred at rank 0)
-template <int MODE>
+template <int MODE, class View>
 __global__ void __launch_bounds__(RM_THREADS)
-k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
+k_merge_tile_rec(View v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__restrict__ sa, PsPlan plan,
                  uint2 *__restrict__ stage, u32 *__restrict__ isa_direct) {
     // shared tile as comparison keys (merge_key_*) + positions: one 8 B key
     // pair per comparison instead of two 16 B records
@@ -1173,18 +1284,19 @@ k_merge_tile_rec(RecMergeView v, i64 na, i64 nb, const u32 *__restrict__ split, 
     }
 }
 
-template <int MODE>
-static int merge_rec_launch(RecMergeView v, i64 na, i64 nb, const u32 *split, u32 *sa, const PsPlan &plan,
+template <int MODE, class View>
+static int merge_rec_launch(View v, i64 na, i64 nb, const u32 *split, u32 *sa, const PsPlan &plan,
                             uint2 *stage, cudaStream_t st, u32 *isa_direct = nullptr) {
     static DeviceFlags attr;
     size_t smem = (size_t)RM_TILE * 24 + 8 * (size_t)PS_MAX_BUCKETS;
     if (attr.need()) {
-        SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_rec<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SAIX_CUDA(cudaFuncSetAttribute(k_merge_tile_rec<MODE, View>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
         attr.set();
     }
     size_t use = (size_t)RM_TILE * 24 + 8 * (size_t)(MODE == EMIT_NONE ? 1 : plan.a.buckets);
-    k_merge_tile_rec<MODE><<<(unsigned)ceil_div(na + nb, RM_TILE), RM_THREADS, use, st>>>(v, na, nb, split, sa, plan,
-                                                                                         stage, isa_direct);
+    k_merge_tile_rec<MODE, View><<<(unsigned)ceil_div(na + nb, RM_TILE), RM_THREADS, use, st>>>(
+        v, na, nb, split, sa, plan, stage, isa_direct);
     SAIX_LAUNCHED();
     return SAIX_OK;
 }
@@ -2548,8 +2660,16 @@ static bool ws_dna_on() {
     }();
     return v != 0;
 }
+// SAIX_COMPACT_RECORDS=0: the 16 B record path after the DNA window sort (A/B)
+static bool compact_records_on() {
+    static int v = [] {
+        const char *e = getenv("SAIX_COMPACT_RECORDS");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    return v != 0;
+}
 static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout &L, u32 *SAc, u32 *ISAc, int depth,
-                           bool &handled, bool &tried) {
+                           bool &handled, bool &tried, u8 *CH) {
     Arena &ar = *c.ar;
     cudaStream_t st = c.st;
     handled = tried = false;
@@ -2621,7 +2741,7 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
         const size_t smem = ws_sort_smem(capA, pu);
         const int per_sm = smem <= (74u << 10) ? 3 : smem <= (112u << 10) ? 2 : 1;
         k_ws_sort<<<kNumSMs * per_sm, WS_ST, smem, st>>>(SB, off, m, L.m1, capA, sorted, pu,
-                                                          reinterpret_cast<uint2 *>(SA_), rsA, rlA, cap, scal);
+                                                          reinterpret_cast<uint2 *>(SA_), rsA, rlA, cap, scal, CH, N);
         SAIX_LAUNCHED();
     }
     u32 h6[9];
@@ -2668,15 +2788,120 @@ static i64 ws_min_m() {
     }();
     return v;
 }
+static bool ws_dna_eligible(const u8 *text, i64 N, u64 sigma, const SampleLayout &L) {
+    return sigma <= 4 && N + 1 < (i64)WS_POS_MASK && L.m >= ws_min_m() && ((uintptr_t)text & 15) == 0 &&
+           ws_dna_on();
+}
+// compact: the DNA window sort named the level and wrote SAc (rank order)
+// and CH (first two characters per rank) -- the records can be compact
 static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const SampleLayout &L, u32 *SAc, u32 *ISAc,
-                       u32 *d_scal, int depth, bool &handled) {
-    if (sigma <= 4 && N + 1 < (i64)WS_POS_MASK && L.m >= ws_min_m() && ((uintptr_t)text & 15) == 0 &&
-        ws_dna_on()) {
+                       u32 *d_scal, int depth, bool &handled, u8 *CH = nullptr, bool *compact = nullptr) {
+    if (compact) *compact = false;
+    if (ws_dna_eligible(text, N, sigma, L)) {
         bool tried = false;
-        SAIX_TRY(window_rank_dna(c, text, N, L, SAc, ISAc, depth, handled, tried));
+        SAIX_TRY(window_rank_dna(c, text, N, L, SAc, ISAc, depth, handled, tried, CH));
+        if (compact) *compact = handled && SAc && CH;
         if (tried) return SAIX_OK;
     }
     return window_rank_generic(c, text, N, sigma, L, SAc, ISAc, d_scal, depth, handled);
+}
+
+// Steps 1-3 of a streaming level over compact records (levels named by the
+// DNA window sort, which left SR = SAc and CH in rank order).
+static int stream_finish_compact(Dc3Ctx &c, const u8 *text, u64 sigma, const SampleLayout &L, const u32 *SR,
+                                 const u32 *ISAc, const u8 *CH, u32 *SA, u32 *ISA, u32 *Phi, bool *phi_done) {
+    Arena &ar = *c.ar;
+    cudaStream_t st = c.st;
+    const i64 m = L.m, k = L.k;
+    const int D1 = (int)sigma + 1;
+    u32 *NX = ar.alloc<u32>(m);
+    uint4 *M0 = ar.alloc<uint4>(k);
+    SAIX_ARENA_OK(ar);
+    const size_t mark_s1 = ar.mark();
+    PsPlan pn = PsPlan::of(m, 4, (i64)4 << RW_SHIFT);
+    if (pn.windows > 1 && pn.s2 != RW_SHIFT) {
+        set_error("dc3: NX window %d != %d", pn.s2, RW_SHIFT);
+        return SAIX_EINVAL;
+    }
+    pn.set_cursors(ar.alloc<u32>(pn.cursor_words()));
+    uint2 *s1 = ar.alloc<uint2>(pn.stage1_items()), *s2 = ar.alloc<uint2>(pn.stage2_items());
+    u32 *hist = ar.alloc<u32>((i64)D1 * pn.windows + 1);
+    u32 *hscan = ar.alloc<u32>(scan_tmp_words((i64)D1 * pn.windows));
+    SAIX_ARENA_OK(ar);
+    SAIX_CUDA(cudaMemsetAsync(pn.a.cursor, 0, (size_t)pn.cursor_words() * 4, st));
+    {
+        Prof prof_("dc3.nx_emit", 12.0 * m + (double)k + 8.0 * m, st);
+        static DeviceFlags attr;
+        if (attr.need()) {
+            SAIX_CUDA(cudaFuncSetAttribute(k_nx_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NX_EMIT_SMEM));
+            attr.set();
+        }
+        const size_t smem = (size_t)2 * NX_THREADS * NX_J * 8 + 8 * (size_t)pn.a.buckets;
+        k_nx_emit<<<(unsigned)ceil_div(L.m1, (i64)NX_THREADS * NX_J), NX_THREADS, smem, st>>>(text, L, ISAc, pn, s1);
+    }
+    SAIX_LAUNCHED();
+    {
+        Prof prof_("dc3.nx_apply", 28.0 * m, st);
+        SAIX_TRY(ps_refine_launch(s1, pn, s2, st));
+        k_nx_window<<<(unsigned)pn.windows, PS_THREADS, 0, st>>>(s2, pn, NX, hist, D1);
+        SAIX_LAUNCHED();
+    }
+    SAIX_TRY(scan_transform(HistIn{hist}, StoreExcl{hist}, (i64)D1 * pn.windows, hscan, nullptr, st,
+                            "dc3.mod0_scan", 8.0 * D1 * pn.windows));
+    const CompactRecSrc src{SR, NX, CH, (u32)L.m1};
+    {
+        Prof prof_("dc3.mod0_split", 9.0 * m + 16.0 * k, st);
+        static DeviceFlags attr;
+        if (attr.need()) {
+            SAIX_CUDA(cudaFuncSetAttribute(k_mod0_window<CompactRecSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)M0_SMEM));
+            attr.set();
+        }
+        u32 dmask = 1;
+        while (dmask < (u32)D1 - 1) dmask = dmask * 2 + 1;
+        k_mod0_window<CompactRecSrc><<<(unsigned)pn.windows, M0_THREADS, M0_SMEM, st>>>(src, m, pn.windows, hist, M0,
+                                                                                        dmask);
+    }
+    SAIX_LAUNCHED();
+    ar.reset(mark_s1);
+
+    // 3: merge (the padding sample has rank 0 and is not a suffix)
+    const i64 pad = L.pad ? 1 : 0;
+    const i64 na = m - pad;
+    const CompactMergeView V{src, pad, M0};
+    const i64 total = na + k;
+    const i64 ntiles = ceil_div(total, RM_TILE);
+    u32 *split = ar.alloc<u32>(ceil_div(total, RM_TILE) + 2);
+    const bool isa_direct = ISA && total < 2 * kDirectScatterItems;
+    const int mode = (ISA && !isa_direct) ? EMIT_ISA : (ISA ? EMIT_NONE : (Phi ? EMIT_PHI : EMIT_NONE));
+    PsPlan pm = PsPlan::of(mode == EMIT_NONE ? 1 : total, 4);
+    pm.set_cursors(ar.alloc<u32>(pm.cursor_words()));
+    uint2 *pst1 = mode == EMIT_NONE ? nullptr : ar.alloc<uint2>(pm.stage1_items());
+    uint2 *pst2 = mode == EMIT_NONE ? nullptr : ar.alloc<uint2>(pm.stage2_items());
+    SAIX_ARENA_OK(ar);
+    SAIX_CUDA(cudaMemsetAsync(pm.a.cursor, 0, (size_t)pm.cursor_words() * 4, st));
+    {
+        Prof prof_("dc3.merge_partition", 18.0 * (ntiles + 1), st);
+        const i64 nc = ceil_div(ntiles, RM_COARSE);
+        u32 *coarse = ar.alloc<u32>(nc + 2);
+        SAIX_ARENA_OK(ar);
+        k_merge_partition_rec<<<grid_for((nc + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, coarse, RM_COARSE,
+                                                                            nullptr);
+        SAIX_LAUNCHED();
+        k_merge_partition_rec<<<grid_for((ntiles + 1) * 32, 128), 128, 0, st>>>(V, na, k, ntiles, split, 1, coarse);
+    }
+    SAIX_LAUNCHED();
+    {
+        Prof prof_("dc3.merge_tile", 9.0 * na + 16.0 * k + (SA ? 4.0 * total : 0) + (mode ? 8.0 * total : 0), st);
+        if (mode == EMIT_ISA) SAIX_TRY(merge_rec_launch<EMIT_ISA>(V, na, k, split, SA, pm, pst1, st));
+        else if (mode == EMIT_PHI) SAIX_TRY(merge_rec_launch<EMIT_PHI>(V, na, k, split, SA, pm, pst1, st));
+        else SAIX_TRY(merge_rec_launch<EMIT_NONE>(V, na, k, split, SA, pm, pst1, st, isa_direct ? ISA : nullptr));
+    }
+    if (mode != EMIT_NONE)
+        SAIX_TRY(ps_finish(pst1, pst2, pm, U32Apply{mode == EMIT_ISA ? ISA : Phi}, st,
+                           mode == EMIT_ISA ? "dc3.isa_apply" : "dc3.phi_apply", 28.0 * total));
+    if (phi_done) *phi_done = mode == EMIT_PHI;
+    return SAIX_OK;
 }
 
 static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA, u32 *ISA, u32 *Phi,
@@ -2696,10 +2921,24 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
     const bool gather = N + 4 * m <= RS_GATHER_BYTES;
     u32 *SAc = gather ? ar.alloc<u32>(m) : nullptr;
     SAIX_ARENA_OK(ar);
-    bool windowed = false;
+    bool windowed = false, compact = false;
     if (depth == 0) g_naming = 0;
-    if (sigma <= 7 && m >= 4096 && window_naming_on())
-        SAIX_TRY(window_rank(c, text, N, sigma, L, SAc, ISAc, d_scal, depth, windowed));
+    if (sigma <= 7 && m >= 4096 && window_naming_on()) {
+        // the DNA window sort can also leave SAc and CH: compact records below
+        u32 *SAw = SAc;
+        u8 *CH = nullptr;
+        if (!gather && ws_dna_eligible(text, N, sigma, L) && compact_records_on()) {
+            SAw = ar.alloc<u32>(m);
+            CH = ar.alloc<u8>(m);
+            SAIX_ARENA_OK(ar);
+        }
+        SAIX_TRY(window_rank(c, text, N, sigma, L, SAw, ISAc, d_scal, depth, windowed, CH, &compact));
+        if (compact) {
+            SAIX_TRY(stream_finish_compact(c, text, sigma, L, SAw, ISAc, CH, SA, ISA, Phi, phi_done));
+            ar.reset(mark0);
+            return SAIX_OK;
+        }
+    }
     if (!windowed) SAIX_TRY(sort_samples<u8>(c, T, L, sigma, tt, SAc, ISAc, d_scal, depth, false, nullptr));
 
     // 1: sample records in rank order
@@ -2772,12 +3011,14 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
         Prof prof_("dc3.mod0_split", 16.0 * m + 16.0 * k, st);
         static DeviceFlags attr;
         if (attr.need()) {
-            SAIX_CUDA(cudaFuncSetAttribute(k_mod0_window, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M0_SMEM));
+            SAIX_CUDA(cudaFuncSetAttribute(k_mod0_window<RsRecSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)M0_SMEM));
             attr.set();
         }
         u32 dmask = 1;
         while (dmask < (u32)D1 - 1) dmask = dmask * 2 + 1;
-        k_mod0_window<<<(unsigned)pr.windows, M0_THREADS, M0_SMEM, st>>>(RS, m, pr.windows, hist, M0, dmask);
+        k_mod0_window<<<(unsigned)pr.windows, M0_THREADS, M0_SMEM, st>>>(RsRecSrc{RS}, m, pr.windows, hist, M0,
+                                                                         dmask);
     }
     SAIX_LAUNCHED();
     ar.reset(mark_s1);  // stage2, histogram and scan temps are dead

@@ -288,13 +288,14 @@ __device__ __forceinline__ u32 ws_sub(u64 r) { return (u32)(r >> WS_SUB_SHIFT) &
 __global__ void __launch_bounds__(WS_ST, 3)
 k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i64 m1, int capA,
           u32 *__restrict__ sorted, PsPlan plan, uint2 *__restrict__ stage1, u32 *__restrict__ rs,
-          u32 *__restrict__ rl, u32 cap_runs, u32 *__restrict__ scal) {
+          u32 *__restrict__ rl, u32 cap_runs, u32 *__restrict__ scal, u8 *__restrict__ ch, i64 N) {
     extern __shared__ __align__(16) unsigned char ws_smem[];
     u64 *IN = reinterpret_cast<u64 *>(ws_smem);
     u64 *S = IN + capA + 2;
     u32 *R = reinterpret_cast<u32 *>(S + capA);
     u32 *scnt = R + capA;  // WS_SUBS 16-bit counters, two per word
     u32 *e_cnt = scnt + WS_SUBS / 2, *e_base = e_cnt + plan.a.buckets;
+    u8 *CHS = reinterpret_cast<u8 *>(e_base + plan.a.buckets);  // (c0 | c1 << 4) per rank
     __shared__ __align__(8) u64 bar;
     __shared__ u32 sh_d;
     const int tid = threadIdx.x;
@@ -406,6 +407,11 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
                 const u32 p = (u32)ws_pos(v);
                 const u32 sidx = (p % 3u == 1u) ? p / 3u : (u32)m1 + p / 3u;
                 R[rank] = sidx;
+                if (ch) {  // the first two characters (ranks; 0 past the end) from the bucket's digits
+                    const u32 c0 = (i64)p < N ? ((f >> 14) & 3u) + 1u : 0u;
+                    const u32 c1 = (i64)p + 1 < N ? ((f >> 12) & 3u) + 1u : 0u;
+                    CHS[rank] = (u8)(c0 | (c1 << 4));
+                }
                 atomicAdd(&e_cnt[sidx >> plan.a.shift], 1u);
             }
             __syncthreads();
@@ -427,6 +433,7 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
             for (int x = tid; x < L; x += WS_ST) {
                 const u32 sidx = R[x];
                 __stcs(sorted + lo + x, sidx);
+                if (ch) ch[lo + x] = CHS[x];
                 E[atomicAdd(&e_cnt[sidx >> plan.a.shift], 1u)] = make_uint2(sidx, (u32)(lo + x));
             }
             __syncthreads();
@@ -450,7 +457,8 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
     if (tid == 0 && sh_d) atomicAdd(&scal[5], sh_d);
 }
 inline size_t ws_sort_smem(int capA, const PsPlan &plan) {
-    return (size_t)(2 * capA + 2) * 8 + (size_t)capA * 4 + (size_t)WS_SUBS * 2 + 8 * (size_t)plan.a.buckets;
+    return (size_t)(2 * capA + 2) * 8 + (size_t)capA * 4 + (size_t)WS_SUBS * 2 + 8 * (size_t)plan.a.buckets +
+           (size_t)capA;
 }
 
 }  // namespace saix

@@ -34,6 +34,8 @@ SCOPES = {
     "dc3.ws_sort": (r"^k_ws_sort", r"^k_ws_sort"),
     "dc3.unique_isa": (r"^k_ps_window<uint2", r"^k_ps_window<uint2|^k_ps_refine<uint2>$"),
     "rmq.block_pack": (r"^k_blk_pack", r"^k_blk_pack"),
+    "dc3.nx_emit": (r"^k_nx_emit", r"^k_nx_emit"),
+    "dc3.nx_apply": (r"^k_nx_window", r"^k_nx_window|^k_ps_refine<uint2>$"),
     "dc3.window_sort": (r"^k_bs_count<Window", r"^k_bs_count<Window|^k_bs_scatter_emit<Window|^k_bs_tiny|^k_bs_small|^k_bs_window|^k_bs_large|^k_ws_"),
     "dc3.unique_ranks": (r"^k_unique_ranks|^k_wn_ranks", r"^k_unique_ranks|^k_wn_ranks"),
     "dc3.tie_resolve": (r"^k_tie", r"^k_tie"),
