@@ -918,9 +918,12 @@ k_rs_gather(const u32 *__restrict__ sac, Text<u8> T, SampleLayout L, const u32 *
 // as runs.
 constexpr int M0_THREADS = 256, M0_WARPS = M0_THREADS / 32;
 constexpr int M0_ITEMS = 8;  // 256 x 8 = 2048 = 1 << RW_SHIFT
-struct RsRecSrc {  // 16 B records RS[rank]
+struct RsRecSrc {  // 16 B records RS[rank]; fetch / decode split so all loads issue first
     const uint4 *rs;
-    __device__ __forceinline__ uint4 operator()(i64 i) const { return __ldcs(rs + i); }
+    using Raw = uint4;
+    __device__ __forceinline__ Raw fetch(i64 i) const { return __ldcs(rs + i); }
+    __device__ __forceinline__ uint4 decode(const Raw &e) const { return e; }
+    __device__ __forceinline__ uint4 operator()(i64 i) const { return fetch(i); }
 };
 template <class Src>
 __global__ void __launch_bounds__(M0_THREADS)
@@ -937,12 +940,18 @@ k_mod0_window(Src rs, i64 m, i64 windows, const u32 *__restrict__ offs, uint4 *_
     // per item: pos, nb, and c0 | digit << 8 | rank-in-digit << 17
     u32 pos[M0_ITEMS], nb[M0_ITEMS], pk[M0_ITEMS];
     const u32 lt = lanemask_lt();
+    typename Src::Raw raw[M0_ITEMS];
+#pragma unroll
+    for (int r = 0; r < M0_ITEMS; r++) {
+        const i64 i = seg + r * 32 + lane;
+        if (i < m) raw[r] = rs.fetch(i);
+    }
 #pragma unroll
     for (int r = 0; r < M0_ITEMS; r++) {
         i64 i = seg + r * 32 + lane;
         pk[r] = 256u << 8;
         if (i < m) {
-            uint4 e = rs(i);
+            uint4 e = rs.decode(raw[r]);
             if (e.x % 3 == 1) {
                 pos[r] = e.x;
                 nb[r] = e.y;
@@ -1028,19 +1037,32 @@ struct CompactRecSrc {
     const u32 *sr, *nx;
     const u8 *ch;
     u32 m1;
-    __device__ __forceinline__ uint4 operator()(i64 i) const {
-        const u32 s = __ldcs(sr + i), x = __ldcs(nx + i), c = __ldcs(ch + i);
+    using Raw = uint3;  // {SR, NX, CH}
+    __device__ __forceinline__ Raw fetch(i64 i) const {
+        return make_uint3(__ldcs(sr + i), __ldcs(nx + i), (u32)__ldcs(ch + i));
+    }
+    __device__ __forceinline__ uint4 decode(const Raw &w) const {
+        const u32 s = w.x, x = w.y, c = w.z;
         const u32 r = x & NX_MASK;
         const u32 cc = (c & 15u) | ((c >> 4) << 8);
         if (s < m1) return make_uint4(3u * s + 1u, r, 0u, cc | ((x >> 29) << 16));
         return make_uint4(3u * (s - m1) + 2u, 0u, r, cc);
     }
+    __device__ __forceinline__ uint4 operator()(i64 i) const { return decode(fetch(i)); }
 };
 struct CompactMergeView {
     CompactRecSrc a;
     i64 off;  // the padding sample (rank 0) is not a suffix
     const uint4 *B;
-    __device__ __forceinline__ uint4 ra(i64 i) const { return a(i + off); }
+    // cached loads: the partition's probes are random, the tile's loads contiguous
+    __device__ __forceinline__ uint4 ra(i64 i) const {
+        i += off;
+        const u32 s = __ldg(a.sr + i), x = __ldg(a.nx + i), c = __ldg(a.ch + i);
+        const u32 r = x & NX_MASK;
+        const u32 cc = (c & 15u) | ((c >> 4) << 8);
+        if (s < a.m1) return make_uint4(3u * s + 1u, r, 0u, cc | ((x >> 29) << 16));
+        return make_uint4(3u * (s - a.m1) + 2u, 0u, r, cc);
+    }
     __device__ __forceinline__ uint4 rb(i64 j) const { return B[j]; }
 };
 
@@ -1056,19 +1078,23 @@ k_nx_emit(const u8 *__restrict__ t, SampleLayout L, const u32 *__restrict__ isac
     const i64 j0 = (i64)blockIdx.x * (NX_THREADS * NX_J);
     uint2 it[2 * NX_J];
     bool ok[2 * NX_J];
+    // all loads first (the kernel is load-latency bound), then the items
+    u32 a1[NX_J], a2[NX_J], a3[NX_J], cp[NX_J];
+#pragma unroll
+    for (int r = 0; r < NX_J; r++) {
+        const i64 j = j0 + r * NX_THREADS + threadIdx.x;
+        a1[r] = j < L.m1 ? __ldcs(isac + j) : 0u;
+        a2[r] = j < L.m2 ? __ldg(isac + L.m1 + j) : 0xFFFFFFFFu;
+        a3[r] = j + 1 < L.m1 ? __ldg(isac + j + 1) : 0xFFFFFFFFu;
+        cp[r] = j < L.m1 ? (u32)__ldg(t + 3 * j) : 0u;
+    }
 #pragma unroll
     for (int r = 0; r < NX_J; r++) {
         const i64 j = j0 + r * NX_THREADS + threadIdx.x;
         ok[2 * r] = j < L.m1;
         ok[2 * r + 1] = j < L.m2;
-        if (ok[2 * r]) {
-            const u32 r2 = j < L.m2 ? __ldcs(isac + L.m1 + j) + 1u : 0u;
-            it[2 * r] = make_uint2(__ldcs(isac + j), r2 | ((u32)__ldg(t + 3 * j) << 29));
-        }
-        if (ok[2 * r + 1]) {
-            const u32 r4 = j + 1 < L.m1 ? __ldg(isac + j + 1) + 1u : 0u;
-            it[2 * r + 1] = make_uint2(__ldg(isac + L.m1 + j), r4 | (NX_MOD2 << 29));
-        }
+        it[2 * r] = make_uint2(a1[r], (a2[r] + 1u) | (cp[r] << 29));        // 0xFFFFFFFF + 1 = 0: no next
+        it[2 * r + 1] = make_uint2(a2[r], (a3[r] + 1u) | (NX_MOD2 << 29));
     }
     ps_block_emit<uint2, NX_THREADS, 2 * NX_J>(it, ok, plan.a, stage, sh_items, sh_cnt, sh_base);
 }
