@@ -258,8 +258,9 @@ k_ws_part2(const u64 *__restrict__ stageA, const u32 *__restrict__ off, const u3
         const i64 x = lo + r * WS_PT + threadIdx.x;
         ok[r] = x < hi;
         rec[r] = ok[r] ? __ldcs(stageA + x) : 0ull;
-        bk[r] = (u8)(rec[r] >> 56);
     }
+#pragma unroll
+    for (int r = 0; r < WS_PI; r++) bk[r] = (u8)(rec[r] >> 56);
     ws_block_emit(rec, bk, ok, cur_fine + c * WS_COARSE, stageB, sh_rec, sh_bk, sh_cnt, sh_start, sh_base);
 }
 
