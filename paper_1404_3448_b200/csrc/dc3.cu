@@ -2747,6 +2747,10 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
         ar.reset(mark);
         return SAIX_OK;
     }
+    if (pu.a.buckets > WS_ST) {  // P3 reserves one ISA run per coarse bucket and thread
+        ar.reset(mark);
+        return SAIX_OK;
+    }
     tried = true;
     const int capA = (int)(h[1] <= (u32)WS_CAP_MIN ? WS_CAP_MIN : ceil_div((i64)h[1], (i64)256) * 256);
     // (the largest bucket fits; emit staging reuses S)

@@ -416,18 +416,16 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
                 atomicAdd(&e_cnt[sidx >> plan.a.shift], 1u);
             }
             __syncthreads();
-            if (tid < 32) {  // run reservation per coarse ISA bucket; local starts
-                u32 carry = 0;
-                for (int q0 = 0; q0 < nq; q0 += 32) {
-                    const int q = q0 + tid;
-                    const u32 c = q < nq ? e_cnt[q] : 0u;
-                    const u32 inc = warp_inclusive_scan(c);
-                    if (q < nq) {
-                        e_base[q] = (c ? atomicAdd(&plan.a.cursor[q], c) : 0u) - (carry + inc - c);
-                        e_cnt[q] = carry + inc - c;
-                    }
-                    carry += __shfl_sync(0xffffffffu, inc, 31);
-                }
+            // run reservation per coarse ISA bucket: one atomic per bucket, all in
+            // flight at once; their results are consumed only after the staging
+            // loop, so the round trip overlaps it (nq <= WS_ST)
+            u32 base_q = 0, start_q = 0;
+            {
+                __shared__ u32 sh_w[WS_ST / 32 + 1];
+                const u32 c = tid < nq ? e_cnt[tid] : 0u;
+                if (c) base_q = atomicAdd(&plan.a.cursor[tid], c);
+                block_exclusive_scan<WS_ST>(c, start_q, sh_w);
+                if (tid < nq) e_cnt[tid] = start_q;
             }
             __syncthreads();
             uint2 *E = reinterpret_cast<uint2 *>(S);  // S is free: emit staging
@@ -437,6 +435,7 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
                 if (ch) ch[lo + x] = CHS[x];
                 E[atomicAdd(&e_cnt[sidx >> plan.a.shift], 1u)] = make_uint2(sidx, (u32)(lo + x));
             }
+            if (tid < nq) e_base[tid] = base_q - start_q;
             __syncthreads();
             // e_base[q] = q's run in its staging region minus its local start
             for (int x = tid; x < L; x += WS_ST) {
