@@ -190,6 +190,31 @@ class OverlapPipeline:
         return self.run_staged(policy)
 
 
+_PIPES: "OrderedDict[tuple, OverlapPipeline]" = None  # type: ignore[assignment]
+_PIPES_LOCK = None
+_PIPES_MAX = 4
+
+
+def _pipeline(na: int, nb: int) -> "OverlapPipeline":
+    """A reusable OverlapPipeline for this (|A|, |B|, device, thread): repeated
+    calls reuse its workspace and pinned staging buffers instead of
+    allocating them per call (small LRU)."""
+    global _PIPES, _PIPES_LOCK
+    import threading
+    from collections import OrderedDict
+    if _PIPES_LOCK is None:
+        _PIPES, _PIPES_LOCK = OrderedDict(), threading.Lock()
+    key = (na, nb, _lib.torch().cuda.current_device(), threading.get_ident())
+    with _PIPES_LOCK:
+        p = _PIPES.pop(key, None)
+        if p is None:
+            p = OverlapPipeline(na, nb)
+        _PIPES[key] = p
+        while len(_PIPES) > _PIPES_MAX:
+            _PIPES.popitem(last=False)
+    return p
+
+
 def longest_overlap(a: DnaSequence, b: DnaSequence,
                     policy: NPolicy = NPolicy.REJECT) -> OverlapResult:
     """Longest common substring of A and B via the generalized suffix array
@@ -197,7 +222,7 @@ def longest_overlap(a: DnaSequence, b: DnaSequence,
     if len(a) == 0 or len(b) == 0:
         return OverlapResult(0, 0, 0)
     ha, hb = _ascii(a), _ascii(b)
-    res = OverlapPipeline(len(ha), len(hb)).run(ha, hb, policy)
+    res = _pipeline(len(ha), len(hb)).run(ha, hb, policy)
     bad = int(res[3])
     if bad != INT64_MAX:
         if bad < len(ha):

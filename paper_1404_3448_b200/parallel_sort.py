@@ -173,24 +173,46 @@ def chunked_sort(keys, config: SortConfig | None = None) -> np.ndarray:
     return _device_sort(keys, config.total_bits)
 
 
-def _engine_key_check(text: RankedText, config: SortConfig) -> None:
+def _engine_key_check(text: RankedText, config: SortConfig, sa: SuffixArray | None = None) -> None:
     """The engine's packed-key limit (parallel_sort.py:270-279): each sorting
-    pass packs (key, lane index); a pass whose key bits + index bits, rounded
-    up to the digit width, exceeds 63 raises.  Checked over the level trace
-    of the device DC3 (triple components <= sigma per level with m samples;
-    non-sample keys <= sigma and sample ranks <= m with k items)."""
+    pass packs (key, lane index) and sizes the key by the pass's actual
+    maximum; a pass whose key bits + index bits, rounded up to the digit
+    width, exceeds 63 raises.  Level 0 uses the text's actual maxima (triple
+    keys t[1:], non-sample characters t[0::3], the largest sample rank of a
+    mod-1 sample from the suffix array); deeper levels read the device DC3's
+    level trace (names are 1..distinct of the level above)."""
     trace = _lib.dc3_trace()
     db = config.digit_bits
-    for n_l, sigma, m, _names in trace:
+
+    def check(key_max: int, items: int) -> None:
+        if items <= 0:
+            return
+        idx_bits = max(1, int(items - 1).bit_length())
+        total = max(1, int(key_max).bit_length()) + idx_bits
+        total = ((total + db - 1) // db) * db
+        if total > MAX_KEY_BITS:
+            raise ValueError("packed sort key exceeds 63 bits")
+
+    for lvl, (n_l, sigma, m, _names) in enumerate(trace):
         k = (n_l + 2) // 3
-        for key_max, items in ((sigma, m), (m, k), (sigma, k)):
-            if items <= 0:
-                continue
-            idx_bits = max(1, int(items - 1).bit_length())
-            total = max(1, int(key_max).bit_length()) + idx_bits
-            total = ((total + db - 1) // db) * db
-            if total > MAX_KEY_BITS:
-                raise ValueError("packed sort key exceeds 63 bits")
+        if lvl == 0 and sa is not None and text.n == n_l:
+            t = np.concatenate([text.ranks, np.zeros(3, np.int64)])  # zero padding
+            limit = n_l + 1 if n_l % 3 == 1 else n_l
+            smp = np.concatenate([np.arange(1, limit, 3), np.arange(2, limit, 3)])
+            for off in (2, 1, 0):  # _name_triples' keys t[s], t[s+1], t[s+2], least significant first
+                check(int(t[smp + off].max()) if smp.size else 0, m)
+            mod1 = np.arange(1, n_l, 3)
+            rank_max = 0
+            if mod1.size:  # 1-based ranks among the samples (pad sample lowest when present)
+                real = np.concatenate([mod1, np.arange(2, n_l, 3)])
+                top = int(sa.rank[mod1].max())
+                rank_max = int(np.count_nonzero(sa.rank[real] <= top)) + (1 if n_l % 3 == 1 else 0)
+            check(rank_max, k)                       # _sort_nonsamples' keys: rank_of[i+1], then t[i]
+            check(int(t[0:n_l:3].max()), k)
+        else:
+            check(sigma, m)
+            check(m, k)
+            check(sigma, k)
 
 
 def parallel_build_sa(text: RankedText, config: SortConfig | None = None) -> SuffixArray:
@@ -207,5 +229,5 @@ def parallel_build_sa(text: RankedText, config: SortConfig | None = None) -> Suf
         if L is not None:
             L.saix_dc3_set_window_naming(prev)
     if text.n > 1:
-        _engine_key_check(text, config)
+        _engine_key_check(text, config, sa)
     return sa
