@@ -202,16 +202,29 @@ k_lcp_direct_p2(Pack2Text tx, i64 n, i64 sep, const u32 *__restrict__ sa, u32 *_
     for (i64 base = (i64)blockIdx.x * 256 * LD_ILP; base < n; base += step) {
         u32 iv[LD_ILP], jv[LD_ILP];
         u64 wi[LD_ILP], wj[LD_ILP];
+        // rank r's predecessor SA[r-1] and its first text word are lane l-1's
+        // own (ranks are consecutive across a warp): one random text load per
+        // rank instead of two; lane 0 loads its predecessor itself
+        const bool lane0 = (threadIdx.x & 31) == 0;
 #pragma unroll
         for (int q = 0; q < LD_ILP; q++) {
             i64 r = base + q * 256 + threadIdx.x;
             jv[q] = r < n ? __ldcs(sa + r) : 0u;
-            iv[q] = (r > 0 && r < n) ? sa[r - 1] : 0u;
+            iv[q] = (lane0 && r > 0 && r < n) ? sa[r - 1] : 0u;
         }
 #pragma unroll
         for (int q = 0; q < LD_ILP; q++) {
-            wi[q] = load2(tx.W, iv[q]);
             wj[q] = load2(tx.W, jv[q]);
+            wi[q] = lane0 ? load2(tx.W, iv[q]) : 0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < LD_ILP; q++) {
+            const u32 up = __shfl_up_sync(0xffffffffu, jv[q], 1);
+            const u64 wup = __shfl_up_sync(0xffffffffu, wj[q], 1);
+            if (!lane0) {
+                iv[q] = up;
+                wi[q] = wup;
+            }
         }
 #pragma unroll
         for (int q = 0; q < LD_ILP; q++) {
