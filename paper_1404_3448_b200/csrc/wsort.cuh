@@ -382,11 +382,17 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
                     atomicMax(&scal[8], 1u);
                     lt = i - s0;
                 } else if (e - s0 > 1) {
-                    // same name: equal characters and flag bits, v a full window
-                    const u64 vh = ((v >> 29) & 1) ? v >> 29 : ~0ull;
+                    // a sub-bucket shares bits 63..44, so 32-bit compares decide:
+                    // hi = bits 43..12 (characters 15..21, flag, top of pos'),
+                    // lo only on equal hi; same name = equal bits 43..29 and v a
+                    // full window (flag bit 29)
+                    const u32 vhi = (u32)(v >> 12), vlo = (u32)v;
+                    const u32 vname = (vhi >> 17) & 1u ? vhi >> 17 : 0xFFFFFFFFu;
                     for (int j = s0; j < e; j++) {
                         const u64 o = S[j];
-                        const bool less = o < v, eq = (o >> 29) == vh;
+                        const u32 ohi = (u32)(o >> 12), olo = (u32)o;
+                        const bool less = ohi < vhi || (ohi == vhi && olo < vlo);
+                        const bool eq = (ohi >> 17) == vname;
                         lt += less;
                         same_lt += less && eq;
                         same += eq;
