@@ -318,14 +318,24 @@ __device__ __forceinline__ i64 load_codes(const u8 *__restrict__ src, i64 len, u
         const uint4 x = ld_seq16<STREAM>(v + q);
         const u32 w[4] = {x.x, x.y, x.z, x.w};
         const i64 base = head + 16 * q;
+        // SWAR: bits 3..1 of A C T G N are 0 1 2 3 7 -- a byte permute maps
+        // them to the codes and to the letter each index must be; bytes that
+        // are not that letter are illegal (code 2 stands in, as below)
+        const u32 codes_lo = 0x04050302u, codes_hi = keep_n ? 0x06000000u : 0u;
+        const u32 lets_lo = 0x47544341u, lets_hi = keep_n ? 0x4E000000u : 0u;
 #pragma unroll
-        for (int k = 0; k < 16; k++) {
-            u32 c = code_of((w[k >> 2] >> (8 * (k & 3))) & 0xFFu, keep_n);
-            if (!c) {
-                bad = base + k < bad ? base + k : bad;
-                c = 2;
+        for (int k = 0; k < 4; k++) {
+            const u32 ix = (w[k] >> 1) & 0x07070707u;
+            const u32 sel = (ix & 7u) | ((ix >> 4) & 0x70u) | ((ix >> 8) & 0x700u) | ((ix >> 12) & 0x7000u);
+            const u32 want = __byte_perm(lets_lo, lets_hi, sel);
+            const u32 ok = __vcmpeq4(w[k], want) & ~__vcmpeq4(want, 0u);
+            u32 c = (__byte_perm(codes_lo, codes_hi, sel) & ok) | (0x02020202u & ~ok);
+            if (ok != 0xFFFFFFFFu) {
+                const i64 at = base + 4 * k + ((__ffs(~ok) - 1) >> 3);
+                bad = at < bad ? at : bad;
             }
-            T[dst + base + k] = (u8)c;
+#pragma unroll
+            for (int y = 0; y < 4; y++) T[dst + base + 4 * k + y] = (u8)(c >> (8 * y));
         }
     }
     for (i64 i = head + 16 * nv + threadIdx.x; i < len; i += THREADS) {
