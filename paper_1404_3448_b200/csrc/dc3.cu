@@ -2712,8 +2712,17 @@ static bool compact_records_on() {
     }();
     return v != 0;
 }
-static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout &L, u32 *SAc, u32 *ISAc, int depth,
-                           bool &handled, bool &tried, u8 *CH) {
+template <bool SEP>
+static int ws_sort_attrs() {
+    SAIX_CUDA(cudaFuncSetAttribute(k_ws_sort<0, SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 << 10));
+    SAIX_CUDA(cudaFuncSetAttribute(k_ws_sort<2, SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 << 10));
+    SAIX_CUDA(cudaFuncSetAttribute(k_ws_sort<4, SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 << 10));
+    SAIX_CUDA(cudaFuncSetAttribute(k_ws_sort<6, SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 << 10));
+    SAIX_CUDA(cudaFuncSetAttribute(k_ws_sort<8, SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 << 10));
+    return SAIX_OK;
+}
+static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout &L, const WsAlpha &A, u32 *SAc,
+                           u32 *ISAc, int depth, bool &handled, bool &tried, u8 *CH) {
     Arena &ar = *c.ar;
     cudaStream_t st = c.st;
     handled = tried = false;
@@ -2741,26 +2750,47 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     const i64 ntiles = ceil_div(N + 1, (i64)WS_TP);
     static DeviceFlags attr;
     if (attr.need()) {
-        SAIX_CUDA(cudaFuncSetAttribute(k_ws_count, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_FINE * 2));
-        SAIX_CUDA(cudaFuncSetAttribute(k_ws_part1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_P2_SMEM));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_FINE * 2));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_FINE * 2));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_part1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)WS_P2_SMEM));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_part1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)WS_P2_SMEM));
         SAIX_CUDA(cudaFuncSetAttribute(k_ws_part2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_P2_SMEM));
-        SAIX_CUDA(cudaFuncSetAttribute(k_ws_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 << 10));
+        SAIX_TRY(ws_sort_attrs<false>());
+        SAIX_TRY(ws_sort_attrs<true>());
         attr.set();
     }
     SAIX_CUDA(cudaMemsetAsync(hist, 0, (size_t)WS_FINE * 4, st));
     SAIX_CUDA(cudaMemsetAsync(scal, 0, 16 * 4, st));
     {
         Prof prof_("dc3.ws_count", (double)N, st);
-        k_ws_count<<<kNumSMs, 1024, WS_FINE * 2, st>>>(text, L, ntiles, hist, scal + 6);
+        if (A.sep >= 0) k_ws_count<true><<<kNumSMs, 1024, WS_FINE * 2, st>>>(text, L, A, ntiles, hist, scal + 6);
+        else k_ws_count<false><<<kNumSMs, 1024, WS_FINE * 2, st>>>(text, L, A, ntiles, hist, scal + 6);
         SAIX_LAUNCHED();
     }
     SAIX_TRY(scan_transform(WsHistIn{hist}, WsOffOut{off, curF, curC, scal + 7}, WS_FINE, tmp, off + WS_FINE, st,
                             "dc3.ws_scan", 16.0 * WS_FINE));
     k_ws_tiles<<<1, WS_COARSE, 0, st>>>(off, m, tstart);
     SAIX_LAUNCHED();
-    u32 h[2];
-    SAIX_CUDA(cudaMemcpyAsync(h, scal + 6, 8, cudaMemcpyDeviceToHost, st));
+    // P3 unit: 2^G fine buckets -- ~3 k records on average, or fewer
+    // buckets per unit where a skewed text makes some unit too large
+    const i64 mean = m >> 16;
+    const int Gmean = mean >= 1024 ? 0 : mean >= 256 ? 2 : mean >= 64 ? 4 : mean >= 16 ? 6 : 8;
+    for (int g = 0; g <= Gmean; g += 2) {
+        k_ws_unit_max<<<(WS_FINE >> g) / 256 + 1, 256, 0, st>>>(off, m, g, scal + 9 + g / 2);
+        SAIX_LAUNCHED();
+    }
+    u32 h[8];
+    SAIX_CUDA(cudaMemcpyAsync(h, scal + 6, 32, cudaMemcpyDeviceToHost, st));
     SAIX_CUDA(cudaStreamSynchronize(st));
+    int G = 0;
+    for (int g = Gmean; g > 0; g -= 2)
+        if (h[3 + g / 2] <= (u32)WS_CAP_MAX) {
+            G = g;
+            break;
+        }
+    h[1] = h[3 + G / 2];  // the largest unit bounds P3's shared buffers
     if (h[0] || h[1] > (u32)WS_CAP_MAX) {  // skewed text: the generic window sort
         ar.reset(mark);
         return SAIX_OK;
@@ -2774,7 +2804,8 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     // (the largest bucket fits; emit staging reuses S)
     {
         Prof prof_("dc3.ws_part1", (double)N + 8.0 * m, st);
-        k_ws_part1<<<(unsigned)ntiles, WS_PT, WS_P2_SMEM, st>>>(text, L, curC, SA_);
+        if (A.sep >= 0) k_ws_part1<true><<<(unsigned)ntiles, WS_PT, WS_P2_SMEM, st>>>(text, L, A, curC, SA_);
+        else k_ws_part1<false><<<(unsigned)ntiles, WS_PT, WS_P2_SMEM, st>>>(text, L, A, curC, SA_);
         SAIX_LAUNCHED();
     }
     {
@@ -2786,10 +2817,23 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     SAIX_CUDA(cudaMemsetAsync(pu.a.cursor, 0, (size_t)pu.cursor_words() * 4, st));
     {
         Prof prof_("dc3.ws_sort", 8.0 * m + 4.0 * m + 8.0 * m, st);
-        const size_t smem = ws_sort_smem(capA, pu);
+        const size_t smem = ws_sort_smem(capA, pu, 4096);
         const int per_sm = smem <= (74u << 10) ? 3 : smem <= (112u << 10) ? 2 : 1;
-        k_ws_sort<<<kNumSMs * per_sm, WS_ST, smem, st>>>(SB, off, m, L.m1, capA, sorted, pu,
-                                                          reinterpret_cast<uint2 *>(SA_), rsA, rlA, cap, scal, CH, N);
+        const unsigned grid = (unsigned)(kNumSMs * per_sm);
+        uint2 *st1 = reinterpret_cast<uint2 *>(SA_);
+#define WS_SORT_G(g)                                                                                            \
+    (A.sep >= 0 ? k_ws_sort<g, true><<<grid, WS_ST, smem, st>>>(SB, off, m, L.m1, capA, sorted, pu, st1, rsA, rlA,  \
+                                                                cap, scal, CH, N, A)                               \
+                : k_ws_sort<g, false><<<grid, WS_ST, smem, st>>>(SB, off, m, L.m1, capA, sorted, pu, st1, rsA, rlA, \
+                                                                 cap, scal, CH, N, A))
+        switch (G) {
+            case 0: WS_SORT_G(0); break;
+            case 2: WS_SORT_G(2); break;
+            case 4: WS_SORT_G(4); break;
+            case 6: WS_SORT_G(6); break;
+            default: WS_SORT_G(8); break;
+        }
+#undef WS_SORT_G
         SAIX_LAUNCHED();
     }
     u32 h6[9];
@@ -2816,7 +2860,7 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
         handled = true;
         if (depth == 0) g_naming = 2;
         if ((size_t)depth >= g_trace.size()) g_trace.resize((size_t)depth + 1);
-        g_trace[(size_t)depth] = LevelRec{L.n, 4, m, (i64)D};
+        g_trace[(size_t)depth] = LevelRec{L.n, A.lo == 2 ? 5 : 4, m, (i64)D};
         g_trace.resize((size_t)depth + 1);
         if (trace_on())
             fprintf(stderr, "[saix dc3] depth %d: N=%lld text=u8 sigma<=4 m=%lld names=%u naming=window21/msd%s\n",
@@ -2837,17 +2881,66 @@ static i64 ws_min_m() {
     return v;
 }
 static bool ws_dna_eligible(const u8 *text, i64 N, u64 sigma, const SampleLayout &L) {
-    return sigma <= 4 && N + 1 < (i64)WS_POS_MASK && L.m >= ws_min_m() && ((uintptr_t)text & 15) == 0 &&
-           ws_dna_on();
+    return (sigma <= 4 || sigma == 5) && N + 1 < (i64)WS_POS_MASK && L.m >= ws_min_m() &&
+           ((uintptr_t)text & 15) == 0 && ws_dna_on();
+}
+// sigma 5: the DNA window sort applies when rank 1 occurs exactly once (the
+// generalized text's separator); out[0] = count, out[1] = first position
+__global__ void k_ws_find_sep(const u8 *__restrict__ t, i64 N, unsigned long long *__restrict__ out) {
+    u32 c = 0;
+    unsigned long long first = ~0ull;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (i64)gridDim.x * blockDim.x)
+        if (t[i] == 1) {
+            c++;
+            first = first < (unsigned long long)i ? first : (unsigned long long)i;
+        }
+    for (int o = 16; o; o >>= 1) {
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, first, o);
+        first = y < first ? y : first;
+    }
+    if (lane_id() == 0 && c) {
+        atomicAdd(&out[0], (unsigned long long)c);
+        atomicMin(&out[1], first);
+    }
+}
+__global__ void k_ws_sep_init(unsigned long long *out) {
+    out[0] = 0;
+    out[1] = ~0ull;
+}
+static int ws_alpha(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, WsAlpha &A, bool &ok) {
+    ok = true;
+    A = WsAlpha{1u, -1};
+    if (sigma <= 4) return SAIX_OK;
+    ok = false;
+    if (sigma != 5) return SAIX_OK;
+    Arena &ar = *c.ar;
+    const size_t mark = ar.mark();
+    unsigned long long *d = ar.alloc<unsigned long long>(2);
+    SAIX_ARENA_OK(ar);
+    k_ws_sep_init<<<1, 1, 0, c.st>>>(d);
+    k_ws_find_sep<<<grid_for(N, 256, kNumSMs * 4), 256, 0, c.st>>>(text, N, d);
+    SAIX_LAUNCHED();
+    unsigned long long h[2];
+    SAIX_CUDA(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, c.st));
+    SAIX_CUDA(cudaStreamSynchronize(c.st));
+    ar.reset(mark);
+    if (h[0] != 1) return SAIX_OK;
+    A = WsAlpha{2u, (i64)h[1]};
+    ok = true;
+    return SAIX_OK;
 }
 // compact: the DNA window sort named the level and wrote SAc (rank order)
 // and CH (first two characters per rank) -- the records can be compact
 static int window_rank(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, const SampleLayout &L, u32 *SAc, u32 *ISAc,
                        u32 *d_scal, int depth, bool &handled, u8 *CH = nullptr, bool *compact = nullptr) {
     if (compact) *compact = false;
-    if (ws_dna_eligible(text, N, sigma, L)) {
+    WsAlpha A;
+    bool alpha_ok = false;
+    if (ws_dna_eligible(text, N, sigma, L)) SAIX_TRY(ws_alpha(c, text, N, sigma, A, alpha_ok));
+    if (alpha_ok) {
         bool tried = false;
-        SAIX_TRY(window_rank_dna(c, text, N, L, SAc, ISAc, depth, handled, tried, CH));
+        SAIX_TRY(window_rank_dna(c, text, N, L, A, SAc, ISAc, depth, handled, tried, CH));
         if (compact) *compact = handled && SAc && CH;
         if (tried) return SAIX_OK;
     }

@@ -44,7 +44,6 @@ constexpr int WS_FINE = 1 << 16;          // fine buckets: 8 leading characters
 constexpr int WS_COARSE = 256;            // coarse regions: 4 leading characters
 constexpr int WS_POS_BITS = 29;
 constexpr u64 WS_POS_MASK = (1ull << WS_POS_BITS) - 1;
-constexpr int WS_SUBS = 4096;             // P3 split: the next 12 bits (characters 9..14)
 constexpr int WS_PT = 512;                // P2 threads
 constexpr int WS_PI = 16;                 // P2 items per thread
 constexpr int WS_PTILE = WS_PT * WS_PI;   // 8192 records
@@ -53,20 +52,31 @@ constexpr int WS_CAP_MIN = 1024;
 constexpr int WS_CAP_MAX = 10240;         // largest fine bucket P3 takes (shared memory <= 227 KB)
 constexpr int WS_MAX_RUN = 4096;          // longest tied run handed to resolve_ties
 
-// 16 ranks (bytes 1..4) -> one 32-bit word of 2-bit digits, first at the top
-__device__ __forceinline__ u32 ws_pack4(u32 x) {
-    const u32 r = __byte_perm(x - 0x01010101u, 0, 0x0123) & 0x03030303u;
+// The text's alphabet: residues lo..lo+3 are the 2-bit digits 0..3; with
+// sep >= 0, position sep holds the one rank below them (the generalized
+// text's separator, overlap.py:25) and, like the end, stops every window
+// that reaches it (its digits from there on are 0, the flag says "stopped").
+struct WsAlpha {
+    u32 lo;   // 1: DNA ranks 1..4; 2: generalized text (separator 1, residues 2..5)
+    i64 sep;  // position of the unique separator, or -1
+};
+
+// 16 ranks -> one 32-bit word of 2-bit digits, first at the top (saturating:
+// the separator's rank lo-1 packs as digit 0; its windows are masked anyway)
+__device__ __forceinline__ u32 ws_pack4(u32 x, u32 lo4) {
+    const u32 r = __byte_perm(__vsubus4(x, lo4), 0, 0x0123) & 0x03030303u;
     const u32 pp = r | (r >> 6);
     return ((pp >> 12) & 0xF0u) | (pp & 0xFu);
 }
-__device__ __forceinline__ u32 ws_pack16(uint4 v) {
-    return (ws_pack4(v.x) << 24) | (ws_pack4(v.y) << 16) | (ws_pack4(v.z) << 8) | ws_pack4(v.w);
+__device__ __forceinline__ u32 ws_pack16(uint4 v, u32 lo4) {
+    return (ws_pack4(v.x, lo4) << 24) | (ws_pack4(v.y, lo4) << 16) | (ws_pack4(v.z, lo4) << 8) | ws_pack4(v.w, lo4);
 }
 
 // stage positions [p0, p0 + WS_TP + 32) as packed words; past the end reads
 // as digit 0 (the flag tells end windows apart)
 __device__ __forceinline__ void ws_stage(const u8 *__restrict__ t, i64 N, i64 p0, u32 *__restrict__ W,
-                                         int nthreads) {
+                                         int nthreads, u32 lo) {
+    const u32 lo4 = lo * 0x01010101u;
     for (int w = threadIdx.x; w < WS_WORDS; w += nthreads) {
         const i64 q = p0 + 16 * (i64)w;
         uint4 v;
@@ -80,13 +90,13 @@ __device__ __forceinline__ void ws_stage(const u8 *__restrict__ t, i64 N, i64 p0
 #pragma unroll
                 for (int b = 0; b < 4; b++) {
                     const i64 at = q + 4 * k + b;
-                    word |= (at < N ? (u32)t[at] : 1u) << (8 * b);
+                    word |= (at < N ? (u32)t[at] : lo) << (8 * b);
                 }
                 x[k] = word;
             }
             v = make_uint4(x[0], x[1], x[2], x[3]);
         }
-        W[w] = ws_pack16(v);
+        W[w] = ws_pack16(v, lo4);
     }
 }
 
@@ -102,17 +112,46 @@ __device__ __forceinline__ u64 ws_key(const u32 *__restrict__ W, int o) {
 // local sample q of a tile: position, validity
 __device__ __forceinline__ int ws_off(int q) { return 3 * (q >> 1) + 1 + (q & 1); }
 __device__ __forceinline__ bool ws_valid(i64 p, const SampleLayout &L) { return p < L.n || (p == L.n && L.pad); }
-__device__ __forceinline__ u64 ws_rec(u64 key, i64 p, i64 N) {
-    const u64 flag = (p + 21 <= N) ? 1ull : 0ull;
-    return ((key & ((1ull << 34) - 1)) << 30) | (flag << 29) | (WS_POS_MASK - (u64)p);
+// A window that reaches the separator keeps only its characters before it.
+template <bool SEP>
+__device__ __forceinline__ u64 ws_mask_sep(u64 key, i64 p, const WsAlpha &A) {
+    if (SEP && A.sep >= p && A.sep < p + 21) {
+        const int keep = (int)(A.sep - p);  // characters before the separator
+        key &= ~((1ull << (42 - 2 * keep)) - 1);
+    }
+    return key;
 }
-__device__ __forceinline__ i64 ws_pos(u64 rec) { return (i64)(WS_POS_MASK - (rec & WS_POS_MASK)); }
+// Low 29 bits: full window -> 2^29-1-pos (any order among equal names);
+// stopped window -> (distance to its stop) << 1 | stop kind (end 0,
+// separator 1): equal 0-filled keys order by the nearer stop, the end
+// before the separator -- the suffix order (pad 0 < separator < residues),
+// and the position follows from (distance, kind).
+template <bool SEP>
+__device__ __forceinline__ u64 ws_rec(u64 key, i64 p, i64 N, const WsAlpha &A) {
+    u64 low;
+    u64 flag = 0;
+    if (SEP && A.sep >= p && A.sep < p + 21) low = ((u64)(A.sep - p) << 1) | 1ull;
+    else if (p + 21 > N) low = (u64)(N - p) << 1;
+    else {
+        flag = 1;
+        low = WS_POS_MASK - (u64)p;
+    }
+    return ((key & ((1ull << 34) - 1)) << 30) | (flag << 29) | low;
+}
+template <bool SEP>
+__device__ __forceinline__ i64 ws_pos(u64 rec, i64 N, const WsAlpha &A) {
+    const u64 low = rec & WS_POS_MASK;
+    if ((rec >> 29) & 1) return (i64)(WS_POS_MASK - low);
+    return (SEP && (low & 1)) ? A.sep - (i64)(low >> 1) : N - (i64)(low >> 1);
+}
 // equal names: same 21 characters and both full windows
 __device__ __forceinline__ bool ws_same(u64 a, u64 b) { return ((a ^ b) >> 29) == 0 && ((a >> 29) & 1); }
 
 // ---------------------------------------------------------------- P1
+template <bool SEP>
 __global__ void __launch_bounds__(1024, 1)
-k_ws_count(const u8 *__restrict__ t, SampleLayout L, i64 ntiles, u32 *__restrict__ hist, u32 *__restrict__ overflow) {
+k_ws_count(const u8 *__restrict__ t, SampleLayout L, WsAlpha A, i64 ntiles, u32 *__restrict__ hist,
+           u32 *__restrict__ overflow) {
     extern __shared__ __align__(16) u32 ws_h16[];  // WS_FINE 16-bit counters, two per word
     __shared__ u32 W[WS_WORDS];
     for (int i = threadIdx.x; i < WS_FINE / 2; i += 1024) ws_h16[i] = 0;
@@ -120,13 +159,13 @@ k_ws_count(const u8 *__restrict__ t, SampleLayout L, i64 ntiles, u32 *__restrict
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 p0 = tile * WS_TP;
         __syncthreads();
-        ws_stage(t, L.n, p0, W, 1024);
+        ws_stage(t, L.n, p0, W, 1024, A.lo);
         __syncthreads();
 #pragma unroll 4
         for (int q = threadIdx.x; q < WS_TS; q += 1024) {
             const int o = ws_off(q);
             if (!ws_valid(p0 + o, L)) continue;
-            const u32 f = (u32)(ws_key(W, o) >> 26);
+            const u32 f = (u32)(ws_mask_sep<SEP>(ws_key(W, o), p0 + o, A) >> 26);
             const int sh = 16 * (f & 1);
             const u32 old = atomicAdd(&ws_h16[f >> 1], 1u << sh);
             ovf |= ((old >> sh) & 0xFFFFu) == 0xFFFFu;
@@ -170,6 +209,21 @@ __global__ void __launch_bounds__(WS_COARSE) k_ws_tiles(const u32 *__restrict__ 
     if (c == 0) tstart[WS_COARSE] = tot;
 }
 
+// largest P3 unit (2^G consecutive fine buckets)
+__global__ void k_ws_unit_max(const u32 *__restrict__ off, i64 m, int G, u32 *__restrict__ out) {
+    const u32 units = WS_FINE >> G;
+    u32 mx = 0;
+    for (u32 u = blockIdx.x * blockDim.x + threadIdx.x; u < units; u += gridDim.x * blockDim.x) {
+        const i64 lo = off[u << G], hi = u + 1 < units ? (i64)off[(u + 1) << G] : m;
+        mx = (u32)(hi - lo) > mx ? (u32)(hi - lo) : mx;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const u32 y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if (lane_id() == 0 && mx) atomicMax(out, mx);
+}
+
 // Block-level bucketed write of WS_PT*WS_PI records into runs reserved on
 // absolute cursors: item r goes to bucket bk[r] (< 256), cursor cur[bk].
 __device__ __forceinline__ void ws_block_emit(const u64 (&rec)[WS_PI], const u8 (&bk)[WS_PI], const bool (&ok)[WS_PI],
@@ -208,15 +262,17 @@ __device__ __forceinline__ void ws_block_emit(const u64 (&rec)[WS_PI], const u8 
 constexpr size_t WS_P2_SMEM = (size_t)WS_PTILE * 9 + 3 * 256 * 4;
 
 // ---------------------------------------------------------------- P2a
+template <bool SEP>
 __global__ void __launch_bounds__(WS_PT, 2)
-k_ws_part1(const u8 *__restrict__ t, SampleLayout L, u32 *__restrict__ cur_coarse, u64 *__restrict__ stageA) {
+k_ws_part1(const u8 *__restrict__ t, SampleLayout L, WsAlpha A, u32 *__restrict__ cur_coarse,
+           u64 *__restrict__ stageA) {
     extern __shared__ __align__(16) unsigned char ws_smem[];
     u64 *sh_rec = reinterpret_cast<u64 *>(ws_smem);
     u8 *sh_bk = ws_smem + (size_t)WS_PTILE * 8;
     u32 *sh_cnt = reinterpret_cast<u32 *>(sh_bk + WS_PTILE), *sh_start = sh_cnt + 256, *sh_base = sh_start + 256;
     __shared__ u32 W[WS_WORDS];
     const i64 p0 = (i64)blockIdx.x * WS_TP;
-    ws_stage(t, L.n, p0, W, WS_PT);
+    ws_stage(t, L.n, p0, W, WS_PT, A.lo);
     __syncthreads();
     u64 rec[WS_PI];
     u8 bk[WS_PI];
@@ -226,8 +282,8 @@ k_ws_part1(const u8 *__restrict__ t, SampleLayout L, u32 *__restrict__ cur_coars
         const int o = ws_off(r * WS_PT + threadIdx.x);
         const i64 p = p0 + o;
         ok[r] = ws_valid(p, L);
-        const u64 key = ws_key(W, o);
-        rec[r] = ws_rec(key, p, L.n);
+        const u64 key = ws_mask_sep<SEP>(ws_key(W, o), p, A);
+        rec[r] = ws_rec<SEP>(key, p, L.n, A);
         bk[r] = (u8)(key >> 34);
     }
     ws_block_emit(rec, bk, ok, cur_coarse, stageA, sh_rec, sh_bk, sh_cnt, sh_start, sh_base);
@@ -282,20 +338,36 @@ k_ws_part2(const u64 *__restrict__ stageA, const u32 *__restrict__ off, const u3
 // set the overflow flag and the caller takes the generic window sort.
 // scal (resolve_ties layout): [2] tied runs, [4] overflow, [5] distinct names;
 // [8] a sub-bucket over WS_BIG_SUB
-constexpr int WS_SUB_SHIFT = 44;
 constexpr int WS_BIG_SUB = 256;
-__device__ __forceinline__ u32 ws_sub(u64 r) { return (u32)(r >> WS_SUB_SHIFT) & (WS_SUBS - 1); }
+// A work unit of P3 is a group of 2^G consecutive fine buckets (G = 0 at
+// C3-size levels; small levels group buckets so a unit still holds ~3 k
+// records).  Its 4096 sub-buckets are record bits SHIFT+11 .. SHIFT: the
+// group's own low G bits of characters 5..8 (bits 63..56), then the next
+// bits -- records of a unit share bits 63..SHIFT+12, so sub-bucket order is
+// suffix order and the unit's sorted order is consecutive ranks.
+template <int G>
+struct WsSub {
+    static constexpr int SUBS = 4096;
+    static constexpr int SHIFT = 44 + G;
+    static constexpr int HI = SHIFT - 32;        // u32 compare window: bits SHIFT-1 .. HI
+    static constexpr int NAME = 29 - HI;         // name bits (.. flag) inside that window
+    static constexpr u32 UNITS = WS_FINE >> G;
+    __device__ __forceinline__ static u32 of(u64 r) { return (u32)(r >> SHIFT) & (SUBS - 1); }
+};
 
+template <int G, bool SEP>
 __global__ void __launch_bounds__(WS_ST, 3)
 k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i64 m1, int capA,
           u32 *__restrict__ sorted, PsPlan plan, uint2 *__restrict__ stage1, u32 *__restrict__ rs,
-          u32 *__restrict__ rl, u32 cap_runs, u32 *__restrict__ scal, u8 *__restrict__ ch, i64 N) {
+          u32 *__restrict__ rl, u32 cap_runs, u32 *__restrict__ scal, u8 *__restrict__ ch, i64 N, WsAlpha A) {
     extern __shared__ __align__(16) unsigned char ws_smem[];
     u64 *IN = reinterpret_cast<u64 *>(ws_smem);
     u64 *S = IN + capA + 2;
     u32 *R = reinterpret_cast<u32 *>(S + capA);
-    u32 *scnt = R + capA;  // WS_SUBS 16-bit counters, two per word
-    u32 *e_cnt = scnt + WS_SUBS / 2, *e_base = e_cnt + plan.a.buckets;
+    using Sb = WsSub<G>;
+    constexpr int SUBS = Sb::SUBS;
+    u32 *scnt = R + capA;  // SUBS 16-bit counters, two per word
+    u32 *e_cnt = scnt + SUBS / 2, *e_base = e_cnt + plan.a.buckets;
     u8 *CHS = reinterpret_cast<u8 *>(e_base + plan.a.buckets);  // (c0 | c1 << 4) per rank
     __shared__ __align__(8) u64 bar;
     __shared__ u32 sh_d;
@@ -309,8 +381,8 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
     }
     __syncthreads();
     auto span = [&](u32 f, i64 &lo, int &L) {
-        lo = off[f];
-        L = (int)((f + 1 < WS_FINE ? (i64)off[f + 1] : m) - lo);
+        lo = off[f << G];
+        L = (int)((f + 1 < Sb::UNITS ? (i64)off[(f + 1) << G] : m) - lo);
     };
     auto issue = [&](i64 lo, int L) {  // one thread: the bucket's 16 B-aligned cover
         const i64 a0 = lo & ~(i64)1, a1 = (lo + L + 1) & ~(i64)1;
@@ -318,35 +390,37 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
         mbar_expect_tx(&bar, bytes);
         bulk_g2s(IN, stageB + a0, bytes, &bar);
     };
-    u32 f = blockIdx.x, parity = 0, d = 0;
+    u32 f = blockIdx.x, parity = 0, d = 0;  // f: unit (group of 2^G fine buckets)
     i64 lo = 0;
     int L = 0;
-    if (f < WS_FINE) span(f, lo, L);
-    if (tid == 0 && f < WS_FINE && L > 0) issue(lo, L);
-    for (; f < WS_FINE; f += gridDim.x) {
+    if (f < Sb::UNITS) span(f, lo, L);
+    if (tid == 0 && f < Sb::UNITS && L > 0) issue(lo, L);
+    for (; f < Sb::UNITS; f += gridDim.x) {
         const u32 fn = f + gridDim.x;
         i64 lo_n = 0;
         int L_n = 0;
-        if (fn < WS_FINE) span(fn, lo_n, L_n);
+        if (fn < Sb::UNITS) span(fn, lo_n, L_n);
         if (L > 0) {
-            for (int i = tid; i < WS_SUBS / 2; i += WS_ST) scnt[i] = 0;
+            for (int i = tid; i < SUBS / 2; i += WS_ST) scnt[i] = 0;
             for (int i = tid; i < nq; i += WS_ST) e_cnt[i] = 0;
             mbar_wait(&bar, parity);
             parity ^= 1;
             const u64 *in = IN + (lo & 1);
             __syncthreads();
             for (int x = tid; x < L; x += WS_ST) {
-                const u32 k = ws_sub(in[x]);
+                const u32 k = Sb::of(in[x]);
                 atomicAdd(&scnt[k >> 1], 1u << (16 * (k & 1)));
             }
             __syncthreads();
             {  // exclusive scan of the sub-bucket counts (16-bit pairs)
-                constexpr int PER = WS_SUBS / 2 / WS_ST;
+                constexpr int WORDS = SUBS / 2;
+                constexpr int PER = WORDS >= WS_ST ? WORDS / WS_ST : 1;
+                const bool own = tid * PER < WORDS;
                 __shared__ u32 sh_warp[WS_ST / 32 + 1];
                 u32 v[PER], sum = 0;
 #pragma unroll
                 for (int k = 0; k < PER; k++) {
-                    v[k] = scnt[tid * PER + k];
+                    v[k] = own ? scnt[tid * PER + k] : 0u;
                     sum += (v[k] & 0xFFFFu) + (v[k] >> 16);
                 }
                 u32 excl;
@@ -354,14 +428,14 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
 #pragma unroll
                 for (int k = 0; k < PER; k++) {
                     const u32 a = excl, b = excl + (v[k] & 0xFFFFu);
-                    scnt[tid * PER + k] = a | (b << 16);
+                    if (own) scnt[tid * PER + k] = a | (b << 16);
                     excl = b + (v[k] >> 16);
                 }
             }
             __syncthreads();
             for (int x = tid; x < L; x += WS_ST) {
                 const u64 r = in[x];
-                const u32 k = ws_sub(r), sh = 16 * (k & 1);
+                const u32 k = Sb::of(r), sh = 16 * (k & 1);
                 S[(atomicAdd(&scnt[k >> 1], 1u << sh) >> sh) & 0xFFFFu] = r;
             }
             __syncthreads();  // IN is free: the next bucket streams in behind the rest
@@ -372,7 +446,7 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
             // scnt[k] = end of sub-bucket k
             for (int i = tid; i < L; i += WS_ST) {
                 const u64 v = S[i];
-                const u32 k = ws_sub(v);
+                const u32 k = Sb::of(v);
                 const u32 wk = scnt[k >> 1];
                 const int e = (int)((k & 1) ? wk >> 16 : wk & 0xFFFFu);
                 const int s0 = (k & 1) ? (int)(wk & 0xFFFFu) : (k ? (int)(scnt[(k >> 1) - 1] >> 16) : 0);
@@ -386,13 +460,13 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
                     // hi = bits 43..12 (characters 15..21, flag, top of pos'),
                     // lo only on equal hi; same name = equal bits 43..29 and v a
                     // full window (flag bit 29)
-                    const u32 vhi = (u32)(v >> 12), vlo = (u32)v;
-                    const u32 vname = (vhi >> 17) & 1u ? vhi >> 17 : 0xFFFFFFFFu;
+                    const u32 vhi = (u32)(v >> Sb::HI), vlo = (u32)v;
+                    const u32 vname = (vhi >> Sb::NAME) & 1u ? vhi >> Sb::NAME : 0xFFFFFFFFu;
                     for (int j = s0; j < e; j++) {
                         const u64 o = S[j];
-                        const u32 ohi = (u32)(o >> 12), olo = (u32)o;
+                        const u32 ohi = (u32)(o >> Sb::HI), olo = (u32)o;
                         const bool less = ohi < vhi || (ohi == vhi && olo < vlo);
-                        const bool eq = (ohi >> 17) == vname;
+                        const bool eq = (ohi >> Sb::NAME) == vname;
                         lt += less;
                         same_lt += less && eq;
                         same += eq;
@@ -411,12 +485,15 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
                         }
                     }
                 }
-                const u32 p = (u32)ws_pos(v);
+                const u32 p = (u32)ws_pos<SEP>(v, N, A);
                 const u32 sidx = (p % 3u == 1u) ? p / 3u : (u32)m1 + p / 3u;
                 R[rank] = sidx;
                 if (ch) {  // the first two characters (ranks; 0 past the end) from the bucket's digits
-                    const u32 c0 = (i64)p < N ? ((f >> 14) & 3u) + 1u : 0u;
-                    const u32 c1 = (i64)p + 1 < N ? ((f >> 12) & 3u) + 1u : 0u;
+                    const u32 fb = f << G;  // its characters 1..2 (G <= 12)
+                    const u32 c0 = (i64)p >= N ? 0u : (SEP && (i64)p == A.sep) ? A.lo - 1u : ((fb >> 14) & 3u) + A.lo;
+                    const u32 c1 = (i64)p + 1 >= N   ? 0u
+                                   : (SEP && (i64)p + 1 == A.sep) ? A.lo - 1u
+                                                                   : ((fb >> 12) & 3u) + A.lo;
                     CHS[rank] = (u8)(c0 | (c1 << 4));
                 }
                 atomicAdd(&e_cnt[sidx >> plan.a.shift], 1u);
@@ -462,8 +539,8 @@ k_ws_sort(const u64 *__restrict__ stageB, const u32 *__restrict__ off, i64 m, i6
     __syncthreads();
     if (tid == 0 && sh_d) atomicAdd(&scal[5], sh_d);
 }
-inline size_t ws_sort_smem(int capA, const PsPlan &plan) {
-    return (size_t)(2 * capA + 2) * 8 + (size_t)capA * 4 + (size_t)WS_SUBS * 2 + 8 * (size_t)plan.a.buckets +
+inline size_t ws_sort_smem(int capA, const PsPlan &plan, int subs) {
+    return (size_t)(2 * capA + 2) * 8 + (size_t)capA * 4 + (size_t)subs * 2 + 8 * (size_t)plan.a.buckets +
            (size_t)capA;
 }
 

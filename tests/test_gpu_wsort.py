@@ -127,3 +127,36 @@ def test_homopolymer_run_in_random_text():
     t = _random(N0, 61)
     t[N0 // 3:N0 // 3 + 4000] = 1
     _check(t, naming=None)
+
+
+def _gsa(a, b):
+    """GeneralizedText ranks (overlap.py:83-95): A+1, separator 1, B+1."""
+    return np.concatenate([a + 1, [1], b + 1]).astype(np.uint8)
+
+
+@pytest.mark.parametrize("la", [1 << 20, 7, 40])
+def test_generalized_text_separator(la):
+    """sigma 5 with one separator (the C2 text): windows reaching the
+    separator stop there like end windows; A of 7 / 40 residues puts the
+    separator among the first windows."""
+    a = _random(la, 71)
+    b = _random(N0 - la, 72)
+    _check(_gsa(a, b), sigma=5)
+
+
+def test_generalized_text_stop_order():
+    """An end window and a separator window with equal 0-filled keys: the
+    nearer stop orders first (A ends ...CGT|, B ends ...CGTAAAAAAA)."""
+    a = _random(1 << 20, 81)
+    b = _random(N0 - (1 << 20), 82)
+    a[-3:] = [2, 3, 4]
+    b[-10:-7] = [2, 3, 4]
+    b[-7:] = 1
+    _check(_gsa(a, b), sigma=5)
+
+
+def test_sigma5_with_two_separators_leaves_the_path():
+    """Two rank-1 characters: not a single separator -> generic window sort."""
+    a = _random(N0, 91) + 1
+    a[[100, 200]] = 1
+    _check(a.astype(np.uint8), sigma=5, naming=None)
