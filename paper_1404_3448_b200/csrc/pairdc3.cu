@@ -1139,7 +1139,7 @@ static const u32 *ready_values() {
     static u32 *vals = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
-        if (cudaMallocHost(&vals, 4097 * sizeof(u32)) != cudaSuccess) {
+        if (cudaHostAlloc(&vals, 4097 * sizeof(u32), cudaHostAllocPortable) != cudaSuccess) {
             vals = nullptr;
             return;
         }

@@ -233,3 +233,26 @@ def test_run_from_host_chunks_match_device_run(stream_chunks):
     host[bad_at] = ord("Q")
     ob.run_from_host(host, stream_chunks=stream_chunks)
     assert ob.first_bad() == bad_at
+
+
+def test_stream_entry_rejects_blocking_copy_stream():
+    """saix_overlap_batch_stream refuses a copy stream the legacy default
+    stream could serialise behind the gated kernel (a deadlock otherwise):
+    no stream, the launch stream itself, or a blocking stream (the
+    per-thread default stream, handle 2)."""
+    import torch
+    from paper_1404_3448_b200 import _lib
+    seqs, offs = c4_pairs(0, 3)
+    ob = sx.OverlapBatch(seqs, offs)
+    host = torch.from_numpy(seqs.copy()).pin_memory()
+    a, b, o, od = ob._calls["waves"][0]
+    L = _lib.load()
+    cur = torch.cuda.current_stream().cuda_stream
+    for cs in (None, cur, 2):
+        rc = L.saix_overlap_batch_stream(_lib.ptr(ob.seqs_dev), host.data_ptr(), o.ctypes.data, _lib.ptr(od), b - a,
+                                         2, 0, _lib.ptr(ob.out), _lib.ptr(ob.bad), _lib.ptr(ob.ws), ob.ws.numel(),
+                                         cur, cs)
+        assert rc == _lib.SAIX_EINVAL, cs
+    assert b"NonBlocking" in L.saix_last_error()
+    ob.run_from_host(host)  # the default path still works afterwards
+    assert np.array_equal(ob.results(), oracle.overlap_batch(seqs, offs))
