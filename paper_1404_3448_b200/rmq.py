@@ -297,22 +297,6 @@ class PlusMinusOneRmq:
         tabs = tab[:ncodes * b * b].cpu().numpy().reshape(ncodes, b, b)
         self.inblock: dict[int, np.ndarray] = {int(c): tabs[c].astype(np.int64) for c in np.flatnonzero(flags)}
 
-    @staticmethod
-    def _table_for(code: int, b: int) -> np.ndarray:
-        """argmin table over the simulated walk for one step pattern (rmq.py:199-213)."""
-        walk = [0]
-        for k in range(b - 1):
-            walk.append(walk[-1] + (-1 if (code >> k) & 1 else 1))
-        table = np.zeros((b, b), dtype=np.int64)
-        for i in range(b):
-            best = i
-            table[i, i] = i
-            for j in range(i + 1, b):
-                if walk[j] < walk[best]:
-                    best = j
-                table[i, j] = best
-        return table
-
     def _inblock_query(self, blk: int, lo: int, hi: int) -> int:
         return blk * self.block + int(self.inblock[int(self.types[blk])][lo, hi])
 

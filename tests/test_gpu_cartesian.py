@@ -146,7 +146,12 @@ class TestPlusMinusOne:
             assert b == max(1, (len(arr).bit_length() - 1) // 2)
             assert len(pm.inblock) <= 2 ** max(b - 1, 0)
             for code, table in pm.inblock.items():
-                assert np.array_equal(table, rmq.PlusMinusOneRmq._table_for(code, b))
+                # the step pattern's walk (bit k set: step k goes down), then
+                # every in-block range's leftmost argmin by the scan oracle
+                walk = np.cumsum([0] + [-1 if (code >> k) & 1 else 1 for k in range(b - 1)])
+                for i in range(b):
+                    for j in range(i, b):
+                        assert int(table[i, j]) == oracle.scan_argmin(walk, i, j), (code, i, j)
             for blk in range(len(pm.types)):
                 lo = blk * b
                 hi = min(len(arr), lo + b)
