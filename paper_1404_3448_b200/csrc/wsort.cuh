@@ -1,5 +1,6 @@
-// wsort.cuh -- level-0 window naming for DNA texts (ranks 1..4, N < 2^29):
-// an MSD sort of the samples' 21-character windows in streaming passes.
+// wsort.cuh -- level-0 window naming for DNA texts (ranks 1..4, or the
+// generalized text's residues 2..5 around one separator; N < 2^29): an MSD
+// sort of the samples' 21-character windows in streaming passes.
 //
 // The generic window sort (bsort.cuh over WindowSrc) builds 63-bit keys
 // twice from unaligned global words, moves 16 B staging records through two
@@ -8,12 +9,14 @@
 // (a 21-character window is three funnel shifts) and every sample becomes
 // ONE 8-byte record that carries the rest of its key:
 //
-//   rec = chars 5..21 (34 bits) | flag (1) | 2^29-1-pos (29)
+//   rec = chars 5..21 (34 bits) | flag (1) | low (29)
 //
-// flag = 1 for a full window, 0 for a window that reaches past the end (at
-// most 20 of them).  Sorting records as u64 orders equal 0-filled windows
-// "end window first, then the shorter one", which is the suffix order, so
-// end windows stay unique names (the property DC3's padding triples give).
+// flag = 1 for a full window (low = 2^29-1-pos), 0 for a window that stops
+// early -- it reaches the end or the separator (at most 41 of them; digits
+// from the stop on are 0 and low = distance << 1 | kind, see ws_rec).
+// Sorting records as u64 orders equal 0-filled windows "nearer stop first,
+// the end before the separator", which is the suffix order, so stopped
+// windows stay unique names (the property DC3's padding triples give).
 //
 //   P1 k_ws_count   text tiles -> 2^16 fine bins (first 8 chars) in 16-bit
 //                   shared-memory counters, one flush per CTA
@@ -22,13 +25,14 @@
 //   P2a k_ws_part1  text tiles -> records bucketed by the first 4 chars
 //                   (256 coarse regions; runs of ~32 records per tile)
 //   P2b k_ws_part2  each coarse region -> 256 fine buckets (chars 5..8)
-//   P3  k_ws_sort   persistent CTAs, one fine bucket at a time (bulk-copy
-//                   prefetch of the next): counting split by the next 12
-//                   bits in shared memory, rank by counting inside the
-//                   ~0.7-record sub-buckets, then in the same pass: the sorted
-//                   sample indices (= SAc), distinct-name count, tied runs
-//                   for resolve_ties, and ISAc[s] = rank through pass A of
-//                   the bucketed scatter (pscatter.cuh).
+//   P3  k_ws_sort   persistent CTAs, one unit of 2^G fine buckets at a time
+//                   (bulk-copy prefetch of the next): counting split into
+//                   4096 sub-buckets in shared memory, rank by counting inside
+//                   the ~0.7-record sub-buckets, then in the same pass: the
+//                   sorted sample indices (= SAc), their first two
+//                   characters (CH, for the compact records), distinct-name
+//                   count, tied runs for resolve_ties, and ISAc[s] = rank
+//                   through pass A of the bucketed scatter (pscatter.cuh).
 // Reference: suffix_index.py:221-253 (_name_triples), 256-271 (_sort_samples).
 #pragma once
 
