@@ -73,6 +73,7 @@ constexpr int BPS = (int)(SBK / BLK);  // blocks per superblock (32 = one warp)
 struct BlkLayout {
     i64 n, nb, ns, n8, o_pre, o_suf, o_min, o_stab;
     int sbits, slevels;
+    int pb;  // > 0: stab entries are (v << pb | position of the leftmost min), else (v << sbits | superblock)
     __host__ __device__ static BlkLayout of(i64 n) {
         BlkLayout L;
         L.n = n;
@@ -87,6 +88,7 @@ struct BlkLayout {
         while (((i64)1 << L.sbits) < L.ns) L.sbits++;
         L.slevels = 0;
         while (L.slevels < 40 && ((i64)1 << L.slevels) <= L.ns) L.slevels++;
+        L.pb = 0;
         return L;
     }
     __host__ __device__ i64 bytes() const { return o_stab + 4 * level_off(ns, slevels); }
@@ -134,7 +136,9 @@ __global__ void k_blk_pack(Vals<V> val, BlkLayout L, i64 bias, u8 *__restrict__ 
         }
         bpre[b] = pre;
         bsuf[b] = suf;
-        if (lane == 0) stab[sb] = ((suf >> 16) << L.sbits) | (u32)sb;
+        if (lane == 0)
+            stab[sb] = L.pb ? ((suf >> 16) << L.pb) | (u32)((sb << SB_SHIFT) + (suf & 0xFFFFu))
+                            : ((suf >> 16) << L.sbits) | (u32)sb;
     }
     if (blockIdx.x == 0 && threadIdx.x < 16) tab[L.n8 - 16 + threadIdx.x] = 0xFF;
 }
@@ -169,8 +173,8 @@ __device__ __forceinline__ u64 blk_scan(const u8 *__restrict__ v8, i64 a, i64 b)
     return ((u64)m << 32) | (u64)(c0 + pos);
 }
 
-__device__ __forceinline__ void blocked_query(const u8 *__restrict__ tab, i64 n, i64 bias, i64 i, i64 j, i64 &idx,
-                                              i64 &val) {
+__device__ __forceinline__ void blocked_query(const u8 *__restrict__ tab, i64 n, i64 bias, int pb, i64 i, i64 j,
+                                              i64 &idx, i64 &val) {
     const BlkLayout L = BlkLayout::of(n);
     const u32 *bpre = reinterpret_cast<const u32 *>(tab + L.o_pre), *bsuf = reinterpret_cast<const u32 *>(tab + L.o_suf);
     const u16 *bmin = reinterpret_cast<const u16 *>(tab + L.o_min);
@@ -200,8 +204,13 @@ __device__ __forceinline__ void blocked_query(const u8 *__restrict__ tab, i64 n,
                 const u32 *lv = stab + level_off(L.ns, k);
                 const u32 a = __ldg(lv + lo), b = __ldg(lv + hi - ((i64)1 << k) + 1);
                 const u32 mn = a <= b ? a : b;
-                const i64 sb = (i64)(mn & ((1u << L.sbits) - 1));
-                cand(((mn >> L.sbits) << 16) | (__ldg(bsuf + sb * BPS) & 0xFFFFu), sb);
+                if (pb) {  // the entry holds the position itself (one probe fewer)
+                    const u64 key = ((u64)(mn >> pb) << 32) | (u64)(mn & ((1u << pb) - 1));
+                    best = key < best ? key : best;
+                } else {
+                    const i64 sb = (i64)(mn & ((1u << L.sbits) - 1));
+                    cand(((mn >> L.sbits) << 16) | (__ldg(bsuf + sb * BPS) & 0xFFFFu), sb);
+                }
             }
             if (bj - 1 >= sj * BPS) cand(__ldg(bpre + bj - 1), sj);
         }
@@ -237,13 +246,18 @@ __device__ __forceinline__ void index_query(const u32 *__restrict__ tab, Vals<V>
 
 struct PlanDev {
     i64 n, bias;
-    int mode, ib;
+    int mode, ib, vb;
 };
+// blocked mode: superblock-table entries carry positions when they fit
+__host__ __device__ inline int blk_pos_bits(int value_bits, int index_bits) {
+    return value_bits + index_bits <= 32 ? (index_bits > 0 ? index_bits : 1) : 0;
+}
 
 template <typename V>
 __device__ __forceinline__ void any_query(const PlanDev &P, const void *tab, Vals<V> val, i64 i, i64 j,
                                           i64 &idx, i64 &v) {
-    if (P.mode == SAIX_SPARSE_BLOCKED) blocked_query((const u8 *)tab, P.n, P.bias, i, j, idx, v);
+    if (P.mode == SAIX_SPARSE_BLOCKED)
+        blocked_query((const u8 *)tab, P.n, P.bias, blk_pos_bits(P.vb, P.ib), i, j, idx, v);
     else if (P.mode == SAIX_SPARSE_PACK32) packed_query<u32>((const u32 *)tab, P.n, P.bias, P.ib, i, j, idx, v);
     else if (P.mode == SAIX_SPARSE_PACK64) packed_query<u64>((const u64 *)tab, P.n, P.bias, P.ib, i, j, idx, v);
     else index_query<V>((const u32 *)tab, val, P.n, i, j, idx, v);
@@ -290,7 +304,9 @@ __global__ void k_lcp_query(PlanDev P, const void *tab, Vals<V> val, const u32 *
     }
 }
 
-static PlanDev dev_plan(const saix_sparse_plan *p) { return PlanDev{p->n, p->value_bias, p->mode, p->index_bits}; }
+static PlanDev dev_plan(const saix_sparse_plan *p) {
+    return PlanDev{p->n, p->value_bias, p->mode, p->index_bits, p->value_bits};
+}
 
 __global__ void k_minmax_init(i64 *out2) {
     out2[0] = INT64_MAX;
@@ -402,7 +418,8 @@ extern "C" int saix_sparse_build(const saix_sparse_plan *plan, const void *value
     }
     cudaStream_t st = (cudaStream_t)stream;
     if (plan->mode == SAIX_SPARSE_BLOCKED) {
-        const BlkLayout B = BlkLayout::of(plan->n);
+        BlkLayout B = BlkLayout::of(plan->n);
+        B.pb = blk_pos_bits(plan->value_bits, plan->index_bits);
         u8 *tab = (u8 *)table;
         u32 *bt = reinterpret_cast<u32 *>(tab + B.o_stab);
         {
