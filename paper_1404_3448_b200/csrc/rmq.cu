@@ -107,13 +107,27 @@ __global__ void k_blk_pack(Vals<V> val, BlkLayout L, i64 bias, u8 *__restrict__ 
         const i64 b = sb * BPS + lane, p0 = b << BLK_SHIFT;
         u32 w[8];
         u32 best = 0xFFFFu;  // (v << 8 | offset in block)
+        u32 raw[32];  // u32 values: the block's 128 bytes as 8 vector loads, all in flight
+        const bool vec = sizeof(V) == 4 && p0 + 32 <= L.n;
+        if (vec) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(val.v + p0);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const uint4 t = __ldcs(src + q);
+                raw[4 * q] = t.x;
+                raw[4 * q + 1] = t.y;
+                raw[4 * q + 2] = t.z;
+                raw[4 * q + 3] = t.w;
+            }
+        }
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             u32 word = 0;
 #pragma unroll
             for (int y = 0; y < 4; y++) {
                 const i64 p = p0 + 4 * q + y;
-                const u32 x = p < L.n ? (u32)((u64)val(p) - (u64)bias) : 0xFFu;
+                const u32 x = vec ? raw[4 * q + y] - (u32)bias
+                                  : (p < L.n ? (u32)((u64)val(p) - (u64)bias) : 0xFFu);
                 word |= x << (8 * y);
                 const u32 key = (x << 8) | (u32)(4 * q + y);
                 best = key < best ? key : best;
