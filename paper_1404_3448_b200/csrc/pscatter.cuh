@@ -101,11 +101,18 @@ __device__ __forceinline__ void ps_block_emit(const P (&it)[ITEMS], const bool (
     __syncthreads();
     // bucket starts: exclusive scan over buckets in chunks of THREADS (one
     // bucket per thread), and one independent global atomic per non-empty
-    // (tile, bucket) to reserve the run inside the bucket's region
+    // (tile, bucket) to reserve the run inside the bucket's region.  The
+    // reservations stay in registers until after the staging loop, so their
+    // L2 round trip overlaps it.
+    constexpr int MAXC = (PS_MAX_BUCKETS + THREADS - 1) / THREADS;
+    u32 res[MAXC];
     __shared__ u32 sh_warp[THREADS / 32 + 1];
     __shared__ u32 sh_total;
     u32 carry = 0;
-    for (int c0 = 0; c0 < nb; c0 += THREADS) {
+#pragma unroll
+    for (int k = 0; k < MAXC; k++) {
+        const int c0 = k * THREADS;
+        if (c0 >= nb) break;  // block-uniform
         int b = c0 + threadIdx.x;
         u32 c = b < nb ? sh_cnt[b] : 0u;
         u32 inc = c;
@@ -127,18 +134,21 @@ __device__ __forceinline__ void ps_block_emit(const P (&it)[ITEMS], const bool (
             if (threadIdx.x == THREADS / 32 - 1) sh_warp[THREADS / 32] = xi;
         }
         __syncthreads();
-        if (b < nb) {
-            sh_base[b] = c ? atomicAdd(&lv.cursor[b], c) : 0u;         // run base inside the region
-            sh_cnt[b] = carry + sh_warp[threadIdx.x >> 5] + inc - c;  // local start of the bucket
-        }
+        res[k] = (b < nb && c) ? atomicAdd(&lv.cursor[b], c) : 0u;  // run base inside the region
+        if (b < nb) sh_cnt[b] = carry + sh_warp[threadIdx.x >> 5] + inc - c;  // local start of the bucket
         carry += sh_warp[THREADS / 32];
         __syncthreads();
     }
     if (threadIdx.x == 0) sh_total = carry;
-    __syncthreads();
 #pragma unroll
     for (int r = 0; r < ITEMS; r++)
         if (ok[r]) sh_items[sh_cnt[(u32)(it[r].x >> lv.shift) - lv.base] + slot[r]] = it[r];
+#pragma unroll
+    for (int k = 0; k < MAXC; k++) {
+        const int b = k * THREADS + threadIdx.x;
+        if (k * THREADS >= nb) break;
+        if (b < nb) sh_base[b] = res[k];
+    }
     __syncthreads();
     const u32 tot = sh_total;
     for (u32 x = threadIdx.x; x < tot; x += THREADS) {
