@@ -245,10 +245,9 @@ __device__ __forceinline__ void ws_block_emit(const u64 (&rec)[WS_PI], const u8 
     const u32 c = threadIdx.x < 256 ? sh_cnt[threadIdx.x] : 0u;
     u32 excl;
     const u32 tot = block_exclusive_scan<WS_PT>(c, excl, sh_warp);
-    if (threadIdx.x < 256) {
-        sh_start[threadIdx.x] = excl;
-        sh_base[threadIdx.x] = c ? atomicAdd(&cur[threadIdx.x], c) : 0u;
-    }
+    // the run reservation's round trip overlaps the staging loop
+    const u32 res = (threadIdx.x < 256 && c) ? atomicAdd(&cur[threadIdx.x], c) : 0u;
+    if (threadIdx.x < 256) sh_start[threadIdx.x] = excl;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < WS_PI; r++)
@@ -257,6 +256,7 @@ __device__ __forceinline__ void ws_block_emit(const u64 (&rec)[WS_PI], const u8 
             sh_rec[at] = rec[r];
             sh_bk[at] = bk[r];
         }
+    if (threadIdx.x < 256) sh_base[threadIdx.x] = res;
     __syncthreads();
     for (u32 x = threadIdx.x; x < tot; x += WS_PT) {
         const u32 b = sh_bk[x];
