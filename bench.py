@@ -964,6 +964,9 @@ def bench(args, rank, world, dist):
                                        "peak": round(smem_peak, 1), "unit": "GB/s",
                                        "frac": round(roof["achieved"] / smem_peak, 4),
                                        "peak_source": f"128 B/clk/SM x 148 SMs x {mhz:.0f} MHz"}
+        if getattr(args, "shared_devices", 0):
+            line["config"]["shared_devices"] = (f"{world} ranks on {args.shared_devices} GPU(s) over gloo: "
+                                                "validates the sharded path, not a scaling number")
         if getattr(wl, "parity", None):
             line["parity"] = wl.parity
         if results is not None:
@@ -1011,11 +1014,18 @@ def main():
         return
 
     import torch
-    torch.cuda.set_device(local)
+    ndev = max(1, torch.cuda.device_count())
+    # more ranks than GPUs (a 1-GPU box validating the N-rank path): ranks
+    # share devices over gloo and the line says so; timings are not scaling
+    args.shared_devices = ndev if world > ndev else 0
+    torch.cuda.set_device(local % ndev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.shared_devices:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
         bench(args, rank, world, dist)
     finally:
