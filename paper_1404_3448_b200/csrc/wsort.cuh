@@ -156,9 +156,15 @@ template <bool SEP>
 __global__ void __launch_bounds__(1024, 1)
 k_ws_count(const u8 *__restrict__ t, SampleLayout L, WsAlpha A, i64 ntiles, u32 *__restrict__ hist,
            u32 *__restrict__ overflow) {
-    extern __shared__ __align__(16) u32 ws_h16[];  // WS_FINE 16-bit counters, two per word
+    // WS_FINE 16-bit counters, two per word, then 4096 u32 counters of the
+    // first 6 characters: a fine counter can only wrap inside a CTA whose
+    // 6-character counter passed 65535, so the adds need no return value
+    // (fire-and-forget shared reductions) and the wrap check is one pass at
+    // the end (false positives only send skewed texts to the generic sort)
+    extern __shared__ __align__(16) u32 ws_h16[];
+    u32 *ws_c6 = ws_h16 + WS_FINE / 2;
     __shared__ u32 W[WS_WORDS];
-    for (int i = threadIdx.x; i < WS_FINE / 2; i += 1024) ws_h16[i] = 0;
+    for (int i = threadIdx.x; i < WS_FINE / 2 + 4096; i += 1024) ws_h16[i] = 0;
     bool ovf = false;
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 p0 = tile * WS_TP;
@@ -170,12 +176,12 @@ k_ws_count(const u8 *__restrict__ t, SampleLayout L, WsAlpha A, i64 ntiles, u32 
             const int o = ws_off(q);
             if (!ws_valid(p0 + o, L)) continue;
             const u32 f = (u32)(ws_mask_sep<SEP>(ws_key(W, o), p0 + o, A) >> 26);
-            const int sh = 16 * (f & 1);
-            const u32 old = atomicAdd(&ws_h16[f >> 1], 1u << sh);
-            ovf |= ((old >> sh) & 0xFFFFu) == 0xFFFFu;
+            atomicAdd(&ws_h16[f >> 1], 1u << (16 * (f & 1)));
+            atomicAdd(&ws_c6[f >> 4], 1u);
         }
     }
     __syncthreads();
+    for (int i = threadIdx.x; i < 4096; i += 1024) ovf |= ws_c6[i] > 0xFFFFu;
     for (int i = threadIdx.x; i < WS_FINE / 2; i += 1024) {
         const u32 v = ws_h16[i];
         if (v & 0xFFFFu) atomicAdd(&hist[2 * i], v & 0xFFFFu);
