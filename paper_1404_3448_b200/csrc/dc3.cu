@@ -2750,8 +2750,8 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     const i64 ntiles = ceil_div(N + 1, (i64)WS_TP);
     static DeviceFlags attr;
     if (attr.need()) {
-        SAIX_CUDA(cudaFuncSetAttribute(k_ws_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_FINE * 2 + 16384));
-        SAIX_CUDA(cudaFuncSetAttribute(k_ws_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_FINE * 2 + 16384));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_COUNT_SMEM));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, WS_COUNT_SMEM));
         SAIX_CUDA(cudaFuncSetAttribute(k_ws_part1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)WS_P2_SMEM));
         SAIX_CUDA(cudaFuncSetAttribute(k_ws_part1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2765,8 +2765,8 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     SAIX_CUDA(cudaMemsetAsync(scal, 0, 16 * 4, st));
     {
         Prof prof_("dc3.ws_count", (double)N, st);
-        if (A.sep >= 0) k_ws_count<true><<<kNumSMs, 1024, WS_FINE * 2 + 16384, st>>>(text, L, A, ntiles, hist, scal + 6);
-        else k_ws_count<false><<<kNumSMs, 1024, WS_FINE * 2 + 16384, st>>>(text, L, A, ntiles, hist, scal + 6);
+        if (A.sep >= 0) k_ws_count<true><<<kNumSMs, 1024, WS_COUNT_SMEM, st>>>(text, L, A, ntiles, hist, scal + 6);
+        else k_ws_count<false><<<kNumSMs, 1024, WS_COUNT_SMEM, st>>>(text, L, A, ntiles, hist, scal + 6);
         SAIX_LAUNCHED();
     }
     SAIX_TRY(scan_transform(WsHistIn{hist}, WsOffOut{off, curF, curC, scal + 7}, WS_FINE, tmp, off + WS_FINE, st,

@@ -152,6 +152,36 @@ __device__ __forceinline__ i64 ws_pos(u64 rec, i64 N, const WsAlpha &A) {
 __device__ __forceinline__ bool ws_same(u64 a, u64 b) { return ((a ^ b) >> 29) == 0 && ((a >> 29) & 1); }
 
 // ---------------------------------------------------------------- P1
+// raw text tile [p0, p0 + WS_TP + 32) -> packed words; bytes past N read as lo
+__device__ __forceinline__ void ws_pack_tile(const u8 *__restrict__ raw, i64 N, i64 p0, u32 *__restrict__ W,
+                                             int nthreads, u32 lo) {
+    const u32 lo4 = lo * 0x01010101u;
+    for (int w = threadIdx.x; w < WS_WORDS; w += nthreads) {
+        const i64 q = p0 + 16 * (i64)w;
+        uint4 v;
+        if (q + 16 <= N) {
+            v = reinterpret_cast<const uint4 *>(raw)[w];
+        } else {
+            u32 x[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                u32 word = 0;
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const i64 at = q + 4 * k + b;
+                    word |= (at < N ? (u32)raw[16 * w + 4 * k + b] : lo) << (8 * b);
+                }
+                x[k] = word;
+            }
+            v = make_uint4(x[0], x[1], x[2], x[3]);
+        }
+        W[w] = ws_pack16(v, lo4);
+    }
+}
+constexpr int WS_RAW = (WS_WORDS * 16 + 15) & ~15;  // raw tile bytes (16-aligned)
+
+// P1: persistent CTAs; the next text tile arrives by a bulk copy (TMA)
+// while the current one is counted
 template <bool SEP>
 __global__ void __launch_bounds__(1024, 1)
 k_ws_count(const u8 *__restrict__ t, SampleLayout L, WsAlpha A, i64 ntiles, u32 *__restrict__ hist,
@@ -160,17 +190,51 @@ k_ws_count(const u8 *__restrict__ t, SampleLayout L, WsAlpha A, i64 ntiles, u32 
     // first 6 characters: a fine counter can only wrap inside a CTA whose
     // 6-character counter passed 65535, so the adds need no return value
     // (fire-and-forget shared reductions) and the wrap check is one pass at
-    // the end (false positives only send skewed texts to the generic sort)
+    // the end (false positives only send skewed texts to the generic sort);
+    // then two raw text tiles
     extern __shared__ __align__(16) u32 ws_h16[];
     u32 *ws_c6 = ws_h16 + WS_FINE / 2;
+    u8 *raw0 = reinterpret_cast<u8 *>(ws_c6 + 4096);
     __shared__ u32 W[WS_WORDS];
+    __shared__ __align__(8) u64 bar;
     for (int i = threadIdx.x; i < WS_FINE / 2 + 4096; i += 1024) ws_h16[i] = 0;
-    bool ovf = false;
-    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_async_smem();
+    }
+    __syncthreads();
+    const i64 N = L.n;
+    auto issue = [&](i64 tile, int slot) {  // one thread: the tile's whole 16-byte words inside the text
         const i64 p0 = tile * WS_TP;
+        i64 end = p0 + WS_RAW < N ? p0 + WS_RAW : N;
+        const u32 bytes = end > p0 ? (u32)((end - p0) & ~(i64)15) : 0u;
+        mbar_expect_tx(&bar, bytes);
+        if (bytes) bulk_g2s(raw0 + slot * WS_RAW, t + p0, bytes, &bar);
+    };
+    bool ovf = false;
+    u32 parity = 0;
+    int slot = 0;
+    i64 tile = blockIdx.x;
+    if (threadIdx.x == 0 && tile < ntiles) issue(tile, 0);
+    for (; tile < ntiles; tile += gridDim.x) {
+        const i64 p0 = tile * WS_TP;
+        u8 *raw = raw0 + slot * WS_RAW;
+        mbar_wait(&bar, parity);
+        parity ^= 1;
+        // bytes the bulk copy did not cover (the text's last < 16) come from global
+        const i64 covered = p0 + (((p0 + WS_RAW < N ? p0 + WS_RAW : N) - p0) & ~(i64)15);
+        if (covered < N && covered < p0 + WS_RAW)
+            for (i64 a = covered + threadIdx.x; a < N && a < p0 + WS_RAW; a += 1024)
+                raw[a - p0] = t[a];
         __syncthreads();
-        ws_stage(t, L.n, p0, W, 1024, A.lo);
-        __syncthreads();
+        ws_pack_tile(raw, N, p0, W, 1024, A.lo);
+        __syncthreads();  // raw[slot] consumed: the next tile may land in the other slot
+        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) {
+            fence_async_smem();
+            issue(tile + gridDim.x, slot ^ 1);
+        }
+        slot ^= 1;
 #pragma unroll 4
         for (int q = threadIdx.x; q < WS_TS; q += 1024) {
             const int o = ws_off(q);
@@ -179,6 +243,7 @@ k_ws_count(const u8 *__restrict__ t, SampleLayout L, WsAlpha A, i64 ntiles, u32 
             atomicAdd(&ws_h16[f >> 1], 1u << (16 * (f & 1)));
             atomicAdd(&ws_c6[f >> 4], 1u);
         }
+        __syncthreads();  // W is rewritten by the next tile
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 4096; i += 1024) ovf |= ws_c6[i] > 0xFFFFu;
@@ -189,6 +254,7 @@ k_ws_count(const u8 *__restrict__ t, SampleLayout L, WsAlpha A, i64 ntiles, u32 
     }
     if (ovf) atomicMax(overflow, 1u);
 }
+constexpr int WS_COUNT_SMEM = WS_FINE * 2 + 16384 + 2 * WS_RAW;
 
 // fine offsets (exclusive), staging cursors and the largest bucket
 struct WsHistIn {

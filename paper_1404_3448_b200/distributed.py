@@ -87,9 +87,12 @@ class NcclComm:
             self._comm = None
 
     def __del__(self):
+        import sys
+        if sys.is_finalizing():  # the CUDA runtime may already be gone: let the process exit free it
+            return
         try:
             self.close()
-        except Exception:  # interpreter shutdown
+        except Exception:
             pass
 
 
