@@ -87,7 +87,7 @@ struct PsPlan {
 // flags); the block stages them by bucket in shared memory and writes each
 // bucket's run contiguously.  smem: THREADS*ITEMS items (sh_items) + 2 *
 // buckets u32 (sh_cnt, sh_base).  All threads of the block must call it.
-template <class P, int THREADS, int ITEMS>
+template <class P, int THREADS, int ITEMS, int MAXB = PS_MAX_BUCKETS>
 __device__ __forceinline__ void ps_block_emit(const P (&it)[ITEMS], const bool (&ok)[ITEMS], const PsLevel &lv,
                                               P *__restrict__ stage, P *__restrict__ sh_items, u32 *__restrict__ sh_cnt,
                                               u32 *__restrict__ sh_base) {
@@ -104,7 +104,7 @@ __device__ __forceinline__ void ps_block_emit(const P (&it)[ITEMS], const bool (
     // (tile, bucket) to reserve the run inside the bucket's region.  The
     // reservations stay in registers until after the staging loop, so their
     // L2 round trip overlaps it.
-    constexpr int MAXC = (PS_MAX_BUCKETS + THREADS - 1) / THREADS;
+    constexpr int MAXC = (MAXB + THREADS - 1) / THREADS;
     u32 res[MAXC];
     __shared__ u32 sh_warp[THREADS / 32 + 1];
     __shared__ u32 sh_total;
@@ -161,7 +161,7 @@ __device__ __forceinline__ void ps_block_emit(const P (&it)[ITEMS], const bool (
 
 // Pass A2: tile t covers stage1[t*TILE, (t+1)*TILE) inside one coarse region.
 template <class P>
-__global__ void __launch_bounds__(PS_REFINE_THREADS)
+__global__ void __launch_bounds__(PS_REFINE_THREADS, sizeof(P) <= 8 ? 3 : 2)
 k_ps_refine(const P *__restrict__ stage1, PsPlan plan, P *__restrict__ stage2) {
     extern __shared__ __align__(16) unsigned char ps_smem[];
     P *sh_items = reinterpret_cast<P *>(ps_smem);
@@ -186,7 +186,7 @@ k_ps_refine(const P *__restrict__ stage1, PsPlan plan, P *__restrict__ stage2) {
         ok[r] = x < fill;
         if (ok[r]) it[r] = ld_stream(stage1 + (b << plan.a.shift) + x);
     }
-    ps_block_emit<P, PS_REFINE_THREADS, PS_REFINE_ITEMS>(it, ok, lv, stage2 + ((i64)lv.base << plan.s2), sh_items,
+    ps_block_emit<P, PS_REFINE_THREADS, PS_REFINE_ITEMS, 256>(it, ok, lv, stage2 + ((i64)lv.base << plan.s2), sh_items,
                                                         sh_cnt, sh_base);
 }
 

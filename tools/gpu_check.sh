@@ -15,6 +15,7 @@ for what in "$@"; do
     ncu_c4|ncu_c5) W=${what#ncu_}; timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/${W}_launches.csv python tools/profile_once.py $W > $O/ncu_$W.log 2>&1; python tools/ncu_summary.py $O/${W}_launches.csv 40 > $O/${W}_launches.txt; head -25 $O/${W}_launches.txt ;;
     ncu_c3) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/c3_launches.csv python tools/profile_once.py 268435456 > $O/ncu_c3.log 2>&1; python tools/ncu_summary.py $O/c3_launches.csv > $O/c3_launches.txt; head -30 $O/c3_launches.txt ;;
     c3full_*) K=${what#c3full_}; timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:$K -c 1 -o $O/c3full_$K python tools/profile_once.py 268435456 > $O/ncu_c3full_$K.log 2>&1; tail -2 $O/ncu_c3full_$K.log ;;
+    c5full_*) K=${what#c5full_}; timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:$K -c 1 -o $O/c5full_$K python tools/profile_once.py c5 > $O/ncu_c5full_$K.log 2>&1; tail -2 $O/ncu_c5full_$K.log ;;
     c4full_*) K=${what#c4full_}; timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:$K -c 1 -o $O/c4full_$K python tools/profile_once.py c4 > $O/ncu_c4full_$K.log 2>&1; tail -2 $O/ncu_c4full_$K.log ;;
     c2full_*) K=${what#c2full_}; timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:$K -c 1 -o $O/c2full_$K python tools/profile_once.py c2 > $O/ncu_c2full_$K.log 2>&1; tail -2 $O/ncu_c2full_$K.log ;;
     full_*) K=${what#full_}; timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:$K -c 1 -o $O/full_$K python tools/profile_once.py c2 > $O/ncu_full_$K.log 2>&1; tail -3 $O/ncu_full_$K.log ;;
