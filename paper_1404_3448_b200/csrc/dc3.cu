@@ -1115,25 +1115,32 @@ k_nx_window(const uint2 *__restrict__ stage2, PsPlan plan, u32 *__restrict__ nx,
     const uint2 *src = stage2 + d0;
     if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
     const bool full = n_in == len;
-    for (i64 x = threadIdx.x; x < n_in; x += PS_THREADS) {
-        const uint2 v = ld_stream(src + x);
-        if (full) win[(i64)v.x - d0] = v.y;
-        else nx[v.x] = v.y;
+    // a window holds at most 2048 items: all loads of a thread in flight at once
+    constexpr int NW_ITEMS = (1 << RW_SHIFT) / PS_THREADS;
+    uint2 v[NW_ITEMS];
+#pragma unroll
+    for (int r = 0; r < NW_ITEMS; r++) {
+        const int x = r * PS_THREADS + threadIdx.x;
+        if (x < n_in) v[r] = ld_stream(src + x);
+    }
+#pragma unroll
+    for (int r = 0; r < NW_ITEMS; r++) {
+        const int x = r * PS_THREADS + threadIdx.x;
+        if (x < n_in) {
+            if (full) win[(i64)v[r].x - d0] = v[r].y;
+            else nx[v[r].x] = v[r].y;
+        }
     }
     __syncthreads();
-    const i64 nc = full ? len : n_in;
+    const int nc = (int)(full ? len : n_in);
     u32 c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (i64 x0 = 0; x0 < nc; x0 += PS_THREADS) {
-        const i64 x = x0 + threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < NW_ITEMS; r++) {
+        const int x = r * PS_THREADS + threadIdx.x;
         u32 dg = NX_MOD2;
         if (x < nc) {
-            u32 e;
-            if (full) {
-                e = win[x];
-                st_stream(nx + d0 + x, e);
-            } else {
-                e = ld_stream(src + x).y;
-            }
+            const u32 e = full ? win[x] : v[r].y;  // not full: item x is this thread's v[r]
+            if (full) st_stream(nx + d0 + x, e);
             dg = e >> 29;
         }
 #pragma unroll
