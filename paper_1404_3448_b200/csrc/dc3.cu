@@ -2765,7 +2765,7 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
                                        (int)WS_P2_SMEM));
         SAIX_CUDA(cudaFuncSetAttribute(k_ws_part1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)WS_P2_SMEM));
-        SAIX_CUDA(cudaFuncSetAttribute(k_ws_part2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_P2_SMEM));
+        SAIX_CUDA(cudaFuncSetAttribute(k_ws_part2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_P2B_SMEM));
         SAIX_TRY(ws_sort_attrs<false>());
         SAIX_TRY(ws_sort_attrs<true>());
         attr.set();
@@ -2819,7 +2819,7 @@ static int window_rank_dna(Dc3Ctx &c, const u8 *text, i64 N, const SampleLayout 
     }
     {
         Prof prof_("dc3.ws_part2", 16.0 * m, st);
-        k_ws_part2<<<(unsigned)(ceil_div(m, (i64)WS_PTILE) + WS_COARSE), WS_PT, WS_P2_SMEM, st>>>(SA_, off, tstart, m,
+        k_ws_part2<<<(unsigned)(ceil_div(m, (i64)WS_PTILE2) + WS_COARSE), WS_PT, WS_P2B_SMEM, st>>>(SA_, off, tstart, m,
                                                                                                   curF, SB);
         SAIX_LAUNCHED();
     }

@@ -51,6 +51,8 @@ constexpr u64 WS_POS_MASK = (1ull << WS_POS_BITS) - 1;
 constexpr int WS_PT = 512;                // P2 threads
 constexpr int WS_PI = 16;                 // P2 items per thread
 constexpr int WS_PTILE = WS_PT * WS_PI;   // 8192 records
+constexpr int WS_PI2 = 8;                 // P2b items per thread (3 CTAs per SM)
+constexpr int WS_PTILE2 = WS_PT * WS_PI2; // 4096 records
 constexpr int WS_ST = 512;                // P3 threads
 constexpr int WS_CAP_MIN = 1024;
 constexpr int WS_CAP_MAX = 10240;         // largest fine bucket P3 takes (shared memory <= 227 KB)
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(WS_COARSE) k_ws_tiles(const u32 *__restrict__ 
     const int c = threadIdx.x;
     const i64 lo = off[c * WS_COARSE];
     const i64 hi = c + 1 < WS_COARSE ? (i64)off[(c + 1) * WS_COARSE] : m;
-    const u32 nt = (u32)ceil_div(hi - lo, (i64)WS_PTILE);
+    const u32 nt = (u32)ceil_div(hi - lo, (i64)WS_PTILE2);
     u32 excl;
     const u32 tot = block_exclusive_scan<WS_COARSE>(nt, excl, sh_warp);
     tstart[c] = excl;
@@ -300,18 +302,19 @@ __global__ void k_ws_unit_max(const u32 *__restrict__ off, i64 m, int G, u32 *__
     if (lane_id() == 0 && mx) atomicMax(out, mx);
 }
 
-// Block-level bucketed write of WS_PT*WS_PI records into runs reserved on
+// Block-level bucketed write of WS_PT*PI records into runs reserved on
 // absolute cursors: item r goes to bucket bk[r] (< 256), cursor cur[bk].
-__device__ __forceinline__ void ws_block_emit(const u64 (&rec)[WS_PI], const u8 (&bk)[WS_PI], const bool (&ok)[WS_PI],
+template <int PI>
+__device__ __forceinline__ void ws_block_emit(const u64 (&rec)[PI], const u8 (&bk)[PI], const bool (&ok)[PI],
                                               u32 *__restrict__ cur, u64 *__restrict__ out, u64 *__restrict__ sh_rec,
                                               u8 *__restrict__ sh_bk, u32 *__restrict__ sh_cnt, u32 *__restrict__ sh_start,
                                               u32 *__restrict__ sh_base) {
     __shared__ u32 sh_warp[WS_PT / 32 + 1];
     if (threadIdx.x < 256) sh_cnt[threadIdx.x] = 0;
     __syncthreads();
-    u32 slot[WS_PI];
+    u32 slot[PI];
 #pragma unroll
-    for (int r = 0; r < WS_PI; r++)
+    for (int r = 0; r < PI; r++)
         if (ok[r]) slot[r] = atomicAdd(&sh_cnt[bk[r]], 1u);
     __syncthreads();
     const u32 c = threadIdx.x < 256 ? sh_cnt[threadIdx.x] : 0u;
@@ -322,7 +325,7 @@ __device__ __forceinline__ void ws_block_emit(const u64 (&rec)[WS_PI], const u8 
     if (threadIdx.x < 256) sh_start[threadIdx.x] = excl;
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < WS_PI; r++)
+    for (int r = 0; r < PI; r++)
         if (ok[r]) {
             const u32 at = sh_start[bk[r]] + slot[r];
             sh_rec[at] = rec[r];
@@ -336,6 +339,7 @@ __device__ __forceinline__ void ws_block_emit(const u64 (&rec)[WS_PI], const u8 
     }
 }
 constexpr size_t WS_P2_SMEM = (size_t)WS_PTILE * 9 + 3 * 256 * 4;
+constexpr size_t WS_P2B_SMEM = (size_t)WS_PTILE2 * 9 + 3 * 256 * 4;
 
 // ---------------------------------------------------------------- P2a
 template <bool SEP>
@@ -366,33 +370,33 @@ k_ws_part1(const u8 *__restrict__ t, SampleLayout L, WsAlpha A, u32 *__restrict_
 }
 
 // ---------------------------------------------------------------- P2b
-__global__ void __launch_bounds__(WS_PT, 2)
+__global__ void __launch_bounds__(WS_PT, 3)
 k_ws_part2(const u64 *__restrict__ stageA, const u32 *__restrict__ off, const u32 *__restrict__ tstart, i64 m,
            u32 *__restrict__ cur_fine, u64 *__restrict__ stageB) {
     extern __shared__ __align__(16) unsigned char ws_smem[];
     u64 *sh_rec = reinterpret_cast<u64 *>(ws_smem);
-    u8 *sh_bk = ws_smem + (size_t)WS_PTILE * 8;
-    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_bk + WS_PTILE), *sh_start = sh_cnt + 256, *sh_base = sh_start + 256;
+    u8 *sh_bk = ws_smem + (size_t)WS_PTILE2 * 8;
+    u32 *sh_cnt = reinterpret_cast<u32 *>(sh_bk + WS_PTILE2), *sh_start = sh_cnt + 256, *sh_base = sh_start + 256;
     const u32 b = blockIdx.x;
     if (b >= tstart[WS_COARSE]) return;
     int c = 0;  // largest region with tstart[c] <= b
 #pragma unroll
     for (int s = 128; s; s >>= 1)
         if (tstart[c + s] <= b) c += s;
-    const i64 lo = off[c * WS_COARSE] + (i64)(b - tstart[c]) * WS_PTILE;
+    const i64 lo = off[c * WS_COARSE] + (i64)(b - tstart[c]) * WS_PTILE2;
     const i64 hi_r = c + 1 < WS_COARSE ? (i64)off[(c + 1) * WS_COARSE] : m;
-    const i64 hi = lo + WS_PTILE < hi_r ? lo + WS_PTILE : hi_r;
-    u64 rec[WS_PI];
-    u8 bk[WS_PI];
-    bool ok[WS_PI];
+    const i64 hi = lo + WS_PTILE2 < hi_r ? lo + WS_PTILE2 : hi_r;
+    u64 rec[WS_PI2];
+    u8 bk[WS_PI2];
+    bool ok[WS_PI2];
 #pragma unroll
-    for (int r = 0; r < WS_PI; r++) {
+    for (int r = 0; r < WS_PI2; r++) {
         const i64 x = lo + r * WS_PT + threadIdx.x;
         ok[r] = x < hi;
         rec[r] = ok[r] ? __ldcs(stageA + x) : 0ull;
     }
 #pragma unroll
-    for (int r = 0; r < WS_PI; r++) bk[r] = (u8)(rec[r] >> 56);
+    for (int r = 0; r < WS_PI2; r++) bk[r] = (u8)(rec[r] >> 56);
     ws_block_emit(rec, bk, ok, cur_fine + c * WS_COARSE, stageB, sh_rec, sh_bk, sh_cnt, sh_start, sh_base);
 }
 
