@@ -332,18 +332,36 @@ class SuffixIndexer:
     def stage(self, ranks: np.ndarray) -> None:
         self.ht.numpy()[: self.n] = ranks
 
-    def run_device(self) -> None:
+    def _dc3(self, s: int) -> None:
         L = _lib.load()
-        s = _lib.stream_ptr()
         _lib.check(L.saix_dc3(_lib.ptr(self.t), self.bytes, self.n, self.sigma, _lib.ptr(self.sa),
                               _lib.ptr(self.isa), _lib.ptr(self.ws), self.ws.numel(), None, s), "saix_dc3")
+
+    def _lcp(self, s: int) -> None:
+        L = _lib.load()
         _lib.check(L.saix_lcp_sigma(_lib.ptr(self.t), self.bytes, self.n, self.sigma, -1, _lib.ptr(self.sa),
                                     _lib.ptr(self.lcp), _lib.ptr(self.ws), self.ws.numel(), s), "saix_lcp_sigma")
 
+    def run_device(self) -> None:
+        s = _lib.stream_ptr()
+        self._dc3(s)
+        self._lcp(s)
+
     def run_staged(self) -> None:
+        """Upload, build, download; the SA download (copy stream) overlaps
+        the LCP kernel, which only reads SA."""
+        t = _lib.torch()
         n = self.n
+        cur = t.cuda.current_stream()
+        if not hasattr(self, "_copy"):
+            self._copy = t.cuda.Stream()
         self.t[:n].copy_(self.ht[:n], non_blocking=True)
-        self.run_device()
-        self.hsa[:n].copy_(self.sa[:n], non_blocking=True)
+        self._dc3(cur.cuda_stream)
+        done = cur.record_event()
+        self._copy.wait_event(done)
+        with t.cuda.stream(self._copy):
+            self.hsa[:n].copy_(self.sa[:n], non_blocking=True)
+        self._lcp(cur.cuda_stream)
         self.hlcp[:n].copy_(self.lcp[:n], non_blocking=True)
-        _lib.torch().cuda.current_stream().synchronize()
+        cur.wait_stream(self._copy)  # the next step's DC3 rewrites SA only after its download
+        cur.synchronize()
