@@ -440,14 +440,31 @@ __device__ __forceinline__ Seg block_seg_exclusive(Seg v, Misc &ms) {
     return carry;
 }
 
+// Streamed batches (saix_overlap_batch_stream): pairs available once chunks
+// 0..c-1 have landed.  The first chunk holds `first` pairs (one per CTA) and
+// sizes double up to `per`, so the kernel starts after a short copy instead of
+// a full 1/nchunks of the batch.
+__host__ __device__ __forceinline__ i64 stream_avail(i64 c, i64 P, i64 per, i64 first) {
+    i64 done = 0, s = first < per ? first : per;
+    for (i64 k = 0; k < c; k++) {
+        if (s >= per) {
+            done += (c - k) * per;
+            break;
+        }
+        done += s;
+        s *= 2;
+    }
+    return done < P ? done : P;
+}
+
 // STREAM: the batch's ASCII is still arriving (saix_overlap_batch_stream):
-// the copy engine publishes chunk c of `per` pairs by writing c + 1 to
-// *ready after its bytes; a CTA takes pair p only once ready * per > p.
+// the copy engine publishes chunk c by writing c + 1 to *ready after its
+// bytes; a CTA takes pair p only once stream_avail(ready) > p.
 template <bool CLK, bool STREAM>
 __global__ void __launch_bounds__(THREADS, 2)
 k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int keep_n, i64 *__restrict__ out,
            i64 *__restrict__ bad, u32 *__restrict__ next_pair, u32 *__restrict__ nfb, u32 *__restrict__ fb,
-           int nmax, unsigned long long *__restrict__ clk, const u32 *ready, u32 per) {
+           int nmax, unsigned long long *__restrict__ clk, const u32 *ready, u32 per, u32 first) {
     extern __shared__ __align__(16) unsigned char smem[];
     u8 *T = smem + OFF_T;
     u16 *SS = reinterpret_cast<u16 *>(smem + OFF_SS);
@@ -476,7 +493,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                 for (;;) {
                     u32 c;
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ready) : "memory");
-                    if ((u64)c * per > (u64)ms.pair) break;
+                    if (stream_avail(c, P, per, first) > (i64)ms.pair) break;
                     __nanosleep(256);
                 }
             }
@@ -1048,6 +1065,32 @@ static i64 fb_capacity(const i64 *offs, i64 P) {
     return cap;
 }
 
+// worst-case wave-global workspace for a fallback wave of <= cap residues
+// over <= pmax pairs; depends on (cap, pmax) only, so it is planned once per
+// shape (the probe layout costs ~1 ms of host time at C4 size, which would
+// otherwise sit in front of every call's first copy)
+static size_t fb_global_ws(i64 cap, i64 pmax) {
+    if (cap <= 0) return 0;
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<i64, i64>, size_t>> memo;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto &e : memo)
+            if (e.first.first == cap && e.first.second == pmax) return e.second;
+    }
+    std::vector<i64> probe(2 * pmax + 1);
+    for (i64 q = 0; q <= 2 * pmax; q++) probe[q] = q * (cap / (2 * pmax > 0 ? 2 * pmax : 1));
+    size_t bytes = overlap_batch_global_ws(probe.data(), pmax);
+    // a wave with fewer, longer pairs needs at most the single-pair workspace
+    i64 one[3] = {0, cap / 2, cap};
+    const size_t s1 = overlap_batch_global_ws(one, 1);
+    if (s1 > bytes) bytes = s1;
+    std::lock_guard<std::mutex> g(mu);
+    if (memo.size() >= 16) memo.erase(memo.begin());
+    memo.push_back({{cap, pmax}, bytes});
+    return bytes;
+}
+
 static size_t pairs_ws(Arena &ar, const i64 *offs, i64 P, PairsWs *w) {
     PairsWs t;
     t.offs = ar.alloc<i64>(2 * P + 1);
@@ -1060,16 +1103,7 @@ static size_t pairs_ws(Arena &ar, const i64 *offs, i64 P, PairsWs *w) {
     i64 pmax = t.cap / 2 + 1;  // pairs per fallback wave (each non-empty pair has >= 2 residues)
     if (pmax > P) pmax = P;
     t.fout = ar.alloc<i64>(3 * pmax + 3);
-    // worst-case wave-global workspace for a wave of <= cap residues over pmax pairs
-    std::vector<i64> probe(2 * pmax + 1);
-    for (i64 q = 0; q <= 2 * pmax; q++) probe[q] = q * (t.cap / (2 * pmax > 0 ? 2 * pmax : 1));
-    t.gws_bytes = t.cap > 0 ? overlap_batch_global_ws(probe.data(), pmax) : 0;
-    // a wave with fewer, longer pairs needs at most the single-pair workspace
-    if (t.cap > 0) {
-        i64 one[3] = {0, t.cap / 2, t.cap};
-        size_t s1 = overlap_batch_global_ws(one, 1);
-        if (s1 > t.gws_bytes) t.gws_bytes = s1;
-    }
+    t.gws_bytes = fb_global_ws(t.cap, pmax);
     t.gws = ar.alloc<char>((i64)t.gws_bytes);
     if (w) *w = t;
     return ar.peak;
@@ -1135,15 +1169,16 @@ extern "C" int saix_overlap_batch_dev(const uint8_t *seqs, const int64_t *offs_h
 
 // chunk counts 1, 2, ... as pinned host words: the flag copies behind each
 // chunk's bytes read from here (constant, so calls in flight never race)
+constexpr u32 kMaxStreamChunks = 4096 + 64;  // caller's chunks + the ramp
 static const u32 *ready_values() {
     static u32 *vals = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
-        if (cudaHostAlloc(&vals, 4097 * sizeof(u32), cudaHostAllocPortable) != cudaSuccess) {
+        if (cudaHostAlloc(&vals, (kMaxStreamChunks + 1) * sizeof(u32), cudaHostAllocPortable) != cudaSuccess) {
             vals = nullptr;
             return;
         }
-        for (u32 k = 0; k <= 4096; k++) vals[k] = k;
+        for (u32 k = 0; k <= kMaxStreamChunks; k++) vals[k] = k;
     });
     return vals;
 }
@@ -1220,7 +1255,7 @@ static int overlap_batch_run(const uint8_t *seqs, const int64_t *offs_host, cons
                 return SAIX_ECUDA;
             }
             cudaStream_t cs = (cudaStream_t)copy_stream;
-            const i64 per = (P + nchunks - 1) / nchunks;
+            const i64 per = (P + nchunks - 1) / nchunks, first = grid;
             cudaEvent_t e0, e1;
             SAIX_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
             SAIX_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
@@ -1228,10 +1263,10 @@ static int overlap_batch_run(const uint8_t *seqs, const int64_t *offs_host, cons
             SAIX_CUDA(cudaStreamWaitEvent(cs, e0, 0));
             pd::k_pair_dc3<false, true><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
                 seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr, w.ctr + 2,
-                (u32)per);
+                (u32)per, (u32)first);
             SAIX_LAUNCHED();
-            for (i64 c = 0; c * per < P; c++) {
-                const i64 a = c * per, b = (c + 1) * per < P ? (c + 1) * per : P;
+            for (i64 c = 0; pd::stream_avail(c, P, per, first) < P; c++) {
+                const i64 a = pd::stream_avail(c, P, per, first), b = pd::stream_avail(c + 1, P, per, first);
                 const i64 lo = offs_host[2 * a], hi = offs_host[2 * b];
                 if (hi > lo)
                     SAIX_CUDA(cudaMemcpyAsync((void *)(seqs + lo), host_seqs + lo, (size_t)(hi - lo),
@@ -1245,10 +1280,10 @@ static int overlap_batch_run(const uint8_t *seqs, const int64_t *offs_host, cons
         } else if (clocks_on()) {
             SAIX_CUDA(cudaMemsetAsync(w.clk, 0, sizeof(unsigned long long) * (pd::NPHASE + 2), st));
             pd::k_pair_dc3<true, false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
-                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk, nullptr, 0);
+                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk, nullptr, 0, 0);
         } else {
             pd::k_pair_dc3<false, false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
-                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr, nullptr, 0);
+                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr, nullptr, 0, 0);
         }
     }
     SAIX_LAUNCHED();
