@@ -86,6 +86,7 @@ constexpr int BIG_CAP = (OFF_Q - OFF_S0 - 2 * NB) / 2;  // u16 scratch after the
 constexpr int SMEM = OFF_MISC + 1024;
 static_assert(2 * NB <= OFF_Q - OFF_S0, "bucket counters must fit the S0 + RK region");
 static_assert(BIG_CAP >= 1024, "big-bucket scratch");
+static_assert(QCAP * WARPS >= MMAX / 2, "in-bucket sort queue: every bucket of >= 2 samples");
 static_assert(MMAX + KMAX >= NMAX + 1, "SA is written over the sample + non-sample runs");
 static_assert(SMEM <= 113 * 1024, "two CTAs per SM");
 
@@ -98,7 +99,7 @@ struct Misc {
     u32 nbig;
     u32 nlist;
     u32 big[MAXBIG][2];
-    u32 red32[WARPS];
+    u32 red32[WARPS];  // [0], [1]: the in-bucket sort queue's length / next entry
     unsigned long long red64[WARPS];
     u32 seg[WARPS + 1][3];
     long long t_prev;
@@ -149,27 +150,29 @@ struct Txt {
     // One comparison step of suffixes i != j at offset h.  0: equal so far
     // (continue at h + step()); 1: i < j; 2: i > j.  When decided, *lcp is
     // their longest common prefix.
+    // packed step on the 32-character words wi = ld32(i + h), wj = ld32(j + h)
+    // (h < L): the first differing character codes come from the words
+    __device__ __forceinline__ int cmp_words(u32 i, u32 j, u32 h, u64 wi, u64 wj, u32 &lcp) const {
+        const u32 li = lim(i), lj = lim(j), L = min(li, lj);
+        const u64 x = wi ^ wj;
+        if (!x && h + 32u < L) return 0;
+        const u32 b = x ? (u32)(__ffsll((long long)x) - 1) & ~1u : 64u;
+        const u32 d = h + (b >> 1);
+        if (d < L) {
+            lcp = d;
+            return ((wi >> b) & 3u) < ((wj >> b) & 3u) ? 1 : 2;
+        }
+        lcp = L;
+        if (li != lj) return li < lj ? 1 : 2;
+        return i > nA ? 1 : 2;  // equal distance: the end (pad) is below the separator
+    }
     __device__ __forceinline__ int cmp(u32 i, u32 j, u32 h, u32 &lcp) const {
         if (packed) {
-            const u32 li = lim(i), lj = lim(j), L = min(li, lj);
-            u32 d = L;
-            if (h < L) {
-                const u64 x = ld32(i + h) ^ ld32(j + h);
-                if (!x) {
-                    if (h + 32u < L) return 0;
-                } else {
-                    d = h + ((u32)(__ffsll((long long)x) - 1) >> 1);
-                }
-            }
-            if (d < L) {
-                lcp = d;
-                const u32 sh = 2u * ((i + d) & 31u), sj = 2u * ((j + d) & 31u);
-                const u32 ci = (u32)(P2[(i + d) >> 5] >> sh) & 3u, cj = (u32)(P2[(j + d) >> 5] >> sj) & 3u;
-                return ci < cj ? 1 : 2;
-            }
-            lcp = L;
+            if (h < min(lim(i), lim(j))) return cmp_words(i, j, h, ld32(i + h), ld32(j + h), lcp);
+            const u32 li = lim(i), lj = lim(j);
+            lcp = min(li, lj);
             if (li != lj) return li < lj ? 1 : 2;
-            return i > nA ? 1 : 2;  // equal distance: the end (pad) is below the separator
+            return i > nA ? 1 : 2;
         }
         const u64 a = ld8(T, i + h), b = ld8(T, j + h);
         if (a == b) return 0;
@@ -489,6 +492,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             ms.pair = atomicAdd(next_pair, 1u);
             ms.fail = 0;
             ms.nbig = 0;
+            ms.red32[0] = ms.red32[1] = 0;
             if (STREAM && ms.pair < P) {
                 for (;;) {
                     u32 c;
@@ -602,71 +606,82 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             // work (a per-lane loop over its own buckets serialises the lanes).
             constexpr int BPT = NB / THREADS;  // 32 buckets per lane, strided: the heavy
                                                // (A/T-rich) prefixes spread over all lanes
-            u16 *Q = QW + (tid >> 5) * QCAP;
+            u16 *Q = QW;  // one CTA-wide queue: warps pull buckets as they finish
             const u32 lane = lane_id(), lt = lanemask_lt();
-            for (int round = 0; round < BPT / QROUND; round++) {
-                u32 qn = 0;
+            // every lane offers its BPT buckets (strided, so the heavy A/T-rich
+            // prefixes spread over all lanes)
 #pragma unroll 4
-                for (int kk = 0; kk < QROUND; kk++) {
-                    const u32 b = tid + (u32)(round * QROUND + kk) * THREADS;
-                    const u32 st = b ? C16[b - 1] : 0u, sz = C16[b] - st;
-                    if (sz > (u32)SMALL) {
-                        const u32 at = atomicAdd(&ms.nbig, 1u);
-                        if (at < MAXBIG) {
-                            ms.big[at][0] = st;
-                            ms.big[at][1] = st + sz;
-                        } else ms.fail = 1;
-                    }
-                    const bool want = sz >= 2 && sz <= (u32)SMALL;
-                    const u32 mask = __ballot_sync(0xffffffffu, want);
-                    if (want) Q[qn + __popc(mask & lt)] = (u16)b;
-                    qn += __popc(mask);
+            for (int kk = 0; kk < BPT; kk++) {
+                const u32 b = tid + (u32)kk * THREADS;
+                const u32 st = b ? C16[b - 1] : 0u, sz = C16[b] - st;
+                if (sz > (u32)SMALL) {
+                    const u32 at = atomicAdd(&ms.nbig, 1u);
+                    if (at < MAXBIG) {
+                        ms.big[at][0] = st;
+                        ms.big[at][1] = st + sz;
+                    } else ms.fail = 1;
                 }
-                __syncwarp();
-                u32 taken = min(qn, 32u);  // tasks handed out so far (warp-uniform)
-                u32 start = 0, end = 0, i = 0, j = 0, x = 0, h = 0;
-                bool live = lane < qn;
+                const bool want = sz >= 2 && sz <= (u32)SMALL;
+                const u32 mask = __ballot_sync(0xffffffffu, want);
+                if (mask) {  // warp-uniform
+                    u32 base = 0;
+                    if (lane == 0) base = atomicAdd(&ms.red32[0], (u32)__popc(mask));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (want) Q[base + __popc(mask & lt)] = (u16)b;
+                }
+            }
+            __syncthreads();
+            const u32 qn = ms.red32[0];
+            u32 t0 = 0;
+            if (lane == 0) t0 = atomicAdd(&ms.red32[1], 32u);
+            t0 = __shfl_sync(0xffffffffu, t0, 0);
+            u32 start = 0, end = 0, i = 0, j = 0, x = 0, h = 0;
+            bool live = t0 + lane < qn;
+            if (live) {
+                const u32 b = Q[t0 + lane];
+                start = b ? C16[b - 1] : 0u;
+                end = C16[b];
+                i = j = start + 1;
+                x = SS[i];
+            }
+            while (__any_sync(0xffffffffu, live)) {
+                bool done = false;
                 if (live) {
-                    const u32 b = Q[lane];
-                    start = b ? C16[b - 1] : 0u;
-                    end = C16[b];
-                    i = j = start + 1;
-                    x = SS[i];
-                }
-                while (__any_sync(0xffffffffu, live)) {
-                    bool done = false;
-                    if (live) {
-                        const u32 y = SS[j - 1];
-                        u32 l_;
-                        const int c = tx.cmp(x, y, h, l_);
-                        if (c == 0) {
-                            h += tx.step();
-                            if (++work > WORK_MAX) {
-                                ms.fail = 1;
-                                live = false;
-                            }
-                        } else {
-                            const bool less = c == 1;
-                            h = 0;
-                            if (less) {
-                                SS[j] = (u16)y;
-                                j--;
-                            }
-                            if (!less || j == start) {
-                                SS[j] = (u16)x;
-                                if (++i < end) {
-                                    x = SS[i];
-                                            j = i;
-                                } else {
-                                    done = true;
-                                }
+                    const u32 y = SS[j - 1];
+                    u32 l_;
+                    const int c = tx.cmp(x, y, h, l_);
+                    if (c == 0) {
+                        h += tx.step();
+                        if (++work > WORK_MAX) {
+                            ms.fail = 1;
+                            live = false;
+                        }
+                    } else {
+                        const bool less = c == 1;
+                        h = 0;
+                        if (less) {
+                            SS[j] = (u16)y;
+                            j--;
+                        }
+                        if (!less || j == start) {
+                            SS[j] = (u16)x;
+                            if (++i < end) {
+                                x = SS[i];
+                                j = i;
+                            } else {
+                                done = true;
                             }
                         }
                     }
-                    // lanes that finished a bucket take the next queued ones
-                    const u32 dm = __ballot_sync(0xffffffffu, done);
+                }
+                // lanes that finished a bucket claim the next queued ones
+                const u32 dm = __ballot_sync(0xffffffffu, done);
+                if (dm) {
+                    u32 tb = 0;
+                    if (lane == 0) tb = atomicAdd(&ms.red32[1], (u32)__popc(dm));
+                    tb = __shfl_sync(0xffffffffu, tb, 0);
                     if (done) {
-                        const u32 t = taken + __popc(dm & lt);
+                        const u32 t = tb + __popc(dm & lt);
                         live = t < qn;
                         if (live) {
                             const u32 b = Q[t];
@@ -676,9 +691,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                             x = SS[i];
                         }
                     }
-                    taken += __popc(dm);
                 }
-                __syncwarp();
             }
             if (CLK) {
                 atomicMax((unsigned long long *)&ms.tmax, (unsigned long long)(clock64() - t_in));
