@@ -505,9 +505,11 @@ extern "C" int saix_sparse_query(const saix_sparse_plan *plan, const void *table
     cudaStream_t st = (cudaStream_t)stream;
     int g = grid_for(q, 256);
     PlanDev P = dev_plan(plan);
-    // 2 x int64 in, int64 out, two random table probes at one 32 B sector each
-    // (blocked mode: the probes are L2 hits; HBM sees the 24 B of queries)
-    Prof prof_("rmq.query", (plan->mode == SAIX_SPARSE_BLOCKED ? 24.0 : 88.0) * q, st);
+    // SURVEY.md 8(d) algorithmic bytes, every layout: 2 x int64 in, int64 out,
+    // two random table probes at one 32 B sector each = 88 B per query (the
+    // blocked layout's ~6 probes are sector-granular too: its 88 MB working
+    // set is past the random-access L2 knee, ~97 B/query of DRAM measured)
+    Prof prof_("rmq.query", 88.0 * q, st);
     if (value_bytes == 4)
         k_sparse_query<u32><<<g, 256, 0, st>>>(P, table, Vals<u32>{(const u32 *)values}, qi, qj, q, out_index, out_value, err);
     else
