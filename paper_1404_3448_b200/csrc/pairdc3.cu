@@ -443,31 +443,48 @@ __device__ __forceinline__ Seg block_seg_exclusive(Seg v, Misc &ms) {
     return carry;
 }
 
-// Streamed batches (saix_overlap_batch_stream): pairs available once chunks
-// 0..c-1 have landed.  The first chunk holds `first` pairs (one per CTA) and
-// sizes double up to `per`, so the kernel starts after a short copy instead of
-// a full 1/nchunks of the batch.
-__host__ __device__ __forceinline__ i64 stream_avail(i64 c, i64 P, i64 per, i64 first) {
-    i64 done = 0, s = first < per ? first : per;
-    for (i64 k = 0; k < c; k++) {
-        if (s >= per) {
-            done += (c - k) * per;
-            break;
-        }
-        done += s;
-        s *= 2;
+// Streamed batches (saix_overlap_batch_stream): the batch is copied in C
+// chunks; bounds[c] = pairs available once chunks 0..c-1 have landed.  Chunk
+// sizes ramp up from `first` pairs (one per CTA) by doubling to `per`, and
+// mirror that ramp down at the end: the kernel starts after a short copy and
+// finishes shortly after the last one.  Returns C (<= kMaxStreamChunks).
+constexpr u32 kMaxStreamChunks = 4096 + 64;  // the caller's chunks + both ramps
+__host__ __device__ inline int stream_plan(i64 P, i64 per, i64 first, u32 *bounds) {
+    i64 up[24];
+    int ku = 0;
+    i64 sum_up = 0;
+    for (i64 s = first; s < per && ku < 24; s *= 2) {
+        up[ku++] = s;
+        sum_up += s;
     }
-    return done < P ? done : P;
+    int c = 0;
+    i64 done = 0;
+    bounds[0] = 0;
+    auto push = [&](i64 sz) {
+        done = done + sz < P ? done + sz : P;
+        bounds[++c] = (u32)done;
+    };
+    if (2 * sum_up >= P) {  // small batch: uniform chunks
+        while (done < P) push(per);
+        return c;
+    }
+    for (int k = 0; k < ku; k++) push(up[k]);
+    const i64 mid_end = P - sum_up;
+    while (done < mid_end) push(mid_end - done < per ? mid_end - done : per);
+    for (int k = ku - 1; k >= 0; k--) push(up[k]);
+    return c;
 }
+
+__global__ void k_stream_bounds(u32 *bounds, i64 P, i64 per, i64 first) { stream_plan(P, per, first, bounds); }
 
 // STREAM: the batch's ASCII is still arriving (saix_overlap_batch_stream):
 // the copy engine publishes chunk c by writing c + 1 to *ready after its
-// bytes; a CTA takes pair p only once stream_avail(ready) > p.
+// bytes; a CTA takes pair p only once bounds[ready] > p.
 template <bool CLK, bool STREAM>
 __global__ void __launch_bounds__(THREADS, 2)
 k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int keep_n, i64 *__restrict__ out,
            i64 *__restrict__ bad, u32 *__restrict__ next_pair, u32 *__restrict__ nfb, u32 *__restrict__ fb,
-           int nmax, unsigned long long *__restrict__ clk, const u32 *ready, u32 per, u32 first) {
+           int nmax, unsigned long long *__restrict__ clk, const u32 *ready, const u32 *bounds) {
     extern __shared__ __align__(16) unsigned char smem[];
     u8 *T = smem + OFF_T;
     u16 *SS = reinterpret_cast<u16 *>(smem + OFF_SS);
@@ -497,7 +514,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                 for (;;) {
                     u32 c;
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ready) : "memory");
-                    if (stream_avail(c, P, per, first) > (i64)ms.pair) break;
+                    if (bounds[c] > ms.pair) break;
                     __nanosleep(256);
                 }
             }
@@ -1056,6 +1073,7 @@ struct PairsWs {
     i64 *offs;     // device copy of the caller's offsets
     u32 *ctr;      // [0] next pair, [1] fallback count
     u32 *fb;       // fallback pair list
+    u32 *bounds;   // streamed chunk plan (pd::stream_plan)
     unsigned long long *clk;  // phase clocks (SAIX_PD_CLOCKS=1)
     i64 *dummy_bad;
     u8 *fseqs;     // compacted fallback residues
@@ -1109,6 +1127,7 @@ static size_t pairs_ws(Arena &ar, const i64 *offs, i64 P, PairsWs *w) {
     t.offs = ar.alloc<i64>(2 * P + 1);
     t.ctr = ar.alloc<u32>(4);
     t.fb = ar.alloc<u32>(P);
+    t.bounds = ar.alloc<u32>(pd::kMaxStreamChunks + 1);
     t.clk = ar.alloc<unsigned long long>(pd::NPHASE + 2);
     t.dummy_bad = ar.alloc<i64>(1);
     t.cap = fb_capacity(offs, P);
@@ -1182,8 +1201,8 @@ extern "C" int saix_overlap_batch_dev(const uint8_t *seqs, const int64_t *offs_h
 
 // chunk counts 1, 2, ... as pinned host words: the flag copies behind each
 // chunk's bytes read from here (constant, so calls in flight never race)
-constexpr u32 kMaxStreamChunks = 4096 + 64;  // caller's chunks + the ramp
 static const u32 *ready_values() {
+    using pd::kMaxStreamChunks;
     static u32 *vals = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -1269,6 +1288,10 @@ static int overlap_batch_run(const uint8_t *seqs, const int64_t *offs_host, cons
             }
             cudaStream_t cs = (cudaStream_t)copy_stream;
             const i64 per = (P + nchunks - 1) / nchunks, first = grid;
+            std::vector<u32> hb(pd::kMaxStreamChunks + 1);
+            const int C = pd::stream_plan(P, per, first, hb.data());
+            pd::k_stream_bounds<<<1, 1, 0, st>>>(w.bounds, P, per, first);  // the same plan, for the gate
+            SAIX_LAUNCHED();
             cudaEvent_t e0, e1;
             SAIX_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
             SAIX_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
@@ -1276,10 +1299,10 @@ static int overlap_batch_run(const uint8_t *seqs, const int64_t *offs_host, cons
             SAIX_CUDA(cudaStreamWaitEvent(cs, e0, 0));
             pd::k_pair_dc3<false, true><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
                 seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr, w.ctr + 2,
-                (u32)per, (u32)first);
+                w.bounds);
             SAIX_LAUNCHED();
-            for (i64 c = 0; pd::stream_avail(c, P, per, first) < P; c++) {
-                const i64 a = pd::stream_avail(c, P, per, first), b = pd::stream_avail(c + 1, P, per, first);
+            for (int c = 0; c < C; c++) {
+                const i64 a = hb[c], b = hb[c + 1];
                 const i64 lo = offs_host[2 * a], hi = offs_host[2 * b];
                 if (hi > lo)
                     SAIX_CUDA(cudaMemcpyAsync((void *)(seqs + lo), host_seqs + lo, (size_t)(hi - lo),
@@ -1293,10 +1316,10 @@ static int overlap_batch_run(const uint8_t *seqs, const int64_t *offs_host, cons
         } else if (clocks_on()) {
             SAIX_CUDA(cudaMemsetAsync(w.clk, 0, sizeof(unsigned long long) * (pd::NPHASE + 2), st));
             pd::k_pair_dc3<true, false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
-                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk, nullptr, 0, 0);
+                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk, nullptr, nullptr);
         } else {
             pd::k_pair_dc3<false, false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
-                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr, nullptr, 0, 0);
+                seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), nullptr, nullptr, nullptr);
         }
     }
     SAIX_LAUNCHED();
