@@ -256,3 +256,23 @@ def test_stream_entry_rejects_blocking_copy_stream():
     assert b"NonBlocking" in L.saix_last_error()
     ob.run_from_host(host)  # the default path still works afterwards
     assert np.array_equal(ob.results(), oracle.overlap_batch(seqs, offs))
+
+
+@pytest.mark.parametrize("stream_chunks", [4, 64])
+def test_run_from_host_ramped_chunk_plan(stream_chunks):
+    """A batch big enough for the streamed chunk plan's ramps (chunks of 296,
+    592, 1184 pairs at both ends around the uniform ones, pd::stream_plan):
+    answers equal the oracle, and an illegal residue inside the last, smallest
+    chunk is reported at its absolute offset."""
+    import torch
+    seqs, offs = c4_pairs(0, 5000)
+    want = oracle.overlap_batch(seqs, offs, threads=16)
+    ob = sx.OverlapBatch(seqs, offs)
+    host = torch.from_numpy(seqs.copy()).pin_memory()
+    ob.seqs_dev.zero_()
+    ob.run_from_host(host, stream_chunks=stream_chunks)
+    assert np.array_equal(ob.results(), want)
+    bad_at = int(offs[2 * 4990]) + 5
+    host[bad_at] = ord("Z")
+    ob.run_from_host(host, stream_chunks=stream_chunks)
+    assert ob.first_bad() == bad_at
