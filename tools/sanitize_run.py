@@ -58,6 +58,16 @@ def main():
     ob = sx.OverlapBatch(seqs, offs)
     ob.run_device()
     step("OverlapBatch", np.array_equal(ob.results(), oracle.overlap_batch(seqs, offs)))
+    # the same kernel gated on a streamed host batch (ramped chunk plan: 1000
+    # short pairs in 2 chunks -> 296 + 408 + 296 pairs)
+    import torch
+    rng = np.random.default_rng(5)
+    lens = rng.integers(20, 200, 2000)
+    sseqs = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, int(lens.sum()))]
+    soffs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    sb = sx.OverlapBatch(sseqs, soffs)
+    sb.run_from_host(torch.from_numpy(sseqs.copy()).pin_memory(), stream_chunks=2)
+    step("OverlapBatch (streamed)", np.array_equal(sb.results(), oracle.overlap_batch(sseqs, soffs)))
     # parallel-sort engine
     keys = np.random.default_rng(9).integers(0, 1 << 31, 50000)
     step("radix_sort", np.array_equal(sx.radix_sort(keys), np.sort(keys, kind="stable")))
