@@ -1,4 +1,6 @@
-// abi.cu -- error reporting and version entry points of libsaix_b200.so.
+// abi.cu -- error reporting and version entry points of libsaix_b200.so
+// (status codes + thread-local message; the Python layer maps them to the
+// reference's exception types, e.g. SequenceError, sequence.py:152-156).
 #include <cstdarg>
 #include <cstring>
 #include <map>

@@ -1,4 +1,6 @@
-// bsort.cuh -- MSD bucket sort for wide keys (large-alphabet DC3 levels).
+// bsort.cuh -- MSD bucket sort for wide keys (large-alphabet DC3 levels):
+// the sort behind _name_triples' lexicographic triple order (reference
+// suffix_index.py:221-253, via _lexsort_keys / _pack_keys, 57-82).
 //
 // Deep DC3 levels sort items whose keys span a large range (level-2 triples
 // of DNA: 3 x 18-bit names); LSD radix needs 7 passes of 8 bits there.  Here

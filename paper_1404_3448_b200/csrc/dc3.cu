@@ -39,6 +39,8 @@ struct Text {
 };
 
 // ------------------------------------------------------------ naming
+// Triple naming of the samples: _name_triples (suffix_index.py:221-253), the
+// sample positions of _sample_positions (149-155) over _padded (143-147).
 // A tile of a byte text staged in shared memory with aligned 4-byte loads
 // (coalesced; the per-character loads of the triple kernels hit shared
 // memory instead of issuing one global byte load each).  Covers absolute
@@ -376,6 +378,8 @@ __global__ void k_unique_from_sorted(const u32 *__restrict__ vals, i64 m, u32 *_
 }
 
 // ------------------------------------------------------------ mod-0 order
+// _sort_nonsamples (suffix_index.py:274-290): non-samples 3j ordered by
+// (T[3j], rank of 3j+1).
 
 // ------------------------------------------------------------ merge
 
@@ -725,6 +729,8 @@ static int merge_run(V v, i64 na, i64 nb, u32 *split, u32 *sa, u32 *isa, cudaStr
 inline i64 merge_split_words(i64 total) { return ceil_div(total > 0 ? total : 1, MT_TILE) + 2; }
 
 // ------------------------------------------------------------ streaming level (u8 text)
+// One level of _dc3 (suffix_index.py:381-392) after the sample sort:
+// _sort_nonsamples (274-290) and _merge / _merge_walk (362-378, 173-218).
 //
 // Levels with a byte text (sigma < 256: DNA levels 0-1) avoid every random
 // gather of the merge and of the mod-0 split.  Each suffix the merge needs is
@@ -1412,6 +1418,9 @@ __global__ void k_iota_pair(u32 *sa, u32 *isa, i64 n) {
 }
 
 // ------------------------------------------------------------ driver
+// _dc3 (suffix_index.py:381-392) / build_sa_dc3 (395-399): per level, name the
+// samples, recurse (_sort_samples, 256-271) unless the names are unique,
+// order the non-samples, merge; SuffixArray.from_order (96-101) is the ISA.
 
 constexpr int K_THREADS = 256;
 constexpr u64 kBitmapMaxCodes = (u64)1 << 31;
@@ -1481,6 +1490,8 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
                      saix_dc3_probe *probe, int depth, u32 *Phi = nullptr, bool *phi_done = nullptr);
 
 // ------------------------------------------------------------ wide-level finish
+// (the _sort_nonsamples / _merge steps, suffix_index.py:274-290, 362-378, of a
+// u32 level)
 //
 // A u32 level whose sample triples are all distinct (the deepest level of
 // DNA-like texts) gets its merge inputs as records built in sorted order,
@@ -1824,6 +1835,8 @@ static int dc3_level_stream(Dc3Ctx &c, const u8 *text, i64 N, u64 sigma, u32 *SA
                             bool *phi_done, int depth);
 
 // ------------------------------------------------------------ tie resolution
+// (replaces the recursion of _sort_samples, suffix_index.py:256-271, when only
+// a few sample names repeat; the order is the one the recursion returns)
 //
 // When a level's sample names are almost all distinct (m - names <= m/32;
 // e.g. the deep levels of DNA pairs with planted repeats), the recursion
@@ -2474,6 +2487,8 @@ static int dc3_level(Dc3Ctx &c, const TT *text, i64 N, u64 sigma, u32 *SA, u32 *
 // Streaming level (see "streaming level" above).  SA / ISA / Phi nullable;
 // Phi is produced only when ISA is not requested (*phi_done tells).
 // ------------------------------------------------ level-0 window naming
+// (replaces _name_triples + the recursion of _sort_samples, suffix_index.py:
+// 221-271, on level 0 of byte texts; same sample order)
 // Byte levels with sigma <= 7: name every sample by its 21-character window
 // (3 bits per character, u64 key, 0 past the end) instead of its triple.  The
 // reduced string's suffix order is unchanged -- equal names mean equal 21

@@ -1,6 +1,8 @@
 // lcp_direct.cuh -- word-compare matching of two suffixes (lcp.cu direct
 // LCP, and the batched-pairs LCP in overlap.cu): a 2-bit packed copy of the
 // text (32 characters per 64-bit word, LSB first) or the byte text itself.
+// lcp[r] = longest common prefix of suffixes sa[r-1], sa[r] -- the values
+// _kasai_scan / build_lcp produce (reference suffix_index.py:461-506).
 #pragma once
 
 #include "common.cuh"

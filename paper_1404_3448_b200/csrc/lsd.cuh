@@ -1,5 +1,7 @@
 // lsd.cuh -- stable LSD radix partition of u32 payloads by a computed key,
-// 8 bits per pass, as three streaming kernels per pass (no look-back chain):
+// 8 bits per pass, as three streaming kernels per pass (no look-back chain);
+// the stable counting pass of _counting_reorder (reference suffix_index.py:
+// 157-171) at batch scale:
 //
 //   k_lsd_hist     per 4096-item tile, the digit histogram -> hist[d][tile]
 //                  (digit-major, so one flat exclusive scan gives every

@@ -5,8 +5,10 @@
 // scattered partial-line writes even inside a small window: a 4 B scatter
 // confined to 256 KB windows still moves ~4x its bytes through DRAM
 // (tools/wprobe.cu, profiles/r1_window_scatter_probe.txt).  Every DC3 level
-// has such permutations (ISA, sample records by rank, Phi), so they are done
-// as three streaming passes whose global writes are all contiguous runs:
+// has such permutations (ISA = SuffixArray.from_order, reference
+// suffix_index.py:96-101; the rank_of tables of _sort_samples / _merge,
+// 256-271 / 362-378; Kasai's Phi, 461-476), so they are done as three
+// streaming passes whose global writes are all contiguous runs:
 //
 //   pass A  (inside the producing kernel, ps_block_emit): a CTA's items are
 //           bucketed in shared memory by dest >> s1 and each bucket's run is

@@ -1,6 +1,9 @@
 // wsort.cuh -- level-0 window naming for DNA texts (ranks 1..4, or the
 // generalized text's residues 2..5 around one separator; N < 2^29): an MSD
-// sort of the samples' 21-character windows in streaming passes.
+// sort of the samples' 21-character windows in streaming passes.  It stands
+// in for _name_triples + the recursion of _sort_samples (reference
+// suffix_index.py:221-271) on level 0 and yields the same sample order; the
+// separator handling follows GeneralizedText.build (overlap.py:83-95).
 //
 // The generic window sort (bsort.cuh over WindowSrc) builds 63-bit keys
 // twice from unaligned global words, moves 16 B staging records through two
