@@ -1314,12 +1314,21 @@ k_merge_tile_rec(View v, i64 na, i64 nb, const u32 *__restrict__ split, u32 *__r
             else hi = mid;
         }
         int i = lo, j = dt - lo;
+        u32 o[RM_ITEMS];
 #pragma unroll
         for (int r = 0; r < RM_ITEMS; r++) {
-            if (dt + r >= cnt) break;
-            bool takeA = j >= nbt || (i < nat && keys_a_first(k1[i], B1, B2, j));
-            out[dt + r] = takeA ? pos[i++] : pos[nat + j++];
+            o[r] = 0;
+            if (dt + r < cnt) {
+                bool takeA = j >= nbt || (i < nat && keys_a_first(k1[i], B1, B2, j));
+                o[r] = takeA ? pos[i++] : pos[nat + j++];
+            }
         }
+        static_assert(RM_ITEMS == 4, "one 16-byte store per thread");
+        if (dt + RM_ITEMS <= cnt) *reinterpret_cast<uint4 *>(out + dt) = make_uint4(o[0], o[1], o[2], o[3]);
+        else
+#pragma unroll
+            for (int r = 0; r < RM_ITEMS; r++)
+                if (dt + r < cnt) out[dt + r] = o[r];
     }
     __syncthreads();
     if (sa)
