@@ -863,10 +863,14 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                 }
             }
             __syncthreads();
-            if (d0 < n) {
+            if (d0 < n) {  // 16-byte stores (a thread's 40 outputs start 80 bytes apart:
+                           // conflict-free at this width); zeros past n stay inside SS + S0
+                static_assert(ITEMS % 8 == 0 && ITEMS * THREADS <= MMAX + KMAX, "whole 8-output groups");
 #pragma unroll
-                for (int q = 0; q < ITEMS / 2; q++)
-                    if (d0 + 2 * q < n) reinterpret_cast<u32 *>(SA)[(d0 >> 1) + q] = outw[q];
+                for (int g = 0; g < ITEMS / 8; g++)
+                    if (d0 + 8 * g < n)
+                        reinterpret_cast<uint4 *>(SA + d0)[g] =
+                            make_uint4(outw[4 * g], outw[4 * g + 1], outw[4 * g + 2], outw[4 * g + 3]);
             }
         }
         __syncthreads();
@@ -881,28 +885,41 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             // 2-bit text: one 32-character word compare decides almost every
             // pair; the word of rank r's suffix is reused as rank r+1's
             // predecessor word
+            // SA read 8 ranks per 16-byte load, LC written 8 per 8-byte store
+            // (a thread's 40 ranks start 80 / 40 bytes apart: conflict-free at
+            // these widths, 4-way / 2-way for single ranks)
             if (r0 < n) {
                 u32 prev = r0 ? SA[r0 - 1] : 0u;
                 u64 wp = r0 ? tx.ld32(prev) : 0ull;
-                for (u32 q = 0; q < (u32)ITEMS && r0 + q < n; q++) {
-                    const u32 cur = SA[r0 + q];
-                    const u64 wc = tx.ld32(cur);
-                    u32 l = 0;
-                    if (r0 + q) {
-                        const u32 L = min(tx.lim(prev), tx.lim(cur));
-                        u64 x = wp ^ wc;
-                        u32 h = 0;
-                        while (!x && h + 32u < L) {
-                            h += 32u;
-                            x = tx.ld32(prev + h) ^ tx.ld32(cur + h);
+                const u32 cnt = min((u32)ITEMS, n - r0);
+                for (u32 q0 = 0; q0 < cnt; q0 += 8) {
+                    const uint4 sv4 = reinterpret_cast<const uint4 *>(SA + r0)[q0 >> 3];  // inside SS + S0
+                    const u32 svw[4] = {sv4.x, sv4.y, sv4.z, sv4.w};
+                    u64 lcw = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        if (q0 + k < cnt) {
+                            const u32 cur = (svw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+                            const u64 wc = tx.ld32(cur);
+                            u32 l = 0;
+                            if (r0 + q0 + k) {
+                                const u32 L = min(tx.lim(prev), tx.lim(cur));
+                                u64 x = wp ^ wc;
+                                u32 h = 0;
+                                while (!x && h + 32u < L) {
+                                    h += 32u;
+                                    x = tx.ld32(prev + h) ^ tx.ld32(cur + h);
+                                }
+                                l = x ? min(L, h + ((u32)(__ffsll((long long)x) - 1) >> 1)) : L;
+                                const bool cross = prev != nA && cur != nA && ((prev < nA) != (cur < nA));
+                                if (cross) mx = max(mx, l);
+                            }
+                            lcw |= (u64)min(l, 255u) << (8 * k);
+                            prev = cur;
+                            wp = wc;
                         }
-                        l = x ? min(L, h + ((u32)(__ffsll((long long)x) - 1) >> 1)) : L;
-                        const bool cross = prev != nA && cur != nA && ((prev < nA) != (cur < nA));
-                        if (cross) mx = max(mx, l);
                     }
-                    LC[r0 + q] = (u8)min(l, 255u);
-                    prev = cur;
-                    wp = wc;
+                    reinterpret_cast<u64 *>(LC + r0)[q0 >> 3] = lcw;  // bytes past n: inside the RK region
                 }
             }
 #pragma unroll
