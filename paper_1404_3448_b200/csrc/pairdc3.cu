@@ -635,11 +635,18 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             u16 *Q = QW;  // one CTA-wide queue: warps pull buckets as they finish
             const u32 lane = lane_id(), lt = lanemask_lt();
             // every lane offers its BPT buckets (strided, so the heavy A/T-rich
-            // prefixes spread over all lanes)
+            // prefixes spread over all lanes).  A warp reserves its whole share
+            // of the queue with one atomic (per-kk reservations from 16 warps
+            // serialised on the one counter), then writes it in kk order.
+            static_assert(BPT <= 32, "one bit per bucket of a lane");
+            u32 wbits = 0, wtotal = 0;
 #pragma unroll 4
             for (int kk = 0; kk < BPT; kk++) {
                 const u32 b = tid + (u32)kk * THREADS;
-                const u32 st = b ? C16[b - 1] : 0u, sz = C16[b] - st;
+                const u32 end = C16[b];
+                u32 st = __shfl_up_sync(0xffffffffu, end, 1);  // bucket b-1 is lane l-1's
+                if (lane == 0) st = b ? C16[b - 1] : 0u;
+                const u32 sz = end - st;
                 if (sz > (u32)SMALL) {
                     const u32 at = atomicAdd(&ms.nbig, 1u);
                     if (at < MAXBIG) {
@@ -648,12 +655,19 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                     } else ms.fail = 1;
                 }
                 const bool want = sz >= 2 && sz <= (u32)SMALL;
-                const u32 mask = __ballot_sync(0xffffffffu, want);
-                if (mask) {  // warp-uniform
-                    u32 base = 0;
-                    if (lane == 0) base = atomicAdd(&ms.red32[0], (u32)__popc(mask));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (want) Q[base + __popc(mask & lt)] = (u16)b;
+                wbits |= (u32)want << kk;
+                wtotal += __popc(__ballot_sync(0xffffffffu, want));
+            }
+            {
+                u32 base = 0;
+                if (lane == 0 && wtotal) base = atomicAdd(&ms.red32[0], wtotal);
+                base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll 4
+                for (int kk = 0; kk < BPT; kk++) {
+                    const bool want = (wbits >> kk) & 1u;
+                    const u32 mask = __ballot_sync(0xffffffffu, want);
+                    if (want) Q[base + __popc(mask & lt)] = (u16)(tid + (u32)kk * THREADS);
+                    base += __popc(mask);
                 }
             }
             __syncthreads();
