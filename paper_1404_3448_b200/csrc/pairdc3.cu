@@ -672,9 +672,14 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             }
             __syncthreads();
             const u32 qn = ms.red32[0];
+            // queue entries are claimed 32 at a time per warp (one atomic on the
+            // shared counter per 32 buckets, not one per step); [cnext, cend) is
+            // the warp's claimed, unassigned remainder (warp-uniform)
+            constexpr u32 QCLAIM = 32;
             u32 t0 = 0;
-            if (lane == 0) t0 = atomicAdd(&ms.red32[1], 32u);
+            if (lane == 0) t0 = atomicAdd(&ms.red32[1], 2 * QCLAIM);
             t0 = __shfl_sync(0xffffffffu, t0, 0);
+            u32 cnext = t0 + 32, cend = t0 + 2 * QCLAIM;
             u32 start = 0, end = 0, i = 0, j = 0, x = 0, h = 0;
             bool live = t0 + lane < qn;
             if (live) {
@@ -717,11 +722,15 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                 // lanes that finished a bucket claim the next queued ones
                 const u32 dm = __ballot_sync(0xffffffffu, done);
                 if (dm) {
-                    u32 tb = 0;
-                    if (lane == 0) tb = atomicAdd(&ms.red32[1], (u32)__popc(dm));
-                    tb = __shfl_sync(0xffffffffu, tb, 0);
+                    const u32 need = __popc(dm), avail = cend - cnext;
+                    u32 nb = 0;
+                    if (need > avail) {  // warp-uniform
+                        if (lane == 0) nb = atomicAdd(&ms.red32[1], QCLAIM);
+                        nb = __shfl_sync(0xffffffffu, nb, 0);
+                    }
                     if (done) {
-                        const u32 t = tb + __popc(dm & lt);
+                        const u32 rk = __popc(dm & lt);
+                        const u32 t = rk < avail ? cnext + rk : nb + (rk - avail);
                         live = t < qn;
                         if (live) {
                             const u32 b = Q[t];
@@ -730,6 +739,12 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                             i = j = start + 1;
                             x = SS[i];
                         }
+                    }
+                    if (need > avail) {
+                        cnext = nb + (need - avail);
+                        cend = nb + QCLAIM;
+                    } else {
+                        cnext += need;
                     }
                 }
             }
