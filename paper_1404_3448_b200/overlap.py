@@ -215,14 +215,80 @@ def _pipeline(na: int, nb: int) -> "OverlapPipeline":
     return p
 
 
+# Largest pair (|A| + 1 + |B| generalized-text residues) the on-chip pair
+# kernel solves in one CTA (pd::NMAX, csrc/pairdc3.cu)
+ONCHIP_RESIDUES = 20480
+
+
+class SmallPairPipeline:
+    """``longest_overlap`` of one pair of up to ONCHIP_RESIDUES residues
+    through the on-chip pair kernel (saix_overlap_batch, one pair): a single
+    launch instead of the multi-pass DC3 pipeline.  One instance serves every
+    pair shape: buffers are sized for the largest pair, A and B are copied
+    back to back into one pinned staging buffer and moved with one H2D copy."""
+
+    def __init__(self):
+        t = _lib.torch()
+        L = _lib.load()
+        dev = _lib.device()
+        cap = ONCHIP_RESIDUES
+        self.seqs = t.empty(cap, dtype=t.uint8, device=dev)
+        self.res = t.zeros(4, dtype=t.int64, device=dev)     # out3 + bad offset
+        self.hseqs = t.empty(cap, dtype=t.uint8, pin_memory=True)
+        self.hres = t.empty(4, dtype=t.int64, pin_memory=True)
+        # workspace for the largest pair, whatever its A/B split
+        need = max(L.saix_overlap_batch_workspace_bytes(
+            np.array([0, na, cap - 1], dtype=np.int64).ctypes.data, 1) for na in (1, cap // 2, cap - 2))
+        self.ws = _lib.workspace(need)
+
+    def run(self, a_host: np.ndarray, b_host: np.ndarray, policy: NPolicy = NPolicy.REJECT) -> np.ndarray:
+        """Host ASCII in, host int64[4] (length, pos_a, pos_b, bad) out, bad in
+        saix_longest_overlap's convention (generalized-text position: B's
+        residue k at |A| + 1 + k; INT64_MAX when every residue is legal)."""
+        na, nb = len(a_host), len(b_host)
+        h = self.hseqs.numpy()
+        h[:na] = a_host
+        h[na: na + nb] = b_host
+        self.seqs[: na + nb].copy_(self.hseqs[: na + nb], non_blocking=True)
+        offs = np.array([0, na, na + nb], dtype=np.int64)
+        r = self.res
+        rc = _lib.load().saix_overlap_batch(_lib.ptr(self.seqs), offs.ctypes.data, 1, int(policy is NPolicy.KEEP),
+                                            _lib.ptr(r), _lib.ptr(r) + 24, _lib.ptr(self.ws), self.ws.numel(),
+                                            _lib.stream_ptr())
+        _lib.check(rc, "saix_overlap_batch")
+        self.hres.copy_(r, non_blocking=True)
+        _lib.torch().cuda.current_stream().synchronize()
+        out = self.hres.numpy().copy()
+        if out[3] != INT64_MAX and out[3] >= na:   # batch offsets put B right after A
+            out[3] += 1
+        return out
+
+
+_SMALL: dict = {}
+
+
+def _small_pipeline() -> SmallPairPipeline:
+    import threading
+    key = (_lib.torch().cuda.current_device(), threading.get_ident())
+    p = _SMALL.get(key)
+    if p is None:
+        p = _SMALL[key] = SmallPairPipeline()
+    return p
+
+
 def longest_overlap(a: DnaSequence, b: DnaSequence,
                     policy: NPolicy = NPolicy.REJECT) -> OverlapResult:
     """Longest common substring of A and B via the generalized suffix array
-    (overlap.py:110-152), ties to the smallest A position then B position."""
+    (overlap.py:110-152), ties to the smallest A position then B position.
+    Pairs of up to ONCHIP_RESIDUES residues run in one CTA's shared memory
+    (SmallPairPipeline), longer ones through the device DC3 pipeline."""
     if len(a) == 0 or len(b) == 0:
         return OverlapResult(0, 0, 0)
     ha, hb = _ascii(a), _ascii(b)
-    res = _pipeline(len(ha), len(hb)).run(ha, hb, policy)
+    if len(ha) + len(hb) + 1 <= ONCHIP_RESIDUES:
+        res = _small_pipeline().run(ha, hb, policy)
+    else:
+        res = _pipeline(len(ha), len(hb)).run(ha, hb, policy)
     bad = int(res[3])
     if bad != INT64_MAX:
         if bad < len(ha):
