@@ -823,17 +823,30 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                 base[c] = acc;
                 acc += (u32)(((c <= 4 ? t0 : t1) >> (16 * (c <= 4 ? c - 1 : c - 5))) & 0xFFFFu);
             }
+            // this thread's cursors, packed like the counts (16-bit lanes: codes
+            // 1-4 in pb0, 5-6 in pb1; every cursor < n < 2^16), so placing a
+            // non-sample is one shift + add instead of a select over six
+            unsigned long long pb0 = 0, pb1 = 0;
 #pragma unroll
-            for (int c = 1; c <= 6; c++)
-                base[c] += (u32)(((c <= 4 ? e0 : e1) >> (16 * (c <= 4 ? c - 1 : c - 5))) & 0xFFFFu);
+            for (int c = 1; c <= 6; c++) {
+                const u32 v = base[c] + (u32)(((c <= 4 ? e0 : e1) >> (16 * (c <= 4 ? c - 1 : c - 5))) & 0xFFFFu);
+                if (c <= 4) pb0 |= (unsigned long long)v << (16 * (c - 1));
+                else pb1 |= (unsigned long long)v << (16 * (c - 5));
+            }
             for (u32 r = r0; r < r1; r++) {
                 const u32 s = SS[r];
                 if (s % 3u == 1u) {
                     const u32 c = T[s - 1];
-                    u32 at = 0;
-#pragma unroll
-                    for (int cc = 1; cc <= 6; cc++)
-                        if (c == (u32)cc) at = base[cc]++;
+                    u32 at;
+                    if (c <= 4) {
+                        const u32 sh = 16u * (c - 1u);
+                        at = (u32)(pb0 >> sh) & 0xFFFFu;
+                        pb0 += 1ull << sh;
+                    } else {
+                        const u32 sh = 16u * (c - 5u);
+                        at = (u32)(pb1 >> sh) & 0xFFFFu;
+                        pb1 += 1ull << sh;
+                    }
                     S0[at] = (u16)(s - 1);
                 }
             }
