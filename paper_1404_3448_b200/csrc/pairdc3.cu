@@ -497,6 +497,8 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
     u64 *P2 = reinterpret_cast<u64 *>(smem + OFF_P2);
     Misc &ms = *reinterpret_cast<Misc *>(smem + OFF_MISC);
     const u32 tid = threadIdx.x;
+    // in-bucket sort counters of this warp / thread 0 (SAIX_PD_CLOCKS=1 only)
+    unsigned long long clk_steps = 0, clk_wsteps = 0, clk_q = 0;
     if (CLK && tid == 0) {
         ms.t_prev = clock64();
         for (int k = 0; k < NPHASE; k++) ms.acc[k] = 0;
@@ -593,15 +595,43 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                 loc[4 * k + 2] = x.z;
                 loc[4 * k + 3] = x.w;
             }
+            // the same pass builds the in-bucket sort's queue: buckets of
+            // 2..SMALL samples (bit 2k / 2k+1 of wm), counted here and packed
+            // above the sample count (m < 2^16), so one block scan yields both
+            // offsets; buckets over SMALL (rare) go to the big list as
+            // (bucket, size) -- their start is end - size after the scatter
+            u32 wm = 0, bm = 0;
 #pragma unroll
-            for (int k = 0; k < W; k++) sum += (loc[k] & 0xFFFFu) + (loc[k] >> 16);
+            for (int k = 0; k < W; k++) {
+                const u32 c0 = loc[k] & 0xFFFFu, c1 = loc[k] >> 16;
+                sum += c0 + c1;
+                wm |= (u32)(c0 - 2u <= (u32)SMALL - 2u) << (2 * k) | (u32)(c1 - 2u <= (u32)SMALL - 2u) << (2 * k + 1);
+                bm |= (u32)(c0 > (u32)SMALL) << (2 * k) | (u32)(c1 > (u32)SMALL) << (2 * k + 1);
+            }
+            const u32 b0 = tid * (2 * W);
+            while (bm) {
+                const u32 b = b0 + (u32)(__ffs(bm) - 1);
+                bm &= bm - 1;
+                const u32 at = atomicAdd(&ms.nbig, 1u);
+                if (at < MAXBIG) {
+                    ms.big[at][0] = b;
+                    ms.big[at][1] = reinterpret_cast<const u16 *>(CNT)[b];  // still the count
+                } else ms.fail = 1;
+            }
             u32 tot;
-            u32 run = block_exsum<u32>(sum, tot, ms.scan32);
+            u32 run = block_exsum<u32>(sum | ((u32)__popc(wm) << 16), tot, ms.scan32);
+            u32 qat = run >> 16;
+            run &= 0xFFFFu;
+            if (tid == 0) ms.red32[0] = tot >> 16;  // the queue's length
 #pragma unroll
             for (int k = 0; k < W; k++) {
                 const u32 lo = run, hi = run + (loc[k] & 0xFFFFu);
                 run = hi + (loc[k] >> 16);
                 loc[k] = lo | (hi << 16);
+            }
+            while (wm) {
+                QW[qat++] = (u16)(b0 + (u32)(__ffs(wm) - 1));
+                wm &= wm - 1;
             }
 #pragma unroll
             for (int k = 0; k < W / 4; k++) C4[k] = make_uint4(loc[4 * k], loc[4 * k + 1], loc[4 * k + 2], loc[4 * k + 3]);
@@ -625,53 +655,16 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             const long long t_in = CLK ? clock64() : 0;
             u32 work = 0;
             const u16 *C16 = reinterpret_cast<const u16 *>(CNT);
-            // Insertion sort of every bucket of 2..SMALL samples, one 8-character
-            // word compare per step.  Buckets are collected into a per-warp queue
-            // (a round of 8 buckets per lane) and the warp's lanes pull buckets
-            // from it as they finish, so the lanes run in lock step with balanced
-            // work (a per-lane loop over its own buckets serialises the lanes).
-            constexpr int BPT = NB / THREADS;  // 32 buckets per lane, strided: the heavy
-                                               // (A/T-rich) prefixes spread over all lanes
-            u16 *Q = QW;  // one CTA-wide queue: warps pull buckets as they finish
-            const u32 lane = lane_id(), lt = lanemask_lt();
-            // every lane offers its BPT buckets (strided, so the heavy A/T-rich
-            // prefixes spread over all lanes).  A warp reserves its whole share
-            // of the queue with one atomic (per-kk reservations from 16 warps
-            // serialised on the one counter), then writes it in kk order.
-            static_assert(BPT <= 32, "one bit per bucket of a lane");
-            u32 wbits = 0, wtotal = 0;
-#pragma unroll 4
-            for (int kk = 0; kk < BPT; kk++) {
-                const u32 b = tid + (u32)kk * THREADS;
-                const u32 end = C16[b];
-                u32 st = __shfl_up_sync(0xffffffffu, end, 1);  // bucket b-1 is lane l-1's
-                if (lane == 0) st = b ? C16[b - 1] : 0u;
-                const u32 sz = end - st;
-                if (sz > (u32)SMALL) {
-                    const u32 at = atomicAdd(&ms.nbig, 1u);
-                    if (at < MAXBIG) {
-                        ms.big[at][0] = st;
-                        ms.big[at][1] = st + sz;
-                    } else ms.fail = 1;
-                }
-                const bool want = sz >= 2 && sz <= (u32)SMALL;
-                wbits |= (u32)want << kk;
-                wtotal += __popc(__ballot_sync(0xffffffffu, want));
-            }
-            {
-                u32 base = 0;
-                if (lane == 0 && wtotal) base = atomicAdd(&ms.red32[0], wtotal);
-                base = __shfl_sync(0xffffffffu, base, 0);
-#pragma unroll 4
-                for (int kk = 0; kk < BPT; kk++) {
-                    const bool want = (wbits >> kk) & 1u;
-                    const u32 mask = __ballot_sync(0xffffffffu, want);
-                    if (want) Q[base + __popc(mask & lt)] = (u16)(tid + (u32)kk * THREADS);
-                    base += __popc(mask);
-                }
-            }
-            __syncthreads();
+            // Insertion sort of every bucket of 2..SMALL samples, one word compare
+            // per step.  The bucket scan queued those buckets (in bucket order) in
+            // one CTA-wide queue; a warp's lanes pull buckets from it as they
+            // finish, so the lanes run in lock step with balanced work (a per-lane
+            // loop over its own buckets serialises the lanes).
+            u16 *Q = QW;
             const u32 qn = ms.red32[0];
+            const u32 lane = lane_id(), lt = lanemask_lt();
+            if (CLK && tid == 0) clk_q += clock64() - t_in;
+            u32 nsteps = 0, nwsteps = 0;
             // queue entries are claimed 32 at a time per warp (one atomic on the
             // shared counter per 32 buckets, not one per step); [cnext, cend) is
             // the warp's claimed, unassigned remainder (warp-uniform)
@@ -691,6 +684,10 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             }
             while (__any_sync(0xffffffffu, live)) {
                 bool done = false;
+                if (CLK) {
+                    nsteps += live;
+                    nwsteps++;
+                }
                 if (live) {
                     const u32 y = SS[j - 1];
                     u32 l_;
@@ -749,6 +746,8 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                 }
             }
             if (CLK) {
+                clk_steps += __reduce_add_sync(0xffffffffu, nsteps);
+                clk_wsteps += nwsteps;
                 atomicMax((unsigned long long *)&ms.tmax, (unsigned long long)(clock64() - t_in));
                 atomicAdd((unsigned long long *)&ms.tsum, (unsigned long long)(clock64() - t_in));
             }
@@ -765,7 +764,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
         {
             const u32 nbig = ms.nbig < MAXBIG ? ms.nbig : MAXBIG;
             for (u32 g = 0; g < nbig && !ms.fail; g++) {
-                const u32 st = ms.big[g][0], sz = ms.big[g][1] - st;
+                const u32 sz = ms.big[g][1], st = reinterpret_cast<const u16 *>(CNT)[ms.big[g][0]] - sz;
                 if (sz > (u32)BIG_CAP) {
                     ms.fail = 1;  // uniform: every thread reads the same sz
                     break;
@@ -1122,6 +1121,11 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
         for (int k = 0; k < NPHASE; k++) atomicAdd(clk + k, (unsigned long long)ms.acc[k]);
         atomicAdd(clk + NPHASE, (unsigned long long)ms.acc2[0]);
         atomicAdd(clk + NPHASE + 1, (unsigned long long)ms.acc2[1]);
+        atomicAdd(clk + NPHASE + 4, clk_q);
+    }
+    if (CLK && lane_id() == 0) {
+        atomicAdd(clk + NPHASE + 2, clk_steps);
+        atomicAdd(clk + NPHASE + 3, clk_wsteps);
     }
 }
 
@@ -1205,7 +1209,7 @@ static size_t pairs_ws(Arena &ar, const i64 *offs, i64 P, PairsWs *w) {
     t.ctr = ar.alloc<u32>(4);
     t.fb = ar.alloc<u32>(P);
     t.bounds = ar.alloc<u32>(pd::kMaxStreamChunks + 1);
-    t.clk = ar.alloc<unsigned long long>(pd::NPHASE + 2);
+    t.clk = ar.alloc<unsigned long long>(pd::NPHASE + 5);
     t.dummy_bad = ar.alloc<i64>(1);
     t.cap = fb_capacity(offs, P);
     t.fseqs = ar.alloc<u8>(t.cap + 16);
@@ -1227,7 +1231,7 @@ using namespace saix;
 static std::atomic<int> g_onchip_nmax{pd::NMAX};
 
 static thread_local long long g_last_fallbacks = 0;
-static unsigned long long g_phase_clk[pd::NPHASE + 2];
+static unsigned long long g_phase_clk[pd::NPHASE + 5];
 
 static bool clocks_on() {
     static const bool on = [] {
@@ -1242,7 +1246,7 @@ static bool clocks_on() {
 // 6 ranks, 7 non-samples, 8 merge, 9 LCP pass 1, 10 runs pass 2, 11 pair fetch.
 extern "C" int saix_overlap_batch_phase_clocks(int64_t *out, int max) {
     int k = 0;
-    for (; k < max && k < pd::NPHASE + 2; k++) out[k] = (int64_t)g_phase_clk[k];
+    for (; k < max && k < pd::NPHASE + 5; k++) out[k] = (int64_t)g_phase_clk[k];
     return k;
 }
 
@@ -1391,7 +1395,7 @@ static int overlap_batch_run(const uint8_t *seqs, const int64_t *offs_host, cons
             SAIX_CUDA(cudaEventDestroy(e0));
             SAIX_CUDA(cudaEventDestroy(e1));
         } else if (clocks_on()) {
-            SAIX_CUDA(cudaMemsetAsync(w.clk, 0, sizeof(unsigned long long) * (pd::NPHASE + 2), st));
+            SAIX_CUDA(cudaMemsetAsync(w.clk, 0, sizeof(unsigned long long) * (pd::NPHASE + 5), st));
             pd::k_pair_dc3<true, false><<<(unsigned)grid, pd::THREADS, pd::SMEM, st>>>(
                 seqs, doffs, P, keep_n, out, bad, w.ctr, w.ctr + 1, w.fb, g_onchip_nmax.load(), w.clk, nullptr, nullptr);
         } else {
