@@ -78,6 +78,7 @@ constexpr int OFF_S0 = OFF_SS + al16(2 * MMAX);
 constexpr int OFF_RK = OFF_S0 + al16(2 * KMAX);
 constexpr int QROUND = 16;            // buckets per lane per queue round
 constexpr int QCAP = QROUND * 32;     // per-warp queue of small buckets
+constexpr int QTOP = QCAP * WARPS;   // queue entries (buckets of >= 2 samples: <= MMAX / 2)
 constexpr int OFF_Q = OFF_RK + al16(2 * RKMAX);
 constexpr int P2W = NMAX / 32 + 2;    // 2-bit packed text words
 constexpr int OFF_P2 = OFF_Q + al16(2 * QCAP * WARPS);
@@ -511,7 +512,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             ms.pair = atomicAdd(next_pair, 1u);
             ms.fail = 0;
             ms.nbig = 0;
-            ms.red32[0] = ms.red32[1] = 0;
+            ms.red32[1] = ms.red32[3] = 0;
             if (STREAM && ms.pair < P) {
                 for (;;) {
                     u32 c;
@@ -600,12 +601,15 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             // above the sample count (m < 2^16), so one block scan yields both
             // offsets; buckets over SMALL (rare) go to the big list as
             // (bucket, size) -- their start is end - size after the scatter
-            u32 wm = 0, bm = 0;
+            // Buckets of exactly 2 (w2, most of them) are queued first and
+            // sorted by one compare each, outside the lock-step loop.
+            u32 w2 = 0, wm = 0, bm = 0;
 #pragma unroll
             for (int k = 0; k < W; k++) {
                 const u32 c0 = loc[k] & 0xFFFFu, c1 = loc[k] >> 16;
                 sum += c0 + c1;
-                wm |= (u32)(c0 - 2u <= (u32)SMALL - 2u) << (2 * k) | (u32)(c1 - 2u <= (u32)SMALL - 2u) << (2 * k + 1);
+                w2 |= (u32)(c0 == 2u) << (2 * k) | (u32)(c1 == 2u) << (2 * k + 1);
+                wm |= (u32)(c0 - 3u <= (u32)SMALL - 3u) << (2 * k) | (u32)(c1 - 3u <= (u32)SMALL - 3u) << (2 * k + 1);
                 bm |= (u32)(c0 > (u32)SMALL) << (2 * k) | (u32)(c1 > (u32)SMALL) << (2 * k + 1);
             }
             const u32 b0 = tid * (2 * W);
@@ -618,16 +622,25 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                     ms.big[at][1] = reinterpret_cast<const u16 *>(CNT)[b];  // still the count
                 } else ms.fail = 1;
             }
+            // buckets of two fill the queue from the front (offsets from the
+            // scan: samples | pairs << 16), longer ones from the back (one
+            // shared atomic per thread that has any; their order is free)
             u32 tot;
-            u32 run = block_exsum<u32>(sum | ((u32)__popc(wm) << 16), tot, ms.scan32);
-            u32 qat = run >> 16;
+            u32 run = block_exsum<u32>(sum | ((u32)__popc(w2) << 16), tot, ms.scan32);
+            u32 qat2 = run >> 16;
             run &= 0xFFFFu;
-            if (tid == 0) ms.red32[0] = tot >> 16;  // the queue's length
+            if (tid == 0) ms.red32[2] = tot >> 16;  // [0, n2): buckets of two
+            u32 qat = 0;
+            if (wm) qat = (u32)QTOP - atomicAdd(&ms.red32[3], (u32)__popc(wm)) - (u32)__popc(wm);
 #pragma unroll
             for (int k = 0; k < W; k++) {
                 const u32 lo = run, hi = run + (loc[k] & 0xFFFFu);
                 run = hi + (loc[k] >> 16);
                 loc[k] = lo | (hi << 16);
+            }
+            while (w2) {
+                QW[qat2++] = (u16)(b0 + (u32)(__ffs(w2) - 1));
+                w2 &= w2 - 1;
             }
             while (wm) {
                 QW[qat++] = (u16)(b0 + (u32)(__ffs(wm) - 1));
@@ -661,7 +674,27 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             // finish, so the lanes run in lock step with balanced work (a per-lane
             // loop over its own buckets serialises the lanes).
             u16 *Q = QW;
-            const u32 qn = ms.red32[0];
+            // [0, n2): buckets of two; [q0, QTOP): buckets of 3..SMALL
+            const u32 n2 = ms.red32[2], q0 = (u32)QTOP - ms.red32[3], qn = (u32)QTOP;
+            // buckets of two: one compare (of as many words as it takes) each
+            for (u32 t = tid; t < n2; t += THREADS) {
+                const u32 b = Q[t];
+                const u32 st = b ? C16[b - 1] : 0u;
+                const u32 y = SS[st], x = SS[st + 1];
+                u32 h = 0, l_;
+                int c;
+                while ((c = tx.cmp(x, y, h, l_)) == 0) {
+                    h += tx.step();
+                    if (++work > WORK_MAX) {
+                        ms.fail = 1;
+                        break;
+                    }
+                }
+                if (c == 1) {
+                    SS[st] = (u16)x;
+                    SS[st + 1] = (u16)y;
+                }
+            }
             const u32 lane = lane_id(), lt = lanemask_lt();
             if (CLK && tid == 0) clk_q += clock64() - t_in;
             u32 nsteps = 0, nwsteps = 0;
@@ -670,7 +703,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             // the warp's claimed, unassigned remainder (warp-uniform)
             constexpr u32 QCLAIM = 32;
             u32 t0 = 0;
-            if (lane == 0) t0 = atomicAdd(&ms.red32[1], 2 * QCLAIM);
+            if (lane == 0) t0 = q0 + atomicAdd(&ms.red32[1], 2 * QCLAIM);
             t0 = __shfl_sync(0xffffffffu, t0, 0);
             u32 cnext = t0 + 32, cend = t0 + 2 * QCLAIM;
             u32 start = 0, end = 0, i = 0, j = 0, x = 0, h = 0;
@@ -722,7 +755,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                     const u32 need = __popc(dm), avail = cend - cnext;
                     u32 nb = 0;
                     if (need > avail) {  // warp-uniform
-                        if (lane == 0) nb = atomicAdd(&ms.red32[1], QCLAIM);
+                        if (lane == 0) nb = q0 + atomicAdd(&ms.red32[1], QCLAIM);
                         nb = __shfl_sync(0xffffffffu, nb, 0);
                     }
                     if (done) {
