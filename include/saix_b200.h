@@ -266,7 +266,11 @@ SAIX_API size_t saix_longest_overlap_workspace_bytes(int64_t na, int64_t nb);
 
 /* longest_overlap (overlap.py:110-152) end to end on the device: encode +
  * GSA + DC3 + LCP + scan.  a_ascii/b_ascii are device buffers; out3 and
- * bad_pos are device int64 (bad_pos set to INT64_MAX by the callee). */
+ * bad_pos are device int64 (bad_pos set to INT64_MAX by the callee; else the
+ * first illegal residue's generalized-text position, B's residue k at
+ * na + 1 + k).  Pairs with na + 1 + nb <= 20480 run through the on-chip pair
+ * kernel as a batch of one (saix_overlap_batch_dev; same results), unless
+ * saix_overlap_batch_set_onchip(0). */
 SAIX_API int saix_longest_overlap(const uint8_t *a_ascii, int64_t na,
                          const uint8_t *b_ascii, int64_t nb, int keep_n,
                          int64_t *out3, int64_t *bad_pos, void *ws,

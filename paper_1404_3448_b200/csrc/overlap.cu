@@ -426,9 +426,34 @@ static size_t pair_ws(Arena &ar, i64 n, PairWs *w) {
 }
 }  // namespace saix
 
+// Pairs of up to pd::NMAX generalized-text residues run through the on-chip
+// pair kernel (pairdc3.cu) as a batch of one: A and B copied back to back
+// into the workspace, then saix_overlap_batch_dev.  One launch instead of the
+// multi-pass DC3 pipeline; pd_onchip_enabled() off (the batch A/B knob) keeps
+// the pipeline.
+constexpr i64 kOnchipResidues = 20480;  // pd::NMAX
+namespace saix {
+int pd_onchip_enabled();  // pairdc3.cu
+}
+
+static size_t small_pair_ws(i64 na, i64 nb) {
+    const int64_t offs[3] = {0, na, na + nb};
+    return (size_t)((na + nb + 15) & ~15ll) + saix_overlap_batch_workspace_bytes(offs, 1);
+}
+
+__global__ void k_small_bad(i64 *__restrict__ bad, i64 na) {
+    // batch offsets put B right after A; the pipeline reports GSA positions
+    if (*bad != INT64_MAX && *bad >= na) *bad += 1;
+}
+
 extern "C" size_t saix_longest_overlap_workspace_bytes(int64_t na, int64_t nb) {
     Arena ar;
-    return pair_ws(ar, na + nb + 1, nullptr) + Arena::kAlign;
+    size_t bytes = pair_ws(ar, na + nb + 1, nullptr) + Arena::kAlign;
+    if (na > 0 && nb > 0 && na + nb + 1 <= kOnchipResidues) {
+        const size_t sm = small_pair_ws(na, nb) + Arena::kAlign;
+        if (sm > bytes) bytes = sm;
+    }
+    return bytes;
 }
 
 extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const uint8_t *b_ascii, int64_t nb,
@@ -444,6 +469,23 @@ extern "C" int saix_longest_overlap(const uint8_t *a_ascii, int64_t na, const ui
     // overlap.py:120-121: empty input returns before encoding (no validation)
     if (na == 0 || nb == 0) return SAIX_OK;
     i64 n = na + nb + 1;
+    if (n <= kOnchipResidues && pd_onchip_enabled()) {
+        char *base = (char *)(((uintptr_t)ws + 15) & ~(uintptr_t)15);
+        const size_t skip = (size_t)(base - (char *)ws), cat = (size_t)((na + nb + 15) & ~15ll);
+        if (!ws || ws_bytes < skip + cat) {
+            set_error("saix_longest_overlap: workspace too small");
+            return SAIX_EINVAL;
+        }
+        uint8_t *seqs = (uint8_t *)base;
+        SAIX_CUDA(cudaMemcpyAsync(seqs, a_ascii, (size_t)na, cudaMemcpyDeviceToDevice, st));
+        SAIX_CUDA(cudaMemcpyAsync(seqs + na, b_ascii, (size_t)nb, cudaMemcpyDeviceToDevice, st));
+        const int64_t offs[3] = {0, na, na + nb};
+        SAIX_TRY(saix_overlap_batch_dev(seqs, offs, nullptr, 1, keep_n, out3, bad_pos, base + cat,
+                                        ws_bytes - skip - cat, stream));
+        k_small_bad<<<1, 1, 0, st>>>(bad_pos, na);
+        SAIX_LAUNCHED();
+        return SAIX_OK;
+    }
     Arena ar{(char *)ws, ws_bytes};
     PairWs w;
     pair_ws(ar, n, &w);

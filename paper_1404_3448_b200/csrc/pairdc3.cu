@@ -1285,6 +1285,10 @@ extern "C" int saix_overlap_batch_phase_clocks(int64_t *out, int max) {
 
 extern "C" int64_t saix_overlap_batch_last_fallbacks(void) { return g_last_fallbacks; }
 
+namespace saix {
+int pd_onchip_enabled() { return g_onchip_nmax.load() != 0; }
+}  // namespace saix
+
 extern "C" int saix_overlap_batch_set_onchip(int on) {
     return g_onchip_nmax.exchange(on ? pd::NMAX : 0) != 0;
 }

@@ -41,14 +41,46 @@ def test_random_splits_vs_oracle():
         _check(a, b)
 
 
+def _pipeline_run(a: str, b: str, onchip: bool, keep=False):
+    """saix_longest_overlap through the C ABI (OverlapPipeline); onchip=False
+    forces the multi-pass DC3 pipeline for pairs the pair kernel would take."""
+    from paper_1404_3448_b200 import _lib
+    L = _lib.load()
+    prev = L.saix_overlap_batch_set_onchip(int(onchip))
+    try:
+        pol = NPolicy.KEEP if keep else NPolicy.REJECT
+        return OverlapPipeline(len(a), len(b)).run(np.frombuffer(a.encode(), np.uint8),
+                                                   np.frombuffer(b.encode(), np.uint8), pol)
+    finally:
+        L.saix_overlap_batch_set_onchip(prev)
+
+
 def test_size_boundary_both_paths_agree():
     rng = np.random.default_rng(11)
     for tot in (ONCHIP_RESIDUES - 2, ONCHIP_RESIDUES - 1, ONCHIP_RESIDUES, ONCHIP_RESIDUES + 1):
         la = tot // 2
         a, b = _rand(rng, la), _rand(rng, tot - 1 - la)   # |A| + 1 + |B| = tot
         r = _check(a, b)
-        big = OverlapPipeline(len(a), len(b)).run(_ascii(DnaSequence("a", a)), _ascii(DnaSequence("b", b)))
-        assert (r.length, r.pos_a, r.pos_b) == tuple(int(v) for v in big[:3])
+        for onchip in (True, False):
+            got = _pipeline_run(a, b, onchip)
+            assert (r.length, r.pos_a, r.pos_b) == tuple(int(v) for v in got[:3]), (tot, onchip)
+
+
+def test_c_abi_routes_small_pairs_with_the_pipeline_conventions():
+    """saix_longest_overlap on a small pair (on-chip route) returns what the
+    multi-pass pipeline returns: the answer and the first illegal residue as a
+    generalized-text position (B's residue k at |A| + 1 + k)."""
+    rng = np.random.default_rng(9)
+    for la, lb in ((1, 1), (3000, 5000), (10000, 10000), (17, 20000)):
+        a, b = _rand(rng, la), _rand(rng, lb)
+        on, off = _pipeline_run(a, b, True), _pipeline_run(a, b, False)
+        assert np.array_equal(on, off)
+        assert tuple(int(v) for v in on[:3]) == oracle.longest_overlap(a, b)
+    a, b = _rand(rng, 900, "ACGTN"), _rand(rng, 700, "ACGTN")
+    assert np.array_equal(_pipeline_run(a, b, True, keep=True), _pipeline_run(a, b, False, keep=True))
+    for a, b in (("ACGXT", "ACGT"), ("ACGT", "ACGTTGX"), ("ACNGT", "AC")):
+        on, off = _pipeline_run(a, b, True), _pipeline_run(a, b, False)
+        assert int(on[3]) == int(off[3]) != np.iinfo(np.int64).max, (a, b, on, off)
 
 
 def test_repeats_and_tiny():

@@ -30,12 +30,17 @@ t0 = time.perf_counter()
 small = [sx.longest_overlap(a, b) for a, b in pairs]
 t_small = (time.perf_counter() - t0) / calls
 
+# the multi-pass DC3 pipeline (saix_longest_overlap with the on-chip route off)
+from paper_1404_3448_b200 import _lib  # noqa: E402
+L = _lib.load()
+prev = L.saix_overlap_batch_set_onchip(0)
 pipe = OverlapPipeline(len(pairs[0][0]), len(pairs[0][1]))
 for a, b in pairs[:5]:
     pipe.run(_ascii(a), _ascii(b))
 t0 = time.perf_counter()
 big = [pipe.run(_ascii(a), _ascii(b)) for a, b in pairs]
 t_big = (time.perf_counter() - t0) / calls
+L.saix_overlap_batch_set_onchip(prev)
 
 same = all((r.length, r.pos_a, r.pos_b) == tuple(int(v) for v in g[:3]) for r, g in zip(small, big))
 print(json.dumps({"calls": calls, "pair_residues": int(offs[2] - offs[0]),
