@@ -512,7 +512,7 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             ms.pair = atomicAdd(next_pair, 1u);
             ms.fail = 0;
             ms.nbig = 0;
-            ms.red32[1] = ms.red32[3] = 0;
+            ms.red32[1] = ms.red32[3] = ms.red32[4] = 0;
             if (STREAM && ms.pair < P) {
                 for (;;) {
                     u32 c;
@@ -676,25 +676,6 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             u16 *Q = QW;
             // [0, n2): buckets of two; [q0, QTOP): buckets of 3..SMALL
             const u32 n2 = ms.red32[2], q0 = (u32)QTOP - ms.red32[3], qn = (u32)QTOP;
-            // buckets of two: one compare (of as many words as it takes) each
-            for (u32 t = tid; t < n2; t += THREADS) {
-                const u32 b = Q[t];
-                const u32 st = b ? C16[b - 1] : 0u;
-                const u32 y = SS[st], x = SS[st + 1];
-                u32 h = 0, l_;
-                int c;
-                while ((c = tx.cmp(x, y, h, l_)) == 0) {
-                    h += tx.step();
-                    if (++work > WORK_MAX) {
-                        ms.fail = 1;
-                        break;
-                    }
-                }
-                if (c == 1) {
-                    SS[st] = (u16)x;
-                    SS[st + 1] = (u16)y;
-                }
-            }
             const u32 lane = lane_id(), lt = lanemask_lt();
             if (CLK && tid == 0) clk_q += clock64() - t_in;
             u32 nsteps = 0, nwsteps = 0;
@@ -775,6 +756,34 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                         cend = nb + QCLAIM;
                     } else {
                         cnext += need;
+                    }
+                }
+            }
+            // buckets of two, one compare (of as many words as it takes) each:
+            // warps take 32 at a time as they leave the lock-step loop, so the
+            // early finishers absorb them and the phase ends balanced
+            for (;;) {
+                u32 base = 0;
+                if (lane == 0) base = atomicAdd(&ms.red32[4], 32u);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base >= n2) break;
+                const u32 t = base + lane;
+                if (t < n2) {
+                    const u32 b = Q[t];
+                    const u32 st = b ? C16[b - 1] : 0u;
+                    const u32 y = SS[st], x = SS[st + 1];
+                    u32 hh = 0, l_;
+                    int c;
+                    while ((c = tx.cmp(x, y, hh, l_)) == 0) {
+                        hh += tx.step();
+                        if (++work > WORK_MAX) {
+                            ms.fail = 1;
+                            break;
+                        }
+                    }
+                    if (c == 1) {
+                        SS[st] = (u16)x;
+                        SS[st + 1] = (u16)y;
                     }
                 }
             }
