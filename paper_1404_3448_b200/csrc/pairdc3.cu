@@ -983,6 +983,10 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             if (r0 < n) {
                 u32 prev = r0 ? SA[r0 - 1] : 0u;
                 u64 wp = r0 ? tx.ld32(prev) : 0ull;
+                // the predecessor's limit and side (0: A, 1: B, 2: the
+                // separator) carry over from the previous rank; a pair is
+                // cross-sequence iff the sides sum to 1
+                u32 lp = tx.lim(prev), sp = prev < nA ? 0u : (prev == nA ? 2u : 1u);
                 const u32 cnt = min((u32)ITEMS, n - r0);
                 for (u32 q0 = 0; q0 < cnt; q0 += 8) {
                     const uint4 sv4 = reinterpret_cast<const uint4 *>(SA + r0)[q0 >> 3];  // inside SS + S0
@@ -993,9 +997,10 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                         if (q0 + k < cnt) {
                             const u32 cur = (svw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
                             const u64 wc = tx.ld32(cur);
+                            const u32 lc = tx.lim(cur), sc = cur < nA ? 0u : (cur == nA ? 2u : 1u);
                             u32 l = 0;
                             if (r0 + q0 + k) {
-                                const u32 L = min(tx.lim(prev), tx.lim(cur));
+                                const u32 L = min(lp, lc);
                                 u64 x = wp ^ wc;
                                 u32 h = 0;
                                 while (!x && h + 32u < L) {
@@ -1003,12 +1008,13 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
                                     x = tx.ld32(prev + h) ^ tx.ld32(cur + h);
                                 }
                                 l = x ? min(L, h + ((u32)(__ffsll((long long)x) - 1) >> 1)) : L;
-                                const bool cross = prev != nA && cur != nA && ((prev < nA) != (cur < nA));
-                                if (cross) mx = max(mx, l);
+                                if (sp + sc == 1u) mx = max(mx, l);
                             }
                             lcw |= (u64)min(l, 255u) << (8 * k);
                             prev = cur;
                             wp = wc;
+                            lp = lc;
+                            sp = sc;
                         }
                     }
                     reinterpret_cast<u64 *>(LC + r0)[q0 >> 3] = lcw;  // bytes past n: inside the RK region
