@@ -832,11 +832,10 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             continue;
         }
 
-        // ---- 3. rank_of (1-based; 0 for positions >= limit)
+        // ---- 3. rank_of (1-based; 0 for positions >= limit): zeroed here, filled
+        //         in the non-sample counting pass below
         const u32 rkn = 2u * ((n + 2u) / 3u + 1u) + 2u;
         for (u32 i = tid; i < (rkn + 1) / 2; i += THREADS) reinterpret_cast<u32 *>(RK)[i] = 0;
-        __syncthreads();
-        for (u32 r = tid; r < m; r += THREADS) RK[slot(SS[r])] = (u16)(r + 1);
         __syncthreads();
         PD_MARK(6);
 
@@ -846,8 +845,11 @@ k_pair_dc3(const u8 *__restrict__ seqs, const i64 *__restrict__ offs, i64 P, int
             const u32 per = (m + THREADS - 1) / THREADS;
             const u32 r0 = tid * per, r1 = min(m, r0 + per);
             unsigned long long c0 = 0, c1 = 0;
+            // the rank table is filled in the same pass (ranks and the
+            // non-sample counts both read only the sorted samples)
             for (u32 r = r0; r < r1; r++) {
                 const u32 s = SS[r];
+                RK[slot(s)] = (u16)(r + 1);
                 if (s % 3u == 1u) {
                     const u32 c = T[s - 1];
                     if (c <= 4) c0 += 1ull << (16 * (c - 1));
